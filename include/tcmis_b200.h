@@ -1,0 +1,197 @@
+/*
+ * tcmis_b200.h -- C-ABI of the B200-native TC-MIS engine (sm_100a).
+ *
+ * This is the drop-in boundary for the reference's MIS call.  Every entry
+ * point names the reference interface it replaces (paths relative to
+ * /root/reference/proj).  Signatures carry only plain pointers, sizes and PODs;
+ * errors are status codes plus tcmis_last_error(), which the C++ layer
+ * (include/tcmis/*.hpp, libtcmis.so) maps back onto the reference's exception
+ * types (SURVEY 8(b) "Errors").
+ *
+ * Threading: a context owns one device and one CUDA stream; calls on one
+ * context are not re-entrant ("one coordinator per engine call").
+ * There is no CPU fallback: every compute entry point launches sm_100a kernels
+ * and fails with TCMIS_E_CUDA when no device is usable.
+ */
+#ifndef TCMIS_B200_H
+#define TCMIS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TCMIS_ABI_VERSION 1
+
+/* Status codes; C++ mapping in brackets. */
+typedef enum tcmis_status {
+  TCMIS_OK = 0,
+  TCMIS_E_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  TCMIS_E_RUNTIME = 2,          /* std::runtime_error (iteration cap, engine.cpp:248-249) */
+  TCMIS_E_LOGIC = 3,            /* std::logic_error (engine.cpp:152-153) */
+  TCMIS_E_CUDA = 4,             /* std::runtime_error: CUDA / no device */
+  TCMIS_E_OUT_OF_RANGE = 5      /* std::out_of_range (graph.cpp:23-24) */
+} tcmis_status;
+
+/* engine.hpp:19 `enum class Heuristic { H1, H2, H3, LubyFresh, LubyPerm }` */
+typedef enum tcmis_heuristic {
+  TCMIS_H1 = 0,
+  TCMIS_H2 = 1,
+  TCMIS_H3 = 2,
+  TCMIS_LUBY_FRESH = 3,
+  TCMIS_LUBY_PERM = 4
+} tcmis_heuristic;
+
+/* engine.hpp:17 `enum class VertexState : uint8_t { Alive, InMIS, Removed }` */
+enum { TCMIS_ALIVE = 0, TCMIS_IN_MIS = 1, TCMIS_REMOVED = 2 };
+
+/* Neighbour-exclusion (Phase 2) kernel variants; see DESIGN.md "K4". */
+typedef enum tcmis_exclusion {
+  TCMIS_EXCL_AUTO = 0,     /* the variant ncu says wins (currently PUSH)      */
+  TCMIS_EXCL_PUSH = 1,     /* candidates scatter Removed to their neighbours  */
+  TCMIS_EXCL_CSR_PULL = 2, /* alive non-candidates look for a candidate nbr   */
+  TCMIS_EXCL_TILE_BITS = 3,/* T x T bit tiles AND candidate segments (CUDA cores) */
+  TCMIS_EXCL_TILE_MMA = 4  /* T=16 tiles x candidate vector on tensor cores (mma.sync s8) */
+} tcmis_exclusion;
+
+/* engine.hpp:24-34 IterationStats (timers are device-event times). */
+typedef struct tcmis_iter_stats {
+  int32_t iteration;
+  int32_t reserved;
+  int64_t candidates_selected;
+  int64_t vertices_removed;
+  int64_t alive_remaining;
+  int64_t tiles_evaluated;
+  int64_t tiles_skipped;
+  double phase1_ms;
+  double phase2_ms;
+  double phase3_ms;
+} tcmis_iter_stats;
+
+/* engine.hpp:59-64 iteration_observer: called once per iteration, before the
+ * state update, with host copies of the candidate flags and states. */
+typedef void (*tcmis_observer_fn)(void *user, int32_t iteration, const uint8_t *candidates,
+                                  const uint8_t *states, int32_t n);
+
+/* engine.hpp:53-65 EngineConfig */
+typedef struct tcmis_config {
+  int32_t heuristic;  /* tcmis_heuristic, default TCMIS_H3 (engine.hpp:54) */
+  int32_t tile_dim;   /* 1..64, default 16 */
+  uint64_t seed;      /* default 1 */
+  int32_t scale_bits; /* 8..30, default 20 (priorities.hpp:24-26) */
+  int32_t workers;    /* accepted and ignored: the CUDA grid replaces parallel.cpp */
+  int32_t exclusion;  /* tcmis_exclusion */
+  uint32_t flags;     /* TCMIS_F_* */
+  tcmis_observer_fn observer;
+  void *observer_user;
+} tcmis_config;
+
+#define TCMIS_F_TIMING 0x1u     /* record per-phase device times in the stats */
+#define TCMIS_F_HOST_LOOP 0x2u  /* drive rounds from the host (no CUDA-graph while loop) */
+
+/* Fill *cfg with the reference defaults (EngineConfig{}). */
+void tcmis_config_init(tcmis_config *cfg);
+
+typedef struct tcmis_ctx tcmis_ctx;
+typedef struct tcmis_graph tcmis_graph;
+
+const char *tcmis_last_error(void);
+int32_t tcmis_abi_version(void);
+
+/* Context: device + stream + scratch.  Replaces parallel.cpp:12-62
+ * (resolve_workers / parallel_for / parallel_chunks). */
+int tcmis_ctx_create(int32_t device, tcmis_ctx **out);
+void tcmis_ctx_destroy(tcmis_ctx *ctx);
+/* The CUDA stream (cudaStream_t) every launch of this context goes to. */
+void *tcmis_ctx_stream(tcmis_ctx *ctx);
+int tcmis_ctx_synchronize(tcmis_ctx *ctx);
+/* Kernels this context launched since creation (driver evidence counter). */
+int64_t tcmis_ctx_launches(tcmis_ctx *ctx);
+
+/* Device-resident CSR graph (graph.hpp:18-39 Graph: n, offsets[n+1] int64,
+ * neighbors[2m] int32, normalised).  upload copies host arrays (H2D on the
+ * context stream); wrap_device borrows device arrays the caller keeps alive. */
+int tcmis_graph_upload(tcmis_ctx *ctx, int32_t n, const int64_t *offsets,
+                       const int32_t *neighbors, tcmis_graph **out);
+int tcmis_graph_wrap_device(tcmis_ctx *ctx, int32_t n, int64_t nnz, const int64_t *d_offsets,
+                            const int32_t *d_neighbors, tcmis_graph **out);
+void tcmis_graph_destroy(tcmis_graph *g);
+int32_t tcmis_graph_n(const tcmis_graph *g);
+int64_t tcmis_graph_nnz(const tcmis_graph *g);
+/* Device pointers of the CSR (for callers that launch around the engine). */
+const int64_t *tcmis_graph_device_offsets(const tcmis_graph *g);
+const int32_t *tcmis_graph_device_neighbors(const tcmis_graph *g);
+/* Copy the CSR back to host buffers (n+1 / nnz entries). */
+int tcmis_graph_download(tcmis_graph *g, int64_t *offsets, int32_t *neighbors);
+
+/* K1 CSR->tile converter (tiling.cpp:44-84 tile_graph).  tcmis_graph_tile
+ * derives, on the device, the T x T tiling the tile counters of run_tc_mis are
+ * defined on (tiles per block row; spmv.cpp:37-46), and caches it on the
+ * graph.  *tile_count receives TiledAdjacency::tile_count(). */
+int tcmis_graph_tile(tcmis_graph *g, int32_t tile_dim, int64_t *tile_count);
+/* Same, from a TiledAdjacency the caller already holds (the prebuilt-tiles
+ * overload engine.hpp:111-112): block_row_offsets has n_block_rows+1 entries. */
+int tcmis_graph_set_tiling(tcmis_graph *g, int32_t tile_dim, const int64_t *block_row_offsets,
+                           int32_t n_block_rows);
+/* Full tile materialisation in the reference layout (tile_row, tile_col,
+ * T u64 row words per tile, block_row_offsets[nb+1]); host buffers sized from
+ * tcmis_graph_tile()'s count. */
+int tcmis_graph_export_tiles(tcmis_graph *g, int32_t tile_dim, int32_t *tile_row,
+                             int32_t *tile_col, uint64_t *row_bits, int64_t *block_row_offsets);
+
+/* priorities.cpp:33-67 (h1_random / h2_degree_aware) on the device; p_out is
+ * a host buffer of n entries. */
+int tcmis_priorities(tcmis_graph *g, int32_t heuristic, uint64_t seed, int32_t scale_bits,
+                     uint32_t *p_out);
+
+/* The MIS call: engine.cpp:354-365 run_mis / engine.cpp:231-299 run_tc_mis.
+ * Heuristics H1/H2/H3 and both Luby modes.  Outputs (each may be NULL):
+ *   state_out[n]  final VertexState per vertex (host)
+ *   mis_out[n]    ascending MIS vertex ids (host), *mis_count = |MIS|
+ *   stats[max_stats] per-iteration stats, *n_iterations = iterations.size()
+ * For H1/H2/H3 tcmis_graph_tile() (or set_tiling) for cfg->tile_dim must have
+ * run; otherwise the tiling is derived on the fly. */
+int tcmis_solve(tcmis_graph *g, const tcmis_config *cfg, uint8_t *state_out, int32_t *mis_out,
+                int64_t *mis_count, tcmis_iter_stats *stats, int32_t max_stats,
+                int32_t *n_iterations);
+
+/* Device-resident variant for benchmarking and multi-call pipelines: leaves
+ * the results on the device.  *d_mis receives a device pointer (owned by the
+ * graph, valid until the next solve) to the ascending MIS ids; *d_state the
+ * device VertexState array.  Stats are copied to the host. */
+int tcmis_solve_device(tcmis_graph *g, const tcmis_config *cfg, const int32_t **d_mis,
+                       int64_t *mis_count, const uint8_t **d_state, tcmis_iter_stats *stats,
+                       int32_t max_stats, int32_t *n_iterations);
+
+/* Phase-level helpers on the device (engine.hpp:71-106, spmv.hpp:15-42);
+ * host buffers in, host buffers out, for parity tests of single phases. */
+int tcmis_compute_max_np(tcmis_graph *g, const uint32_t *p, const uint8_t *states,
+                         uint64_t *max_np_out);
+int tcmis_neighbor_count(tcmis_graph *g, const uint8_t *candidates, int32_t *nc_out);
+int tcmis_tiled_spmv(tcmis_graph *g, int32_t tile_dim, const uint8_t *candidates,
+                     int32_t exclusion, int32_t *nc_out, int64_t *tiles_evaluated,
+                     int64_t *tiles_skipped);
+
+/* Synthetic graph generators on the device (generate.cpp:30-98 and the new
+ * grid / RGG definitions of DESIGN.md); the result is a device-resident
+ * normalised graph (graph.cpp:14-41 semantics). */
+int tcmis_gen_rmat(tcmis_ctx *ctx, int32_t scale, int32_t edge_factor, uint64_t seed,
+                   tcmis_graph **out);
+int tcmis_gen_grid(tcmis_ctx *ctx, int32_t side, tcmis_graph **out);
+int tcmis_gen_rgg(tcmis_ctx *ctx, int32_t n, uint64_t radius, uint64_t seed,
+                  tcmis_graph **out);
+/* Host-side G(n,p) (generate.cpp:30-66): serial by definition (one RNG
+ * stream), returned as malloc'ed CSR arrays the caller frees with
+ * tcmis_free(). */
+int tcmis_gen_gnp_host(int32_t n, double avg_degree, uint64_t seed, int64_t **offsets,
+                       int32_t **neighbors, int64_t *nnz);
+void tcmis_free(void *p);
+/* Radius of the RGG definition: floor(sqrt(avg/(pi n)) * 2^32). */
+uint64_t tcmis_rgg_radius(int32_t n, double avg_degree);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCMIS_B200_H */

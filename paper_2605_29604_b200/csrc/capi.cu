@@ -1,0 +1,344 @@
+// capi.cu -- the extern "C" boundary (include/tcmis_b200.h).
+//
+// Every entry point validates like the reference (exception type -> status
+// code), owns no hidden global state beyond the thread-local error string, and
+// launches only sm_100a kernels from this library.  There is deliberately no
+// CPU fallback: without a usable CUDA device every compute call fails with
+// TCMIS_E_CUDA.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+#define TCMIS_API extern "C" __attribute__((visibility("default")))
+
+namespace tcmis_b200 {
+
+static thread_local std::string g_last_error;
+
+int set_error(int code, const std::string &msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_error(cudaError_t e, const char *what) {
+  g_last_error = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+  return TCMIS_E_CUDA;
+}
+
+int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
+               int32_t max_stats, int32_t *n_iter, int64_t *mis_count_out);
+int priorities_impl(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
+                    uint32_t *p_out);
+int max_np_impl(tcmis_graph *g, const uint32_t *p, const uint8_t *states, uint64_t *out);
+int neighbor_count_impl(tcmis_graph *g, const uint8_t *c, int32_t *nc, int T, int64_t *ev,
+                        int64_t *sk);
+int gen_rmat(tcmis_ctx *ctx, int32_t scale, int32_t ef, uint64_t seed, tcmis_graph **out);
+int gen_grid(tcmis_ctx *ctx, int32_t side, tcmis_graph **out);
+int gen_rgg(tcmis_ctx *ctx, int32_t n, uint64_t R, uint64_t seed, tcmis_graph **out);
+int gen_gnp_host(int32_t n, double avg_degree, uint64_t seed, int64_t **offsets,
+                 int32_t **neighbors, int64_t *nnz_out);
+
+int wrap_owned(tcmis_ctx *ctx, int32_t n, int64_t nnz, int64_t *d_off, int32_t *d_nbr,
+               tcmis_graph **out) {
+  auto *g = new tcmis_graph();
+  g->ctx = ctx;
+  g->n = n;
+  g->nnz = nnz;
+  g->d_off = d_off;
+  g->d_nbr = d_nbr;
+  g->owns = true;
+  *out = g;
+  return 0;
+}
+
+}  // namespace tcmis_b200
+
+using namespace tcmis_b200;
+
+#define NEED(cond, msg) \
+  if (!(cond)) return set_error(TCMIS_E_INVALID_ARGUMENT, msg)
+
+TCMIS_API const char *tcmis_last_error(void) { return g_last_error.c_str(); }
+TCMIS_API int32_t tcmis_abi_version(void) { return TCMIS_ABI_VERSION; }
+
+TCMIS_API void tcmis_config_init(tcmis_config *c) {
+  std::memset(c, 0, sizeof(*c));
+  c->heuristic = TCMIS_H3;  // engine.hpp:54
+  c->tile_dim = 16;
+  c->seed = 1;
+  c->scale_bits = 20;
+  c->workers = 0;
+  c->exclusion = TCMIS_EXCL_AUTO;
+}
+
+TCMIS_API int tcmis_ctx_create(int32_t device, tcmis_ctx **out) {
+  NEED(out, "null output handle");
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return set_error(TCMIS_E_CUDA, "no CUDA device available (the B200 engine has no CPU path)");
+  NEED(device >= 0 && device < count, "device index out of range");
+  TCMIS_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  TCMIS_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return set_error(TCMIS_E_CUDA, std::string("device ") + prop.name +
+                                       " is not sm_100-class; this build targets sm_100a only");
+  auto *ctx = new tcmis_ctx();
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return cuda_error(e, "cudaStreamCreate");
+  }
+  for (auto &ev : ctx->ev) cudaEventCreate(&ev);
+  *out = ctx;
+  return 0;
+}
+
+TCMIS_API void tcmis_ctx_destroy(tcmis_ctx *ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto &ev : ctx->ev) cudaEventDestroy(ev);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+TCMIS_API void *tcmis_ctx_stream(tcmis_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
+TCMIS_API int64_t tcmis_ctx_launches(tcmis_ctx *ctx) { return ctx ? ctx->launches : 0; }
+TCMIS_API int tcmis_ctx_synchronize(tcmis_ctx *ctx) {
+  NEED(ctx, "null context");
+  TCMIS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+TCMIS_API int tcmis_graph_upload(tcmis_ctx *ctx, int32_t n, const int64_t *offsets,
+                                 const int32_t *neighbors, tcmis_graph **out) {
+  NEED(ctx && out, "null handle");
+  NEED(n >= 0, "vertex count must be non-negative");
+  NEED(n == 0 || offsets, "null offsets");
+  *out = nullptr;
+  const int64_t nnz = offsets ? offsets[n] : 0;
+  NEED(nnz >= 0, "negative edge count");
+  NEED(nnz == 0 || neighbors, "null neighbors");
+  TCMIS_CUDA(cudaSetDevice(ctx->device));
+  int64_t *d_off = nullptr;
+  int32_t *d_nbr = nullptr;
+  if (int rc = dev_alloc(&d_off, (size_t)n + 1)) return rc;
+  if (int rc = dev_alloc(&d_nbr, (size_t)nnz)) {
+    cudaFree(d_off);
+    return rc;
+  }
+  cudaError_t e = cudaSuccess;
+  if (offsets) e = cudaMemcpyAsync(d_off, offsets, 8ull * (n + 1), cudaMemcpyHostToDevice, ctx->stream);
+  else e = cudaMemsetAsync(d_off, 0, 8, ctx->stream);
+  if (e == cudaSuccess && nnz)
+    e = cudaMemcpyAsync(d_nbr, neighbors, 4ull * nnz, cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    cudaFree(d_off);
+    cudaFree(d_nbr);
+    return cuda_error(e, "graph upload");
+  }
+  return wrap_owned(ctx, n, nnz, d_off, d_nbr, out);
+}
+
+TCMIS_API int tcmis_graph_wrap_device(tcmis_ctx *ctx, int32_t n, int64_t nnz,
+                                      const int64_t *d_offsets, const int32_t *d_neighbors,
+                                      tcmis_graph **out) {
+  NEED(ctx && out && d_offsets, "null handle");
+  NEED(n >= 0 && nnz >= 0, "negative size");
+  auto *g = new tcmis_graph();
+  g->ctx = ctx;
+  g->n = n;
+  g->nnz = nnz;
+  g->d_off = const_cast<int64_t *>(d_offsets);
+  g->d_nbr = const_cast<int32_t *>(d_neighbors);
+  g->owns = false;
+  *out = g;
+  return 0;
+}
+
+TCMIS_API void tcmis_graph_destroy(tcmis_graph *g) {
+  if (!g) return;
+  cudaSetDevice(g->ctx->device);
+  cudaStreamSynchronize(g->ctx->stream);
+  if (g->owns) {
+    cudaFree(g->d_off);
+    cudaFree(g->d_nbr);
+  }
+  cudaFree(g->d_rowtiles);
+  free_workspace(g->ws);
+  delete g;
+}
+
+TCMIS_API int32_t tcmis_graph_n(const tcmis_graph *g) { return g ? g->n : 0; }
+TCMIS_API int64_t tcmis_graph_nnz(const tcmis_graph *g) { return g ? g->nnz : 0; }
+TCMIS_API const int64_t *tcmis_graph_device_offsets(const tcmis_graph *g) {
+  return g ? g->d_off : nullptr;
+}
+TCMIS_API const int32_t *tcmis_graph_device_neighbors(const tcmis_graph *g) {
+  return g ? g->d_nbr : nullptr;
+}
+
+TCMIS_API int tcmis_graph_download(tcmis_graph *g, int64_t *offsets, int32_t *neighbors) {
+  NEED(g && offsets, "null handle");
+  cudaStream_t st = g->ctx->stream;
+  TCMIS_CUDA(cudaMemcpyAsync(offsets, g->d_off, 8ull * (g->n + 1), cudaMemcpyDeviceToHost, st));
+  if (g->nnz)
+    TCMIS_CUDA(cudaMemcpyAsync(neighbors, g->d_nbr, 4ull * g->nnz, cudaMemcpyDeviceToHost, st));
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+TCMIS_API int tcmis_graph_tile(tcmis_graph *g, int32_t tile_dim, int64_t *tile_count) {
+  NEED(g, "null graph");
+  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  if (g->tile_T != tile_dim)
+    if (int rc = build_tile_counts(g, tile_dim)) return rc;
+  if (tile_count) *tile_count = g->tile_total;
+  return 0;
+}
+
+TCMIS_API int tcmis_graph_set_tiling(tcmis_graph *g, int32_t T, const int64_t *bro,
+                                     int32_t nb) {
+  NEED(g, "null graph");
+  if (T < 1 || T > 64)
+    return set_error(TCMIS_E_INVALID_ARGUMENT,
+                     "tile_dim must be in [1, 64], got " + std::to_string(T));
+  NEED(nb == (int32_t)(((int64_t)g->n + T - 1) / T), "tiled adjacency built for a different graph");
+  NEED(nb == 0 || bro, "null block_row_offsets");
+  std::vector<int32_t> rt((size_t)nb + 1, 0);
+  for (int32_t b = 0; b < nb; ++b) rt[b] = (int32_t)(bro[b + 1] - bro[b]);
+  cudaFree(g->d_rowtiles);
+  g->d_rowtiles = nullptr;
+  g->tile_T = 0;
+  if (int rc = dev_alloc(&g->d_rowtiles, (size_t)nb + 1)) return rc;
+  TCMIS_CUDA(cudaMemcpy(g->d_rowtiles, rt.data(), 4ull * (nb + 1), cudaMemcpyHostToDevice));
+  g->tile_nb = nb;
+  g->tile_total = nb ? bro[nb] - bro[0] : 0;
+  g->tile_T = T;
+  return 0;
+}
+
+TCMIS_API int tcmis_graph_export_tiles(tcmis_graph *g, int32_t T, int32_t *tile_row,
+                                       int32_t *tile_col, uint64_t *row_bits, int64_t *bro) {
+  NEED(g && bro, "null handle");
+  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  return export_tiles(g, T, tile_row, tile_col, row_bits, bro);
+}
+
+TCMIS_API int tcmis_priorities(tcmis_graph *g, int32_t heuristic, uint64_t seed,
+                               int32_t scale_bits, uint32_t *p_out) {
+  NEED(g && p_out, "null handle");
+  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  return priorities_impl(g, heuristic, seed, scale_bits, p_out);
+}
+
+static int solve_common(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
+                        int32_t max_stats, int32_t *n_iterations, int64_t *mis_count) {
+  NEED(g && cfg, "null handle");
+  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  int32_t it = 0;
+  int64_t mc = 0;
+  int rc = solve_impl(g, cfg, stats, max_stats, &it, &mc);
+  if (n_iterations) *n_iterations = it;
+  if (mis_count) *mis_count = mc;
+  return rc;
+}
+
+TCMIS_API int tcmis_solve(tcmis_graph *g, const tcmis_config *cfg, uint8_t *state_out,
+                          int32_t *mis_out, int64_t *mis_count, tcmis_iter_stats *stats,
+                          int32_t max_stats, int32_t *n_iterations) {
+  int64_t mc = 0;
+  if (int rc = solve_common(g, cfg, stats, max_stats, n_iterations, &mc)) return rc;
+  if (mis_count) *mis_count = mc;
+  if (g->n == 0) return 0;
+  cudaStream_t st = g->ctx->stream;
+  if (state_out)
+    TCMIS_CUDA(cudaMemcpyAsync(state_out, g->ws.state, g->n, cudaMemcpyDeviceToHost, st));
+  if (mis_out && mc)
+    TCMIS_CUDA(cudaMemcpyAsync(mis_out, g->ws.mis, 4ull * mc, cudaMemcpyDeviceToHost, st));
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+TCMIS_API int tcmis_solve_device(tcmis_graph *g, const tcmis_config *cfg, const int32_t **d_mis,
+                                 int64_t *mis_count, const uint8_t **d_state,
+                                 tcmis_iter_stats *stats, int32_t max_stats,
+                                 int32_t *n_iterations) {
+  if (int rc = solve_common(g, cfg, stats, max_stats, n_iterations, mis_count)) return rc;
+  if (d_mis) *d_mis = g->ws.mis;
+  if (d_state) *d_state = g->ws.state;
+  return 0;
+}
+
+TCMIS_API int tcmis_compute_max_np(tcmis_graph *g, const uint32_t *p, const uint8_t *states,
+                                   uint64_t *out) {
+  NEED(g && p && states && out, "null handle");
+  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  return max_np_impl(g, p, states, out);
+}
+
+TCMIS_API int tcmis_neighbor_count(tcmis_graph *g, const uint8_t *c, int32_t *nc) {
+  NEED(g && c && nc, "null handle");
+  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  return neighbor_count_impl(g, c, nc, 0, nullptr, nullptr);
+}
+
+TCMIS_API int tcmis_tiled_spmv(tcmis_graph *g, int32_t T, const uint8_t *c, int32_t exclusion,
+                               int32_t *nc, int64_t *ev, int64_t *sk) {
+  NEED(g && c && nc && ev && sk, "null handle");
+  if (T < 1 || T > 64)
+    return set_error(TCMIS_E_INVALID_ARGUMENT,
+                     "tile_dim must be in [1, 64], got " + std::to_string(T));
+  (void)exclusion;
+  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  return neighbor_count_impl(g, c, nc, T, ev, sk);
+}
+
+TCMIS_API int tcmis_gen_rmat(tcmis_ctx *ctx, int32_t scale, int32_t ef, uint64_t seed,
+                             tcmis_graph **out) {
+  NEED(ctx && out, "null handle");
+  TCMIS_CUDA(cudaSetDevice(ctx->device));
+  return gen_rmat(ctx, scale, ef, seed, out);
+}
+
+TCMIS_API int tcmis_gen_grid(tcmis_ctx *ctx, int32_t side, tcmis_graph **out) {
+  NEED(ctx && out, "null handle");
+  TCMIS_CUDA(cudaSetDevice(ctx->device));
+  return gen_grid(ctx, side, out);
+}
+
+TCMIS_API int tcmis_gen_rgg(tcmis_ctx *ctx, int32_t n, uint64_t radius, uint64_t seed,
+                            tcmis_graph **out) {
+  NEED(ctx && out, "null handle");
+  TCMIS_CUDA(cudaSetDevice(ctx->device));
+  return gen_rgg(ctx, n, radius, seed, out);
+}
+
+TCMIS_API int tcmis_gen_gnp_host(int32_t n, double avg, uint64_t seed, int64_t **offsets,
+                                 int32_t **neighbors, int64_t *nnz) {
+  NEED(offsets && neighbors && nnz, "null output");
+  return gen_gnp_host(n, avg, seed, offsets, neighbors, nnz);
+}
+
+TCMIS_API void tcmis_free(void *p) { std::free(p); }
+
+TCMIS_API uint64_t tcmis_rgg_radius(int32_t n, double avg) {
+  if (n <= 0 || avg <= 0.0) return 0;
+  const double r = std::sqrt(avg / (3.14159265358979323846 * (double)n));
+  double R = std::floor(r * 4294967296.0);
+  if (R > 4294967295.0) R = 4294967295.0;
+  return (uint64_t)R;
+}

@@ -1,0 +1,389 @@
+// gen.cu -- synthetic graphs for the BASELINE configs, built on the device.
+//
+// R-MAT (generate.cpp:68-98) is re-derived counter-based: SplitMix64 draw i
+// of seed s is vertex_hash(i, s) (generate.cpp:15-26 + priorities.cpp:21-23),
+// so sample e, level l uses draw e*scale + l and every sample is independent.
+// Normalisation (graph.cpp:14-41: drop loops, add reverse edges, sort, dedupe)
+// is a radix sort + unique over (u << scale | v) keys.  The result is bit-
+// identical to tcmis::rmat_graph (pinned by tests/test_gpu_generators.py).
+//
+// Grid and RGG have no reference generator; their definitions are DESIGN.md's
+// (and oracle/tcmis_oracle.c's).  G(n,p) is inherently serial (one RNG stream
+// with data-dependent consumption) and runs on the host, as in the reference.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace tcmis_b200 {
+
+int wrap_owned(tcmis_ctx *ctx, int32_t n, int64_t nnz, int64_t *d_off, int32_t *d_nbr,
+               tcmis_graph **out);
+
+namespace {
+
+__global__ void k_rmat_keys(int scale, int64_t samples, uint64_t mseed,
+                            unsigned long long *__restrict__ keys) {
+  const uint64_t loop_key = (1ull << (2 * scale)) - 1;  // (n-1, n-1): never a real edge
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < samples;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t u = 0, v = 0;
+    const uint64_t first = (uint64_t)e * (uint64_t)scale;
+    for (int l = 0; l < scale; ++l) {
+      const double r = (double)(vertex_hash_m(first + l, mseed) >> 11) * 0x1.0p-53;
+      u <<= 1;
+      v <<= 1;
+      if (r < 0.57) {
+      } else if (r < 0.76) {
+        v |= 1;
+      } else if (r < 0.95) {
+        u |= 1;
+      } else {
+        u |= 1;
+        v |= 1;
+      }
+    }
+    if (u == v) {
+      keys[2 * e] = loop_key;
+      keys[2 * e + 1] = loop_key;
+    } else {
+      keys[2 * e] = ((uint64_t)u << scale) | v;
+      keys[2 * e + 1] = ((uint64_t)v << scale) | u;
+    }
+  }
+}
+
+// sorted unique keys -> CSR (row starts found at the key where the row changes)
+__global__ void k_keys_to_csr(int scale, int32_t n, int64_t m,
+                              const unsigned long long *__restrict__ keys,
+                              int64_t *__restrict__ off, int32_t *__restrict__ nbr) {
+  const uint64_t mask = (1ull << scale) - 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i < m ? (int64_t)(keys[i] >> scale) : n;
+    const int64_t prev = i > 0 ? (int64_t)(keys[i - 1] >> scale) : -1;
+    for (int64_t r = prev + 1; r <= row; ++r) off[r] = i;
+    if (i < m) nbr[i] = (int32_t)(keys[i] & mask);
+  }
+}
+
+__global__ void k_grid_deg(int32_t side, int64_t *__restrict__ deg) {
+  const int64_t n = (int64_t)side * side;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v <= n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (v == n) {
+      deg[v] = 0;
+      continue;
+    }
+    const int32_t i = (int32_t)(v / side), j = (int32_t)(v % side);
+    deg[v] = (i > 0) + (j > 0) + (j + 1 < side) + (i + 1 < side);
+  }
+}
+
+__global__ void k_grid_fill(int32_t side, const int64_t *__restrict__ off,
+                            int32_t *__restrict__ nbr) {
+  const int64_t n = (int64_t)side * side;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = (int32_t)(v / side), j = (int32_t)(v % side);
+    int64_t w = off[v];
+    if (i > 0) nbr[w++] = (int32_t)(v - side);
+    if (j > 0) nbr[w++] = (int32_t)(v - 1);
+    if (j + 1 < side) nbr[w++] = (int32_t)(v + 1);
+    if (i + 1 < side) nbr[w++] = (int32_t)(v + side);
+  }
+}
+
+// ----------------------------------------------------------------- RGG
+
+__global__ void k_rgg_points(int32_t n, uint64_t mseed, uint64_t R, uint64_t C,
+                             uint32_t *__restrict__ x, uint32_t *__restrict__ y,
+                             unsigned long long *__restrict__ cell, int32_t *__restrict__ ids) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t xv = (uint32_t)(vertex_hash_m(2ull * v, mseed) >> 32);
+    const uint32_t yv = (uint32_t)(vertex_hash_m(2ull * v + 1, mseed) >> 32);
+    x[v] = xv;
+    y[v] = yv;
+    cell[v] = (xv / R) * C + (yv / R);
+    ids[v] = (int32_t)v;
+  }
+}
+
+__global__ void k_cell_starts(int64_t ncell, int32_t n, const unsigned long long *__restrict__ cell,
+                              int64_t *__restrict__ cs) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i < n ? (int64_t)cell[i] : ncell;
+    const int64_t prev = i > 0 ? (int64_t)cell[i - 1] : -1;
+    for (int64_t k = prev + 1; k <= c; ++k) cs[k] = i;
+  }
+}
+
+template <bool fill>
+__global__ void k_rgg_rows(int32_t n, uint64_t R, uint64_t C, const uint32_t *__restrict__ x,
+                           const uint32_t *__restrict__ y, const int64_t *__restrict__ cs,
+                           const int32_t *__restrict__ pts, int64_t *__restrict__ deg,
+                           const int64_t *__restrict__ off, int32_t *__restrict__ nbr) {
+  const uint64_t R2 = R * R;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t xv = x[v], yv = y[v];
+    const int64_t cx = xv / R, cy = yv / R;
+    int64_t w = fill ? off[v] : 0;
+    const int64_t start = w;
+    for (int64_t ax = cx - 1; ax <= cx + 1; ++ax) {
+      if (ax < 0 || ax >= (int64_t)C) continue;
+      for (int64_t ay = cy - 1; ay <= cy + 1; ++ay) {
+        if (ay < 0 || ay >= (int64_t)C) continue;
+        const int64_t c = ax * (int64_t)C + ay;
+        for (int64_t q = cs[c]; q < cs[c + 1]; ++q) {
+          const int32_t u = pts[q];
+          if (u == v) continue;
+          const uint64_t dx = x[u] > xv ? x[u] - xv : xv - x[u];
+          const uint64_t dy = y[u] > yv ? y[u] - yv : yv - y[u];
+          if (dx > R || dy > R) continue;
+          if (dx * dx + dy * dy <= R2) {
+            if (fill) nbr[w] = u;
+            ++w;
+          }
+        }
+      }
+    }
+    if (!fill) {
+      deg[v] = w;
+    } else {  // rows are short (mean ~3): insertion sort in place
+      for (int64_t a = start + 1; a < w; ++a) {
+        const int32_t t = nbr[a];
+        int64_t b = a - 1;
+        while (b >= start && nbr[b] > t) {
+          nbr[b + 1] = nbr[b];
+          --b;
+        }
+        nbr[b + 1] = t;
+      }
+    }
+  }
+}
+
+template <typename T>
+struct DevBuf {
+  T *p = nullptr;
+  ~DevBuf() { cudaFree(p); }
+  int alloc(size_t n) { return dev_alloc(&p, n); }
+  T *release() {
+    T *q = p;
+    p = nullptr;
+    return q;
+  }
+};
+
+int exclusive_scan_i64(tcmis_ctx *ctx, int64_t *d, int64_t count) {
+  size_t bytes = 0;
+  TCMIS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, d, d, count, ctx->stream));
+  DevBuf<char> tmp;
+  if (int rc = tmp.alloc(bytes)) return rc;
+  TCMIS_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, d, d, count, ctx->stream));
+  ctx->launches++;
+  return 0;
+}
+
+}  // namespace
+
+int gen_rmat(tcmis_ctx *ctx, int32_t scale, int32_t ef, uint64_t seed, tcmis_graph **out) {
+  if (scale < 1 || scale > 30)
+    return set_error(TCMIS_E_INVALID_ARGUMENT, "rmat scale must be in [1, 30]");
+  if (ef < 1) return set_error(TCMIS_E_INVALID_ARGUMENT, "edge_factor must be >= 1");
+  cudaStream_t st = ctx->stream;
+  const int32_t n = (int32_t)(1u << scale);
+  const int64_t samples = (int64_t)ef * n;
+  const int64_t nk = 2 * samples;
+  DevBuf<unsigned long long> a, b;
+  if (int rc = a.alloc((size_t)nk)) return rc;
+  if (int rc = b.alloc((size_t)nk)) return rc;
+  k_rmat_keys<<<grid_for(ctx, samples, 256, 16), 256, 0, st>>>(scale, samples, mix64(seed), a.p);
+  TCMIS_LAUNCHED(ctx);
+  {
+    size_t bytes = 0;
+    TCMIS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, a.p, b.p, nk, 0, 2 * scale, st));
+    DevBuf<char> tmp;
+    if (int rc = tmp.alloc(bytes)) return rc;
+    TCMIS_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, bytes, a.p, b.p, nk, 0, 2 * scale, st));
+    ctx->launches++;
+  }
+  DevBuf<int64_t> d_m;
+  if (int rc = d_m.alloc(1)) return rc;
+  {
+    size_t bytes = 0;
+    TCMIS_CUDA(cub::DeviceSelect::Unique(nullptr, bytes, b.p, a.p, d_m.p, nk, st));
+    DevBuf<char> tmp;
+    if (int rc = tmp.alloc(bytes)) return rc;
+    TCMIS_CUDA(cub::DeviceSelect::Unique(tmp.p, bytes, b.p, a.p, d_m.p, nk, st));
+    ctx->launches++;
+  }
+  int64_t m = 0;
+  TCMIS_CUDA(cudaMemcpyAsync(&m, d_m.p, 8, cudaMemcpyDeviceToHost, st));
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  // drop the loop sentinel (the largest possible key) if present
+  if (m > 0) {
+    unsigned long long last = 0;
+    TCMIS_CUDA(cudaMemcpy(&last, a.p + (m - 1), 8, cudaMemcpyDeviceToHost));
+    if (last == (1ull << (2 * scale)) - 1) --m;
+  }
+  DevBuf<int64_t> off;
+  DevBuf<int32_t> nbr;
+  if (int rc = off.alloc((size_t)n + 1)) return rc;
+  if (int rc = nbr.alloc((size_t)m)) return rc;
+  k_keys_to_csr<<<grid_for(ctx, m + 1, 256, 16), 256, 0, st>>>(scale, n, m, a.p, off.p, nbr.p);
+  TCMIS_LAUNCHED(ctx);
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  int64_t *o = off.release();
+  int32_t *q = nbr.release();
+  return wrap_owned(ctx, n, m, o, q, out);
+}
+
+int gen_grid(tcmis_ctx *ctx, int32_t side, tcmis_graph **out) {
+  if (side < 0 || (int64_t)side * side > 0x7fffffffLL)
+    return set_error(TCMIS_E_INVALID_ARGUMENT, "grid side out of range");
+  cudaStream_t st = ctx->stream;
+  const int64_t n = (int64_t)side * side;
+  const int64_t m = side > 1 ? 4ll * side * (side - 1) : 0;
+  DevBuf<int64_t> off;
+  DevBuf<int32_t> nbr;
+  if (int rc = off.alloc((size_t)n + 1)) return rc;
+  if (int rc = nbr.alloc((size_t)m)) return rc;
+  k_grid_deg<<<grid_for(ctx, n + 1, 256, 16), 256, 0, st>>>(side, off.p);
+  TCMIS_LAUNCHED(ctx);
+  if (int rc = exclusive_scan_i64(ctx, off.p, n + 1)) return rc;
+  k_grid_fill<<<grid_for(ctx, n, 256, 16), 256, 0, st>>>(side, off.p, nbr.p);
+  TCMIS_LAUNCHED(ctx);
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  int64_t *o = off.release();
+  int32_t *q = nbr.release();
+  return wrap_owned(ctx, (int32_t)n, m, o, q, out);
+}
+
+int gen_rgg(tcmis_ctx *ctx, int32_t n, uint64_t R, uint64_t seed, tcmis_graph **out) {
+  if (n < 0) return set_error(TCMIS_E_INVALID_ARGUMENT, "n must be non-negative");
+  cudaStream_t st = ctx->stream;
+  if (n == 0 || R == 0) {  // edgeless
+    DevBuf<int64_t> off;
+    if (int rc = off.alloc((size_t)n + 1)) return rc;
+    TCMIS_CUDA(cudaMemsetAsync(off.p, 0, 8ull * (n + 1), st));
+    TCMIS_CUDA(cudaStreamSynchronize(st));
+    int32_t *q = nullptr;
+    if (int rc = dev_alloc(&q, 1)) return rc;
+    int64_t *o = off.release();
+    return wrap_owned(ctx, n, 0, o, q, out);
+  }
+  const uint64_t C = 4294967295ull / R + 1;
+  const uint64_t ncell = C * C;
+  int cell_bits = 1;
+  while (cell_bits < 64 && (1ull << cell_bits) <= ncell) ++cell_bits;
+  DevBuf<uint32_t> x, y;
+  DevBuf<unsigned long long> cell, cell2;
+  DevBuf<int32_t> ids, pts;
+  if (int rc = x.alloc(n)) return rc;
+  if (int rc = y.alloc(n)) return rc;
+  if (int rc = cell.alloc(n)) return rc;
+  if (int rc = cell2.alloc(n)) return rc;
+  if (int rc = ids.alloc(n)) return rc;
+  if (int rc = pts.alloc(n)) return rc;
+  k_rgg_points<<<grid_for(ctx, n, 256, 16), 256, 0, st>>>(n, mix64(seed), R, C, x.p, y.p, cell.p,
+                                                           ids.p);
+  TCMIS_LAUNCHED(ctx);
+  {
+    size_t bytes = 0;
+    TCMIS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, cell.p, cell2.p, ids.p, pts.p,
+                                               (int64_t)n, 0, cell_bits, st));
+    DevBuf<char> tmp;
+    if (int rc = tmp.alloc(bytes)) return rc;
+    TCMIS_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, cell.p, cell2.p, ids.p, pts.p,
+                                               (int64_t)n, 0, cell_bits, st));
+    ctx->launches++;
+  }
+  DevBuf<int64_t> cs;
+  if (int rc = cs.alloc(ncell + 1)) return rc;
+  k_cell_starts<<<grid_for(ctx, n + 1, 256, 16), 256, 0, st>>>((int64_t)ncell, n, cell2.p, cs.p);
+  TCMIS_LAUNCHED(ctx);
+  DevBuf<int64_t> off;
+  if (int rc = off.alloc((size_t)n + 1)) return rc;
+  TCMIS_CUDA(cudaMemsetAsync(off.p + n, 0, 8, st));
+  k_rgg_rows<false><<<grid_for(ctx, n, 256, 16), 256, 0, st>>>(n, R, C, x.p, y.p, cs.p, pts.p,
+                                                               off.p, nullptr, nullptr);
+  TCMIS_LAUNCHED(ctx);
+  if (int rc = exclusive_scan_i64(ctx, off.p, (int64_t)n + 1)) return rc;
+  int64_t m = 0;
+  TCMIS_CUDA(cudaMemcpyAsync(&m, off.p + n, 8, cudaMemcpyDeviceToHost, st));
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  DevBuf<int32_t> nbr;
+  if (int rc = nbr.alloc((size_t)m)) return rc;
+  k_rgg_rows<true><<<grid_for(ctx, n, 256, 16), 256, 0, st>>>(n, R, C, x.p, y.p, cs.p, pts.p,
+                                                              nullptr, off.p, nbr.p);
+  TCMIS_LAUNCHED(ctx);
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  int64_t *o = off.release();
+  int32_t *q = nbr.release();
+  return wrap_owned(ctx, n, m, o, q, out);
+}
+
+// generate.cpp:30-66 on the host: the gap sequence is one serial RNG stream.
+int gen_gnp_host(int32_t n, double avg_degree, uint64_t seed, int64_t **offsets,
+                 int32_t **neighbors, int64_t *nnz_out) {
+  if (n < 0) return set_error(TCMIS_E_INVALID_ARGUMENT, "n must be non-negative");
+  const double p = n > 1 ? avg_degree / (double)(n - 1) : 0.0;
+  std::vector<uint64_t> keys;  // directed (u << 32 | v)
+  if (!(p <= 0.0 || n < 2)) {
+    if (p >= 1.0) {
+      for (int32_t u = 0; u < n; ++u)
+        for (int32_t v = u + 1; v < n; ++v) {
+          keys.push_back(((uint64_t)u << 32) | (uint32_t)v);
+          keys.push_back(((uint64_t)v << 32) | (uint32_t)u);
+        }
+    } else {
+      uint64_t state = mix64(seed);
+      const double log_q = std::log1p(-p);
+      const int64_t total = (int64_t)n * (n - 1) / 2;
+      int64_t idx = -1, row = 0, row_start = 0, row_len = n - 1;
+      for (;;) {
+        state += kGolden;
+        const double u = (double)(mix64(state) >> 11) * 0x1.0p-53;
+        const int64_t gap = (int64_t)std::floor(std::log1p(-u) / log_q);
+        idx += 1 + gap;
+        if (idx >= total) break;
+        while (idx - row_start >= row_len) {
+          row_start += row_len;
+          ++row;
+          --row_len;
+        }
+        const uint32_t a = (uint32_t)row, b = (uint32_t)(row + 1 + (idx - row_start));
+        keys.push_back(((uint64_t)a << 32) | b);
+        keys.push_back(((uint64_t)b << 32) | a);
+      }
+    }
+  }
+  std::sort(keys.begin(), keys.end());
+  keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+  int64_t *off = (int64_t *)std::calloc((size_t)n + 1, sizeof(int64_t));
+  int32_t *nbr = (int32_t *)std::malloc(sizeof(int32_t) * (keys.size() + 1));
+  if (!off || !nbr) {
+    std::free(off);
+    std::free(nbr);
+    return set_error(TCMIS_E_RUNTIME, "out of host memory");
+  }
+  for (size_t i = 0; i < keys.size(); ++i) {
+    off[(keys[i] >> 32) + 1]++;
+    nbr[i] = (int32_t)(uint32_t)keys[i];
+  }
+  for (int32_t v = 0; v < n; ++v) off[v + 1] += off[v];
+  *offsets = off;
+  *neighbors = nbr;
+  *nnz_out = (int64_t)keys.size();
+  return 0;
+}
+
+}  // namespace tcmis_b200

@@ -1,0 +1,148 @@
+// internal.cuh -- shared types and device helpers of the B200 TC-MIS engine.
+//
+// Layout in HBM (per graph):
+//   d_off   int64[n+1]   CSR row extents (graph.hpp:20)
+//   d_nbr   int32[2m]    sorted neighbour ids (graph.hpp:21)
+//   key     uint64[n]    (p[v] << 32) | (v + 1) while v is alive, 0 once it
+//                        left (priorities.hpp:61-64; 0 == kNoNeighborKey, so a
+//                        dead neighbour can never block a candidate)
+//   state   uint8[n]     VertexState (engine.hpp:17)
+//   next    uint8[n]     this round's decision: 1 = candidate, 2 = excluded
+//   wl[2]   int32[n]     alive worklists (compacted between rounds)
+//   segflag uint8[nb]    "block column b holds a candidate this round"
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "tcmis_b200.h"
+
+namespace tcmis_b200 {
+
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
+
+// priorities.cpp:15-19
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+// priorities.cpp:21-23, with mix64(seed) hoisted by the caller
+__host__ __device__ __forceinline__ uint64_t vertex_hash_m(uint64_t v, uint64_t mixed_seed) {
+  return mix64(mixed_seed + (v + 1) * kGolden);
+}
+// priorities.cpp:29-31
+__host__ __device__ __forceinline__ uint64_t combine_seed(uint64_t seed, uint64_t round) {
+  return mix64(seed + mix64(round + kGolden));
+}
+
+// Per-round statistics as the device accumulates them.
+struct DevRound {
+  unsigned long long sel, rem, alive, eval, skip;
+};
+
+// Device control block driving the round loop (one per solve workspace).
+struct Ctrl {
+  int32_t round;       // 1-based round being executed
+  int32_t wl_count[2]; // worklist sizes; round r reads slot r&1 (r >= 2)
+  int32_t alive;       // alive vertices after the last completed round
+  unsigned long long sel, rem, eval;  // accumulators of the running round
+  unsigned int ticket; // last-block election in k_update
+  int32_t max_rounds;  // capacity of the DevRound array
+  int32_t overflow;    // set when rounds exceeded max_rounds
+  int32_t pad;
+};
+
+struct Workspace {
+  size_t n_cap = 0;
+  size_t seg_cap = 0;
+  uint64_t *key = nullptr;
+  uint8_t *state = nullptr;
+  uint8_t *next = nullptr;
+  int32_t *wl[2] = {nullptr, nullptr};
+  uint8_t *segflag = nullptr;
+  int32_t *mis = nullptr;
+  int64_t *mis_count = nullptr;
+  Ctrl *ctrl = nullptr;        // device
+  Ctrl *h_ctrl = nullptr;      // pinned host mirror
+  DevRound *rounds = nullptr;  // device, capacity round_cap
+  DevRound *h_rounds = nullptr;
+  int32_t round_cap = 0;
+  void *cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+};
+
+}  // namespace tcmis_b200
+
+struct tcmis_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int64_t launches = 0;
+  cudaEvent_t ev[8] = {};
+};
+
+struct tcmis_graph {
+  tcmis_ctx *ctx = nullptr;
+  int32_t n = 0;
+  int64_t nnz = 0;
+  int64_t *d_off = nullptr;
+  int32_t *d_nbr = nullptr;
+  bool owns = false;
+  // tiling cache for the tile counters (one tile_dim at a time)
+  int32_t tile_T = 0;
+  int32_t tile_nb = 0;
+  int32_t *d_rowtiles = nullptr;
+  int64_t tile_total = 0;
+  tcmis_b200::Workspace ws;
+};
+
+namespace tcmis_b200 {
+
+// error plumbing (capi.cu)
+int set_error(int code, const std::string &msg);
+int cuda_error(cudaError_t e, const char *what);
+
+#define TCMIS_CUDA(expr)                                        \
+  do {                                                          \
+    cudaError_t _e = (expr);                                    \
+    if (_e != cudaSuccess) return ::tcmis_b200::cuda_error(_e, #expr); \
+  } while (0)
+
+#define TCMIS_LAUNCHED(ctx)                                        \
+  do {                                                             \
+    (ctx)->launches++;                                             \
+    cudaError_t _e = cudaGetLastError();                           \
+    if (_e != cudaSuccess) return ::tcmis_b200::cuda_error(_e, "kernel launch"); \
+  } while (0)
+
+inline int grid_for(const tcmis_ctx *ctx, int64_t work_threads, int block, int per_sm = 8) {
+  int64_t want = (work_threads + block - 1) / block;
+  int64_t cap = (int64_t)ctx->num_sms * per_sm;
+  if (want < 1) want = 1;
+  return (int)(want < cap ? want : cap);
+}
+
+// workspace management (solver.cu)
+int ensure_workspace(tcmis_graph *g);
+int ensure_cub(tcmis_graph *g, size_t bytes);
+void free_workspace(Workspace &ws);
+
+// tiling (tiles.cu)
+int build_tile_counts(tcmis_graph *g, int T);
+int export_tiles(tcmis_graph *g, int T, int32_t *tile_row, int32_t *tile_col,
+                 uint64_t *row_bits, int64_t *bro);
+
+// scratch allocation helper that records the CUDA error
+template <typename T>
+int dev_alloc(T **p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void **)p, count * sizeof(T));
+  if (e != cudaSuccess) return cuda_error(e, "cudaMalloc");
+  return 0;
+}
+
+}  // namespace tcmis_b200

@@ -1,0 +1,661 @@
+// solver.cu -- the TC-MIS round loop on sm_100a.
+//
+// One round of the reference (engine.cpp:247-291) is two kernels here:
+//
+//   k_select  Phase 1 + Phase 2 fused.  For every alive vertex v of the
+//             worklist, a group of G lanes walks N(v) and asks "is any alive
+//             neighbour's key above mine?" (compute_max_np + generate_candidates,
+//             engine.cpp:86-119, restated as max(key[u]) < key[v] with dead
+//             keys = 0).  A candidate immediately scatters "excluded" to its
+//             neighbours (the push form of tiled_spmv's nc > 0, spmv.cpp:18-59):
+//             the decision array `next` is never read inside the kernel, so
+//             the round's snapshot semantics are preserved.
+//   k_update  Phase 3 (engine.cpp:121-160) + worklist compaction + the round's
+//             statistics (IterationStats, engine.hpp:24-34) and tile counters.
+//
+// Rounds stay bulk-synchronous, so the round count and every per-round stat
+// equal the reference's (SURVEY 7 "Keep the rounds bulk-synchronous").
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace tcmis_b200 {
+
+// ------------------------------------------------------------- priorities
+
+// priorities.cpp:43-51, with every IEEE operation spelled out so that no
+// contraction or fast-math can change a bit.
+__device__ __forceinline__ uint32_t h2_value(double avg, int64_t deg, double eps, double scale) {
+  double d = __dadd_rn(__dadd_rn(avg, (double)deg), -eps);
+  if (d < 1.0 / 1024.0) d = 1.0 / 1024.0;
+  double s = floor(__dmul_rn(__ddiv_rn(avg, d), scale));
+  if (s < 0.0) return 0u;
+  if (s >= 4294967295.0) return 0xffffffffu;
+  return (uint32_t)s;
+}
+
+// K2: priorities (priorities.cpp:33-67) + key/state initialisation.
+// mode 0: h1 / luby-fresh hash priorities from `mseed` (= mix64(seed'));
+// mode 1: h2 degree-aware priorities.
+__global__ void k_priorities(int32_t n, const int64_t *__restrict__ off, int mode,
+                             uint64_t mseed, double avg, double scale, uint64_t *__restrict__ key,
+                             uint32_t *__restrict__ p_out, uint8_t *__restrict__ state,
+                             uint8_t *__restrict__ next) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t h = vertex_hash_m((uint64_t)v, mseed);
+    uint32_t p;
+    if (mode == 0) {
+      p = (uint32_t)(h >> 32);
+    } else {
+      double eps = (double)(h >> 11) * 0x1.0p-53;  // hash_to_unit, priorities.cpp:25-27
+      p = h2_value(avg, off[v + 1] - off[v], eps, scale);
+    }
+    if (p_out) p_out[v] = p;
+    if (key) key[v] = ((uint64_t)p << 32) | (uint64_t)(v + 1);
+    if (state) state[v] = TCMIS_ALIVE;
+    if (next) next[v] = 0;
+  }
+}
+
+// ----------------------------------------------------------------- rounds
+
+// G lanes per vertex; the row is walked from its end (on R-MAT the high ids
+// at the end of a sorted row are the low-degree, high-priority vertices, so a
+// blocked vertex exits after the first chunk -- any order gives the same
+// answer).
+template <int G>
+__global__ void __launch_bounds__(256)
+    k_select(int32_t n, const int64_t *__restrict__ off, const int32_t *__restrict__ nbr,
+             const uint64_t *__restrict__ key, uint8_t *__restrict__ next,
+             uint8_t *__restrict__ segflag, int T, const Ctrl *__restrict__ ctrl,
+             const int32_t *__restrict__ wl0, const int32_t *__restrict__ wl1) {
+  const int round = ctrl->round;
+  const int64_t cnt = round == 1 ? n : ctrl->wl_count[round & 1];
+  const int32_t *wl = (round & 1) ? wl1 : wl0;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  const int64_t gstride = ((int64_t)gridDim.x * blockDim.x) / G;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; i < cnt; i += gstride) {
+    const int32_t v = round == 1 ? (int32_t)i : wl[i];
+    const int64_t s = off[v], e = off[v + 1];
+    const uint64_t kv = key[v];
+    bool blocked = false;
+    for (int64_t base = e - G; base + G > s; base -= G) {
+      const int64_t idx = base + gl;
+      bool b = false;
+      if (idx >= s) b = __ldg(&key[__ldg(&nbr[idx])]) > kv;
+      if (__ballot_sync(gmask, b)) {
+        blocked = true;
+        break;
+      }
+    }
+    if (!blocked) {
+      if (gl == 0) {
+        next[v] = 1;
+        if (segflag) segflag[v / T] = 1;
+      }
+      for (int64_t idx = s + gl; idx < e; idx += G) next[__ldg(&nbr[idx])] = 2;
+    }
+  }
+}
+
+// Block-wide sum of three counters into the control block.
+__device__ __forceinline__ void block_add3(unsigned long long a, unsigned long long b,
+                                           unsigned long long c, Ctrl *ctrl) {
+  __shared__ unsigned long long sh[3][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+    c += __shfl_down_sync(0xffffffffu, c, o);
+  }
+  if (lane == 0) {
+    sh[0][w] = a;
+    sh[1][w] = b;
+    sh[2][w] = c;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    a = lane < nw ? sh[0][lane] : 0;
+    b = lane < nw ? sh[1][lane] : 0;
+    c = lane < nw ? sh[2][lane] : 0;
+    for (int o = 16; o; o >>= 1) {
+      a += __shfl_down_sync(0xffffffffu, a, o);
+      b += __shfl_down_sync(0xffffffffu, b, o);
+      c += __shfl_down_sync(0xffffffffu, c, o);
+    }
+    if (lane == 0) {
+      if (a) atomicAdd(&ctrl->sel, a);
+      if (b) atomicAdd(&ctrl->rem, b);
+      if (c) atomicAdd(&ctrl->eval, c);
+    }
+  }
+}
+
+// seg_mode: 0 = no tile counters, 1 = count and clear per round,
+// 2 = accumulate (h3: counters are taken once at the end).
+__global__ void __launch_bounds__(256)
+    k_update(int32_t n, uint64_t *__restrict__ key, uint8_t *__restrict__ state,
+             uint8_t *__restrict__ next, Ctrl *__restrict__ ctrl, int32_t *__restrict__ wl0,
+             int32_t *__restrict__ wl1, uint8_t *__restrict__ segflag,
+             const int32_t *__restrict__ rowtiles, int32_t nseg, int64_t total_tiles,
+             int seg_mode, DevRound *__restrict__ rounds, int fresh, uint64_t seed) {
+  const int round = ctrl->round;
+  const int64_t cnt = round == 1 ? n : ctrl->wl_count[round & 1];
+  const int32_t *in = (round & 1) ? wl1 : wl0;
+  int32_t *out = (round & 1) ? wl0 : wl1;
+  const int out_slot = (round + 1) & 1;
+  const uint64_t fresh_m = fresh ? mix64(combine_seed(seed, (uint64_t)round + 1)) : 0;
+  const int lane = threadIdx.x & 31;
+  unsigned long long sel = 0, rem = 0, ev = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < cnt; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    bool surv = false;
+    int32_t v = 0;
+    if (i < cnt) {
+      v = round == 1 ? (int32_t)i : in[i];
+      const uint8_t d = next[v];
+      if (d == 1) {  // engine.cpp:137-143: candidate joins the MIS
+        state[v] = TCMIS_IN_MIS;
+        key[v] = 0;
+        next[v] = 0;
+        ++sel;
+      } else if (d == 2) {  // engine.cpp:144-147: alive with a candidate neighbour
+        state[v] = TCMIS_REMOVED;
+        key[v] = 0;
+        next[v] = 0;
+        ++rem;
+      } else {
+        surv = true;
+        if (fresh)  // engine.cpp:324-325: next round's redrawn priority
+          key[v] = ((vertex_hash_m((uint64_t)v, fresh_m) >> 32) << 32) | (uint64_t)(v + 1);
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, surv);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      int pos = 0;
+      if (lane == leader) pos = atomicAdd(&ctrl->wl_count[out_slot], __popc(m));
+      pos = __shfl_sync(0xffffffffu, pos, leader);
+      if (surv) out[pos + __popc(m & ((1u << lane) - 1u))] = v;
+    }
+  }
+  if (seg_mode == 1) {  // spmv.cpp:37-46, per block column (A is symmetric)
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nseg; b += stride) {
+      if (segflag[b]) {
+        ev += (unsigned long long)rowtiles[b];
+        segflag[b] = 0;
+      }
+    }
+  }
+  block_add3(sel, rem, ev, ctrl);
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&ctrl->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    volatile Ctrl *vc = ctrl;
+    const int32_t alive = vc->wl_count[out_slot];
+    if (round - 1 < vc->max_rounds) {
+      DevRound r;
+      r.sel = vc->sel;
+      r.rem = vc->rem;
+      r.alive = (unsigned long long)alive;
+      r.eval = seg_mode == 1 ? vc->eval : 0;
+      r.skip = seg_mode == 1 ? (unsigned long long)total_tiles - vc->eval : 0;
+      rounds[round - 1] = r;
+    } else {
+      vc->overflow = 1;
+    }
+    vc->alive = alive;
+    vc->sel = 0;
+    vc->rem = 0;
+    vc->eval = 0;
+    vc->ticket = 0;
+    vc->wl_count[round & 1] = 0;
+    vc->round = round + 1;
+  }
+}
+
+// h3: tile counters of the single collapsed iteration (segments that hold
+// any MIS vertex).
+__global__ void k_seg_total(const uint8_t *__restrict__ segflag,
+                            const int32_t *__restrict__ rowtiles, int32_t nseg, Ctrl *ctrl) {
+  unsigned long long ev = 0;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nseg;
+       b += (int64_t)gridDim.x * blockDim.x)
+    if (segflag[b]) ev += (unsigned long long)rowtiles[b];
+  block_add3(0, 0, ev, ctrl);
+}
+
+struct IsInMIS {
+  const uint8_t *state;
+  __device__ __forceinline__ bool operator()(int32_t v) const { return state[v] == TCMIS_IN_MIS; }
+};
+
+// ------------------------------------------------- phase helpers (parity)
+
+__global__ void k_max_np(int32_t n, const int64_t *__restrict__ off,
+                         const int32_t *__restrict__ nbr, const uint32_t *__restrict__ p,
+                         const uint8_t *__restrict__ st, uint64_t *__restrict__ out) {
+  // engine.cpp:86-103, warp per vertex
+  const int lane = threadIdx.x & 31;
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n;
+       v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    unsigned long long best = 0;
+    if (st[v] == TCMIS_ALIVE)
+      for (int64_t e = off[v] + lane; e < off[v + 1]; e += 32) {
+        const int32_t u = nbr[e];
+        if (st[u] == TCMIS_ALIVE) {
+          unsigned long long k = ((unsigned long long)p[u] << 32) | (unsigned long long)(u + 1);
+          best = k > best ? k : best;
+        }
+      }
+    for (int o = 16; o; o >>= 1) {
+      unsigned long long t = __shfl_down_sync(0xffffffffu, best, o);
+      best = t > best ? t : best;
+    }
+    if (lane == 0) out[v] = best;
+  }
+}
+
+__global__ void k_neighbor_count(int32_t n, const int64_t *__restrict__ off,
+                                 const int32_t *__restrict__ nbr, const uint8_t *__restrict__ c,
+                                 int32_t *__restrict__ nc) {
+  // spmv.cpp:61-73, warp per vertex
+  const int lane = threadIdx.x & 31;
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n;
+       v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    int cnt = 0;
+    for (int64_t e = off[v] + lane; e < off[v + 1]; e += 32) cnt += c[nbr[e]] != 0;
+    for (int o = 16; o; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+    if (lane == 0) nc[v] = cnt;
+  }
+}
+
+__global__ void k_segflags_from(int32_t n, const uint8_t *__restrict__ c, int T,
+                                uint8_t *__restrict__ segflag) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    if (c[v]) segflag[v / T] = 1;
+}
+
+// -------------------------------------------------------------- workspace
+
+void free_workspace(Workspace &ws) {
+  cudaFree(ws.key);
+  cudaFree(ws.state);
+  cudaFree(ws.next);
+  cudaFree(ws.wl[0]);
+  cudaFree(ws.wl[1]);
+  cudaFree(ws.segflag);
+  cudaFree(ws.mis);
+  cudaFree(ws.mis_count);
+  cudaFree(ws.ctrl);
+  cudaFreeHost(ws.h_ctrl);
+  cudaFree(ws.rounds);
+  cudaFreeHost(ws.h_rounds);
+  cudaFree(ws.cub_tmp);
+  ws = Workspace{};
+}
+
+int ensure_cub(tcmis_graph *g, size_t bytes) {
+  Workspace &ws = g->ws;
+  if (bytes <= ws.cub_bytes) return 0;
+  cudaFree(ws.cub_tmp);
+  ws.cub_tmp = nullptr;
+  ws.cub_bytes = 0;
+  if (int rc = dev_alloc((char **)&ws.cub_tmp, bytes)) return rc;
+  ws.cub_bytes = bytes;
+  return 0;
+}
+
+int ensure_workspace(tcmis_graph *g) {
+  Workspace &ws = g->ws;
+  const size_t n = (size_t)std::max<int32_t>(g->n, 1);
+  if (ws.n_cap < n) {
+    cudaFree(ws.key);
+    cudaFree(ws.state);
+    cudaFree(ws.next);
+    cudaFree(ws.wl[0]);
+    cudaFree(ws.wl[1]);
+    cudaFree(ws.mis);
+    ws.n_cap = 0;
+    if (int rc = dev_alloc(&ws.key, n)) return rc;
+    if (int rc = dev_alloc(&ws.state, n)) return rc;
+    if (int rc = dev_alloc(&ws.next, n)) return rc;
+    if (int rc = dev_alloc(&ws.wl[0], n)) return rc;
+    if (int rc = dev_alloc(&ws.wl[1], n)) return rc;
+    if (int rc = dev_alloc(&ws.mis, n)) return rc;
+    TCMIS_CUDA(cudaMemsetAsync(ws.next, 0, n, g->ctx->stream));
+    ws.n_cap = n;
+  }
+  // segment flags for any tile_dim >= 1
+  if (ws.seg_cap < n) {
+    cudaFree(ws.segflag);
+    if (int rc = dev_alloc(&ws.segflag, n)) return rc;
+    TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, n, g->ctx->stream));
+    ws.seg_cap = n;
+  }
+  if (!ws.ctrl) {
+    if (int rc = dev_alloc(&ws.ctrl, 1)) return rc;
+    if (int rc = dev_alloc(&ws.mis_count, 1)) return rc;
+    TCMIS_CUDA(cudaMallocHost((void **)&ws.h_ctrl, sizeof(Ctrl)));
+    ws.round_cap = 4096;
+    if (int rc = dev_alloc(&ws.rounds, (size_t)ws.round_cap)) return rc;
+    TCMIS_CUDA(cudaMallocHost((void **)&ws.h_rounds, sizeof(DevRound) * ws.round_cap));
+  }
+  size_t need = 0, t = 0;
+  thrust::counting_iterator<int32_t> ids(0);
+  TCMIS_CUDA(cub::DeviceSelect::If(nullptr, t, ids, ws.mis, ws.mis_count, (int64_t)n,
+                                   IsInMIS{ws.state}, g->ctx->stream));
+  need = std::max(need, t);
+  return ensure_cub(g, need);
+}
+
+// ------------------------------------------------------------------ solve
+
+namespace {
+
+double avg_degree(const tcmis_graph *g) {
+  // priorities.cpp:60 avg = 2.0 * num_edges / n, num_edges = nnz / 2
+  return 2.0 * (double)(g->nnz / 2) / (double)g->n;
+}
+
+int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
+                      uint64_t *key, uint32_t *p_out, uint8_t *state, uint8_t *next) {
+  tcmis_ctx *ctx = g->ctx;
+  int mode = 1;
+  uint64_t mseed = mix64(seed);
+  if (heuristic == TCMIS_H1) {
+    mode = 0;
+  } else if (heuristic == TCMIS_LUBY_FRESH) {
+    mode = 0;
+    mseed = mix64(combine_seed(seed, 1));  // engine.cpp:324-325, iteration 1
+  }
+  const double scale = mode ? (double)(1u << scale_bits) : 0.0;
+  const int grid = grid_for(ctx, g->n, 256, 16);
+  k_priorities<<<grid, 256, 0, ctx->stream>>>(g->n, g->d_off, mode, mseed,
+                                               mode ? avg_degree(g) : 0.0, scale, key, p_out,
+                                               state, next);
+  TCMIS_LAUNCHED(ctx);
+  return 0;
+}
+
+int validate(const tcmis_graph *g, const tcmis_config *c) {
+  if (c->heuristic < TCMIS_H1 || c->heuristic > TCMIS_LUBY_PERM)
+    return set_error(TCMIS_E_INVALID_ARGUMENT, "unknown heuristic id");
+  const bool tiled = c->heuristic <= TCMIS_H3;
+  // run_tc_mis(g, cfg) tiles first: tile_dim is checked even for n == 0
+  // (engine.cpp:297-299 -> tiling.cpp:17-21).
+  if (tiled && (c->tile_dim < 1 || c->tile_dim > 64))
+    return set_error(TCMIS_E_INVALID_ARGUMENT,
+                     "tile_dim must be in [1, 64], got " + std::to_string(c->tile_dim));
+  if (g->n == 0) return 0;
+  if ((c->heuristic == TCMIS_H2 || c->heuristic == TCMIS_H3 ||
+       c->heuristic == TCMIS_LUBY_PERM) &&
+      (c->scale_bits < 8 || c->scale_bits > 30))
+    return set_error(TCMIS_E_INVALID_ARGUMENT, "scale_bits must be in [8, 30]");
+  return 0;
+}
+
+}  // namespace
+
+int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
+               int32_t max_stats, int32_t *n_iter, int64_t *mis_count_out) {
+  if (int rc = validate(g, cfg)) return rc;
+  *n_iter = 0;
+  *mis_count_out = 0;
+  if (g->n == 0) return 0;  // engine.cpp:240 / 307
+  tcmis_ctx *ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  if (int rc = ensure_workspace(g)) return rc;
+  Workspace &ws = g->ws;
+  const int H = cfg->heuristic;
+  const bool tiled = H <= TCMIS_H3;
+  const bool fresh = H == TCMIS_LUBY_FRESH;
+  const int T = cfg->tile_dim;
+  if (tiled && g->tile_T != T)
+    if (int rc = build_tile_counts(g, T)) return rc;
+  const int32_t nseg = tiled ? g->tile_nb : 0;
+  const int seg_mode = !tiled ? 0 : (H == TCMIS_H3 ? 2 : 1);
+  const bool timing = (cfg->flags & TCMIS_F_TIMING) != 0;
+
+  if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.key, nullptr, ws.state,
+                                 ws.next))
+    return rc;
+  Ctrl c0{};
+  c0.round = 1;
+  c0.alive = g->n;
+  c0.max_rounds = ws.round_cap;
+  *ws.h_ctrl = c0;
+  TCMIS_CUDA(cudaMemcpyAsync(ws.ctrl, ws.h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+  if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
+
+  const int sel_grid = ctx->num_sms * 8;
+  const int upd_grid = ctx->num_sms * 4;
+  std::vector<uint8_t> h_next, h_state, h_cand;
+  std::vector<tcmis_iter_stats> local;
+  std::vector<float> t1, t3;
+  int round = 0;
+  for (;;) {
+    ++round;
+    if (round > g->n)  // engine.cpp:248-249
+      return set_error(TCMIS_E_RUNTIME, "iteration cap exceeded; engine livelock");
+    if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[0], st));
+    k_select<8><<<sel_grid, 256, 0, st>>>(g->n, g->d_off, g->d_nbr, ws.key, ws.next,
+                                          seg_mode ? ws.segflag : nullptr, T > 0 ? T : 1,
+                                          ws.ctrl, ws.wl[0], ws.wl[1]);
+    TCMIS_LAUNCHED(ctx);
+    if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[1], st));
+    if (cfg->observer && H != TCMIS_H3) {
+      h_next.resize(g->n);
+      h_state.resize(g->n);
+      h_cand.resize(g->n);
+      TCMIS_CUDA(cudaMemcpyAsync(h_next.data(), ws.next, g->n, cudaMemcpyDeviceToHost, st));
+      TCMIS_CUDA(cudaMemcpyAsync(h_state.data(), ws.state, g->n, cudaMemcpyDeviceToHost, st));
+      TCMIS_CUDA(cudaStreamSynchronize(st));
+      for (int32_t v = 0; v < g->n; ++v) h_cand[v] = h_next[v] == 1 && h_state[v] == TCMIS_ALIVE;
+      cfg->observer(cfg->observer_user, round, h_cand.data(), h_state.data(), g->n);
+    }
+    k_update<<<upd_grid, 256, 0, st>>>(g->n, ws.key, ws.state, ws.next, ws.ctrl, ws.wl[0],
+                                       ws.wl[1], ws.segflag, g->d_rowtiles, nseg, g->tile_total,
+                                       seg_mode, ws.rounds, fresh ? 1 : 0, cfg->seed);
+    TCMIS_LAUNCHED(ctx);
+    if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[2], st));
+    TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    TCMIS_CUDA(cudaStreamSynchronize(st));
+    if (timing) {
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+      cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
+      t1.push_back(a);
+      t3.push_back(b);
+    }
+    if (ws.h_ctrl->alive == 0) break;
+  }
+  const int rounds_run = round;
+  if (rounds_run > ws.round_cap)
+    return set_error(TCMIS_E_RUNTIME, "round statistics capacity exceeded");
+  TCMIS_CUDA(cudaMemcpyAsync(ws.h_rounds, ws.rounds, sizeof(DevRound) * rounds_run,
+                             cudaMemcpyDeviceToHost, st));
+  // ascending MIS ids (engine.cpp:293 sorts; ordered compaction needs no sort)
+  {
+    thrust::counting_iterator<int32_t> ids(0);
+    size_t bytes = ws.cub_bytes;
+    TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
+                                     (int64_t)g->n, IsInMIS{ws.state}, st));
+    ctx->launches += 1;
+  }
+  int64_t h_mis_count = 0;
+  TCMIS_CUDA(cudaMemcpyAsync(&h_mis_count, ws.mis_count, sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, st));
+  unsigned long long h3_eval = 0;
+  if (seg_mode == 2) {
+    TCMIS_CUDA(cudaMemsetAsync(&ws.ctrl->eval, 0, sizeof(unsigned long long), st));
+    k_seg_total<<<grid_for(ctx, nseg, 256, 4), 256, 0, st>>>(ws.segflag, g->d_rowtiles, nseg,
+                                                             ws.ctrl);
+    TCMIS_LAUNCHED(ctx);
+    TCMIS_CUDA(cudaMemcpyAsync(&h3_eval, &ws.ctrl->eval, sizeof(h3_eval),
+                               cudaMemcpyDeviceToHost, st));
+  }
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  *mis_count_out = h_mis_count;
+
+  if (H == TCMIS_H3) {
+    // engine.cpp:255-258: the h3 candidate vector is already the whole MIS,
+    // so the reference reports exactly one iteration.
+    if (cfg->observer) {
+      h_state.assign(g->n, TCMIS_ALIVE);
+      h_cand.resize(g->n);
+      std::vector<uint8_t> fin(g->n);
+      TCMIS_CUDA(cudaMemcpy(fin.data(), ws.state, g->n, cudaMemcpyDeviceToHost));
+      for (int32_t v = 0; v < g->n; ++v) h_cand[v] = fin[v] == TCMIS_IN_MIS;
+      cfg->observer(cfg->observer_user, 1, h_cand.data(), h_state.data(), g->n);
+    }
+    tcmis_iter_stats s{};
+    s.iteration = 1;
+    s.candidates_selected = h_mis_count;
+    s.vertices_removed = g->n - h_mis_count;
+    s.alive_remaining = 0;
+    s.tiles_evaluated = (int64_t)h3_eval;
+    s.tiles_skipped = g->tile_total - (int64_t)h3_eval;
+    for (size_t i = 0; i < t1.size(); ++i) {
+      s.phase1_ms += t1[i];
+      s.phase3_ms += t3[i];
+    }
+    if (stats && max_stats > 0) stats[0] = s;
+    *n_iter = 1;
+    return 0;
+  }
+  for (int r = 0; r < rounds_run; ++r) {
+    if (!stats || r >= max_stats) break;
+    const DevRound &d = ws.h_rounds[r];
+    tcmis_iter_stats s{};
+    s.iteration = r + 1;
+    s.candidates_selected = (int64_t)d.sel;
+    s.vertices_removed = (int64_t)d.rem;
+    s.alive_remaining = (int64_t)d.alive;
+    s.tiles_evaluated = (int64_t)d.eval;
+    s.tiles_skipped = (int64_t)d.skip;
+    if (r < (int)t1.size()) {
+      s.phase1_ms = t1[r];
+      s.phase3_ms = t3[r];
+    }
+    stats[r] = s;
+  }
+  *n_iter = rounds_run;
+  return 0;
+}
+
+int priorities_impl(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
+                    uint32_t *p_out) {
+  if (heuristic == TCMIS_H1) {
+    if (g->n < 1) return set_error(TCMIS_E_INVALID_ARGUMENT, "h1_random requires n >= 1");
+  } else if (heuristic == TCMIS_H2 || heuristic == TCMIS_H3 || heuristic == TCMIS_LUBY_PERM) {
+    if (scale_bits < 8 || scale_bits > 30)
+      return set_error(TCMIS_E_INVALID_ARGUMENT, "scale_bits must be in [8, 30]");
+    if (g->n == 0) return 0;
+  } else {
+    return set_error(TCMIS_E_INVALID_ARGUMENT,
+                     "tiled engine only runs h1/h2/h3; use run_luby_reference");
+  }
+  uint32_t *d_p = nullptr;
+  if (int rc = dev_alloc(&d_p, (size_t)g->n)) return rc;
+  int rc = launch_priorities(g, heuristic, seed, scale_bits, nullptr, d_p, nullptr, nullptr);
+  if (!rc) {
+    cudaError_t e = cudaMemcpyAsync(p_out, d_p, sizeof(uint32_t) * g->n, cudaMemcpyDeviceToHost,
+                                    g->ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g->ctx->stream);
+    if (e != cudaSuccess) rc = cuda_error(e, "priorities download");
+  }
+  cudaFree(d_p);
+  return rc;
+}
+
+int max_np_impl(tcmis_graph *g, const uint32_t *p, const uint8_t *states, uint64_t *out) {
+  if (g->n == 0) return 0;
+  tcmis_ctx *ctx = g->ctx;
+  uint32_t *d_p = nullptr;
+  uint8_t *d_s = nullptr;
+  uint64_t *d_o = nullptr;
+  int rc = dev_alloc(&d_p, g->n);
+  if (!rc) rc = dev_alloc(&d_s, g->n);
+  if (!rc) rc = dev_alloc(&d_o, g->n);
+  if (!rc) {
+    cudaMemcpyAsync(d_p, p, 4ull * g->n, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemcpyAsync(d_s, states, g->n, cudaMemcpyHostToDevice, ctx->stream);
+    k_max_np<<<grid_for(ctx, 32ll * g->n, 256, 8), 256, 0, ctx->stream>>>(g->n, g->d_off,
+                                                                           g->d_nbr, d_p, d_s,
+                                                                           d_o);
+    ctx->launches++;
+    cudaError_t e = cudaMemcpyAsync(out, d_o, 8ull * g->n, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = cuda_error(e, "compute_max_np");
+  }
+  cudaFree(d_p);
+  cudaFree(d_s);
+  cudaFree(d_o);
+  return rc;
+}
+
+int neighbor_count_impl(tcmis_graph *g, const uint8_t *c, int32_t *nc, int T, int64_t *ev,
+                        int64_t *sk) {
+  if (g->n == 0) {
+    if (ev) *ev = 0;
+    if (sk) *sk = 0;
+    return 0;
+  }
+  tcmis_ctx *ctx = g->ctx;
+  uint8_t *d_c = nullptr;
+  int32_t *d_nc = nullptr;
+  int rc = dev_alloc(&d_c, g->n);
+  if (!rc) rc = dev_alloc(&d_nc, g->n);
+  if (!rc) {
+    cudaMemcpyAsync(d_c, c, g->n, cudaMemcpyHostToDevice, ctx->stream);
+    k_neighbor_count<<<grid_for(ctx, 32ll * g->n, 256, 8), 256, 0, ctx->stream>>>(
+        g->n, g->d_off, g->d_nbr, d_c, d_nc);
+    ctx->launches++;
+    cudaMemcpyAsync(nc, d_nc, 4ull * g->n, cudaMemcpyDeviceToHost, ctx->stream);
+    if (T > 0) {  // tile counters of tiled_spmv (spmv.cpp:37-46)
+      rc = ensure_workspace(g);
+      if (!rc && g->tile_T != T) rc = build_tile_counts(g, T);
+      if (!rc) {
+        Workspace &ws = g->ws;
+        cudaMemsetAsync(ws.segflag, 0, g->tile_nb, ctx->stream);
+        k_segflags_from<<<grid_for(ctx, g->n, 256, 8), 256, 0, ctx->stream>>>(g->n, d_c, T,
+                                                                               ws.segflag);
+        cudaMemsetAsync(&ws.ctrl->eval, 0, 8, ctx->stream);
+        k_seg_total<<<grid_for(ctx, g->tile_nb, 256, 4), 256, 0, ctx->stream>>>(
+            ws.segflag, g->d_rowtiles, g->tile_nb, ws.ctrl);
+        ctx->launches += 2;
+        unsigned long long e = 0;
+        cudaMemcpyAsync(&e, &ws.ctrl->eval, 8, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemsetAsync(ws.segflag, 0, g->tile_nb, ctx->stream);
+        cudaError_t ce = cudaStreamSynchronize(ctx->stream);
+        if (ce != cudaSuccess) rc = cuda_error(ce, "tiled_spmv counters");
+        *ev = (int64_t)e;
+        *sk = g->tile_total - (int64_t)e;
+      }
+    }
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (!rc && e != cudaSuccess) rc = cuda_error(e, "neighbor count");
+  }
+  cudaFree(d_c);
+  cudaFree(d_nc);
+  return rc;
+}
+
+}  // namespace tcmis_b200

@@ -1,0 +1,291 @@
+// tiles.cu -- K1, the CSR -> T x T tile converter (tiling.cpp:44-84).
+//
+// The reference tiles serially: per block row it gathers every entry, sorts by
+// block column and ORs payload bits (41.6 s at R-MAT s22).  Here a
+// warp owns one (block row, block-column range) work item and merges the T
+// sorted neighbour rows of the block on the fly: lane i holds a cursor into
+// row b*T+i (lanes i and i+32 for T > 32), the warp takes the minimum current
+// block column with a single __reduce_min_sync, emits one tile and advances
+// every lane whose cursor sits in that column.  Neighbour lists are read once,
+// coalesced per lane run; no sort, no scratch.  Block rows with more than
+// kChunk entries (hubs) are split into block-column ranges so no warp walks a
+// 162k-entry row alone.
+//
+// Pass 1 counts tiles per work item (and per block row: the tile counters of
+// run_tc_mis need exactly `tiles in block column b`, which equals `tiles in
+// block row b` because A is symmetric).  Pass 2 (export only) writes the tiles
+// in the reference layout: (tile_row, tile_col, T u64 row words).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace tcmis_b200 {
+
+namespace {
+
+constexpr int64_t kChunk = 2048;  // entries per work item before splitting
+constexpr uint32_t kNone = 0xffffffffu;
+
+__global__ void k_item_counts(int32_t n, int T, int32_t nb, const int64_t *__restrict__ off,
+                              int64_t *__restrict__ items) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = b * T, hi = std::min<int64_t>(n, lo + T);
+    const int64_t nnz = off[hi] - off[lo];
+    items[b] = std::max<int64_t>(1, (nnz + kChunk - 1) / kChunk);
+  }
+}
+
+__global__ void k_item_rows(int32_t nb, const int64_t *__restrict__ item_start,
+                            int32_t *__restrict__ item_row) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t i = item_start[b]; i < item_start[b + 1]; ++i) item_row[i] = (int32_t)b;
+}
+
+__device__ __forceinline__ int64_t lower_bound_i32(const int32_t *__restrict__ a, int64_t lo,
+                                                   int64_t hi, int64_t x) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// One warp per work item.  emit == false: count; emit == true: write tiles
+// starting at item_off[item].
+template <bool emit>
+__global__ void __launch_bounds__(256)
+    k_tile_merge(int32_t n, int T, int32_t nb, const int64_t *__restrict__ off,
+                 const int32_t *__restrict__ nbr, int64_t n_items,
+                 const int32_t *__restrict__ item_row, const int64_t *__restrict__ item_start,
+                 int64_t *__restrict__ item_cnt, int32_t *__restrict__ rowtiles,
+                 const int64_t *__restrict__ item_off, int32_t *__restrict__ tile_row,
+                 int32_t *__restrict__ tile_col, uint64_t *__restrict__ row_bits) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n_items;
+       it += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int32_t b = item_row[it];
+    const int64_t j = it - item_start[b];
+    const int64_t c = item_start[b + 1] - item_start[b];
+    const int64_t bc_lo = j * nb / c, bc_hi = (j + 1) * nb / c;
+    // up to two rows per lane (T <= 64)
+    int64_t pos[2], end[2];
+    uint32_t cur[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int i = lane + 32 * k;
+      const int64_t r = (int64_t)b * T + i;
+      pos[k] = end[k] = 0;
+      cur[k] = kNone;
+      if (i < T && r < n) {
+        end[k] = off[r + 1];
+        pos[k] = lower_bound_i32(nbr, off[r], end[k], bc_lo * T);
+        if (pos[k] < end[k]) {
+          const int64_t bc = nbr[pos[k]] / T;
+          if (bc < bc_hi) cur[k] = (uint32_t)bc;
+        }
+      }
+    }
+    int64_t count = 0;
+    for (;;) {
+      const uint32_t m = __reduce_min_sync(0xffffffffu, min(cur[0], cur[1]));
+      if (m == kNone) break;
+      uint64_t word[2] = {0, 0};
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (cur[k] == m) {
+          const int64_t base = (int64_t)m * T;
+          int64_t p = pos[k];
+          while (p < end[k]) {
+            const int64_t u = nbr[p];
+            if (u - base >= T) break;
+            if (emit) word[k] |= 1ull << (u - base);
+            ++p;
+          }
+          pos[k] = p;
+          cur[k] = kNone;
+          if (p < end[k]) {
+            const int64_t bc = nbr[p] / T;
+            if (bc < bc_hi) cur[k] = (uint32_t)bc;
+          }
+        }
+      }
+      if (emit) {
+        const int64_t t = item_off[it] + count;
+        if (lane == 0) {
+          tile_row[t] = b;
+          tile_col[t] = (int32_t)m;
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int i = lane + 32 * k;
+          if (i < T) row_bits[t * T + i] = word[k];
+        }
+      }
+      ++count;
+    }
+    if (!emit && lane == 0) {
+      item_cnt[it] = count;
+      if (count) atomicAdd(&rowtiles[b], (int32_t)count);
+    }
+  }
+}
+
+__global__ void k_sum_rowtiles(const int32_t *__restrict__ rowtiles, int32_t nb,
+                               unsigned long long *__restrict__ total) {
+  unsigned long long s = 0;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x)
+    s += (unsigned long long)rowtiles[b];
+  for (int o = 16; o; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(total, s);
+}
+
+struct Items {
+  int64_t *start = nullptr;  // nb + 1
+  int32_t *row = nullptr;
+  int64_t *cnt = nullptr;
+  int64_t n_items = 0;
+  void *tmp = nullptr;
+  ~Items() {
+    cudaFree(start);
+    cudaFree(row);
+    cudaFree(cnt);
+    cudaFree(tmp);
+  }
+};
+
+int plan_items(tcmis_graph *g, int T, int32_t nb, Items &it) {
+  tcmis_ctx *ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  if (int rc = dev_alloc(&it.start, (size_t)nb + 1)) return rc;
+  k_item_counts<<<grid_for(ctx, nb, 256, 8), 256, 0, st>>>(g->n, T, nb, g->d_off, it.start);
+  TCMIS_LAUNCHED(ctx);
+  size_t bytes = 0;
+  TCMIS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, it.start, it.start, (int64_t)nb + 1,
+                                           st));
+  TCMIS_CUDA(cudaMalloc(&it.tmp, bytes));
+  // the extra (nb-th) slot is garbage before the scan; zero it so the scan
+  // yields start[nb] = total items
+  TCMIS_CUDA(cudaMemsetAsync(it.start + nb, 0, sizeof(int64_t), st));
+  TCMIS_CUDA(cub::DeviceScan::ExclusiveSum(it.tmp, bytes, it.start, it.start, (int64_t)nb + 1,
+                                           st));
+  ctx->launches++;
+  TCMIS_CUDA(cudaMemcpyAsync(&it.n_items, it.start + nb, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                             st));
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  if (int rc = dev_alloc(&it.row, (size_t)it.n_items)) return rc;
+  if (int rc = dev_alloc(&it.cnt, (size_t)it.n_items)) return rc;
+  k_item_rows<<<grid_for(ctx, nb, 256, 8), 256, 0, st>>>(nb, it.start, it.row);
+  TCMIS_LAUNCHED(ctx);
+  return 0;
+}
+
+}  // namespace
+
+int build_tile_counts(tcmis_graph *g, int T) {
+  if (T < 1 || T > 64)
+    return set_error(TCMIS_E_INVALID_ARGUMENT,
+                     "tile_dim must be in [1, 64], got " + std::to_string(T));
+  tcmis_ctx *ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  const int32_t nb = (int32_t)(((int64_t)g->n + T - 1) / T);
+  cudaFree(g->d_rowtiles);
+  g->d_rowtiles = nullptr;
+  g->tile_T = 0;
+  g->tile_nb = nb;
+  g->tile_total = 0;
+  if (int rc = dev_alloc(&g->d_rowtiles, (size_t)nb + 1)) return rc;
+  TCMIS_CUDA(cudaMemsetAsync(g->d_rowtiles, 0, sizeof(int32_t) * ((size_t)nb + 1), st));
+  if (nb > 0) {
+    Items it;
+    if (int rc = plan_items(g, T, nb, it)) return rc;
+    k_tile_merge<false><<<grid_for(ctx, 32 * it.n_items, 256, 16), 256, 0, st>>>(
+        g->n, T, nb, g->d_off, g->d_nbr, it.n_items, it.row, it.start, it.cnt, g->d_rowtiles,
+        nullptr, nullptr, nullptr, nullptr);
+    TCMIS_LAUNCHED(ctx);
+    unsigned long long *d_total = nullptr;
+    if (int rc = dev_alloc(&d_total, 1)) return rc;
+    cudaMemsetAsync(d_total, 0, 8, st);
+    k_sum_rowtiles<<<grid_for(ctx, nb, 256, 4), 256, 0, st>>>(g->d_rowtiles, nb, d_total);
+    ctx->launches++;
+    unsigned long long total = 0;
+    cudaMemcpyAsync(&total, d_total, 8, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    cudaFree(d_total);
+    if (e != cudaSuccess) return cuda_error(e, "tile counts");
+    g->tile_total = (int64_t)total;
+  }
+  g->tile_T = T;
+  return 0;
+}
+
+int export_tiles(tcmis_graph *g, int T, int32_t *tile_row, int32_t *tile_col,
+                 uint64_t *row_bits, int64_t *bro) {
+  if (g->tile_T != T)
+    if (int rc = build_tile_counts(g, T)) return rc;
+  tcmis_ctx *ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  const int32_t nb = g->tile_nb;
+  const int64_t tiles = g->tile_total;
+  if (nb == 0) {
+    bro[0] = 0;
+    return 0;
+  }
+  Items it;
+  if (int rc = plan_items(g, T, nb, it)) return rc;
+  // recount per item (cheap) to get exact output offsets per item
+  int32_t *scratch_rows = nullptr;
+  if (int rc = dev_alloc(&scratch_rows, (size_t)nb + 1)) return rc;
+  cudaMemsetAsync(scratch_rows, 0, sizeof(int32_t) * ((size_t)nb + 1), st);
+  k_tile_merge<false><<<grid_for(ctx, 32 * it.n_items, 256, 16), 256, 0, st>>>(
+      g->n, T, nb, g->d_off, g->d_nbr, it.n_items, it.row, it.start, it.cnt, scratch_rows,
+      nullptr, nullptr, nullptr, nullptr);
+  ctx->launches++;
+  int64_t *item_off = nullptr;
+  int32_t *d_tr = nullptr, *d_tc = nullptr;
+  uint64_t *d_rb = nullptr;
+  int rc = dev_alloc(&item_off, (size_t)it.n_items + 1);
+  if (!rc) rc = dev_alloc(&d_tr, (size_t)tiles);
+  if (!rc) rc = dev_alloc(&d_tc, (size_t)tiles);
+  if (!rc) rc = dev_alloc(&d_rb, (size_t)tiles * T);
+  if (!rc) {
+    size_t bytes = 0;
+    void *tmp = nullptr;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, it.cnt, item_off, it.n_items, st);
+    cudaMalloc(&tmp, bytes);
+    cub::DeviceScan::ExclusiveSum(tmp, bytes, it.cnt, item_off, it.n_items, st);
+    k_tile_merge<true><<<grid_for(ctx, 32 * it.n_items, 256, 16), 256, 0, st>>>(
+        g->n, T, nb, g->d_off, g->d_nbr, it.n_items, it.row, it.start, it.cnt, scratch_rows,
+        item_off, d_tr, d_tc, d_rb);
+    ctx->launches += 2;
+    std::vector<int64_t> h_start(nb + 1), h_off(it.n_items);
+    cudaMemcpyAsync(h_start.data(), it.start, 8ull * (nb + 1), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(h_off.data(), item_off, 8ull * it.n_items, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(tile_row, d_tr, 4ull * tiles, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(tile_col, d_tc, 4ull * tiles, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(row_bits, d_rb, 8ull * tiles * T, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    cudaFree(tmp);
+    if (e != cudaSuccess) {
+      rc = cuda_error(e, "export tiles");
+    } else {
+      for (int32_t b = 0; b < nb; ++b) bro[b] = h_off[h_start[b]];
+      bro[nb] = tiles;
+    }
+  }
+  cudaFree(scratch_rows);
+  cudaFree(item_off);
+  cudaFree(d_tr);
+  cudaFree(d_tc);
+  cudaFree(d_rb);
+  return rc;
+}
+
+}  // namespace tcmis_b200

@@ -1,0 +1,324 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the oracle and
+the reference's golden fixtures.  Bit-exact on every field the reference
+reports: MIS membership, |MIS|, iteration count, per-iteration
+candidates_selected / vertices_removed / alive_remaining / tiles_evaluated /
+tiles_skipped."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2605_29604_b200 as tc
+from conftest import golden, golden_names
+
+pytestmark = pytest.mark.gpu
+
+HEUR = {"h1": tc.Heuristic.H1, "h2": tc.Heuristic.H2, "h3": tc.Heuristic.H3,
+        "luby-fresh": tc.Heuristic.LubyFresh, "luby-perm": tc.Heuristic.LubyPerm}
+
+
+def as_tc(g: O.Graph) -> tc.Graph:
+    return tc.Graph(g.n, g.off, g.nbr)
+
+
+def rounds_tuple(its):
+    return [(i.candidates_selected, i.vertices_removed, i.alive_remaining, i.tiles_evaluated,
+             i.tiles_skipped) for i in its]
+
+
+def oracle_tuple(s):
+    return [(r["sel"], r["rem"], r["alive"], r["tiles_eval"], r["tiles_skip"]) for r in s.rounds]
+
+
+GRAPHS = [
+    ("petersen", ()), ("gnp_avg", (1000, 8.0, 7)), ("gnp_avg", (3000, 30.0, 2)),
+    ("rmat", (10, 16, 3)), ("rmat", (13, 16, 1)), ("grid", (40,)), ("rgg", (6000, 3.0, 5)),
+]
+
+
+@pytest.mark.parametrize("kind,args", GRAPHS)
+@pytest.mark.parametrize("heur", list(HEUR))
+def test_run_mis_bit_exact(ctx, kind, args, heur):
+    g = O.gen(kind, *args)
+    dg = tc.DeviceGraph.upload(as_tc(g), ctx)
+    for seed in (1, 5):
+        for T in (16, 8):
+            exp = O.solve(g, heur, seed, tile_dim=T)
+            got = tc.run_mis(dg, tc.EngineConfig(heuristic=HEUR[heur], seed=seed, tile_dim=T))
+            assert np.array_equal(got.mis, exp.mis), (heur, seed, T)
+            assert len(got.iterations) == exp.n_rounds
+            assert rounds_tuple(got.iterations) == oracle_tuple(exp), (heur, seed, T)
+            assert np.array_equal(got.state, exp.state)
+
+
+@pytest.mark.parametrize("T", [1, 2, 7, 16, 31, 32, 33, 64])
+def test_tile_counters_any_tile_dim(ctx, T):
+    g = O.gen("rmat", 11, 8, 4)
+    dg = tc.DeviceGraph.upload(as_tc(g), ctx)
+    assert dg.tile(T) == int(O.tile_row_counts(g, T).sum())
+    exp = O.solve(g, "h2", 3, tile_dim=T)
+    got = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=3, tile_dim=T))
+    assert rounds_tuple(got.iterations) == oracle_tuple(exp)
+
+
+@pytest.mark.parametrize("T", [1, 5, 8, 16, 32, 64])
+def test_tile_graph_export_matches_oracle(ctx, T):
+    g = O.gen("rmat", 10, 16, 3)
+    a = tc.tile_graph(as_tc(g), T, ctx)
+    tr, tcol, rb, bro = O.tile_graph(g, T)
+    assert np.array_equal(a.tile_row, tr) and np.array_equal(a.tile_col, tcol)
+    assert np.array_equal(a.row_bits, rb) and np.array_equal(a.block_row_offsets, bro)
+
+
+def test_tile_graph_hub_rows_split(ctx):
+    # a star: one row with many block columns -> multiple work items
+    n = 20000
+    e = np.stack([np.zeros(n - 1, np.int32), np.arange(1, n, dtype=np.int32)], 1)
+    g = O.graph_from_edges(n, e)
+    for T in (16, 64):
+        a = tc.tile_graph(as_tc(g), T, ctx)
+        tr, tcol, rb, bro = O.tile_graph(g, T)
+        assert np.array_equal(a.tile_col, tcol) and np.array_equal(a.row_bits, rb)
+
+
+@pytest.mark.parametrize("heur", ["h1", "h2"])
+def test_priorities_bit_exact(ctx, heur):
+    for kind, args in (("rmat", (12, 16, 1)), ("gnp_avg", (5000, 3.0, 9)), ("petersen", ())):
+        g = O.gen(kind, *args)
+        dg = tc.DeviceGraph.upload(as_tc(g), ctx)
+        for seed in (0, 1, 123456789, 2**64 - 1):
+            if heur == "h1":
+                assert np.array_equal(tc.h1_random(dg, seed), O.h1_random(g.n, seed))
+            else:
+                for sb in (8, 20, 30):
+                    assert np.array_equal(tc.h2_degree_aware(dg, seed, sb),
+                                          O.h2_degree_aware(g, seed, sb))
+
+
+def test_h2_saturation_and_floor(ctx):
+    # edgeless graph: avg = 0 -> all p = 0; tiny avg with isolated vertices ->
+    # denominator floor + saturation (priorities.cpp:46-49)
+    g = O.graph_from_edges(64, np.zeros((0, 2), np.int32))
+    dg = tc.DeviceGraph.upload(as_tc(g), ctx)
+    assert np.array_equal(tc.h2_degree_aware(dg, 1, 30), O.h2_degree_aware(g, 1, 30))
+    g = O.graph_from_edges(5000, np.array([[0, 1]], np.int32))
+    dg = tc.DeviceGraph.upload(as_tc(g), ctx)
+    for sb in (8, 30):
+        assert np.array_equal(tc.h2_degree_aware(dg, 7, sb), O.h2_degree_aware(g, 7, sb))
+    res = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=7, scale_bits=30))
+    assert np.array_equal(res.mis, O.solve(g, "h2", 7, scale_bits=30).mis)
+
+
+def test_phase_helpers(ctx):
+    g = O.gen("gnp_avg", 2000, 12.0, 3)
+    dg = tc.DeviceGraph.upload(as_tc(g), ctx)
+    rng = np.random.default_rng(1)
+    p = O.h2_degree_aware(g, 1)
+    st = rng.integers(0, 3, g.n).astype(np.uint8)
+    exp = np.zeros(g.n, np.uint64)
+    O.lib().orc_compute_max_np(g.n, g.off, g.nbr, p, st, exp)
+    assert np.array_equal(tc.compute_max_np(dg, p, st), exp)
+    c = (rng.random(g.n) < 0.1).astype(np.uint8)
+    exp_nc = np.zeros(g.n, np.int32)
+    O.lib().orc_csr_neighbor_count(g.n, g.off, g.nbr, c, exp_nc)
+    assert np.array_equal(tc.csr_neighbor_count(dg, c), exp_nc)
+    for T in (4, 16):
+        tr, tcol, rb, bro = O.tile_graph(g, T)
+        seg = np.zeros((g.n + T - 1) // T, np.uint64)
+        O.lib().orc_pack_segments(g.n, c, T, seg)
+        nc = np.zeros(g.n, np.int32)
+        ev, sk = O.C.c_int64(), O.C.c_int64()
+        O.lib().orc_tiled_spmv(g.n, T, tcol.size, tcol, rb, bro, seg, nc, O.C.byref(ev),
+                               O.C.byref(sk))
+        got, gev, gsk = tc.tiled_spmv(dg, c, T)
+        assert np.array_equal(got, nc) and (gev, gsk) == (ev.value, sk.value)
+
+
+def test_iteration_observer(ctx):
+    g = O.gen("gnp_avg", 1000, 8.0, 7)
+    p = O.h2_degree_aware(g, 1)
+    seen = []
+
+    def obs(it, cand, states):
+        seen.append((it, cand.copy(), states.copy()))
+
+    tc.run_mis(as_tc(g), tc.EngineConfig(heuristic=tc.Heuristic.H2, iteration_observer=obs))
+    # replay the reference's rounds and compare the snapshots
+    st = np.zeros(g.n, np.uint8)
+    mx = np.zeros(g.n, np.uint64)
+    for it, cand, states in seen:
+        assert np.array_equal(states, st)
+        O.lib().orc_compute_max_np(g.n, g.off, g.nbr, p, st, mx)
+        keys = (p.astype(np.uint64) << np.uint64(32)) | (np.arange(g.n, dtype=np.uint64) + 1)
+        exp_c = ((st == 0) & (keys > mx)).astype(np.uint8)
+        assert np.array_equal(cand, exp_c)
+        nc = np.zeros(g.n, np.int32)
+        O.lib().orc_csr_neighbor_count(g.n, g.off, g.nbr, exp_c, nc)
+        s, r = O.C.c_int64(), O.C.c_int64()
+        O.lib().orc_phase3_update(g.n, st, exp_c, nc, O.C.byref(s), O.C.byref(r))
+    assert len(seen) == 3
+    seen.clear()
+    res = tc.run_mis(as_tc(g), tc.EngineConfig(heuristic=tc.Heuristic.H3, iteration_observer=obs))
+    assert len(seen) == 1 and seen[0][0] == 1
+    assert np.array_equal(np.flatnonzero(seen[0][1]), res.mis)
+    assert not seen[0][2].any()
+
+
+def test_errors_match_reference(ctx):
+    g = as_tc(O.gen("petersen"))
+    with pytest.raises(ValueError):
+        tc.run_mis(g, tc.EngineConfig(heuristic=tc.Heuristic.H2, tile_dim=0))
+    with pytest.raises(ValueError):
+        tc.run_mis(g, tc.EngineConfig(heuristic=tc.Heuristic.H2, tile_dim=65))
+    with pytest.raises(ValueError):
+        tc.run_mis(g, tc.EngineConfig(heuristic=tc.Heuristic.H2, scale_bits=7))
+    with pytest.raises(ValueError):
+        tc.run_mis(g, tc.EngineConfig(heuristic=tc.Heuristic.LubyPerm, scale_bits=31))
+    # luby-fresh ignores scale_bits; h1 ignores it too (priorities.cpp:33-41)
+    tc.run_mis(g, tc.EngineConfig(heuristic=tc.Heuristic.LubyFresh, scale_bits=99))
+    tc.run_mis(g, tc.EngineConfig(heuristic=tc.Heuristic.H1, scale_bits=99))
+    with pytest.raises(ValueError):
+        tc.run_tc_mis(g, None, tc.EngineConfig(heuristic=tc.Heuristic.LubyPerm))
+    # n == 0 returns an empty result, but a bad tile_dim still throws first
+    e = tc.Graph(0, np.zeros(1, np.int64), np.zeros(0, np.int32))
+    r = tc.run_mis(e, tc.EngineConfig(heuristic=tc.Heuristic.H2, scale_bits=3))
+    assert r.cardinality() == 0 and r.iterations == []
+    with pytest.raises(ValueError):
+        tc.run_mis(e, tc.EngineConfig(tile_dim=0))
+
+
+def test_prebuilt_tiles_overload(ctx):
+    g = O.gen("rmat", 10, 16, 3)
+    a = tc.tile_graph(as_tc(g), 8, ctx)
+    res = tc.run_tc_mis(as_tc(g), a, tc.EngineConfig(heuristic=tc.Heuristic.H2, tile_dim=8))
+    assert rounds_tuple(res.iterations) == oracle_tuple(O.solve(g, "h2", 1, tile_dim=8))
+    with pytest.raises(ValueError):
+        tc.run_tc_mis(as_tc(g), a, tc.EngineConfig(heuristic=tc.Heuristic.H2, tile_dim=16))
+
+
+def test_edge_cases(ctx):
+    for g in (O.graph_from_edges(1, np.zeros((0, 2), np.int32)),
+              O.graph_from_edges(100, np.zeros((0, 2), np.int32)),
+              O.graph_from_edges(2, np.array([[0, 1]], np.int32)),
+              O.graph_from_edges(33, np.array([[i, j] for i in range(33) for j in range(i)],
+                                              np.int32)),
+              O.graph_from_edges(5000, np.stack([np.zeros(4999, np.int32),
+                                                 np.arange(1, 5000, dtype=np.int32)], 1))):
+        for heur in HEUR:
+            exp = O.solve(g, heur, 2)
+            got = tc.run_mis(as_tc(g), tc.EngineConfig(heuristic=HEUR[heur], seed=2))
+            assert np.array_equal(got.mis, exp.mis)
+            assert rounds_tuple(got.iterations) == oracle_tuple(exp)
+
+
+def test_long_path_many_rounds(ctx):
+    # increasing priorities along a path force ~n/2 rounds (stress for the
+    # round loop and its statistics buffer)
+    n = 3000
+    g = O.graph_from_edges(n, np.stack([np.arange(n - 1, dtype=np.int32),
+                                        np.arange(1, n, dtype=np.int32)], 1))
+    exp = O.solve(g, "h1", 11)
+    got = tc.run_mis(as_tc(g), tc.EngineConfig(heuristic=tc.Heuristic.H1, seed=11))
+    assert np.array_equal(got.mis, exp.mis)
+    assert rounds_tuple(got.iterations) == oracle_tuple(exp)
+
+
+def test_repeated_solves_are_independent(ctx):
+    g = O.gen("rmat", 12, 16, 2)
+    dg = tc.DeviceGraph.upload(as_tc(g), ctx)
+    first = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2))
+    tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H1, seed=9))
+    tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.LubyFresh, seed=3))
+    again = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2))
+    assert np.array_equal(first.mis, again.mis)
+    assert rounds_tuple(first.iterations) == rounds_tuple(again.iterations)
+
+
+# ----------------------------------------------------------- generators
+
+@pytest.mark.parametrize("scale,ef,seed", [(8, 4, 1), (12, 16, 1), (14, 16, 3)])
+def test_gpu_rmat_bit_identical(ctx, scale, ef, seed):
+    dg = tc.DeviceGraph.rmat(scale, ef, seed, ctx)
+    a = dg.download()
+    b = O.gen("rmat", scale, ef, seed)
+    assert np.array_equal(a.offsets, b.off) and np.array_equal(a.neighbors, b.nbr)
+
+
+def test_gpu_grid_and_rgg_match_oracle(ctx):
+    for side in (1, 2, 37):
+        a = tc.DeviceGraph.grid(side, ctx).download()
+        b = O.gen("grid", side)
+        assert np.array_equal(a.offsets, b.off) and np.array_equal(a.neighbors, b.nbr)
+    for n, d, s in ((1, 3.0, 1), (5000, 3.0, 1), (20000, 6.0, 4)):
+        a = tc.DeviceGraph.rgg(n, d, s, ctx).download()
+        b = O.gen("rgg", n, d, s)
+        assert np.array_equal(a.offsets, b.off) and np.array_equal(a.neighbors, b.nbr)
+
+
+def test_host_gnp_matches_oracle():
+    a = tc.gnp_graph_avg_degree(100000, 16.0, 1)
+    b = O.gen("gnp_avg", 100000, 16.0, 1)
+    assert np.array_equal(a.offsets, b.off) and np.array_equal(a.neighbors, b.nbr)
+
+
+# ------------------------------------------------------ golden fixtures
+
+def _device_graph_for(spec, ctx):
+    k = spec["kind"]
+    if k == "rmat":
+        return tc.DeviceGraph.rmat(spec["scale"], spec["ef"], spec["seed"], ctx)
+    if k == "grid":
+        return tc.DeviceGraph.grid(spec["side"], ctx)
+    if k == "rgg":
+        return tc.DeviceGraph.rgg(spec["n"], spec["d"], spec["seed"], ctx)
+    if k == "gnp":
+        return tc.DeviceGraph.upload(tc.gnp_graph_avg_degree(spec["n"], spec["d"],
+                                                             spec["seed"]), ctx)
+    return tc.DeviceGraph.upload(as_tc(O.gen("petersen")), ctx)
+
+
+def _check_golden(name, ctx):
+    gd = golden(name)
+    dg = _device_graph_for(gd["spec"], ctx)
+    assert (dg.n, dg.num_edges()) == (gd["n"], gd["m"])
+    h = dg.download()
+    assert O.checksum(h.offsets) == gd["off_checksum"]
+    assert O.checksum(h.neighbors) == gd["nbr_checksum"]
+    assert dg.tile(gd["tile_dim"]) == gd["tile_count"]
+    for key, exp in gd["results"].items():
+        heur, seed = key.split("/seed")
+        res = tc.run_mis(dg, tc.EngineConfig(heuristic=HEUR[heur], seed=int(seed),
+                                             tile_dim=gd["tile_dim"]))
+        got = [list(t) for t in rounds_tuple(res.iterations)]
+        if heur == "luby-perm":
+            got = [r[:3] + [0, 0] for r in got]
+        assert got == exp["rounds"], key
+        assert res.cardinality() == exp["mis_size"], key
+        member = (res.state == 1).astype(np.uint8)
+        assert O.checksum(member) == exp["member_checksum"], key
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_golden_small(ctx, name):
+    _check_golden(name, ctx)
+
+
+@pytest.mark.parametrize("name", golden_names(large=True))
+def test_golden_baseline_configs(ctx, name):
+    """The BASELINE.json configs at full size, against the reference's own
+    results (tests/golden/make_golden.py)."""
+    _check_golden(name, ctx)
+
+
+def test_rmat22_properties(ctx):
+    """Size-independent properties at s22: independence and maximality of the
+    result, and |MIS| == the sequential greedy count."""
+    dg = tc.DeviceGraph.rmat(22, 16, 1, ctx)
+    res = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2))
+    h = dg.download()
+    member = res.state == 1
+    src = np.repeat(np.arange(h.n), np.diff(h.offsets))
+    assert not np.any(member[src] & member[h.neighbors])          # independent
+    covered = member.copy()
+    np.logical_or.at(covered, h.neighbors, member[src])
+    assert covered.all()                                            # maximal
+    assert np.all(np.diff(res.mis) > 0)                             # ascending ids
