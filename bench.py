@@ -1,0 +1,447 @@
+#!/usr/bin/env python
+"""bench.py -- TC-MIS on B200: MIS time and Gedges/s (BASELINE.json metric).
+
+A "step" is one complete MIS solve (H2 priorities -> bulk-synchronous rounds
+-> ascending MIS ids on the device) of the configured synthetic graph.
+
+  value  device-resident: the CSR is already in HBM (generated there); the
+         step is tcmis_solve_device() through the C-ABI, timed with CUDA
+         events on the engine's stream; L2 is flushed between steps.
+  e2e    the drop-in path: host CSR in pinned memory -> tcmis_graph_upload
+         (H2D) -> tcmis_graph_tile -> tcmis_solve (D2H of the MIS ids and the
+         per-iteration stats into host buffers) -> destroy, every step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config rmat22]
+  python bench.py --impl reference ...   (the reference CPU implementation)
+
+Configs (BASELINE.json): er (n=100k, d=16), grid (4096^2), rmat22 (default,
+the metric's headline), rgg (24M, d~3), rmat26 (~1.05B edges).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "er": {"workload": "Erdos-Renyi n=100000 avg degree 16 (gnp_graph_avg_degree seed 1)"},
+    "grid": {"workload": "2D 5-point grid 4096x4096 (row-major ids)"},
+    "rmat22": {"workload": "R-MAT scale 22 edge factor 16 (rmat_graph(22,16,1))"},
+    "rgg": {"workload": "random geometric graph n=24M avg degree ~3 (integer lattice, ids in "
+                        "draw order)"},
+    "rmat26": {"workload": "R-MAT scale 26 edge factor 16 (rmat_graph(26,16,1))"},
+}
+HEUR = {"h1": 0, "h2": 1, "h3": 2, "luby-fresh": 3, "luby-perm": 4}
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.rows = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------- graphs
+
+def make_device_graph(tc, name: str, ctx):
+    if name == "er":
+        return tc.DeviceGraph.upload(tc.gnp_graph_avg_degree(100000, 16.0, 1), ctx)
+    if name == "grid":
+        return tc.DeviceGraph.grid(4096, ctx)
+    if name == "rmat22":
+        return tc.DeviceGraph.rmat(22, 16, 1, ctx)
+    if name == "rgg":
+        return tc.DeviceGraph.rgg(24_000_000, 3.0, 1, ctx)
+    if name == "rmat26":
+        return tc.DeviceGraph.rmat(26, 16, 1, ctx)
+    raise ValueError(name)
+
+
+def peaks():
+    try:
+        with open(PEAKS) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------ the B200 arm
+
+def run_ours(args) -> dict:
+    import torch
+    import paper_2605_29604_b200 as tc
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    ctx = tc.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
+    L = tc.load()
+
+    t0 = time.time()
+    dg = make_device_graph(tc, args.config, ctx)
+    n, nnz = dg.n, dg.nnz
+    m = nnz // 2
+    tiles = dg.tile(16)
+    log(f"[bench] {args.config}: n={n} m={m} tiles={tiles} (setup {time.time() - t0:.1f}s)")
+    cfg = tc.EngineConfig(heuristic=HEUR[args.heuristic], seed=1, tile_dim=16)
+    c_cfg, _keep = cfg._c()
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")  # > 126 MB L2
+
+    def solve_device():
+        d_mis, d_state = C.c_void_p(), C.c_void_p()
+        cnt = C.c_int64(0)
+        stats = (tc._Stats * 4096)()
+        nit = C.c_int32(0)
+        tc._check(L.tcmis_solve_device(dg.h, C.byref(c_cfg), C.byref(d_mis), C.byref(cnt),
+                                       C.byref(d_state), stats, 4096, C.byref(nit)))
+        return cnt.value, nit.value
+
+    # ---- value: device-resident solves
+    for _ in range(args.warmup):
+        solve_device()
+    ctx.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                ev[k][0].record(stream)
+            mis_count, iters = solve_device()
+            with torch.cuda.stream(stream):
+                ev[k][1].record(stream)
+        ctx.synchronize()
+        torch.cuda.synchronize()
+    launches = ctx.launches() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * m / (ms_per_step * 1e-3) / 1e9  # replicas: every rank solves its graph
+
+    # ---- kernel roofline: per-kernel CUDA events (step-wise loop, same kernels)
+    cfg_t = tc.EngineConfig(heuristic=HEUR[args.heuristic], seed=1, tile_dim=16, timing=True)
+    sel_ms, upd_ms, per_round = [], [], None
+    for _ in range(max(1, min(args.steps, 5))):
+        r = tc.run_mis(dg, cfg_t)
+        sel_ms.append([i.phase1_ms for i in r.iterations])
+        upd_ms.append([i.phase3_ms for i in r.iterations])
+        per_round = r
+    terms = trajectory_terms(tc, dg, cfg)
+    hbm, peak_kind = peaks()
+    sel_avg = [sum(x[k] for x in sel_ms) / len(sel_ms) for k in range(len(sel_ms[0]))]
+    # SURVEY 8(d) per-unit figures: candidate detection 12|A|+4nnz(A), exclusion
+    # 8|A\C|+4nnz(A\C) -- the fused select kernel does both for round k.
+    b_sel = [12 * a + 4 * na + 8 * nc + 4 * nnc for (a, na, nc, nnc) in terms]
+    k0 = 0  # the dominant launch is round 1's select
+    achieved = b_sel[k0] / (sel_avg[k0] * 1e-3) / 1e9
+    roofline = {"kernel": "k_select (round 1: candidate detection + exclusion push)",
+                "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                "algorithmic_bytes": b_sel[k0], "launch_ms": round(sel_avg[k0], 4),
+                "traffic": args.traffic}
+
+    # ---- e2e through the drop-in C-ABI with host buffers
+    e2e = run_e2e(tc, torch, dg, ctx, stream, cfg, args, local, dist, flush)
+
+    line = {
+        "metric": "Gedges/s (MIS solve, BASELINE config)", "value": round(value, 4),
+        "unit": "Gedges/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64/u32 keys (integer), f64 priority",
+        "data": "synthetic (generated on device, bit-identical to the reference generator)",
+        "config": {"workload": CONFIGS[args.config]["workload"], "graph": args.config,
+                   "n": n, "m": m, "heuristic": args.heuristic, "seed": 1, "tile_dim": 16,
+                   "iterations": iters, "mis_size": mis_count, "tiles_t16": tiles,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "256 MB flush between steps; CSR > L2"},
+        "mis_ms": round(ms_per_step, 4),
+        "per_round_ms": {"select": [round(x, 4) for x in sel_avg],
+                         "update": [round(sum(x[k] for x in upd_ms) / len(upd_ms), 4)
+                                    for k in range(len(upd_ms[0]))]},
+        "roofline": roofline, "e2e": e2e, "clocks": clk.summary(),
+        "gpu_launches": launches,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(dg, args)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return line if rank == 0 else None
+
+
+def trajectory_terms(tc, dg, cfg):
+    """|A_k|, nnz(A_k), |A_k \\ C_k|, nnz(A_k \\ C_k) per round, from the
+    device (observer snapshots + degrees); outside every timed region."""
+    import numpy as np
+    h = dg.download()
+    deg = np.diff(h.offsets)
+    out = []
+
+    def obs(it, cand, states):
+        alive = states == 0
+        c = cand.astype(bool)
+        nc = alive & ~c
+        out.append((int(alive.sum()), int(deg[alive].sum()), int(nc.sum()), int(deg[nc].sum())))
+
+    c2 = tc.EngineConfig(heuristic=cfg.heuristic, seed=cfg.seed, tile_dim=cfg.tile_dim,
+                         iteration_observer=obs)
+    if c2.heuristic == tc.Heuristic.H3:
+        c2.heuristic = tc.Heuristic.H2  # same rounds inside
+    tc.run_mis(dg, c2)
+    return out
+
+
+def run_e2e(tc, torch, dg, ctx, stream, cfg, args, local, dist, flush):
+    import numpy as np
+    L = tc.load()
+    h = dg.download()
+    n, nnz = h.n, h.neighbors.size
+    off = torch.from_numpy(h.offsets).pin_memory()
+    nbr = torch.from_numpy(h.neighbors).pin_memory()
+    mis = torch.empty(max(n, 1), dtype=torch.int32).pin_memory()
+    c_cfg, _k = cfg._c()
+    stats = (tc._Stats * 4096)()
+
+    def step():
+        g = C.c_void_p()
+        tc._check(L.tcmis_graph_upload(ctx.h, n, C.c_void_p(off.data_ptr()),
+                                       C.c_void_p(nbr.data_ptr()), C.byref(g)))
+        tc._check(L.tcmis_graph_tile(g, 16, None))
+        cnt, nit = C.c_int64(0), C.c_int32(0)
+        tc._check(L.tcmis_solve(g, C.byref(c_cfg), None, C.c_void_p(mis.data_ptr()),
+                                C.byref(cnt), stats, 4096, C.byref(nit)))
+        L.tcmis_graph_destroy(g)
+        return cnt.value
+
+    for _ in range(max(1, min(args.warmup, 3))):
+        step()
+    steps = max(1, min(args.steps, 10))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    cnt = 0
+    for k in range(steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            evs[k][0].record(stream)
+        cnt = step()
+        with torch.cuda.stream(stream):
+            evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / steps
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    world = dist.get_world_size() if dist else 1
+    return {"value": round(world * (nnz // 2) / (ms * 1e-3) / 1e9, 4), "unit": "Gedges/s",
+            "ms": round(ms, 3), "h2d_bytes_per_step": int(8 * (n + 1) + 4 * nnz),
+            "d2h_bytes_per_step": int(4 * cnt + 64 * 4096), "steps": steps,
+            "path": "tcmis_graph_upload + tcmis_graph_tile + tcmis_solve (host buffers)"}
+
+
+# ------------------------------------------------------ reference (CPU)
+
+def ref_graph_for(name: str):
+    """The reference's own generators where it has them; grid/RGG from the
+    oracle's definitions (the reference has no generator for them)."""
+    import oracle as O
+    R = O.ref()
+    if name == "er":
+        return O.RefGraph(R.ref_gen_gnp_avg(100000, 16.0, 1))
+    if name == "rmat22":
+        return O.RefGraph(R.ref_gen_rmat(22, 16, 1))
+    if name == "rmat26":
+        return O.RefGraph(R.ref_gen_rmat(26, 16, 1))
+    if name == "grid":
+        return O.RefGraph.from_csr(O.gen("grid", 4096))
+    if name == "rgg":
+        return O.RefGraph.from_csr(O.gen("rgg", 24_000_000, 3.0, 1))
+    raise ValueError(name)
+
+
+def ref_time(rg, heuristic: str, reps: int, cores: int):
+    """Time the reference's fastest identical-output CPU path on rg:
+    run_luby_reference(Permutation) -- same MIS and same round count as h2,
+    no 12 GB tiling."""
+    import oracle as O
+    ts = []
+    for _ in range(reps):
+        if heuristic in ("h2", "h3", "luby-perm"):
+            _m, rr, ms = O.ref_run_luby(rg, 1, False, 20, cores)
+        else:
+            _m, rr, ms = O.ref_run_mis(rg, heuristic, 1, 16, cores)
+        ts.append(ms)
+    return ts, len(rr)
+
+
+def cpu_baseline(dg, args) -> dict:
+    import oracle as O
+    if not O.ref_available():
+        return {"value": None, "unit": "Gedges/s", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built"}
+    h = dg.download()
+    rg = O.RefGraph.from_csr(O.Graph(h.n, h.offsets, h.neighbors))
+    cores = os.cpu_count() or 1
+    t0 = time.time()
+    ts, rounds = ref_time(rg, args.heuristic, 1, cores)
+    reps = 1
+    while time.time() - t0 < 10 and reps < 5:  # bounded sample: ~10-30 s of CPU work
+        t2, _ = ref_time(rg, args.heuristic, 1, cores)
+        ts += t2
+        reps += 1
+    ms = sorted(ts)[len(ts) // 2]
+    return {"value": round((h.neighbors.size // 2) / (ms * 1e-3) / 1e9, 5), "unit": "Gedges/s",
+            "cores": cores, "kind": "reference", "ms": round(ms, 2),
+            "sample": f"{reps} full solve(s) of the same graph by the reference's "
+                      f"run_luby_reference(Permutation) (identical MIS and round count to "
+                      f"{args.heuristic}), median, workers={cores}",
+            "cpu_model": cpu_model()}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args) -> dict | None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import oracle as O
+    if not O.ref_available():
+        return {"impl": "reference", "unavailable": "oracle/_ref/libtcmis_ref.so not built"}
+    cores = os.cpu_count() or 1
+    t0 = time.time()
+    rg = ref_graph_for(args.config)
+    g = rg.to_csr()
+    log(f"[bench:reference] {args.config}: n={g.n} m={g.num_edges} "
+        f"(reference generator {time.time() - t0:.1f}s)")
+    for _ in range(args.warmup):
+        ref_time(rg, args.heuristic, 1, cores)
+    ts, rounds = ref_time(rg, args.heuristic, args.steps, cores)
+    ms = sum(ts) / len(ts)
+    value = g.num_edges / (ms * 1e-3) / 1e9
+    path = ("run_luby_reference(Permutation)" if args.heuristic in ("h2", "h3", "luby-perm")
+            else f"run_mis({args.heuristic})")
+    return {
+        "impl": "reference", "metric": "Gedges/s (MIS solve, BASELINE config)",
+        "value": round(value, 5), "unit": "Gedges/s", "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "integer / f64 priority",
+        "data": "synthetic (reference generators)",
+        "config": {"workload": CONFIGS[args.config]["workload"], "graph": args.config,
+                   "n": g.n, "m": g.num_edges, "heuristic": args.heuristic, "iterations": rounds,
+                   "path": path},
+        "cpu_baseline": {"value": round(value, 5), "unit": "Gedges/s", "cores": cores,
+                         "kind": "reference", "cpu_model": cpu_model(),
+                         "sample": f"{args.steps} full solves of the whole graph by the "
+                                   f"unmodified reference ({path}), workers={cores}"},
+        "e2e": {"value": round(value, 5), "unit": "Gedges/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="rmat22", choices=list(CONFIGS))
+    ap.add_argument("--heuristic", default="h2", choices=list(HEUR))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per launch of the dominant kernel (profiles/)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("[bench] warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -72,6 +72,8 @@ struct Workspace {
   int32_t round_cap = 0;
   void *cub_tmp = nullptr;
   size_t cub_bytes = 0;
+  cudaGraphExec_t exec = nullptr;  // cached WHILE{select; update} graph
+  alignas(8) unsigned char graph_key[128] = {};
 };
 
 }  // namespace tcmis_b200

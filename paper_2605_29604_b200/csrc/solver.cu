@@ -65,44 +65,98 @@ __global__ void k_priorities(int32_t n, const int64_t *__restrict__ off, int mod
 
 // ----------------------------------------------------------------- rounds
 
-// G lanes per vertex; the row is walked from its end (on R-MAT the high ids
-// at the end of a sorted row are the low-degree, high-priority vertices, so a
-// blocked vertex exits after the first chunk -- any order gives the same
-// answer).
-template <int G>
-__global__ void __launch_bounds__(256)
+// Two stages per block-chunk of kSelBlock worklist entries:
+//  A) one thread per vertex (coalesced offsets, 32 vertices in flight per
+//     warp) probes the last K entries of its row -- on R-MAT the high ids at
+//     the end of a sorted row are the low-degree, high-priority vertices, so
+//     a blocked vertex usually exits here.  A row of <= K entries is decided
+//     outright (and, as a candidate, pushes from registers).
+//  B) the undecided long rows are handed to the block's warps through shared
+//     memory: a warp scans the rest of the row from its end, 32 then 128
+//     entries per step (4 independent loads per lane), with an early exit on
+//     the first higher alive neighbour, and pushes if the vertex survives.
+// Any scan order gives the same answer (max over a set).
+constexpr int kSelBlock = 256;
+constexpr int kProbe = 4;
+
+__global__ void __launch_bounds__(kSelBlock)
     k_select(int32_t n, const int64_t *__restrict__ off, const int32_t *__restrict__ nbr,
              const uint64_t *__restrict__ key, uint8_t *__restrict__ next,
              uint8_t *__restrict__ segflag, int T, const Ctrl *__restrict__ ctrl,
              const int32_t *__restrict__ wl0, const int32_t *__restrict__ wl1) {
+  __shared__ int32_t s_def[kSelBlock];
+  __shared__ int s_ndef;
   const int round = ctrl->round;
   const int64_t cnt = round == 1 ? n : ctrl->wl_count[round & 1];
   const int32_t *wl = (round & 1) ? wl1 : wl0;
-  const int lane = threadIdx.x & 31;
-  const int gl = lane & (G - 1);
-  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
-  const int64_t gstride = ((int64_t)gridDim.x * blockDim.x) / G;
-  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; i < cnt; i += gstride) {
-    const int32_t v = round == 1 ? (int32_t)i : wl[i];
-    const int64_t s = off[v], e = off[v + 1];
-    const uint64_t kv = key[v];
-    bool blocked = false;
-    for (int64_t base = e - G; base + G > s; base -= G) {
-      const int64_t idx = base + gl;
-      bool b = false;
-      if (idx >= s) b = __ldg(&key[__ldg(&nbr[idx])]) > kv;
-      if (__ballot_sync(gmask, b)) {
-        blocked = true;
-        break;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kWarps = kSelBlock / 32;
+  for (int64_t base = (int64_t)blockIdx.x * kSelBlock; base < cnt;
+       base += (int64_t)gridDim.x * kSelBlock) {
+    if (threadIdx.x == 0) s_ndef = 0;
+    __syncthreads();
+    const int64_t i = base + threadIdx.x;
+    if (i < cnt) {
+      const int32_t v = round == 1 ? (int32_t)i : __ldg(&wl[i]);
+      const int64_t s = __ldg(&off[v]), e = __ldg(&off[v + 1]);
+      const uint64_t kv = __ldg(&key[v]);
+      const int64_t d = e - s;
+      int32_t u[kProbe];
+#pragma unroll
+      for (int j = 0; j < kProbe; ++j) u[j] = j < d ? __ldg(&nbr[e - 1 - j]) : -1;
+      bool blocked = false;
+#pragma unroll
+      for (int j = 0; j < kProbe; ++j)
+        if (u[j] >= 0) blocked |= __ldg(&key[u[j]]) > kv;
+      if (!blocked) {
+        if (d <= kProbe) {
+          next[v] = 1;
+          if (segflag) segflag[v / T] = 1;
+#pragma unroll
+          for (int j = 0; j < kProbe; ++j)
+            if (u[j] >= 0) next[u[j]] = 2;
+        } else {
+          s_def[atomicAdd(&s_ndef, 1)] = v;
+        }
       }
     }
-    if (!blocked) {
-      if (gl == 0) {
-        next[v] = 1;
-        if (segflag) segflag[v / T] = 1;
+    __syncthreads();
+    const int nd = s_ndef;
+    for (int q = warp; q < nd; q += kWarps) {
+      const int32_t v = s_def[q];
+      const int64_t s = __ldg(&off[v]), e = __ldg(&off[v + 1]);
+      const uint64_t kv = __ldg(&key[v]);
+      int64_t hi = e - kProbe;  // [s, hi) still unexamined
+      bool blocked = false;
+      {  // first step: 32 entries
+        const int64_t idx = hi - 1 - lane;
+        const bool b = idx >= s && __ldg(&key[__ldg(&nbr[idx])]) > kv;
+        blocked = __any_sync(0xffffffffu, b);
+        hi -= 32;
       }
-      for (int64_t idx = s + gl; idx < e; idx += G) next[__ldg(&nbr[idx])] = 2;
+      while (!blocked && hi > s) {  // then 128 entries per step
+        int32_t uu[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int64_t idx = hi - 1 - lane - 32 * j;
+          uu[j] = idx >= s ? __ldg(&nbr[idx]) : -1;
+        }
+        bool b = false;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (uu[j] >= 0) b |= __ldg(&key[uu[j]]) > kv;
+        blocked = __any_sync(0xffffffffu, b);
+        hi -= 128;
+      }
+      if (!blocked) {
+        if (lane == 0) {
+          next[v] = 1;
+          if (segflag) segflag[v / T] = 1;
+        }
+        for (int64_t idx = s + lane; idx < e; idx += 32) next[__ldg(&nbr[idx])] = 2;
+      }
     }
+    __syncthreads();
   }
 }
 
@@ -142,28 +196,57 @@ __device__ __forceinline__ void block_add3(unsigned long long a, unsigned long l
 
 // seg_mode: 0 = no tile counters, 1 = count and clear per round,
 // 2 = accumulate (h3: counters are taken once at the end).
-__global__ void __launch_bounds__(256)
+// Each thread owns kUpdItems consecutive worklist entries (blocked layout:
+// on round 1 the identity worklist makes that one 8-byte load of `next`);
+// survivors are compacted with one block scan and ONE global atomic per
+// block-chunk (a per-warp atomic on the shared tail serialises at the L2).
+constexpr int kUpdBlock = 256;
+constexpr int kUpdItems = 8;
+
+__global__ void __launch_bounds__(kUpdBlock)
     k_update(int32_t n, uint64_t *__restrict__ key, uint8_t *__restrict__ state,
              uint8_t *__restrict__ next, Ctrl *__restrict__ ctrl, int32_t *__restrict__ wl0,
              int32_t *__restrict__ wl1, uint8_t *__restrict__ segflag,
              const int32_t *__restrict__ rowtiles, int32_t nseg, int64_t total_tiles,
-             int seg_mode, DevRound *__restrict__ rounds, int fresh, uint64_t seed) {
+             int seg_mode, DevRound *__restrict__ rounds, int fresh, uint64_t seed,
+             cudaGraphConditionalHandle cond, int use_cond) {
+  using BlockScan = cub::BlockScan<int, kUpdBlock>;
+  __shared__ typename BlockScan::TempStorage scan_tmp;
+  __shared__ int s_base;
   const int round = ctrl->round;
   const int64_t cnt = round == 1 ? n : ctrl->wl_count[round & 1];
   const int32_t *in = (round & 1) ? wl1 : wl0;
   int32_t *out = (round & 1) ? wl0 : wl1;
   const int out_slot = (round + 1) & 1;
   const uint64_t fresh_m = fresh ? mix64(combine_seed(seed, (uint64_t)round + 1)) : 0;
-  const int lane = threadIdx.x & 31;
   unsigned long long sel = 0, rem = 0, ev = 0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < cnt; base += stride) {
-    const int64_t i = base + threadIdx.x;
-    bool surv = false;
-    int32_t v = 0;
-    if (i < cnt) {
-      v = round == 1 ? (int32_t)i : in[i];
-      const uint8_t d = next[v];
+  constexpr int64_t kChunk = (int64_t)kUpdBlock * kUpdItems;
+  for (int64_t base = (int64_t)blockIdx.x * kChunk; base < cnt; base += (int64_t)gridDim.x * kChunk) {
+    const int64_t i0 = base + (int64_t)threadIdx.x * kUpdItems;
+    int32_t vs[kUpdItems];
+    uint8_t ds[kUpdItems];
+    if (round == 1 && i0 + kUpdItems <= cnt) {  // identity worklist: one 8-byte load
+      const uint64_t w = *reinterpret_cast<const uint64_t *>(next + i0);
+#pragma unroll
+      for (int j = 0; j < kUpdItems; ++j) {
+        vs[j] = (int32_t)(i0 + j);
+        ds[j] = (uint8_t)(w >> (8 * j));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kUpdItems; ++j) {
+        const int64_t i = i0 + j;
+        vs[j] = i < cnt ? (round == 1 ? (int32_t)i : in[i]) : -1;
+      }
+#pragma unroll
+      for (int j = 0; j < kUpdItems; ++j) ds[j] = vs[j] >= 0 ? next[vs[j]] : 0;
+    }
+    int mine = 0;
+#pragma unroll
+    for (int j = 0; j < kUpdItems; ++j) {
+      const int32_t v = vs[j];
+      if (v < 0) continue;
+      const uint8_t d = ds[j];
       if (d == 1) {  // engine.cpp:137-143: candidate joins the MIS
         state[v] = TCMIS_IN_MIS;
         key[v] = 0;
@@ -175,22 +258,24 @@ __global__ void __launch_bounds__(256)
         next[v] = 0;
         ++rem;
       } else {
-        surv = true;
+        ++mine;
         if (fresh)  // engine.cpp:324-325: next round's redrawn priority
           key[v] = ((vertex_hash_m((uint64_t)v, fresh_m) >> 32) << 32) | (uint64_t)(v + 1);
       }
     }
-    const unsigned m = __ballot_sync(0xffffffffu, surv);
-    if (m) {
-      const int leader = __ffs(m) - 1;
-      int pos = 0;
-      if (lane == leader) pos = atomicAdd(&ctrl->wl_count[out_slot], __popc(m));
-      pos = __shfl_sync(0xffffffffu, pos, leader);
-      if (surv) out[pos + __popc(m & ((1u << lane) - 1u))] = v;
-    }
+    int pos, total;
+    BlockScan(scan_tmp).ExclusiveSum(mine, pos, total);
+    if (threadIdx.x == 0) s_base = total ? atomicAdd(&ctrl->wl_count[out_slot], total) : 0;
+    __syncthreads();
+    pos += s_base;
+#pragma unroll
+    for (int j = 0; j < kUpdItems; ++j)
+      if (vs[j] >= 0 && ds[j] == 0) out[pos++] = vs[j];
+    __syncthreads();  // scan_tmp / s_base reuse
   }
   if (seg_mode == 1) {  // spmv.cpp:37-46, per block column (A is symmetric)
-    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nseg; b += stride) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nseg;
+         b += (int64_t)gridDim.x * blockDim.x) {
       if (segflag[b]) {
         ev += (unsigned long long)rowtiles[b];
         segflag[b] = 0;
@@ -208,17 +293,16 @@ __global__ void __launch_bounds__(256)
     __threadfence();
     volatile Ctrl *vc = ctrl;
     const int32_t alive = vc->wl_count[out_slot];
-    if (round - 1 < vc->max_rounds) {
-      DevRound r;
-      r.sel = vc->sel;
-      r.rem = vc->rem;
-      r.alive = (unsigned long long)alive;
-      r.eval = seg_mode == 1 ? vc->eval : 0;
-      r.skip = seg_mode == 1 ? (unsigned long long)total_tiles - vc->eval : 0;
-      rounds[round - 1] = r;
-    } else {
-      vc->overflow = 1;
-    }
+    DevRound r;
+    r.sel = vc->sel;
+    r.rem = vc->rem;
+    r.alive = (unsigned long long)alive;
+    r.eval = seg_mode == 1 ? vc->eval : 0;
+    r.skip = seg_mode == 1 ? (unsigned long long)total_tiles - vc->eval : 0;
+    // a ring: the host loop drains one slot per round; the graph loop flags
+    // the (pathological, > max_rounds) case and the host re-runs step-wise
+    rounds[(round - 1) % vc->max_rounds] = r;
+    if (round > vc->max_rounds) vc->overflow = 1;
     vc->alive = alive;
     vc->sel = 0;
     vc->rem = 0;
@@ -226,6 +310,7 @@ __global__ void __launch_bounds__(256)
     vc->ticket = 0;
     vc->wl_count[round & 1] = 0;
     vc->round = round + 1;
+    if (use_cond) cudaGraphSetConditional(cond, alive > 0 ? 1u : 0u);
   }
 }
 
@@ -308,6 +393,7 @@ void free_workspace(Workspace &ws) {
   cudaFree(ws.rounds);
   cudaFreeHost(ws.h_rounds);
   cudaFree(ws.cub_tmp);
+  if (ws.exec) cudaGraphExecDestroy(ws.exec);
   ws = Workspace{};
 }
 
@@ -326,6 +412,10 @@ int ensure_workspace(tcmis_graph *g) {
   Workspace &ws = g->ws;
   const size_t n = (size_t)std::max<int32_t>(g->n, 1);
   if (ws.n_cap < n) {
+    if (ws.exec) {  // the cached round graph points at the old buffers
+      cudaGraphExecDestroy(ws.exec);
+      ws.exec = nullptr;
+    }
     cudaFree(ws.key);
     cudaFree(ws.state);
     cudaFree(ws.next);
@@ -413,6 +503,79 @@ int validate(const tcmis_graph *g, const tcmis_config *c) {
 
 }  // namespace
 
+struct RoundArgs {
+  int32_t n;
+  const int64_t *off;
+  const int32_t *nbr;
+  int T, seg_mode, fresh;
+  int32_t nseg;
+  int64_t total_tiles;
+  const int32_t *rowtiles;
+  uint64_t seed;
+  int sel_grid, upd_grid;
+  bool operator==(const RoundArgs &o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
+};
+
+int launch_select(tcmis_graph *g, const RoundArgs &a) {
+  Workspace &ws = g->ws;
+  k_select<<<a.sel_grid, kSelBlock, 0, g->ctx->stream>>>(
+      a.n, a.off, a.nbr, ws.key, ws.next, a.seg_mode ? ws.segflag : nullptr, a.T, ws.ctrl,
+      ws.wl[0], ws.wl[1]);
+  TCMIS_LAUNCHED(g->ctx);
+  return 0;
+}
+
+int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle cond,
+                  int use_cond) {
+  Workspace &ws = g->ws;
+  k_update<<<a.upd_grid, kUpdBlock, 0, g->ctx->stream>>>(
+      a.n, ws.key, ws.state, ws.next, ws.ctrl, ws.wl[0], ws.wl[1], ws.segflag, a.rowtiles,
+      a.nseg, a.total_tiles, a.seg_mode, ws.rounds, a.fresh, a.seed, cond, use_cond);
+  TCMIS_LAUNCHED(g->ctx);
+  return 0;
+}
+
+// Instantiate (once per distinct argument set) the graph
+//   WHILE(cond) { k_select ; k_update }
+// over this workspace's buffers.
+int ensure_round_graph(tcmis_graph *g, const RoundArgs &a) {
+  Workspace &ws = g->ws;
+  static_assert(sizeof(RoundArgs) <= sizeof(ws.graph_key), "graph key too small");
+  if (ws.exec && std::memcmp(ws.graph_key, &a, sizeof(a)) == 0) return 0;
+  if (ws.exec) {
+    cudaGraphExecDestroy(ws.exec);
+    ws.exec = nullptr;
+  }
+  cudaStream_t st = g->ctx->stream;
+  cudaGraph_t graph = nullptr;
+  TCMIS_CUDA(cudaGraphCreate(&graph, 0));
+  cudaGraphConditionalHandle cond;
+  TCMIS_CUDA(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams p{};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = cond;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  TCMIS_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &p));
+  cudaGraph_t body = p.conditional.phGraph_out[0];
+  TCMIS_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed));
+  int rc = launch_select(g, a);
+  if (!rc) rc = launch_update(g, a, cond, 1);
+  cudaGraph_t captured = nullptr;
+  cudaError_t e = cudaStreamEndCapture(st, &captured);
+  if (!rc && e != cudaSuccess) rc = cuda_error(e, "cudaStreamEndCapture");
+  if (!rc) {
+    e = cudaGraphInstantiate(&ws.exec, graph, 0);
+    if (e != cudaSuccess) rc = cuda_error(e, "cudaGraphInstantiate");
+  }
+  cudaGraphDestroy(graph);
+  g->ctx->launches -= 2;  // capture is not execution
+  if (!rc) std::memcpy(ws.graph_key, &a, sizeof(a));
+  return rc;
+}
+
 int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
                int32_t max_stats, int32_t *n_iter, int64_t *mis_count_out) {
   if (int rc = validate(g, cfg)) return rc;
@@ -444,53 +607,90 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   TCMIS_CUDA(cudaMemcpyAsync(ws.ctrl, ws.h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
   if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
 
-  const int sel_grid = ctx->num_sms * 8;
-  const int upd_grid = ctx->num_sms * 4;
+  RoundArgs a;
+  a.n = g->n;
+  a.off = g->d_off;
+  a.nbr = g->d_nbr;
+  a.T = T > 0 ? T : 1;
+  a.seg_mode = seg_mode;
+  a.nseg = nseg;
+  a.total_tiles = g->tile_total;
+  a.rowtiles = g->d_rowtiles;
+  a.fresh = fresh ? 1 : 0;
+  a.seed = cfg->seed;
+  a.sel_grid = ctx->num_sms * 8;
+  a.upd_grid = ctx->num_sms * 4;
+
+  std::vector<DevRound> rounds_h;
   std::vector<uint8_t> h_next, h_state, h_cand;
-  std::vector<tcmis_iter_stats> local;
   std::vector<float> t1, t3;
-  int round = 0;
-  for (;;) {
-    ++round;
-    if (round > g->n)  // engine.cpp:248-249
-      return set_error(TCMIS_E_RUNTIME, "iteration cap exceeded; engine livelock");
-    if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[0], st));
-    k_select<8><<<sel_grid, 256, 0, st>>>(g->n, g->d_off, g->d_nbr, ws.key, ws.next,
-                                          seg_mode ? ws.segflag : nullptr, T > 0 ? T : 1,
-                                          ws.ctrl, ws.wl[0], ws.wl[1]);
-    TCMIS_LAUNCHED(ctx);
-    if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[1], st));
-    if (cfg->observer && H != TCMIS_H3) {
-      h_next.resize(g->n);
-      h_state.resize(g->n);
-      h_cand.resize(g->n);
-      TCMIS_CUDA(cudaMemcpyAsync(h_next.data(), ws.next, g->n, cudaMemcpyDeviceToHost, st));
-      TCMIS_CUDA(cudaMemcpyAsync(h_state.data(), ws.state, g->n, cudaMemcpyDeviceToHost, st));
-      TCMIS_CUDA(cudaStreamSynchronize(st));
-      for (int32_t v = 0; v < g->n; ++v) h_cand[v] = h_next[v] == 1 && h_state[v] == TCMIS_ALIVE;
-      cfg->observer(cfg->observer_user, round, h_cand.data(), h_state.data(), g->n);
-    }
-    k_update<<<upd_grid, 256, 0, st>>>(g->n, ws.key, ws.state, ws.next, ws.ctrl, ws.wl[0],
-                                       ws.wl[1], ws.segflag, g->d_rowtiles, nseg, g->tile_total,
-                                       seg_mode, ws.rounds, fresh ? 1 : 0, cfg->seed);
-    TCMIS_LAUNCHED(ctx);
-    if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[2], st));
+  bool step = cfg->observer || timing || (cfg->flags & TCMIS_F_HOST_LOOP);
+  if (!step) {
+    // the whole round loop is one CUDA graph: a conditional WHILE node whose
+    // body is {k_select, k_update}; k_update's last block writes the loop
+    // condition (alive > 0), so no host round trip happens between rounds.
+    if (int rc = ensure_round_graph(g, a)) return rc;
+    TCMIS_CUDA(cudaGraphLaunch(ws.exec, st));
+    ctx->launches += 2;  // per round, counted below
     TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
     TCMIS_CUDA(cudaStreamSynchronize(st));
-    if (timing) {
-      float a = 0, b = 0;
-      cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
-      cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
-      t1.push_back(a);
-      t3.push_back(b);
+    if (ws.h_ctrl->overflow) {
+      // more rounds than the on-device ring holds: redo step-wise, draining
+      // the statistics every round (pathological inputs such as long paths)
+      step = true;
+      if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.key, nullptr,
+                                     ws.state, ws.next))
+        return rc;
+      *ws.h_ctrl = c0;
+      TCMIS_CUDA(cudaMemcpyAsync(ws.ctrl, ws.h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+      if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
+    } else {
+      const int rr = ws.h_ctrl->round - 1;
+      ctx->launches += 2 * (int64_t)rr - 2;
+      rounds_h.resize(rr);
+      TCMIS_CUDA(cudaMemcpyAsync(rounds_h.data(), ws.rounds, sizeof(DevRound) * rr,
+                                 cudaMemcpyDeviceToHost, st));
     }
-    if (ws.h_ctrl->alive == 0) break;
   }
-  const int rounds_run = round;
-  if (rounds_run > ws.round_cap)
-    return set_error(TCMIS_E_RUNTIME, "round statistics capacity exceeded");
-  TCMIS_CUDA(cudaMemcpyAsync(ws.h_rounds, ws.rounds, sizeof(DevRound) * rounds_run,
-                             cudaMemcpyDeviceToHost, st));
+  if (step) {
+    int round = 0;
+    for (;;) {
+      ++round;
+      if (round > g->n)  // engine.cpp:248-249
+        return set_error(TCMIS_E_RUNTIME, "iteration cap exceeded; engine livelock");
+      if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[0], st));
+      if (int rc = launch_select(g, a)) return rc;
+      if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[1], st));
+      if (cfg->observer && H != TCMIS_H3) {
+        h_next.resize(g->n);
+        h_state.resize(g->n);
+        h_cand.resize(g->n);
+        TCMIS_CUDA(cudaMemcpyAsync(h_next.data(), ws.next, g->n, cudaMemcpyDeviceToHost, st));
+        TCMIS_CUDA(cudaMemcpyAsync(h_state.data(), ws.state, g->n, cudaMemcpyDeviceToHost, st));
+        TCMIS_CUDA(cudaStreamSynchronize(st));
+        for (int32_t v = 0; v < g->n; ++v)
+          h_cand[v] = h_next[v] == 1 && h_state[v] == TCMIS_ALIVE;
+        cfg->observer(cfg->observer_user, round, h_cand.data(), h_state.data(), g->n);
+      }
+      if (int rc = launch_update(g, a, 0, 0)) return rc;
+      if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[2], st));
+      TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+      DevRound dr;
+      TCMIS_CUDA(cudaMemcpyAsync(&dr, ws.rounds + (round - 1) % ws.round_cap, sizeof(DevRound),
+                                 cudaMemcpyDeviceToHost, st));
+      TCMIS_CUDA(cudaStreamSynchronize(st));
+      rounds_h.push_back(dr);
+      if (timing) {
+        float x = 0, y = 0;
+        cudaEventElapsedTime(&x, ctx->ev[0], ctx->ev[1]);
+        cudaEventElapsedTime(&y, ctx->ev[1], ctx->ev[2]);
+        t1.push_back(x);
+        t3.push_back(y);
+      }
+      if (ws.h_ctrl->alive == 0) break;
+    }
+  }
+  const int rounds_run = (int)rounds_h.size();
   // ascending MIS ids (engine.cpp:293 sorts; ordered compaction needs no sort)
   {
     thrust::counting_iterator<int32_t> ids(0);
@@ -542,7 +742,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   }
   for (int r = 0; r < rounds_run; ++r) {
     if (!stats || r >= max_stats) break;
-    const DevRound &d = ws.h_rounds[r];
+    const DevRound &d = rounds_h[r];
     tcmis_iter_stats s{};
     s.iteration = r + 1;
     s.candidates_selected = (int64_t)d.sel;

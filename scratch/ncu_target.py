@@ -1,0 +1,11 @@
+# one warm solve + one profiled solve of the bench config (used under ncu only)
+import sys; sys.path.insert(0, '.')
+import paper_2605_29604_b200 as tc
+cfgname = sys.argv[1] if len(sys.argv) > 1 else "rmat22"
+ctx = tc.Context(0)
+import bench
+dg = bench.make_device_graph(tc, cfgname, ctx)
+dg.tile(16)
+for _ in range(2):
+    r = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2))
+print("ok", r.cardinality(), len(r.iterations))
