@@ -52,7 +52,7 @@ struct Ctrl {
   unsigned int ticket; // last-block election in k_update
   int32_t max_rounds;  // capacity of the DevRound array
   int32_t overflow;    // set when rounds exceeded max_rounds
-  int32_t pad;
+  int32_t long_count;  // entries of the long-row list this round
 };
 
 struct Workspace {
@@ -64,6 +64,7 @@ struct Workspace {
   int32_t *wl[2] = {nullptr, nullptr};
   uint8_t *segflag = nullptr;
   int32_t *mis = nullptr;
+  int32_t *long_list = nullptr;  // vertices whose row outlived the thread probe
   int64_t *mis_count = nullptr;
   Ctrl *ctrl = nullptr;        // device
   Ctrl *h_ctrl = nullptr;      // pinned host mirror

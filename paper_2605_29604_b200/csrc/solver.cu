@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "select.cuh"
 
 namespace tcmis_b200 {
 
@@ -64,101 +65,6 @@ __global__ void k_priorities(int32_t n, const int64_t *__restrict__ off, int mod
 }
 
 // ----------------------------------------------------------------- rounds
-
-// Two stages per block-chunk of kSelBlock worklist entries:
-//  A) one thread per vertex (coalesced offsets, 32 vertices in flight per
-//     warp) probes the last K entries of its row -- on R-MAT the high ids at
-//     the end of a sorted row are the low-degree, high-priority vertices, so
-//     a blocked vertex usually exits here.  A row of <= K entries is decided
-//     outright (and, as a candidate, pushes from registers).
-//  B) the undecided long rows are handed to the block's warps through shared
-//     memory: a warp scans the rest of the row from its end, 32 then 128
-//     entries per step (4 independent loads per lane), with an early exit on
-//     the first higher alive neighbour, and pushes if the vertex survives.
-// Any scan order gives the same answer (max over a set).
-constexpr int kSelBlock = 256;
-constexpr int kProbe = 4;
-
-__global__ void __launch_bounds__(kSelBlock)
-    k_select(int32_t n, const int64_t *__restrict__ off, const int32_t *__restrict__ nbr,
-             const uint64_t *__restrict__ key, uint8_t *__restrict__ next,
-             uint8_t *__restrict__ segflag, int T, const Ctrl *__restrict__ ctrl,
-             const int32_t *__restrict__ wl0, const int32_t *__restrict__ wl1) {
-  __shared__ int32_t s_def[kSelBlock];
-  __shared__ int s_ndef;
-  const int round = ctrl->round;
-  const int64_t cnt = round == 1 ? n : ctrl->wl_count[round & 1];
-  const int32_t *wl = (round & 1) ? wl1 : wl0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int kWarps = kSelBlock / 32;
-  for (int64_t base = (int64_t)blockIdx.x * kSelBlock; base < cnt;
-       base += (int64_t)gridDim.x * kSelBlock) {
-    if (threadIdx.x == 0) s_ndef = 0;
-    __syncthreads();
-    const int64_t i = base + threadIdx.x;
-    if (i < cnt) {
-      const int32_t v = round == 1 ? (int32_t)i : __ldg(&wl[i]);
-      const int64_t s = __ldg(&off[v]), e = __ldg(&off[v + 1]);
-      const uint64_t kv = __ldg(&key[v]);
-      const int64_t d = e - s;
-      int32_t u[kProbe];
-#pragma unroll
-      for (int j = 0; j < kProbe; ++j) u[j] = j < d ? __ldg(&nbr[e - 1 - j]) : -1;
-      bool blocked = false;
-#pragma unroll
-      for (int j = 0; j < kProbe; ++j)
-        if (u[j] >= 0) blocked |= __ldg(&key[u[j]]) > kv;
-      if (!blocked) {
-        if (d <= kProbe) {
-          next[v] = 1;
-          if (segflag) segflag[v / T] = 1;
-#pragma unroll
-          for (int j = 0; j < kProbe; ++j)
-            if (u[j] >= 0) next[u[j]] = 2;
-        } else {
-          s_def[atomicAdd(&s_ndef, 1)] = v;
-        }
-      }
-    }
-    __syncthreads();
-    const int nd = s_ndef;
-    for (int q = warp; q < nd; q += kWarps) {
-      const int32_t v = s_def[q];
-      const int64_t s = __ldg(&off[v]), e = __ldg(&off[v + 1]);
-      const uint64_t kv = __ldg(&key[v]);
-      int64_t hi = e - kProbe;  // [s, hi) still unexamined
-      bool blocked = false;
-      {  // first step: 32 entries
-        const int64_t idx = hi - 1 - lane;
-        const bool b = idx >= s && __ldg(&key[__ldg(&nbr[idx])]) > kv;
-        blocked = __any_sync(0xffffffffu, b);
-        hi -= 32;
-      }
-      while (!blocked && hi > s) {  // then 128 entries per step
-        int32_t uu[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int64_t idx = hi - 1 - lane - 32 * j;
-          uu[j] = idx >= s ? __ldg(&nbr[idx]) : -1;
-        }
-        bool b = false;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (uu[j] >= 0) b |= __ldg(&key[uu[j]]) > kv;
-        blocked = __any_sync(0xffffffffu, b);
-        hi -= 128;
-      }
-      if (!blocked) {
-        if (lane == 0) {
-          next[v] = 1;
-          if (segflag) segflag[v / T] = 1;
-        }
-        for (int64_t idx = s + lane; idx < e; idx += 32) next[__ldg(&nbr[idx])] = 2;
-      }
-    }
-    __syncthreads();
-  }
-}
 
 // Block-wide sum of three counters into the control block.
 __device__ __forceinline__ void block_add3(unsigned long long a, unsigned long long b,
@@ -309,6 +215,7 @@ __global__ void __launch_bounds__(kUpdBlock)
     vc->eval = 0;
     vc->ticket = 0;
     vc->wl_count[round & 1] = 0;
+    vc->long_count = 0;
     vc->round = round + 1;
     if (use_cond) cudaGraphSetConditional(cond, alive > 0 ? 1u : 0u);
   }
@@ -387,6 +294,7 @@ void free_workspace(Workspace &ws) {
   cudaFree(ws.wl[1]);
   cudaFree(ws.segflag);
   cudaFree(ws.mis);
+  cudaFree(ws.long_list);
   cudaFree(ws.mis_count);
   cudaFree(ws.ctrl);
   cudaFreeHost(ws.h_ctrl);
@@ -422,6 +330,7 @@ int ensure_workspace(tcmis_graph *g) {
     cudaFree(ws.wl[0]);
     cudaFree(ws.wl[1]);
     cudaFree(ws.mis);
+    cudaFree(ws.long_list);
     ws.n_cap = 0;
     if (int rc = dev_alloc(&ws.key, n)) return rc;
     if (int rc = dev_alloc(&ws.state, n)) return rc;
@@ -429,6 +338,7 @@ int ensure_workspace(tcmis_graph *g) {
     if (int rc = dev_alloc(&ws.wl[0], n)) return rc;
     if (int rc = dev_alloc(&ws.wl[1], n)) return rc;
     if (int rc = dev_alloc(&ws.mis, n)) return rc;
+    if (int rc = dev_alloc(&ws.long_list, n)) return rc;
     TCMIS_CUDA(cudaMemsetAsync(ws.next, 0, n, g->ctx->stream));
     ws.n_cap = n;
   }
@@ -518,9 +428,13 @@ struct RoundArgs {
 
 int launch_select(tcmis_graph *g, const RoundArgs &a) {
   Workspace &ws = g->ws;
-  k_select<<<a.sel_grid, kSelBlock, 0, g->ctx->stream>>>(
-      a.n, a.off, a.nbr, ws.key, ws.next, a.seg_mode ? ws.segflag : nullptr, a.T, ws.ctrl,
-      ws.wl[0], ws.wl[1]);
+  cudaStream_t st = g->ctx->stream;
+  uint8_t *seg = a.seg_mode ? ws.segflag : nullptr;
+  k_select<<<a.sel_grid, kSelBlock, 0, st>>>(a.n, a.off, a.nbr, ws.key, ws.next, seg, a.T, 1,
+                                             ws.ctrl, ws.wl[0], ws.wl[1], ws.long_list);
+  TCMIS_LAUNCHED(g->ctx);
+  k_select_long<<<a.sel_grid, kSelBlock, 0, st>>>(a.off, a.nbr, ws.key, ws.next, seg, a.T, 1,
+                                                  ws.ctrl, ws.long_list);
   TCMIS_LAUNCHED(g->ctx);
   return 0;
 }
@@ -571,7 +485,7 @@ int ensure_round_graph(tcmis_graph *g, const RoundArgs &a) {
     if (e != cudaSuccess) rc = cuda_error(e, "cudaGraphInstantiate");
   }
   cudaGraphDestroy(graph);
-  g->ctx->launches -= 2;  // capture is not execution
+  g->ctx->launches -= 3;  // capture is not execution
   if (!rc) std::memcpy(ws.graph_key, &a, sizeof(a));
   return rc;
 }
@@ -631,7 +545,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     // condition (alive > 0), so no host round trip happens between rounds.
     if (int rc = ensure_round_graph(g, a)) return rc;
     TCMIS_CUDA(cudaGraphLaunch(ws.exec, st));
-    ctx->launches += 2;  // per round, counted below
+    ctx->launches += 3;  // per round, counted below
     TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
     TCMIS_CUDA(cudaStreamSynchronize(st));
     if (ws.h_ctrl->overflow) {
@@ -646,7 +560,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
     } else {
       const int rr = ws.h_ctrl->round - 1;
-      ctx->launches += 2 * (int64_t)rr - 2;
+      ctx->launches += 3 * (int64_t)rr - 3;
       rounds_h.resize(rr);
       TCMIS_CUDA(cudaMemcpyAsync(rounds_h.data(), ws.rounds, sizeof(DevRound) * rr,
                                  cudaMemcpyDeviceToHost, st));

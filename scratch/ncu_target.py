@@ -7,5 +7,5 @@ import bench
 dg = bench.make_device_graph(tc, cfgname, ctx)
 dg.tile(16)
 for _ in range(2):
-    r = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2))
+    r = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, host_loop=True))
 print("ok", r.cardinality(), len(r.iterations))
