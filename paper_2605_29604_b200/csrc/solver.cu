@@ -128,25 +128,17 @@ __global__ void __launch_bounds__(kUpdBlock)
   unsigned long long sel = 0, rem = 0, ev = 0;
   constexpr int64_t kChunk = (int64_t)kUpdBlock * kUpdItems;
   for (int64_t base = (int64_t)blockIdx.x * kChunk; base < cnt; base += (int64_t)gridDim.x * kChunk) {
-    const int64_t i0 = base + (int64_t)threadIdx.x * kUpdItems;
+    // striped: item j of thread t is base + j*kUpdBlock + t, so every load and
+    // store instruction of the warp is coalesced on the identity worklist
     int32_t vs[kUpdItems];
     uint8_t ds[kUpdItems];
-    if (round == 1 && i0 + kUpdItems <= cnt) {  // identity worklist: one 8-byte load
-      const uint64_t w = *reinterpret_cast<const uint64_t *>(next + i0);
 #pragma unroll
-      for (int j = 0; j < kUpdItems; ++j) {
-        vs[j] = (int32_t)(i0 + j);
-        ds[j] = (uint8_t)(w >> (8 * j));
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < kUpdItems; ++j) {
-        const int64_t i = i0 + j;
-        vs[j] = i < cnt ? (round == 1 ? (int32_t)i : in[i]) : -1;
-      }
-#pragma unroll
-      for (int j = 0; j < kUpdItems; ++j) ds[j] = vs[j] >= 0 ? next[vs[j]] : 0;
+    for (int j = 0; j < kUpdItems; ++j) {
+      const int64_t i = base + (int64_t)j * kUpdBlock + threadIdx.x;
+      vs[j] = i < cnt ? (round == 1 ? (int32_t)i : in[i]) : -1;
     }
+#pragma unroll
+    for (int j = 0; j < kUpdItems; ++j) ds[j] = vs[j] >= 0 ? next[vs[j]] : 0;
     int mine = 0;
 #pragma unroll
     for (int j = 0; j < kUpdItems; ++j) {

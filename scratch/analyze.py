@@ -29,3 +29,14 @@ for K in (1,2,4,8,16,32):
 for lo,hi in ((5,8),(9,16),(17,32),(33,64),(65,256),(257,1024),(1025,8192),(8193,1<<40)):
     s=(exam>=lo)&(exam<=hi)
     print(f'exam in [{lo},{hi}]: {s.sum()} vertices, entries {exam[s].sum()}, cand {(cand&s).sum()}')
+# push-store hotness in round 1
+cs = cand[src]
+tgt = g.nbr[cs]
+print('push stores', tgt.size)
+lines = tgt // 128
+cnt = np.bincount(lines)
+top = np.sort(cnt)[::-1][:10]
+print('stores to hottest 128B lines of next[]:', top.tolist())
+kl = (tgt // 16)  # key lines (8 B keys, 16 per line)
+c2 = np.bincount(g.nbr // 16)
+print('gathers (all entries) to hottest key lines:', np.sort(c2)[::-1][:5].tolist())
