@@ -148,7 +148,9 @@ def run_ours(args) -> dict:
     m = nnz // 2
     tiles = dg.tile(16)
     log(f"[bench] {args.config}: n={n} m={m} tiles={tiles} (setup {time.time() - t0:.1f}s)")
-    cfg = tc.EngineConfig(heuristic=HEUR[args.heuristic], seed=1, tile_dim=16)
+    excl = {"auto": tc.Exclusion.AUTO, "push": tc.Exclusion.PUSH,
+            "pull": tc.Exclusion.CSR_PULL}[args.exclusion]
+    cfg = tc.EngineConfig(heuristic=HEUR[args.heuristic], seed=1, tile_dim=16, exclusion=excl)
     c_cfg, _keep = cfg._c()
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")  # > 126 MB L2
@@ -193,7 +195,8 @@ def run_ours(args) -> dict:
     value = world * m / (ms_per_step * 1e-3) / 1e9  # replicas: every rank solves its graph
 
     # ---- kernel roofline: per-kernel CUDA events (step-wise loop, same kernels)
-    cfg_t = tc.EngineConfig(heuristic=HEUR[args.heuristic], seed=1, tile_dim=16, timing=True)
+    cfg_t = tc.EngineConfig(heuristic=HEUR[args.heuristic], seed=1, tile_dim=16, timing=True,
+                            exclusion=excl)
     sel_ms, upd_ms, per_round = [], [], None
     for _ in range(max(1, min(args.steps, 5))):
         r = tc.run_mis(dg, cfg_t)
@@ -432,6 +435,7 @@ def main():
     ap.add_argument("--heuristic", default="h2", choices=list(HEUR))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exclusion", default="auto", choices=["auto", "push", "pull"])
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the dominant kernel (profiles/)")
     args = ap.parse_args()

@@ -28,7 +28,7 @@ NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC,-fvisibility=hidden,-ffp-contract=off",
     "-I", INC, "-I", CSRC,
-]
+] + os.environ.get("TCMIS_NVCC_EXTRA", "").split()
 CU_SOURCES = ["capi.cu", "solver.cu", "tiles.cu", "gen.cu"]
 CXX_SOURCES = ["engine.cpp"]
 

@@ -178,6 +178,7 @@ TCMIS_API void tcmis_graph_destroy(tcmis_graph *g) {
     cudaFree(g->d_nbr);
   }
   cudaFree(g->d_rowtiles);
+  cudaFree(g->d_nz);
   free_workspace(g->ws);
   delete g;
 }

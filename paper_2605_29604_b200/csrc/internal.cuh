@@ -52,7 +52,9 @@ struct Ctrl {
   unsigned int ticket; // last-block election in k_update
   int32_t max_rounds;  // capacity of the DevRound array
   int32_t overflow;    // set when rounds exceeded max_rounds
-  int32_t long_count;  // entries of the long-row list this round
+  int32_t long_count;  // entries of the select long-row list this round
+  int32_t pull_count;  // entries of the pull long-row list this round
+  int32_t pad2;
 };
 
 struct Workspace {
@@ -64,7 +66,8 @@ struct Workspace {
   int32_t *wl[2] = {nullptr, nullptr};
   uint8_t *segflag = nullptr;
   int32_t *mis = nullptr;
-  int32_t *long_list = nullptr;  // vertices whose row outlived the thread probe
+  int32_t *long_list = nullptr;   // select: rows that outlived the thread probe
+  int32_t *long_list2 = nullptr;  // pull exclusion: same, for k_round_end
   int64_t *mis_count = nullptr;
   Ctrl *ctrl = nullptr;        // device
   Ctrl *h_ctrl = nullptr;      // pinned host mirror
@@ -99,6 +102,11 @@ struct tcmis_graph {
   int32_t tile_nb = 0;
   int32_t *d_rowtiles = nullptr;
   int64_t tile_total = 0;
+  // per-graph preparation for the solve (computed once)
+  bool prepared = false;
+  int32_t *d_nz = nullptr;  // ascending ids of non-isolated vertices (round-1 select list)
+  int32_t nz_count = 0;
+  int64_t max_degree = 0;
   tcmis_b200::Workspace ws;
 };
 

@@ -35,7 +35,6 @@
 namespace tcmis_b200 {
 
 constexpr int kSelBlock = 256;
-constexpr int kProbe = 4;
 constexpr int kStep = 4;
 constexpr int kThreadMax = 32;
 
@@ -47,95 +46,141 @@ __device__ __forceinline__ void mark_candidate(int32_t v, uint8_t *next, uint8_t
 // push: every neighbour of a candidate is excluded this round (spmv.cpp:18-59
 // nc > 0, engine.cpp:144-147).  Neighbours of a candidate are never
 // candidates, so next[u] is 0 or 2 and the filtered store is idempotent.
-__device__ __forceinline__ void exclude(uint8_t *__restrict__ next, int32_t u) {
+#ifndef TCMIS_PUSH_FILTER
+#define TCMIS_PUSH_FILTER 2  // 0 none, 1 ld.ca of next[u], 2 per-block shared-memory tag table
+#endif
+#ifndef TCMIS_FILTER_LOG
+#define TCMIS_FILTER_LOG 11
+#endif
+constexpr int kFilterLog = TCMIS_FILTER_LOG;
+constexpr int kFilterSlots = 1 << kFilterLog;
+
+struct PushFilter {
+  int32_t *tags;  // shared memory, kFilterSlots entries, -1 = empty
+};
+
+__device__ __forceinline__ void exclude(uint8_t *__restrict__ next, int32_t u, PushFilter f) {
+#if TCMIS_PUSH_FILTER == 1
   if (__ldca(&next[u]) != 2) next[u] = 2;
+#elif TCMIS_PUSH_FILTER == 2
+  // hub neighbours are pushed by thousands of candidates; a per-block
+  // direct-mapped table of recent targets removes the repeats (a miss or a
+  // racing duplicate only costs one redundant, idempotent store)
+  // hashed: R-MAT hubs are ids with many zero low bits and would all
+  // collide in a table indexed by the low bits
+  int32_t *slot = &f.tags[((uint32_t)u * 2654435761u) >> (32 - kFilterLog)];
+  if (*slot != u) {
+    *slot = u;
+    next[u] = 2;
+  }
+#else
+  next[u] = 2;
+#endif
 }
 
 __device__ __forceinline__ void push_row_thread(const int32_t *__restrict__ nbr, int64_t s,
-                                                int64_t e, uint8_t *__restrict__ next) {
+                                                int64_t e, uint8_t *__restrict__ next,
+                                                PushFilter f) {
   for (int64_t p = s; p < e; p += kStep) {
     int32_t u[kStep];
 #pragma unroll
     for (int j = 0; j < kStep; ++j) u[j] = p + j < e ? __ldg(&nbr[p + j]) : -1;
 #pragma unroll
     for (int j = 0; j < kStep; ++j)
-      if (u[j] >= 0) exclude(next, u[j]);
+      if (u[j] >= 0) exclude(next, u[j], f);
   }
 }
 
-__global__ void __launch_bounds__(kSelBlock)
-    k_select(int32_t n, const int64_t *__restrict__ off, const int32_t *__restrict__ nbr,
+#ifndef TCMIS_SEL_MINB
+#define TCMIS_SEL_MINB 8
+#endif
+
+// Per-thread state machine: every loop iteration each lane does ONE unit of
+// work -- fetch a vertex and probe the last kStep entries of its row, probe
+// the next kStep entries, or push to kStep neighbours -- so lanes never wait
+// for the slowest vertex of their warp (the SIMT lockstep of a plain
+// per-vertex loop cost ~4x at R-MAT s22, where a few candidates per warp have
+// 20-50-entry rows to scan and push).
+enum : int { kFetch = 0, kScan = 1, kPush = 2, kDone = 3 };
+
+__global__ void __launch_bounds__(kSelBlock, TCMIS_SEL_MINB)
+    k_select(int32_t n1, const int32_t *__restrict__ nz, const int64_t *__restrict__ off,
+             const int32_t *__restrict__ nbr,
              const uint64_t *__restrict__ key, uint8_t *__restrict__ next,
              uint8_t *__restrict__ segflag, int T, int push, Ctrl *__restrict__ ctrl,
              const int32_t *__restrict__ wl0, const int32_t *__restrict__ wl1,
              int32_t *__restrict__ long_list) {
   const int round = ctrl->round;
-  const int64_t cnt = round == 1 ? n : ctrl->wl_count[round & 1];
-  const int32_t *wl = (round & 1) ? wl1 : wl0;
+  // round 1 visits only the non-isolated vertices (k_priorities already
+  // marked the isolated ones as candidates)
+  const int64_t cnt = round == 1 ? n1 : ctrl->wl_count[round & 1];
+  const int32_t *wl = round == 1 ? nz : ((round & 1) ? wl1 : wl0);
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * kSelBlock;
-  // software pipeline: (v, s, e, kv) of the next vertex are loaded while the
-  // current row is being scanned
-  int64_t i = (int64_t)blockIdx.x * kSelBlock + threadIdx.x;
-  int32_t nv = 0;
-  int64_t ns = 0, ne = 0;
-  uint64_t nk = 0;
-  if (i < cnt) {
-    nv = round == 1 ? (int32_t)i : __ldg(&wl[i]);
-    ns = __ldg(&off[nv]);
-    ne = __ldg(&off[nv + 1]);
-    nk = __ldg(&key[nv]);
+  __shared__ int32_t s_tags[TCMIS_PUSH_FILTER == 2 ? kFilterSlots : 1];
+  PushFilter f{s_tags};
+  if (TCMIS_PUSH_FILTER == 2) {
+    for (int t = threadIdx.x; t < kFilterSlots; t += kSelBlock) s_tags[t] = -1;
+    __syncthreads();
   }
-  // the loop bound is uniform per warp (i advances by the grid stride), so
-  // the ballot below sees the whole warp
-  for (int64_t wbase = i - lane; wbase < cnt; wbase += stride, i += stride) {
-    const bool have = i < cnt;
-    const int32_t v = nv;
-    const int64_t s = ns, e = ne;
-    const uint64_t kv = nk;
-    const int64_t inext = i + stride;
-    if (inext < cnt) {
-      nv = round == 1 ? (int32_t)inext : __ldg(&wl[inext]);
-      ns = __ldg(&off[nv]);
-      ne = __ldg(&off[nv + 1]);
-      nk = __ldg(&key[nv]);
+  int64_t i = (int64_t)blockIdx.x * kSelBlock + threadIdx.x - stride;
+  int mode = kFetch;
+  int32_t v = 0;
+  int64_t s = 0, e = 0, hi = 0;
+  uint64_t kv = 0;
+  // fetch: the next vertex of this thread's strided sequence; issued at the
+  // end of an iteration so its loads overlap the loop back-edge
+  auto fetch = [&]() {
+    i += stride;
+    if (i < cnt) {
+      v = __ldg(&wl[i]);
+      s = __ldg(&off[v]);
+      e = __ldg(&off[v + 1]);
+      kv = __ldg(&key[v]);
+      hi = e;
+      mode = kScan;
+    } else {
+      mode = kDone;
     }
+  };
+  fetch();
+  while (__any_sync(0xffffffffu, mode != kDone)) {
     bool defer = false;
-    if (have) {
-      int64_t hi = e;  // [s, hi) not yet examined
+    if (mode == kScan) {
+      int32_t u[kStep];
+#pragma unroll
+      for (int j = 0; j < kStep; ++j) u[j] = hi - 1 - j >= s ? __ldg(&nbr[hi - 1 - j]) : -1;
       bool blocked = false;
-      int32_t u[kProbe];
 #pragma unroll
-      for (int j = 0; j < kProbe; ++j) u[j] = hi - 1 - j >= s ? __ldg(&nbr[hi - 1 - j]) : -1;
-#pragma unroll
-      for (int j = 0; j < kProbe; ++j)
+      for (int j = 0; j < kStep; ++j)
         if (u[j] >= 0) blocked |= __ldg(&key[u[j]]) > kv;
-      hi -= kProbe;
-      while (!blocked && hi > s && e - hi < kThreadMax) {
-        int32_t w[kStep];
+      hi -= kStep;
+      if (blocked) {
+        mode = kFetch;
+      } else if (hi <= s) {
+        mark_candidate(v, next, segflag, T);
+        if (push && e - s <= kStep) {  // the whole row is still in registers
 #pragma unroll
-        for (int j = 0; j < kStep; ++j) w[j] = hi - 1 - j >= s ? __ldg(&nbr[hi - 1 - j]) : -1;
-#pragma unroll
-        for (int j = 0; j < kStep; ++j)
-          if (w[j] >= 0) blocked |= __ldg(&key[w[j]]) > kv;
-        hi -= kStep;
-      }
-      if (!blocked) {
-        if (hi <= s) {
-          mark_candidate(v, next, segflag, T);
-          if (push) {
-            if (e - s <= kProbe) {  // the whole row is still in registers
-#pragma unroll
-              for (int j = 0; j < kProbe; ++j)
-                if (u[j] >= 0) exclude(next, u[j]);
-            } else {
-              push_row_thread(nbr, s, e, next);
-            }
-          }
+          for (int j = 0; j < kStep; ++j)
+            if (u[j] >= 0) exclude(next, u[j], f);
+          mode = kFetch;
         } else {
-          defer = true;
+          mode = push ? kPush : kFetch;
+          hi = s;  // push cursor runs upward from s
         }
+      } else if (e - hi >= kThreadMax) {
+        defer = true;
+        mode = kFetch;
       }
+    } else if (mode == kPush) {
+      int32_t u[kStep];
+#pragma unroll
+      for (int j = 0; j < kStep; ++j) u[j] = hi + j < e ? __ldg(&nbr[hi + j]) : -1;
+#pragma unroll
+      for (int j = 0; j < kStep; ++j)
+        if (u[j] >= 0) exclude(next, u[j], f);
+      hi += kStep;
+      if (hi >= e) mode = kFetch;
     }
     const unsigned m = __ballot_sync(0xffffffffu, defer);
     if (m) {
@@ -145,6 +190,7 @@ __global__ void __launch_bounds__(kSelBlock)
       pos = __shfl_sync(0xffffffffu, pos, leader);
       if (defer) long_list[pos + __popc(m & ((1u << lane) - 1u))] = v;
     }
+    if (mode == kFetch) fetch();
   }
 }
 
@@ -155,6 +201,14 @@ __global__ void __launch_bounds__(kSelBlock)
                   const int32_t *__restrict__ long_list) {
   const int lane = threadIdx.x & 31;
   const int cnt = ctrl->long_count;
+  if (cnt == 0) return;
+  __shared__ int32_t s_tags[TCMIS_PUSH_FILTER == 2 ? kFilterSlots : 1];
+  PushFilter f{s_tags};
+  if (TCMIS_PUSH_FILTER == 2) {
+    for (int t = threadIdx.x; t < kFilterSlots; t += kSelBlock) s_tags[t] = -1;
+    __syncthreads();
+  }
+
   for (int64_t q = ((int64_t)blockIdx.x * kSelBlock + threadIdx.x) >> 5; q < cnt;
        q += ((int64_t)gridDim.x * kSelBlock) >> 5) {
     const int32_t v = long_list[q];
@@ -179,7 +233,7 @@ __global__ void __launch_bounds__(kSelBlock)
     if (!blocked) {
       if (lane == 0) mark_candidate(v, next, segflag, T);
       if (push)
-        for (int64_t idx = s + lane; idx < e; idx += 32) exclude(next, __ldg(&nbr[idx]));
+        for (int64_t idx = s + lane; idx < e; idx += 32) exclude(next, __ldg(&nbr[idx]), f);
     }
   }
 }

@@ -24,6 +24,7 @@
 
 #include "internal.cuh"
 #include "select.cuh"
+#include "update.cuh"
 
 namespace tcmis_b200 {
 
@@ -46,172 +47,52 @@ __device__ __forceinline__ uint32_t h2_value(double avg, int64_t deg, double eps
 __global__ void k_priorities(int32_t n, const int64_t *__restrict__ off, int mode,
                              uint64_t mseed, double avg, double scale, uint64_t *__restrict__ key,
                              uint32_t *__restrict__ p_out, uint8_t *__restrict__ state,
-                             uint8_t *__restrict__ next) {
+                             uint8_t *__restrict__ next, uint8_t *__restrict__ segflag, int T) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t h = vertex_hash_m((uint64_t)v, mseed);
+    const uint64_t h = vertex_hash_m((uint64_t)v, mseed);
+    const int64_t deg = off[v + 1] - off[v];
     uint32_t p;
     if (mode == 0) {
       p = (uint32_t)(h >> 32);
     } else {
       double eps = (double)(h >> 11) * 0x1.0p-53;  // hash_to_unit, priorities.cpp:25-27
-      p = h2_value(avg, off[v + 1] - off[v], eps, scale);
+      p = h2_value(avg, deg, eps, scale);
     }
     if (p_out) p_out[v] = p;
     if (key) key[v] = ((uint64_t)p << 32) | (uint64_t)(v + 1);
     if (state) state[v] = TCMIS_ALIVE;
-    if (next) next[v] = 0;
+    if (next) {
+      // an isolated vertex has no alive neighbour: it is a round-1 candidate
+      // (engine.cpp:94-99 leaves max_np at kNoNeighborKey) and round 1's
+      // select never has to visit it
+      next[v] = deg == 0 ? 1 : 0;
+      if (deg == 0 && segflag) segflag[v / T] = 1;
+    }
   }
 }
+
+__global__ void k_max_degree(int32_t n, const int64_t *__restrict__ off,
+                             unsigned long long *__restrict__ out) {
+  unsigned long long mx = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long d = (unsigned long long)(off[v + 1] - off[v]);
+    mx = d > mx ? d : mx;
+  }
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long t = __shfl_down_sync(0xffffffffu, mx, o);
+    mx = t > mx ? t : mx;
+  }
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
+}
+
+struct HasEdges {
+  const int64_t *off;
+  __device__ __forceinline__ bool operator()(int32_t v) const { return off[v + 1] > off[v]; }
+};
 
 // ----------------------------------------------------------------- rounds
-
-// Block-wide sum of three counters into the control block.
-__device__ __forceinline__ void block_add3(unsigned long long a, unsigned long long b,
-                                           unsigned long long c, Ctrl *ctrl) {
-  __shared__ unsigned long long sh[3][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int o = 16; o; o >>= 1) {
-    a += __shfl_down_sync(0xffffffffu, a, o);
-    b += __shfl_down_sync(0xffffffffu, b, o);
-    c += __shfl_down_sync(0xffffffffu, c, o);
-  }
-  if (lane == 0) {
-    sh[0][w] = a;
-    sh[1][w] = b;
-    sh[2][w] = c;
-  }
-  __syncthreads();
-  if (w == 0) {
-    const int nw = blockDim.x >> 5;
-    a = lane < nw ? sh[0][lane] : 0;
-    b = lane < nw ? sh[1][lane] : 0;
-    c = lane < nw ? sh[2][lane] : 0;
-    for (int o = 16; o; o >>= 1) {
-      a += __shfl_down_sync(0xffffffffu, a, o);
-      b += __shfl_down_sync(0xffffffffu, b, o);
-      c += __shfl_down_sync(0xffffffffu, c, o);
-    }
-    if (lane == 0) {
-      if (a) atomicAdd(&ctrl->sel, a);
-      if (b) atomicAdd(&ctrl->rem, b);
-      if (c) atomicAdd(&ctrl->eval, c);
-    }
-  }
-}
-
-// seg_mode: 0 = no tile counters, 1 = count and clear per round,
-// 2 = accumulate (h3: counters are taken once at the end).
-// Each thread owns kUpdItems consecutive worklist entries (blocked layout:
-// on round 1 the identity worklist makes that one 8-byte load of `next`);
-// survivors are compacted with one block scan and ONE global atomic per
-// block-chunk (a per-warp atomic on the shared tail serialises at the L2).
-constexpr int kUpdBlock = 256;
-constexpr int kUpdItems = 8;
-
-__global__ void __launch_bounds__(kUpdBlock)
-    k_update(int32_t n, uint64_t *__restrict__ key, uint8_t *__restrict__ state,
-             uint8_t *__restrict__ next, Ctrl *__restrict__ ctrl, int32_t *__restrict__ wl0,
-             int32_t *__restrict__ wl1, uint8_t *__restrict__ segflag,
-             const int32_t *__restrict__ rowtiles, int32_t nseg, int64_t total_tiles,
-             int seg_mode, DevRound *__restrict__ rounds, int fresh, uint64_t seed,
-             cudaGraphConditionalHandle cond, int use_cond) {
-  using BlockScan = cub::BlockScan<int, kUpdBlock>;
-  __shared__ typename BlockScan::TempStorage scan_tmp;
-  __shared__ int s_base;
-  const int round = ctrl->round;
-  const int64_t cnt = round == 1 ? n : ctrl->wl_count[round & 1];
-  const int32_t *in = (round & 1) ? wl1 : wl0;
-  int32_t *out = (round & 1) ? wl0 : wl1;
-  const int out_slot = (round + 1) & 1;
-  const uint64_t fresh_m = fresh ? mix64(combine_seed(seed, (uint64_t)round + 1)) : 0;
-  unsigned long long sel = 0, rem = 0, ev = 0;
-  constexpr int64_t kChunk = (int64_t)kUpdBlock * kUpdItems;
-  for (int64_t base = (int64_t)blockIdx.x * kChunk; base < cnt; base += (int64_t)gridDim.x * kChunk) {
-    // striped: item j of thread t is base + j*kUpdBlock + t, so every load and
-    // store instruction of the warp is coalesced on the identity worklist
-    int32_t vs[kUpdItems];
-    uint8_t ds[kUpdItems];
-#pragma unroll
-    for (int j = 0; j < kUpdItems; ++j) {
-      const int64_t i = base + (int64_t)j * kUpdBlock + threadIdx.x;
-      vs[j] = i < cnt ? (round == 1 ? (int32_t)i : in[i]) : -1;
-    }
-#pragma unroll
-    for (int j = 0; j < kUpdItems; ++j) ds[j] = vs[j] >= 0 ? next[vs[j]] : 0;
-    int mine = 0;
-#pragma unroll
-    for (int j = 0; j < kUpdItems; ++j) {
-      const int32_t v = vs[j];
-      if (v < 0) continue;
-      const uint8_t d = ds[j];
-      if (d == 1) {  // engine.cpp:137-143: candidate joins the MIS
-        state[v] = TCMIS_IN_MIS;
-        key[v] = 0;
-        next[v] = 0;
-        ++sel;
-      } else if (d == 2) {  // engine.cpp:144-147: alive with a candidate neighbour
-        state[v] = TCMIS_REMOVED;
-        key[v] = 0;
-        next[v] = 0;
-        ++rem;
-      } else {
-        ++mine;
-        if (fresh)  // engine.cpp:324-325: next round's redrawn priority
-          key[v] = ((vertex_hash_m((uint64_t)v, fresh_m) >> 32) << 32) | (uint64_t)(v + 1);
-      }
-    }
-    int pos, total;
-    BlockScan(scan_tmp).ExclusiveSum(mine, pos, total);
-    if (threadIdx.x == 0) s_base = total ? atomicAdd(&ctrl->wl_count[out_slot], total) : 0;
-    __syncthreads();
-    pos += s_base;
-#pragma unroll
-    for (int j = 0; j < kUpdItems; ++j)
-      if (vs[j] >= 0 && ds[j] == 0) out[pos++] = vs[j];
-    __syncthreads();  // scan_tmp / s_base reuse
-  }
-  if (seg_mode == 1) {  // spmv.cpp:37-46, per block column (A is symmetric)
-    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nseg;
-         b += (int64_t)gridDim.x * blockDim.x) {
-      if (segflag[b]) {
-        ev += (unsigned long long)rowtiles[b];
-        segflag[b] = 0;
-      }
-    }
-  }
-  block_add3(sel, rem, ev, ctrl);
-  __shared__ bool last;
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(&ctrl->ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    volatile Ctrl *vc = ctrl;
-    const int32_t alive = vc->wl_count[out_slot];
-    DevRound r;
-    r.sel = vc->sel;
-    r.rem = vc->rem;
-    r.alive = (unsigned long long)alive;
-    r.eval = seg_mode == 1 ? vc->eval : 0;
-    r.skip = seg_mode == 1 ? (unsigned long long)total_tiles - vc->eval : 0;
-    // a ring: the host loop drains one slot per round; the graph loop flags
-    // the (pathological, > max_rounds) case and the host re-runs step-wise
-    rounds[(round - 1) % vc->max_rounds] = r;
-    if (round > vc->max_rounds) vc->overflow = 1;
-    vc->alive = alive;
-    vc->sel = 0;
-    vc->rem = 0;
-    vc->eval = 0;
-    vc->ticket = 0;
-    vc->wl_count[round & 1] = 0;
-    vc->long_count = 0;
-    vc->round = round + 1;
-    if (use_cond) cudaGraphSetConditional(cond, alive > 0 ? 1u : 0u);
-  }
-}
 
 // h3: tile counters of the single collapsed iteration (segments that hold
 // any MIS vertex).
@@ -287,6 +168,7 @@ void free_workspace(Workspace &ws) {
   cudaFree(ws.segflag);
   cudaFree(ws.mis);
   cudaFree(ws.long_list);
+  cudaFree(ws.long_list2);
   cudaFree(ws.mis_count);
   cudaFree(ws.ctrl);
   cudaFreeHost(ws.h_ctrl);
@@ -323,6 +205,7 @@ int ensure_workspace(tcmis_graph *g) {
     cudaFree(ws.wl[1]);
     cudaFree(ws.mis);
     cudaFree(ws.long_list);
+    cudaFree(ws.long_list2);
     ws.n_cap = 0;
     if (int rc = dev_alloc(&ws.key, n)) return rc;
     if (int rc = dev_alloc(&ws.state, n)) return rc;
@@ -331,6 +214,7 @@ int ensure_workspace(tcmis_graph *g) {
     if (int rc = dev_alloc(&ws.wl[1], n)) return rc;
     if (int rc = dev_alloc(&ws.mis, n)) return rc;
     if (int rc = dev_alloc(&ws.long_list, n)) return rc;
+    if (int rc = dev_alloc(&ws.long_list2, n)) return rc;
     TCMIS_CUDA(cudaMemsetAsync(ws.next, 0, n, g->ctx->stream));
     ws.n_cap = n;
   }
@@ -354,7 +238,35 @@ int ensure_workspace(tcmis_graph *g) {
   TCMIS_CUDA(cub::DeviceSelect::If(nullptr, t, ids, ws.mis, ws.mis_count, (int64_t)n,
                                    IsInMIS{ws.state}, g->ctx->stream));
   need = std::max(need, t);
-  return ensure_cub(g, need);
+  TCMIS_CUDA(cub::DeviceSelect::If(nullptr, t, ids, ws.mis, ws.mis_count, (int64_t)n,
+                                   HasEdges{g->d_off}, g->ctx->stream));
+  need = std::max(need, t);
+  if (int rc = ensure_cub(g, need)) return rc;
+  if (!g->prepared) {
+    // once per graph: the round-1 select list (non-isolated ids, ascending)
+    // and the degree skew that picks the exclusion form
+    cudaStream_t st = g->ctx->stream;
+    if (int rc = dev_alloc(&g->d_nz, n)) return rc;
+    size_t bytes = ws.cub_bytes;
+    TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, g->d_nz, ws.mis_count,
+                                     (int64_t)g->n, HasEdges{g->d_off}, st));
+    unsigned long long *d_mx = nullptr;
+    if (int rc = dev_alloc(&d_mx, 1)) return rc;
+    cudaMemsetAsync(d_mx, 0, 8, st);
+    k_max_degree<<<grid_for(g->ctx, g->n, 256, 8), 256, 0, st>>>(g->n, g->d_off, d_mx);
+    g->ctx->launches += 2;
+    int64_t nz = 0;
+    unsigned long long mx = 0;
+    cudaMemcpyAsync(&nz, ws.mis_count, 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&mx, d_mx, 8, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    cudaFree(d_mx);
+    if (e != cudaSuccess) return cuda_error(e, "graph preparation");
+    g->nz_count = (int32_t)nz;
+    g->max_degree = (int64_t)mx;
+    g->prepared = true;
+  }
+  return 0;
 }
 
 // ------------------------------------------------------------------ solve
@@ -367,7 +279,8 @@ double avg_degree(const tcmis_graph *g) {
 }
 
 int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
-                      uint64_t *key, uint32_t *p_out, uint8_t *state, uint8_t *next) {
+                      uint64_t *key, uint32_t *p_out, uint8_t *state, uint8_t *next,
+                      uint8_t *segflag = nullptr, int T = 1) {
   tcmis_ctx *ctx = g->ctx;
   int mode = 1;
   uint64_t mseed = mix64(seed);
@@ -381,7 +294,7 @@ int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bi
   const int grid = grid_for(ctx, g->n, 256, 16);
   k_priorities<<<grid, 256, 0, ctx->stream>>>(g->n, g->d_off, mode, mseed,
                                                mode ? avg_degree(g) : 0.0, scale, key, p_out,
-                                               state, next);
+                                               state, next, segflag, T);
   TCMIS_LAUNCHED(ctx);
   return 0;
 }
@@ -415,6 +328,9 @@ struct RoundArgs {
   const int32_t *rowtiles;
   uint64_t seed;
   int sel_grid, upd_grid;
+  int pull;             // exclusion form: 0 push (in k_select), 1 pull (in k_update_pull)
+  int32_t nz_count;     // round-1 select list
+  const int32_t *nz;
   bool operator==(const RoundArgs &o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
 
@@ -422,10 +338,12 @@ int launch_select(tcmis_graph *g, const RoundArgs &a) {
   Workspace &ws = g->ws;
   cudaStream_t st = g->ctx->stream;
   uint8_t *seg = a.seg_mode ? ws.segflag : nullptr;
-  k_select<<<a.sel_grid, kSelBlock, 0, st>>>(a.n, a.off, a.nbr, ws.key, ws.next, seg, a.T, 1,
-                                             ws.ctrl, ws.wl[0], ws.wl[1], ws.long_list);
+  const int push = a.pull ? 0 : 1;
+  k_select<<<a.sel_grid, kSelBlock, 0, st>>>(a.nz_count, a.nz, a.off, a.nbr, ws.key, ws.next,
+                                             seg, a.T, push, ws.ctrl, ws.wl[0], ws.wl[1],
+                                             ws.long_list);
   TCMIS_LAUNCHED(g->ctx);
-  k_select_long<<<a.sel_grid, kSelBlock, 0, st>>>(a.off, a.nbr, ws.key, ws.next, seg, a.T, 1,
+  k_select_long<<<a.sel_grid, kSelBlock, 0, st>>>(a.off, a.nbr, ws.key, ws.next, seg, a.T, push,
                                                   ws.ctrl, ws.long_list);
   TCMIS_LAUNCHED(g->ctx);
   return 0;
@@ -434,12 +352,25 @@ int launch_select(tcmis_graph *g, const RoundArgs &a) {
 int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle cond,
                   int use_cond) {
   Workspace &ws = g->ws;
-  k_update<<<a.upd_grid, kUpdBlock, 0, g->ctx->stream>>>(
-      a.n, ws.key, ws.state, ws.next, ws.ctrl, ws.wl[0], ws.wl[1], ws.segflag, a.rowtiles,
-      a.nseg, a.total_tiles, a.seg_mode, ws.rounds, a.fresh, a.seed, cond, use_cond);
+  cudaStream_t st = g->ctx->stream;
+  if (a.pull) {
+    k_update_pull<<<a.sel_grid, kSelBlock, 0, st>>>(a.n, a.off, a.nbr, ws.key, ws.state,
+                                                     ws.next, ws.ctrl, ws.wl[0], ws.wl[1],
+                                                     a.fresh, a.seed, ws.long_list2);
+  } else {
+    k_update<<<a.upd_grid, kUpdBlock, 0, st>>>(a.n, ws.key, ws.state, ws.next, ws.ctrl,
+                                               ws.wl[0], ws.wl[1], a.fresh, a.seed);
+  }
+  TCMIS_LAUNCHED(g->ctx);
+  k_round_end<<<a.upd_grid, kSelBlock, 0, st>>>(
+      a.off, a.nbr, ws.key, ws.state, ws.next, ws.ctrl, ws.wl[0], ws.wl[1], a.fresh, a.seed,
+      ws.long_list2, ws.segflag, a.rowtiles, a.nseg, a.total_tiles, a.seg_mode, ws.rounds, cond,
+      use_cond);
   TCMIS_LAUNCHED(g->ctx);
   return 0;
 }
+
+constexpr int kLaunchesPerRound = 4;
 
 // Instantiate (once per distinct argument set) the graph
 //   WHILE(cond) { k_select ; k_update }
@@ -477,7 +408,7 @@ int ensure_round_graph(tcmis_graph *g, const RoundArgs &a) {
     if (e != cudaSuccess) rc = cuda_error(e, "cudaGraphInstantiate");
   }
   cudaGraphDestroy(graph);
-  g->ctx->launches -= 3;  // capture is not execution
+  g->ctx->launches -= kLaunchesPerRound;  // capture is not execution
   if (!rc) std::memcpy(ws.graph_key, &a, sizeof(a));
   return rc;
 }
@@ -502,8 +433,10 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   const int seg_mode = !tiled ? 0 : (H == TCMIS_H3 ? 2 : 1);
   const bool timing = (cfg->flags & TCMIS_F_TIMING) != 0;
 
+  if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
+  uint8_t *seg0 = seg_mode ? ws.segflag : nullptr;
   if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.key, nullptr, ws.state,
-                                 ws.next))
+                                 ws.next, seg0, T > 0 ? T : 1))
     return rc;
   Ctrl c0{};
   c0.round = 1;
@@ -511,9 +444,9 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   c0.max_rounds = ws.round_cap;
   *ws.h_ctrl = c0;
   TCMIS_CUDA(cudaMemcpyAsync(ws.ctrl, ws.h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
-  if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
 
   RoundArgs a;
+  std::memset(&a, 0, sizeof(a));
   a.n = g->n;
   a.off = g->d_off;
   a.nbr = g->d_nbr;
@@ -526,6 +459,14 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   a.seed = cfg->seed;
   a.sel_grid = ctx->num_sms * 8;
   a.upd_grid = ctx->num_sms * 4;
+  a.nz = g->d_nz;
+  a.nz_count = g->nz_count;
+  // exclusion form: pull on degree-skewed graphs, where the
+  // neighbours of candidates concentrate on hubs and early-exit pulls are
+  // cheap; push elsewhere.  Both produce the same next[] decisions.
+  if (cfg->exclusion == TCMIS_EXCL_PUSH) a.pull = 0;
+  else if (cfg->exclusion == TCMIS_EXCL_CSR_PULL) a.pull = 1;
+  else a.pull = (double)g->max_degree > 64.0 * std::max(1.0, avg_degree(g)) ? 1 : 0;
 
   std::vector<DevRound> rounds_h;
   std::vector<uint8_t> h_next, h_state, h_cand;
@@ -537,22 +478,22 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     // condition (alive > 0), so no host round trip happens between rounds.
     if (int rc = ensure_round_graph(g, a)) return rc;
     TCMIS_CUDA(cudaGraphLaunch(ws.exec, st));
-    ctx->launches += 3;  // per round, counted below
+    ctx->launches += kLaunchesPerRound;  // per round, counted below
     TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
     TCMIS_CUDA(cudaStreamSynchronize(st));
     if (ws.h_ctrl->overflow) {
       // more rounds than the on-device ring holds: redo step-wise, draining
       // the statistics every round (pathological inputs such as long paths)
       step = true;
+      if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
       if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.key, nullptr,
-                                     ws.state, ws.next))
+                                     ws.state, ws.next, seg0, T > 0 ? T : 1))
         return rc;
       *ws.h_ctrl = c0;
       TCMIS_CUDA(cudaMemcpyAsync(ws.ctrl, ws.h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
-      if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
     } else {
       const int rr = ws.h_ctrl->round - 1;
-      ctx->launches += 3 * (int64_t)rr - 3;
+      ctx->launches += kLaunchesPerRound * ((int64_t)rr - 1);
       rounds_h.resize(rr);
       TCMIS_CUDA(cudaMemcpyAsync(rounds_h.data(), ws.rounds, sizeof(DevRound) * rr,
                                  cudaMemcpyDeviceToHost, st));

@@ -322,3 +322,20 @@ def test_rmat22_properties(ctx):
     np.logical_or.at(covered, h.neighbors, member[src])
     assert covered.all()                                            # maximal
     assert np.all(np.diff(res.mis) > 0)                             # ascending ids
+
+
+@pytest.mark.parametrize("kind,args", GRAPHS + [("rmat", (14, 16, 2))])
+@pytest.mark.parametrize("excl", ["push", "pull"])
+@pytest.mark.parametrize("heur", ["h1", "h2", "h3", "luby-fresh"])
+def test_exclusion_forms_bit_exact(ctx, kind, args, excl, heur):
+    """Both Phase-2 forms (candidates push / non-candidates pull) reproduce the
+    reference's rounds exactly."""
+    g = O.gen(kind, *args)
+    dg = tc.DeviceGraph.upload(as_tc(g), ctx)
+    mode = tc.Exclusion.PUSH if excl == "push" else tc.Exclusion.CSR_PULL
+    exp = O.solve(g, heur, 3, tile_dim=16)
+    for host_loop in (False, True):
+        got = tc.run_mis(dg, tc.EngineConfig(heuristic=HEUR[heur], seed=3, tile_dim=16,
+                                             exclusion=mode, host_loop=host_loop))
+        assert np.array_equal(got.mis, exp.mis)
+        assert rounds_tuple(got.iterations) == oracle_tuple(exp)
