@@ -1,0 +1,126 @@
+// common.cuh -- device helpers shared by the round kernels.
+#pragma once
+
+#include "internal.cuh"
+
+namespace tcmis_b200 {
+
+constexpr int kBlock = 256;    // threads per block of the round kernels
+constexpr int kStep = 4;       // row entries per thread-level step
+constexpr int kThreadMax = 32; // entries a thread examines before handing a row to a warp
+
+// per-thread work modes of the state-machine kernels
+enum : int { kFetch = 0, kScan = 1, kPush = 2, kDone = 3 };
+
+// Block-wide sum of three counters into the control block.
+__device__ __forceinline__ void block_add3(unsigned long long a, unsigned long long b,
+                                           unsigned long long c, Ctrl *ctrl) {
+  __shared__ unsigned long long sh[3][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+    c += __shfl_down_sync(0xffffffffu, c, o);
+  }
+  if (lane == 0) {
+    sh[0][w] = a;
+    sh[1][w] = b;
+    sh[2][w] = c;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    a = lane < nw ? sh[0][lane] : 0;
+    b = lane < nw ? sh[1][lane] : 0;
+    c = lane < nw ? sh[2][lane] : 0;
+    for (int o = 16; o; o >>= 1) {
+      a += __shfl_down_sync(0xffffffffu, a, o);
+      b += __shfl_down_sync(0xffffffffu, b, o);
+      c += __shfl_down_sync(0xffffffffu, c, o);
+    }
+    if (lane == 0) {
+      if (a) atomicAdd(&ctrl->sel, a);
+      if (b) atomicAdd(&ctrl->rem, b);
+      if (c) atomicAdd(&ctrl->eval, c);
+    }
+  }
+  __syncthreads();  // sh reuse by a later call
+}
+
+// A candidate joins the MIS (engine.cpp:137-143).  Its key is left in place:
+// every neighbour of a candidate leaves in the same round, so no alive vertex
+// ever reads it again.  next[v] = 1 is what neighbours test this round (and
+// it is never cleared: see update.cuh).
+__device__ __forceinline__ void mark_candidate(int32_t v, uint8_t *next, uint8_t *state,
+                                               uint8_t *segflag, int T) {
+  next[v] = 1;
+  state[v] = TCMIS_IN_MIS;
+  if (segflag) segflag[v / T] = 1;
+}
+
+// An alive non-candidate with a candidate neighbour is removed
+// (engine.cpp:144-147); key 0 == kNoNeighborKey makes it invisible to the
+// alive vertices that still neighbour it.
+__device__ __forceinline__ void mark_removed(int32_t v, uint8_t *state, uint64_t *key) {
+  state[v] = TCMIS_REMOVED;
+  key[v] = 0;
+}
+
+__device__ __forceinline__ uint64_t fresh_key(int32_t v, uint64_t fresh_m) {
+  // engine.cpp:324-325: next round's redrawn h1 priority
+  return ((vertex_hash_m((uint64_t)v, fresh_m) >> 32) << 32) | (uint64_t)(v + 1);
+}
+
+// Per-warp output buffer in shared memory (64 entries), flushed 32 at a time
+// with one atomic on the list tail: lanes of the state-machine kernels emit
+// at different loop iterations, so a warp-aggregated atomic per emission
+// would serialise on the tail.
+struct WarpOut {
+  int32_t *buf;
+  int fill;  // warp-uniform
+};
+
+__device__ __forceinline__ void warp_emit(WarpOut &w, bool have, int32_t v, int32_t *out,
+                                          int *tail) {
+  const int lane = threadIdx.x & 31;
+  const unsigned m = __ballot_sync(0xffffffffu, have);
+  if (!m) return;
+  if (have) w.buf[w.fill + __popc(m & ((1u << lane) - 1u))] = v;
+  w.fill += __popc(m);
+  __syncwarp();
+  if (w.fill >= 32) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(tail, 32);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    out[base + lane] = w.buf[lane];
+    __syncwarp();
+    if (lane < w.fill - 32) w.buf[lane] = w.buf[lane + 32];
+    __syncwarp();
+    w.fill -= 32;
+  }
+}
+
+__device__ __forceinline__ void warp_flush(WarpOut &w, int32_t *out, int *tail) {
+  const int lane = threadIdx.x & 31;
+  if (w.fill == 0) return;
+  int base = 0;
+  if (lane == 0) base = atomicAdd(tail, w.fill);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (lane < w.fill) out[base + lane] = w.buf[lane];
+  __syncwarp();
+  w.fill = 0;
+}
+
+// warp-aggregated append of a rare item (one atomic per warp per call)
+__device__ __forceinline__ void warp_append(bool have, int32_t v, int32_t *out, int *tail) {
+  const int lane = threadIdx.x & 31;
+  const unsigned m = __ballot_sync(0xffffffffu, have);
+  if (!m) return;
+  const int leader = __ffs(m) - 1;
+  int pos = 0;
+  if (lane == leader) pos = atomicAdd(tail, __popc(m));
+  pos = __shfl_sync(0xffffffffu, pos, leader);
+  if (have) out[pos + __popc(m & ((1u << lane) - 1u))] = v;
+}
+
+}  // namespace tcmis_b200

@@ -54,7 +54,7 @@ struct Ctrl {
   int32_t overflow;    // set when rounds exceeded max_rounds
   int32_t long_count;  // entries of the select long-row list this round
   int32_t pull_count;  // entries of the pull long-row list this round
-  int32_t pad2;
+  int32_t check_count; // pull: non-candidates emitted by the select kernels
 };
 
 struct Workspace {
@@ -68,6 +68,7 @@ struct Workspace {
   int32_t *mis = nullptr;
   int32_t *long_list = nullptr;   // select: rows that outlived the thread probe
   int32_t *long_list2 = nullptr;  // pull exclusion: same, for k_round_end
+  int32_t *check = nullptr;       // pull exclusion: this round's non-candidates
   int64_t *mis_count = nullptr;
   Ctrl *ctrl = nullptr;        // device
   Ctrl *h_ctrl = nullptr;      // pinned host mirror

@@ -10,132 +10,79 @@
 // adjacency entries must be examined (scanning each row from its end: the
 // high ids there are the low-degree, high-priority vertices), and 99.9 % of
 // the vertices are settled within their last 32 entries.  The kernel is
-// therefore bound by memory latency and L1 wavefronts of random key gathers,
-// not by HBM bytes.  Layout of the work:
+// bound by memory latency and L1 wavefronts of the random key gathers, not by
+// HBM bytes.  Layout of the work:
 //
-//  k_select       one thread per worklist vertex (coalesced offsets, the next
-//                 vertex's row extent prefetched while the current one is
-//                 scanned), probing the last kProbe entries, then kStep-entry
-//                 chunks up to kThreadMax entries, independent loads per
-//                 chunk.  A decided candidate with a short row pushes
-//                 "excluded" to its neighbours itself.  A vertex still
-//                 undecided after kThreadMax entries goes to a global list.
-//  k_select_long  one warp per long-list vertex over the whole grid: 128
-//                 entries per step (4 independent loads per lane), early exit,
-//                 and the push of long candidates.
+//  k_select       one thread per worklist vertex, as a per-thread state
+//                 machine: every loop iteration each lane does ONE unit --
+//                 probe the next kStep entries of its row (from the end), or
+//                 push to kStep neighbours, or fetch its next vertex -- so a
+//                 lane never idles behind the slowest vertex of its warp.  A
+//                 vertex unsettled after kThreadMax entries goes to a global
+//                 list for k_select_long.
+//  k_select_long  one warp per listed vertex over the whole grid: 128 entries
+//                 per step (4 independent loads per lane), early exit.
 //
-// Push stores are filtered through L1 (`ld.ca` of next[u] first): on R-MAT
-// the neighbours of candidates concentrate on hubs -- one 128-byte line of
-// next[] receives 139k of the 7.1M round-1 stores at s22 -- and unfiltered
-// same-line stores serialise at one L2 slice.
+// Outputs: candidates get next = 1 and state = InMIS; in push mode their
+// neighbours get next = 2; in pull mode the non-candidates are emitted to the
+// check list that k_update_pull scans (update.cuh).
 #pragma once
 
-#include "internal.cuh"
+#include "common.cuh"
 
 namespace tcmis_b200 {
-
-constexpr int kSelBlock = 256;
-constexpr int kStep = 4;
-constexpr int kThreadMax = 32;
-
-__device__ __forceinline__ void mark_candidate(int32_t v, uint8_t *next, uint8_t *segflag, int T) {
-  next[v] = 1;
-  if (segflag) segflag[v / T] = 1;
-}
-
-// push: every neighbour of a candidate is excluded this round (spmv.cpp:18-59
-// nc > 0, engine.cpp:144-147).  Neighbours of a candidate are never
-// candidates, so next[u] is 0 or 2 and the filtered store is idempotent.
-#ifndef TCMIS_PUSH_FILTER
-#define TCMIS_PUSH_FILTER 2  // 0 none, 1 ld.ca of next[u], 2 per-block shared-memory tag table
-#endif
-#ifndef TCMIS_FILTER_LOG
-#define TCMIS_FILTER_LOG 11
-#endif
-constexpr int kFilterLog = TCMIS_FILTER_LOG;
-constexpr int kFilterSlots = 1 << kFilterLog;
-
-struct PushFilter {
-  int32_t *tags;  // shared memory, kFilterSlots entries, -1 = empty
-};
-
-__device__ __forceinline__ void exclude(uint8_t *__restrict__ next, int32_t u, PushFilter f) {
-#if TCMIS_PUSH_FILTER == 1
-  if (__ldca(&next[u]) != 2) next[u] = 2;
-#elif TCMIS_PUSH_FILTER == 2
-  // hub neighbours are pushed by thousands of candidates; a per-block
-  // direct-mapped table of recent targets removes the repeats (a miss or a
-  // racing duplicate only costs one redundant, idempotent store)
-  // hashed: R-MAT hubs are ids with many zero low bits and would all
-  // collide in a table indexed by the low bits
-  int32_t *slot = &f.tags[((uint32_t)u * 2654435761u) >> (32 - kFilterLog)];
-  if (*slot != u) {
-    *slot = u;
-    next[u] = 2;
-  }
-#else
-  next[u] = 2;
-#endif
-}
-
-__device__ __forceinline__ void push_row_thread(const int32_t *__restrict__ nbr, int64_t s,
-                                                int64_t e, uint8_t *__restrict__ next,
-                                                PushFilter f) {
-  for (int64_t p = s; p < e; p += kStep) {
-    int32_t u[kStep];
-#pragma unroll
-    for (int j = 0; j < kStep; ++j) u[j] = p + j < e ? __ldg(&nbr[p + j]) : -1;
-#pragma unroll
-    for (int j = 0; j < kStep; ++j)
-      if (u[j] >= 0) exclude(next, u[j], f);
-  }
-}
 
 #ifndef TCMIS_SEL_MINB
 #define TCMIS_SEL_MINB 8
 #endif
 
-// Per-thread state machine: every loop iteration each lane does ONE unit of
-// work -- fetch a vertex and probe the last kStep entries of its row, probe
-// the next kStep entries, or push to kStep neighbours -- so lanes never wait
-// for the slowest vertex of their warp (the SIMT lockstep of a plain
-// per-vertex loop cost ~4x at R-MAT s22, where a few candidates per warp have
-// 20-50-entry rows to scan and push).
-enum : int { kFetch = 0, kScan = 1, kPush = 2, kDone = 3 };
+struct SelectArgs {
+  int32_t n1;              // round-1 list length (non-isolated vertices)
+  const int32_t *nz;       // round-1 list
+  const int64_t *off;
+  const int32_t *nbr;
+  const uint64_t *key;
+  uint8_t *next;
+  uint8_t *state;
+  uint8_t *segflag;        // null: no tile counters
+  int T;
+  int push;                // 1: push exclusion, 0: emit non-candidates for pull
+  Ctrl *ctrl;
+  const int32_t *wl0, *wl1;
+  int32_t *long_list;      // rows outliving the thread probe (ctrl->long_count)
+  int32_t *check;          // pull mode: non-candidates (ctrl->check_count)
+};
 
-__global__ void __launch_bounds__(kSelBlock, TCMIS_SEL_MINB)
-    k_select(int32_t n1, const int32_t *__restrict__ nz, const int64_t *__restrict__ off,
-             const int32_t *__restrict__ nbr,
-             const uint64_t *__restrict__ key, uint8_t *__restrict__ next,
-             uint8_t *__restrict__ segflag, int T, int push, Ctrl *__restrict__ ctrl,
-             const int32_t *__restrict__ wl0, const int32_t *__restrict__ wl1,
-             int32_t *__restrict__ long_list) {
+// push: every neighbour of a candidate is excluded this round (spmv.cpp:18-59
+// nc > 0, engine.cpp:144-147).  Neighbours of a candidate are never
+// candidates, so the store is idempotent.
+__device__ __forceinline__ void exclude(uint8_t *__restrict__ next, int32_t u) { next[u] = 2; }
+
+__global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a) {
+  __shared__ int32_t s_out[kBlock / 32][64];
+  Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
-  // round 1 visits only the non-isolated vertices (k_priorities already
-  // marked the isolated ones as candidates)
-  const int64_t cnt = round == 1 ? n1 : ctrl->wl_count[round & 1];
-  const int32_t *wl = round == 1 ? nz : ((round & 1) ? wl1 : wl0);
-  const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * kSelBlock;
-  __shared__ int32_t s_tags[TCMIS_PUSH_FILTER == 2 ? kFilterSlots : 1];
-  PushFilter f{s_tags};
-  if (TCMIS_PUSH_FILTER == 2) {
-    for (int t = threadIdx.x; t < kFilterSlots; t += kSelBlock) s_tags[t] = -1;
-    __syncthreads();
-  }
-  int64_t i = (int64_t)blockIdx.x * kSelBlock + threadIdx.x - stride;
+  // round 1 visits only the non-isolated vertices (k_priorities already made
+  // the isolated ones candidates)
+  const int64_t cnt = round == 1 ? a.n1 : ctrl->wl_count[round & 1];
+  if ((int64_t)blockIdx.x * kBlock >= cnt) return;
+  const int32_t *wl = round == 1 ? a.nz : ((round & 1) ? a.wl1 : a.wl0);
+  const int32_t *__restrict__ nbr = a.nbr;
+  const uint64_t *__restrict__ key = a.key;
+  const int64_t stride = (int64_t)gridDim.x * kBlock;
+  WarpOut wo{s_out[threadIdx.x >> 5], 0};
+  unsigned long long sel = 0;
+  int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x - stride;
   int mode = kFetch;
   int32_t v = 0;
   int64_t s = 0, e = 0, hi = 0;
   uint64_t kv = 0;
-  // fetch: the next vertex of this thread's strided sequence; issued at the
-  // end of an iteration so its loads overlap the loop back-edge
   auto fetch = [&]() {
     i += stride;
     if (i < cnt) {
       v = __ldg(&wl[i]);
-      s = __ldg(&off[v]);
-      e = __ldg(&off[v + 1]);
+      s = __ldg(&a.off[v]);
+      e = __ldg(&a.off[v + 1]);
       kv = __ldg(&key[v]);
       hi = e;
       mode = kScan;
@@ -145,7 +92,7 @@ __global__ void __launch_bounds__(kSelBlock, TCMIS_SEL_MINB)
   };
   fetch();
   while (__any_sync(0xffffffffu, mode != kDone)) {
-    bool defer = false;
+    bool defer = false, noncand = false;
     if (mode == kScan) {
       int32_t u[kStep];
 #pragma unroll
@@ -156,16 +103,18 @@ __global__ void __launch_bounds__(kSelBlock, TCMIS_SEL_MINB)
         if (u[j] >= 0) blocked |= __ldg(&key[u[j]]) > kv;
       hi -= kStep;
       if (blocked) {
+        noncand = !a.push;
         mode = kFetch;
       } else if (hi <= s) {
-        mark_candidate(v, next, segflag, T);
-        if (push && e - s <= kStep) {  // the whole row is still in registers
+        mark_candidate(v, a.next, a.state, a.segflag, a.T);
+        ++sel;
+        if (a.push && e - s <= kStep) {  // the whole row is still in registers
 #pragma unroll
           for (int j = 0; j < kStep; ++j)
-            if (u[j] >= 0) exclude(next, u[j], f);
+            if (u[j] >= 0) exclude(a.next, u[j]);
           mode = kFetch;
         } else {
-          mode = push ? kPush : kFetch;
+          mode = a.push ? kPush : kFetch;
           hi = s;  // push cursor runs upward from s
         }
       } else if (e - hi >= kThreadMax) {
@@ -178,41 +127,30 @@ __global__ void __launch_bounds__(kSelBlock, TCMIS_SEL_MINB)
       for (int j = 0; j < kStep; ++j) u[j] = hi + j < e ? __ldg(&nbr[hi + j]) : -1;
 #pragma unroll
       for (int j = 0; j < kStep; ++j)
-        if (u[j] >= 0) exclude(next, u[j], f);
+        if (u[j] >= 0) exclude(a.next, u[j]);
       hi += kStep;
       if (hi >= e) mode = kFetch;
     }
-    const unsigned m = __ballot_sync(0xffffffffu, defer);
-    if (m) {
-      const int leader = __ffs(m) - 1;
-      int pos = 0;
-      if (lane == leader) pos = atomicAdd(&ctrl->long_count, __popc(m));
-      pos = __shfl_sync(0xffffffffu, pos, leader);
-      if (defer) long_list[pos + __popc(m & ((1u << lane) - 1u))] = v;
-    }
+    if (!a.push) warp_emit(wo, noncand, v, a.check, &ctrl->check_count);
+    warp_append(defer, v, a.long_list, &ctrl->long_count);
     if (mode == kFetch) fetch();
   }
+  if (!a.push) warp_flush(wo, a.check, &ctrl->check_count);
+  block_add3(sel, 0, 0, ctrl);
 }
 
-__global__ void __launch_bounds__(kSelBlock)
-    k_select_long(const int64_t *__restrict__ off, const int32_t *__restrict__ nbr,
-                  const uint64_t *__restrict__ key, uint8_t *__restrict__ next,
-                  uint8_t *__restrict__ segflag, int T, int push, Ctrl *__restrict__ ctrl,
-                  const int32_t *__restrict__ long_list) {
-  const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
+  Ctrl *ctrl = a.ctrl;
   const int cnt = ctrl->long_count;
-  if (cnt == 0) return;
-  __shared__ int32_t s_tags[TCMIS_PUSH_FILTER == 2 ? kFilterSlots : 1];
-  PushFilter f{s_tags};
-  if (TCMIS_PUSH_FILTER == 2) {
-    for (int t = threadIdx.x; t < kFilterSlots; t += kSelBlock) s_tags[t] = -1;
-    __syncthreads();
-  }
-
-  for (int64_t q = ((int64_t)blockIdx.x * kSelBlock + threadIdx.x) >> 5; q < cnt;
-       q += ((int64_t)gridDim.x * kSelBlock) >> 5) {
-    const int32_t v = long_list[q];
-    const int64_t s = __ldg(&off[v]), e = __ldg(&off[v + 1]);
+  if ((int64_t)blockIdx.x * (kBlock / 32) >= cnt) return;
+  const int lane = threadIdx.x & 31;
+  const int32_t *__restrict__ nbr = a.nbr;
+  const uint64_t *__restrict__ key = a.key;
+  unsigned long long sel = 0;
+  for (int64_t q = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5; q < cnt;
+       q += ((int64_t)gridDim.x * kBlock) >> 5) {
+    const int32_t v = a.long_list[q];
+    const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
     const uint64_t kv = __ldg(&key[v]);
     int64_t hi = e - kThreadMax;
     bool blocked = false;
@@ -231,11 +169,17 @@ __global__ void __launch_bounds__(kSelBlock)
       hi -= 128;
     }
     if (!blocked) {
-      if (lane == 0) mark_candidate(v, next, segflag, T);
-      if (push)
-        for (int64_t idx = s + lane; idx < e; idx += 32) exclude(next, __ldg(&nbr[idx]), f);
+      if (lane == 0) {
+        mark_candidate(v, a.next, a.state, a.segflag, a.T);
+        ++sel;
+      }
+      if (a.push)
+        for (int64_t idx = s + lane; idx < e; idx += 32) exclude(a.next, __ldg(&nbr[idx]));
+    } else if (!a.push && lane == 0) {
+      a.check[atomicAdd(&ctrl->check_count, 1)] = v;
     }
   }
+  block_add3(sel, 0, 0, ctrl);
 }
 
 }  // namespace tcmis_b200

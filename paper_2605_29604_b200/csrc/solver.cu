@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "common.cuh"
 #include "select.cuh"
 #include "update.cuh"
 
@@ -61,7 +62,7 @@ __global__ void k_priorities(int32_t n, const int64_t *__restrict__ off, int mod
     }
     if (p_out) p_out[v] = p;
     if (key) key[v] = ((uint64_t)p << 32) | (uint64_t)(v + 1);
-    if (state) state[v] = TCMIS_ALIVE;
+    if (state) state[v] = (next && deg == 0) ? TCMIS_IN_MIS : TCMIS_ALIVE;
     if (next) {
       // an isolated vertex has no alive neighbour: it is a round-1 candidate
       // (engine.cpp:94-99 leaves max_np at kNoNeighborKey) and round 1's
@@ -169,6 +170,7 @@ void free_workspace(Workspace &ws) {
   cudaFree(ws.mis);
   cudaFree(ws.long_list);
   cudaFree(ws.long_list2);
+  cudaFree(ws.check);
   cudaFree(ws.mis_count);
   cudaFree(ws.ctrl);
   cudaFreeHost(ws.h_ctrl);
@@ -206,6 +208,7 @@ int ensure_workspace(tcmis_graph *g) {
     cudaFree(ws.mis);
     cudaFree(ws.long_list);
     cudaFree(ws.long_list2);
+    cudaFree(ws.check);
     ws.n_cap = 0;
     if (int rc = dev_alloc(&ws.key, n)) return rc;
     if (int rc = dev_alloc(&ws.state, n)) return rc;
@@ -215,6 +218,7 @@ int ensure_workspace(tcmis_graph *g) {
     if (int rc = dev_alloc(&ws.mis, n)) return rc;
     if (int rc = dev_alloc(&ws.long_list, n)) return rc;
     if (int rc = dev_alloc(&ws.long_list2, n)) return rc;
+    if (int rc = dev_alloc(&ws.check, n)) return rc;
     TCMIS_CUDA(cudaMemsetAsync(ws.next, 0, n, g->ctx->stream));
     ws.n_cap = n;
   }
@@ -334,38 +338,70 @@ struct RoundArgs {
   bool operator==(const RoundArgs &o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
 
-int launch_select(tcmis_graph *g, const RoundArgs &a) {
+SelectArgs select_args(tcmis_graph *g, const RoundArgs &a) {
   Workspace &ws = g->ws;
+  SelectArgs s;
+  s.n1 = a.nz_count;
+  s.nz = a.nz;
+  s.off = a.off;
+  s.nbr = a.nbr;
+  s.key = ws.key;
+  s.next = ws.next;
+  s.state = ws.state;
+  s.segflag = a.seg_mode ? ws.segflag : nullptr;
+  s.T = a.T;
+  s.push = a.pull ? 0 : 1;
+  s.ctrl = ws.ctrl;
+  s.wl0 = ws.wl[0];
+  s.wl1 = ws.wl[1];
+  s.long_list = ws.long_list;
+  s.check = ws.check;
+  return s;
+}
+
+UpdateArgs update_args(tcmis_graph *g, const RoundArgs &a) {
+  Workspace &ws = g->ws;
+  UpdateArgs u;
+  u.n = a.n;
+  u.off = a.off;
+  u.nbr = a.nbr;
+  u.key = ws.key;
+  u.state = ws.state;
+  u.next = ws.next;
+  u.ctrl = ws.ctrl;
+  u.wl0 = ws.wl[0];
+  u.wl1 = ws.wl[1];
+  u.fresh = a.fresh;
+  u.seed = a.seed;
+  u.check = ws.check;
+  u.long_list = ws.long_list2;
+  u.segflag = ws.segflag;
+  u.rowtiles = a.rowtiles;
+  u.nseg = a.nseg;
+  u.total_tiles = a.total_tiles;
+  u.seg_mode = a.seg_mode;
+  u.rounds = ws.rounds;
+  return u;
+}
+
+int launch_select(tcmis_graph *g, const RoundArgs &a) {
   cudaStream_t st = g->ctx->stream;
-  uint8_t *seg = a.seg_mode ? ws.segflag : nullptr;
-  const int push = a.pull ? 0 : 1;
-  k_select<<<a.sel_grid, kSelBlock, 0, st>>>(a.nz_count, a.nz, a.off, a.nbr, ws.key, ws.next,
-                                             seg, a.T, push, ws.ctrl, ws.wl[0], ws.wl[1],
-                                             ws.long_list);
+  const SelectArgs s = select_args(g, a);
+  k_select<<<a.sel_grid, kBlock, 0, st>>>(s);
   TCMIS_LAUNCHED(g->ctx);
-  k_select_long<<<a.sel_grid, kSelBlock, 0, st>>>(a.off, a.nbr, ws.key, ws.next, seg, a.T, push,
-                                                  ws.ctrl, ws.long_list);
+  k_select_long<<<a.sel_grid, kBlock, 0, st>>>(s);
   TCMIS_LAUNCHED(g->ctx);
   return 0;
 }
 
 int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle cond,
                   int use_cond) {
-  Workspace &ws = g->ws;
   cudaStream_t st = g->ctx->stream;
-  if (a.pull) {
-    k_update_pull<<<a.sel_grid, kSelBlock, 0, st>>>(a.n, a.off, a.nbr, ws.key, ws.state,
-                                                     ws.next, ws.ctrl, ws.wl[0], ws.wl[1],
-                                                     a.fresh, a.seed, ws.long_list2);
-  } else {
-    k_update<<<a.upd_grid, kUpdBlock, 0, st>>>(a.n, ws.key, ws.state, ws.next, ws.ctrl,
-                                               ws.wl[0], ws.wl[1], a.fresh, a.seed);
-  }
+  const UpdateArgs u = update_args(g, a);
+  if (a.pull) k_update_pull<<<a.sel_grid, kBlock, 0, st>>>(u);
+  else k_update<<<a.upd_grid, kBlock, 0, st>>>(u);
   TCMIS_LAUNCHED(g->ctx);
-  k_round_end<<<a.upd_grid, kSelBlock, 0, st>>>(
-      a.off, a.nbr, ws.key, ws.state, ws.next, ws.ctrl, ws.wl[0], ws.wl[1], a.fresh, a.seed,
-      ws.long_list2, ws.segflag, a.rowtiles, a.nseg, a.total_tiles, a.seg_mode, ws.rounds, cond,
-      use_cond);
+  k_round_end<<<a.upd_grid, kBlock, 0, st>>>(u, cond, use_cond);
   TCMIS_LAUNCHED(g->ctx);
   return 0;
 }
@@ -442,6 +478,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   c0.round = 1;
   c0.alive = g->n;
   c0.max_rounds = ws.round_cap;
+  c0.sel = (unsigned long long)(g->n - g->nz_count);  // isolated: round-1 candidates
   *ws.h_ctrl = c0;
   TCMIS_CUDA(cudaMemcpyAsync(ws.ctrl, ws.h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
 
@@ -509,17 +546,21 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       if (int rc = launch_select(g, a)) return rc;
       if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[1], st));
       if (cfg->observer && H != TCMIS_H3) {
+        // the select kernels already moved this round's candidates to InMIS;
+        // the hook gets the states the candidates were generated against
+        // (engine.cpp:275-278), i.e. the host copy taken after the last round
+        if (h_state.empty()) h_state.assign(g->n, TCMIS_ALIVE);
         h_next.resize(g->n);
-        h_state.resize(g->n);
         h_cand.resize(g->n);
         TCMIS_CUDA(cudaMemcpyAsync(h_next.data(), ws.next, g->n, cudaMemcpyDeviceToHost, st));
-        TCMIS_CUDA(cudaMemcpyAsync(h_state.data(), ws.state, g->n, cudaMemcpyDeviceToHost, st));
         TCMIS_CUDA(cudaStreamSynchronize(st));
         for (int32_t v = 0; v < g->n; ++v)
           h_cand[v] = h_next[v] == 1 && h_state[v] == TCMIS_ALIVE;
         cfg->observer(cfg->observer_user, round, h_cand.data(), h_state.data(), g->n);
       }
       if (int rc = launch_update(g, a, 0, 0)) return rc;
+      if (cfg->observer && H != TCMIS_H3)
+        TCMIS_CUDA(cudaMemcpyAsync(h_state.data(), ws.state, g->n, cudaMemcpyDeviceToHost, st));
       if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[2], st));
       TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
       DevRound dr;
