@@ -55,6 +55,8 @@ struct Ctrl {
   int32_t long_count;  // entries of the select long-row list this round
   int32_t pull_count;  // entries of the pull long-row list this round
   int32_t check_count; // pull: non-candidates emitted by the select kernels
+  int32_t main_rounds; // rounds run by the per-round kernels (the rest ran in k_tail)
+  int32_t pad3;
 };
 
 struct Workspace {
@@ -69,6 +71,8 @@ struct Workspace {
   int32_t *long_list = nullptr;   // select: rows that outlived the thread probe
   int32_t *long_list2 = nullptr;  // pull exclusion: same, for k_round_end
   int32_t *check = nullptr;       // pull exclusion: this round's non-candidates
+  uint32_t *segmark = nullptr;    // tail rounds: round that last counted a block column
+  unsigned *bar = nullptr;        // grid barrier of k_tail
   int64_t *mis_count = nullptr;
   Ctrl *ctrl = nullptr;        // device
   Ctrl *h_ctrl = nullptr;      // pinned host mirror
@@ -87,6 +91,7 @@ struct tcmis_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   int num_sms = 148;
+  int tail_blocks_per_sm = 0;  // co-resident k_tail blocks per SM (occupancy)
   int64_t launches = 0;
   cudaEvent_t ev[8] = {};
 };

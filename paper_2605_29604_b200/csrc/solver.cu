@@ -19,6 +19,7 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -26,6 +27,7 @@
 #include "common.cuh"
 #include "select.cuh"
 #include "update.cuh"
+#include "tail.cuh"
 
 namespace tcmis_b200 {
 
@@ -171,6 +173,8 @@ void free_workspace(Workspace &ws) {
   cudaFree(ws.long_list);
   cudaFree(ws.long_list2);
   cudaFree(ws.check);
+  cudaFree(ws.segmark);
+  cudaFree(ws.bar);
   cudaFree(ws.mis_count);
   cudaFree(ws.ctrl);
   cudaFreeHost(ws.h_ctrl);
@@ -209,6 +213,7 @@ int ensure_workspace(tcmis_graph *g) {
     cudaFree(ws.long_list);
     cudaFree(ws.long_list2);
     cudaFree(ws.check);
+    cudaFree(ws.segmark);
     ws.n_cap = 0;
     if (int rc = dev_alloc(&ws.key, n)) return rc;
     if (int rc = dev_alloc(&ws.state, n)) return rc;
@@ -219,6 +224,7 @@ int ensure_workspace(tcmis_graph *g) {
     if (int rc = dev_alloc(&ws.long_list, n)) return rc;
     if (int rc = dev_alloc(&ws.long_list2, n)) return rc;
     if (int rc = dev_alloc(&ws.check, n)) return rc;
+    if (int rc = dev_alloc(&ws.segmark, n)) return rc;
     TCMIS_CUDA(cudaMemsetAsync(ws.next, 0, n, g->ctx->stream));
     ws.n_cap = n;
   }
@@ -232,6 +238,8 @@ int ensure_workspace(tcmis_graph *g) {
   if (!ws.ctrl) {
     if (int rc = dev_alloc(&ws.ctrl, 1)) return rc;
     if (int rc = dev_alloc(&ws.mis_count, 1)) return rc;
+    if (int rc = dev_alloc(&ws.bar, 2)) return rc;
+    TCMIS_CUDA(cudaMemsetAsync(ws.bar, 0, 2 * sizeof(unsigned), g->ctx->stream));
     TCMIS_CUDA(cudaMallocHost((void **)&ws.h_ctrl, sizeof(Ctrl)));
     ws.round_cap = 4096;
     if (int rc = dev_alloc(&ws.rounds, (size_t)ws.round_cap)) return rc;
@@ -335,6 +343,8 @@ struct RoundArgs {
   int pull;             // exclusion form: 0 push (in k_select), 1 pull (in k_update_pull)
   int32_t nz_count;     // round-1 select list
   const int32_t *nz;
+  int32_t tail_thr;     // rounds start in k_tail once alive <= tail_thr
+  int tail_grid;
   bool operator==(const RoundArgs &o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
 
@@ -381,7 +391,61 @@ UpdateArgs update_args(tcmis_graph *g, const RoundArgs &a) {
   u.total_tiles = a.total_tiles;
   u.seg_mode = a.seg_mode;
   u.rounds = ws.rounds;
+  u.tail_thr = a.tail_thr;
   return u;
+}
+
+TailArgs tail_args(tcmis_graph *g, const RoundArgs &a) {
+  Workspace &ws = g->ws;
+  TailArgs t;
+  t.off = a.off;
+  t.nbr = a.nbr;
+  t.key = ws.key;
+  t.next = ws.next;
+  t.state = ws.state;
+  t.segflag = ws.segflag;
+  t.segmark = ws.segmark;
+  t.rowtiles = a.rowtiles;
+  t.nseg = a.nseg;
+  t.total_tiles = a.total_tiles;
+  t.seg_mode = a.seg_mode;
+  t.T = a.T;
+  t.push = a.pull ? 0 : 1;
+  t.fresh = a.fresh;
+  t.seed = a.seed;
+  t.ctrl = ws.ctrl;
+  t.wl0 = ws.wl[0];
+  t.wl1 = ws.wl[1];
+  t.check = ws.check;
+  t.rounds = ws.rounds;
+  t.bar = ws.bar;
+  return t;
+}
+
+// cooperative launch: the grid barriers of k_tail need every block resident
+int launch_tail(tcmis_graph *g, const RoundArgs &a) {
+  TailArgs t = tail_args(g, a);
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(a.tail_grid);
+  lc.blockDim = dim3(kTailBlock);
+  lc.stream = g->ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  TCMIS_CUDA(cudaLaunchKernelEx(&lc, k_tail, t));
+  g->ctx->launches++;
+  return 0;
+}
+
+int tail_grid(tcmis_ctx *ctx) {
+  if (ctx->tail_blocks_per_sm == 0) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail, kTailBlock, 0);
+    ctx->tail_blocks_per_sm = per_sm > 0 ? per_sm : 1;
+  }
+  return ctx->num_sms * ctx->tail_blocks_per_sm;
 }
 
 int launch_select(tcmis_graph *g, const RoundArgs &a) {
@@ -439,6 +503,15 @@ int ensure_round_graph(tcmis_graph *g, const RoundArgs &a) {
   cudaGraph_t captured = nullptr;
   cudaError_t e = cudaStreamEndCapture(st, &captured);
   if (!rc && e != cudaSuccess) rc = cuda_error(e, "cudaStreamEndCapture");
+  // then the persistent tail kernel finishes the small rounds
+  if (!rc && a.tail_thr > 0) {
+    e = cudaStreamBeginCaptureToGraph(st, graph, &node, nullptr, 1, cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) rc = cuda_error(e, "cudaStreamBeginCaptureToGraph(tail)");
+    if (!rc) rc = launch_tail(g, a);
+    e = cudaStreamEndCapture(st, &captured);
+    if (!rc && e != cudaSuccess) rc = cuda_error(e, "cudaStreamEndCapture(tail)");
+    g->ctx->launches--;
+  }
   if (!rc) {
     e = cudaGraphInstantiate(&ws.exec, graph, 0);
     if (e != cudaSuccess) rc = cuda_error(e, "cudaGraphInstantiate");
@@ -504,6 +577,16 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   if (cfg->exclusion == TCMIS_EXCL_PUSH) a.pull = 0;
   else if (cfg->exclusion == TCMIS_EXCL_CSR_PULL) a.pull = 1;
   else a.pull = (double)g->max_degree > 64.0 * std::max(1.0, avg_degree(g)) ? 1 : 0;
+  // small late rounds run in the persistent k_tail (not with the per-round
+  // observer hook, which needs every round's snapshot)
+  a.tail_thr = 0;
+  if (!cfg->observer) {
+    a.tail_thr = 1 << 16;
+    if (const char *env = std::getenv("TCMIS_TAIL_THRESHOLD")) a.tail_thr = std::atoi(env);
+    a.tail_grid = tail_grid(ctx);
+  }
+  if (seg_mode == 1 && a.tail_thr > 0)
+    TCMIS_CUDA(cudaMemsetAsync(ws.segmark, 0, sizeof(uint32_t) * (size_t)nseg, st));
 
   std::vector<DevRound> rounds_h;
   std::vector<uint8_t> h_next, h_state, h_cand;
@@ -522,6 +605,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       // more rounds than the on-device ring holds: redo step-wise, draining
       // the statistics every round (pathological inputs such as long paths)
       step = true;
+      a.tail_thr = 0;
       if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
       if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.key, nullptr,
                                      ws.state, ws.next, seg0, T > 0 ? T : 1))
@@ -530,7 +614,8 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       TCMIS_CUDA(cudaMemcpyAsync(ws.ctrl, ws.h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
     } else {
       const int rr = ws.h_ctrl->round - 1;
-      ctx->launches += kLaunchesPerRound * ((int64_t)rr - 1);
+      const int mr = ws.h_ctrl->main_rounds;
+      ctx->launches += kLaunchesPerRound * ((int64_t)mr - 1) + (rr > mr ? 1 : 0);
       rounds_h.resize(rr);
       TCMIS_CUDA(cudaMemcpyAsync(rounds_h.data(), ws.rounds, sizeof(DevRound) * rr,
                                  cudaMemcpyDeviceToHost, st));
@@ -576,6 +661,29 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
         t3.push_back(y);
       }
       if (ws.h_ctrl->alive == 0) break;
+      if (a.tail_thr > 0 && ws.h_ctrl->alive <= a.tail_thr) {
+        if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[0], st));
+        if (int rc = launch_tail(g, a)) return rc;
+        if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[1], st));
+        TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+        TCMIS_CUDA(cudaStreamSynchronize(st));
+        const int rr = ws.h_ctrl->round - 1;
+        if (rr - round > ws.round_cap)
+          return set_error(TCMIS_E_RUNTIME, "round statistics capacity exceeded in k_tail");
+        float x = 0;
+        if (timing) cudaEventElapsedTime(&x, ctx->ev[0], ctx->ev[1]);
+        for (int r = round; r < rr; ++r) {
+          DevRound dr;
+          TCMIS_CUDA(cudaMemcpy(&dr, ws.rounds + r % ws.round_cap, sizeof(DevRound),
+                                cudaMemcpyDeviceToHost));
+          rounds_h.push_back(dr);
+          if (timing) {  // the tail's rounds share one launch: report it on the first
+            t1.push_back(r == round ? x : 0.f);
+            t3.push_back(0.f);
+          }
+        }
+        break;
+      }
     }
   }
   const int rounds_run = (int)rounds_h.size();

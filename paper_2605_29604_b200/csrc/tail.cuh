@@ -1,0 +1,213 @@
+// tail.cuh -- the small late rounds of a solve in ONE persistent kernel.
+//
+// After the first one or two rounds the alive worklist is small (R-MAT s22:
+// 57k, 1.7k, 23 vertices in rounds 2-4), and four kernel launches per round
+// plus the per-thread scan latency (8 dependent steps for a 32-entry row)
+// cost ~50 us per round while the work is a few microseconds.  k_tail runs
+// all remaining rounds with grid-wide barriers instead of kernel boundaries:
+//
+//   S  select: a group of kGroup lanes per worklist vertex scans its row from
+//      the end, kGroup*4 entries per step (4 independent loads per lane), and
+//      stops at the first higher alive neighbour (engine.cpp:86-119).  A
+//      candidate is marked (next = 1, state = InMIS) and, in push mode,
+//      excludes its neighbours; in pull mode non-candidates go to the check
+//      list.
+//   U  update (engine.cpp:121-160): push mode reads next[v] of every worklist
+//      vertex; pull mode scans each check-list row for a candidate neighbour.
+//      Survivors form the next worklist.
+//   F  one thread publishes the round's IterationStats exactly like
+//      k_round_end and advances the round.
+//
+// The rounds stay bulk-synchronous (barriers between S, U and F), so round
+// count and every statistic equal the reference's.  Launched cooperatively,
+// which guarantees that all blocks are co-resident for the barriers.  Data
+// written by other blocks in an earlier phase is read with ld.global.cg (L2),
+// never through the SM's non-coherent L1.
+#pragma once
+
+#include "common.cuh"
+
+namespace tcmis_b200 {
+
+constexpr int kGroup = 8;             // lanes per vertex in the tail kernel
+constexpr int kTailBlock = 512;
+
+struct TailArgs {
+  const int64_t *off;
+  const int32_t *nbr;
+  uint64_t *key;
+  uint8_t *next;
+  uint8_t *state;
+  uint8_t *segflag;         // byte flags (seg_mode 2) -- also mode 1 sanity
+  uint32_t *segmark;        // seg_mode 1: round that last counted the segment
+  const int32_t *rowtiles;
+  int32_t nseg;
+  int64_t total_tiles;
+  int seg_mode;
+  int T;
+  int push;
+  int fresh;
+  uint64_t seed;
+  Ctrl *ctrl;
+  int32_t *wl0, *wl1;
+  int32_t *check;
+  DevRound *rounds;
+  unsigned *bar;            // [0] arrivals, [1] generation
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned *bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned *gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// the lanes of one group stay converged (same vertex, same trip count);
+// different groups of a warp may diverge, so the vote uses the group's mask
+__device__ __forceinline__ unsigned group_any(bool b, unsigned gmask) {
+  return __ballot_sync(gmask, b);
+}
+
+__global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
+  Ctrl *ctrl = a.ctrl;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (kGroup - 1);
+  const unsigned gmask = ((1u << kGroup) - 1u) << (lane & ~(kGroup - 1));
+  const int64_t gid = ((int64_t)blockIdx.x * kTailBlock + threadIdx.x) / kGroup;
+  const int64_t ngroups = ((int64_t)gridDim.x * kTailBlock) / kGroup;
+  constexpr int kW = kGroup * 4;  // entries per group step
+  for (;;) {
+    const int round = *(volatile int *)&ctrl->round;
+    const int64_t cnt = *(volatile int *)&ctrl->wl_count[round & 1];
+    if (cnt == 0) break;  // nothing alive (alive == 0 after the last round)
+    const int32_t *in = (round & 1) ? a.wl1 : a.wl0;
+    int32_t *out = (round & 1) ? a.wl0 : a.wl1;
+    int *tail = &ctrl->wl_count[(round + 1) & 1];
+    const uint64_t fresh_m = a.fresh ? mix64(combine_seed(a.seed, (uint64_t)round + 1)) : 0;
+    unsigned long long sel = 0, rem = 0, ev = 0;
+
+    // ---- S: candidate detection (+ push)
+    for (int64_t q = gid; q < cnt; q += ngroups) {
+      const int32_t v = __ldcg(&in[q]);
+      const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
+      const uint64_t kv = __ldcg(&a.key[v]);
+      bool blocked = false;
+      for (int64_t hi = e; hi > s && !blocked; hi -= kW) {
+        int32_t u[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int64_t idx = hi - 1 - gl - kGroup * j;
+          u[j] = idx >= s ? __ldg(&a.nbr[idx]) : -1;
+        }
+        bool b = false;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (u[j] >= 0) b |= __ldcg(&a.key[u[j]]) > kv;
+        blocked = group_any(b, gmask) != 0;
+      }
+      if (!blocked) {
+        if (gl == 0) {
+          a.next[v] = 1;
+          a.state[v] = TCMIS_IN_MIS;
+          ++sel;
+          const int32_t sb = v / a.T;
+          if (a.seg_mode == 2) {
+            a.segflag[sb] = 1;
+          } else if (a.seg_mode == 1) {
+            // exactly one candidate of this round counts the block column
+            if (atomicMax(&a.segmark[sb], (unsigned)round) < (unsigned)round)
+              ev += (unsigned long long)a.rowtiles[sb];
+          }
+        }
+        if (a.push)
+          for (int64_t idx = s + gl; idx < e; idx += kGroup) a.next[__ldg(&a.nbr[idx])] = 2;
+      } else if (!a.push && gl == 0) {
+        a.check[atomicAdd(&ctrl->check_count, 1)] = v;
+      }
+    }
+    grid_barrier(a.bar);
+
+    // ---- U: exclusion (pull) + state update + compaction
+    if (a.push) {
+      for (int64_t q = (int64_t)blockIdx.x * kTailBlock + threadIdx.x; q < cnt;
+           q += (int64_t)gridDim.x * kTailBlock) {
+        const int32_t v = __ldcg(&in[q]);
+        const uint8_t d = __ldcg(&a.next[v]);
+        if (d == 2) {
+          mark_removed(v, a.state, a.key);
+          ++rem;
+        } else if (d == 0) {
+          if (a.fresh) a.key[v] = fresh_key(v, fresh_m);
+          out[atomicAdd(tail, 1)] = v;
+        }
+      }
+    } else {
+      const int64_t nc = *(volatile int *)&ctrl->check_count;
+      for (int64_t q = gid; q < nc; q += ngroups) {
+        const int32_t v = __ldcg(&a.check[q]);
+        const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
+        bool hit = false;
+        for (int64_t hi = e; hi > s && !hit; hi -= kW) {
+          int32_t u[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int64_t idx = hi - 1 - gl - kGroup * j;
+            u[j] = idx >= s ? __ldg(&a.nbr[idx]) : -1;
+          }
+          bool b = false;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (u[j] >= 0) b |= __ldcg(&a.next[u[j]]) == 1;
+          hit = group_any(b, gmask) != 0;
+        }
+        if (gl == 0) {
+          if (hit) {
+            mark_removed(v, a.state, a.key);
+            ++rem;
+          } else {
+            if (a.fresh) a.key[v] = fresh_key(v, fresh_m);
+            out[atomicAdd(tail, 1)] = v;
+          }
+        }
+      }
+    }
+    block_add3(sel, rem, ev, ctrl);
+    grid_barrier(a.bar);
+
+    // ---- F: publish the round (k_round_end's epilogue)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      volatile Ctrl *vc = ctrl;
+      const int32_t alive = vc->wl_count[(round + 1) & 1];
+      DevRound r;
+      r.sel = vc->sel;
+      r.rem = vc->rem;
+      r.alive = (unsigned long long)alive;
+      r.eval = a.seg_mode == 1 ? vc->eval : 0;
+      r.skip = a.seg_mode == 1 ? (unsigned long long)a.total_tiles - vc->eval : 0;
+      a.rounds[(round - 1) % vc->max_rounds] = r;
+      if (round > vc->max_rounds) vc->overflow = 1;
+      vc->alive = alive;
+      vc->sel = 0;
+      vc->rem = 0;
+      vc->eval = 0;
+      vc->wl_count[round & 1] = 0;
+      vc->check_count = 0;
+      vc->round = round + 1;
+      __threadfence();
+    }
+    grid_barrier(a.bar);
+  }
+}
+
+}  // namespace tcmis_b200

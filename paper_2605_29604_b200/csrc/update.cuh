@@ -52,6 +52,7 @@ struct UpdateArgs {
   int64_t total_tiles;
   int seg_mode;            // 0 none, 1 count + clear per round, 2 accumulate (h3)
   DevRound *rounds;
+  int32_t tail_thr;        // the WHILE loop continues while alive > tail_thr
 };
 
 // ---------------------------------------------------------------- push
@@ -258,8 +259,9 @@ __global__ void __launch_bounds__(kBlock)
     vc->long_count = 0;
     vc->pull_count = 0;
     vc->check_count = 0;
+    vc->main_rounds = vc->main_rounds + 1;
     vc->round = round + 1;
-    if (use_cond) cudaGraphSetConditional(cond, alive > 0 ? 1u : 0u);
+    if (use_cond) cudaGraphSetConditional(cond, alive > a.tail_thr ? 1u : 0u);
   }
 }
 

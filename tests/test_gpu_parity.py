@@ -339,3 +339,21 @@ def test_exclusion_forms_bit_exact(ctx, kind, args, excl, heur):
                                              exclusion=mode, host_loop=host_loop))
         assert np.array_equal(got.mis, exp.mis)
         assert rounds_tuple(got.iterations) == oracle_tuple(exp)
+
+
+@pytest.mark.parametrize("thr", ["0", "1", "100", "1000000000"])
+def test_tail_threshold_invariance(ctx, thr, monkeypatch):
+    """The persistent tail kernel (k_tail) and the per-round kernels give the
+    same rounds; the switch point must not matter."""
+    monkeypatch.setenv("TCMIS_TAIL_THRESHOLD", thr)
+    for kind, args in (("rmat", (13, 16, 4)), ("grid", (50,)), ("gnp_avg", (4000, 12.0, 3))):
+        g = O.gen(kind, *args)
+        dg = tc.DeviceGraph.upload(as_tc(g), ctx)
+        for heur in ("h2", "h1", "h3", "luby-fresh", "luby-perm"):
+            for excl in (tc.Exclusion.PUSH, tc.Exclusion.CSR_PULL):
+                exp = O.solve(g, heur, 2, tile_dim=16)
+                for host_loop in (False, True):
+                    got = tc.run_mis(dg, tc.EngineConfig(heuristic=HEUR[heur], seed=2,
+                                                         exclusion=excl, host_loop=host_loop))
+                    assert np.array_equal(got.mis, exp.mis), (kind, heur, excl, host_loop)
+                    assert rounds_tuple(got.iterations) == oracle_tuple(exp)
