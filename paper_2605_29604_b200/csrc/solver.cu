@@ -247,10 +247,10 @@ int ensure_workspace(tcmis_graph *g) {
   }
   size_t need = 0, t = 0;
   thrust::counting_iterator<int32_t> ids(0);
-  TCMIS_CUDA(cub::DeviceSelect::If(nullptr, t, ids, ws.mis, ws.mis_count, (int64_t)n,
+  TCMIS_CUDA(cub::DeviceSelect::If(nullptr, t, ids, ws.mis, ws.mis_count, (int)n,
                                    IsInMIS{ws.state}, g->ctx->stream));
   need = std::max(need, t);
-  TCMIS_CUDA(cub::DeviceSelect::If(nullptr, t, ids, ws.mis, ws.mis_count, (int64_t)n,
+  TCMIS_CUDA(cub::DeviceSelect::If(nullptr, t, ids, ws.mis, ws.mis_count, (int)n,
                                    HasEdges{g->d_off}, g->ctx->stream));
   need = std::max(need, t);
   if (int rc = ensure_cub(g, need)) return rc;
@@ -261,7 +261,7 @@ int ensure_workspace(tcmis_graph *g) {
     if (int rc = dev_alloc(&g->d_nz, n)) return rc;
     size_t bytes = ws.cub_bytes;
     TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, g->d_nz, ws.mis_count,
-                                     (int64_t)g->n, HasEdges{g->d_off}, st));
+                                     (int)g->n, HasEdges{g->d_off}, st));
     unsigned long long *d_mx = nullptr;
     if (int rc = dev_alloc(&d_mx, 1)) return rc;
     cudaMemsetAsync(d_mx, 0, 8, st);
@@ -692,7 +692,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     thrust::counting_iterator<int32_t> ids(0);
     size_t bytes = ws.cub_bytes;
     TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
-                                     (int64_t)g->n, IsInMIS{ws.state}, st));
+                                     (int)g->n, IsInMIS{ws.state}, st));
     ctx->launches += 1;
   }
   int64_t h_mis_count = 0;

@@ -30,7 +30,7 @@
 namespace tcmis_b200 {
 
 constexpr int kGroup = 8;             // lanes per vertex in the tail kernel
-constexpr int kTailBlock = 512;
+constexpr int kTailBlock = 1024;  // one block per SM: 148 arrivals per barrier
 
 struct TailArgs {
   const int64_t *off;
@@ -87,16 +87,42 @@ __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
   const int64_t gid = ((int64_t)blockIdx.x * kTailBlock + threadIdx.x) / kGroup;
   const int64_t ngroups = ((int64_t)gridDim.x * kTailBlock) / kGroup;
   constexpr int kW = kGroup * 4;  // entries per group step
-  for (;;) {
-    const int round = *(volatile int *)&ctrl->round;
+  // Every block walks the rounds in lockstep, so the round number is local.
+  // Two barriers per round (after S, after U).  Block 0 publishes round r-1's
+  // IterationStats at the start of round r and clears the counters; nobody
+  // else touches them before the next barrier.  The pull check list is
+  // double-buffered by round parity for the same reason.
+  int round = *(volatile int *)&ctrl->round;
+  for (;; ++round) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && round > *(volatile int *)&ctrl->round) {
+      volatile Ctrl *vc = ctrl;
+      const int pr = round - 1;
+      const int32_t alive = vc->wl_count[round & 1];
+      DevRound r;
+      r.sel = vc->sel;
+      r.rem = vc->rem;
+      r.alive = (unsigned long long)alive;
+      r.eval = a.seg_mode == 1 ? vc->eval : 0;
+      r.skip = a.seg_mode == 1 ? (unsigned long long)a.total_tiles - vc->eval : 0;
+      a.rounds[(pr - 1) % vc->max_rounds] = r;
+      if (pr > vc->max_rounds) vc->overflow = 1;
+      vc->alive = alive;
+      vc->sel = 0;
+      vc->rem = 0;
+      vc->eval = 0;
+      vc->wl_count[pr & 1] = 0;       // this round's output slot (U, after a barrier)
+      vc->tail_check[pr & 1] = 0;     // next round's check list
+      vc->round = round;
+      __threadfence();
+    }
     const int64_t cnt = *(volatile int *)&ctrl->wl_count[round & 1];
     if (cnt == 0) break;  // nothing alive (alive == 0 after the last round)
+    int *check_count = &ctrl->tail_check[round & 1];
     const int32_t *in = (round & 1) ? a.wl1 : a.wl0;
     int32_t *out = (round & 1) ? a.wl0 : a.wl1;
     int *tail = &ctrl->wl_count[(round + 1) & 1];
     const uint64_t fresh_m = a.fresh ? mix64(combine_seed(a.seed, (uint64_t)round + 1)) : 0;
     unsigned long long sel = 0, rem = 0, ev = 0;
-
     // ---- S: candidate detection (+ push)
     for (int64_t q = gid; q < cnt; q += ngroups) {
       const int32_t v = __ldcg(&in[q]);
@@ -133,7 +159,7 @@ __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
         if (a.push)
           for (int64_t idx = s + gl; idx < e; idx += kGroup) a.next[__ldg(&a.nbr[idx])] = 2;
       } else if (!a.push && gl == 0) {
-        a.check[atomicAdd(&ctrl->check_count, 1)] = v;
+        a.check[atomicAdd(check_count, 1)] = v;
       }
     }
     grid_barrier(a.bar);
@@ -153,7 +179,7 @@ __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
         }
       }
     } else {
-      const int64_t nc = *(volatile int *)&ctrl->check_count;
+      const int64_t nc = *(volatile int *)check_count;
       for (int64_t q = gid; q < nc; q += ngroups) {
         const int32_t v = __ldcg(&a.check[q]);
         const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
@@ -183,29 +209,6 @@ __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
       }
     }
     block_add3(sel, rem, ev, ctrl);
-    grid_barrier(a.bar);
-
-    // ---- F: publish the round (k_round_end's epilogue)
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      volatile Ctrl *vc = ctrl;
-      const int32_t alive = vc->wl_count[(round + 1) & 1];
-      DevRound r;
-      r.sel = vc->sel;
-      r.rem = vc->rem;
-      r.alive = (unsigned long long)alive;
-      r.eval = a.seg_mode == 1 ? vc->eval : 0;
-      r.skip = a.seg_mode == 1 ? (unsigned long long)a.total_tiles - vc->eval : 0;
-      a.rounds[(round - 1) % vc->max_rounds] = r;
-      if (round > vc->max_rounds) vc->overflow = 1;
-      vc->alive = alive;
-      vc->sel = 0;
-      vc->rem = 0;
-      vc->eval = 0;
-      vc->wl_count[round & 1] = 0;
-      vc->check_count = 0;
-      vc->round = round + 1;
-      __threadfence();
-    }
     grid_barrier(a.bar);
   }
 }
