@@ -57,7 +57,8 @@ struct Ctrl {
   int32_t check_count; // pull: non-candidates emitted by the select kernels
   int32_t main_rounds; // rounds run by the per-round kernels (the rest ran in k_tail)
   int32_t tail_check[2]; // k_tail pull check-list length, by round parity
-  int32_t pad3;
+  int32_t sel_cursor;  // k_select work dispenser
+  int32_t pull_cursor; // k_update_pull work dispenser
 };
 
 struct Workspace {

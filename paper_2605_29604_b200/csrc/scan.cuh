@@ -1,0 +1,108 @@
+// scan.cuh -- the per-thread row-scan engine shared by the round kernels.
+//
+// Both Phase 1 (candidate detection: "is any neighbour key above mine?") and
+// the pull form of Phase 2 ("is any neighbour a candidate?") are an
+// early-exit search over one CSR row per worklist vertex.  Profiling the
+// first version (one scalar load per entry, one vertex fetch per lane at
+// arbitrary times) showed the kernel bound by L1 wavefronts: every
+// thread-private access of a warp touches a different 128-byte line, so each
+// scalar load costs ~32 wavefronts per warp instruction.  The engine
+// therefore
+//   * hands vertices to lanes in warp batches from a global cursor, so the
+//     worklist / offset / own-key loads of one batch are coalesced;
+//   * reads the row in 16-byte aligned windows (one LDG.128 per lane per
+//     step, 1-4 entries), newest entries first, so a step costs one
+//     wavefront per lane for the row plus one per gathered entry;
+//   * keeps every lane busy with its own vertex (no lockstep over vertices).
+// A vertex whose row is not settled within kThreadMax entries is handed to a
+// warp-wide kernel through a list.
+#pragma once
+
+#include "common.cuh"
+
+namespace tcmis_b200 {
+
+constexpr int kBatch = 64;  // worklist entries a warp claims per cursor bump
+
+// Warp-cooperative vertex dispenser over worklist[0, cnt) with a global
+// cursor; lanes that `need` a vertex get consecutive indices.
+struct Dispenser {
+  int64_t base = 0, end = 0;  // warp-uniform local range
+  __device__ __forceinline__ int64_t take(bool need, int64_t cnt, int *cursor) {
+    const int lane = threadIdx.x & 31;
+    unsigned m = __ballot_sync(0xffffffffu, need);
+    int64_t idx = -1;
+    while (m) {
+      if (base >= end) {
+        int64_t b = 0;
+        if (lane == 0) b = atomicAdd(cursor, kBatch);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if (b >= cnt) {  // nothing left for anybody
+          base = end = cnt;
+          break;
+        }
+        base = b;
+        end = b + kBatch < cnt ? b + kBatch : cnt;
+      }
+      const int avail = (int)(end - base);
+      const int want = __popc(m);
+      const int give = want < avail ? want : avail;
+      // the first `give` requesting lanes (by lane order) are served
+      const int rank = __popc(m & ((1u << lane) - 1u));
+      if (need && idx < 0 && rank < give) idx = base + rank;
+      base += give;
+      // lanes still unserved retry against a fresh batch
+      const unsigned served = __ballot_sync(0xffffffffu, need && idx >= 0);
+      m &= ~served;
+    }
+    return idx;
+  }
+};
+
+// One aligned 16-byte window of a row, read downward: entries
+// [max(s, w), hi) with w = (hi - 1) & ~3, newest first in u[0..3] (unused
+// slots = -1).  Returns w, i.e. the new exclusive upper end once this window
+// is examined.  Falls back to scalar loads when the window would cross the
+// end of the neighbour array (nnz not a multiple of 4).
+__device__ __forceinline__ int64_t load_window_down(const int32_t *__restrict__ nbr, int64_t nnz,
+                                                    int64_t s, int64_t hi, int32_t u[4]) {
+  const int64_t w = (hi - 1) & ~(int64_t)3;
+  int4 q;
+  if (w + 4 <= nnz) {  // nnz < 0 flags a neighbour array that is not 16-byte aligned
+    q = __ldg(reinterpret_cast<const int4 *>(nbr + w));
+  } else {
+    const int64_t lim = nnz < 0 ? -nnz : nnz;
+    q.x = w < lim ? __ldg(&nbr[w]) : -1;
+    q.y = w + 1 < lim ? __ldg(&nbr[w + 1]) : -1;
+    q.z = w + 2 < lim ? __ldg(&nbr[w + 2]) : -1;
+    q.w = w + 3 < lim ? __ldg(&nbr[w + 3]) : -1;
+  }
+  u[0] = (w + 3 < hi && w + 3 >= s) ? q.w : -1;
+  u[1] = (w + 2 < hi && w + 2 >= s) ? q.z : -1;
+  u[2] = (w + 1 < hi && w + 1 >= s) ? q.y : -1;
+  u[3] = (w >= s) ? q.x : -1;
+  return w;
+}
+
+// Upward window for pushes: entries [p, min(e, w + 4)) with w = p & ~3.
+__device__ __forceinline__ int64_t load_window_up(const int32_t *__restrict__ nbr, int64_t nnz,
+                                                  int64_t p, int64_t e, int32_t u[4]) {
+  const int64_t w = p & ~(int64_t)3;
+  int4 q;
+  if (w + 4 <= nnz) {  // nnz < 0: scalar path (unaligned neighbour array)
+    q = __ldg(reinterpret_cast<const int4 *>(nbr + w));
+  } else {
+    const int64_t lim = nnz < 0 ? -nnz : nnz;
+    q.x = w < lim ? __ldg(&nbr[w]) : -1;
+    q.y = w + 1 < lim ? __ldg(&nbr[w + 1]) : -1;
+    q.z = w + 2 < lim ? __ldg(&nbr[w + 2]) : -1;
+    q.w = w + 3 < lim ? __ldg(&nbr[w + 3]) : -1;
+  }
+  u[0] = (w >= p && w < e) ? q.x : -1;
+  u[1] = (w + 1 >= p && w + 1 < e) ? q.y : -1;
+  u[2] = (w + 2 >= p && w + 2 < e) ? q.z : -1;
+  u[3] = (w + 3 >= p && w + 3 < e) ? q.w : -1;
+  return w + 4;
+}
+
+}  // namespace tcmis_b200

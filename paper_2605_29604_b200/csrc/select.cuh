@@ -29,6 +29,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "scan.cuh"
 
 namespace tcmis_b200 {
 
@@ -41,6 +42,7 @@ struct SelectArgs {
   const int32_t *nz;       // round-1 list
   const int64_t *off;
   const int32_t *nbr;
+  int64_t vnnz;            // nnz, negated if nbr is not 16-byte aligned (scan.cuh)
   const uint64_t *key;
   uint8_t *next;
   uint8_t *state;
@@ -65,52 +67,51 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
   // round 1 visits only the non-isolated vertices (k_priorities already made
   // the isolated ones candidates)
   const int64_t cnt = round == 1 ? a.n1 : ctrl->wl_count[round & 1];
-  if ((int64_t)blockIdx.x * kBlock >= cnt) return;
   const int32_t *wl = round == 1 ? a.nz : ((round & 1) ? a.wl1 : a.wl0);
   const int32_t *__restrict__ nbr = a.nbr;
   const uint64_t *__restrict__ key = a.key;
-  const int64_t stride = (int64_t)gridDim.x * kBlock;
   WarpOut wo{s_out[threadIdx.x >> 5], 0};
+  Dispenser disp;
   unsigned long long sel = 0;
-  int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x - stride;
   int mode = kFetch;
   int32_t v = 0;
   int64_t s = 0, e = 0, hi = 0;
   uint64_t kv = 0;
-  auto fetch = [&]() {
-    i += stride;
-    if (i < cnt) {
-      v = __ldg(&wl[i]);
-      s = __ldg(&a.off[v]);
-      e = __ldg(&a.off[v + 1]);
-      kv = __ldg(&key[v]);
-      hi = e;
-      mode = kScan;
-    } else {
-      mode = kDone;
+  for (;;) {
+    const bool need = mode == kFetch;
+    const int64_t idx = disp.take(need, cnt, &ctrl->sel_cursor);
+    if (need) {
+      if (idx < 0) {
+        mode = kDone;
+      } else {
+        v = __ldg(&wl[idx]);
+        s = __ldg(&a.off[v]);
+        e = __ldg(&a.off[v + 1]);
+        kv = __ldg(&key[v]);
+        hi = e;
+        mode = kScan;
+      }
     }
-  };
-  fetch();
-  while (__any_sync(0xffffffffu, mode != kDone)) {
+    if (!__any_sync(0xffffffffu, mode != kDone)) break;
     bool defer = false, noncand = false;
     if (mode == kScan) {
-      int32_t u[kStep];
-#pragma unroll
-      for (int j = 0; j < kStep; ++j) u[j] = hi - 1 - j >= s ? __ldg(&nbr[hi - 1 - j]) : -1;
+      int32_t u[4];
+      const int64_t w = load_window_down(nbr, a.vnnz, s, hi, u);
       bool blocked = false;
 #pragma unroll
-      for (int j = 0; j < kStep; ++j)
+      for (int j = 0; j < 4; ++j)
         if (u[j] >= 0) blocked |= __ldg(&key[u[j]]) > kv;
-      hi -= kStep;
+      const bool whole = w <= s;  // this window held the rest of the row
+      hi = w;
       if (blocked) {
         noncand = !a.push;
         mode = kFetch;
-      } else if (hi <= s) {
+      } else if (whole) {
         mark_candidate(v, a.next, a.state, a.segflag, a.T);
         ++sel;
-        if (a.push && e - s <= kStep) {  // the whole row is still in registers
+        if (a.push && hi + 4 >= e) {  // the whole row was this one window
 #pragma unroll
-          for (int j = 0; j < kStep; ++j)
+          for (int j = 0; j < 4; ++j)
             if (u[j] >= 0) exclude(a.next, u[j]);
           mode = kFetch;
         } else {
@@ -122,18 +123,16 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
         mode = kFetch;
       }
     } else if (mode == kPush) {
-      int32_t u[kStep];
+      int32_t u[4];
+      const int64_t p = load_window_up(nbr, a.vnnz, hi, e, u);
 #pragma unroll
-      for (int j = 0; j < kStep; ++j) u[j] = hi + j < e ? __ldg(&nbr[hi + j]) : -1;
-#pragma unroll
-      for (int j = 0; j < kStep; ++j)
+      for (int j = 0; j < 4; ++j)
         if (u[j] >= 0) exclude(a.next, u[j]);
-      hi += kStep;
+      hi = p;
       if (hi >= e) mode = kFetch;
     }
     if (!a.push) warp_emit(wo, noncand, v, a.check, &ctrl->check_count);
     warp_append(defer, v, a.long_list, &ctrl->long_count);
-    if (mode == kFetch) fetch();
   }
   if (!a.push) warp_flush(wo, a.check, &ctrl->check_count);
   block_add3(sel, 0, 0, ctrl);
@@ -152,7 +151,9 @@ __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
     const int32_t v = a.long_list[q];
     const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
     const uint64_t kv = __ldg(&key[v]);
-    int64_t hi = e - kThreadMax;
+    // the thread stage examined at least the last kThreadMax - 3 entries (its
+    // first window may be short); rescanning an entry is harmless
+    int64_t hi = e - (kThreadMax - 3);
     bool blocked = false;
     while (!blocked && hi > s) {
       int32_t u[4];

@@ -344,6 +344,7 @@ struct RoundArgs {
   int32_t nz_count;     // round-1 select list
   const int32_t *nz;
   int32_t tail_thr;     // rounds start in k_tail once alive <= tail_thr
+  int64_t vnnz;         // nnz, negated when the neighbour array is not 16-byte aligned
   int tail_grid;
   bool operator==(const RoundArgs &o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
@@ -355,6 +356,7 @@ SelectArgs select_args(tcmis_graph *g, const RoundArgs &a) {
   s.nz = a.nz;
   s.off = a.off;
   s.nbr = a.nbr;
+  s.vnnz = a.vnnz;
   s.key = ws.key;
   s.next = ws.next;
   s.state = ws.state;
@@ -375,6 +377,7 @@ UpdateArgs update_args(tcmis_graph *g, const RoundArgs &a) {
   u.n = a.n;
   u.off = a.off;
   u.nbr = a.nbr;
+  u.vnnz = a.vnnz;
   u.key = ws.key;
   u.state = ws.state;
   u.next = ws.next;
@@ -570,6 +573,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   a.sel_grid = ctx->num_sms * 8;
   a.upd_grid = ctx->num_sms * 4;
   a.nz = g->d_nz;
+  a.vnnz = ((uintptr_t)g->d_nbr & 15) == 0 ? g->nnz : -g->nnz;
   a.nz_count = g->nz_count;
   // exclusion form: pull on degree-skewed graphs, where the
   // neighbours of candidates concentrate on hubs and early-exit pulls are

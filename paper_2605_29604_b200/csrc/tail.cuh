@@ -30,6 +30,10 @@
 namespace tcmis_b200 {
 
 constexpr int kGroup = 8;             // lanes per vertex in the tail kernel
+#ifndef TCMIS_TAIL_UNROLL
+#define TCMIS_TAIL_UNROLL 16
+#endif
+constexpr int kTU = TCMIS_TAIL_UNROLL;  // independent loads per lane per step
 constexpr int kTailBlock = 1024;  // one block per SM: 148 arrivals per barrier
 
 struct TailArgs {
@@ -86,7 +90,7 @@ __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
   const unsigned gmask = ((1u << kGroup) - 1u) << (lane & ~(kGroup - 1));
   const int64_t gid = ((int64_t)blockIdx.x * kTailBlock + threadIdx.x) / kGroup;
   const int64_t ngroups = ((int64_t)gridDim.x * kTailBlock) / kGroup;
-  constexpr int kW = kGroup * 4;  // entries per group step
+  constexpr int kW = kGroup * kTU;  // entries per group step: short rows settle in one step
   // Every block walks the rounds in lockstep, so the round number is local.
   // Two barriers per round (after S, after U).  Block 0 publishes round r-1's
   // IterationStats at the start of round r and clears the counters; nobody
@@ -130,15 +134,15 @@ __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
       const uint64_t kv = __ldcg(&a.key[v]);
       bool blocked = false;
       for (int64_t hi = e; hi > s && !blocked; hi -= kW) {
-        int32_t u[4];
+        int32_t u[kTU];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < kTU; ++j) {
           const int64_t idx = hi - 1 - gl - kGroup * j;
           u[j] = idx >= s ? __ldg(&a.nbr[idx]) : -1;
         }
         bool b = false;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < kTU; ++j)
           if (u[j] >= 0) b |= __ldcg(&a.key[u[j]]) > kv;
         blocked = group_any(b, gmask) != 0;
       }
@@ -185,15 +189,15 @@ __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
         const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
         bool hit = false;
         for (int64_t hi = e; hi > s && !hit; hi -= kW) {
-          int32_t u[4];
+          int32_t u[kTU];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < kTU; ++j) {
             const int64_t idx = hi - 1 - gl - kGroup * j;
             u[j] = idx >= s ? __ldg(&a.nbr[idx]) : -1;
           }
           bool b = false;
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
+          for (int j = 0; j < kTU; ++j)
             if (u[j] >= 0) b |= __ldcg(&a.next[u[j]]) == 1;
           hit = group_any(b, gmask) != 0;
         }

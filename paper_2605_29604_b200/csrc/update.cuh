@@ -28,6 +28,7 @@
 #include <cub/cub.cuh>
 
 #include "common.cuh"
+#include "scan.cuh"
 
 namespace tcmis_b200 {
 
@@ -37,6 +38,7 @@ struct UpdateArgs {
   int32_t n;
   const int64_t *off;
   const int32_t *nbr;
+  int64_t vnnz;            // nnz, negated if nbr is not 16-byte aligned (scan.cuh)
   uint64_t *key;
   uint8_t *state;
   const uint8_t *next;
@@ -117,43 +119,41 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
   Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
   const int64_t cnt = ctrl->check_count;
-  if ((int64_t)blockIdx.x * kBlock >= cnt) return;
   int32_t *out = (round & 1) ? a.wl0 : a.wl1;
   int *tail = &ctrl->wl_count[(round + 1) & 1];
   const uint64_t fresh_m = a.fresh ? mix64(combine_seed(a.seed, (uint64_t)round + 1)) : 0;
   const int32_t *__restrict__ nbr = a.nbr;
   const uint8_t *__restrict__ next = a.next;
   WarpOut wo{s_buf[threadIdx.x >> 5], 0};
-  const int64_t stride = (int64_t)gridDim.x * kBlock;
+  Dispenser disp;
   unsigned long long rem = 0;
-  int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x - stride;
   int mode = kFetch;
   int32_t v = 0;
   int64_t s = 0, e = 0, hi = 0;
-  auto fetch = [&]() {
-    i += stride;
-    if (i < cnt) {
-      v = __ldg(&a.check[i]);
-      s = __ldg(&a.off[v]);
-      e = __ldg(&a.off[v + 1]);
-      hi = e;
-      mode = kScan;
-    } else {
-      mode = kDone;
+  for (;;) {
+    const bool need = mode == kFetch;
+    const int64_t idx = disp.take(need, cnt, &ctrl->pull_cursor);
+    if (need) {
+      if (idx < 0) {
+        mode = kDone;
+      } else {
+        v = __ldg(&a.check[idx]);
+        s = __ldg(&a.off[v]);
+        e = __ldg(&a.off[v + 1]);
+        hi = e;
+        mode = kScan;
+      }
     }
-  };
-  fetch();
-  while (__any_sync(0xffffffffu, mode != kDone)) {
+    if (!__any_sync(0xffffffffu, mode != kDone)) break;
     bool survive = false, defer = false;
     if (mode == kScan) {
-      int32_t u[kStep];
-#pragma unroll
-      for (int j = 0; j < kStep; ++j) u[j] = hi - 1 - j >= s ? __ldg(&nbr[hi - 1 - j]) : -1;
+      int32_t u[4];
+      const int64_t w = load_window_down(nbr, a.vnnz, s, hi, u);
       bool hit = false;
 #pragma unroll
-      for (int j = 0; j < kStep; ++j)
+      for (int j = 0; j < 4; ++j)
         if (u[j] >= 0) hit |= next[u[j]] == 1;
-      hi -= kStep;
+      hi = w;
       if (hit) {
         mark_removed(v, a.state, a.key);
         ++rem;
@@ -169,7 +169,6 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
     }
     warp_emit(wo, survive, v, out, tail);
     warp_append(defer, v, a.long_list, &ctrl->pull_count);
-    if (mode == kFetch) fetch();
   }
   warp_flush(wo, out, tail);
   block_add3(0, rem, 0, ctrl);
@@ -259,6 +258,8 @@ __global__ void __launch_bounds__(kBlock)
     vc->long_count = 0;
     vc->pull_count = 0;
     vc->check_count = 0;
+    vc->sel_cursor = 0;
+    vc->pull_cursor = 0;
     vc->main_rounds = vc->main_rounds + 1;
     vc->round = round + 1;
     if (use_cond) cudaGraphSetConditional(cond, alive > a.tail_thr ? 1u : 0u);
