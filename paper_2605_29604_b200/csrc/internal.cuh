@@ -57,8 +57,8 @@ struct Ctrl {
   int32_t check_count; // pull: non-candidates emitted by the select kernels
   int32_t main_rounds; // rounds run by the per-round kernels (the rest ran in k_tail)
   int32_t tail_check[2]; // k_tail pull check-list length, by round parity
-  int32_t sel_cursor;  // k_select work dispenser
-  int32_t pull_cursor; // k_update_pull work dispenser
+  int32_t sel_undec;   // rows k_probe_select left to the k_select engine
+  int32_t pull_undec;  // rows k_probe_pull left to the k_update_pull engine
 };
 
 struct Workspace {
@@ -73,6 +73,8 @@ struct Workspace {
   int32_t *long_list = nullptr;   // select: rows that outlived the thread probe
   int32_t *long_list2 = nullptr;  // pull exclusion: same, for k_round_end
   int32_t *check = nullptr;       // pull exclusion: this round's non-candidates
+  int32_t *undec_sel = nullptr;   // probe leftovers for the select engine
+  int32_t *undec_pull = nullptr;  // probe leftovers for the pull engine
   uint32_t *segmark = nullptr;    // tail rounds: round that last counted a block column
   unsigned *bar = nullptr;        // grid barrier of k_tail
   int64_t *mis_count = nullptr;

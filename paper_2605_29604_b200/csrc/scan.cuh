@@ -106,3 +106,40 @@ __device__ __forceinline__ int64_t load_window_up(const int32_t *__restrict__ nb
 }
 
 }  // namespace tcmis_b200
+
+namespace tcmis_b200 {
+
+// The last <= 8 entries of a row [s, e) with two aligned 16-byte loads:
+// u[0] = nbr[e-1], u[1] = nbr[e-2], ... (-1 where outside [s, e)).  Covers
+// the whole row when e - s <= 5, and always at least min(5, e - s) entries.
+__device__ __forceinline__ void load_tail8(const int32_t *__restrict__ nbr, int64_t nnz,
+                                           int64_t s, int64_t e, int32_t u[8]) {
+  const int64_t w1 = (e - 1) & ~(int64_t)3;  // window holding e-1
+  const int64_t w0 = w1 - 4;
+  int4 a, b;
+  if (w0 >= 0 && w1 + 4 <= nnz) {
+    a = __ldg(reinterpret_cast<const int4 *>(nbr + w0));
+    b = __ldg(reinterpret_cast<const int4 *>(nbr + w1));
+  } else {
+    const int64_t lim = nnz < 0 ? -nnz : nnz;
+    int32_t t[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t[j] = (w0 + j >= 0 && w0 + j < lim) ? __ldg(&nbr[w0 + j]) : -1;
+    a = make_int4(t[0], t[1], t[2], t[3]);
+    b = make_int4(t[4], t[5], t[6], t[7]);
+  }
+  // e-1 sits at offset r of window b; u[j] = c[4 + r - j] over c = (a, b)
+  const int r = (int)((e - 1) - w1);
+  int32_t c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  int32_t t[8];
+  switch (r) {
+    case 0: t[0] = c[4]; t[1] = c[3]; t[2] = c[2]; t[3] = c[1]; t[4] = c[0]; t[5] = t[6] = t[7] = -1; break;
+    case 1: t[0] = c[5]; t[1] = c[4]; t[2] = c[3]; t[3] = c[2]; t[4] = c[1]; t[5] = c[0]; t[6] = t[7] = -1; break;
+    case 2: t[0] = c[6]; t[1] = c[5]; t[2] = c[4]; t[3] = c[3]; t[4] = c[2]; t[5] = c[1]; t[6] = c[0]; t[7] = -1; break;
+    default: t[0] = c[7]; t[1] = c[6]; t[2] = c[5]; t[3] = c[4]; t[4] = c[3]; t[5] = c[2]; t[6] = c[1]; t[7] = c[0]; break;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) u[j] = e - 1 - j >= s ? t[j] : -1;
+}
+
+}  // namespace tcmis_b200

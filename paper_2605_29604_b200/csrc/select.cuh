@@ -53,6 +53,7 @@ struct SelectArgs {
   const int32_t *wl0, *wl1;
   int32_t *long_list;      // rows outliving the thread probe (ctrl->long_count)
   int32_t *check;          // pull mode: non-candidates (ctrl->check_count)
+  int32_t *undecided;      // rows the probe could not settle (ctrl->sel_undec)
 };
 
 // push: every neighbour of a candidate is excluded this round (spmv.cpp:18-59
@@ -60,39 +61,98 @@ struct SelectArgs {
 // candidates, so the store is idempotent.
 __device__ __forceinline__ void exclude(uint8_t *__restrict__ next, int32_t u) { next[u] = 2; }
 
-__global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a) {
-  __shared__ int32_t s_out[kBlock / 32][64];
+constexpr int kProbeK = 4;  // row entries the straight-line probe examines
+
+// Probe: one thread per worklist vertex, straight-line code in warp lockstep
+// (no per-lane loop): coalesced row extents and own key, the last <= 8 row
+// entries with two aligned 16-byte loads, keys of the last kProbeK gathered.
+// This settles 84 % of R-MAT s22's round-1 vertices and every vertex of
+// rows <= kProbeK (the whole grid, most of the RGG).
+__global__ void __launch_bounds__(kBlock) k_probe_select(SelectArgs a) {
+  __shared__ int32_t s_chk[kBlock / 32][64];
+  __shared__ int32_t s_und[kBlock / 32][64];
   Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
   // round 1 visits only the non-isolated vertices (k_priorities already made
   // the isolated ones candidates)
   const int64_t cnt = round == 1 ? a.n1 : ctrl->wl_count[round & 1];
+  if ((int64_t)blockIdx.x * kBlock >= cnt) return;
   const int32_t *wl = round == 1 ? a.nz : ((round & 1) ? a.wl1 : a.wl0);
   const int32_t *__restrict__ nbr = a.nbr;
   const uint64_t *__restrict__ key = a.key;
-  WarpOut wo{s_out[threadIdx.x >> 5], 0};
-  Dispenser disp;
+  const int lane = threadIdx.x & 31;
+  WarpOut chk{s_chk[threadIdx.x >> 5], 0}, und{s_und[threadIdx.x >> 5], 0};
   unsigned long long sel = 0;
+  const int64_t stride = (int64_t)gridDim.x * kBlock;
+  for (int64_t wb = (int64_t)blockIdx.x * kBlock + (threadIdx.x & ~31); wb < cnt; wb += stride) {
+    const int64_t i = wb + lane;
+    bool noncand = false, undecided = false;
+    int32_t v = 0;
+    if (i < cnt) {
+      v = __ldg(&wl[i]);
+      const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
+      const uint64_t kv = __ldg(&key[v]);
+      int32_t u[8];
+      load_tail8(nbr, a.vnnz, s, e, u);
+      bool blocked = false;
+#pragma unroll
+      for (int j = 0; j < kProbeK; ++j)
+        if (u[j] >= 0) blocked |= __ldg(&key[u[j]]) > kv;
+      if (blocked) {
+        noncand = !a.push;
+      } else if (e - s <= kProbeK) {
+        mark_candidate(v, a.next, a.state, a.segflag, a.T);
+        ++sel;
+        if (a.push) {
+#pragma unroll
+          for (int j = 0; j < kProbeK; ++j)
+            if (u[j] >= 0) exclude(a.next, u[j]);
+        }
+      } else {
+        undecided = true;
+      }
+    }
+    if (!a.push) warp_emit(chk, noncand, v, a.check, &ctrl->check_count);
+    warp_emit(und, undecided, v, a.undecided, &ctrl->sel_undec);
+  }
+  if (!a.push) warp_flush(chk, a.check, &ctrl->check_count);
+  warp_flush(und, a.undecided, &ctrl->sel_undec);
+  block_add3(sel, 0, 0, ctrl);
+}
+
+// Engine: the probe's undecided rows, one lane per row as a per-lane state
+// machine (scan down in 16-byte windows from e - kProbeK; push up), so a
+// lane never idles behind another lane's longer row.
+__global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a) {
+  __shared__ int32_t s_out[kBlock / 32][64];
+  Ctrl *ctrl = a.ctrl;
+  const int64_t cnt = ctrl->sel_undec;
+  if ((int64_t)blockIdx.x * kBlock >= cnt) return;
+  const int32_t *__restrict__ nbr = a.nbr;
+  const uint64_t *__restrict__ key = a.key;
+  const int64_t stride = (int64_t)gridDim.x * kBlock;
+  WarpOut wo{s_out[threadIdx.x >> 5], 0};
+  unsigned long long sel = 0;
+  int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x - stride;
   int mode = kFetch;
   int32_t v = 0;
   int64_t s = 0, e = 0, hi = 0;
   uint64_t kv = 0;
-  for (;;) {
-    const bool need = mode == kFetch;
-    const int64_t idx = disp.take(need, cnt, &ctrl->sel_cursor);
-    if (need) {
-      if (idx < 0) {
-        mode = kDone;
-      } else {
-        v = __ldg(&wl[idx]);
-        s = __ldg(&a.off[v]);
-        e = __ldg(&a.off[v + 1]);
-        kv = __ldg(&key[v]);
-        hi = e;
-        mode = kScan;
-      }
+  auto fetch = [&]() {
+    i += stride;
+    if (i < cnt) {
+      v = __ldg(&a.undecided[i]);
+      s = __ldg(&a.off[v]);
+      e = __ldg(&a.off[v + 1]);
+      kv = __ldg(&key[v]);
+      hi = e - kProbeK;  // the probe examined the last kProbeK entries
+      mode = kScan;
+    } else {
+      mode = kDone;
     }
-    if (!__any_sync(0xffffffffu, mode != kDone)) break;
+  };
+  fetch();
+  while (__any_sync(0xffffffffu, mode != kDone)) {
     bool defer = false, noncand = false;
     if (mode == kScan) {
       int32_t u[4];
@@ -101,23 +161,15 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if (u[j] >= 0) blocked |= __ldg(&key[u[j]]) > kv;
-      const bool whole = w <= s;  // this window held the rest of the row
       hi = w;
       if (blocked) {
         noncand = !a.push;
         mode = kFetch;
-      } else if (whole) {
+      } else if (hi <= s) {
         mark_candidate(v, a.next, a.state, a.segflag, a.T);
         ++sel;
-        if (a.push && hi + 4 >= e) {  // the whole row was this one window
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (u[j] >= 0) exclude(a.next, u[j]);
-          mode = kFetch;
-        } else {
-          mode = a.push ? kPush : kFetch;
-          hi = s;  // push cursor runs upward from s
-        }
+        mode = a.push ? kPush : kFetch;
+        hi = s;  // push cursor runs upward from s
       } else if (e - hi >= kThreadMax) {
         defer = true;
         mode = kFetch;
@@ -133,6 +185,7 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
     }
     if (!a.push) warp_emit(wo, noncand, v, a.check, &ctrl->check_count);
     warp_append(defer, v, a.long_list, &ctrl->long_count);
+    if (mode == kFetch) fetch();
   }
   if (!a.push) warp_flush(wo, a.check, &ctrl->check_count);
   block_add3(sel, 0, 0, ctrl);

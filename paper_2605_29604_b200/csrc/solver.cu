@@ -173,6 +173,8 @@ void free_workspace(Workspace &ws) {
   cudaFree(ws.long_list);
   cudaFree(ws.long_list2);
   cudaFree(ws.check);
+  cudaFree(ws.undec_sel);
+  cudaFree(ws.undec_pull);
   cudaFree(ws.segmark);
   cudaFree(ws.bar);
   cudaFree(ws.mis_count);
@@ -213,6 +215,8 @@ int ensure_workspace(tcmis_graph *g) {
     cudaFree(ws.long_list);
     cudaFree(ws.long_list2);
     cudaFree(ws.check);
+    cudaFree(ws.undec_sel);
+    cudaFree(ws.undec_pull);
     cudaFree(ws.segmark);
     ws.n_cap = 0;
     if (int rc = dev_alloc(&ws.key, n)) return rc;
@@ -224,6 +228,8 @@ int ensure_workspace(tcmis_graph *g) {
     if (int rc = dev_alloc(&ws.long_list, n)) return rc;
     if (int rc = dev_alloc(&ws.long_list2, n)) return rc;
     if (int rc = dev_alloc(&ws.check, n)) return rc;
+    if (int rc = dev_alloc(&ws.undec_sel, n)) return rc;
+    if (int rc = dev_alloc(&ws.undec_pull, n)) return rc;
     if (int rc = dev_alloc(&ws.segmark, n)) return rc;
     TCMIS_CUDA(cudaMemsetAsync(ws.next, 0, n, g->ctx->stream));
     ws.n_cap = n;
@@ -368,6 +374,7 @@ SelectArgs select_args(tcmis_graph *g, const RoundArgs &a) {
   s.wl1 = ws.wl[1];
   s.long_list = ws.long_list;
   s.check = ws.check;
+  s.undecided = ws.undec_sel;
   return s;
 }
 
@@ -388,6 +395,7 @@ UpdateArgs update_args(tcmis_graph *g, const RoundArgs &a) {
   u.seed = a.seed;
   u.check = ws.check;
   u.long_list = ws.long_list2;
+  u.undecided = ws.undec_pull;
   u.segflag = ws.segflag;
   u.rowtiles = a.rowtiles;
   u.nseg = a.nseg;
@@ -454,6 +462,8 @@ int tail_grid(tcmis_ctx *ctx) {
 int launch_select(tcmis_graph *g, const RoundArgs &a) {
   cudaStream_t st = g->ctx->stream;
   const SelectArgs s = select_args(g, a);
+  k_probe_select<<<a.sel_grid, kBlock, 0, st>>>(s);
+  TCMIS_LAUNCHED(g->ctx);
   k_select<<<a.sel_grid, kBlock, 0, st>>>(s);
   TCMIS_LAUNCHED(g->ctx);
   k_select_long<<<a.sel_grid, kBlock, 0, st>>>(s);
@@ -465,15 +475,20 @@ int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle
                   int use_cond) {
   cudaStream_t st = g->ctx->stream;
   const UpdateArgs u = update_args(g, a);
-  if (a.pull) k_update_pull<<<a.sel_grid, kBlock, 0, st>>>(u);
-  else k_update<<<a.upd_grid, kBlock, 0, st>>>(u);
+  if (a.pull) {
+    k_probe_pull<<<a.sel_grid, kBlock, 0, st>>>(u);
+    TCMIS_LAUNCHED(g->ctx);
+    k_update_pull<<<a.sel_grid, kBlock, 0, st>>>(u);
+  } else {
+    k_update<<<a.upd_grid, kBlock, 0, st>>>(u);
+  }
   TCMIS_LAUNCHED(g->ctx);
   k_round_end<<<a.upd_grid, kBlock, 0, st>>>(u, cond, use_cond);
   TCMIS_LAUNCHED(g->ctx);
   return 0;
 }
 
-constexpr int kLaunchesPerRound = 4;
+inline int launches_per_round(const RoundArgs &a) { return a.pull ? 6 : 5; }
 
 // Instantiate (once per distinct argument set) the graph
 //   WHILE(cond) { k_select ; k_update }
@@ -520,7 +535,7 @@ int ensure_round_graph(tcmis_graph *g, const RoundArgs &a) {
     if (e != cudaSuccess) rc = cuda_error(e, "cudaGraphInstantiate");
   }
   cudaGraphDestroy(graph);
-  g->ctx->launches -= kLaunchesPerRound;  // capture is not execution
+  g->ctx->launches -= launches_per_round(a);  // capture is not execution
   if (!rc) std::memcpy(ws.graph_key, &a, sizeof(a));
   return rc;
 }
@@ -602,7 +617,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     // condition (alive > 0), so no host round trip happens between rounds.
     if (int rc = ensure_round_graph(g, a)) return rc;
     TCMIS_CUDA(cudaGraphLaunch(ws.exec, st));
-    ctx->launches += kLaunchesPerRound;  // per round, counted below
+    ctx->launches += launches_per_round(a);  // per round, counted below
     TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
     TCMIS_CUDA(cudaStreamSynchronize(st));
     if (ws.h_ctrl->overflow) {
@@ -619,7 +634,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     } else {
       const int rr = ws.h_ctrl->round - 1;
       const int mr = ws.h_ctrl->main_rounds;
-      ctx->launches += kLaunchesPerRound * ((int64_t)mr - 1) + (rr > mr ? 1 : 0);
+      ctx->launches += launches_per_round(a) * ((int64_t)mr - 1) + (rr > mr ? 1 : 0);
       rounds_h.resize(rr);
       TCMIS_CUDA(cudaMemcpyAsync(rounds_h.data(), ws.rounds, sizeof(DevRound) * rr,
                                  cudaMemcpyDeviceToHost, st));

@@ -48,6 +48,7 @@ struct UpdateArgs {
   uint64_t seed;
   const int32_t *check;    // pull: non-candidates of this round
   int32_t *long_list;      // pull: rows outliving the thread probe (ctrl->pull_count)
+  int32_t *undecided;      // pull: rows the probe could not settle (ctrl->pull_undec)
   uint8_t *segflag;
   const int32_t *rowtiles;
   int32_t nseg;
@@ -114,37 +115,90 @@ __global__ void __launch_bounds__(kBlock) k_update(UpdateArgs a) {
 
 // ---------------------------------------------------------------- pull
 
+constexpr int kPullK = 4;  // row entries the straight-line pull probe examines
+
+// Pull probe: one thread per non-candidate, straight-line: the last <= 8 row
+// entries with two aligned 16-byte loads, candidate flags of the last kPullK.
+__global__ void __launch_bounds__(kBlock) k_probe_pull(UpdateArgs a) {
+  __shared__ int32_t s_srv[kBlock / 32][64];
+  __shared__ int32_t s_und[kBlock / 32][64];
+  Ctrl *ctrl = a.ctrl;
+  const int round = ctrl->round;
+  const int64_t cnt = ctrl->check_count;
+  if ((int64_t)blockIdx.x * kBlock >= cnt) return;
+  int32_t *out = (round & 1) ? a.wl0 : a.wl1;
+  int *tail = &ctrl->wl_count[(round + 1) & 1];
+  const uint64_t fresh_m = a.fresh ? mix64(combine_seed(a.seed, (uint64_t)round + 1)) : 0;
+  const uint8_t *__restrict__ next = a.next;
+  const int lane = threadIdx.x & 31;
+  WarpOut srv{s_srv[threadIdx.x >> 5], 0}, und{s_und[threadIdx.x >> 5], 0};
+  unsigned long long rem = 0;
+  const int64_t stride = (int64_t)gridDim.x * kBlock;
+  for (int64_t wb = (int64_t)blockIdx.x * kBlock + (threadIdx.x & ~31); wb < cnt; wb += stride) {
+    const int64_t i = wb + lane;
+    bool survive = false, undecided = false;
+    int32_t v = 0;
+    if (i < cnt) {
+      v = __ldg(&a.check[i]);
+      const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
+      int32_t u[8];
+      load_tail8(a.nbr, a.vnnz, s, e, u);
+      bool hit = false;
+#pragma unroll
+      for (int j = 0; j < kPullK; ++j)
+        if (u[j] >= 0) hit |= next[u[j]] == 1;
+      if (hit) {
+        mark_removed(v, a.state, a.key);
+        ++rem;
+      } else if (e - s <= kPullK) {
+        survive = true;
+        if (a.fresh) a.key[v] = fresh_key(v, fresh_m);
+      } else {
+        undecided = true;
+      }
+    }
+    warp_emit(srv, survive, v, out, tail);
+    warp_emit(und, undecided, v, a.undecided, &ctrl->pull_undec);
+  }
+  warp_flush(srv, out, tail);
+  warp_flush(und, a.undecided, &ctrl->pull_undec);
+  block_add3(0, rem, 0, ctrl);
+}
+
+// Pull engine over the probe's undecided rows (per-lane state machine,
+// 16-byte windows downward from e - kPullK).
 __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
   __shared__ int32_t s_buf[kBlock / 32][64];
   Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
-  const int64_t cnt = ctrl->check_count;
+  const int64_t cnt = ctrl->pull_undec;
+  if ((int64_t)blockIdx.x * kBlock >= cnt) return;
   int32_t *out = (round & 1) ? a.wl0 : a.wl1;
   int *tail = &ctrl->wl_count[(round + 1) & 1];
   const uint64_t fresh_m = a.fresh ? mix64(combine_seed(a.seed, (uint64_t)round + 1)) : 0;
   const int32_t *__restrict__ nbr = a.nbr;
   const uint8_t *__restrict__ next = a.next;
   WarpOut wo{s_buf[threadIdx.x >> 5], 0};
-  Dispenser disp;
+  const int64_t stride = (int64_t)gridDim.x * kBlock;
   unsigned long long rem = 0;
+  int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x - stride;
   int mode = kFetch;
   int32_t v = 0;
   int64_t s = 0, e = 0, hi = 0;
-  for (;;) {
-    const bool need = mode == kFetch;
-    const int64_t idx = disp.take(need, cnt, &ctrl->pull_cursor);
-    if (need) {
-      if (idx < 0) {
-        mode = kDone;
-      } else {
-        v = __ldg(&a.check[idx]);
-        s = __ldg(&a.off[v]);
-        e = __ldg(&a.off[v + 1]);
-        hi = e;
-        mode = kScan;
-      }
+  auto fetch = [&]() {
+    i += stride;
+    if (i < cnt) {
+      v = __ldg(&a.undecided[i]);
+      s = __ldg(&a.off[v]);
+      e = __ldg(&a.off[v + 1]);
+      hi = e - kPullK;
+      mode = kScan;
+    } else {
+      mode = kDone;
     }
-    if (!__any_sync(0xffffffffu, mode != kDone)) break;
+  };
+  fetch();
+  while (__any_sync(0xffffffffu, mode != kDone)) {
     bool survive = false, defer = false;
     if (mode == kScan) {
       int32_t u[4];
@@ -169,6 +223,7 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
     }
     warp_emit(wo, survive, v, out, tail);
     warp_append(defer, v, a.long_list, &ctrl->pull_count);
+    if (mode == kFetch) fetch();
   }
   warp_flush(wo, out, tail);
   block_add3(0, rem, 0, ctrl);
@@ -258,8 +313,8 @@ __global__ void __launch_bounds__(kBlock)
     vc->long_count = 0;
     vc->pull_count = 0;
     vc->check_count = 0;
-    vc->sel_cursor = 0;
-    vc->pull_cursor = 0;
+    vc->sel_undec = 0;
+    vc->pull_undec = 0;
     vc->main_rounds = vc->main_rounds + 1;
     vc->round = round + 1;
     if (use_cond) cudaGraphSetConditional(cond, alive > a.tail_thr ? 1u : 0u);
