@@ -8,8 +8,6 @@
 // thread-private access of a warp touches a different 128-byte line, so each
 // scalar load costs ~32 wavefronts per warp instruction.  The engine
 // therefore
-//   * hands vertices to lanes in warp batches from a global cursor, so the
-//     worklist / offset / own-key loads of one batch are coalesced;
 //   * reads the row in 16-byte aligned windows (one LDG.128 per lane per
 //     step, 1-4 entries), newest entries first, so a step costs one
 //     wavefront per lane for the row plus one per gathered entry;
@@ -21,43 +19,6 @@
 #include "common.cuh"
 
 namespace tcmis_b200 {
-
-constexpr int kBatch = 64;  // worklist entries a warp claims per cursor bump
-
-// Warp-cooperative vertex dispenser over worklist[0, cnt) with a global
-// cursor; lanes that `need` a vertex get consecutive indices.
-struct Dispenser {
-  int64_t base = 0, end = 0;  // warp-uniform local range
-  __device__ __forceinline__ int64_t take(bool need, int64_t cnt, int *cursor) {
-    const int lane = threadIdx.x & 31;
-    unsigned m = __ballot_sync(0xffffffffu, need);
-    int64_t idx = -1;
-    while (m) {
-      if (base >= end) {
-        int64_t b = 0;
-        if (lane == 0) b = atomicAdd(cursor, kBatch);
-        b = __shfl_sync(0xffffffffu, b, 0);
-        if (b >= cnt) {  // nothing left for anybody
-          base = end = cnt;
-          break;
-        }
-        base = b;
-        end = b + kBatch < cnt ? b + kBatch : cnt;
-      }
-      const int avail = (int)(end - base);
-      const int want = __popc(m);
-      const int give = want < avail ? want : avail;
-      // the first `give` requesting lanes (by lane order) are served
-      const int rank = __popc(m & ((1u << lane) - 1u));
-      if (need && idx < 0 && rank < give) idx = base + rank;
-      base += give;
-      // lanes still unserved retry against a fresh batch
-      const unsigned served = __ballot_sync(0xffffffffu, need && idx >= 0);
-      m &= ~served;
-    }
-    return idx;
-  }
-};
 
 // One aligned 16-byte window of a row, read downward: entries
 // [max(s, w), hi) with w = (hi - 1) & ~3, newest first in u[0..3] (unused

@@ -40,6 +40,7 @@ namespace tcmis_b200 {
 struct SelectArgs {
   int32_t n1;              // round-1 list length (non-isolated vertices)
   const int32_t *nz;       // round-1 list
+  int nz_identity;         // no isolated vertices: the round-1 list is 0..n-1
   const int64_t *off;
   const int32_t *nbr;
   int64_t vnnz;            // nnz, negated if nbr is not 16-byte aligned (scan.cuh)
@@ -68,7 +69,7 @@ constexpr int kProbeK = 4;  // row entries the straight-line probe examines
 // entries with two aligned 16-byte loads, keys of the last kProbeK gathered.
 // This settles 84 % of R-MAT s22's round-1 vertices and every vertex of
 // rows <= kProbeK (the whole grid, most of the RGG).
-__global__ void __launch_bounds__(kBlock) k_probe_select(SelectArgs a) {
+__global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
   __shared__ int32_t s_chk[kBlock / 32][64];
   __shared__ int32_t s_und[kBlock / 32][64];
   Ctrl *ctrl = a.ctrl;
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(kBlock) k_probe_select(SelectArgs a) {
     bool noncand = false, undecided = false;
     int32_t v = 0;
     if (i < cnt) {
-      v = __ldg(&wl[i]);
+      v = (round == 1 && a.nz_identity) ? (int32_t)i : __ldg(&wl[i]);
       const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
       const uint64_t kv = __ldg(&key[v]);
       int32_t u[8];

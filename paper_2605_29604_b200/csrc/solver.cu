@@ -360,6 +360,7 @@ SelectArgs select_args(tcmis_graph *g, const RoundArgs &a) {
   SelectArgs s;
   s.n1 = a.nz_count;
   s.nz = a.nz;
+  s.nz_identity = a.nz_count == a.n ? 1 : 0;
   s.off = a.off;
   s.nbr = a.nbr;
   s.vnnz = a.vnnz;
