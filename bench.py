@@ -50,52 +50,71 @@ def log(*a):
 # ------------------------------------------------------------------ clocks
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML in a
+    1 ms polling thread (nvidia-smi's 100 ms floor misses a ~5 ms region);
+    nvidia-smi as a fallback."""
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
         self.rows = []
+        self.stop = threading.Event()
+        self.nvml = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except FileNotFoundError:
-            self.proc = None
+            import pynvml as N
+            N.nvmlInit()
+            self.nvml = N
+            self.h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_sm = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+        self.t = threading.Thread(target=self._poll, daemon=True)
+        self.t.start()
+        time.sleep(0.02)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 7:
-                self.rows.append(parts)
+    def _poll(self):
+        N = self.nvml
+        while not self.stop.is_set():
+            if N is not None:
+                try:
+                    sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+                    r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    self.rows.append((sm, r))
+                except Exception:
+                    pass
+                time.sleep(0.001)
+            else:
+                try:
+                    out = subprocess.run(
+                        ["nvidia-smi", "-i", str(self.index),
+                         "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                         "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                        timeout=5).stdout.strip().split(",")
+                    self.max_sm = float(out[1])
+                    self.rows.append((float(out[0]), int(out[2], 16)))
+                except Exception:
+                    return
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        time.sleep(0.01)
+        self.stop.set()
+        self.t.join(timeout=2)
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
-        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if r[3 + i].lower().startswith("active")})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
-                "reasons": reasons, "samples": len(self.rows)}
+        sm = sorted(r[0] for r in self.rows)
+        bits = 0
+        for r in self.rows:
+            bits |= int(r[1])
+        names = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                 0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
+        reasons = sorted(v for k, v in names.items() if bits & k and k != 0x1)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": getattr(self, "max_sm", None),
+                "reasons": reasons, "samples": len(self.rows),
+                "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 # --------------------------------------------------------------- graphs
@@ -194,29 +213,23 @@ def run_ours(args) -> dict:
     ms_per_step = total_ms / args.steps
     value = world * m / (ms_per_step * 1e-3) / 1e9  # replicas: every rank solves its graph
 
-    # ---- kernel roofline: per-kernel CUDA events (step-wise loop, same kernels)
+    # ---- kernel roofline: per-kernel CUDA events around every launch of a
+    # step-wise solve (same kernels as the graph; TCMIS_F_TIMING)
     cfg_t = tc.EngineConfig(heuristic=HEUR[args.heuristic], seed=1, tile_dim=16, timing=True,
                             exclusion=excl)
-    sel_ms, upd_ms, per_round = [], [], None
-    for _ in range(max(1, min(args.steps, 5))):
-        r = tc.run_mis(dg, cfg_t)
-        sel_ms.append([i.phase1_ms for i in r.iterations])
-        upd_ms.append([i.phase3_ms for i in r.iterations])
-        per_round = r
-    terms = trajectory_terms(tc, dg, cfg)
-    hbm, peak_kind = peaks()
-    sel_avg = [sum(x[k] for x in sel_ms) / len(sel_ms) for k in range(len(sel_ms[0]))]
-    # SURVEY 8(d) per-unit figures: candidate detection 12|A|+4nnz(A), exclusion
-    # 8|A\C|+4nnz(A\C) -- the fused select kernel does both for round k.
-    b_sel = [12 * a + 4 * na + 8 * nc + 4 * nnc for (a, na, nc, nnc) in terms]
-    k0 = 0  # the dominant launch is round 1's select
-    achieved = b_sel[k0] / (sel_avg[k0] * 1e-3) / 1e9
-    roofline = {"kernel": "k_select (round 1: candidate detection + exclusion push)",
-                "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
-                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                "algorithmic_bytes": b_sel[k0], "launch_ms": round(sel_avg[k0], 4),
-                "traffic": args.traffic}
-
+    runs = []
+    for _ in range(max(3, min(args.steps, 5))):
+        tc.run_mis(dg, cfg_t)
+        runs.append(timeline(tc, ctx))
+    kern = {}
+    for tl in runs:
+        for name, rnd, ms in tl:
+            kern.setdefault((name, rnd), []).append(ms)
+    kernels = sorted(((k[0], k[1], sum(v) / len(v)) for k, v in kern.items()),
+                     key=lambda x: -x[2])
+    roofline = kernel_roofline(tc, dg, cfg, kernels, args)
+    if roofline:
+        roofline["share_of_step"] = round(roofline["launch_ms"] / ms_per_step, 4)
     # ---- e2e through the drop-in C-ABI with host buffers
     e2e = run_e2e(tc, torch, dg, ctx, stream, cfg, args, local, dist, flush)
 
@@ -232,9 +245,7 @@ def run_ours(args) -> dict:
                    "parallelism": "replicas" if world > 1 else "single",
                    "l2": "256 MB flush between steps; CSR > L2"},
         "mis_ms": round(ms_per_step, 4),
-        "per_round_ms": {"select": [round(x, 4) for x in sel_avg],
-                         "update": [round(sum(x[k] for x in upd_ms) / len(upd_ms), 4)
-                                    for k in range(len(upd_ms[0]))]},
+        "kernels_ms": [[k, r, round(ms, 4)] for k, r, ms in kernels],
         "roofline": roofline, "e2e": e2e, "clocks": clk.summary(),
         "gpu_launches": launches,
     }
@@ -244,6 +255,90 @@ def run_ours(args) -> dict:
         dist.barrier()
         dist.destroy_process_group()
     return line if rank == 0 else None
+
+
+def timeline(tc, ctx):
+    """[(kernel, round, ms)] of the context's last TCMIS_F_TIMING solve."""
+    L = tc.load()
+
+    class KT(C.Structure):
+        _fields_ = [("name", C.c_char * 32), ("round", C.c_int32), ("ms", C.c_float)]
+    L.tcmis_ctx_timeline.restype = C.c_int32
+    L.tcmis_ctx_timeline.argtypes = [C.c_void_p, C.c_void_p, C.c_int32]
+    n = L.tcmis_ctx_timeline(ctx.h, None, 0)
+    buf = (KT * max(n, 1))()
+    L.tcmis_ctx_timeline(ctx.h, buf, n)
+    return [(buf[i].name.decode(), int(buf[i].round), float(buf[i].ms)) for i in range(n)]
+
+
+K_PROBE = 4  # entries the probe kernels examine (select.cuh kProbeK, update.cuh kPullK)
+
+
+def kernel_roofline(tc, dg, cfg, kernels, args):
+    """Roofline of the dominant kernel that has a byte model (DESIGN.md
+    "Roofline").  k_probe_select, per launch over its worklist W:
+      sum_{v in W} [4 (list) + 8 (row extent) + 8 (own key)
+                    + min(deg v, 4) * (4 B neighbour id + 8 B neighbour key)]
+      + 2 B per settled candidate (next, state) [+ 1 B per pushed neighbour].
+    The algorithm's bytes at element granularity, computed from the round-1
+    degrees on the host; the kernel time is the CUDA-event time above."""
+    import numpy as np
+    h = dg.download()
+    deg = np.diff(h.offsets)
+    hbm, peak_kind = peaks()
+    times = {(k, r): ms for k, r, ms in kernels}
+    nz = deg[deg > 0]
+    kk = np.minimum(nz, K_PROBE)
+    b_probe = int((4 + 8 + 8) * nz.size + 12 * kk.sum())
+    # candidates settled by the probe: rows <= 4 that nobody blocks; counted
+    # from the observer snapshot of round 1
+    cand1 = round1_candidates(tc, dg, cfg)
+    small = cand1 & (deg <= K_PROBE) & (deg > 0)
+    b_probe += int(2 * small.sum())
+    models = {("k_probe_select", 1): b_probe}
+    best = None
+    for (name, rnd), b in models.items():
+        if (name, rnd) in times:
+            ms = times[(name, rnd)]
+            if best is None or ms > best[2]:
+                best = (name, rnd, ms, b)
+    if best is None:
+        return None
+    name, rnd, ms, b = best
+    ach = b / (ms * 1e-3) / 1e9
+    return {"kernel": f"{name} (round {rnd})", "bound": "hbm", "achieved": round(ach, 1),
+            "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / hbm, 4),
+            "algorithmic_bytes": b, "launch_ms": round(ms, 4),
+            "traffic": traffic_from_profiles(args.config, name),
+            "share_of_step": None}
+
+
+def round1_candidates(tc, dg, cfg):
+    import numpy as np
+    out = {}
+
+    def obs(it, cand, states):
+        if it == 1:
+            out["c"] = cand.astype(bool)
+
+    c2 = tc.EngineConfig(heuristic=cfg.heuristic, seed=cfg.seed, tile_dim=cfg.tile_dim,
+                         iteration_observer=obs)
+    if c2.heuristic == tc.Heuristic.H3:
+        c2.heuristic = tc.Heuristic.H2
+    tc.run_mis(dg, c2)
+    return out.get("c", np.zeros(dg.n, bool))
+
+
+def traffic_from_profiles(config, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the
+    committed ncu --set full summary (profiles/ncu_summary.json), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d[config][kernel]["dram_bytes"]
+    except Exception:
+        return None
 
 
 def trajectory_terms(tc, dg, cfg):

@@ -110,6 +110,16 @@ int tcmis_ctx_synchronize(tcmis_ctx *ctx);
 /* Kernels this context launched since creation (driver evidence counter). */
 int64_t tcmis_ctx_launches(tcmis_ctx *ctx);
 
+/* Per-kernel device times of the last solve run with TCMIS_F_TIMING (CUDA
+ * events around every launch on the context stream).  Returns the number of
+ * entries (copies at most cap). */
+typedef struct tcmis_kernel_time {
+  char name[32];
+  int32_t round;
+  float ms;
+} tcmis_kernel_time;
+int32_t tcmis_ctx_timeline(tcmis_ctx *ctx, tcmis_kernel_time *out, int32_t cap);
+
 /* Device-resident CSR graph (graph.hpp:18-39 Graph: n, offsets[n+1] int64,
  * neighbors[2m] int32, normalised).  upload copies host arrays (H2D on the
  * context stream); wrap_device borrows device arrays the caller keeps alive. */

@@ -110,12 +110,19 @@ TCMIS_API void tcmis_ctx_destroy(tcmis_ctx *ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (auto &ev : ctx->ev) cudaEventDestroy(ev);
+  for (auto &ev : ctx->event_pool) cudaEventDestroy(ev);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
 
 TCMIS_API void *tcmis_ctx_stream(tcmis_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
 TCMIS_API int64_t tcmis_ctx_launches(tcmis_ctx *ctx) { return ctx ? ctx->launches : 0; }
+TCMIS_API int32_t tcmis_ctx_timeline(tcmis_ctx *ctx, tcmis_kernel_time *out, int32_t cap) {
+  if (!ctx) return 0;
+  const int32_t n = (int32_t)ctx->timeline.size();
+  for (int32_t i = 0; i < n && i < cap && out; ++i) out[i] = ctx->timeline[i];
+  return n;
+}
 TCMIS_API int tcmis_ctx_synchronize(tcmis_ctx *ctx) {
   NEED(ctx, "null context");
   TCMIS_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -16,6 +16,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "tcmis_b200.h"
 
@@ -92,6 +93,19 @@ struct Workspace {
 }  // namespace tcmis_b200
 
 struct tcmis_ctx {
+  // per-kernel device timeline of the last TCMIS_F_TIMING solve (events
+  // recorded around every launch on the context stream)
+  struct Mark {
+    const char *name;
+    int32_t round;
+    cudaEvent_t a, b;
+  };
+  bool recording = false;
+  int32_t rec_round = 0;
+  std::vector<Mark> marks;
+  std::vector<cudaEvent_t> event_pool;
+  size_t pool_next = 0;
+  std::vector<tcmis_kernel_time> timeline;
   int device = 0;
   cudaStream_t stream = nullptr;
   int num_sms = 148;
@@ -145,6 +159,24 @@ inline int grid_for(const tcmis_ctx *ctx, int64_t work_threads, int block, int p
   if (want < 1) want = 1;
   return (int)(want < cap ? want : cap);
 }
+
+// timeline recording (solver.cu): wraps one launch in an event pair when the
+// context is recording
+cudaEvent_t pool_event(tcmis_ctx *ctx);
+#define TCMIS_TIMED(ctx, kname, launch_stmt)                                   \
+  do {                                                                        \
+    cudaEvent_t _a = nullptr, _b = nullptr;                                   \
+    if ((ctx)->recording) {                                                   \
+      _a = ::tcmis_b200::pool_event(ctx);                                     \
+      _b = ::tcmis_b200::pool_event(ctx);                                     \
+      cudaEventRecord(_a, (ctx)->stream);                                     \
+    }                                                                         \
+    launch_stmt;                                                              \
+    if ((ctx)->recording) {                                                   \
+      cudaEventRecord(_b, (ctx)->stream);                                     \
+      (ctx)->marks.push_back({kname, (ctx)->rec_round, _a, _b});              \
+    }                                                                         \
+  } while (0)
 
 // workspace management (solver.cu)
 int ensure_workspace(tcmis_graph *g);

@@ -19,6 +19,7 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -158,6 +159,38 @@ __global__ void k_segflags_from(int32_t n, const uint8_t *__restrict__ c, int T,
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x)
     if (c[v]) segflag[v / T] = 1;
+}
+
+// --------------------------------------------------------------- timeline
+
+cudaEvent_t pool_event(tcmis_ctx *ctx) {
+  if (ctx->pool_next >= ctx->event_pool.size()) {
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    ctx->event_pool.push_back(ev);
+  }
+  return ctx->event_pool[ctx->pool_next++];
+}
+
+void timeline_begin(tcmis_ctx *ctx) {
+  ctx->marks.clear();
+  ctx->timeline.clear();
+  ctx->recording = true;
+  ctx->rec_round = 0;
+  ctx->pool_next = 0;
+}
+
+void timeline_end(tcmis_ctx *ctx) {
+  ctx->recording = false;
+  cudaStreamSynchronize(ctx->stream);
+  for (const auto &m : ctx->marks) {
+    tcmis_kernel_time t{};
+    std::snprintf(t.name, sizeof(t.name), "%s", m.name);
+    t.round = m.round;
+    cudaEventElapsedTime(&t.ms, m.a, m.b);
+    ctx->timeline.push_back(t);
+  }
+  ctx->marks.clear();
 }
 
 // -------------------------------------------------------------- workspace
@@ -310,9 +343,10 @@ int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bi
   }
   const double scale = mode ? (double)(1u << scale_bits) : 0.0;
   const int grid = grid_for(ctx, g->n, 256, 16);
-  k_priorities<<<grid, 256, 0, ctx->stream>>>(g->n, g->d_off, mode, mseed,
-                                               mode ? avg_degree(g) : 0.0, scale, key, p_out,
-                                               state, next, segflag, T);
+  TCMIS_TIMED(ctx, "k_priorities",
+              (k_priorities<<<grid, 256, 0, ctx->stream>>>(g->n, g->d_off, mode, mseed,
+                                                          mode ? avg_degree(g) : 0.0, scale, key,
+                                                          p_out, state, next, segflag, T)));
   TCMIS_LAUNCHED(ctx);
   return 0;
 }
@@ -446,7 +480,9 @@ int launch_tail(tcmis_graph *g, const RoundArgs &a) {
   attr[0].val.cooperative = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  TCMIS_CUDA(cudaLaunchKernelEx(&lc, k_tail, t));
+  cudaError_t e = cudaSuccess;
+  TCMIS_TIMED(g->ctx, "k_tail", (e = cudaLaunchKernelEx(&lc, k_tail, t)));
+  TCMIS_CUDA(e);
   g->ctx->launches++;
   return 0;
 }
@@ -461,31 +497,33 @@ int tail_grid(tcmis_ctx *ctx) {
 }
 
 int launch_select(tcmis_graph *g, const RoundArgs &a) {
-  cudaStream_t st = g->ctx->stream;
+  tcmis_ctx *ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
   const SelectArgs s = select_args(g, a);
-  k_probe_select<<<a.sel_grid, kBlock, 0, st>>>(s);
-  TCMIS_LAUNCHED(g->ctx);
-  k_select<<<a.sel_grid, kBlock, 0, st>>>(s);
-  TCMIS_LAUNCHED(g->ctx);
-  k_select_long<<<a.sel_grid, kBlock, 0, st>>>(s);
-  TCMIS_LAUNCHED(g->ctx);
+  TCMIS_TIMED(ctx, "k_probe_select", (k_probe_select<<<a.sel_grid, kBlock, 0, st>>>(s)));
+  TCMIS_LAUNCHED(ctx);
+  TCMIS_TIMED(ctx, "k_select", (k_select<<<a.sel_grid, kBlock, 0, st>>>(s)));
+  TCMIS_LAUNCHED(ctx);
+  TCMIS_TIMED(ctx, "k_select_long", (k_select_long<<<a.sel_grid, kBlock, 0, st>>>(s)));
+  TCMIS_LAUNCHED(ctx);
   return 0;
 }
 
 int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle cond,
                   int use_cond) {
-  cudaStream_t st = g->ctx->stream;
+  tcmis_ctx *ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
   const UpdateArgs u = update_args(g, a);
   if (a.pull) {
-    k_probe_pull<<<a.sel_grid, kBlock, 0, st>>>(u);
-    TCMIS_LAUNCHED(g->ctx);
-    k_update_pull<<<a.sel_grid, kBlock, 0, st>>>(u);
+    TCMIS_TIMED(ctx, "k_probe_pull", (k_probe_pull<<<a.sel_grid, kBlock, 0, st>>>(u)));
+    TCMIS_LAUNCHED(ctx);
+    TCMIS_TIMED(ctx, "k_update_pull", (k_update_pull<<<a.sel_grid, kBlock, 0, st>>>(u)));
   } else {
-    k_update<<<a.upd_grid, kBlock, 0, st>>>(u);
+    TCMIS_TIMED(ctx, "k_update", (k_update<<<a.upd_grid, kBlock, 0, st>>>(u)));
   }
-  TCMIS_LAUNCHED(g->ctx);
-  k_round_end<<<a.upd_grid, kBlock, 0, st>>>(u, cond, use_cond);
-  TCMIS_LAUNCHED(g->ctx);
+  TCMIS_LAUNCHED(ctx);
+  TCMIS_TIMED(ctx, "k_round_end", (k_round_end<<<a.upd_grid, kBlock, 0, st>>>(u, cond, use_cond)));
+  TCMIS_LAUNCHED(ctx);
   return 0;
 }
 
@@ -561,6 +599,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   const int seg_mode = !tiled ? 0 : (H == TCMIS_H3 ? 2 : 1);
   const bool timing = (cfg->flags & TCMIS_F_TIMING) != 0;
 
+  if (timing) timeline_begin(ctx);
   if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
   uint8_t *seg0 = seg_mode ? ws.segflag : nullptr;
   if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.key, nullptr, ws.state,
@@ -610,7 +649,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
 
   std::vector<DevRound> rounds_h;
   std::vector<uint8_t> h_next, h_state, h_cand;
-  std::vector<float> t1, t3;
+  std::vector<float> t1, t2, t3;  // per-round phase times (TCMIS_F_TIMING)
   bool step = cfg->observer || timing || (cfg->flags & TCMIS_F_HOST_LOOP);
   if (!step) {
     // the whole round loop is one CUDA graph: a conditional WHILE node whose
@@ -647,9 +686,8 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       ++round;
       if (round > g->n)  // engine.cpp:248-249
         return set_error(TCMIS_E_RUNTIME, "iteration cap exceeded; engine livelock");
-      if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[0], st));
+      ctx->rec_round = round;
       if (int rc = launch_select(g, a)) return rc;
-      if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[1], st));
       if (cfg->observer && H != TCMIS_H3) {
         // the select kernels already moved this round's candidates to InMIS;
         // the hook gets the states the candidates were generated against
@@ -666,41 +704,26 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       if (int rc = launch_update(g, a, 0, 0)) return rc;
       if (cfg->observer && H != TCMIS_H3)
         TCMIS_CUDA(cudaMemcpyAsync(h_state.data(), ws.state, g->n, cudaMemcpyDeviceToHost, st));
-      if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[2], st));
       TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
       DevRound dr;
       TCMIS_CUDA(cudaMemcpyAsync(&dr, ws.rounds + (round - 1) % ws.round_cap, sizeof(DevRound),
                                  cudaMemcpyDeviceToHost, st));
       TCMIS_CUDA(cudaStreamSynchronize(st));
       rounds_h.push_back(dr);
-      if (timing) {
-        float x = 0, y = 0;
-        cudaEventElapsedTime(&x, ctx->ev[0], ctx->ev[1]);
-        cudaEventElapsedTime(&y, ctx->ev[1], ctx->ev[2]);
-        t1.push_back(x);
-        t3.push_back(y);
-      }
       if (ws.h_ctrl->alive == 0) break;
       if (a.tail_thr > 0 && ws.h_ctrl->alive <= a.tail_thr) {
-        if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[0], st));
+        ctx->rec_round = round + 1;
         if (int rc = launch_tail(g, a)) return rc;
-        if (timing) TCMIS_CUDA(cudaEventRecord(ctx->ev[1], st));
         TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
         TCMIS_CUDA(cudaStreamSynchronize(st));
         const int rr = ws.h_ctrl->round - 1;
         if (rr - round > ws.round_cap)
           return set_error(TCMIS_E_RUNTIME, "round statistics capacity exceeded in k_tail");
-        float x = 0;
-        if (timing) cudaEventElapsedTime(&x, ctx->ev[0], ctx->ev[1]);
         for (int r = round; r < rr; ++r) {
           DevRound dr;
           TCMIS_CUDA(cudaMemcpy(&dr, ws.rounds + r % ws.round_cap, sizeof(DevRound),
                                 cudaMemcpyDeviceToHost));
           rounds_h.push_back(dr);
-          if (timing) {  // the tail's rounds share one launch: report it on the first
-            t1.push_back(r == round ? x : 0.f);
-            t3.push_back(0.f);
-          }
         }
         break;
       }
@@ -729,6 +752,23 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   }
   TCMIS_CUDA(cudaStreamSynchronize(st));
   *mis_count_out = h_mis_count;
+  if (timing) {
+    // Phase 1 = the select kernels, Phase 2 = the pull-form exclusion
+    // kernels (push-form exclusion is fused into Phase 1), Phase 3 = update;
+    // the tail kernel's rounds share one launch (reported on its first round)
+    timeline_end(ctx);
+    t1.assign(rounds_h.size(), 0.f);
+    t2.assign(rounds_h.size(), 0.f);
+    t3.assign(rounds_h.size(), 0.f);
+    for (const auto &k : ctx->timeline) {
+      const int r = k.round - 1;
+      if (r < 0 || r >= (int)rounds_h.size()) continue;
+      const std::string nm(k.name);
+      if (nm == "k_probe_pull" || nm == "k_update_pull") t2[r] += k.ms;
+      else if (nm == "k_update" || nm == "k_round_end") t3[r] += k.ms;
+      else t1[r] += k.ms;
+    }
+  }
 
   if (H == TCMIS_H3) {
     // engine.cpp:255-258: the h3 candidate vector is already the whole MIS,
@@ -750,6 +790,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     s.tiles_skipped = g->tile_total - (int64_t)h3_eval;
     for (size_t i = 0; i < t1.size(); ++i) {
       s.phase1_ms += t1[i];
+      s.phase2_ms += t2[i];
       s.phase3_ms += t3[i];
     }
     if (stats && max_stats > 0) stats[0] = s;
@@ -768,6 +809,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     s.tiles_skipped = (int64_t)d.skip;
     if (r < (int)t1.size()) {
       s.phase1_ms = t1[r];
+      s.phase2_ms = t2[r];
       s.phase3_ms = t3[r];
     }
     stats[r] = s;
