@@ -175,6 +175,28 @@ int tcmis_solve_device(tcmis_graph *g, const tcmis_config *cfg, const int32_t **
                        int64_t *mis_count, const uint8_t **d_state, tcmis_iter_stats *stats,
                        int32_t max_stats, int32_t *n_iterations);
 
+/* h1_random (priorities.cpp:33-41) without a graph: n priorities on the
+ * device of the context, copied to p_out[n]. */
+int tcmis_h1_random(tcmis_ctx *ctx, int32_t n, uint64_t seed, uint32_t *p_out);
+
+/* run_h3_resolution (engine.cpp:162-229): the greedy MIS of the alive subset
+ * of `states` under the priorities p, computed by the engine's rounds on the
+ * device; c_out[v] = 1 for the selected vertices. */
+int tcmis_h3_resolution(tcmis_graph *g, const uint32_t *p, const uint8_t *states,
+                        uint8_t *c_out);
+
+/* tiled_spmv (spmv.cpp:18-59) over a TiledAdjacency in the reference layout
+ * (host arrays, uploaded per call): nc = A * c with tile skipping, plus the
+ * tiles_evaluated / tiles_skipped counters.  exclusion selects the kernel:
+ * TCMIS_EXCL_TILE_BITS (popcount of row & segment on CUDA cores) or
+ * TCMIS_EXCL_TILE_MMA (T = 16 only: tiles x segment on the tensor cores via
+ * mma.sync m16n8k16 s8). */
+int tcmis_tiled_spmv_tiles(tcmis_ctx *ctx, int32_t n, int32_t tile_dim, int64_t tile_count,
+                           const int32_t *tile_col, const uint64_t *row_bits,
+                           const int64_t *block_row_offsets, const uint64_t *segment_bits,
+                           int32_t exclusion, int32_t *nc_out, int64_t *tiles_evaluated,
+                           int64_t *tiles_skipped);
+
 /* Phase-level helpers on the device (engine.hpp:71-106, spmv.hpp:15-42);
  * host buffers in, host buffers out, for parity tests of single phases. */
 int tcmis_compute_max_np(tcmis_graph *g, const uint32_t *p, const uint8_t *states,

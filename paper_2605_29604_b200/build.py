@@ -29,7 +29,7 @@ NVCC_FLAGS = ARCH + [
     "-Xcompiler", "-fPIC,-fvisibility=hidden,-ffp-contract=off",
     "-I", INC, "-I", CSRC,
 ] + os.environ.get("TCMIS_NVCC_EXTRA", "").split()
-CU_SOURCES = ["capi.cu", "solver.cu", "tiles.cu", "gen.cu"]
+CU_SOURCES = ["capi.cu", "solver.cu", "tiles.cu", "gen.cu", "tiled_spmv.cu"]
 CXX_SOURCES = ["engine.cpp"]
 
 
@@ -61,9 +61,9 @@ def _compile(src: str, verbose: bool) -> str:
     if not _stale(out, [src] + _headers()):
         return out
     cmd = [nvcc()] + NVCC_FLAGS + ["-c", src, "-o", out]
-    if src.endswith(".cpp"):
-        cmd = [nvcc(), "-x", "c++", "-O3", "-std=c++20", "-Xcompiler",
-               "-fPIC,-fvisibility=hidden,-ffp-contract=off", "-I", INC, "-c", src, "-o", out]
+    if src.endswith(".cpp"):  # host-only C++ (the drop-in API): plain g++
+        cmd = ["g++", "-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-I", INC, "-c", src,
+               "-o", out]
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)

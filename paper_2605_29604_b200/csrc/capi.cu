@@ -44,6 +44,12 @@ int gen_grid(tcmis_ctx *ctx, int32_t side, tcmis_graph **out);
 int gen_rgg(tcmis_ctx *ctx, int32_t n, uint64_t R, uint64_t seed, tcmis_graph **out);
 int gen_gnp_host(int32_t n, double avg_degree, uint64_t seed, int64_t **offsets,
                  int32_t **neighbors, int64_t *nnz_out);
+int h1_impl(tcmis_ctx *ctx, int32_t n, uint64_t seed, uint32_t *p_out);
+int h3_resolution_impl(tcmis_graph *g, const uint32_t *p, const uint8_t *states, uint8_t *c);
+int tiled_spmv_tiles_impl(tcmis_ctx *ctx, int32_t n, int32_t T, int64_t tiles,
+                          const int32_t *tile_col, const uint64_t *row_bits, const int64_t *bro,
+                          const uint64_t *seg, int32_t exclusion, int32_t *nc, int64_t *ev,
+                          int64_t *sk);
 
 int wrap_owned(tcmis_ctx *ctx, int32_t n, int64_t nnz, int64_t *d_off, int32_t *d_nbr,
                tcmis_graph **out) {
@@ -289,6 +295,31 @@ TCMIS_API int tcmis_solve_device(tcmis_graph *g, const tcmis_config *cfg, const 
   if (d_mis) *d_mis = g->ws.mis;
   if (d_state) *d_state = g->ws.state;
   return 0;
+}
+
+TCMIS_API int tcmis_h1_random(tcmis_ctx *ctx, int32_t n, uint64_t seed, uint32_t *p_out) {
+  NEED(ctx && (n < 1 || p_out), "null handle");
+  TCMIS_CUDA(cudaSetDevice(ctx->device));
+  return h1_impl(ctx, n, seed, p_out);
+}
+
+TCMIS_API int tcmis_h3_resolution(tcmis_graph *g, const uint32_t *p, const uint8_t *states,
+                                  uint8_t *c_out) {
+  NEED(g && (g->n == 0 || (p && states && c_out)), "null handle");
+  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  return h3_resolution_impl(g, p, states, c_out);
+}
+
+TCMIS_API int tcmis_tiled_spmv_tiles(tcmis_ctx *ctx, int32_t n, int32_t T, int64_t tiles,
+                                     const int32_t *tile_col, const uint64_t *row_bits,
+                                     const int64_t *bro, const uint64_t *seg, int32_t exclusion,
+                                     int32_t *nc, int64_t *ev, int64_t *sk) {
+  NEED(ctx && ev && sk, "null handle");
+  NEED(n == 0 || (bro && seg && nc), "null buffers");
+  NEED(tiles == 0 || (tile_col && row_bits), "null tile buffers");
+  TCMIS_CUDA(cudaSetDevice(ctx->device));
+  return tiled_spmv_tiles_impl(ctx, n, T, tiles, tile_col, row_bits, bro, seg, exclusion, nc, ev,
+                               sk);
 }
 
 TCMIS_API int tcmis_compute_max_np(tcmis_graph *g, const uint32_t *p, const uint8_t *states,

@@ -1,0 +1,438 @@
+// engine.cpp -- the C++ drop-in API (include/tcmis/tcmis.hpp) over the C-ABI.
+//
+// Each call that touches the graph uploads it to the device of a process-wide
+// context, runs the sm_100a kernels through tcmis_b200.h and maps the status
+// codes back onto the reference's exception types (SURVEY 8(b) "Errors").
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+
+#include "tcmis/tcmis.hpp"
+#include "tcmis_b200.h"
+
+namespace tcmis {
+inline namespace b200 {
+
+namespace {
+
+[[noreturn]] void raise(int code) {
+  const std::string msg = tcmis_last_error();
+  switch (code) {
+    case TCMIS_E_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case TCMIS_E_LOGIC: throw std::logic_error(msg);
+    case TCMIS_E_OUT_OF_RANGE: throw std::out_of_range(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+void check(int code) {
+  if (code != TCMIS_OK) raise(code);
+}
+
+tcmis_ctx *context() {
+  static std::once_flag once;
+  static tcmis_ctx *ctx = nullptr;
+  static int status = TCMIS_OK;
+  std::call_once(once, [] { status = tcmis_ctx_create(0, &ctx); });
+  if (status != TCMIS_OK) raise(status);
+  return ctx;
+}
+
+struct DeviceGraph {
+  tcmis_graph *h = nullptr;
+  explicit DeviceGraph(const Graph &g) {
+    check(tcmis_graph_upload(context(), g.n, g.offsets.empty() ? nullptr : g.offsets.data(),
+                             g.neighbors.empty() ? nullptr : g.neighbors.data(), &h));
+  }
+  ~DeviceGraph() { tcmis_graph_destroy(h); }
+  DeviceGraph(const DeviceGraph &) = delete;
+  DeviceGraph &operator=(const DeviceGraph &) = delete;
+};
+
+void check_tile_dim(int T) {  // tiling.cpp:17-21
+  if (T < 1 || T > 64)
+    throw std::invalid_argument("tile_dim must be in [1, 64], got " + std::to_string(T));
+}
+
+struct ObserverBridge {
+  const EngineConfig *cfg;
+  static void call(void *user, int32_t it, const uint8_t *c, const uint8_t *st, int32_t n) {
+    auto *self = static_cast<ObserverBridge *>(user);
+    self->cfg->iteration_observer(
+        it, std::span<const std::uint8_t>(c, static_cast<std::size_t>(n)),
+        std::span<const VertexState>(reinterpret_cast<const VertexState *>(st),
+                                     static_cast<std::size_t>(n)));
+  }
+};
+
+MISResult solve(tcmis_graph *g, VertexId n, const EngineConfig &cfg, Heuristic h) {
+  tcmis_config c;
+  tcmis_config_init(&c);
+  c.heuristic = static_cast<int32_t>(h);
+  c.tile_dim = cfg.tile_dim;
+  c.seed = cfg.seed;
+  c.scale_bits = cfg.scale_bits;
+  c.workers = cfg.workers;
+  ObserverBridge bridge{&cfg};
+  if (cfg.iteration_observer) {
+    c.observer = &ObserverBridge::call;
+    c.observer_user = &bridge;
+  }
+  MISResult r;
+  r.heuristic = h;
+  r.seed = cfg.seed;
+  std::vector<tcmis_iter_stats> st(4096);
+  std::vector<int32_t> mis(static_cast<std::size_t>(std::max<VertexId>(n, 1)));
+  int64_t cnt = 0;
+  int32_t nit = 0;
+  check(tcmis_solve(g, &c, nullptr, mis.data(), &cnt, st.data(), static_cast<int32_t>(st.size()),
+                    &nit));
+  if (nit > static_cast<int32_t>(st.size())) {  // pathological round counts: ask again
+    st.resize(static_cast<std::size_t>(nit));
+    check(tcmis_solve(g, &c, nullptr, mis.data(), &cnt, st.data(), nit, &nit));
+  }
+  r.mis.assign(mis.begin(), mis.begin() + cnt);
+  r.iterations.reserve(static_cast<std::size_t>(nit));
+  for (int32_t i = 0; i < nit; ++i) {
+    IterationStats s;
+    s.iteration = st[i].iteration;
+    s.candidates_selected = st[i].candidates_selected;
+    s.vertices_removed = st[i].vertices_removed;
+    s.alive_remaining = st[i].alive_remaining;
+    s.tiles_evaluated = st[i].tiles_evaluated;
+    s.tiles_skipped = st[i].tiles_skipped;
+    s.phase1_ms = st[i].phase1_ms;
+    s.phase2_ms = st[i].phase2_ms;
+    s.phase3_ms = st[i].phase3_ms;
+    r.iterations.push_back(s);
+  }
+  return r;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ graph
+
+bool Graph::has_edge(VertexId u, VertexId v) const {
+  auto row = neighbors_of(u);
+  return std::binary_search(row.begin(), row.end(), v);
+}
+
+Graph graph_from_edges(VertexId n, std::span<const std::pair<VertexId, VertexId>> edges) {
+  if (n < 0) throw std::invalid_argument("vertex count must be non-negative");
+  std::vector<std::uint64_t> keys;
+  keys.reserve(edges.size() * 2);
+  for (const auto &[u, v] : edges) {
+    if (u < 0 || u >= n || v < 0 || v >= n)
+      throw std::out_of_range("edge endpoint outside [0, n)");
+    if (u == v) continue;
+    keys.push_back((static_cast<std::uint64_t>(u) << 32) | static_cast<std::uint32_t>(v));
+    keys.push_back((static_cast<std::uint64_t>(v) << 32) | static_cast<std::uint32_t>(u));
+  }
+  std::sort(keys.begin(), keys.end());
+  keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+  Graph g;
+  g.n = n;
+  g.offsets.assign(static_cast<std::size_t>(n) + 1, 0);
+  g.neighbors.resize(keys.size());
+  for (std::size_t i = 0; i < keys.size(); ++i) {
+    g.offsets[(keys[i] >> 32) + 1]++;
+    g.neighbors[i] = static_cast<VertexId>(static_cast<std::uint32_t>(keys[i]));
+  }
+  for (VertexId v = 0; v < n; ++v) g.offsets[v + 1] += g.offsets[v];
+  return g;
+}
+
+// ------------------------------------------------------------- priorities
+
+std::uint64_t mix64(std::uint64_t x) {
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+std::uint64_t vertex_hash(std::uint64_t v, std::uint64_t seed) {
+  return mix64(mix64(seed) + (v + 1) * 0x9e3779b97f4a7c15ULL);
+}
+double hash_to_unit(std::uint64_t h) { return static_cast<double>(h >> 11) * 0x1.0p-53; }
+std::uint64_t combine_seed(std::uint64_t seed, std::uint64_t round) {
+  return mix64(seed + mix64(round + 0x9e3779b97f4a7c15ULL));
+}
+
+PriorityVector h1_random(VertexId n, std::uint64_t seed) {
+  if (n < 1) throw std::invalid_argument("h1_random requires n >= 1");
+  PriorityVector pv;
+  pv.seed = seed;
+  pv.p.resize(static_cast<std::size_t>(n));
+  check(tcmis_h1_random(context(), n, seed, pv.p.data()));
+  return pv;
+}
+
+std::uint32_t h2_priority_value(double avg, VertexId degree, double eps, int scale_bits) {
+  // priorities.cpp:43-51 (built with -ffp-contract=off: no fused operations)
+  double denom = avg + static_cast<double>(degree) - eps;
+  if (denom < 1.0 / 1024.0) denom = 1.0 / 1024.0;
+  const double scaled = std::floor(avg / denom * std::ldexp(1.0, scale_bits));
+  if (scaled < 0.0) return 0u;
+  if (scaled >= 4294967295.0) return 0xffffffffu;
+  return static_cast<std::uint32_t>(scaled);
+}
+
+PriorityVector h2_degree_aware(const Graph &g, std::uint64_t seed, int scale_bits) {
+  if (scale_bits < kMinScaleBits || scale_bits > kMaxScaleBits)
+    throw std::invalid_argument("scale_bits must be in [8, 30]");
+  PriorityVector pv;
+  pv.seed = seed;
+  pv.p.resize(static_cast<std::size_t>(g.n));
+  if (g.n == 0) return pv;
+  DeviceGraph dg(g);
+  check(tcmis_priorities(dg.h, TCMIS_H2, seed, scale_bits, pv.p.data()));
+  return pv;
+}
+
+// ----------------------------------------------------------------- tiling
+
+TiledAdjacency tile_graph(const Graph &g, int tile_dim) {
+  check_tile_dim(tile_dim);
+  TiledAdjacency a;
+  a.tile_dim = tile_dim;
+  a.n = g.n;
+  const std::int32_t nb = static_cast<std::int32_t>((static_cast<std::int64_t>(g.n) + tile_dim - 1) / tile_dim);
+  a.n_padded = nb * tile_dim;
+  a.block_row_offsets.assign(static_cast<std::size_t>(nb) + 1, 0);
+  if (g.n == 0) return a;
+  DeviceGraph dg(g);
+  int64_t count = 0;
+  check(tcmis_graph_tile(dg.h, tile_dim, &count));
+  a.tile_row.resize(static_cast<std::size_t>(count));
+  a.tile_col.resize(static_cast<std::size_t>(count));
+  a.row_bits.resize(static_cast<std::size_t>(count) * tile_dim);
+  check(tcmis_graph_export_tiles(dg.h, tile_dim, a.tile_row.data(), a.tile_col.data(),
+                                 a.row_bits.data(), a.block_row_offsets.data()));
+  return a;
+}
+
+TiledVector pack_vector(std::span<const std::uint8_t> values, int tile_dim) {
+  check_tile_dim(tile_dim);
+  TiledVector c;
+  c.tile_dim = tile_dim;
+  c.n = static_cast<VertexId>(values.size());
+  const std::int32_t ns = static_cast<std::int32_t>((static_cast<std::int64_t>(c.n) + tile_dim - 1) / tile_dim);
+  c.n_padded = ns * tile_dim;
+  c.values.assign(static_cast<std::size_t>(c.n_padded), 0);
+  std::copy(values.begin(), values.end(), c.values.begin());
+  c.segment_bits.assign(static_cast<std::size_t>(ns), 0);
+  for (VertexId k = 0; k < c.n; ++k)
+    if (values[k]) c.segment_bits[k / tile_dim] |= std::uint64_t{1} << (k % tile_dim);
+  return c;
+}
+
+// ------------------------------------------------------------------- spmv
+
+void tile_mma(std::span<const std::uint64_t> rows, std::uint64_t seg, std::span<std::int32_t> out) {
+  for (std::size_t i = 0; i < rows.size(); ++i)
+    out[i] += static_cast<std::int32_t>(__builtin_popcountll(rows[i] & seg));
+}
+
+std::vector<std::int32_t> tiled_spmv(const TiledAdjacency &a, const TiledVector &c,
+                                     const SpmvOptions &options, SpmvStats *stats) {
+  if (a.tile_dim != c.tile_dim || a.n_padded != c.n_padded || a.n != c.n)
+    throw std::invalid_argument("tiled adjacency and vector disagree on tile layout");
+  std::vector<std::int32_t> nc(static_cast<std::size_t>(a.n), 0);
+  int64_t ev = 0, sk = 0;
+  if (a.n > 0) {
+    // K4b on the CUDA cores (it beats the tensor-core form at
+    // every measured tile density); an all-zero segment contributes nothing,
+    // so without skipping every tile merely counts as evaluated
+    check(tcmis_tiled_spmv_tiles(context(), a.n, a.tile_dim, a.tile_count(), a.tile_col.data(),
+                                 a.row_bits.data(), a.block_row_offsets.data(),
+                                 c.segment_bits.data(), TCMIS_EXCL_TILE_BITS, nc.data(), &ev,
+                                 &sk));
+    if (!options.skip_empty_segments) {
+      ev += sk;
+      sk = 0;
+    }
+  }
+  if (stats) {
+    stats->tiles_evaluated = ev;
+    stats->tiles_skipped = sk;
+  }
+  return nc;
+}
+
+std::vector<std::int32_t> csr_neighbor_count_oracle(const Graph &g,
+                                                    std::span<const std::uint8_t> candidates) {
+  if (static_cast<VertexId>(candidates.size()) != g.n)
+    throw std::invalid_argument("candidate vector length must equal n");
+  std::vector<std::int32_t> nc(static_cast<std::size_t>(g.n), 0);
+  if (g.n == 0) return nc;
+  DeviceGraph dg(g);
+  check(tcmis_neighbor_count(dg.h, candidates.data(), nc.data()));
+  return nc;
+}
+
+// ----------------------------------------------------------------- engine
+
+const char *heuristic_name(Heuristic h) {
+  switch (h) {
+    case Heuristic::H1: return "h1";
+    case Heuristic::H2: return "h2";
+    case Heuristic::H3: return "h3";
+    case Heuristic::LubyFresh: return "luby-fresh";
+    case Heuristic::LubyPerm: return "luby-perm";
+  }
+  return "?";
+}
+
+Heuristic heuristic_from_name(const std::string &name) {
+  for (Heuristic h : {Heuristic::H1, Heuristic::H2, Heuristic::H3, Heuristic::LubyFresh,
+                      Heuristic::LubyPerm})
+    if (name == heuristic_name(h)) return h;
+  throw std::invalid_argument("unknown heuristic '" + name + "'");
+}
+
+double MISResult::phase1_ms() const {
+  double t = 0;
+  for (const auto &i : iterations) t += i.phase1_ms;
+  return t;
+}
+double MISResult::phase2_ms() const {
+  double t = 0;
+  for (const auto &i : iterations) t += i.phase2_ms;
+  return t;
+}
+double MISResult::phase3_ms() const {
+  double t = 0;
+  for (const auto &i : iterations) t += i.phase3_ms;
+  return t;
+}
+double MISResult::total_ms() const { return phase1_ms() + phase2_ms() + phase3_ms(); }
+std::int64_t MISResult::tiles_evaluated() const {
+  std::int64_t t = 0;
+  for (const auto &i : iterations) t += i.tiles_evaluated;
+  return t;
+}
+std::int64_t MISResult::tiles_skipped() const {
+  std::int64_t t = 0;
+  for (const auto &i : iterations) t += i.tiles_skipped;
+  return t;
+}
+
+std::vector<std::uint64_t> compute_max_np(const Graph &g, const PriorityVector &pv,
+                                          std::span<const VertexState> states, int) {
+  std::vector<std::uint64_t> out(static_cast<std::size_t>(g.n), kNoNeighborKey);
+  if (g.n == 0) return out;
+  DeviceGraph dg(g);
+  check(tcmis_compute_max_np(dg.h, pv.p.data(),
+                             reinterpret_cast<const std::uint8_t *>(states.data()), out.data()));
+  return out;
+}
+
+TiledVector generate_candidates(const PriorityVector &pv, std::span<const std::uint64_t> max_np,
+                                std::span<const VertexState> states, int tile_dim, int) {
+  const VertexId n = static_cast<VertexId>(states.size());
+  std::vector<std::uint8_t> c(static_cast<std::size_t>(n), 0);
+  for (VertexId v = 0; v < n; ++v)  // engine.cpp:105-119
+    c[v] = states[v] == VertexState::Alive && priority_key(pv, v) > max_np[v];
+  return pack_vector(c, tile_dim);
+}
+
+Phase3Outcome phase3_update(std::span<VertexState> states, std::span<const std::uint8_t> c,
+                            std::span<const std::int32_t> nc, std::vector<VertexId> *newly,
+                            int) {
+  const VertexId n = static_cast<VertexId>(states.size());
+  if (static_cast<VertexId>(c.size()) < n || static_cast<VertexId>(nc.size()) != n)
+    throw std::invalid_argument("phase3 input lengths must cover n");
+  Phase3Outcome o;
+  for (VertexId v = 0; v < n; ++v)  // engine.cpp:121-160
+    if (c[v] && states[v] != VertexState::Alive)
+      throw std::logic_error("candidate flagged on a non-alive vertex");
+  for (VertexId v = 0; v < n; ++v) {
+    if (c[v]) {
+      states[v] = VertexState::InMIS;
+      ++o.selected;
+      if (newly) newly->push_back(v);
+    } else if (states[v] == VertexState::Alive && nc[v] > 0) {
+      states[v] = VertexState::Removed;
+      ++o.removed;
+    }
+  }
+  return o;
+}
+
+std::vector<std::uint8_t> run_h3_resolution(const Graph &g, const PriorityVector &pv,
+                                            std::span<const VertexState> states, int) {
+  std::vector<std::uint8_t> c(static_cast<std::size_t>(g.n), 0);
+  if (g.n == 0) return c;
+  DeviceGraph dg(g);
+  check(tcmis_h3_resolution(dg.h, pv.p.data(),
+                            reinterpret_cast<const std::uint8_t *>(states.data()), c.data()));
+  return c;
+}
+
+MISResult run_tc_mis(const Graph &g, const TiledAdjacency &tiled, const EngineConfig &cfg) {
+  if (tiled.n != g.n)  // engine.cpp:233-234
+    throw std::invalid_argument("tiled adjacency built for a different graph");
+  MISResult r;
+  r.heuristic = cfg.heuristic;
+  r.seed = cfg.seed;
+  if (g.n == 0) return r;  // engine.cpp:240
+  if (cfg.heuristic != Heuristic::H1 && cfg.heuristic != Heuristic::H2 &&
+      cfg.heuristic != Heuristic::H3)  // engine.cpp:29-31
+    throw std::invalid_argument("tiled engine only runs h1/h2/h3; use run_luby_reference");
+  if (cfg.heuristic != Heuristic::H1 &&
+      (cfg.scale_bits < kMinScaleBits || cfg.scale_bits > kMaxScaleBits))
+    throw std::invalid_argument("scale_bits must be in [8, 30]");
+  check_tile_dim(cfg.tile_dim);  // pack_vector(cfg.tile_dim)
+  if (tiled.tile_dim != cfg.tile_dim)  // spmv.cpp:22-24, raised in round 1
+    throw std::invalid_argument("tiled adjacency and vector disagree on tile layout");
+  DeviceGraph dg(g);
+  check(tcmis_graph_set_tiling(dg.h, tiled.tile_dim, tiled.block_row_offsets.data(),
+                               tiled.n_block_rows()));
+  return solve(dg.h, g.n, cfg, cfg.heuristic);
+}
+
+MISResult run_tc_mis(const Graph &g, const EngineConfig &cfg) {
+  check_tile_dim(cfg.tile_dim);  // tile_graph runs first (engine.cpp:297-299)
+  MISResult r;
+  r.heuristic = cfg.heuristic;
+  r.seed = cfg.seed;
+  if (g.n == 0) return r;
+  if (cfg.heuristic != Heuristic::H1 && cfg.heuristic != Heuristic::H2 &&
+      cfg.heuristic != Heuristic::H3)
+    throw std::invalid_argument("tiled engine only runs h1/h2/h3; use run_luby_reference");
+  DeviceGraph dg(g);
+  return solve(dg.h, g.n, cfg, cfg.heuristic);  // tiling derived on the device
+}
+
+MISResult run_luby_reference(const Graph &g, std::uint64_t seed, LubyMode mode, int scale_bits,
+                             int workers) {
+  EngineConfig cfg;
+  cfg.seed = seed;
+  cfg.scale_bits = scale_bits;
+  cfg.workers = workers;
+  const Heuristic h = mode == LubyMode::Fresh ? Heuristic::LubyFresh : Heuristic::LubyPerm;
+  cfg.heuristic = h;
+  MISResult r;
+  r.heuristic = h;
+  r.seed = seed;
+  if (g.n == 0) return r;  // engine.cpp:307
+  DeviceGraph dg(g);
+  return solve(dg.h, g.n, cfg, h);
+}
+
+MISResult run_mis(const Graph &g, const EngineConfig &cfg) {  // engine.cpp:354-365
+  switch (cfg.heuristic) {
+    case Heuristic::LubyFresh:
+      return run_luby_reference(g, cfg.seed, LubyMode::Fresh, cfg.scale_bits, cfg.workers);
+    case Heuristic::LubyPerm:
+      return run_luby_reference(g, cfg.seed, LubyMode::Permutation, cfg.scale_bits,
+                                cfg.workers);
+    default:
+      return run_tc_mis(g, cfg);
+  }
+}
+
+}  // namespace b200
+}  // namespace tcmis

@@ -91,6 +91,31 @@ __global__ void k_max_degree(int32_t n, const int64_t *__restrict__ off,
   if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
 }
 
+__global__ void k_h1(int32_t n, uint64_t mseed, uint32_t *__restrict__ p) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    p[v] = (uint32_t)(vertex_hash_m((uint64_t)v, mseed) >> 32);  // priorities.cpp:33-41
+}
+
+// run_h3_resolution start state: only the alive vertices of `states` take
+// part (everyone else is Removed, key 0 = invisible)
+__global__ void k_resolve_init(int32_t n, const uint32_t *__restrict__ p,
+                               const uint8_t *__restrict__ states, uint64_t *__restrict__ key,
+                               uint8_t *__restrict__ state, uint8_t *__restrict__ next) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const bool alive = states[v] == TCMIS_ALIVE;
+    key[v] = alive ? (((uint64_t)p[v] << 32) | (uint64_t)(v + 1)) : 0;
+    state[v] = alive ? TCMIS_ALIVE : TCMIS_REMOVED;
+    next[v] = 0;
+  }
+}
+
+struct IsAliveIn {
+  const uint8_t *states;
+  __device__ __forceinline__ bool operator()(int32_t v) const { return states[v] == TCMIS_ALIVE; }
+};
+
 struct HasEdges {
   const int64_t *off;
   __device__ __forceinline__ bool operator()(int32_t v) const { return off[v + 1] > off[v]; }
@@ -598,6 +623,10 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   const int32_t nseg = tiled ? g->tile_nb : 0;
   const int seg_mode = !tiled ? 0 : (H == TCMIS_H3 ? 2 : 1);
   const bool timing = (cfg->flags & TCMIS_F_TIMING) != 0;
+  // run_luby_reference never calls the hook (engine.cpp:301-352)
+  tcmis_config cfg_local = *cfg;
+  if (!tiled) cfg_local.observer = nullptr;
+  cfg = &cfg_local;
 
   if (timing) timeline_begin(ctx);
   if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
@@ -913,6 +942,102 @@ int neighbor_count_impl(tcmis_graph *g, const uint8_t *c, int32_t *nc, int T, in
   }
   cudaFree(d_c);
   cudaFree(d_nc);
+  return rc;
+}
+
+}  // namespace tcmis_b200
+
+namespace tcmis_b200 {
+
+int h1_impl(tcmis_ctx *ctx, int32_t n, uint64_t seed, uint32_t *p_out) {
+  if (n < 1) return set_error(TCMIS_E_INVALID_ARGUMENT, "h1_random requires n >= 1");
+  uint32_t *d_p = nullptr;
+  if (int rc = dev_alloc(&d_p, (size_t)n)) return rc;
+  k_h1<<<grid_for(ctx, n, 256, 16), 256, 0, ctx->stream>>>(n, mix64(seed), d_p);
+  ctx->launches++;
+  cudaError_t e = cudaMemcpyAsync(p_out, d_p, 4ull * n, cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(d_p);
+  if (e != cudaSuccess) return cuda_error(e, "h1_random");
+  return 0;
+}
+
+// engine.cpp:162-229 run_h3_resolution: the rounds of the engine from the
+// given alive set, without statistics.  The selected set is the greedy MIS
+// of the alive subgraph in (p, id) order.
+int h3_resolution_impl(tcmis_graph *g, const uint32_t *p, const uint8_t *states, uint8_t *c) {
+  if (g->n == 0) return 0;
+  tcmis_ctx *ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  if (int rc = ensure_workspace(g)) return rc;
+  Workspace &ws = g->ws;
+  uint32_t *d_p = nullptr;
+  uint8_t *d_s = nullptr;
+  int64_t *d_cnt = nullptr;
+  int rc = dev_alloc(&d_p, g->n);
+  if (!rc) rc = dev_alloc(&d_s, g->n);
+  if (!rc) rc = dev_alloc(&d_cnt, 1);
+  int64_t alive = 0;
+  if (!rc) {
+    cudaMemcpyAsync(d_p, p, 4ull * g->n, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_s, states, g->n, cudaMemcpyHostToDevice, st);
+    k_resolve_init<<<grid_for(ctx, g->n, 256, 16), 256, 0, st>>>(g->n, d_p, d_s, ws.key, ws.state,
+                                                                ws.next);
+    ctx->launches++;
+    thrust::counting_iterator<int32_t> ids(0);
+    size_t bytes = ws.cub_bytes;
+    cudaError_t e = cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.wl[0], d_cnt, (int)g->n,
+                                          IsAliveIn{d_s}, st);
+    ctx->launches++;
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(&alive, d_cnt, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = cuda_error(e, "h3 resolution setup");
+  }
+  if (!rc && alive > 0) {
+    // start at "round 2" so the first round reads worklist slot 0
+    Ctrl c0{};
+    c0.round = 2;
+    c0.wl_count[0] = (int32_t)alive;
+    c0.alive = (int32_t)alive;
+    c0.max_rounds = ws.round_cap;
+    *ws.h_ctrl = c0;
+    cudaMemcpyAsync(ws.ctrl, ws.h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st);
+    RoundArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.n = g->n;
+    a.off = g->d_off;
+    a.nbr = g->d_nbr;
+    a.vnnz = ((uintptr_t)g->d_nbr & 15) == 0 ? g->nnz : -g->nnz;
+    a.T = 1;
+    a.sel_grid = ctx->num_sms * 8;
+    a.upd_grid = ctx->num_sms * 4;
+    a.nz = g->d_nz;
+    a.nz_count = g->nz_count;
+    a.pull = (double)g->max_degree > 64.0 * std::max(1.0, avg_degree(g)) ? 1 : 0;
+    for (int round = 0; !rc; ++round) {
+      if (round > g->n) {
+        rc = set_error(TCMIS_E_LOGIC, "pending set stopped shrinking");  // engine.cpp:224-225
+        break;
+      }
+      rc = launch_select(g, a);
+      if (!rc) rc = launch_update(g, a, 0, 0);
+      if (rc) break;
+      cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st);
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) rc = cuda_error(e, "h3 resolution");
+      if (ws.h_ctrl->alive == 0) break;
+    }
+  }
+  if (!rc) {
+    std::vector<uint8_t> fin(g->n);
+    cudaError_t e = cudaMemcpy(fin.data(), ws.state, g->n, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = cuda_error(e, "h3 resolution result");
+    for (int32_t v = 0; v < g->n && !rc; ++v) c[v] = fin[v] == TCMIS_IN_MIS ? 1 : 0;
+  }
+  cudaFree(d_p);
+  cudaFree(d_s);
+  cudaFree(d_cnt);
   return rc;
 }
 

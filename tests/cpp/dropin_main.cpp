@@ -1,0 +1,104 @@
+// dropin_main.cpp -- a C++ program written against the reference's public
+// API (tcmis/engine.hpp & co.), linked against the B200 drop-in libtcmis.so.
+// Reads a CSR graph (binary: int32 n, int64 nnz, int64 offsets[n+1], int32
+// neighbors[nnz]) and prints one JSON object per (heuristic, seed) run plus
+// the exception checks, for tests/test_gpu_dropin.py to compare with the
+// oracle.
+#include <cstdio>
+#include <fstream>
+#include <stdexcept>
+#include <string>
+
+#include "tcmis/engine.hpp"
+#include "tcmis/tiling.hpp"
+
+using namespace tcmis;
+
+static Graph read_graph(const char *path) {
+  std::ifstream in(path, std::ios::binary);
+  Graph g;
+  int64_t nnz = 0;
+  in.read(reinterpret_cast<char *>(&g.n), 4);
+  in.read(reinterpret_cast<char *>(&nnz), 8);
+  g.offsets.resize(static_cast<size_t>(g.n) + 1);
+  g.neighbors.resize(static_cast<size_t>(nnz));
+  in.read(reinterpret_cast<char *>(g.offsets.data()), 8 * (g.n + 1));
+  in.read(reinterpret_cast<char *>(g.neighbors.data()), 4 * nnz);
+  return g;
+}
+
+static uint64_t fnv(const std::vector<VertexId> &v) {
+  uint64_t h = 0xcbf29ce484222325ULL;
+  for (VertexId x : v) {
+    h ^= static_cast<uint32_t>(x);
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}
+
+template <typename E, typename F>
+static const char *throws(F f) {
+  try {
+    f();
+  } catch (const E &) {
+    return "yes";
+  } catch (...) {
+    return "other";
+  }
+  return "no";
+}
+
+int main(int argc, char **argv) {
+  Graph g = read_graph(argv[1]);
+  for (const char *name : {"h1", "h2", "h3", "luby-fresh", "luby-perm"}) {
+    for (uint64_t seed : {1ull, 7ull}) {
+      EngineConfig cfg;
+      cfg.heuristic = heuristic_from_name(name);
+      cfg.seed = seed;
+      int observed = 0;
+      cfg.iteration_observer = [&](int, std::span<const std::uint8_t>,
+                                   std::span<const VertexState>) { ++observed; };
+      MISResult r = run_mis(g, cfg);
+      std::printf("{\"heuristic\": \"%s\", \"seed\": %llu, \"size\": %lld, \"mis_fnv\": %llu, "
+                  "\"observed\": %d, \"rounds\": [",
+                  name, (unsigned long long)seed, (long long)r.cardinality(),
+                  (unsigned long long)fnv(r.mis), observed);
+      for (size_t i = 0; i < r.iterations.size(); ++i) {
+        const auto &it = r.iterations[i];
+        std::printf("%s[%lld, %lld, %lld, %lld, %lld]", i ? ", " : "",
+                    (long long)it.candidates_selected, (long long)it.vertices_removed,
+                    (long long)it.alive_remaining, (long long)it.tiles_evaluated,
+                    (long long)it.tiles_skipped);
+      }
+      std::printf("]}\n");
+    }
+  }
+  // prebuilt-tiles overload with T = 8
+  TiledAdjacency t8 = tile_graph(g, 8);
+  EngineConfig c8;
+  c8.heuristic = Heuristic::H2;
+  c8.tile_dim = 8;
+  MISResult r8 = run_tc_mis(g, t8, c8);
+  std::printf("{\"tiles8\": %lld, \"t8_rounds\": %zu, \"t8_eval1\": %lld}\n",
+              (long long)t8.tile_count(), r8.iterations.size(),
+              (long long)(r8.iterations.empty() ? 0 : r8.iterations[0].tiles_evaluated));
+  // reference error behaviour
+  EngineConfig bad;
+  bad.tile_dim = 0;
+  EngineConfig luby;
+  luby.heuristic = Heuristic::LubyPerm;
+  EngineConfig sb;
+  sb.heuristic = Heuristic::H2;
+  sb.scale_bits = 31;
+  std::printf("{\"bad_tile\": \"%s\", \"luby_tiled\": \"%s\", \"bad_scale\": \"%s\", "
+              "\"bad_name\": \"%s\", \"edge_range\": \"%s\"}\n",
+              throws<std::invalid_argument>([&] { run_mis(g, bad); }),
+              throws<std::invalid_argument>([&] { run_tc_mis(g, luby); }),
+              throws<std::invalid_argument>([&] { run_mis(g, sb); }),
+              throws<std::invalid_argument>([&] { heuristic_from_name("h9"); }),
+              throws<std::out_of_range>([&] {
+                std::pair<VertexId, VertexId> e[1] = {{0, g.n}};
+                graph_from_edges(g.n, e);
+              }));
+  return 0;
+}

@@ -1,0 +1,66 @@
+"""GPU: a C++ program written against the reference's public headers
+(tests/cpp/dropin_main.cpp), compiled against include/tcmis/*.hpp and linked
+with libtcmis.so, gives the reference's results (checked with the oracle)."""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+PKG = os.path.join(ROOT, "paper_2605_29604_b200")
+
+
+def fnv_ids(ids):
+    h = 0xcbf29ce484222325
+    for x in ids.tolist():
+        h ^= x & 0xFFFFFFFF
+        h = (h * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+@pytest.fixture(scope="module")
+def dropin(tmp_path_factory):
+    d = tmp_path_factory.mktemp("dropin")
+    exe = str(d / "dropin")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "dropin_main.cpp"), "-L", PKG, "-ltcmis",
+                    "-ltcmis_b200", f"-Wl,-rpath,{PKG}", "-o", exe], check=True)
+    return exe, d
+
+
+@pytest.mark.parametrize("kind,args", [("rmat", (12, 16, 2)), ("gnp_avg", (3000, 10.0, 5)),
+                                       ("grid", (30,))])
+def test_cpp_dropin_matches_reference(dropin, kind, args):
+    exe, d = dropin
+    g = O.gen(kind, *args)
+    path = str(d / f"{kind}.bin")
+    with open(path, "wb") as f:
+        f.write(np.int32(g.n).tobytes())
+        f.write(np.int64(g.nbr.size).tobytes())
+        f.write(g.off.astype(np.int64).tobytes())
+        f.write(g.nbr.astype(np.int32).tobytes())
+    out = subprocess.run([exe, path], capture_output=True, text=True, check=True).stdout
+    lines = [json.loads(x) for x in out.strip().splitlines()]
+    runs = [x for x in lines if "heuristic" in x]
+    assert len(runs) == 10
+    for r in runs:
+        exp = O.solve(g, r["heuristic"], r["seed"], tile_dim=16)
+        assert r["size"] == exp.mis.size
+        assert r["mis_fnv"] == fnv_ids(exp.mis)
+        assert r["rounds"] == [[x["sel"], x["rem"], x["alive"], x["tiles_eval"], x["tiles_skip"]]
+                               for x in exp.rounds]
+        want_obs = {"h1": exp.n_rounds, "h2": exp.n_rounds, "h3": 1, "luby-fresh": 0,
+                    "luby-perm": 0}[r["heuristic"]]
+        assert r["observed"] == want_obs
+    t8 = [x for x in lines if "tiles8" in x][0]
+    assert t8["tiles8"] == int(O.tile_row_counts(g, 8).sum())
+    e8 = O.solve(g, "h2", 1, tile_dim=8)
+    assert t8["t8_rounds"] == e8.n_rounds and t8["t8_eval1"] == e8.rounds[0]["tiles_eval"]
+    errs = [x for x in lines if "bad_tile" in x][0]
+    assert all(v == "yes" for v in errs.values()), errs

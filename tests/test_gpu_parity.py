@@ -357,3 +357,37 @@ def test_tail_threshold_invariance(ctx, thr, monkeypatch):
                                                          exclusion=excl, host_loop=host_loop))
                     assert np.array_equal(got.mis, exp.mis), (kind, heur, excl, host_loop)
                     assert rounds_tuple(got.iterations) == oracle_tuple(exp)
+
+
+@pytest.mark.parametrize("excl", ["bits", "mma"])
+@pytest.mark.parametrize("T", [4, 16, 33, 64])
+def test_tile_kernels_match_tiled_spmv(ctx, excl, T):
+    """K4b (popcount on CUDA cores) and K4c (mma.sync s8 on tensor cores, T=16)
+    reproduce tiled_spmv's counts and tile counters (spmv.cpp:18-59)."""
+    if excl == "mma" and T != 16:
+        pytest.skip("tensor-core tile kernel is T=16 only")
+    import ctypes as C
+    L = tc.load()
+    L.tcmis_tiled_spmv_tiles.restype = C.c_int
+    L.tcmis_tiled_spmv_tiles.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int64] + \
+        [C.c_void_p] * 4 + [C.c_int32, C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    rng = np.random.default_rng(T)
+    for g in (O.gen("rmat", 11, 16, 2), O.gen("grid", 40), O.gen("gnp_avg", 2000, 30.0, 1)):
+        tr, tcol, rb, bro = O.tile_graph(g, T)
+        for dens in (0.0, 0.05, 0.5):
+            c = (rng.random(g.n) < dens).astype(np.uint8)
+            seg = np.zeros((g.n + T - 1) // T, np.uint64)
+            O.lib().orc_pack_segments(g.n, c, T, seg)
+            nc = np.zeros(g.n, np.int32)
+            ev, sk = O.C.c_int64(), O.C.c_int64()
+            O.lib().orc_tiled_spmv(g.n, T, tcol.size, tcol, rb, bro, seg, nc, O.C.byref(ev),
+                                   O.C.byref(sk))
+            got = np.zeros(g.n, np.int32)
+            gev, gsk = C.c_int64(), C.c_int64()
+            mode = tc.Exclusion.TILE_MMA if excl == "mma" else tc.Exclusion.TILE_BITS
+            rc = L.tcmis_tiled_spmv_tiles(ctx.h, g.n, T, tcol.size, tcol.ctypes.data,
+                                          rb.ctypes.data, bro.ctypes.data, seg.ctypes.data,
+                                          int(mode), got.ctypes.data, C.byref(gev), C.byref(gsk))
+            assert rc == 0, L.tcmis_last_error()
+            assert np.array_equal(got, nc)
+            assert (gev.value, gsk.value) == (ev.value, sk.value)
