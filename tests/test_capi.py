@@ -49,8 +49,10 @@ def test_cxx_dropin_library_exports_engine_api():
     names = subprocess.run(["nm", "-DC", "--defined-only", lib], capture_output=True, text=True,
                            check=True).stdout
     for sym in ("tcmis::run_mis(", "tcmis::run_tc_mis(", "tcmis::tile_graph(",
-                "tcmis::h2_degree_aware(", "tcmis::h1_random(", "tcmis::compute_max_np(",
-                "tcmis::tiled_spmv(", "tcmis::phase3_update(", "tcmis::run_h3_resolution("):
+                "tcmis::b200::h2_degree_aware(", "tcmis::b200::h1_random(",
+                "tcmis::b200::compute_max_np(",
+                "tcmis::b200::tiled_spmv(", "tcmis::b200::phase3_update(",
+                "tcmis::b200::run_h3_resolution("):
         assert sym in names, sym
 
 
