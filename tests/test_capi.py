@@ -48,7 +48,7 @@ def test_cxx_dropin_library_exports_engine_api():
         pytest.skip("libtcmis.so not built")
     names = subprocess.run(["nm", "-DC", "--defined-only", lib], capture_output=True, text=True,
                            check=True).stdout
-    for sym in ("tcmis::run_mis(", "tcmis::run_tc_mis(", "tcmis::tile_graph(",
+    for sym in ("tcmis::b200::run_mis(", "tcmis::b200::run_tc_mis(", "tcmis::b200::tile_graph(",
                 "tcmis::b200::h2_degree_aware(", "tcmis::b200::h1_random(",
                 "tcmis::b200::compute_max_np(",
                 "tcmis::b200::tiled_spmv(", "tcmis::b200::phase3_update(",
