@@ -175,6 +175,32 @@ int tcmis_solve_device(tcmis_graph *g, const tcmis_config *cfg, const int32_t **
                        int64_t *mis_count, const uint8_t **d_state, tcmis_iter_stats *stats,
                        int32_t max_stats, int32_t *n_iterations);
 
+/* Row-partitioned multi-GPU solve (host driver in
+ * paper_2605_29604_b200/distributed.py).  Rank r uploads its rows [lo, hi)
+ * with the full offsets (n+1, for global degrees) and the neighbour lists of
+ * its rows (full_offsets[hi] - full_offsets[lo] ids).  Per round:
+ *   tcmis_dist_select  -> own candidates as bitmap slice d_bits (bit v - lo)
+ *   (host all-gathers the slices, rank r's at word r * maxw)
+ *   tcmis_dist_apply(what = 0) -> remote candidates marked
+ *   tcmis_dist_update  -> own removals as bitmap slice; counts[5] = this
+ *                         rank's (selected, removed, alive, tiles_eval, tiles_skip)
+ *   (host all-gathers, all-reduces the counts)
+ *   tcmis_dist_apply(what = 1) -> remote removals applied
+ * until the all-reduced alive count is 0; tcmis_dist_state copies the own
+ * range's VertexStates.  rank_lo has world + 1 entries (rank_lo[world] = n). */
+int tcmis_graph_upload_partition(tcmis_ctx *ctx, int32_t n, int32_t lo, int32_t hi,
+                                 const int64_t *full_offsets, const int32_t *row_neighbors,
+                                 tcmis_graph **out);
+int tcmis_dist_begin(tcmis_graph *g, const tcmis_config *cfg);
+int tcmis_dist_select(tcmis_graph *g, uint32_t *d_bits, int32_t words);
+int tcmis_dist_apply(tcmis_graph *g, const uint32_t *d_gathered, const int32_t *rank_lo,
+                     int32_t world, int32_t maxw, int32_t me, int32_t what);
+int tcmis_dist_update(tcmis_graph *g, uint32_t *d_bits, int32_t words, int64_t *counts);
+int tcmis_dist_state(tcmis_graph *g, uint8_t *own_state);
+/* h3 on a partition: after the rounds, this rank's share of the collapsed
+ * iteration's tiles_evaluated and its tile total (sum over ranks on the host). */
+int tcmis_dist_h3_tiles(tcmis_graph *g, int64_t *tiles_evaluated, int64_t *tile_total);
+
 /* h1_random (priorities.cpp:33-41) without a graph: n priorities on the
  * device of the context, copied to p_out[n]. */
 int tcmis_h1_random(tcmis_ctx *ctx, int32_t n, uint64_t seed, uint32_t *p_out);

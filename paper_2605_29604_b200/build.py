@@ -29,7 +29,7 @@ NVCC_FLAGS = ARCH + [
     "-Xcompiler", "-fPIC,-fvisibility=hidden,-ffp-contract=off",
     "-I", INC, "-I", CSRC,
 ] + os.environ.get("TCMIS_NVCC_EXTRA", "").split()
-CU_SOURCES = ["capi.cu", "solver.cu", "tiles.cu", "gen.cu", "tiled_spmv.cu"]
+CU_SOURCES = ["capi.cu", "solver.cu", "tiles.cu", "gen.cu", "tiled_spmv.cu", "dist.cu"]
 CXX_SOURCES = ["engine.cpp"]
 
 

@@ -45,6 +45,15 @@ int gen_rgg(tcmis_ctx *ctx, int32_t n, uint64_t R, uint64_t seed, tcmis_graph **
 int gen_gnp_host(int32_t n, double avg_degree, uint64_t seed, int64_t **offsets,
                  int32_t **neighbors, int64_t *nnz_out);
 int h1_impl(tcmis_ctx *ctx, int32_t n, uint64_t seed, uint32_t *p_out);
+int upload_partition(tcmis_ctx *ctx, int32_t n, int32_t lo, int32_t hi, const int64_t *full,
+                     const int32_t *rows, tcmis_graph **out);
+int dist_begin(tcmis_graph *g, const tcmis_config *cfg);
+int dist_select(tcmis_graph *g, uint32_t *d_bits, int32_t words);
+int dist_apply(tcmis_graph *g, const uint32_t *d_gathered, const int32_t *h_rank_lo,
+               int32_t world, int32_t maxw, int32_t me, int32_t what);
+int dist_update(tcmis_graph *g, uint32_t *d_bits, int32_t words, int64_t *counts);
+int dist_state_out(tcmis_graph *g, uint8_t *own_state);
+int dist_h3_tiles(tcmis_graph *g, int64_t *ev, int64_t *total);
 int h3_resolution_impl(tcmis_graph *g, const uint32_t *p, const uint8_t *states, uint8_t *c);
 int tiled_spmv_tiles_impl(tcmis_ctx *ctx, int32_t n, int32_t T, int64_t tiles,
                           const int32_t *tile_col, const uint64_t *row_bits, const int64_t *bro,
@@ -192,6 +201,7 @@ TCMIS_API void tcmis_graph_destroy(tcmis_graph *g) {
   }
   cudaFree(g->d_rowtiles);
   cudaFree(g->d_nz);
+  cudaFree(g->d_off_full);
   free_workspace(g->ws);
   delete g;
 }
@@ -295,6 +305,56 @@ TCMIS_API int tcmis_solve_device(tcmis_graph *g, const tcmis_config *cfg, const 
   if (d_mis) *d_mis = g->ws.mis;
   if (d_state) *d_state = g->ws.state;
   return 0;
+}
+
+TCMIS_API int tcmis_graph_upload_partition(tcmis_ctx *ctx, int32_t n, int32_t lo, int32_t hi,
+                                           const int64_t *full_offsets,
+                                           const int32_t *row_neighbors, tcmis_graph **out) {
+  NEED(ctx && out && full_offsets, "null handle");
+  NEED(n >= 0, "vertex count must be non-negative");
+  TCMIS_CUDA(cudaSetDevice(ctx->device));
+  return upload_partition(ctx, n, lo, hi, full_offsets, row_neighbors, out);
+}
+
+TCMIS_API int tcmis_dist_begin(tcmis_graph *g, const tcmis_config *cfg) {
+  NEED(g && cfg, "null handle");
+  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  return dist_begin(g, cfg);
+}
+
+TCMIS_API int tcmis_dist_select(tcmis_graph *g, uint32_t *d_bits, int32_t words) {
+  NEED(g && d_bits, "null handle");
+  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  return dist_select(g, d_bits, words);
+}
+
+TCMIS_API int tcmis_dist_apply(tcmis_graph *g, const uint32_t *d_gathered,
+                               const int32_t *rank_lo, int32_t world, int32_t maxw, int32_t me,
+                               int32_t what) {
+  NEED(g && d_gathered && rank_lo, "null handle");
+  NEED(world >= 1 && me >= 0 && me < world && maxw >= 0, "bad rank layout");
+  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  return dist_apply(g, d_gathered, rank_lo, world, maxw, me, what);
+}
+
+TCMIS_API int tcmis_dist_update(tcmis_graph *g, uint32_t *d_bits, int32_t words,
+                                int64_t *counts) {
+  NEED(g && d_bits && counts, "null handle");
+  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  return dist_update(g, d_bits, words, counts);
+}
+
+TCMIS_API int tcmis_dist_state(tcmis_graph *g, uint8_t *own_state) {
+  NEED(g, "null handle");
+  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  return dist_state_out(g, own_state);
+}
+
+TCMIS_API int tcmis_dist_h3_tiles(tcmis_graph *g, int64_t *tiles_evaluated,
+                                  int64_t *tile_total) {
+  NEED(g && tiles_evaluated && tile_total, "null handle");
+  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  return dist_h3_tiles(g, tiles_evaluated, tile_total);
 }
 
 TCMIS_API int tcmis_h1_random(tcmis_ctx *ctx, int32_t n, uint64_t seed, uint32_t *p_out) {

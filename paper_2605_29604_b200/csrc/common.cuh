@@ -58,6 +58,17 @@ __device__ __forceinline__ void mark_candidate(int32_t v, uint8_t *next, uint8_t
   if (segflag) segflag[v / T] = 1;
 }
 
+// Multi-GPU: a rank publishes its own range's decisions as a bitmap slice
+// (bit v - lo) that the host allgathers over NCCL (distributed.py).
+struct Publish {
+  uint32_t *bits;  // null on a single GPU
+  int32_t lo;
+};
+
+__device__ __forceinline__ void publish(const Publish &p, int32_t v) {
+  if (p.bits) atomicOr(&p.bits[(uint32_t)(v - p.lo) >> 5], 1u << ((uint32_t)(v - p.lo) & 31u));
+}
+
 // An alive non-candidate with a candidate neighbour is removed
 // (engine.cpp:144-147); key 0 == kNoNeighborKey makes it invisible to the
 // alive vertices that still neighbour it.

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -131,6 +132,11 @@ struct tcmis_graph {
   int32_t *d_nz = nullptr;  // ascending ids of non-isolated vertices (round-1 select list)
   int32_t nz_count = 0;
   int64_t max_degree = 0;
+  // row partition of a multi-GPU solve (distributed.py): this rank's CSR
+  // holds rows [part_lo, part_hi) only; priorities need the full degrees
+  int32_t part_lo = 0, part_hi = -1;  // part_hi < 0: not partitioned
+  int64_t *d_off_full = nullptr;
+  int64_t nnz_global = -1;
   tcmis_b200::Workspace ws;
 };
 
@@ -177,6 +183,36 @@ cudaEvent_t pool_event(tcmis_ctx *ctx);
       (ctx)->marks.push_back({kname, (ctx)->rec_round, _a, _b});              \
     }                                                                         \
   } while (0)
+
+// the per-round kernel launches (solver.cu), shared with the multi-GPU driver
+struct RoundArgs {
+  int32_t n;
+  const int64_t *off;
+  const int32_t *nbr;
+  int T, seg_mode, fresh;
+  int32_t nseg;
+  int64_t total_tiles;
+  const int32_t *rowtiles;
+  uint64_t seed;
+  int sel_grid, upd_grid;
+  int pull;             // exclusion form: 0 push (in k_select), 1 pull (in k_update_pull)
+  int32_t nz_count;     // round-1 select list
+  const int32_t *nz;
+  int32_t tail_thr;     // rounds start in k_tail once alive <= tail_thr
+  int64_t vnnz;         // nnz, negated when the neighbour array is not 16-byte aligned
+  uint32_t *pub_cand;   // multi-GPU publish slices (null on one GPU)
+  uint32_t *pub_dead;
+  int32_t pub_lo;
+  int tail_grid;
+  bool operator==(const RoundArgs &o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
+};
+
+int launch_select(tcmis_graph *g, const RoundArgs &a);
+int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle cond, int use_cond);
+int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
+                      uint64_t *key, uint32_t *p_out, uint8_t *state, uint8_t *next,
+                      uint8_t *segflag = nullptr, int T = 1);
+double avg_degree(const tcmis_graph *g);
 
 // workspace management (solver.cu)
 int ensure_workspace(tcmis_graph *g);

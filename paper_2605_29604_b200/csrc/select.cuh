@@ -55,6 +55,7 @@ struct SelectArgs {
   int32_t *long_list;      // rows outliving the thread probe (ctrl->long_count)
   int32_t *check;          // pull mode: non-candidates (ctrl->check_count)
   int32_t *undecided;      // rows the probe could not settle (ctrl->sel_undec)
+  Publish pub;             // multi-GPU: this round's candidates of the own range
 };
 
 // push: every neighbour of a candidate is excluded this round (spmv.cpp:18-59
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
         noncand = !a.push;
       } else if (e - s <= kProbeK) {
         mark_candidate(v, a.next, a.state, a.segflag, a.T);
+        publish(a.pub, v);
         ++sel;
         if (a.push) {
 #pragma unroll
@@ -168,6 +170,7 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
         mode = kFetch;
       } else if (hi <= s) {
         mark_candidate(v, a.next, a.state, a.segflag, a.T);
+        publish(a.pub, v);
         ++sel;
         mode = a.push ? kPush : kFetch;
         hi = s;  // push cursor runs upward from s
@@ -226,6 +229,7 @@ __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
     if (!blocked) {
       if (lane == 0) {
         mark_candidate(v, a.next, a.state, a.segflag, a.T);
+        publish(a.pub, v);
         ++sel;
       }
       if (a.push)

@@ -347,16 +347,20 @@ int ensure_workspace(tcmis_graph *g) {
 
 // ------------------------------------------------------------------ solve
 
+double avg_degree(const tcmis_graph *g) {
+  // priorities.cpp:60 avg = 2.0 * num_edges / n, num_edges = nnz / 2 (of the
+  // whole graph, also on a rank that holds only a row partition)
+  const int64_t nnz = g->nnz_global >= 0 ? g->nnz_global : g->nnz;
+  return 2.0 * (double)(nnz / 2) / (double)g->n;
+}
+
 namespace {
 
-double avg_degree(const tcmis_graph *g) {
-  // priorities.cpp:60 avg = 2.0 * num_edges / n, num_edges = nnz / 2
-  return 2.0 * (double)(g->nnz / 2) / (double)g->n;
-}
+}  // namespace
 
 int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
                       uint64_t *key, uint32_t *p_out, uint8_t *state, uint8_t *next,
-                      uint8_t *segflag = nullptr, int T = 1) {
+                      uint8_t *segflag, int T) {
   tcmis_ctx *ctx = g->ctx;
   int mode = 1;
   uint64_t mseed = mix64(seed);
@@ -369,12 +373,14 @@ int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bi
   const double scale = mode ? (double)(1u << scale_bits) : 0.0;
   const int grid = grid_for(ctx, g->n, 256, 16);
   TCMIS_TIMED(ctx, "k_priorities",
-              (k_priorities<<<grid, 256, 0, ctx->stream>>>(g->n, g->d_off, mode, mseed,
+              (k_priorities<<<grid, 256, 0, ctx->stream>>>(g->n, g->d_off_full ? g->d_off_full : g->d_off, mode, mseed,
                                                           mode ? avg_degree(g) : 0.0, scale, key,
                                                           p_out, state, next, segflag, T)));
   TCMIS_LAUNCHED(ctx);
   return 0;
 }
+
+namespace {
 
 int validate(const tcmis_graph *g, const tcmis_config *c) {
   if (c->heuristic < TCMIS_H1 || c->heuristic > TCMIS_LUBY_PERM)
@@ -395,24 +401,6 @@ int validate(const tcmis_graph *g, const tcmis_config *c) {
 
 }  // namespace
 
-struct RoundArgs {
-  int32_t n;
-  const int64_t *off;
-  const int32_t *nbr;
-  int T, seg_mode, fresh;
-  int32_t nseg;
-  int64_t total_tiles;
-  const int32_t *rowtiles;
-  uint64_t seed;
-  int sel_grid, upd_grid;
-  int pull;             // exclusion form: 0 push (in k_select), 1 pull (in k_update_pull)
-  int32_t nz_count;     // round-1 select list
-  const int32_t *nz;
-  int32_t tail_thr;     // rounds start in k_tail once alive <= tail_thr
-  int64_t vnnz;         // nnz, negated when the neighbour array is not 16-byte aligned
-  int tail_grid;
-  bool operator==(const RoundArgs &o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
-};
 
 SelectArgs select_args(tcmis_graph *g, const RoundArgs &a) {
   Workspace &ws = g->ws;
@@ -435,6 +423,7 @@ SelectArgs select_args(tcmis_graph *g, const RoundArgs &a) {
   s.long_list = ws.long_list;
   s.check = ws.check;
   s.undecided = ws.undec_sel;
+  s.pub = Publish{a.pub_cand, a.pub_lo};
   return s;
 }
 
@@ -456,6 +445,7 @@ UpdateArgs update_args(tcmis_graph *g, const RoundArgs &a) {
   u.check = ws.check;
   u.long_list = ws.long_list2;
   u.undecided = ws.undec_pull;
+  u.pub = Publish{a.pub_dead, a.pub_lo};
   u.segflag = ws.segflag;
   u.rowtiles = a.rowtiles;
   u.nseg = a.nseg;
@@ -602,6 +592,70 @@ int ensure_round_graph(tcmis_graph *g, const RoundArgs &a) {
   g->ctx->launches -= launches_per_round(a);  // capture is not execution
   if (!rc) std::memcpy(ws.graph_key, &a, sizeof(a));
   return rc;
+}
+
+// Tiles in the block columns holding any flagged segment (h3's single
+// iteration counter, also used per rank by the multi-GPU driver).
+int seg_total(tcmis_graph *g, int64_t *ev) {
+  tcmis_ctx *ctx = g->ctx;
+  Workspace &ws = g->ws;
+  unsigned long long h = 0;
+  TCMIS_CUDA(cudaMemsetAsync(&ws.ctrl->eval, 0, sizeof(unsigned long long), ctx->stream));
+  k_seg_total<<<grid_for(ctx, g->tile_nb, 256, 4), 256, 0, ctx->stream>>>(
+      ws.segflag, g->d_rowtiles, g->tile_nb, ws.ctrl);
+  TCMIS_LAUNCHED(ctx);
+  TCMIS_CUDA(cudaMemcpyAsync(&h, &ws.ctrl->eval, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  TCMIS_CUDA(cudaStreamSynchronize(ctx->stream));
+  *ev = (int64_t)h;
+  return 0;
+}
+
+// The setup of a solve (validation, tile counts, priorities, round state and
+// the kernel arguments) for the multi-GPU driver (dist.cu): `isolated` is the
+// number of round-1 candidates settled by k_priorities on this rank.
+int solve_prepare(tcmis_graph *g, const tcmis_config *cfg, RoundArgs &a, int64_t isolated) {
+  if (int rc = validate(g, cfg)) return rc;
+  tcmis_ctx *ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  if (int rc = ensure_workspace(g)) return rc;
+  Workspace &ws = g->ws;
+  const int H = cfg->heuristic;
+  const bool tiled = H <= TCMIS_H3;
+  const int T = cfg->tile_dim;
+  if (tiled && g->tile_T != T)
+    if (int rc = build_tile_counts(g, T)) return rc;
+  const int32_t nseg = tiled ? g->tile_nb : 0;
+  const int seg_mode = !tiled ? 0 : (H == TCMIS_H3 ? 2 : 1);
+  if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
+  if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.key, nullptr, ws.state,
+                                 ws.next, seg_mode ? ws.segflag : nullptr, T > 0 ? T : 1))
+    return rc;
+  Ctrl c0{};
+  c0.round = 1;
+  c0.alive = g->n;
+  c0.max_rounds = ws.round_cap;
+  c0.sel = (unsigned long long)isolated;
+  *ws.h_ctrl = c0;
+  TCMIS_CUDA(cudaMemcpyAsync(ws.ctrl, ws.h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+  std::memset(&a, 0, sizeof(a));
+  a.n = g->n;
+  a.off = g->d_off;
+  a.nbr = g->d_nbr;
+  a.T = T > 0 ? T : 1;
+  a.seg_mode = seg_mode;
+  a.nseg = nseg;
+  a.total_tiles = g->tile_total;
+  a.rowtiles = g->d_rowtiles;
+  a.fresh = H == TCMIS_LUBY_FRESH ? 1 : 0;
+  a.seed = cfg->seed;
+  a.sel_grid = ctx->num_sms * 8;
+  a.upd_grid = ctx->num_sms * 4;
+  a.nz = g->d_nz;
+  a.vnnz = ((uintptr_t)g->d_nbr & 15) == 0 ? g->nnz : -g->nnz;
+  a.nz_count = g->nz_count;
+  a.pull = 1;
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  return 0;
 }
 
 int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,

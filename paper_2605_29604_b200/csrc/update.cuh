@@ -49,6 +49,7 @@ struct UpdateArgs {
   const int32_t *check;    // pull: non-candidates of this round
   int32_t *long_list;      // pull: rows outliving the thread probe (ctrl->pull_count)
   int32_t *undecided;      // pull: rows the probe could not settle (ctrl->pull_undec)
+  Publish pub;             // multi-GPU: this round's removals of the own range
   uint8_t *segflag;
   const int32_t *rowtiles;
   int32_t nseg;
@@ -94,6 +95,7 @@ __global__ void __launch_bounds__(kBlock) k_update(UpdateArgs a) {
       if (v < 0 || ds[j] == 1) continue;  // candidates were settled by k_select
       if (ds[j] == 2) {
         mark_removed(v, a.state, a.key);
+        publish(a.pub, v);
         ++rem;
       } else {
         ++mine;
@@ -149,6 +151,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
         if (u[j] >= 0) hit |= next[u[j]] == 1;
       if (hit) {
         mark_removed(v, a.state, a.key);
+        publish(a.pub, v);
         ++rem;
       } else if (e - s <= kPullK) {
         survive = true;
@@ -210,6 +213,7 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
       hi = w;
       if (hit) {
         mark_removed(v, a.state, a.key);
+        publish(a.pub, v);
         ++rem;
         mode = kFetch;
       } else if (hi <= s) {
@@ -267,6 +271,7 @@ __global__ void __launch_bounds__(kBlock)
     if (lane == 0) {
       if (hit) {
         mark_removed(v, a.state, a.key);
+        publish(a.pub, v);
         ++rem;
       } else {
         if (a.fresh) a.key[v] = fresh_key(v, fresh_m);

@@ -1,0 +1,230 @@
+"""Row-partitioned multi-GPU MIS: one process per GPU,
+``torch.distributed`` (NCCL over NVLink/NVSwitch) for the per-round exchange.
+
+Rank r owns the contiguous rows [lo_r, hi_r).  The boundaries balance the
+adjacency entries (R-MAT puts its hubs at the lowest ids) and are aligned to a
+multiple of 64 vertices and of the tile dimension, so every bitmap slice is
+whole 32-bit words and every T x T block row / block column belongs to one
+rank (the tile counters then stay rank-local: tiles in block column b = tiles
+in block row b by symmetry).
+
+Per round (the reference's bulk-synchronous round, engine.cpp:247-291):
+
+    select own worklist          -> own candidates, bitmap slice (n_r / 32 words)
+    all_gather(candidate slices) -> remote candidates marked on every rank
+    pull exclusion + update      -> own removals, bitmap slice
+    all_gather(removal slices)   -> remote removed keys zeroed on every rank
+    all_reduce(sel, rem, alive, tiles_eval, tiles_skip)
+
+so the MIS, the round count and every per-round statistic equal the
+single-GPU solve (tests/test_distributed.py checks world sizes 2 and 3 with
+gloo on CPU through the same driver; the device side is csrc/dist.cu).
+Slices are padded to the largest rank's word count (``maxw``) so one
+all_gather_into_tensor moves them; rank r's slice sits at word r * maxw.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HEURISTICS = {"h1": 0, "h2": 1, "h3": 2, "luby-perm": 4}  # fixed priorities only
+
+
+def partition_rows(offsets: np.ndarray, world: int, tile_dim: int = 16) -> list[int]:
+    """Edge-balanced contiguous row ranges: rank_lo[0..world], rank_lo[0] = 0,
+    rank_lo[world] = n, boundaries at multiples of lcm(64, tile_dim)."""
+    n = int(offsets.size - 1)
+    align = 64 * tile_dim // math.gcd(64, tile_dim)
+    total = int(offsets[-1])
+    lo = [0]
+    for r in range(1, world):
+        target = total * r // world
+        v = int(np.searchsorted(offsets, target, side="left"))
+        v = min(n, max(lo[-1], (v + align // 2) // align * align))
+        lo.append(v)
+    lo.append(n)
+    return lo
+
+
+def slice_words(rank_lo: list[int]) -> int:
+    return max(1, max((rank_lo[r + 1] - rank_lo[r] + 31) // 32 for r in range(len(rank_lo) - 1)))
+
+
+@dataclass
+class RoundStats:
+    iteration: int
+    candidates_selected: int
+    vertices_removed: int
+    alive_remaining: int
+    tiles_evaluated: int
+    tiles_skipped: int
+
+
+@dataclass
+class PartitionedResult:
+    own_state: np.ndarray            # VertexState of [lo, hi)
+    rounds: list = field(default_factory=list)
+    rank_lo: list = field(default_factory=list)
+
+
+class GpuRank:
+    """The device side of one rank (csrc/dist.cu through the C-ABI)."""
+
+    def __init__(self, ctx, n: int, lo: int, hi: int, offsets: np.ndarray,
+                 neighbors: np.ndarray, device: str):
+        import torch
+
+        import paper_2605_29604_b200 as tc
+        self.tc, self.torch, self.ctx, self.device = tc, torch, ctx, device
+        self.L = L = tc.load()
+        for name, args in (
+                ("tcmis_graph_upload_partition",
+                 [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                  C.POINTER(C.c_void_p)]),
+                ("tcmis_dist_begin", [C.c_void_p, C.c_void_p]),
+                ("tcmis_dist_select", [C.c_void_p, C.c_void_p, C.c_int32]),
+                ("tcmis_dist_apply", [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                      C.c_int32, C.c_int32, C.c_int32]),
+                ("tcmis_dist_update", [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
+                ("tcmis_dist_state", [C.c_void_p, C.c_void_p]),
+                ("tcmis_dist_h3_tiles", [C.c_void_p, C.c_void_p, C.c_void_p])):
+            fn = getattr(L, name)
+            fn.restype = C.c_int
+            fn.argtypes = args
+        off = np.ascontiguousarray(offsets, np.int64)
+        rows = np.ascontiguousarray(neighbors[off[lo]:off[hi]], np.int32)
+        h = C.c_void_p()
+        tc._check(L.tcmis_graph_upload_partition(
+            ctx.h, n, lo, hi, C.c_void_p(off.ctypes.data),
+            C.c_void_p(rows.ctypes.data) if rows.size else None, C.byref(h)))
+        self.g = tc.DeviceGraph(h, ctx)
+        self.n, self.lo, self.hi = n, lo, hi
+        self.stream = torch.cuda.ExternalStream(ctx.stream, device=device)
+
+    def words_tensor(self, words: int):
+        return self.torch.zeros(words, dtype=self.torch.int32, device=self.device)
+
+    def begin(self, heuristic: str, seed: int, tile_dim: int, scale_bits: int):
+        cfg = self.tc.EngineConfig(heuristic=HEURISTICS[heuristic], seed=seed,
+                                   tile_dim=tile_dim, scale_bits=scale_bits)
+        c, _ = cfg._c()
+        self.tc._check(self.L.tcmis_dist_begin(self.g.h, C.byref(c)))
+
+    def select(self, bits):
+        self.tc._check(self.L.tcmis_dist_select(self.g.h, C.c_void_p(bits.data_ptr()),
+                                                 bits.numel()))
+
+    def apply(self, gathered, rank_lo, me: int, maxw: int, what: int):
+        lo = np.ascontiguousarray(rank_lo, np.int32)
+        self.tc._check(self.L.tcmis_dist_apply(self.g.h, C.c_void_p(gathered.data_ptr()),
+                                                C.c_void_p(lo.ctypes.data), len(rank_lo) - 1,
+                                                maxw, me, what))
+
+    def update(self, bits) -> np.ndarray:
+        counts = np.zeros(5, np.int64)
+        self.tc._check(self.L.tcmis_dist_update(self.g.h, C.c_void_p(bits.data_ptr()),
+                                                 bits.numel(), C.c_void_p(counts.ctypes.data)))
+        return counts
+
+    def h3_tiles(self):
+        ev, tot = C.c_int64(0), C.c_int64(0)
+        self.tc._check(self.L.tcmis_dist_h3_tiles(self.g.h, C.byref(ev), C.byref(tot)))
+        return ev.value, tot.value
+
+    def state(self) -> np.ndarray:
+        out = np.zeros(max(self.hi - self.lo, 1), np.uint8)
+        self.tc._check(self.L.tcmis_dist_state(self.g.h, C.c_void_p(out.ctypes.data)))
+        return out[:self.hi - self.lo]
+
+    def collective_stream(self):
+        return self.torch.cuda.stream(self.stream)
+
+
+def solve_partitioned(rank_obj, rank_lo: list[int], rank: int, world: int, dist,
+                      heuristic: str = "h2", seed: int = 1, tile_dim: int = 16,
+                      scale_bits: int = 20, max_rounds: int | None = None) -> PartitionedResult:
+    """The per-round protocol; `rank_obj` is a GpuRank (or the CPU stand-in of
+    the tests) and `dist` is torch.distributed (NCCL on GPUs, gloo on CPU)."""
+    import torch
+    n = rank_lo[-1]
+    if any((rank_lo[r] % 64) or (rank_lo[r] % tile_dim) for r in range(world)):
+        raise ValueError("partition boundaries must be multiples of 64 and of tile_dim")
+    if heuristic not in HEURISTICS:
+        raise ValueError(f"partitioned solve runs {sorted(HEURISTICS)}, not {heuristic!r}")
+    maxw = slice_words(rank_lo)
+    rank_obj.begin(heuristic, seed, tile_dim, scale_bits)
+    mine = rank_obj.words_tensor(maxw)
+    gathered = rank_obj.words_tensor(maxw * world)
+    rounds = []
+    cap = max_rounds or max(n, 1)
+    with rank_obj.collective_stream():
+        for it in range(1, cap + 1):
+            rank_obj.select(mine)
+            dist.all_gather_into_tensor(gathered, mine)
+            rank_obj.apply(gathered, rank_lo, rank, maxw, 0)
+            counts = rank_obj.update(mine)
+            dist.all_gather_into_tensor(gathered, mine)
+            rank_obj.apply(gathered, rank_lo, rank, maxw, 1)
+            t = torch.tensor(counts, dtype=torch.int64, device=mine.device)
+            dist.all_reduce(t)
+            sel, rem, alive, ev, sk = (int(x) for x in t.cpu().tolist())
+            rounds.append(RoundStats(it, sel, rem, alive, ev, sk))
+            if alive == 0:
+                break
+        else:
+            raise RuntimeError("iteration cap exceeded; engine livelock")  # engine.cpp:248-249
+        if heuristic == "h3":
+            ev, tot = rank_obj.h3_tiles()
+            t = torch.tensor([ev, tot], dtype=torch.int64, device=mine.device)
+            dist.all_reduce(t)
+            rounds = collapse_h3(rounds, n, int(t[0]), int(t[1]))
+    return PartitionedResult(rank_obj.state(), rounds, rank_lo)
+
+
+def collapse_h3(rounds: list, n: int, tiles_evaluated: int, total_tiles: int) -> list:
+    """h3 reports the whole resolution as one iteration (engine.cpp:255-258)."""
+    sel = sum(r.candidates_selected for r in rounds)
+    return [RoundStats(1, sel, n - sel, 0, tiles_evaluated, total_tiles - tiles_evaluated)]
+
+
+def solve_partitioned_local(ranks: list, rank_lo: list[int], heuristic: str = "h2",
+                            seed: int = 1, tile_dim: int = 16, scale_bits: int = 20):
+    """The same protocol as solve_partitioned with all `world` ranks in one
+    process (one GPU): the collectives become device copies.  Used to test
+    the device side of the partitioned solve on the single-GPU test box."""
+    import torch
+    world = len(ranks)
+    n = rank_lo[-1]
+    maxw = slice_words(rank_lo)
+    for r in ranks:
+        r.begin(heuristic, seed, tile_dim, scale_bits)
+    mine = [r.words_tensor(maxw) for r in ranks]
+    gathered = ranks[0].words_tensor(maxw * world)
+    rounds = []
+    for it in range(1, max(n, 1) + 1):
+        for r, m in zip(ranks, mine):
+            r.select(m)
+        torch.cuda.synchronize()
+        gathered.copy_(torch.cat(mine))
+        for k, r in enumerate(ranks):
+            r.apply(gathered, rank_lo, k, maxw, 0)
+        counts = sum(r.update(m) for r, m in zip(ranks, mine))
+        torch.cuda.synchronize()
+        gathered.copy_(torch.cat(mine))
+        for k, r in enumerate(ranks):
+            r.apply(gathered, rank_lo, k, maxw, 1)
+        sel, rem, alive, ev, sk = (int(x) for x in counts)
+        rounds.append(RoundStats(it, sel, rem, alive, ev, sk))
+        if alive == 0:
+            break
+    if heuristic == "h3":
+        ev = tot = 0
+        for r in ranks:
+            e, t = r.h3_tiles()
+            ev, tot = ev + e, tot + t
+        rounds = collapse_h3(rounds, n, ev, tot)
+    state = np.concatenate([r.state() for r in ranks])
+    return state, rounds
