@@ -21,6 +21,7 @@
 namespace tcmis_b200 {
 
 static thread_local std::string g_last_error;
+thread_local cudaStream_t t_alloc_stream = nullptr;
 
 int set_error(int code, const std::string &msg) {
   g_last_error = msg;
@@ -77,6 +78,14 @@ int wrap_owned(tcmis_ctx *ctx, int32_t n, int64_t nnz, int64_t *d_off, int32_t *
 
 using namespace tcmis_b200;
 
+// every entry point: the context's device, and its stream for the
+// stream-ordered allocations of this call (internal.cuh dev_alloc)
+#define ENTER(c)                                   \
+  do {                                             \
+    TCMIS_CUDA(cudaSetDevice((c)->device));        \
+    t_alloc_stream = (c)->stream;                  \
+  } while (0)
+
 #define NEED(cond, msg) \
   if (!(cond)) return set_error(TCMIS_E_INVALID_ARGUMENT, msg)
 
@@ -116,6 +125,13 @@ TCMIS_API int tcmis_ctx_create(int32_t device, tcmis_ctx **out) {
     return cuda_error(e, "cudaStreamCreate");
   }
   for (auto &ev : ctx->ev) cudaEventCreate(&ev);
+  // keep freed blocks in the device pool (dev_alloc / dev_free): repeated
+  // upload -> solve -> destroy cycles then never return to the driver
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
   *out = ctx;
   return 0;
 }
@@ -124,6 +140,11 @@ TCMIS_API void tcmis_ctx_destroy(tcmis_ctx *ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  t_alloc_stream = ctx->stream;
+  free_workspace(ctx->spare);
+  cudaStreamSynchronize(ctx->stream);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
   for (auto &ev : ctx->ev) cudaEventDestroy(ev);
   for (auto &ev : ctx->event_pool) cudaEventDestroy(ev);
   cudaStreamDestroy(ctx->stream);
@@ -153,12 +174,12 @@ TCMIS_API int tcmis_graph_upload(tcmis_ctx *ctx, int32_t n, const int64_t *offse
   const int64_t nnz = offsets ? offsets[n] : 0;
   NEED(nnz >= 0, "negative edge count");
   NEED(nnz == 0 || neighbors, "null neighbors");
-  TCMIS_CUDA(cudaSetDevice(ctx->device));
+  ENTER(ctx);
   int64_t *d_off = nullptr;
   int32_t *d_nbr = nullptr;
   if (int rc = dev_alloc(&d_off, (size_t)n + 1)) return rc;
   if (int rc = dev_alloc(&d_nbr, (size_t)nnz)) {
-    cudaFree(d_off);
+    dev_free(d_off);
     return rc;
   }
   cudaError_t e = cudaSuccess;
@@ -168,8 +189,8 @@ TCMIS_API int tcmis_graph_upload(tcmis_ctx *ctx, int32_t n, const int64_t *offse
     e = cudaMemcpyAsync(d_nbr, neighbors, 4ull * nnz, cudaMemcpyHostToDevice, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) {
-    cudaFree(d_off);
-    cudaFree(d_nbr);
+    dev_free(d_off);
+    dev_free(d_nbr);
     return cuda_error(e, "graph upload");
   }
   return wrap_owned(ctx, n, nnz, d_off, d_nbr, out);
@@ -194,15 +215,22 @@ TCMIS_API int tcmis_graph_wrap_device(tcmis_ctx *ctx, int32_t n, int64_t nnz,
 TCMIS_API void tcmis_graph_destroy(tcmis_graph *g) {
   if (!g) return;
   cudaSetDevice(g->ctx->device);
-  cudaStreamSynchronize(g->ctx->stream);
+  t_alloc_stream = g->ctx->stream;  // frees are stream-ordered behind its work
   if (g->owns) {
-    cudaFree(g->d_off);
-    cudaFree(g->d_nbr);
+    dev_free(g->d_off);
+    dev_free(g->d_nbr);
   }
-  cudaFree(g->d_rowtiles);
-  cudaFree(g->d_nz);
-  cudaFree(g->d_off_full);
-  free_workspace(g->ws);
+  dev_free(g->d_rowtiles);
+  dev_free(g->d_nz);
+  dev_free(g->d_off_full);
+  Workspace &sp = g->ctx->spare;
+  if (g->ws.ctrl && g->ws.n_cap >= sp.n_cap) {
+    free_workspace(sp);
+    sp = g->ws;
+    g->ws = Workspace{};
+  } else {
+    free_workspace(g->ws);
+  }
   delete g;
 }
 
@@ -227,7 +255,7 @@ TCMIS_API int tcmis_graph_download(tcmis_graph *g, int64_t *offsets, int32_t *ne
 
 TCMIS_API int tcmis_graph_tile(tcmis_graph *g, int32_t tile_dim, int64_t *tile_count) {
   NEED(g, "null graph");
-  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  ENTER(g->ctx);
   if (g->tile_T != tile_dim)
     if (int rc = build_tile_counts(g, tile_dim)) return rc;
   if (tile_count) *tile_count = g->tile_total;
@@ -244,7 +272,7 @@ TCMIS_API int tcmis_graph_set_tiling(tcmis_graph *g, int32_t T, const int64_t *b
   NEED(nb == 0 || bro, "null block_row_offsets");
   std::vector<int32_t> rt((size_t)nb + 1, 0);
   for (int32_t b = 0; b < nb; ++b) rt[b] = (int32_t)(bro[b + 1] - bro[b]);
-  cudaFree(g->d_rowtiles);
+  dev_free(g->d_rowtiles);
   g->d_rowtiles = nullptr;
   g->tile_T = 0;
   if (int rc = dev_alloc(&g->d_rowtiles, (size_t)nb + 1)) return rc;
@@ -258,21 +286,21 @@ TCMIS_API int tcmis_graph_set_tiling(tcmis_graph *g, int32_t T, const int64_t *b
 TCMIS_API int tcmis_graph_export_tiles(tcmis_graph *g, int32_t T, int32_t *tile_row,
                                        int32_t *tile_col, uint64_t *row_bits, int64_t *bro) {
   NEED(g && bro, "null handle");
-  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  ENTER(g->ctx);
   return export_tiles(g, T, tile_row, tile_col, row_bits, bro);
 }
 
 TCMIS_API int tcmis_priorities(tcmis_graph *g, int32_t heuristic, uint64_t seed,
                                int32_t scale_bits, uint32_t *p_out) {
   NEED(g && p_out, "null handle");
-  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  ENTER(g->ctx);
   return priorities_impl(g, heuristic, seed, scale_bits, p_out);
 }
 
 static int solve_common(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
                         int32_t max_stats, int32_t *n_iterations, int64_t *mis_count) {
   NEED(g && cfg, "null handle");
-  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  ENTER(g->ctx);
   int32_t it = 0;
   int64_t mc = 0;
   int rc = solve_impl(g, cfg, stats, max_stats, &it, &mc);
@@ -312,19 +340,19 @@ TCMIS_API int tcmis_graph_upload_partition(tcmis_ctx *ctx, int32_t n, int32_t lo
                                            const int32_t *row_neighbors, tcmis_graph **out) {
   NEED(ctx && out && full_offsets, "null handle");
   NEED(n >= 0, "vertex count must be non-negative");
-  TCMIS_CUDA(cudaSetDevice(ctx->device));
+  ENTER(ctx);
   return upload_partition(ctx, n, lo, hi, full_offsets, row_neighbors, out);
 }
 
 TCMIS_API int tcmis_dist_begin(tcmis_graph *g, const tcmis_config *cfg) {
   NEED(g && cfg, "null handle");
-  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  ENTER(g->ctx);
   return dist_begin(g, cfg);
 }
 
 TCMIS_API int tcmis_dist_select(tcmis_graph *g, uint32_t *d_bits, int32_t words) {
   NEED(g && d_bits, "null handle");
-  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  ENTER(g->ctx);
   return dist_select(g, d_bits, words);
 }
 
@@ -333,40 +361,40 @@ TCMIS_API int tcmis_dist_apply(tcmis_graph *g, const uint32_t *d_gathered,
                                int32_t what) {
   NEED(g && d_gathered && rank_lo, "null handle");
   NEED(world >= 1 && me >= 0 && me < world && maxw >= 0, "bad rank layout");
-  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  ENTER(g->ctx);
   return dist_apply(g, d_gathered, rank_lo, world, maxw, me, what);
 }
 
 TCMIS_API int tcmis_dist_update(tcmis_graph *g, uint32_t *d_bits, int32_t words,
                                 int64_t *counts) {
   NEED(g && d_bits && counts, "null handle");
-  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  ENTER(g->ctx);
   return dist_update(g, d_bits, words, counts);
 }
 
 TCMIS_API int tcmis_dist_state(tcmis_graph *g, uint8_t *own_state) {
   NEED(g, "null handle");
-  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  ENTER(g->ctx);
   return dist_state_out(g, own_state);
 }
 
 TCMIS_API int tcmis_dist_h3_tiles(tcmis_graph *g, int64_t *tiles_evaluated,
                                   int64_t *tile_total) {
   NEED(g && tiles_evaluated && tile_total, "null handle");
-  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  ENTER(g->ctx);
   return dist_h3_tiles(g, tiles_evaluated, tile_total);
 }
 
 TCMIS_API int tcmis_h1_random(tcmis_ctx *ctx, int32_t n, uint64_t seed, uint32_t *p_out) {
   NEED(ctx && (n < 1 || p_out), "null handle");
-  TCMIS_CUDA(cudaSetDevice(ctx->device));
+  ENTER(ctx);
   return h1_impl(ctx, n, seed, p_out);
 }
 
 TCMIS_API int tcmis_h3_resolution(tcmis_graph *g, const uint32_t *p, const uint8_t *states,
                                   uint8_t *c_out) {
   NEED(g && (g->n == 0 || (p && states && c_out)), "null handle");
-  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  ENTER(g->ctx);
   return h3_resolution_impl(g, p, states, c_out);
 }
 
@@ -377,7 +405,7 @@ TCMIS_API int tcmis_tiled_spmv_tiles(tcmis_ctx *ctx, int32_t n, int32_t T, int64
   NEED(ctx && ev && sk, "null handle");
   NEED(n == 0 || (bro && seg && nc), "null buffers");
   NEED(tiles == 0 || (tile_col && row_bits), "null tile buffers");
-  TCMIS_CUDA(cudaSetDevice(ctx->device));
+  ENTER(ctx);
   return tiled_spmv_tiles_impl(ctx, n, T, tiles, tile_col, row_bits, bro, seg, exclusion, nc, ev,
                                sk);
 }
@@ -385,13 +413,13 @@ TCMIS_API int tcmis_tiled_spmv_tiles(tcmis_ctx *ctx, int32_t n, int32_t T, int64
 TCMIS_API int tcmis_compute_max_np(tcmis_graph *g, const uint32_t *p, const uint8_t *states,
                                    uint64_t *out) {
   NEED(g && p && states && out, "null handle");
-  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  ENTER(g->ctx);
   return max_np_impl(g, p, states, out);
 }
 
 TCMIS_API int tcmis_neighbor_count(tcmis_graph *g, const uint8_t *c, int32_t *nc) {
   NEED(g && c && nc, "null handle");
-  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  ENTER(g->ctx);
   return neighbor_count_impl(g, c, nc, 0, nullptr, nullptr);
 }
 
@@ -402,27 +430,27 @@ TCMIS_API int tcmis_tiled_spmv(tcmis_graph *g, int32_t T, const uint8_t *c, int3
     return set_error(TCMIS_E_INVALID_ARGUMENT,
                      "tile_dim must be in [1, 64], got " + std::to_string(T));
   (void)exclusion;
-  TCMIS_CUDA(cudaSetDevice(g->ctx->device));
+  ENTER(g->ctx);
   return neighbor_count_impl(g, c, nc, T, ev, sk);
 }
 
 TCMIS_API int tcmis_gen_rmat(tcmis_ctx *ctx, int32_t scale, int32_t ef, uint64_t seed,
                              tcmis_graph **out) {
   NEED(ctx && out, "null handle");
-  TCMIS_CUDA(cudaSetDevice(ctx->device));
+  ENTER(ctx);
   return gen_rmat(ctx, scale, ef, seed, out);
 }
 
 TCMIS_API int tcmis_gen_grid(tcmis_ctx *ctx, int32_t side, tcmis_graph **out) {
   NEED(ctx && out, "null handle");
-  TCMIS_CUDA(cudaSetDevice(ctx->device));
+  ENTER(ctx);
   return gen_grid(ctx, side, out);
 }
 
 TCMIS_API int tcmis_gen_rgg(tcmis_ctx *ctx, int32_t n, uint64_t radius, uint64_t seed,
                             tcmis_graph **out) {
   NEED(ctx && out, "null handle");
-  TCMIS_CUDA(cudaSetDevice(ctx->device));
+  ENTER(ctx);
   return gen_rgg(ctx, n, radius, seed, out);
 }
 

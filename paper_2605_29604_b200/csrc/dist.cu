@@ -156,7 +156,7 @@ int dist_apply(tcmis_graph *g, const uint32_t *d_gathered, const int32_t *h_rank
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  cudaFree(d_lo);
+  dev_free(d_lo);
   if (e != cudaSuccess) return cuda_error(e, "dist apply");
   return 0;
 }

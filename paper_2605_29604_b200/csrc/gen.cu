@@ -173,7 +173,7 @@ __global__ void k_rgg_rows(int32_t n, uint64_t R, uint64_t C, const uint32_t *__
 template <typename T>
 struct DevBuf {
   T *p = nullptr;
-  ~DevBuf() { cudaFree(p); }
+  ~DevBuf() { dev_free(p); }
   int alloc(size_t n) { return dev_alloc(&p, n); }
   T *release() {
     T *q = p;

@@ -113,6 +113,10 @@ struct tcmis_ctx {
   int tail_blocks_per_sm = 0;  // co-resident k_tail blocks per SM (occupancy)
   int64_t launches = 0;
   cudaEvent_t ev[8] = {};
+  // the largest solve workspace of a destroyed graph, adopted by the next
+  // graph that fits (upload -> solve -> destroy loops re-use buffers, pinned
+  // staging and the instantiated round graph)
+  tcmis_b200::Workspace spare;
 };
 
 struct tcmis_graph {
@@ -224,14 +228,25 @@ int build_tile_counts(tcmis_graph *g, int T);
 int export_tiles(tcmis_graph *g, int T, int32_t *tile_row, int32_t *tile_col,
                  uint64_t *row_bits, int64_t *bro);
 
-// scratch allocation helper that records the CUDA error
+// Device memory comes from the device's stream-ordered pool (release
+// threshold = unlimited, set in tcmis_ctx_create), allocated and freed in
+// order on the stream of the context the current C-ABI call runs on
+// (t_alloc_stream, set by every entry point).  A graph upload / solve /
+// destroy cycle therefore re-uses pool memory instead of paying cudaMalloc
+// and the device-wide synchronisation of cudaFree every time.
+extern thread_local cudaStream_t t_alloc_stream;
+
 template <typename T>
 int dev_alloc(T **p, size_t count) {
   *p = nullptr;
   if (count == 0) count = 1;
-  cudaError_t e = cudaMalloc((void **)p, count * sizeof(T));
-  if (e != cudaSuccess) return cuda_error(e, "cudaMalloc");
+  cudaError_t e = cudaMallocAsync((void **)p, count * sizeof(T), t_alloc_stream);
+  if (e != cudaSuccess) return cuda_error(e, "cudaMallocAsync");
   return 0;
+}
+
+inline void dev_free(void *p) {
+  if (p) cudaFreeAsync(p, t_alloc_stream);
 }
 
 }  // namespace tcmis_b200

@@ -221,26 +221,26 @@ void timeline_end(tcmis_ctx *ctx) {
 // -------------------------------------------------------------- workspace
 
 void free_workspace(Workspace &ws) {
-  cudaFree(ws.key);
-  cudaFree(ws.state);
-  cudaFree(ws.next);
-  cudaFree(ws.wl[0]);
-  cudaFree(ws.wl[1]);
-  cudaFree(ws.segflag);
-  cudaFree(ws.mis);
-  cudaFree(ws.long_list);
-  cudaFree(ws.long_list2);
-  cudaFree(ws.check);
-  cudaFree(ws.undec_sel);
-  cudaFree(ws.undec_pull);
-  cudaFree(ws.segmark);
-  cudaFree(ws.bar);
-  cudaFree(ws.mis_count);
-  cudaFree(ws.ctrl);
+  dev_free(ws.key);
+  dev_free(ws.state);
+  dev_free(ws.next);
+  dev_free(ws.wl[0]);
+  dev_free(ws.wl[1]);
+  dev_free(ws.segflag);
+  dev_free(ws.mis);
+  dev_free(ws.long_list);
+  dev_free(ws.long_list2);
+  dev_free(ws.check);
+  dev_free(ws.undec_sel);
+  dev_free(ws.undec_pull);
+  dev_free(ws.segmark);
+  dev_free(ws.bar);
+  dev_free(ws.mis_count);
+  dev_free(ws.ctrl);
   cudaFreeHost(ws.h_ctrl);
-  cudaFree(ws.rounds);
+  dev_free(ws.rounds);
   cudaFreeHost(ws.h_rounds);
-  cudaFree(ws.cub_tmp);
+  dev_free(ws.cub_tmp);
   if (ws.exec) cudaGraphExecDestroy(ws.exec);
   ws = Workspace{};
 }
@@ -248,7 +248,7 @@ void free_workspace(Workspace &ws) {
 int ensure_cub(tcmis_graph *g, size_t bytes) {
   Workspace &ws = g->ws;
   if (bytes <= ws.cub_bytes) return 0;
-  cudaFree(ws.cub_tmp);
+  dev_free(ws.cub_tmp);
   ws.cub_tmp = nullptr;
   ws.cub_bytes = 0;
   if (int rc = dev_alloc((char **)&ws.cub_tmp, bytes)) return rc;
@@ -259,23 +259,28 @@ int ensure_cub(tcmis_graph *g, size_t bytes) {
 int ensure_workspace(tcmis_graph *g) {
   Workspace &ws = g->ws;
   const size_t n = (size_t)std::max<int32_t>(g->n, 1);
+  Workspace &spare = g->ctx->spare;
+  if (!ws.ctrl && spare.ctrl && spare.n_cap >= n && spare.seg_cap >= n) {
+    ws = spare;  // adopt a destroyed graph's buffers (tcmis_graph_destroy)
+    spare = Workspace{};
+  }
   if (ws.n_cap < n) {
     if (ws.exec) {  // the cached round graph points at the old buffers
       cudaGraphExecDestroy(ws.exec);
       ws.exec = nullptr;
     }
-    cudaFree(ws.key);
-    cudaFree(ws.state);
-    cudaFree(ws.next);
-    cudaFree(ws.wl[0]);
-    cudaFree(ws.wl[1]);
-    cudaFree(ws.mis);
-    cudaFree(ws.long_list);
-    cudaFree(ws.long_list2);
-    cudaFree(ws.check);
-    cudaFree(ws.undec_sel);
-    cudaFree(ws.undec_pull);
-    cudaFree(ws.segmark);
+    dev_free(ws.key);
+    dev_free(ws.state);
+    dev_free(ws.next);
+    dev_free(ws.wl[0]);
+    dev_free(ws.wl[1]);
+    dev_free(ws.mis);
+    dev_free(ws.long_list);
+    dev_free(ws.long_list2);
+    dev_free(ws.check);
+    dev_free(ws.undec_sel);
+    dev_free(ws.undec_pull);
+    dev_free(ws.segmark);
     ws.n_cap = 0;
     if (int rc = dev_alloc(&ws.key, n)) return rc;
     if (int rc = dev_alloc(&ws.state, n)) return rc;
@@ -294,7 +299,7 @@ int ensure_workspace(tcmis_graph *g) {
   }
   // segment flags for any tile_dim >= 1
   if (ws.seg_cap < n) {
-    cudaFree(ws.segflag);
+    dev_free(ws.segflag);
     if (int rc = dev_alloc(&ws.segflag, n)) return rc;
     TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, n, g->ctx->stream));
     ws.seg_cap = n;
@@ -336,7 +341,7 @@ int ensure_workspace(tcmis_graph *g) {
     cudaMemcpyAsync(&nz, ws.mis_count, 8, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(&mx, d_mx, 8, cudaMemcpyDeviceToHost, st);
     cudaError_t e = cudaStreamSynchronize(st);
-    cudaFree(d_mx);
+    dev_free(d_mx);
     if (e != cudaSuccess) return cuda_error(e, "graph preparation");
     g->nz_count = (int32_t)nz;
     g->max_degree = (int64_t)mx;
@@ -922,7 +927,7 @@ int priorities_impl(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits
     if (e == cudaSuccess) e = cudaStreamSynchronize(g->ctx->stream);
     if (e != cudaSuccess) rc = cuda_error(e, "priorities download");
   }
-  cudaFree(d_p);
+  dev_free(d_p);
   return rc;
 }
 
@@ -946,9 +951,9 @@ int max_np_impl(tcmis_graph *g, const uint32_t *p, const uint8_t *states, uint64
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) rc = cuda_error(e, "compute_max_np");
   }
-  cudaFree(d_p);
-  cudaFree(d_s);
-  cudaFree(d_o);
+  dev_free(d_p);
+  dev_free(d_s);
+  dev_free(d_o);
   return rc;
 }
 
@@ -994,8 +999,8 @@ int neighbor_count_impl(tcmis_graph *g, const uint8_t *c, int32_t *nc, int T, in
     cudaError_t e = cudaStreamSynchronize(ctx->stream);
     if (!rc && e != cudaSuccess) rc = cuda_error(e, "neighbor count");
   }
-  cudaFree(d_c);
-  cudaFree(d_nc);
+  dev_free(d_c);
+  dev_free(d_nc);
   return rc;
 }
 
@@ -1011,7 +1016,7 @@ int h1_impl(tcmis_ctx *ctx, int32_t n, uint64_t seed, uint32_t *p_out) {
   ctx->launches++;
   cudaError_t e = cudaMemcpyAsync(p_out, d_p, 4ull * n, cudaMemcpyDeviceToHost, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  cudaFree(d_p);
+  dev_free(d_p);
   if (e != cudaSuccess) return cuda_error(e, "h1_random");
   return 0;
 }
@@ -1089,9 +1094,9 @@ int h3_resolution_impl(tcmis_graph *g, const uint32_t *p, const uint8_t *states,
     if (e != cudaSuccess) rc = cuda_error(e, "h3 resolution result");
     for (int32_t v = 0; v < g->n && !rc; ++v) c[v] = fin[v] == TCMIS_IN_MIS ? 1 : 0;
   }
-  cudaFree(d_p);
-  cudaFree(d_s);
-  cudaFree(d_cnt);
+  dev_free(d_p);
+  dev_free(d_s);
+  dev_free(d_cnt);
   return rc;
 }
 

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(256)
 template <typename T>
 struct Dev {
   T *p = nullptr;
-  ~Dev() { cudaFree(p); }
+  ~Dev() { dev_free(p); }
 };
 
 }  // namespace

@@ -137,6 +137,148 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ------------------------------------------------------------ tile counts
+//
+// The solve needs only rowtiles[b] = |{distinct block columns among the
+// entries of block row b}| (tiles in block column b by symmetry), not the
+// tiles themselves.  The entries of a block row are contiguous in the CSR
+// (rows b*T .. b*T+T-1), so both kernels stream them coalesced and count
+// distinct block columns in shared memory -- one pass over nbr, no merge:
+//
+//  k_count_light  one warp per block row with <= kHashMax entries (88 % of
+//                 R-MAT s22's block rows): a 1024-slot open-addressing set
+//                 in shared memory (atomicCAS), cleared after each row.
+//  k_count_heavy  the rest, one CTA per (block row, window of kBmBits block
+//                 columns) from a dynamic work counter: a 32 KB shared
+//                 bitmap, atomicOr's old value tells a first occurrence.
+constexpr int kLightBlock = 256;
+constexpr int kHashSlots = 1024;
+constexpr int64_t kHashMax = 512;
+constexpr int kHeavyBlock = 512;
+constexpr int64_t kBmBits = 1 << 18;
+
+__global__ void __launch_bounds__(kLightBlock)
+    k_count_light(int32_t n, int T, int32_t nb, const int64_t *__restrict__ off,
+                  const int32_t *__restrict__ nbr, int32_t *__restrict__ rowtiles,
+                  int32_t *__restrict__ heavy, int32_t *__restrict__ heavy_count) {
+  __shared__ __align__(16) uint32_t tab[kLightBlock / 32][kHashSlots];
+  const int lane = threadIdx.x & 31;
+  uint32_t *t = tab[threadIdx.x >> 5];
+  uint4 *t4 = reinterpret_cast<uint4 *>(t);
+  for (int i = lane; i < kHashSlots / 4; i += 32) t4[i] = make_uint4(0, 0, 0, 0);
+  __syncwarp();
+  const uint32_t uT = (uint32_t)T;
+  for (int64_t b = ((int64_t)blockIdx.x * kLightBlock + threadIdx.x) >> 5; b < nb;
+       b += ((int64_t)gridDim.x * kLightBlock) >> 5) {
+    const int64_t r0 = b * T, r1 = min((int64_t)n, r0 + T);
+    const int64_t s = off[r0], e = off[r1];
+    if (e - s > kHashMax) {
+      if (lane == 0) heavy[atomicAdd(heavy_count, 1)] = (int32_t)b;
+      continue;
+    }
+    int cnt = 0;
+    for (int64_t base = s; base < e; base += 128) {
+      uint32_t c[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t p = base + lane + 32 * j;
+        c[j] = p < e ? (uint32_t)__ldg(&nbr[p]) / uT + 1u : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!c[j]) continue;
+        uint32_t h = (c[j] * 0x9E3779B1u) >> 22;
+        for (;;) {
+          const uint32_t old = atomicCAS(&t[h], 0u, c[j]);
+          if (old == 0u) {
+            ++cnt;
+            break;
+          }
+          if (old == c[j]) break;
+          h = (h + 1) & (kHashSlots - 1);
+        }
+      }
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0) rowtiles[b] = cnt;
+    if (e > s) {
+      __syncwarp();
+      for (int i = lane; i < kHashSlots / 4; i += 32) t4[i] = make_uint4(0, 0, 0, 0);
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kHeavyBlock)
+    k_count_heavy(int32_t n, int T, int32_t nb, const int64_t *__restrict__ off,
+                  const int32_t *__restrict__ nbr, int32_t *__restrict__ rowtiles,
+                  const int32_t *__restrict__ heavy, const int32_t *__restrict__ heavy_count,
+                  int32_t windows, unsigned long long *__restrict__ next_item) {
+  __shared__ __align__(16) uint32_t bm[kBmBits / 32];
+  __shared__ int64_t s_lo[64], s_hi[64];
+  __shared__ unsigned long long s_item;
+  __shared__ int s_red[kHeavyBlock / 32];
+  uint4 *bm4 = reinterpret_cast<uint4 *>(bm);
+  for (int i = threadIdx.x; i < kBmBits / 128; i += kHeavyBlock) bm4[i] = make_uint4(0, 0, 0, 0);
+  const unsigned long long items = (unsigned long long)*heavy_count * (unsigned)windows;
+  const uint32_t uT = (uint32_t)T;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_item = atomicAdd(next_item, 1ull);
+    __syncthreads();
+    const unsigned long long it = s_item;
+    if (it >= items) break;
+    const int32_t b = heavy[it / windows];
+    const int64_t c0 = (int64_t)(it % windows) * kBmBits;
+    const int64_t c1 = min((int64_t)nb, c0 + kBmBits);
+    const int64_t r0 = (int64_t)b * T;
+    const int rows = (int)min((int64_t)T, (int64_t)n - r0);
+    int nseg;
+    if (windows == 1) {  // the whole block row is one contiguous range
+      if (threadIdx.x == 0) {
+        s_lo[0] = off[r0];
+        s_hi[0] = off[r0 + rows];
+      }
+      nseg = 1;
+    } else {
+      if (threadIdx.x < rows) {
+        const int64_t rs = off[r0 + threadIdx.x], re = off[r0 + threadIdx.x + 1];
+        s_lo[threadIdx.x] = lower_bound_i32(nbr, rs, re, c0 * T);
+        s_hi[threadIdx.x] = lower_bound_i32(nbr, rs, re, c1 * T);
+      }
+      nseg = rows;
+    }
+    __syncthreads();
+    int cnt = 0;
+    for (int k = 0; k < nseg; ++k) {
+      const int64_t lo = s_lo[k], hi = s_hi[k];
+      for (int64_t base = lo; base < hi; base += 4 * kHeavyBlock) {
+        uint32_t c[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int64_t p = base + threadIdx.x + (int64_t)kHeavyBlock * j;
+          c[j] = p < hi ? (uint32_t)((uint32_t)__ldg(&nbr[p]) / uT - (uint32_t)c0) : 0xffffffffu;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (c[j] == 0xffffffffu) continue;
+          const uint32_t bit = 1u << (c[j] & 31);
+          cnt += (atomicOr(&bm[c[j] >> 5], bit) & bit) ? 0 : 1;
+        }
+      }
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int v = threadIdx.x < kHeavyBlock / 32 ? s_red[threadIdx.x] : 0;
+      v = __reduce_add_sync(0xffffffffu, v);
+      if (threadIdx.x == 0 && v) atomicAdd(&rowtiles[b], v);
+    }
+    for (int i = threadIdx.x; i < kBmBits / 128; i += kHeavyBlock) bm4[i] = make_uint4(0, 0, 0, 0);
+  }
+}
+
 __global__ void k_sum_rowtiles(const int32_t *__restrict__ rowtiles, int32_t nb,
                                unsigned long long *__restrict__ total) {
   unsigned long long s = 0;
@@ -154,10 +296,10 @@ struct Items {
   int64_t n_items = 0;
   void *tmp = nullptr;
   ~Items() {
-    cudaFree(start);
-    cudaFree(row);
-    cudaFree(cnt);
-    cudaFree(tmp);
+    dev_free(start);
+    dev_free(row);
+    dev_free(cnt);
+    dev_free(tmp);
   }
 };
 
@@ -170,7 +312,7 @@ int plan_items(tcmis_graph *g, int T, int32_t nb, Items &it) {
   size_t bytes = 0;
   TCMIS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, it.start, it.start, (int64_t)nb + 1,
                                            st));
-  TCMIS_CUDA(cudaMalloc(&it.tmp, bytes));
+  if (int rc_ = dev_alloc((char **)&it.tmp, bytes)) return rc_;
   // the extra (nb-th) slot is garbage before the scan; zero it so the scan
   // yields start[nb] = total items
   TCMIS_CUDA(cudaMemsetAsync(it.start + nb, 0, sizeof(int64_t), st));
@@ -196,7 +338,7 @@ int build_tile_counts(tcmis_graph *g, int T) {
   tcmis_ctx *ctx = g->ctx;
   cudaStream_t st = ctx->stream;
   const int32_t nb = (int32_t)(((int64_t)g->n + T - 1) / T);
-  cudaFree(g->d_rowtiles);
+  dev_free(g->d_rowtiles);
   g->d_rowtiles = nullptr;
   g->tile_T = 0;
   g->tile_nb = nb;
@@ -204,12 +346,24 @@ int build_tile_counts(tcmis_graph *g, int T) {
   if (int rc = dev_alloc(&g->d_rowtiles, (size_t)nb + 1)) return rc;
   TCMIS_CUDA(cudaMemsetAsync(g->d_rowtiles, 0, sizeof(int32_t) * ((size_t)nb + 1), st));
   if (nb > 0) {
-    Items it;
-    if (int rc = plan_items(g, T, nb, it)) return rc;
-    k_tile_merge<false><<<grid_for(ctx, 32 * it.n_items, 256, 16), 256, 0, st>>>(
-        g->n, T, nb, g->d_off, g->d_nbr, it.n_items, it.row, it.start, it.cnt, g->d_rowtiles,
-        nullptr, nullptr, nullptr, nullptr);
+    int32_t *heavy = nullptr, *cnt = nullptr;
+    if (int rc = dev_alloc(&heavy, (size_t)nb)) return rc;
+    unsigned long long *next_item = nullptr;
+    if (int rc = dev_alloc(&cnt, 1)) return rc;
+    if (int rc = dev_alloc(&next_item, 1)) return rc;
+    TCMIS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t), st));
+    TCMIS_CUDA(cudaMemsetAsync(next_item, 0, sizeof(unsigned long long), st));
+    k_count_light<<<grid_for(ctx, 32ll * nb, kLightBlock, 8), kLightBlock, 0, st>>>(
+        g->n, T, nb, g->d_off, g->d_nbr, g->d_rowtiles, heavy, cnt);
     TCMIS_LAUNCHED(ctx);
+    const int32_t windows = (int32_t)(((int64_t)nb + kBmBits - 1) / kBmBits);
+    k_count_heavy<<<ctx->num_sms * 4, kHeavyBlock, 0, st>>>(
+        g->n, T, nb, g->d_off, g->d_nbr, g->d_rowtiles, heavy, cnt, windows,
+        next_item);
+    TCMIS_LAUNCHED(ctx);
+    dev_free(heavy);
+    dev_free(cnt);
+    dev_free(next_item);
     unsigned long long *d_total = nullptr;
     if (int rc = dev_alloc(&d_total, 1)) return rc;
     cudaMemsetAsync(d_total, 0, 8, st);
@@ -218,7 +372,7 @@ int build_tile_counts(tcmis_graph *g, int T) {
     unsigned long long total = 0;
     cudaMemcpyAsync(&total, d_total, 8, cudaMemcpyDeviceToHost, st);
     cudaError_t e = cudaStreamSynchronize(st);
-    cudaFree(d_total);
+    dev_free(d_total);
     if (e != cudaSuccess) return cuda_error(e, "tile counts");
     g->tile_total = (int64_t)total;
   }
@@ -259,7 +413,7 @@ int export_tiles(tcmis_graph *g, int T, int32_t *tile_row, int32_t *tile_col,
     size_t bytes = 0;
     void *tmp = nullptr;
     cub::DeviceScan::ExclusiveSum(nullptr, bytes, it.cnt, item_off, it.n_items, st);
-    cudaMalloc(&tmp, bytes);
+    dev_alloc((char **)&tmp, bytes);
     cub::DeviceScan::ExclusiveSum(tmp, bytes, it.cnt, item_off, it.n_items, st);
     k_tile_merge<true><<<grid_for(ctx, 32 * it.n_items, 256, 16), 256, 0, st>>>(
         g->n, T, nb, g->d_off, g->d_nbr, it.n_items, it.row, it.start, it.cnt, scratch_rows,
@@ -272,7 +426,7 @@ int export_tiles(tcmis_graph *g, int T, int32_t *tile_row, int32_t *tile_col,
     cudaMemcpyAsync(tile_col, d_tc, 4ull * tiles, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(row_bits, d_rb, 8ull * tiles * T, cudaMemcpyDeviceToHost, st);
     cudaError_t e = cudaStreamSynchronize(st);
-    cudaFree(tmp);
+    dev_free(tmp);
     if (e != cudaSuccess) {
       rc = cuda_error(e, "export tiles");
     } else {
@@ -280,11 +434,11 @@ int export_tiles(tcmis_graph *g, int T, int32_t *tile_row, int32_t *tile_col,
       bro[nb] = tiles;
     }
   }
-  cudaFree(scratch_rows);
-  cudaFree(item_off);
-  cudaFree(d_tr);
-  cudaFree(d_tc);
-  cudaFree(d_rb);
+  dev_free(scratch_rows);
+  dev_free(item_off);
+  dev_free(d_tr);
+  dev_free(d_tc);
+  dev_free(d_rb);
   return rc;
 }
 
