@@ -14,8 +14,19 @@ A "step" is one complete MIS solve (H2 priorities -> bulk-synchronous rounds
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config rmat22]
   python bench.py --impl reference ...   (the reference CPU implementation)
 
-Configs (BASELINE.json): er (n=100k, d=16), grid (4096^2), rmat22 (default,
-the metric's headline), rgg (24M, d~3), rmat26 (~1.05B edges).
+Configs (BASELINE.json): er (n=100k, d=16), grid (4096^2), rmat22 (default at
+N = 1, the metric's headline), rgg (24M, d~3), rmat26 (~1.05B edges; default
+at N > 1).
+
+N > 1 (torchrun, one rank per GPU): the north-star's row-partitioned solve
+(paper_2605_29604_b200/distributed.py): every rank generates the
+graph on its GPU, keeps its edge-balanced row range, and the ranks run the
+bulk-synchronous rounds with NCCL all-gathers of the candidate / removal
+bitmaps and an all-reduce of the round counters.  One step = one solve of the
+WHOLE graph by all ranks together ("scaling": "strong"); the time is the max
+over ranks of CUDA-event time on each rank's engine stream.  Rank 0 also
+solves the same graph alone on its GPU before partitioning
+("single_gpu_same_graph"), so the line carries its own 1-GPU denominator.
 """
 from __future__ import annotations
 
@@ -151,11 +162,9 @@ def run_ours(args) -> dict:
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    dist = None
     if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        return run_partitioned(args, rank, world, local)
+    dist = None
     torch.cuda.set_device(local)
     ctx = tc.Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
@@ -168,7 +177,8 @@ def run_ours(args) -> dict:
     tiles = dg.tile(16)
     log(f"[bench] {args.config}: n={n} m={m} tiles={tiles} (setup {time.time() - t0:.1f}s)")
     excl = {"auto": tc.Exclusion.AUTO, "push": tc.Exclusion.PUSH,
-            "pull": tc.Exclusion.CSR_PULL}[args.exclusion]
+            "pull": tc.Exclusion.CSR_PULL, "tile-bits": tc.Exclusion.TILE_BITS,
+            "tile-mma": tc.Exclusion.TILE_MMA}[args.exclusion]
     cfg = tc.EngineConfig(heuristic=HEUR[args.heuristic], seed=1, tile_dim=16, exclusion=excl)
     c_cfg, _keep = cfg._c()
 
@@ -227,9 +237,7 @@ def run_ours(args) -> dict:
             kern.setdefault((name, rnd), []).append(ms)
     kernels = sorted(((k[0], k[1], sum(v) / len(v)) for k, v in kern.items()),
                      key=lambda x: -x[2])
-    roofline = kernel_roofline(tc, dg, cfg, kernels, args)
-    if roofline:
-        roofline["share_of_step"] = round(roofline["launch_ms"] / ms_per_step, 4)
+    roofline = kernel_roofline(tc, dg, cfg, kernels, args, ms_per_step)
     # ---- e2e through the drop-in C-ABI with host buffers
     e2e = run_e2e(tc, torch, dg, ctx, stream, cfg, args, local, dist, flush)
 
@@ -271,74 +279,85 @@ def timeline(tc, ctx):
     return [(buf[i].name.decode(), int(buf[i].round), float(buf[i].ms)) for i in range(n)]
 
 
-K_PROBE = 4  # entries the probe kernels examine (select.cuh kProbeK, update.cuh kPullK)
+# kernel -> phase of the reference's round (engine.cpp:247-291); k_round_end
+# also scans the pull exclusion's longest rows but is booked as Phase 3
+PHASE = {"k_probe_select": 1, "k_select": 1, "k_select_long": 1,
+         "k_probe_pull": 2, "k_update_pull": 2, "k_tile_excl_bits": 2, "k_tile_excl_mma": 2,
+         "k_update": 3, "k_round_end": 3, "k_priorities": 0}
+PHASE_NAME = {0: "init (priorities, states)", 1: "Phase 1 candidate detection",
+              2: "Phase 2 neighbour exclusion (SpMV)", 3: "Phase 3 state update + compaction",
+              12: "Phases 1+2 (push exclusion fused into candidate detection)"}
 
 
-def kernel_roofline(tc, dg, cfg, kernels, args):
-    """Roofline of the dominant kernel that has a byte model (DESIGN.md
-    "Roofline").  k_probe_select, per launch over its worklist W:
-      sum_{v in W} [4 (list) + 8 (row extent) + 8 (own key)
-                    + min(deg v, 4) * (4 B neighbour id + 8 B neighbour key)]
-      + 2 B per settled candidate (next, state) [+ 1 B per pushed neighbour].
-    The algorithm's bytes at element granularity, computed from the round-1
-    degrees on the host; the kernel time is the CUDA-event time above."""
+def kernel_roofline(tc, dg, cfg, kernels, args, ms_per_step):
+    """Roofline of the dominant phase-round, SURVEY 8(d) algorithmic bytes.
+
+    The unit of one "launch" is the kernel sequence of one phase in one round
+    (the kernels split the phase's vertices between a straight-line probe and
+    the scan engines, so no single kernel owns a unit).  Bytes per unit
+    (SURVEY 8(d), format-independent): init 13 n; Phase 1 12 |A_k| + 4 nnz(A_k);
+    Phase 2 8 |A_k \\ C_k| + 4 nnz(A_k \\ C_k); Phase 3 2 |A_k|, from the
+    round's own trajectory (observer snapshots, outside the timed region).
+    Time = the mean CUDA-event duration of those kernels.  Early exit means the
+    kernels read fewer bytes than the algorithm's: `traffic` (ncu DRAM bytes,
+    profiles/ncu_summary.json) shows what they actually moved."""
     import numpy as np
-    h = dg.download()
-    deg = np.diff(h.offsets)
     hbm, peak_kind = peaks()
-    times = {(k, r): ms for k, r, ms in kernels}
-    nz = deg[deg > 0]
-    kk = np.minimum(nz, K_PROBE)
-    b_probe = int((4 + 8 + 8) * nz.size + 12 * kk.sum())
-    # candidates settled by the probe: rows <= 4 that nobody blocks; counted
-    # from the observer snapshot of round 1
-    cand1 = round1_candidates(tc, dg, cfg)
-    small = cand1 & (deg <= K_PROBE) & (deg > 0)
-    b_probe += int(2 * small.sum())
-    models = {("k_probe_select", 1): b_probe}
-    best = None
-    for (name, rnd), b in models.items():
-        if (name, rnd) in times:
-            ms = times[(name, rnd)]
-            if best is None or ms > best[2]:
-                best = (name, rnd, ms, b)
-    if best is None:
+    traj = trajectory_terms(tc, dg, cfg)
+    n = dg.n
+    push = not any(k in ("k_probe_pull", "k_update_pull", "k_tile_excl_bits", "k_tile_excl_mma")
+                   for k, _, _ in kernels)
+    acc = {}
+    for name, rnd, ms in kernels:
+        ph = PHASE.get(name)
+        if ph is None:
+            continue
+        if push and ph in (1, 2):
+            ph = 12
+        key = (ph, rnd if ph else 0)
+        e = acc.setdefault(key, {"ms": 0.0, "kernels": []})
+        e["ms"] += ms
+        e["kernels"].append(name)
+    phases = []
+    for (ph, rnd), e in sorted(acc.items()):
+        if ph == 0:
+            b = 13 * n
+        else:
+            if rnd < 1 or rnd > len(traj):
+                continue
+            A, nnzA, NC, nnzNC = traj[rnd - 1]
+            b1, b2, b3 = 12 * A + 4 * nnzA, 8 * NC + 4 * nnzNC, 2 * A
+            b = {1: b1, 2: b2, 3: b3, 12: b1 + b2}[ph]
+        ach = b / (e["ms"] * 1e-3) / 1e9 if e["ms"] > 0 else 0.0
+        phases.append({"phase": PHASE_NAME[ph], "round": rnd, "kernels": e["kernels"],
+                       "algorithmic_bytes": int(b), "ms": round(e["ms"], 4),
+                       "achieved": round(ach, 1), "frac": round(ach / hbm, 4)})
+    if not phases:
         return None
-    name, rnd, ms, b = best
-    ach = b / (ms * 1e-3) / 1e9
-    return {"kernel": f"{name} (round {rnd})", "bound": "hbm", "achieved": round(ach, 1),
-            "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / hbm, 4),
-            "algorithmic_bytes": b, "launch_ms": round(ms, 4),
-            "traffic": traffic_from_profiles(args.config, name),
-            "share_of_step": None}
-
-
-def round1_candidates(tc, dg, cfg):
-    import numpy as np
-    out = {}
-
-    def obs(it, cand, states):
-        if it == 1:
-            out["c"] = cand.astype(bool)
-
-    c2 = tc.EngineConfig(heuristic=cfg.heuristic, seed=cfg.seed, tile_dim=cfg.tile_dim,
-                         iteration_observer=obs)
-    if c2.heuristic == tc.Heuristic.H3:
-        c2.heuristic = tc.Heuristic.H2
-    tc.run_mis(dg, c2)
-    return out.get("c", np.zeros(dg.n, bool))
-
-
-def traffic_from_profiles(config, kernel):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the
-    committed ncu --set full summary (profiles/ncu_summary.json), or None."""
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    dom = max(phases, key=lambda p: p["ms"])
+    traffic = None
     try:
-        with open(path) as f:
-            d = json.load(f)
-        return d[config][kernel]["dram_bytes"]
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            summ = json.load(f).get(args.config, {})
+        parts = [summ[k]["dram_bytes"] for k in dom["kernels"] if k in summ]
+        if parts and len(parts) == len(dom["kernels"]):
+            traffic = int(sum(parts))
     except Exception:
-        return None
+        traffic = None
+    total_b = 13 * n + sum(12 * A + 4 * nnzA + 8 * NC + 4 * nnzNC + 2 * A
+                           for A, nnzA, NC, nnzNC in traj)
+    solve_ach = total_b / (ms_per_step * 1e-3) / 1e9
+    return {"kernel": f"{dom['phase']}, round {dom['round']}: " + " + ".join(dom["kernels"]),
+            "bound": "hbm", "achieved": dom["achieved"], "peak": hbm, "peak_kind": peak_kind,
+            "unit": "GB/s", "frac": dom["frac"], "traffic": traffic,
+            "algorithmic_bytes": dom["algorithmic_bytes"], "launch_ms": dom["ms"],
+            "share_of_step": round(dom["ms"] / ms_per_step, 4),
+            "definition": "SURVEY 8(d) algorithmic bytes of the phase-round / summed CUDA-event "
+                          "time of its kernels (step-wise timing solve); traffic = ncu DRAM "
+                          "bytes of the same kernels",
+            "phases": phases,
+            "solve": {"algorithmic_bytes": int(total_b), "ms": round(ms_per_step, 4),
+                      "achieved": round(solve_ach, 1), "frac": round(solve_ach / hbm, 4)}}
 
 
 def trajectory_terms(tc, dg, cfg):
@@ -432,6 +451,163 @@ def run_e2e(tc, torch, dg, ctx, stream, cfg, args, local, dist, flush):
             "ms": round(ms, 3), "h2d_bytes_per_step": int(8 * (n + 1) + 4 * nnz),
             "d2h_bytes_per_step": int(4 * cnt + 64 * 4096), "steps": steps,
             "path": "tcmis_graph_upload + tcmis_graph_tile + tcmis_solve (host buffers)"}
+
+
+# ------------------------------------------- N > 1: row-partitioned solve
+
+def run_partitioned(args, rank: int, world: int, local: int) -> dict | None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_29604_b200 as tc
+    from paper_2605_29604_b200 import distributed as D
+
+    ndev = max(1, torch.cuda.device_count())
+    dev = local % ndev  # one GPU per rank; ranks share a GPU only in emulation runs
+    torch.cuda.set_device(dev)
+    device = f"cuda:{dev}"
+    dist.init_process_group(args.dist_backend)
+    ctx = tc.Context(dev)
+    L = tc.load()
+    t0 = time.time()
+    full = make_device_graph(tc, args.config, ctx)
+    n, nnz = full.n, full.nnz
+    m = nnz // 2
+    off = np.zeros(n + 1, np.int64)
+    tc._check(L.tcmis_graph_download(full.h, tc._ptr(off), None))
+    rank_lo = D.partition_rows(off, world, 16)
+    log(f"[bench:rank{rank}] {args.config}: n={n} m={m} rows [{rank_lo[rank]}, "
+        f"{rank_lo[rank + 1]}) (setup {time.time() - t0:.1f}s)")
+    single = None
+    if rank == 0 and not args.no_single:
+        # the same graph solved by one GPU (this rank's, alone), device-resident
+        cfg1 = tc.EngineConfig(heuristic=HEUR[args.heuristic], seed=1, tile_dim=16)
+        full.tile(16)
+        for _ in range(2):
+            tc.run_mis(full, cfg1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st1 = torch.cuda.ExternalStream(ctx.stream, device=device)
+        ms1 = []
+        for _ in range(3):
+            with torch.cuda.stream(st1):
+                e0.record(st1)
+            r1 = tc.run_mis(full, cfg1)
+            with torch.cuda.stream(st1):
+                e1.record(st1)
+            torch.cuda.synchronize()
+            ms1.append(e0.elapsed_time(e1))
+        single = {"ms": round(sorted(ms1)[1], 4),
+                  "value": round(m / (sorted(ms1)[1] * 1e-3) / 1e9, 4),
+                  "iterations": len(r1.iterations), "mis_size": r1.cardinality()}
+    me = D.GpuRank(ctx, n, rank_lo[rank], rank_lo[rank + 1], None, None, device, full=full)
+    full.close()
+    stream = torch.cuda.ExternalStream(ctx.stream, device=device)
+
+    def solve():
+        return D.solve_partitioned(me, rank_lo, rank, world, dist, heuristic=args.heuristic,
+                                   seed=1, tile_dim=16)
+
+    for _ in range(args.warmup):
+        res = solve()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches()
+    with ClockSampler(dev) as clk:
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                ev[k][0].record(stream)
+            res = solve()
+            with torch.cuda.stream(stream):
+                ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.launches() - launches0
+    tdev = device if args.dist_backend == "nccl" else "cpu"  # gloo reduces host tensors
+    total = torch.tensor([sum(a.elapsed_time(b) for a, b in ev)], device=tdev)
+    dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    ms_per_step = float(total.item()) / args.steps
+    # result: |MIS| over all ranks (own ranges), rounds from the all-reduced stats
+    mis_own = torch.tensor([int((res.own_state == 1).sum())], device=tdev)
+    dist.all_reduce(mis_own)
+    mis_size = int(mis_own.item())
+    # e2e: the drop-in host path per rank (own rows uploaded from pinned host
+    # CSR with the full offsets, solve, own VertexStates back to the host)
+    e2e = None
+    if not args.no_e2e:
+        own_rows = np.zeros(max(1, int(off[rank_lo[rank + 1]] - off[rank_lo[rank]])), np.int32)
+        tc._check(L.tcmis_graph_download(me.g.h, tc._ptr(np.zeros(n + 1, np.int64)),
+                                         tc._ptr(own_rows)))
+        own_rows = torch.from_numpy(own_rows[:int(off[rank_lo[rank + 1]] - off[rank_lo[rank]])])
+        own_rows = own_rows.pin_memory().numpy()
+        h_off = torch.from_numpy(off).pin_memory().numpy()
+        steps = max(1, min(args.steps, 5))
+        e_ms = []
+        for k in range(steps + 1):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t_a = time.perf_counter()
+            rk = D.GpuRank(ctx, n, rank_lo[rank], rank_lo[rank + 1], h_off, None, device,
+                           rows=own_rows)
+            D.solve_partitioned(rk, rank_lo, rank, world, dist, heuristic=args.heuristic,
+                                seed=1, tile_dim=16)
+            rk.close()
+            torch.cuda.synchronize()
+            t_b = time.perf_counter()
+            if k:
+                e_ms.append((t_b - t_a) * 1e3)
+        t = torch.tensor([sum(e_ms) / len(e_ms)], device=tdev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms1 = float(t.item())
+        own_nnz = int(own_rows.size)
+        hb = torch.tensor([8 * (n + 1) + 4 * own_nnz, max(0, rank_lo[rank + 1] - rank_lo[rank])],
+                          device=tdev, dtype=torch.int64)
+        dist.all_reduce(hb)
+        e2e = {"value": round(m / (e_ms1 * 1e-3) / 1e9, 4), "unit": "Gedges/s",
+               "ms": round(e_ms1, 3), "h2d_bytes_per_step": int(hb[0]),
+               "d2h_bytes_per_step": int(hb[1]), "steps": steps,
+               "clock": "host wall clock between barriers (max over ranks)",
+               "path": "tcmis_graph_upload_partition (own rows, pinned host CSR) + the "
+                       "partitioned rounds + tcmis_dist_state, per rank"}
+    line = {
+        "metric": "Gedges/s (MIS solve, BASELINE config)",
+        "value": round(m / (ms_per_step * 1e-3) / 1e9, 4), "unit": "Gedges/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32 priorities (integer), f64 priority value",
+        "data": "synthetic (generated on every GPU, bit-identical to the reference generator)",
+        "config": {"workload": CONFIGS[args.config]["workload"], "graph": args.config, "n": n,
+                   "m": m, "heuristic": args.heuristic, "seed": 1, "tile_dim": 16,
+                   "iterations": len(res.rounds), "mis_size": mis_size,
+                   "parallelism": f"row-partitioned x{world} (NCCL all-gather of candidate / "
+                                  f"removal bitmaps, all-reduce of round counters)",
+                   "rank_lo": rank_lo, "backend": args.dist_backend,
+                   "l2": "no flush: the per-rank CSR slices exceed L2 at s26"},
+        "mis_ms": round(ms_per_step, 4),
+        "single_gpu_same_graph": single,
+        "roofline": None, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sampled(tc, ctx, args)
+    dist.barrier()
+    dist.destroy_process_group()
+    return line if rank == 0 else None
+
+
+def cpu_baseline_sampled(tc, ctx, args) -> dict:
+    """Bounded CPU sample for the s26 workload: the reference's identical-output
+    path on rmat_graph(SAMPLE_SCALE, 16, 1) (its P2 is serial, so the CPU's
+    Gedges/s falls with scale: the sample OVER-states the CPU on s26)."""
+    dg = tc.DeviceGraph.rmat(SAMPLE_SCALE, 16, 1, ctx)
+    b = cpu_baseline(dg, args)
+    b["sample"] = (f"rmat_graph({SAMPLE_SCALE},16,1) (a bounded sample of the {args.config} "
+                   f"workload): " + b.get("sample", ""))
+    dg.close()
+    return b
+
+
+SAMPLE_SCALE = 23
 
 
 # ------------------------------------------------------ reference (CPU)
@@ -546,14 +722,22 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="rmat22", choices=list(CONFIGS))
+    ap.add_argument("--config", default=None, choices=list(CONFIGS),
+                    help="default: rmat22 at N = 1, rmat26 (row-partitioned) at N > 1")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: single-GPU emulation of N ranks (test only)")
+    ap.add_argument("--no-single", action="store_true",
+                    help="N > 1: skip rank 0's single-GPU solve of the same graph")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--heuristic", default="h2", choices=list(HEUR))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exclusion", default="auto", choices=["auto", "push", "pull"])
+    ap.add_argument("--exclusion", default="auto", choices=["auto", "push", "pull", "tile-bits", "tile-mma"])
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the dominant kernel (profiles/)")
     args = ap.parse_args()
+    if args.config is None:
+        args.config = "rmat26" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "rmat22"
     if args.warmup < 3:
         log("[bench] warmup raised to 3 (timing rules)")
         args.warmup = 3

@@ -150,6 +150,13 @@ int tcmis_graph_set_tiling(tcmis_graph *g, int32_t tile_dim, const int64_t *bloc
  * tcmis_graph_tile()'s count. */
 int tcmis_graph_export_tiles(tcmis_graph *g, int32_t tile_dim, int32_t *tile_row,
                              int32_t *tile_col, uint64_t *row_bits, int64_t *block_row_offsets);
+/* The compact device tile store the tile-form exclusion kernels read
+ * (tile_dim 8 or 16; same tile set and order as tile_graph, tiling.cpp:44-84):
+ * builds it if needed and reports its tile count; with non-null buffers also
+ * copies block_row_offsets[nb+1], tile_col[tiles] and the payload (T rows of
+ * T bits per tile: u16 rows for T = 16, u8 rows for T = 8) to the host. */
+int tcmis_graph_tile_store(tcmis_graph *g, int32_t tile_dim, int64_t *tile_count,
+                           int64_t *block_row_offsets, int32_t *tile_col, void *payload);
 
 /* priorities.cpp:33-67 (h1_random / h2_degree_aware) on the device; p_out is
  * a host buffer of n entries. */
@@ -182,20 +189,25 @@ int tcmis_solve_device(tcmis_graph *g, const tcmis_config *cfg, const int32_t **
  *   tcmis_dist_select  -> own candidates as bitmap slice d_bits (bit v - lo)
  *   (host all-gathers the slices, rank r's at word r * maxw)
  *   tcmis_dist_apply(what = 0) -> remote candidates marked
- *   tcmis_dist_update  -> own removals as bitmap slice; counts[5] = this
- *                         rank's (selected, removed, alive, tiles_eval, tiles_skip)
- *   (host all-gathers, all-reduces the counts)
+ *   tcmis_dist_update  -> own removals as bitmap slice; d_counts[5] (DEVICE
+ *                         memory) = this rank's (selected, removed, alive,
+ *                         tiles_eval, tiles_skip)
+ *   (host all-gathers, all-reduces the counts on the device)
  *   tcmis_dist_apply(what = 1) -> remote removals applied
  * until the all-reduced alive count is 0; tcmis_dist_state copies the own
- * range's VertexStates.  rank_lo has world + 1 entries (rank_lo[world] = n). */
+ * range's VertexStates.  rank_lo has world + 1 entries (rank_lo[world] = n).
+ * Every call is stream-ordered on the context stream without a host sync, so
+ * NCCL collectives enqueued on that stream (tcmis_ctx_stream) interleave. */
 int tcmis_graph_upload_partition(tcmis_ctx *ctx, int32_t n, int32_t lo, int32_t hi,
                                  const int64_t *full_offsets, const int32_t *row_neighbors,
                                  tcmis_graph **out);
+/* The same partition cut from a device-resident full graph (device to device). */
+int tcmis_graph_partition(tcmis_graph *full, int32_t lo, int32_t hi, tcmis_graph **out);
 int tcmis_dist_begin(tcmis_graph *g, const tcmis_config *cfg);
 int tcmis_dist_select(tcmis_graph *g, uint32_t *d_bits, int32_t words);
 int tcmis_dist_apply(tcmis_graph *g, const uint32_t *d_gathered, const int32_t *rank_lo,
                      int32_t world, int32_t maxw, int32_t me, int32_t what);
-int tcmis_dist_update(tcmis_graph *g, uint32_t *d_bits, int32_t words, int64_t *counts);
+int tcmis_dist_update(tcmis_graph *g, uint32_t *d_bits, int32_t words, int64_t *d_counts);
 int tcmis_dist_state(tcmis_graph *g, uint8_t *own_state);
 /* h3 on a partition: after the rounds, this rank's share of the collapsed
  * iteration's tiles_evaluated and its tile total (sum over ranks on the host). */

@@ -132,6 +132,7 @@ def load():
         "tcmis_graph_tile": (C.c_int, [vp, i32, P(i64)]),
         "tcmis_graph_set_tiling": (C.c_int, [vp, i32, vp, i32]),
         "tcmis_graph_export_tiles": (C.c_int, [vp, i32, vp, vp, vp, vp]),
+        "tcmis_graph_tile_store": (C.c_int, [vp, i32, P(i64), vp, vp, vp]),
         "tcmis_priorities": (C.c_int, [vp, i32, u64, i32, vp]),
         "tcmis_solve": (C.c_int, [vp, P(_Config), vp, vp, P(i64), P(_Stats), i32, P(i32)]),
         "tcmis_solve_device": (C.c_int, [vp, P(_Config), P(vp), P(i64), P(vp), P(_Stats), i32,
@@ -521,6 +522,23 @@ def tile_graph(g, tile_dim: int = 16, ctx: Optional[Context] = None) -> TiledAdj
                                            _ptr(bro)))
     return TiledAdjacency(tile_dim, dg.n, nb * tile_dim, tr[:cnt], tc[:cnt], rb[:cnt * tile_dim],
                           bro)
+
+
+def tile_store(g, tile_dim: int = 16, ctx: Optional[Context] = None):
+    """The compact device tile store (T = 8 / 16) the tile-form exclusion
+    kernels read: (block_row_offsets, tile_col, rows) with rows[t, i] the T
+    bits of row i of tile t."""
+    dg = _as_device(g, ctx)
+    cnt = C.c_int64(0)
+    L = load()
+    _check(L.tcmis_graph_tile_store(dg.h, tile_dim, C.byref(cnt), None, None, None))
+    nb = (dg.n + tile_dim - 1) // tile_dim
+    bro = np.zeros(nb + 1, np.int64)
+    col = np.zeros(max(cnt.value, 1), np.int32)
+    rows = np.zeros((max(cnt.value, 1), tile_dim), np.uint16 if tile_dim == 16 else np.uint8)
+    _check(L.tcmis_graph_tile_store(dg.h, tile_dim, C.byref(cnt), _ptr(bro), _ptr(col),
+                                    _ptr(rows)))
+    return bro, col[:cnt.value], rows[:cnt.value]
 
 
 def _priorities(g, heuristic: Heuristic, seed: int, scale_bits: int, ctx=None) -> np.ndarray:

@@ -46,6 +46,7 @@ int gen_rgg(tcmis_ctx *ctx, int32_t n, uint64_t R, uint64_t seed, tcmis_graph **
 int gen_gnp_host(int32_t n, double avg_degree, uint64_t seed, int64_t **offsets,
                  int32_t **neighbors, int64_t *nnz_out);
 int h1_impl(tcmis_ctx *ctx, int32_t n, uint64_t seed, uint32_t *p_out);
+int partition_device(tcmis_graph *full, int32_t lo, int32_t hi, tcmis_graph **out);
 int upload_partition(tcmis_ctx *ctx, int32_t n, int32_t lo, int32_t hi, const int64_t *full,
                      const int32_t *rows, tcmis_graph **out);
 int dist_begin(tcmis_graph *g, const tcmis_config *cfg);
@@ -223,6 +224,7 @@ TCMIS_API void tcmis_graph_destroy(tcmis_graph *g) {
   dev_free(g->d_rowtiles);
   dev_free(g->d_nz);
   dev_free(g->d_off_full);
+  free_tile_store(g);
   Workspace &sp = g->ctx->spare;
   if (g->ws.ctrl && g->ws.n_cap >= sp.n_cap) {
     free_workspace(sp);
@@ -247,7 +249,7 @@ TCMIS_API int tcmis_graph_download(tcmis_graph *g, int64_t *offsets, int32_t *ne
   NEED(g && offsets, "null handle");
   cudaStream_t st = g->ctx->stream;
   TCMIS_CUDA(cudaMemcpyAsync(offsets, g->d_off, 8ull * (g->n + 1), cudaMemcpyDeviceToHost, st));
-  if (g->nnz)
+  if (g->nnz && neighbors)
     TCMIS_CUDA(cudaMemcpyAsync(neighbors, g->d_nbr, 4ull * g->nnz, cudaMemcpyDeviceToHost, st));
   TCMIS_CUDA(cudaStreamSynchronize(st));
   return 0;
@@ -288,6 +290,27 @@ TCMIS_API int tcmis_graph_export_tiles(tcmis_graph *g, int32_t T, int32_t *tile_
   NEED(g && bro, "null handle");
   ENTER(g->ctx);
   return export_tiles(g, T, tile_row, tile_col, row_bits, bro);
+}
+
+TCMIS_API int tcmis_graph_tile_store(tcmis_graph *g, int32_t T, int64_t *tile_count,
+                                     int64_t *bro, int32_t *tile_col, void *payload) {
+  NEED(g, "null graph");
+  ENTER(g->ctx);
+  if (int rc = build_tile_store(g, T)) return rc;
+  const int32_t nb = (int32_t)(((int64_t)g->n + T - 1) / T);
+  int64_t tiles = 0;
+  cudaStream_t st = g->ctx->stream;
+  TCMIS_CUDA(cudaMemcpyAsync(&tiles, g->d_tbro + nb, 8, cudaMemcpyDeviceToHost, st));
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  if (tile_count) *tile_count = tiles;
+  if (bro) TCMIS_CUDA(cudaMemcpyAsync(bro, g->d_tbro, 8ull * (nb + 1), cudaMemcpyDeviceToHost, st));
+  if (tile_col && tiles)
+    TCMIS_CUDA(cudaMemcpyAsync(tile_col, g->d_tcol, 4ull * tiles, cudaMemcpyDeviceToHost, st));
+  if (payload && tiles)
+    TCMIS_CUDA(cudaMemcpyAsync(payload, g->d_tbits, (size_t)tiles * T * (T / 8),
+                               cudaMemcpyDeviceToHost, st));
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  return 0;
 }
 
 TCMIS_API int tcmis_priorities(tcmis_graph *g, int32_t heuristic, uint64_t seed,
@@ -344,6 +367,13 @@ TCMIS_API int tcmis_graph_upload_partition(tcmis_ctx *ctx, int32_t n, int32_t lo
   return upload_partition(ctx, n, lo, hi, full_offsets, row_neighbors, out);
 }
 
+TCMIS_API int tcmis_graph_partition(tcmis_graph *full, int32_t lo, int32_t hi,
+                                    tcmis_graph **out) {
+  NEED(full && out, "null handle");
+  ENTER(full->ctx);
+  return partition_device(full, lo, hi, out);
+}
+
 TCMIS_API int tcmis_dist_begin(tcmis_graph *g, const tcmis_config *cfg) {
   NEED(g && cfg, "null handle");
   ENTER(g->ctx);
@@ -367,7 +397,7 @@ TCMIS_API int tcmis_dist_apply(tcmis_graph *g, const uint32_t *d_gathered,
 
 TCMIS_API int tcmis_dist_update(tcmis_graph *g, uint32_t *d_bits, int32_t words,
                                 int64_t *counts) {
-  NEED(g && d_bits && counts, "null handle");
+  NEED(g && d_bits && counts, "null handle");  // counts: device int64[5]
   ENTER(g->ctx);
   return dist_update(g, d_bits, words, counts);
 }

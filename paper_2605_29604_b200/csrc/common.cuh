@@ -9,6 +9,21 @@ constexpr int kBlock = 256;    // threads per block of the round kernels
 constexpr int kStep = 4;       // row entries per thread-level step
 constexpr int kThreadMax = 32; // entries a thread examines before handing a row to a warp
 
+// Loads of the CSR (offsets, neighbour ids): read once per phase, so they are
+// marked evict-first (ld.global.cs) and do not push the randomly gathered
+// priority / state / decision vectors out of L2.
+#ifndef TCMIS_STREAM_HINTS
+#define TCMIS_STREAM_HINTS 1
+#endif
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T *p) {
+#if TCMIS_STREAM_HINTS
+  return __ldcs(p);
+#else
+  return __ldg(p);
+#endif
+}
+
 // per-thread work modes of the state-machine kernels
 enum : int { kFetch = 0, kScan = 1, kPush = 2, kDone = 3 };
 
@@ -70,16 +85,33 @@ __device__ __forceinline__ void publish(const Publish &p, int32_t v) {
 }
 
 // An alive non-candidate with a candidate neighbour is removed
-// (engine.cpp:144-147); key 0 == kNoNeighborKey makes it invisible to the
-// alive vertices that still neighbour it.
-__device__ __forceinline__ void mark_removed(int32_t v, uint8_t *state, uint64_t *key) {
+// (engine.cpp:144-147); state Removed makes it invisible (kNoNeighborKey) to
+// the alive vertices that still neighbour it from the next round on.
+__device__ __forceinline__ void mark_removed(int32_t v, uint8_t *state) {
   state[v] = TCMIS_REMOVED;
-  key[v] = 0;
 }
 
-__device__ __forceinline__ uint64_t fresh_key(int32_t v, uint64_t fresh_m) {
+// priority_key (priorities.hpp:61-64): strict (p, id) order, never 0
+__device__ __forceinline__ uint64_t key_of(uint32_t p, int32_t v) {
+  return ((uint64_t)p << 32) | (uint64_t)(uint32_t)(v + 1);
+}
+
+// A neighbour u blocks v (compute_max_np + generate_candidates,
+// engine.cpp:86-119) iff u is alive at the start of the round and its key is
+// above v's.  Round 1 starts with every vertex alive, so the state gather is
+// skipped there.  Candidates of the running round turn InMIS while the
+// select kernels run; they stay visible (only Removed hides a vertex, and
+// removals are written by the update kernels after the select kernels).
+__device__ __forceinline__ bool blocks(const uint32_t *__restrict__ prio,
+                                       const uint8_t *state, bool r1, int32_t u, uint64_t kv) {
+  const uint32_t pu = __ldg(&prio[u]);
+  const bool vis = r1 || state[u] != TCMIS_REMOVED;
+  return vis && key_of(pu, u) > kv;
+}
+
+__device__ __forceinline__ uint32_t fresh_prio(int32_t v, uint64_t fresh_m) {
   // engine.cpp:324-325: next round's redrawn h1 priority
-  return ((vertex_hash_m((uint64_t)v, fresh_m) >> 32) << 32) | (uint64_t)(v + 1);
+  return (uint32_t)(vertex_hash_m((uint64_t)v, fresh_m) >> 32);
 }
 
 // Per-warp output buffer in shared memory (64 entries), flushed 32 at a time

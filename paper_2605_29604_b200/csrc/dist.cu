@@ -9,7 +9,7 @@
 //   select (own worklist)  -> publish own candidates as a bitmap slice
 //   NCCL all-gather        -> every rank marks the remote candidates (next = 1)
 //   pull exclusion + update (own check list) -> publish own removals
-//   NCCL all-gather        -> every rank zeroes the remote removed keys
+//   NCCL all-gather        -> every rank marks the remote removals (state Removed)
 //   NCCL all-reduce of the round counters (host, distributed.py)
 //
 // i.e. exactly the reference's bulk-synchronous round (engine.cpp:247-291),
@@ -49,7 +49,7 @@ __global__ void k_partial_offsets(int32_t n, int32_t lo, int32_t hi,
 __global__ void k_apply_bits(const uint32_t *__restrict__ gathered,
                              const int32_t *__restrict__ rank_lo, int32_t world, int32_t maxw,
                              int32_t me, int what, uint8_t *__restrict__ next,
-                             uint64_t *__restrict__ key, uint8_t *__restrict__ state) {
+                             uint8_t *__restrict__ state) {
   const int64_t total = (int64_t)world * maxw;
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
        w += (int64_t)gridDim.x * blockDim.x) {
@@ -66,7 +66,6 @@ __global__ void k_apply_bits(const uint32_t *__restrict__ gathered,
         next[v] = 1;
         state[v] = TCMIS_IN_MIS;
       } else {  // remote removal: invisible from now on
-        key[v] = 0;
         state[v] = TCMIS_REMOVED;
       }
     }
@@ -103,6 +102,9 @@ int upload_partition(tcmis_ctx *ctx, int32_t n, int32_t lo, int32_t hi, const in
 struct DistState {
   RoundArgs a;
   bool active = false;
+  int32_t round = 0;                 // rounds updated so far (all run in the round kernels)
+  std::vector<int32_t> h_rank_lo;    // cached copy of the last rank layout ...
+  int32_t *d_rank_lo = nullptr;      // ... and its device mirror (uploaded once)
 };
 
 static DistState &dist_state(tcmis_graph *g) {
@@ -130,6 +132,7 @@ int dist_begin(tcmis_graph *g, const tcmis_config *cfg) {
   d.a.tail_thr = 0;
   d.a.pub_lo = g->part_lo;
   d.active = true;
+  d.round = 0;
   return 0;
 }
 
@@ -142,26 +145,34 @@ int dist_select(tcmis_graph *g, uint32_t *d_bits, int32_t words) {
   return launch_select(g, d.a);
 }
 
+// Stream-ordered, no host synchronisation: the host driver enqueues
+// select -> all-gather -> apply -> update -> all-gather -> apply -> all-reduce
+// on the engine stream and reads one counter vector per round.
 int dist_apply(tcmis_graph *g, const uint32_t *d_gathered, const int32_t *h_rank_lo,
                int32_t world, int32_t maxw, int32_t me, int32_t what) {
   tcmis_ctx *ctx = g->ctx;
-  int32_t *d_lo = nullptr;
-  if (int rc = dev_alloc(&d_lo, (size_t)world + 1)) return rc;
-  cudaError_t e = cudaMemcpyAsync(d_lo, h_rank_lo, 4ull * (world + 1), cudaMemcpyHostToDevice,
-                                  ctx->stream);
-  if (e == cudaSuccess) {
-    k_apply_bits<<<grid_for(ctx, (int64_t)world * maxw, 256, 8), 256, 0, ctx->stream>>>(
-        d_gathered, d_lo, world, maxw, me, what, g->ws.next, g->ws.key, g->ws.state);
-    ctx->launches++;
-    e = cudaGetLastError();
+  DistState &d = dist_state(g);
+  if (d.h_rank_lo.size() != (size_t)world + 1 ||
+      !std::equal(d.h_rank_lo.begin(), d.h_rank_lo.end(), h_rank_lo)) {
+    dev_free(d.d_rank_lo);
+    d.d_rank_lo = nullptr;
+    if (int rc = dev_alloc(&d.d_rank_lo, (size_t)world + 1)) return rc;
+    d.h_rank_lo.assign(h_rank_lo, h_rank_lo + world + 1);
+    TCMIS_CUDA(cudaMemcpyAsync(d.d_rank_lo, d.h_rank_lo.data(), 4ull * (world + 1),
+                               cudaMemcpyHostToDevice, ctx->stream));
+    TCMIS_CUDA(cudaStreamSynchronize(ctx->stream));  // h_rank_lo storage may change
   }
-  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  dev_free(d_lo);
-  if (e != cudaSuccess) return cuda_error(e, "dist apply");
+  k_apply_bits<<<grid_for(ctx, (int64_t)world * maxw, 256, 8), 256, 0, ctx->stream>>>(
+      d_gathered, d.d_rank_lo, world, maxw, me, what, g->ws.next, g->ws.state);
+  TCMIS_LAUNCHED(ctx);
   return 0;
 }
 
-int dist_update(tcmis_graph *g, uint32_t *d_bits, int32_t words, int64_t *counts) {
+// d_counts: DEVICE int64[5] = this rank's (selected, removed, alive,
+// tiles_evaluated, tiles_skipped) of the round, copied stream-ordered from
+// the DevRound k_round_end publishes (DevRound is 5 x u64 in that order).
+int dist_update(tcmis_graph *g, uint32_t *d_bits, int32_t words, int64_t *d_counts) {
+  static_assert(sizeof(DevRound) == 5 * sizeof(int64_t), "DevRound layout");
   DistState &d = dist_state(g);
   if (!d.active) return set_error(TCMIS_E_LOGIC, "tcmis_dist_begin first");
   cudaStream_t st = g->ctx->stream;
@@ -170,17 +181,9 @@ int dist_update(tcmis_graph *g, uint32_t *d_bits, int32_t words, int64_t *counts
   d.a.pub_dead = d_bits;
   if (int rc = launch_update(g, d.a, 0, 0)) return rc;
   Workspace &ws = g->ws;
-  TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
-  TCMIS_CUDA(cudaStreamSynchronize(st));
-  const int round = ws.h_ctrl->round - 1;
-  DevRound r;
-  TCMIS_CUDA(cudaMemcpy(&r, ws.rounds + (round - 1) % ws.round_cap, sizeof(DevRound),
-                        cudaMemcpyDeviceToHost));
-  counts[0] = (int64_t)r.sel;
-  counts[1] = (int64_t)r.rem;
-  counts[2] = (int64_t)r.alive;
-  counts[3] = (int64_t)r.eval;
-  counts[4] = (int64_t)r.skip;
+  const int32_t round = ++d.round;
+  TCMIS_CUDA(cudaMemcpyAsync(d_counts, ws.rounds + (round - 1) % ws.round_cap, sizeof(DevRound),
+                             cudaMemcpyDeviceToDevice, st));
   return 0;
 }
 
@@ -189,6 +192,43 @@ int dist_update(tcmis_graph *g, uint32_t *d_bits, int32_t words, int64_t *counts
 int dist_h3_tiles(tcmis_graph *g, int64_t *ev, int64_t *total) {
   if (int rc = seg_total(g, ev)) return rc;
   *total = g->tile_total;
+  return 0;
+}
+
+// A rank's partition built from a device-resident full graph (e.g. the
+// device generators): offsets copied, own rows' neighbour lists sliced, both
+// device to device.
+int partition_device(tcmis_graph *full, int32_t lo, int32_t hi, tcmis_graph **out) {
+  tcmis_ctx *ctx = full->ctx;
+  const int32_t n = full->n;
+  if (lo < 0 || hi < lo || hi > n)
+    return set_error(TCMIS_E_INVALID_ARGUMENT, "partition range outside [0, n]");
+  cudaStream_t st = ctx->stream;
+  int64_t ends[2] = {0, 0};
+  TCMIS_CUDA(cudaMemcpyAsync(&ends[0], full->d_off + lo, 8, cudaMemcpyDeviceToHost, st));
+  TCMIS_CUDA(cudaMemcpyAsync(&ends[1], full->d_off + hi, 8, cudaMemcpyDeviceToHost, st));
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  const int64_t nnz = ends[1] - ends[0];
+  int64_t *d_full = nullptr, *d_part = nullptr;
+  int32_t *d_nbr = nullptr;
+  if (int rc = dev_alloc(&d_full, (size_t)n + 1)) return rc;
+  if (int rc = dev_alloc(&d_part, (size_t)n + 1)) return rc;
+  if (int rc = dev_alloc(&d_nbr, (size_t)nnz)) return rc;
+  TCMIS_CUDA(cudaMemcpyAsync(d_full, full->d_off, 8ull * (n + 1), cudaMemcpyDeviceToDevice, st));
+  if (nnz)
+    TCMIS_CUDA(cudaMemcpyAsync(d_nbr, full->d_nbr + ends[0], 4ull * nnz, cudaMemcpyDeviceToDevice,
+                               st));
+  k_partial_offsets<<<grid_for(ctx, (int64_t)n + 1, 256, 16), 256, 0, st>>>(n, lo, hi, d_full,
+                                                                            d_part);
+  TCMIS_LAUNCHED(ctx);
+  int64_t total = 0;
+  TCMIS_CUDA(cudaMemcpyAsync(&total, full->d_off + n, 8, cudaMemcpyDeviceToHost, st));
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  if (int rc = wrap_owned(ctx, n, nnz, d_part, d_nbr, out)) return rc;
+  (*out)->d_off_full = d_full;
+  (*out)->nnz_global = total;
+  (*out)->part_lo = lo;
+  (*out)->part_hi = hi;
   return 0;
 }
 

@@ -3,9 +3,10 @@
 // Layout in HBM (per graph):
 //   d_off   int64[n+1]   CSR row extents (graph.hpp:20)
 //   d_nbr   int32[2m]    sorted neighbour ids (graph.hpp:21)
-//   key     uint64[n]    (p[v] << 32) | (v + 1) while v is alive, 0 once it
-//                        left (priorities.hpp:61-64; 0 == kNoNeighborKey, so a
-//                        dead neighbour can never block a candidate)
+//   prio    uint32[n]    p[v] (PriorityVector::p, priorities.hpp:33); the key of
+//                        v is (p[v] << 32) | (v + 1) (priorities.hpp:61-64), built
+//                        in registers; a neighbour u is visible iff state[u] is
+//                        not Removed (dead keys = kNoNeighborKey, priorities.hpp:57)
 //   state   uint8[n]     VertexState (engine.hpp:17)
 //   next    uint8[n]     this round's decision: 1 = candidate, 2 = excluded
 //   wl[2]   int32[n]     alive worklists (compacted between rounds)
@@ -56,7 +57,7 @@ struct Ctrl {
   int32_t overflow;    // set when rounds exceeded max_rounds
   int32_t long_count;  // entries of the select long-row list this round
   int32_t pull_count;  // entries of the pull long-row list this round
-  int32_t check_count; // pull: non-candidates emitted by the select kernels
+  int32_t check_unused; // (was the select kernels' pull check list)
   int32_t main_rounds; // rounds run by the per-round kernels (the rest ran in k_tail)
   int32_t tail_check[2]; // k_tail pull check-list length, by round parity
   int32_t sel_undec;   // rows k_probe_select left to the k_select engine
@@ -66,7 +67,7 @@ struct Ctrl {
 struct Workspace {
   size_t n_cap = 0;
   size_t seg_cap = 0;
-  uint64_t *key = nullptr;
+  uint32_t *prio = nullptr;
   uint8_t *state = nullptr;
   uint8_t *next = nullptr;
   int32_t *wl[2] = {nullptr, nullptr};
@@ -88,7 +89,9 @@ struct Workspace {
   void *cub_tmp = nullptr;
   size_t cub_bytes = 0;
   cudaGraphExec_t exec = nullptr;  // cached WHILE{select; update} graph
-  alignas(8) unsigned char graph_key[128] = {};
+  uint32_t *cbits = nullptr;      // tile exclusion: this round's candidates, bit per vertex
+  uint32_t *tile_hit = nullptr;   // tile exclusion: per T=16 block row, rows with a candidate nbr
+  alignas(8) unsigned char graph_key[256] = {};
 };
 
 }  // namespace tcmis_b200
@@ -131,6 +134,14 @@ struct tcmis_graph {
   int32_t tile_nb = 0;
   int32_t *d_rowtiles = nullptr;
   int64_t tile_total = 0;
+  // compact device tile store (tiles.cu build_tile_store), T = 8 or 16:
+  // block-row offsets, one block column and T*T/8 payload bytes per tile
+  int32_t store_T = 0;
+  int64_t *d_tbro = nullptr;
+  int64_t store_tiles = 0;
+  int32_t *d_trow = nullptr;
+  int32_t *d_tcol = nullptr;
+  void *d_tbits = nullptr;
   // per-graph preparation for the solve (computed once)
   bool prepared = false;
   int32_t *d_nz = nullptr;  // ascending ids of non-isolated vertices (round-1 select list)
@@ -208,13 +219,19 @@ struct RoundArgs {
   uint32_t *pub_dead;
   int32_t pub_lo;
   int tail_grid;
+  int tile;             // tile exclusion over the compact T = 16 store: 0 off, 1 bits, 2 mma
+  int32_t nb16;         // block rows of the store
+  int64_t store_tiles;
+  const int32_t *trow;
+  const int32_t *tcol;
+  const uint16_t *tbits;
   bool operator==(const RoundArgs &o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
 
 int launch_select(tcmis_graph *g, const RoundArgs &a);
 int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle cond, int use_cond);
 int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
-                      uint64_t *key, uint32_t *p_out, uint8_t *state, uint8_t *next,
+                      uint32_t *p_out, uint8_t *state, uint8_t *next,
                       uint8_t *segflag = nullptr, int T = 1);
 double avg_degree(const tcmis_graph *g);
 
@@ -227,6 +244,8 @@ void free_workspace(Workspace &ws);
 int build_tile_counts(tcmis_graph *g, int T);
 int export_tiles(tcmis_graph *g, int T, int32_t *tile_row, int32_t *tile_col,
                  uint64_t *row_bits, int64_t *bro);
+int build_tile_store(tcmis_graph *g, int T);
+void free_tile_store(tcmis_graph *g);
 
 // Device memory comes from the device's stream-ordered pool (release
 // threshold = unlimited, set in tcmis_ctx_create), allocated and freed in

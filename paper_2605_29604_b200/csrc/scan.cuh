@@ -30,7 +30,7 @@ __device__ __forceinline__ int64_t load_window_down(const int32_t *__restrict__ 
   const int64_t w = (hi - 1) & ~(int64_t)3;
   int4 q;
   if (w + 4 <= nnz) {  // nnz < 0 flags a neighbour array that is not 16-byte aligned
-    q = __ldg(reinterpret_cast<const int4 *>(nbr + w));
+    q = ld_stream(reinterpret_cast<const int4 *>(nbr + w));
   } else {
     const int64_t lim = nnz < 0 ? -nnz : nnz;
     q.x = w < lim ? __ldg(&nbr[w]) : -1;
@@ -51,7 +51,7 @@ __device__ __forceinline__ int64_t load_window_up(const int32_t *__restrict__ nb
   const int64_t w = p & ~(int64_t)3;
   int4 q;
   if (w + 4 <= nnz) {  // nnz < 0: scalar path (unaligned neighbour array)
-    q = __ldg(reinterpret_cast<const int4 *>(nbr + w));
+    q = ld_stream(reinterpret_cast<const int4 *>(nbr + w));
   } else {
     const int64_t lim = nnz < 0 ? -nnz : nnz;
     q.x = w < lim ? __ldg(&nbr[w]) : -1;
@@ -79,8 +79,8 @@ __device__ __forceinline__ void load_tail8(const int32_t *__restrict__ nbr, int6
   const int64_t w0 = w1 - 4;
   int4 a, b;
   if (w0 >= 0 && w1 + 4 <= nnz) {
-    a = __ldg(reinterpret_cast<const int4 *>(nbr + w0));
-    b = __ldg(reinterpret_cast<const int4 *>(nbr + w1));
+    a = ld_stream(reinterpret_cast<const int4 *>(nbr + w0));
+    b = ld_stream(reinterpret_cast<const int4 *>(nbr + w1));
   } else {
     const int64_t lim = nnz < 0 ? -nnz : nnz;
     int32_t t[8];

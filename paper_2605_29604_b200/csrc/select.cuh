@@ -24,8 +24,8 @@
 //                 per step (4 independent loads per lane), early exit.
 //
 // Outputs: candidates get next = 1 and state = InMIS; in push mode their
-// neighbours get next = 2; in pull mode the non-candidates are emitted to the
-// check list that k_update_pull scans (update.cuh).
+// neighbours get next = 2; in pull mode nothing else (the pull kernels walk
+// the same worklist and test state == Alive, update.cuh).
 #pragma once
 
 #include "common.cuh"
@@ -44,16 +44,15 @@ struct SelectArgs {
   const int64_t *off;
   const int32_t *nbr;
   int64_t vnnz;            // nnz, negated if nbr is not 16-byte aligned (scan.cuh)
-  const uint64_t *key;
+  const uint32_t *prio;
   uint8_t *next;
   uint8_t *state;
   uint8_t *segflag;        // null: no tile counters
   int T;
-  int push;                // 1: push exclusion, 0: emit non-candidates for pull
+  int push;                // 1: push exclusion (candidates scatter next = 2)
   Ctrl *ctrl;
   const int32_t *wl0, *wl1;
   int32_t *long_list;      // rows outliving the thread probe (ctrl->long_count)
-  int32_t *check;          // pull mode: non-candidates (ctrl->check_count)
   int32_t *undecided;      // rows the probe could not settle (ctrl->sel_undec)
   Publish pub;             // multi-GPU: this round's candidates of the own range
 };
@@ -71,37 +70,37 @@ constexpr int kProbeK = 4;  // row entries the straight-line probe examines
 // This settles 84 % of R-MAT s22's round-1 vertices and every vertex of
 // rows <= kProbeK (the whole grid, most of the RGG).
 __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
-  __shared__ int32_t s_chk[kBlock / 32][64];
   __shared__ int32_t s_und[kBlock / 32][64];
   Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
+  const bool r1 = round == 1;
   // round 1 visits only the non-isolated vertices (k_priorities already made
   // the isolated ones candidates)
   const int64_t cnt = round == 1 ? a.n1 : ctrl->wl_count[round & 1];
   if ((int64_t)blockIdx.x * kBlock >= cnt) return;
   const int32_t *wl = round == 1 ? a.nz : ((round & 1) ? a.wl1 : a.wl0);
   const int32_t *__restrict__ nbr = a.nbr;
-  const uint64_t *__restrict__ key = a.key;
+  const uint32_t *__restrict__ prio = a.prio;
   const int lane = threadIdx.x & 31;
-  WarpOut chk{s_chk[threadIdx.x >> 5], 0}, und{s_und[threadIdx.x >> 5], 0};
+  WarpOut und{s_und[threadIdx.x >> 5], 0};
   unsigned long long sel = 0;
   const int64_t stride = (int64_t)gridDim.x * kBlock;
   for (int64_t wb = (int64_t)blockIdx.x * kBlock + (threadIdx.x & ~31); wb < cnt; wb += stride) {
     const int64_t i = wb + lane;
-    bool noncand = false, undecided = false;
+    bool undecided = false;
     int32_t v = 0;
     if (i < cnt) {
       v = (round == 1 && a.nz_identity) ? (int32_t)i : __ldg(&wl[i]);
-      const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
-      const uint64_t kv = __ldg(&key[v]);
+      const int64_t s = ld_stream(&a.off[v]), e = ld_stream(&a.off[v + 1]);
+      const uint64_t kv = key_of(__ldg(&prio[v]), v);
       int32_t u[8];
       load_tail8(nbr, a.vnnz, s, e, u);
       bool blocked = false;
 #pragma unroll
       for (int j = 0; j < kProbeK; ++j)
-        if (u[j] >= 0) blocked |= __ldg(&key[u[j]]) > kv;
+        if (u[j] >= 0) blocked |= blocks(prio, a.state, r1, u[j], kv);
       if (blocked) {
-        noncand = !a.push;
+        // a non-candidate: the pull exclusion finds it on the worklist
       } else if (e - s <= kProbeK) {
         mark_candidate(v, a.next, a.state, a.segflag, a.T);
         publish(a.pub, v);
@@ -115,10 +114,8 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
         undecided = true;
       }
     }
-    if (!a.push) warp_emit(chk, noncand, v, a.check, &ctrl->check_count);
     warp_emit(und, undecided, v, a.undecided, &ctrl->sel_undec);
   }
-  if (!a.push) warp_flush(chk, a.check, &ctrl->check_count);
   warp_flush(und, a.undecided, &ctrl->sel_undec);
   block_add3(sel, 0, 0, ctrl);
 }
@@ -127,14 +124,13 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
 // machine (scan down in 16-byte windows from e - kProbeK; push up), so a
 // lane never idles behind another lane's longer row.
 __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a) {
-  __shared__ int32_t s_out[kBlock / 32][64];
   Ctrl *ctrl = a.ctrl;
   const int64_t cnt = ctrl->sel_undec;
   if ((int64_t)blockIdx.x * kBlock >= cnt) return;
+  const bool r1 = ctrl->round == 1;
   const int32_t *__restrict__ nbr = a.nbr;
-  const uint64_t *__restrict__ key = a.key;
+  const uint32_t *__restrict__ prio = a.prio;
   const int64_t stride = (int64_t)gridDim.x * kBlock;
-  WarpOut wo{s_out[threadIdx.x >> 5], 0};
   unsigned long long sel = 0;
   int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x - stride;
   int mode = kFetch;
@@ -147,7 +143,7 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
       v = __ldg(&a.undecided[i]);
       s = __ldg(&a.off[v]);
       e = __ldg(&a.off[v + 1]);
-      kv = __ldg(&key[v]);
+      kv = key_of(__ldg(&prio[v]), v);
       hi = e - kProbeK;  // the probe examined the last kProbeK entries
       mode = kScan;
     } else {
@@ -156,17 +152,16 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
   };
   fetch();
   while (__any_sync(0xffffffffu, mode != kDone)) {
-    bool defer = false, noncand = false;
+    bool defer = false;
     if (mode == kScan) {
       int32_t u[4];
       const int64_t w = load_window_down(nbr, a.vnnz, s, hi, u);
       bool blocked = false;
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (u[j] >= 0) blocked |= __ldg(&key[u[j]]) > kv;
+        if (u[j] >= 0) blocked |= blocks(prio, a.state, r1, u[j], kv);
       hi = w;
       if (blocked) {
-        noncand = !a.push;
         mode = kFetch;
       } else if (hi <= s) {
         mark_candidate(v, a.next, a.state, a.segflag, a.T);
@@ -187,11 +182,9 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
       hi = p;
       if (hi >= e) mode = kFetch;
     }
-    if (!a.push) warp_emit(wo, noncand, v, a.check, &ctrl->check_count);
     warp_append(defer, v, a.long_list, &ctrl->long_count);
     if (mode == kFetch) fetch();
   }
-  if (!a.push) warp_flush(wo, a.check, &ctrl->check_count);
   block_add3(sel, 0, 0, ctrl);
 }
 
@@ -199,15 +192,16 @@ __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
   Ctrl *ctrl = a.ctrl;
   const int cnt = ctrl->long_count;
   if ((int64_t)blockIdx.x * (kBlock / 32) >= cnt) return;
+  const bool r1 = ctrl->round == 1;
   const int lane = threadIdx.x & 31;
   const int32_t *__restrict__ nbr = a.nbr;
-  const uint64_t *__restrict__ key = a.key;
+  const uint32_t *__restrict__ prio = a.prio;
   unsigned long long sel = 0;
   for (int64_t q = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5; q < cnt;
        q += ((int64_t)gridDim.x * kBlock) >> 5) {
     const int32_t v = a.long_list[q];
     const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
-    const uint64_t kv = __ldg(&key[v]);
+    const uint64_t kv = key_of(__ldg(&prio[v]), v);
     // the thread stage examined at least the last kThreadMax - 3 entries (its
     // first window may be short); rescanning an entry is harmless
     int64_t hi = e - (kThreadMax - 3);
@@ -222,7 +216,7 @@ __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
       bool b = false;
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (u[j] >= 0) b |= __ldg(&key[u[j]]) > kv;
+        if (u[j] >= 0) b |= blocks(prio, a.state, r1, u[j], kv);
       blocked = __any_sync(0xffffffffu, b);
       hi -= 128;
     }
@@ -234,8 +228,6 @@ __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
       }
       if (a.push)
         for (int64_t idx = s + lane; idx < e; idx += 32) exclude(a.next, __ldg(&nbr[idx]));
-    } else if (!a.push && lane == 0) {
-      a.check[atomicAdd(&ctrl->check_count, 1)] = v;
     }
   }
   block_add3(sel, 0, 0, ctrl);

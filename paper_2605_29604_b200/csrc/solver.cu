@@ -29,49 +29,85 @@
 #include "select.cuh"
 #include "update.cuh"
 #include "tail.cuh"
+#include "tile_excl.cuh"
 
 namespace tcmis_b200 {
 
 // ------------------------------------------------------------- priorities
 
 // priorities.cpp:43-51, with every IEEE operation spelled out so that no
-// contraction or fast-math can change a bit.
-__device__ __forceinline__ uint32_t h2_value(double avg, int64_t deg, double eps, double scale) {
+// contraction or fast-math can change a bit.  floor + the two range checks of
+// the reference are one cvt.rmi.u32.f64 (round toward -inf, saturating to
+// [0, 0xffffffff]; the argument is never NaN).
+__device__ __forceinline__ uint32_t h2_value(double avg, int32_t deg, double eps, double scale) {
   double d = __dadd_rn(__dadd_rn(avg, (double)deg), -eps);
   if (d < 1.0 / 1024.0) d = 1.0 / 1024.0;
-  double s = floor(__dmul_rn(__ddiv_rn(avg, d), scale));
-  if (s < 0.0) return 0u;
-  if (s >= 4294967295.0) return 0xffffffffu;
-  return (uint32_t)s;
+  return __double2uint_rd(__dmul_rn(__ddiv_rn(avg, d), scale));
 }
 
-// K2: priorities (priorities.cpp:33-67) + key/state initialisation.
+// K2: priorities (priorities.cpp:33-67) + state / decision initialisation.
 // mode 0: h1 / luby-fresh hash priorities from `mseed` (= mix64(seed'));
 // mode 1: h2 degree-aware priorities.
-__global__ void k_priorities(int32_t n, const int64_t *__restrict__ off, int mode,
-                             uint64_t mseed, double avg, double scale, uint64_t *__restrict__ key,
-                             uint32_t *__restrict__ p_out, uint8_t *__restrict__ state,
-                             uint8_t *__restrict__ next, uint8_t *__restrict__ segflag, int T) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t h = vertex_hash_m((uint64_t)v, mseed);
-    const int64_t deg = off[v + 1] - off[v];
-    uint32_t p;
-    if (mode == 0) {
-      p = (uint32_t)(h >> 32);
+// Instruction-bound (ncu: 136 warp instructions per vertex, 62 % issue, 14 %
+// of DRAM peak), so each thread takes 4 consecutive vertices: two 16-byte
+// offset loads, the (v+1)*golden term of vertex_hash by addition, one 16-byte
+// priority store and one 4-byte store each for state and next.
+constexpr int kPrioV = 4;
+
+__global__ void __launch_bounds__(256)
+    k_priorities(int32_t n, const int64_t *__restrict__ off, int aligned, int mode,
+                 uint64_t mseed, double avg, double scale, uint32_t *__restrict__ p_out,
+                 uint8_t *__restrict__ state, uint8_t *__restrict__ next,
+                 uint8_t *__restrict__ segflag, int T, int tshift) {
+  const int32_t quads = (int32_t)(((int64_t)n + kPrioV - 1) / kPrioV);
+  for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < quads;
+       q += gridDim.x * blockDim.x) {
+    const int32_t v0 = q * kPrioV;
+    const bool full = v0 + kPrioV <= n;
+    int64_t o[kPrioV + 1];
+    if (full && aligned) {
+      const longlong2 a = __ldg(reinterpret_cast<const longlong2 *>(off + v0));
+      const longlong2 b = __ldg(reinterpret_cast<const longlong2 *>(off + v0 + 2));
+      o[0] = a.x;
+      o[1] = a.y;
+      o[2] = b.x;
+      o[3] = b.y;
+      o[4] = __ldg(&off[v0 + 4]);
     } else {
-      double eps = (double)(h >> 11) * 0x1.0p-53;  // hash_to_unit, priorities.cpp:25-27
-      p = h2_value(avg, deg, eps, scale);
+#pragma unroll
+      for (int j = 0; j <= kPrioV; ++j) o[j] = v0 + j <= n ? __ldg(&off[v0 + j]) : 0;
     }
-    if (p_out) p_out[v] = p;
-    if (key) key[v] = ((uint64_t)p << 32) | (uint64_t)(v + 1);
-    if (state) state[v] = (next && deg == 0) ? TCMIS_IN_MIS : TCMIS_ALIVE;
-    if (next) {
+    uint32_t pv[kPrioV];
+    uint32_t st4 = 0, nx4 = 0;
+    uint64_t x = mseed + (uint64_t)(v0 + 1) * kGolden;  // vertex_hash, priorities.cpp:21-23
+#pragma unroll
+    for (int j = 0; j < kPrioV; ++j, x += kGolden) {
+      const uint64_t h = mix64(x);
+      const int32_t deg = (int32_t)(o[j + 1] - o[j]);
+      if (mode == 0) {
+        pv[j] = (uint32_t)(h >> 32);
+      } else {
+        const double eps = (double)(h >> 11) * 0x1.0p-53;  // hash_to_unit, priorities.cpp:25-27
+        pv[j] = h2_value(avg, deg, eps, scale);
+      }
       // an isolated vertex has no alive neighbour: it is a round-1 candidate
       // (engine.cpp:94-99 leaves max_np at kNoNeighborKey) and round 1's
       // select never has to visit it
-      next[v] = deg == 0 ? 1 : 0;
-      if (deg == 0 && segflag) segflag[v / T] = 1;
+      const bool iso = next && deg == 0 && v0 + j < n;
+      st4 |= (uint32_t)(iso ? TCMIS_IN_MIS : TCMIS_ALIVE) << (8 * j);
+      nx4 |= (uint32_t)(iso ? 1 : 0) << (8 * j);
+      if (iso && segflag) segflag[tshift >= 0 ? (v0 + j) >> tshift : (v0 + j) / T] = 1;
+    }
+    if (full) {
+      if (p_out) *reinterpret_cast<uint4 *>(p_out + v0) = make_uint4(pv[0], pv[1], pv[2], pv[3]);
+      if (state) *reinterpret_cast<uint32_t *>(state + v0) = st4;
+      if (next) *reinterpret_cast<uint32_t *>(next + v0) = nx4;
+    } else {
+      for (int j = 0; j < kPrioV && v0 + j < n; ++j) {
+        if (p_out) p_out[v0 + j] = pv[j];
+        if (state) state[v0 + j] = (uint8_t)(st4 >> (8 * j));
+        if (next) next[v0 + j] = (uint8_t)(nx4 >> (8 * j));
+      }
     }
   }
 }
@@ -100,12 +136,12 @@ __global__ void k_h1(int32_t n, uint64_t mseed, uint32_t *__restrict__ p) {
 // run_h3_resolution start state: only the alive vertices of `states` take
 // part (everyone else is Removed, key 0 = invisible)
 __global__ void k_resolve_init(int32_t n, const uint32_t *__restrict__ p,
-                               const uint8_t *__restrict__ states, uint64_t *__restrict__ key,
+                               const uint8_t *__restrict__ states, uint32_t *__restrict__ prio,
                                uint8_t *__restrict__ state, uint8_t *__restrict__ next) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     const bool alive = states[v] == TCMIS_ALIVE;
-    key[v] = alive ? (((uint64_t)p[v] << 32) | (uint64_t)(v + 1)) : 0;
+    prio[v] = p[v];
     state[v] = alive ? TCMIS_ALIVE : TCMIS_REMOVED;
     next[v] = 0;
   }
@@ -221,7 +257,7 @@ void timeline_end(tcmis_ctx *ctx) {
 // -------------------------------------------------------------- workspace
 
 void free_workspace(Workspace &ws) {
-  dev_free(ws.key);
+  dev_free(ws.prio);
   dev_free(ws.state);
   dev_free(ws.next);
   dev_free(ws.wl[0]);
@@ -241,6 +277,8 @@ void free_workspace(Workspace &ws) {
   dev_free(ws.rounds);
   cudaFreeHost(ws.h_rounds);
   dev_free(ws.cub_tmp);
+  dev_free(ws.cbits);
+  dev_free(ws.tile_hit);
   if (ws.exec) cudaGraphExecDestroy(ws.exec);
   ws = Workspace{};
 }
@@ -269,7 +307,7 @@ int ensure_workspace(tcmis_graph *g) {
       cudaGraphExecDestroy(ws.exec);
       ws.exec = nullptr;
     }
-    dev_free(ws.key);
+    dev_free(ws.prio);
     dev_free(ws.state);
     dev_free(ws.next);
     dev_free(ws.wl[0]);
@@ -281,8 +319,10 @@ int ensure_workspace(tcmis_graph *g) {
     dev_free(ws.undec_sel);
     dev_free(ws.undec_pull);
     dev_free(ws.segmark);
+    dev_free(ws.cbits);
+    dev_free(ws.tile_hit);
     ws.n_cap = 0;
-    if (int rc = dev_alloc(&ws.key, n)) return rc;
+    if (int rc = dev_alloc(&ws.prio, n)) return rc;
     if (int rc = dev_alloc(&ws.state, n)) return rc;
     if (int rc = dev_alloc(&ws.next, n)) return rc;
     if (int rc = dev_alloc(&ws.wl[0], n)) return rc;
@@ -294,6 +334,8 @@ int ensure_workspace(tcmis_graph *g) {
     if (int rc = dev_alloc(&ws.undec_sel, n)) return rc;
     if (int rc = dev_alloc(&ws.undec_pull, n)) return rc;
     if (int rc = dev_alloc(&ws.segmark, n)) return rc;
+    if (int rc = dev_alloc(&ws.cbits, n / 32 + 2)) return rc;
+    if (int rc = dev_alloc(&ws.tile_hit, n / 16 + 2)) return rc;
     TCMIS_CUDA(cudaMemsetAsync(ws.next, 0, n, g->ctx->stream));
     ws.n_cap = n;
   }
@@ -364,7 +406,7 @@ namespace {
 }  // namespace
 
 int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
-                      uint64_t *key, uint32_t *p_out, uint8_t *state, uint8_t *next,
+                      uint32_t *p_out, uint8_t *state, uint8_t *next,
                       uint8_t *segflag, int T) {
   tcmis_ctx *ctx = g->ctx;
   int mode = 1;
@@ -376,11 +418,15 @@ int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bi
     mseed = mix64(combine_seed(seed, 1));  // engine.cpp:324-325, iteration 1
   }
   const double scale = mode ? (double)(1u << scale_bits) : 0.0;
-  const int grid = grid_for(ctx, g->n, 256, 16);
+  const int64_t *off = g->d_off_full ? g->d_off_full : g->d_off;
+  const int aligned = ((uintptr_t)off & 15) == 0 ? 1 : 0;
+  const int tshift = (T & (T - 1)) == 0 ? __builtin_ctz((unsigned)T) : -1;
+  const int grid = grid_for(ctx, ((int64_t)g->n + kPrioV - 1) / kPrioV, 256, 8);
   TCMIS_TIMED(ctx, "k_priorities",
-              (k_priorities<<<grid, 256, 0, ctx->stream>>>(g->n, g->d_off_full ? g->d_off_full : g->d_off, mode, mseed,
-                                                          mode ? avg_degree(g) : 0.0, scale, key,
-                                                          p_out, state, next, segflag, T)));
+              (k_priorities<<<grid, 256, 0, ctx->stream>>>(g->n, off, aligned, mode, mseed,
+                                                          mode ? avg_degree(g) : 0.0, scale,
+                                                          p_out, state, next, segflag, T,
+                                                          tshift)));
   TCMIS_LAUNCHED(ctx);
   return 0;
 }
@@ -416,19 +462,19 @@ SelectArgs select_args(tcmis_graph *g, const RoundArgs &a) {
   s.off = a.off;
   s.nbr = a.nbr;
   s.vnnz = a.vnnz;
-  s.key = ws.key;
+  s.prio = ws.prio;
   s.next = ws.next;
   s.state = ws.state;
   s.segflag = a.seg_mode ? ws.segflag : nullptr;
   s.T = a.T;
-  s.push = a.pull ? 0 : 1;
+  s.push = (a.pull || a.tile) ? 0 : 1;
   s.ctrl = ws.ctrl;
   s.wl0 = ws.wl[0];
   s.wl1 = ws.wl[1];
   s.long_list = ws.long_list;
-  s.check = ws.check;
   s.undecided = ws.undec_sel;
   s.pub = Publish{a.pub_cand, a.pub_lo};
+  if (a.tile) s.pub = Publish{ws.cbits, 0};  // the candidate segments of the tile kernels
   return s;
 }
 
@@ -439,7 +485,7 @@ UpdateArgs update_args(tcmis_graph *g, const RoundArgs &a) {
   u.off = a.off;
   u.nbr = a.nbr;
   u.vnnz = a.vnnz;
-  u.key = ws.key;
+  u.prio = ws.prio;
   u.state = ws.state;
   u.next = ws.next;
   u.ctrl = ws.ctrl;
@@ -447,11 +493,14 @@ UpdateArgs update_args(tcmis_graph *g, const RoundArgs &a) {
   u.wl1 = ws.wl[1];
   u.fresh = a.fresh;
   u.seed = a.seed;
-  u.check = ws.check;
+  u.n1 = a.nz_count;
+  u.nz = a.nz;
+  u.nz_identity = a.nz_count == a.n ? 1 : 0;
   u.long_list = ws.long_list2;
   u.undecided = ws.undec_pull;
   u.pub = Publish{a.pub_dead, a.pub_lo};
   u.segflag = ws.segflag;
+  u.tile_hit = a.tile ? ws.tile_hit : nullptr;
   u.rowtiles = a.rowtiles;
   u.nseg = a.nseg;
   u.total_tiles = a.total_tiles;
@@ -466,7 +515,7 @@ TailArgs tail_args(tcmis_graph *g, const RoundArgs &a) {
   TailArgs t;
   t.off = a.off;
   t.nbr = a.nbr;
-  t.key = ws.key;
+  t.prio = ws.prio;
   t.next = ws.next;
   t.state = ws.state;
   t.segflag = ws.segflag;
@@ -520,6 +569,8 @@ int launch_select(tcmis_graph *g, const RoundArgs &a) {
   tcmis_ctx *ctx = g->ctx;
   cudaStream_t st = ctx->stream;
   const SelectArgs s = select_args(g, a);
+  if (a.tile)
+    TCMIS_CUDA(cudaMemsetAsync(g->ws.cbits, 0, 4 * ((size_t)a.n / 32 + 1), st));
   TCMIS_TIMED(ctx, "k_probe_select", (k_probe_select<<<a.sel_grid, kBlock, 0, st>>>(s)));
   TCMIS_LAUNCHED(ctx);
   TCMIS_TIMED(ctx, "k_select", (k_select<<<a.sel_grid, kBlock, 0, st>>>(s)));
@@ -538,6 +589,16 @@ int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle
     TCMIS_TIMED(ctx, "k_probe_pull", (k_probe_pull<<<a.sel_grid, kBlock, 0, st>>>(u)));
     TCMIS_LAUNCHED(ctx);
     TCMIS_TIMED(ctx, "k_update_pull", (k_update_pull<<<a.sel_grid, kBlock, 0, st>>>(u)));
+  } else if (a.tile) {
+    TCMIS_CUDA(cudaMemsetAsync(g->ws.tile_hit, 0, 4 * ((size_t)a.nb16 + 1), st));
+    TileExclArgs t{a.store_tiles, a.trow, a.tcol, a.tbits, g->ws.cbits, g->ws.tile_hit};
+    const int grid = grid_for(ctx, a.store_tiles, 256, 8);
+    if (a.tile == 2)
+      TCMIS_TIMED(ctx, "k_tile_excl_mma", (k_tile_excl_mma<<<grid, 256, 0, st>>>(t)));
+    else
+      TCMIS_TIMED(ctx, "k_tile_excl_bits", (k_tile_excl_bits<<<grid, 256, 0, st>>>(t)));
+    TCMIS_LAUNCHED(ctx);
+    TCMIS_TIMED(ctx, "k_update", (k_update<<<a.upd_grid, kBlock, 0, st>>>(u)));
   } else {
     TCMIS_TIMED(ctx, "k_update", (k_update<<<a.upd_grid, kBlock, 0, st>>>(u)));
   }
@@ -547,7 +608,7 @@ int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle
   return 0;
 }
 
-inline int launches_per_round(const RoundArgs &a) { return a.pull ? 6 : 5; }
+inline int launches_per_round(const RoundArgs &a) { return (a.pull || a.tile) ? 6 : 5; }
 
 // Instantiate (once per distinct argument set) the graph
 //   WHILE(cond) { k_select ; k_update }
@@ -632,7 +693,7 @@ int solve_prepare(tcmis_graph *g, const tcmis_config *cfg, RoundArgs &a, int64_t
   const int32_t nseg = tiled ? g->tile_nb : 0;
   const int seg_mode = !tiled ? 0 : (H == TCMIS_H3 ? 2 : 1);
   if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
-  if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.key, nullptr, ws.state,
+  if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio, ws.state,
                                  ws.next, seg_mode ? ws.segflag : nullptr, T > 0 ? T : 1))
     return rc;
   Ctrl c0{};
@@ -690,7 +751,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   if (timing) timeline_begin(ctx);
   if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
   uint8_t *seg0 = seg_mode ? ws.segflag : nullptr;
-  if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.key, nullptr, ws.state,
+  if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio, ws.state,
                                  ws.next, seg0, T > 0 ? T : 1))
     return rc;
   Ctrl c0{};
@@ -721,9 +782,24 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   // exclusion form: pull on degree-skewed graphs, where the
   // neighbours of candidates concentrate on hubs and early-exit pulls are
   // cheap; push elsewhere.  Both produce the same next[] decisions.
-  if (cfg->exclusion == TCMIS_EXCL_PUSH) a.pull = 0;
-  else if (cfg->exclusion == TCMIS_EXCL_CSR_PULL) a.pull = 1;
-  else a.pull = (double)g->max_degree > 64.0 * std::max(1.0, avg_degree(g)) ? 1 : 0;
+  if (cfg->exclusion == TCMIS_EXCL_PUSH) {
+    a.pull = 0;
+  } else if (cfg->exclusion == TCMIS_EXCL_CSR_PULL) {
+    a.pull = 1;
+  } else if (cfg->exclusion == TCMIS_EXCL_TILE_BITS || cfg->exclusion == TCMIS_EXCL_TILE_MMA) {
+    // the paper's tile form over the compact T = 16 store (tile_excl.cuh);
+    // built once per graph, like tile_graph in run_tc_mis(g, cfg)
+    if (int rc = build_tile_store(g, 16)) return rc;
+    a.pull = 0;
+    a.tile = cfg->exclusion == TCMIS_EXCL_TILE_MMA ? 2 : 1;
+    a.nb16 = (int32_t)(((int64_t)g->n + 15) / 16);
+    a.store_tiles = g->store_tiles;
+    a.trow = g->d_trow;
+    a.tcol = g->d_tcol;
+    a.tbits = static_cast<const uint16_t *>(g->d_tbits);
+  } else {
+    a.pull = (double)g->max_degree > 64.0 * std::max(1.0, avg_degree(g)) ? 1 : 0;
+  }
   // small late rounds run in the persistent k_tail (not with the per-round
   // observer hook, which needs every round's snapshot)
   a.tail_thr = 0;
@@ -754,7 +830,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       step = true;
       a.tail_thr = 0;
       if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
-      if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.key, nullptr,
+      if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio,
                                      ws.state, ws.next, seg0, T > 0 ? T : 1))
         return rc;
       *ws.h_ctrl = c0;
@@ -852,7 +928,9 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       const int r = k.round - 1;
       if (r < 0 || r >= (int)rounds_h.size()) continue;
       const std::string nm(k.name);
-      if (nm == "k_probe_pull" || nm == "k_update_pull") t2[r] += k.ms;
+      if (nm == "k_probe_pull" || nm == "k_update_pull" || nm == "k_tile_excl_bits" ||
+          nm == "k_tile_excl_mma")
+        t2[r] += k.ms;
       else if (nm == "k_update" || nm == "k_round_end") t3[r] += k.ms;
       else t1[r] += k.ms;
     }
@@ -920,7 +998,7 @@ int priorities_impl(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits
   }
   uint32_t *d_p = nullptr;
   if (int rc = dev_alloc(&d_p, (size_t)g->n)) return rc;
-  int rc = launch_priorities(g, heuristic, seed, scale_bits, nullptr, d_p, nullptr, nullptr);
+  int rc = launch_priorities(g, heuristic, seed, scale_bits, d_p, nullptr, nullptr);
   if (!rc) {
     cudaError_t e = cudaMemcpyAsync(p_out, d_p, sizeof(uint32_t) * g->n, cudaMemcpyDeviceToHost,
                                     g->ctx->stream);
@@ -1040,7 +1118,7 @@ int h3_resolution_impl(tcmis_graph *g, const uint32_t *p, const uint8_t *states,
   if (!rc) {
     cudaMemcpyAsync(d_p, p, 4ull * g->n, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(d_s, states, g->n, cudaMemcpyHostToDevice, st);
-    k_resolve_init<<<grid_for(ctx, g->n, 256, 16), 256, 0, st>>>(g->n, d_p, d_s, ws.key, ws.state,
+    k_resolve_init<<<grid_for(ctx, g->n, 256, 16), 256, 0, st>>>(g->n, d_p, d_s, ws.prio, ws.state,
                                                                 ws.next);
     ctx->launches++;
     thrust::counting_iterator<int32_t> ids(0);

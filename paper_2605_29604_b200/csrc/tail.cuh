@@ -39,7 +39,7 @@ constexpr int kTailBlock = 1024;  // one block per SM: 148 arrivals per barrier
 struct TailArgs {
   const int64_t *off;
   const int32_t *nbr;
-  uint64_t *key;
+  uint32_t *prio;
   uint8_t *next;
   uint8_t *state;
   uint8_t *segflag;         // byte flags (seg_mode 2) -- also mode 1 sanity
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
     for (int64_t q = gid; q < cnt; q += ngroups) {
       const int32_t v = __ldcg(&in[q]);
       const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
-      const uint64_t kv = __ldcg(&a.key[v]);
+      const uint64_t kv = key_of(__ldcg(&a.prio[v]), v);
       bool blocked = false;
       for (int64_t hi = e; hi > s && !blocked; hi -= kW) {
         int32_t u[kTU];
@@ -143,7 +143,9 @@ __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
         bool b = false;
 #pragma unroll
         for (int j = 0; j < kTU; ++j)
-          if (u[j] >= 0) b |= __ldcg(&a.key[u[j]]) > kv;
+          if (u[j] >= 0)
+            b |= __ldcg(&a.state[u[j]]) != TCMIS_REMOVED &&
+                 key_of(__ldcg(&a.prio[u[j]]), u[j]) > kv;
         blocked = group_any(b, gmask) != 0;
       }
       if (!blocked) {
@@ -175,10 +177,10 @@ __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
         const int32_t v = __ldcg(&in[q]);
         const uint8_t d = __ldcg(&a.next[v]);
         if (d == 2) {
-          mark_removed(v, a.state, a.key);
+          mark_removed(v, a.state);
           ++rem;
         } else if (d == 0) {
-          if (a.fresh) a.key[v] = fresh_key(v, fresh_m);
+          if (a.fresh) a.prio[v] = fresh_prio(v, fresh_m);
           out[atomicAdd(tail, 1)] = v;
         }
       }
@@ -203,10 +205,10 @@ __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
         }
         if (gl == 0) {
           if (hit) {
-            mark_removed(v, a.state, a.key);
+            mark_removed(v, a.state);
             ++rem;
           } else {
-            if (a.fresh) a.key[v] = fresh_key(v, fresh_m);
+            if (a.fresh) a.prio[v] = fresh_prio(v, fresh_m);
             out[atomicAdd(tail, 1)] = v;
           }
         }

@@ -58,7 +58,9 @@ __device__ __forceinline__ int64_t lower_bound_i32(const int32_t *__restrict__ a
 }
 
 // One warp per work item.  emit == false: count; emit == true: write tiles
-// starting at item_off[item].
+// starting at item_off[item], each row word as `row_bytes` bytes: 8 = the
+// reference layout (u64 per row, tiling.hpp:21-24), 2 / 1 = the compact
+// device layout of T = 16 / T = 8 (internal.cuh "tile store").
 template <bool emit>
 __global__ void __launch_bounds__(256)
     k_tile_merge(int32_t n, int T, int32_t nb, const int64_t *__restrict__ off,
@@ -66,7 +68,7 @@ __global__ void __launch_bounds__(256)
                  const int32_t *__restrict__ item_row, const int64_t *__restrict__ item_start,
                  int64_t *__restrict__ item_cnt, int32_t *__restrict__ rowtiles,
                  const int64_t *__restrict__ item_off, int32_t *__restrict__ tile_row,
-                 int32_t *__restrict__ tile_col, uint64_t *__restrict__ row_bits) {
+                 int32_t *__restrict__ tile_col, void *__restrict__ row_bits, int row_bytes) {
   const int lane = threadIdx.x & 31;
   for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n_items;
        it += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -119,13 +121,17 @@ __global__ void __launch_bounds__(256)
       if (emit) {
         const int64_t t = item_off[it] + count;
         if (lane == 0) {
-          tile_row[t] = b;
+          if (tile_row) tile_row[t] = b;
           tile_col[t] = (int32_t)m;
         }
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           const int i = lane + 32 * k;
-          if (i < T) row_bits[t * T + i] = word[k];
+          if (i < T) {
+            if (row_bytes == 8) static_cast<uint64_t *>(row_bits)[t * T + i] = word[k];
+            else if (row_bytes == 2) static_cast<uint16_t *>(row_bits)[t * T + i] = (uint16_t)word[k];
+            else static_cast<uint8_t *>(row_bits)[t * T + i] = (uint8_t)word[k];
+          }
         }
       }
       ++count;
@@ -400,7 +406,7 @@ int export_tiles(tcmis_graph *g, int T, int32_t *tile_row, int32_t *tile_col,
   cudaMemsetAsync(scratch_rows, 0, sizeof(int32_t) * ((size_t)nb + 1), st);
   k_tile_merge<false><<<grid_for(ctx, 32 * it.n_items, 256, 16), 256, 0, st>>>(
       g->n, T, nb, g->d_off, g->d_nbr, it.n_items, it.row, it.start, it.cnt, scratch_rows,
-      nullptr, nullptr, nullptr, nullptr);
+      nullptr, nullptr, nullptr, nullptr, 8);
   ctx->launches++;
   int64_t *item_off = nullptr;
   int32_t *d_tr = nullptr, *d_tc = nullptr;
@@ -417,7 +423,7 @@ int export_tiles(tcmis_graph *g, int T, int32_t *tile_row, int32_t *tile_col,
     cub::DeviceScan::ExclusiveSum(tmp, bytes, it.cnt, item_off, it.n_items, st);
     k_tile_merge<true><<<grid_for(ctx, 32 * it.n_items, 256, 16), 256, 0, st>>>(
         g->n, T, nb, g->d_off, g->d_nbr, it.n_items, it.row, it.start, it.cnt, scratch_rows,
-        item_off, d_tr, d_tc, d_rb);
+        item_off, d_tr, d_tc, d_rb, 8);
     ctx->launches += 2;
     std::vector<int64_t> h_start(nb + 1), h_off(it.n_items);
     cudaMemcpyAsync(h_start.data(), it.start, 8ull * (nb + 1), cudaMemcpyDeviceToHost, st);
@@ -439,6 +445,105 @@ int export_tiles(tcmis_graph *g, int T, int32_t *tile_row, int32_t *tile_col,
   dev_free(d_tr);
   dev_free(d_tc);
   dev_free(d_rb);
+  return rc;
+}
+
+namespace {
+
+__global__ void k_store_bro(int32_t nb, const int64_t *__restrict__ start,
+                            const int64_t *__restrict__ item_off, int64_t tiles,
+                            int64_t *__restrict__ bro) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= nb;
+       b += (int64_t)gridDim.x * blockDim.x)
+    bro[b] = b < nb ? item_off[start[b]] : tiles;
+}
+
+}  // namespace
+
+void free_tile_store(tcmis_graph *g) {
+  dev_free(g->d_tbro);
+  dev_free(g->d_trow);
+  dev_free(g->d_tcol);
+  dev_free(g->d_tbits);
+  g->d_tbro = nullptr;
+  g->d_trow = nullptr;
+  g->store_tiles = 0;
+  g->d_tcol = nullptr;
+  g->d_tbits = nullptr;
+  g->store_T = 0;
+}
+
+// The compact device tile store of T = 16 (32 B payload: 16 u16 rows) or
+// T = 8 (8 B: 8 u8 rows) plus one int32 block column per tile and int64
+// block-row offsets -- the layout SURVEY 8 "format byte budget" prices
+// (36 B / 12 B per tile against the reference's 136 B).  Same tile set and
+// order as tile_graph (tiling.cpp:44-84): per block row, ascending columns.
+int build_tile_store(tcmis_graph *g, int T) {
+  if (T != 8 && T != 16)
+    return set_error(TCMIS_E_INVALID_ARGUMENT, "the compact tile store holds T = 8 or T = 16");
+  if (g->store_T == T) return 0;
+  free_tile_store(g);
+  tcmis_ctx *ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  const int32_t nb = (int32_t)(((int64_t)g->n + T - 1) / T);
+  const int row_bytes = T / 8;
+  if (int rc = dev_alloc(&g->d_tbro, (size_t)nb + 1)) return rc;
+  if (nb == 0) {
+    TCMIS_CUDA(cudaMemsetAsync(g->d_tbro, 0, sizeof(int64_t), st));
+    if (int rc = dev_alloc(&g->d_tcol, 1)) return rc;
+    if (int rc = dev_alloc(&g->d_trow, 1)) return rc;
+    if (int rc = dev_alloc((uint8_t **)&g->d_tbits, 16)) return rc;
+    g->store_T = T;
+    return 0;
+  }
+  // (the solve's own tile counts, g->tile_T, are left alone: the store is
+  // independent of cfg.tile_dim)
+  Items it;
+  if (int rc = plan_items(g, T, nb, it)) return rc;
+  int32_t *scratch_rows = nullptr;
+  int64_t *item_off = nullptr;
+  void *tmp = nullptr;
+  size_t bytes = 0;
+  int64_t tiles = 0;
+  int rc = dev_alloc(&scratch_rows, (size_t)nb + 1);
+  if (!rc) rc = dev_alloc(&item_off, (size_t)it.n_items + 1);
+  if (!rc) {
+    cudaMemsetAsync(scratch_rows, 0, sizeof(int32_t) * ((size_t)nb + 1), st);
+    k_tile_merge<false><<<grid_for(ctx, 32 * it.n_items, 256, 16), 256, 0, st>>>(
+        g->n, T, nb, g->d_off, g->d_nbr, it.n_items, it.row, it.start, it.cnt, scratch_rows,
+        nullptr, nullptr, nullptr, nullptr, row_bytes);
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, it.cnt, item_off, it.n_items, st);
+    rc = dev_alloc((char **)&tmp, bytes);
+  }
+  if (!rc) {
+    cub::DeviceScan::ExclusiveSum(tmp, bytes, it.cnt, item_off, it.n_items, st);
+    int64_t last[2] = {0, 0};
+    cudaMemcpyAsync(&last[0], item_off + it.n_items - 1, 8, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&last[1], it.cnt + it.n_items - 1, 8, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = cuda_error(e, "tile store count");
+    tiles = last[0] + last[1];
+  }
+  if (!rc) rc = dev_alloc(&g->d_tcol, (size_t)tiles);
+  if (!rc) rc = dev_alloc(&g->d_trow, (size_t)tiles);
+  if (!rc) rc = dev_alloc((uint8_t **)&g->d_tbits, (size_t)tiles * T * row_bytes + 16);
+  if (!rc) {
+    k_tile_merge<true><<<grid_for(ctx, 32 * it.n_items, 256, 16), 256, 0, st>>>(
+        g->n, T, nb, g->d_off, g->d_nbr, it.n_items, it.row, it.start, it.cnt, scratch_rows,
+        item_off, g->d_trow, g->d_tcol, g->d_tbits, row_bytes);
+    k_store_bro<<<grid_for(ctx, (int64_t)nb + 1, 256, 8), 256, 0, st>>>(nb, it.start, item_off,
+                                                                        tiles, g->d_tbro);
+    ctx->launches += 4;
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = cuda_error(e, "tile store");
+  }
+  dev_free(scratch_rows);
+  dev_free(item_off);
+  dev_free(tmp);
+  if (!rc) {
+    g->store_T = T;
+    g->store_tiles = tiles;
+  }
   return rc;
 }
 

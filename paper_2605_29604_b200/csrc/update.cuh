@@ -16,11 +16,15 @@
 //   push  k_select already wrote next[u] = 2 for every neighbour of every
 //         candidate; k_update is a coalesced striped pass over the worklist
 //         (block-scan compaction, one atomic per 2048 vertices).
-//   pull  k_select emitted the non-candidates to a check list; k_update_pull
-//         scans each listed row from its end for next[u] == 1 and stops at the
-//         first hit (R-MAT s22 round 1: 5.3M entries examined instead of 7.1M
-//         push stores concentrated on hub lines).  Rows still unsettled after
-//         kThreadMax entries go to a list that k_round_end scans warp-wide.
+//   pull  k_probe_pull walks the round's worklist again; every vertex still
+//         Alive after the select kernels is a non-candidate, and its row is
+//         scanned from the end for next[u] == 1, stopping at the first hit
+//         (R-MAT s22 round 1: 5.3M entries examined instead of 7.1M push
+//         stores concentrated on hub lines).  Rows the probe cannot settle go
+//         to k_update_pull; rows still unsettled after kThreadMax entries go
+//         to a list that k_round_end scans warp-wide.  (A first version had
+//         the select kernels emit a non-candidate list: on the grid that
+//         emission alone cost as much as the select, ncu round 1.)
 // k_round_end then also folds the tile counters, elects the last block, and
 // publishes the round's IterationStats and the graph's loop condition.
 #pragma once
@@ -39,17 +43,20 @@ struct UpdateArgs {
   const int64_t *off;
   const int32_t *nbr;
   int64_t vnnz;            // nnz, negated if nbr is not 16-byte aligned (scan.cuh)
-  uint64_t *key;
+  uint32_t *prio;
   uint8_t *state;
   const uint8_t *next;
   Ctrl *ctrl;
   int32_t *wl0, *wl1;
   int fresh;
   uint64_t seed;
-  const int32_t *check;    // pull: non-candidates of this round
+  int32_t n1;              // round-1 list (non-isolated vertices) for the pull probe
+  const int32_t *nz;
+  int nz_identity;
   int32_t *long_list;      // pull: rows outliving the thread probe (ctrl->pull_count)
   int32_t *undecided;      // pull: rows the probe could not settle (ctrl->pull_undec)
   Publish pub;             // multi-GPU: this round's removals of the own range
+  const uint32_t *tile_hit;  // tile exclusion: per T=16 block row, rows with a candidate nbr
   uint8_t *segflag;
   const int32_t *rowtiles;
   int32_t nseg;
@@ -88,18 +95,23 @@ __global__ void __launch_bounds__(kBlock) k_update(UpdateArgs a) {
     }
 #pragma unroll
     for (int j = 0; j < kUpdItems; ++j) ds[j] = vs[j] >= 0 ? a.next[vs[j]] : 1;
+    if (a.tile_hit) {  // tile-form exclusion (tile_excl.cuh): nc > 0 from the row masks
+#pragma unroll
+      for (int j = 0; j < kUpdItems; ++j)
+        if (ds[j] == 0 && ((__ldg(&a.tile_hit[vs[j] >> 4]) >> (vs[j] & 15)) & 1u)) ds[j] = 2;
+    }
     int mine = 0;
 #pragma unroll
     for (int j = 0; j < kUpdItems; ++j) {
       const int32_t v = vs[j];
       if (v < 0 || ds[j] == 1) continue;  // candidates were settled by k_select
       if (ds[j] == 2) {
-        mark_removed(v, a.state, a.key);
+        mark_removed(v, a.state);
         publish(a.pub, v);
         ++rem;
       } else {
         ++mine;
-        if (a.fresh) a.key[v] = fresh_key(v, fresh_m);
+        if (a.fresh) a.prio[v] = fresh_prio(v, fresh_m);
       }
     }
     int pos, total;
@@ -119,15 +131,19 @@ __global__ void __launch_bounds__(kBlock) k_update(UpdateArgs a) {
 
 constexpr int kPullK = 4;  // row entries the straight-line pull probe examines
 
-// Pull probe: one thread per non-candidate, straight-line: the last <= 8 row
-// entries with two aligned 16-byte loads, candidate flags of the last kPullK.
+// Pull probe: one thread per vertex of the round's worklist (the same list the
+// select kernels walked); the select kernels turned this round's candidates
+// InMIS, so state == Alive marks exactly the alive non-candidates.
+// Straight-line: the last <= 8 row entries with two aligned 16-byte loads,
+// candidate flags of the last kPullK.
 __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
   __shared__ int32_t s_srv[kBlock / 32][64];
   __shared__ int32_t s_und[kBlock / 32][64];
   Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
-  const int64_t cnt = ctrl->check_count;
+  const int64_t cnt = round == 1 ? a.n1 : ctrl->wl_count[round & 1];
   if ((int64_t)blockIdx.x * kBlock >= cnt) return;
+  const int32_t *wl = round == 1 ? a.nz : ((round & 1) ? a.wl1 : a.wl0);
   int32_t *out = (round & 1) ? a.wl0 : a.wl1;
   int *tail = &ctrl->wl_count[(round + 1) & 1];
   const uint64_t fresh_m = a.fresh ? mix64(combine_seed(a.seed, (uint64_t)round + 1)) : 0;
@@ -141,8 +157,10 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
     bool survive = false, undecided = false;
     int32_t v = 0;
     if (i < cnt) {
-      v = __ldg(&a.check[i]);
-      const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
+      v = (round == 1 && a.nz_identity) ? (int32_t)i : __ldg(&wl[i]);
+    }
+    if (i < cnt && a.state[v] == TCMIS_ALIVE) {
+      const int64_t s = ld_stream(&a.off[v]), e = ld_stream(&a.off[v + 1]);
       int32_t u[8];
       load_tail8(a.nbr, a.vnnz, s, e, u);
       bool hit = false;
@@ -150,12 +168,12 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
       for (int j = 0; j < kPullK; ++j)
         if (u[j] >= 0) hit |= next[u[j]] == 1;
       if (hit) {
-        mark_removed(v, a.state, a.key);
+        mark_removed(v, a.state);
         publish(a.pub, v);
         ++rem;
       } else if (e - s <= kPullK) {
         survive = true;
-        if (a.fresh) a.key[v] = fresh_key(v, fresh_m);
+        if (a.fresh) a.prio[v] = fresh_prio(v, fresh_m);
       } else {
         undecided = true;
       }
@@ -212,13 +230,13 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
         if (u[j] >= 0) hit |= next[u[j]] == 1;
       hi = w;
       if (hit) {
-        mark_removed(v, a.state, a.key);
+        mark_removed(v, a.state);
         publish(a.pub, v);
         ++rem;
         mode = kFetch;
       } else if (hi <= s) {
         survive = true;
-        if (a.fresh) a.key[v] = fresh_key(v, fresh_m);
+        if (a.fresh) a.prio[v] = fresh_prio(v, fresh_m);
         mode = kFetch;
       } else if (e - hi >= kThreadMax) {
         defer = true;
@@ -270,11 +288,11 @@ __global__ void __launch_bounds__(kBlock)
     }
     if (lane == 0) {
       if (hit) {
-        mark_removed(v, a.state, a.key);
+        mark_removed(v, a.state);
         publish(a.pub, v);
         ++rem;
       } else {
-        if (a.fresh) a.key[v] = fresh_key(v, fresh_m);
+        if (a.fresh) a.prio[v] = fresh_prio(v, fresh_m);
         out[atomicAdd(&ctrl->wl_count[out_slot], 1)] = v;
       }
     }
@@ -317,7 +335,6 @@ __global__ void __launch_bounds__(kBlock)
     vc->wl_count[round & 1] = 0;
     vc->long_count = 0;
     vc->pull_count = 0;
-    vc->check_count = 0;
     vc->sel_undec = 0;
     vc->pull_undec = 0;
     vc->main_rounds = vc->main_rounds + 1;

@@ -73,8 +73,11 @@ class PartitionedResult:
 class GpuRank:
     """The device side of one rank (csrc/dist.cu through the C-ABI)."""
 
-    def __init__(self, ctx, n: int, lo: int, hi: int, offsets: np.ndarray,
-                 neighbors: np.ndarray, device: str):
+    def __init__(self, ctx, n: int, lo: int, hi: int, offsets: np.ndarray | None,
+                 neighbors: np.ndarray | None, device: str, full=None, rows=None):
+        """Upload rows [lo, hi) from host CSR (full offsets + the full neighbour
+        array, or just the own `rows`), or cut them from a device-resident full
+        graph `full` (a DeviceGraph) with no host round trip."""
         import torch
 
         import paper_2605_29604_b200 as tc
@@ -84,6 +87,8 @@ class GpuRank:
                 ("tcmis_graph_upload_partition",
                  [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                   C.POINTER(C.c_void_p)]),
+                ("tcmis_graph_partition",
+                 [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
                 ("tcmis_dist_begin", [C.c_void_p, C.c_void_p]),
                 ("tcmis_dist_select", [C.c_void_p, C.c_void_p, C.c_int32]),
                 ("tcmis_dist_apply", [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
@@ -94,15 +99,24 @@ class GpuRank:
             fn = getattr(L, name)
             fn.restype = C.c_int
             fn.argtypes = args
-        off = np.ascontiguousarray(offsets, np.int64)
-        rows = np.ascontiguousarray(neighbors[off[lo]:off[hi]], np.int32)
         h = C.c_void_p()
-        tc._check(L.tcmis_graph_upload_partition(
-            ctx.h, n, lo, hi, C.c_void_p(off.ctypes.data),
-            C.c_void_p(rows.ctypes.data) if rows.size else None, C.byref(h)))
+        if full is not None:
+            tc._check(L.tcmis_graph_partition(full.h, lo, hi, C.byref(h)))
+        else:
+            off = np.ascontiguousarray(offsets, np.int64)
+            if rows is None:
+                rows = neighbors[off[lo]:off[hi]]
+            rows = np.ascontiguousarray(rows, np.int32)
+            tc._check(L.tcmis_graph_upload_partition(
+                ctx.h, n, lo, hi, C.c_void_p(off.ctypes.data),
+                C.c_void_p(rows.ctypes.data) if rows.size else None, C.byref(h)))
         self.g = tc.DeviceGraph(h, ctx)
         self.n, self.lo, self.hi = n, lo, hi
         self.stream = torch.cuda.ExternalStream(ctx.stream, device=device)
+        self.counts = torch.zeros(5, dtype=torch.int64, device=device)
+
+    def close(self):
+        self.g.close()
 
     def words_tensor(self, words: int):
         return self.torch.zeros(words, dtype=self.torch.int32, device=self.device)
@@ -123,11 +137,12 @@ class GpuRank:
                                                 C.c_void_p(lo.ctypes.data), len(rank_lo) - 1,
                                                 maxw, me, what))
 
-    def update(self, bits) -> np.ndarray:
-        counts = np.zeros(5, np.int64)
+    def update(self, bits):
+        """Stream-ordered; returns this rank's counters as a device tensor."""
         self.tc._check(self.L.tcmis_dist_update(self.g.h, C.c_void_p(bits.data_ptr()),
-                                                 bits.numel(), C.c_void_p(counts.ctypes.data)))
-        return counts
+                                                 bits.numel(),
+                                                 C.c_void_p(self.counts.data_ptr())))
+        return self.counts
 
     def h3_tiles(self):
         ev, tot = C.c_int64(0), C.c_int64(0)
@@ -141,6 +156,30 @@ class GpuRank:
 
     def collective_stream(self):
         return self.torch.cuda.stream(self.stream)
+
+
+def _staged(dist, t) -> bool:
+    """gloo cannot run these collectives on device tensors (the single-GPU
+    emulation runs of bench.py): stage through host memory."""
+    return t.is_cuda and dist.get_backend() == "gloo"
+
+
+def _all_gather(dist, out, inp):
+    if _staged(dist, inp):
+        o = out.cpu()
+        dist.all_gather_into_tensor(o, inp.cpu())
+        out.copy_(o)
+    else:
+        dist.all_gather_into_tensor(out, inp)
+
+
+def _all_reduce(dist, t):
+    if _staged(dist, t):
+        c = t.cpu()
+        dist.all_reduce(c)
+        t.copy_(c)
+    else:
+        dist.all_reduce(t)
 
 
 def solve_partitioned(rank_obj, rank_lo: list[int], rank: int, world: int, dist,
@@ -163,13 +202,15 @@ def solve_partitioned(rank_obj, rank_lo: list[int], rank: int, world: int, dist,
     with rank_obj.collective_stream():
         for it in range(1, cap + 1):
             rank_obj.select(mine)
-            dist.all_gather_into_tensor(gathered, mine)
+            _all_gather(dist, gathered, mine)
             rank_obj.apply(gathered, rank_lo, rank, maxw, 0)
             counts = rank_obj.update(mine)
-            dist.all_gather_into_tensor(gathered, mine)
+            _all_gather(dist, gathered, mine)
             rank_obj.apply(gathered, rank_lo, rank, maxw, 1)
-            t = torch.tensor(counts, dtype=torch.int64, device=mine.device)
-            dist.all_reduce(t)
+            t = (counts.clone() if torch.is_tensor(counts)
+                 else torch.tensor(counts, dtype=torch.int64, device=mine.device))
+            _all_reduce(dist, t)
+            # the round's only host synchronisation: the termination test
             sel, rem, alive, ev, sk = (int(x) for x in t.cpu().tolist())
             rounds.append(RoundStats(it, sel, rem, alive, ev, sk))
             if alive == 0:
@@ -179,7 +220,7 @@ def solve_partitioned(rank_obj, rank_lo: list[int], rank: int, world: int, dist,
         if heuristic == "h3":
             ev, tot = rank_obj.h3_tiles()
             t = torch.tensor([ev, tot], dtype=torch.int64, device=mine.device)
-            dist.all_reduce(t)
+            _all_reduce(dist, t)
             rounds = collapse_h3(rounds, n, int(t[0]), int(t[1]))
     return PartitionedResult(rank_obj.state(), rounds, rank_lo)
 
@@ -211,8 +252,10 @@ def solve_partitioned_local(ranks: list, rank_lo: list[int], heuristic: str = "h
         gathered.copy_(torch.cat(mine))
         for k, r in enumerate(ranks):
             r.apply(gathered, rank_lo, k, maxw, 0)
-        counts = sum(r.update(m) for r, m in zip(ranks, mine))
+        for r, m in zip(ranks, mine):
+            r.update(m)
         torch.cuda.synchronize()
+        counts = sum(r.counts.cpu() for r in ranks)
         gathered.copy_(torch.cat(mine))
         for k, r in enumerate(ranks):
             r.apply(gathered, rank_lo, k, maxw, 1)

@@ -1,11 +1,14 @@
 # one warm solve + one profiled solve of the bench config (used under ncu only)
-import sys; sys.path.insert(0, '.')
+# env EXCL = auto | push | pull | tile-bits | tile-mma
+import os, sys; sys.path.insert(0, '.')
 import paper_2605_29604_b200 as tc
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "rmat22"
 ctx = tc.Context(0)
 import bench
 dg = bench.make_device_graph(tc, cfgname, ctx)
 dg.tile(16)
+ex = {"auto": tc.Exclusion.AUTO, "push": tc.Exclusion.PUSH, "pull": tc.Exclusion.CSR_PULL,
+      "tile-bits": tc.Exclusion.TILE_BITS, "tile-mma": tc.Exclusion.TILE_MMA}[os.environ.get("EXCL", "auto")]
 for _ in range(2):
-    r = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, host_loop=True))
+    r = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, host_loop=True, exclusion=ex))
 print("ok", r.cardinality(), len(r.iterations))

@@ -3,12 +3,14 @@ the reference's golden fixtures.  Bit-exact on every field the reference
 reports: MIS membership, |MIS|, iteration count, per-iteration
 candidates_selected / vertices_removed / alive_remaining / tiles_evaluated /
 tiles_skipped."""
+import os
+
 import numpy as np
 import pytest
 
 import oracle as O
 import paper_2605_29604_b200 as tc
-from conftest import golden, golden_names
+from conftest import GOLDEN, golden, golden_names
 
 pytestmark = pytest.mark.gpu
 
@@ -276,7 +278,7 @@ def _device_graph_for(spec, ctx):
     return tc.DeviceGraph.upload(as_tc(O.gen("petersen")), ctx)
 
 
-def _check_golden(name, ctx):
+def _check_golden(name, ctx, exclusion=tc.Exclusion.AUTO, only=None):
     gd = golden(name)
     dg = _device_graph_for(gd["spec"], ctx)
     assert (dg.n, dg.num_edges()) == (gd["n"], gd["m"])
@@ -285,9 +287,11 @@ def _check_golden(name, ctx):
     assert O.checksum(h.neighbors) == gd["nbr_checksum"]
     assert dg.tile(gd["tile_dim"]) == gd["tile_count"]
     for key, exp in gd["results"].items():
+        if only and key != only:
+            continue
         heur, seed = key.split("/seed")
         res = tc.run_mis(dg, tc.EngineConfig(heuristic=HEUR[heur], seed=int(seed),
-                                             tile_dim=gd["tile_dim"]))
+                                             tile_dim=gd["tile_dim"], exclusion=exclusion))
         got = [list(t) for t in rounds_tuple(res.iterations)]
         if heur == "luby-perm":
             got = [r[:3] + [0, 0] for r in got]
@@ -309,6 +313,25 @@ def test_golden_baseline_configs(ctx, name):
     _check_golden(name, ctx)
 
 
+def test_rmat26_golden_rounds(ctx):
+    """R-MAT s26 (~1.05B edges) on one GPU against the reference's rounds
+    (tests/golden/rmat26_ef16.json): n, m, max degree, the
+    T=16 tile count, |MIS|, the iteration count and every round's selected /
+    removed / alive, plus the round-1 trajectory terms."""
+    gd = golden("rmat26_ef16")
+    dg = tc.DeviceGraph.rmat(26, 16, 1, ctx)
+    assert (dg.n, dg.num_edges()) == (gd["n"], gd["m"])
+    assert dg.tile(16) == gd["tile_count"]
+    res = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=1, tile_dim=16))
+    exp = gd["h2_seed1"]
+    assert res.cardinality() == exp["mis_size"]
+    got = [[i.candidates_selected, i.vertices_removed, i.alive_remaining] for i in res.iterations]
+    assert got == exp["rounds_sel_rem_alive"]
+    member = res.state == 1
+    assert int(member.sum()) == exp["mis_size"]
+    dg.close()
+
+
 def test_rmat22_properties(ctx):
     """Size-independent properties at s22: independence and maximality of the
     result, and |MIS| == the sequential greedy count."""
@@ -324,15 +347,20 @@ def test_rmat22_properties(ctx):
     assert np.all(np.diff(res.mis) > 0)                             # ascending ids
 
 
+EXCL = {"push": tc.Exclusion.PUSH, "pull": tc.Exclusion.CSR_PULL,
+        "tile-bits": tc.Exclusion.TILE_BITS, "tile-mma": tc.Exclusion.TILE_MMA}
+
+
 @pytest.mark.parametrize("kind,args", GRAPHS + [("rmat", (14, 16, 2))])
-@pytest.mark.parametrize("excl", ["push", "pull"])
+@pytest.mark.parametrize("excl", list(EXCL))
 @pytest.mark.parametrize("heur", ["h1", "h2", "h3", "luby-fresh"])
 def test_exclusion_forms_bit_exact(ctx, kind, args, excl, heur):
-    """Both Phase-2 forms (candidates push / non-candidates pull) reproduce the
+    """Every Phase-2 form (candidates push / non-candidates pull / T=16 bit
+    tiles on CUDA cores / T=16 tiles on tensor cores) reproduces the
     reference's rounds exactly."""
     g = O.gen(kind, *args)
     dg = tc.DeviceGraph.upload(as_tc(g), ctx)
-    mode = tc.Exclusion.PUSH if excl == "push" else tc.Exclusion.CSR_PULL
+    mode = EXCL[excl]
     exp = O.solve(g, heur, 3, tile_dim=16)
     for host_loop in (False, True):
         got = tc.run_mis(dg, tc.EngineConfig(heuristic=HEUR[heur], seed=3, tile_dim=16,
@@ -357,6 +385,32 @@ def test_tail_threshold_invariance(ctx, thr, monkeypatch):
                                                          exclusion=excl, host_loop=host_loop))
                     assert np.array_equal(got.mis, exp.mis), (kind, heur, excl, host_loop)
                     assert rounds_tuple(got.iterations) == oracle_tuple(exp)
+
+
+@pytest.mark.parametrize("T", [8, 16])
+def test_tile_store_matches_tile_graph(ctx, T):
+    """The compact device store holds exactly tile_graph's tiles
+    (tiling.cpp:44-84): same block-row offsets, columns and row bits."""
+    n = 5000
+    star = O.graph_from_edges(n, np.stack([np.zeros(n - 1, np.int32),
+                                           np.arange(1, n, dtype=np.int32)], 1))
+    for g in (O.gen("rmat", 11, 16, 2), O.gen("grid", 37), O.gen("gnp_avg", 2000, 30.0, 1),
+              O.gen("rgg", 3000, 3.0, 2), star):
+        bro, col, rows = tc.tile_store(as_tc(g), T, ctx)
+        tr, tcol, rb, obro = O.tile_graph(g, T)
+        assert np.array_equal(bro, obro)
+        assert np.array_equal(col, tcol)
+        assert np.array_equal(rows.reshape(-1).astype(np.uint64), rb)
+
+
+@pytest.mark.parametrize("name", ["grid4096", "rmat22_ef16", "rgg24m_d3"])
+@pytest.mark.parametrize("excl", ["tile-bits", "tile-mma"])
+def test_golden_baseline_tile_forms(ctx, name, excl):
+    """The tile-form exclusion kernels at full BASELINE size, h2, against the
+    reference's golden rounds."""
+    if not os.path.exists(os.path.join(GOLDEN, name + ".json")):
+        pytest.skip("no golden")
+    _check_golden(name, ctx, exclusion=EXCL[excl], only="h2/seed1")
 
 
 @pytest.mark.parametrize("excl", ["bits", "mma"])
