@@ -84,11 +84,25 @@ __device__ __forceinline__ void publish(const Publish &p, int32_t v) {
   if (p.bits) atomicOr(&p.bits[(uint32_t)(v - p.lo) >> 5], 1u << ((uint32_t)(v - p.lo) & 31u));
 }
 
+// The gathered summary of the key order: q[v] = clamp(p[v] >> shift, 1,
+// 0xffff) is monotone in p, so q[u] != q[v] decides key(u) > key(v) with a
+// 2-byte gather from a vector half the size of p (RGG 24M: 48 MB against
+// 96 MB of p, against the 126 MB L2); only q[u] == q[v] needs p[u].  q = 0
+// marks a vertex that left the alive set (kNoNeighborKey, priorities.hpp:57),
+// so no state gather is needed either.  shift = scale_bits + 1 - 16 for the
+// degree-aware priorities (p <= 2^scale_bits for every vertex with an edge,
+// priorities.cpp:43-51) and 16 for hash priorities.
+__host__ __device__ __forceinline__ uint16_t q_of(uint32_t p, int shift) {
+  const uint32_t x = p >> shift;
+  return (uint16_t)(x > 0xffffu ? 0xffffu : (x ? x : 1u));
+}
+
 // An alive non-candidate with a candidate neighbour is removed
-// (engine.cpp:144-147); state Removed makes it invisible (kNoNeighborKey) to
-// the alive vertices that still neighbour it from the next round on.
-__device__ __forceinline__ void mark_removed(int32_t v, uint8_t *state) {
+// (engine.cpp:144-147); q = 0 makes it invisible to the alive vertices that
+// still neighbour it from the next round on.
+__device__ __forceinline__ void mark_removed(int32_t v, uint8_t *state, uint16_t *q) {
   state[v] = TCMIS_REMOVED;
+  q[v] = 0;
 }
 
 // priority_key (priorities.hpp:61-64): strict (p, id) order, never 0
@@ -98,20 +112,27 @@ __device__ __forceinline__ uint64_t key_of(uint32_t p, int32_t v) {
 
 // A neighbour u blocks v (compute_max_np + generate_candidates,
 // engine.cpp:86-119) iff u is alive at the start of the round and its key is
-// above v's.  Round 1 starts with every vertex alive, so the state gather is
-// skipped there.  Candidates of the running round turn InMIS while the
-// select kernels run; they stay visible (only Removed hides a vertex, and
-// removals are written by the update kernels after the select kernels).
-__device__ __forceinline__ bool blocks(const uint32_t *__restrict__ prio,
-                                       const uint8_t *state, bool r1, int32_t u, uint64_t kv) {
-  const uint32_t pu = __ldg(&prio[u]);
-  const bool vis = r1 || state[u] != TCMIS_REMOVED;
-  return vis && key_of(pu, u) > kv;
+// above v's.  Candidates of the running round turn InMIS while the select
+// kernels run but keep their q (only removals, written by the update kernels
+// after the select kernels, zero it).
+__device__ __forceinline__ bool blocks(const uint16_t *__restrict__ q,
+                                       const uint32_t *__restrict__ prio, int32_t u,
+                                       uint32_t qv, uint64_t kv) {
+  const uint32_t qu = __ldg(&q[u]);
+  if (qu != qv) return qu > qv;  // qu == 0 (removed) never blocks: qv >= 1
+  return key_of(__ldg(&prio[u]), u) > kv;
 }
 
 __device__ __forceinline__ uint32_t fresh_prio(int32_t v, uint64_t fresh_m) {
   // engine.cpp:324-325: next round's redrawn h1 priority
   return (uint32_t)(vertex_hash_m((uint64_t)v, fresh_m) >> 32);
+}
+
+__device__ __forceinline__ void set_fresh(uint32_t *prio, uint16_t *q, int32_t v,
+                                          uint64_t fresh_m) {
+  const uint32_t p = fresh_prio(v, fresh_m);
+  prio[v] = p;
+  q[v] = q_of(p, 16);
 }
 
 // Per-warp output buffer in shared memory (64 entries), flushed 32 at a time

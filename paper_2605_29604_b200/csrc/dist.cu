@@ -49,7 +49,7 @@ __global__ void k_partial_offsets(int32_t n, int32_t lo, int32_t hi,
 __global__ void k_apply_bits(const uint32_t *__restrict__ gathered,
                              const int32_t *__restrict__ rank_lo, int32_t world, int32_t maxw,
                              int32_t me, int what, uint8_t *__restrict__ next,
-                             uint8_t *__restrict__ state) {
+                             uint8_t *__restrict__ state, uint16_t *__restrict__ q) {
   const int64_t total = (int64_t)world * maxw;
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
        w += (int64_t)gridDim.x * blockDim.x) {
@@ -67,6 +67,7 @@ __global__ void k_apply_bits(const uint32_t *__restrict__ gathered,
         state[v] = TCMIS_IN_MIS;
       } else {  // remote removal: invisible from now on
         state[v] = TCMIS_REMOVED;
+        q[v] = 0;
       }
     }
   }
@@ -163,7 +164,7 @@ int dist_apply(tcmis_graph *g, const uint32_t *d_gathered, const int32_t *h_rank
     TCMIS_CUDA(cudaStreamSynchronize(ctx->stream));  // h_rank_lo storage may change
   }
   k_apply_bits<<<grid_for(ctx, (int64_t)world * maxw, 256, 8), 256, 0, ctx->stream>>>(
-      d_gathered, d.d_rank_lo, world, maxw, me, what, g->ws.next, g->ws.state);
+      d_gathered, d.d_rank_lo, world, maxw, me, what, g->ws.next, g->ws.state, g->ws.q);
   TCMIS_LAUNCHED(ctx);
   return 0;
 }

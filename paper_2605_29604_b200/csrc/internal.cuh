@@ -68,6 +68,7 @@ struct Workspace {
   size_t n_cap = 0;
   size_t seg_cap = 0;
   uint32_t *prio = nullptr;
+  uint16_t *q = nullptr;          // q_of(prio) (common.cuh), 0 once removed
   uint8_t *state = nullptr;
   uint8_t *next = nullptr;
   int32_t *wl[2] = {nullptr, nullptr};
@@ -231,7 +232,7 @@ struct RoundArgs {
 int launch_select(tcmis_graph *g, const RoundArgs &a);
 int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle cond, int use_cond);
 int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
-                      uint32_t *p_out, uint8_t *state, uint8_t *next,
+                      uint32_t *p_out, uint16_t *q_out, uint8_t *state, uint8_t *next,
                       uint8_t *segflag = nullptr, int T = 1);
 double avg_degree(const tcmis_graph *g);
 

@@ -45,6 +45,7 @@ struct SelectArgs {
   const int32_t *nbr;
   int64_t vnnz;            // nnz, negated if nbr is not 16-byte aligned (scan.cuh)
   const uint32_t *prio;
+  const uint16_t *q;        // q_of(p), 0 once removed (common.cuh)
   uint8_t *next;
   uint8_t *state;
   uint8_t *segflag;        // null: no tile counters
@@ -73,7 +74,6 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
   __shared__ int32_t s_und[kBlock / 32][64];
   Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
-  const bool r1 = round == 1;
   // round 1 visits only the non-isolated vertices (k_priorities already made
   // the isolated ones candidates)
   const int64_t cnt = round == 1 ? a.n1 : ctrl->wl_count[round & 1];
@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
   const int32_t *wl = round == 1 ? a.nz : ((round & 1) ? a.wl1 : a.wl0);
   const int32_t *__restrict__ nbr = a.nbr;
   const uint32_t *__restrict__ prio = a.prio;
+  const uint16_t *__restrict__ q = a.q;
   const int lane = threadIdx.x & 31;
   WarpOut und{s_und[threadIdx.x >> 5], 0};
   unsigned long long sel = 0;
@@ -93,12 +94,13 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
       v = (round == 1 && a.nz_identity) ? (int32_t)i : __ldg(&wl[i]);
       const int64_t s = ld_stream(&a.off[v]), e = ld_stream(&a.off[v + 1]);
       const uint64_t kv = key_of(__ldg(&prio[v]), v);
+      const uint32_t qv = __ldg(&q[v]);
       int32_t u[8];
       load_tail8(nbr, a.vnnz, s, e, u);
       bool blocked = false;
 #pragma unroll
       for (int j = 0; j < kProbeK; ++j)
-        if (u[j] >= 0) blocked |= blocks(prio, a.state, r1, u[j], kv);
+        if (u[j] >= 0) blocked |= blocks(q, prio, u[j], qv, kv);
       if (blocked) {
         // a non-candidate: the pull exclusion finds it on the worklist
       } else if (e - s <= kProbeK) {
@@ -127,9 +129,9 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
   Ctrl *ctrl = a.ctrl;
   const int64_t cnt = ctrl->sel_undec;
   if ((int64_t)blockIdx.x * kBlock >= cnt) return;
-  const bool r1 = ctrl->round == 1;
   const int32_t *__restrict__ nbr = a.nbr;
   const uint32_t *__restrict__ prio = a.prio;
+  const uint16_t *__restrict__ q = a.q;
   const int64_t stride = (int64_t)gridDim.x * kBlock;
   unsigned long long sel = 0;
   int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x - stride;
@@ -137,6 +139,7 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
   int32_t v = 0;
   int64_t s = 0, e = 0, hi = 0;
   uint64_t kv = 0;
+  uint32_t qv = 0;
   auto fetch = [&]() {
     i += stride;
     if (i < cnt) {
@@ -144,6 +147,7 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
       s = __ldg(&a.off[v]);
       e = __ldg(&a.off[v + 1]);
       kv = key_of(__ldg(&prio[v]), v);
+      qv = __ldg(&q[v]);
       hi = e - kProbeK;  // the probe examined the last kProbeK entries
       mode = kScan;
     } else {
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
       bool blocked = false;
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (u[j] >= 0) blocked |= blocks(prio, a.state, r1, u[j], kv);
+        if (u[j] >= 0) blocked |= blocks(q, prio, u[j], qv, kv);
       hi = w;
       if (blocked) {
         mode = kFetch;
@@ -192,7 +196,6 @@ __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
   Ctrl *ctrl = a.ctrl;
   const int cnt = ctrl->long_count;
   if ((int64_t)blockIdx.x * (kBlock / 32) >= cnt) return;
-  const bool r1 = ctrl->round == 1;
   const int lane = threadIdx.x & 31;
   const int32_t *__restrict__ nbr = a.nbr;
   const uint32_t *__restrict__ prio = a.prio;
@@ -202,6 +205,7 @@ __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
     const int32_t v = a.long_list[q];
     const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
     const uint64_t kv = key_of(__ldg(&prio[v]), v);
+    const uint32_t qv = __ldg(&a.q[v]);
     // the thread stage examined at least the last kThreadMax - 3 entries (its
     // first window may be short); rescanning an entry is harmless
     int64_t hi = e - (kThreadMax - 3);
@@ -216,7 +220,7 @@ __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
       bool b = false;
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (u[j] >= 0) b |= blocks(prio, a.state, r1, u[j], kv);
+        if (u[j] >= 0) b |= blocks(a.q, prio, u[j], qv, kv);
       blocked = __any_sync(0xffffffffu, b);
       hi -= 128;
     }

@@ -57,7 +57,7 @@ constexpr int kPrioV = 4;
 __global__ void __launch_bounds__(256)
     k_priorities(int32_t n, const int64_t *__restrict__ off, int aligned, int mode,
                  uint64_t mseed, double avg, double scale, uint32_t *__restrict__ p_out,
-                 uint8_t *__restrict__ state, uint8_t *__restrict__ next,
+                 uint16_t *__restrict__ q_out, int qshift, uint8_t *__restrict__ state, uint8_t *__restrict__ next,
                  uint8_t *__restrict__ segflag, int T, int tshift) {
   const int32_t quads = (int32_t)(((int64_t)n + kPrioV - 1) / kPrioV);
   for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < quads;
@@ -100,11 +100,16 @@ __global__ void __launch_bounds__(256)
     }
     if (full) {
       if (p_out) *reinterpret_cast<uint4 *>(p_out + v0) = make_uint4(pv[0], pv[1], pv[2], pv[3]);
+      if (q_out)
+        *reinterpret_cast<uint2 *>(q_out + v0) =
+            make_uint2((uint32_t)q_of(pv[0], qshift) | ((uint32_t)q_of(pv[1], qshift) << 16),
+                       (uint32_t)q_of(pv[2], qshift) | ((uint32_t)q_of(pv[3], qshift) << 16));
       if (state) *reinterpret_cast<uint32_t *>(state + v0) = st4;
       if (next) *reinterpret_cast<uint32_t *>(next + v0) = nx4;
     } else {
       for (int j = 0; j < kPrioV && v0 + j < n; ++j) {
         if (p_out) p_out[v0 + j] = pv[j];
+        if (q_out) q_out[v0 + j] = q_of(pv[j], qshift);
         if (state) state[v0 + j] = (uint8_t)(st4 >> (8 * j));
         if (next) next[v0 + j] = (uint8_t)(nx4 >> (8 * j));
       }
@@ -137,11 +142,13 @@ __global__ void k_h1(int32_t n, uint64_t mseed, uint32_t *__restrict__ p) {
 // part (everyone else is Removed, key 0 = invisible)
 __global__ void k_resolve_init(int32_t n, const uint32_t *__restrict__ p,
                                const uint8_t *__restrict__ states, uint32_t *__restrict__ prio,
+                               uint16_t *__restrict__ q,
                                uint8_t *__restrict__ state, uint8_t *__restrict__ next) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     const bool alive = states[v] == TCMIS_ALIVE;
     prio[v] = p[v];
+    q[v] = alive ? q_of(p[v], 16) : 0;  // any monotone summary works
     state[v] = alive ? TCMIS_ALIVE : TCMIS_REMOVED;
     next[v] = 0;
   }
@@ -258,6 +265,7 @@ void timeline_end(tcmis_ctx *ctx) {
 
 void free_workspace(Workspace &ws) {
   dev_free(ws.prio);
+  dev_free(ws.q);
   dev_free(ws.state);
   dev_free(ws.next);
   dev_free(ws.wl[0]);
@@ -308,6 +316,7 @@ int ensure_workspace(tcmis_graph *g) {
       ws.exec = nullptr;
     }
     dev_free(ws.prio);
+  dev_free(ws.q);
     dev_free(ws.state);
     dev_free(ws.next);
     dev_free(ws.wl[0]);
@@ -323,6 +332,7 @@ int ensure_workspace(tcmis_graph *g) {
     dev_free(ws.tile_hit);
     ws.n_cap = 0;
     if (int rc = dev_alloc(&ws.prio, n)) return rc;
+    if (int rc = dev_alloc(&ws.q, n + 8)) return rc;
     if (int rc = dev_alloc(&ws.state, n)) return rc;
     if (int rc = dev_alloc(&ws.next, n)) return rc;
     if (int rc = dev_alloc(&ws.wl[0], n)) return rc;
@@ -405,8 +415,15 @@ namespace {
 
 }  // namespace
 
+// common.cuh q_of: the degree-aware priorities of vertices with an edge are
+// <= 2^scale_bits (avg / (avg + deg - eps) <= 1), hash priorities span u32
+int q_shift(int heuristic, int scale_bits) {
+  if (heuristic == TCMIS_H1 || heuristic == TCMIS_LUBY_FRESH) return 16;
+  return scale_bits + 1 > 16 ? scale_bits + 1 - 16 : 0;
+}
+
 int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
-                      uint32_t *p_out, uint8_t *state, uint8_t *next,
+                      uint32_t *p_out, uint16_t *q_out, uint8_t *state, uint8_t *next,
                       uint8_t *segflag, int T) {
   tcmis_ctx *ctx = g->ctx;
   int mode = 1;
@@ -425,8 +442,8 @@ int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bi
   TCMIS_TIMED(ctx, "k_priorities",
               (k_priorities<<<grid, 256, 0, ctx->stream>>>(g->n, off, aligned, mode, mseed,
                                                           mode ? avg_degree(g) : 0.0, scale,
-                                                          p_out, state, next, segflag, T,
-                                                          tshift)));
+                                                          p_out, q_out, q_shift(heuristic, scale_bits),
+                                                          state, next, segflag, T, tshift)));
   TCMIS_LAUNCHED(ctx);
   return 0;
 }
@@ -463,6 +480,7 @@ SelectArgs select_args(tcmis_graph *g, const RoundArgs &a) {
   s.nbr = a.nbr;
   s.vnnz = a.vnnz;
   s.prio = ws.prio;
+  s.q = ws.q;
   s.next = ws.next;
   s.state = ws.state;
   s.segflag = a.seg_mode ? ws.segflag : nullptr;
@@ -486,6 +504,7 @@ UpdateArgs update_args(tcmis_graph *g, const RoundArgs &a) {
   u.nbr = a.nbr;
   u.vnnz = a.vnnz;
   u.prio = ws.prio;
+  u.q = ws.q;
   u.state = ws.state;
   u.next = ws.next;
   u.ctrl = ws.ctrl;
@@ -516,6 +535,7 @@ TailArgs tail_args(tcmis_graph *g, const RoundArgs &a) {
   t.off = a.off;
   t.nbr = a.nbr;
   t.prio = ws.prio;
+  t.q = ws.q;
   t.next = ws.next;
   t.state = ws.state;
   t.segflag = ws.segflag;
@@ -693,7 +713,7 @@ int solve_prepare(tcmis_graph *g, const tcmis_config *cfg, RoundArgs &a, int64_t
   const int32_t nseg = tiled ? g->tile_nb : 0;
   const int seg_mode = !tiled ? 0 : (H == TCMIS_H3 ? 2 : 1);
   if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
-  if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio, ws.state,
+  if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio, ws.q, ws.state,
                                  ws.next, seg_mode ? ws.segflag : nullptr, T > 0 ? T : 1))
     return rc;
   Ctrl c0{};
@@ -751,7 +771,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   if (timing) timeline_begin(ctx);
   if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
   uint8_t *seg0 = seg_mode ? ws.segflag : nullptr;
-  if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio, ws.state,
+  if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio, ws.q, ws.state,
                                  ws.next, seg0, T > 0 ? T : 1))
     return rc;
   Ctrl c0{};
@@ -830,7 +850,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       step = true;
       a.tail_thr = 0;
       if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
-      if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio,
+      if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio, ws.q,
                                      ws.state, ws.next, seg0, T > 0 ? T : 1))
         return rc;
       *ws.h_ctrl = c0;
@@ -998,7 +1018,7 @@ int priorities_impl(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits
   }
   uint32_t *d_p = nullptr;
   if (int rc = dev_alloc(&d_p, (size_t)g->n)) return rc;
-  int rc = launch_priorities(g, heuristic, seed, scale_bits, d_p, nullptr, nullptr);
+  int rc = launch_priorities(g, heuristic, seed, scale_bits, d_p, nullptr, nullptr, nullptr);
   if (!rc) {
     cudaError_t e = cudaMemcpyAsync(p_out, d_p, sizeof(uint32_t) * g->n, cudaMemcpyDeviceToHost,
                                     g->ctx->stream);
@@ -1118,7 +1138,7 @@ int h3_resolution_impl(tcmis_graph *g, const uint32_t *p, const uint8_t *states,
   if (!rc) {
     cudaMemcpyAsync(d_p, p, 4ull * g->n, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(d_s, states, g->n, cudaMemcpyHostToDevice, st);
-    k_resolve_init<<<grid_for(ctx, g->n, 256, 16), 256, 0, st>>>(g->n, d_p, d_s, ws.prio, ws.state,
+    k_resolve_init<<<grid_for(ctx, g->n, 256, 16), 256, 0, st>>>(g->n, d_p, d_s, ws.prio, ws.q, ws.state,
                                                                 ws.next);
     ctx->launches++;
     thrust::counting_iterator<int32_t> ids(0);

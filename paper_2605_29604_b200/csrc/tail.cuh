@@ -40,6 +40,7 @@ struct TailArgs {
   const int64_t *off;
   const int32_t *nbr;
   uint32_t *prio;
+  uint16_t *q;
   uint8_t *next;
   uint8_t *state;
   uint8_t *segflag;         // byte flags (seg_mode 2) -- also mode 1 sanity
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
       const int32_t v = __ldcg(&in[q]);
       const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
       const uint64_t kv = key_of(__ldcg(&a.prio[v]), v);
+      const uint32_t qv = __ldcg(&a.q[v]);
       bool blocked = false;
       for (int64_t hi = e; hi > s && !blocked; hi -= kW) {
         int32_t u[kTU];
@@ -143,9 +145,10 @@ __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
         bool b = false;
 #pragma unroll
         for (int j = 0; j < kTU; ++j)
-          if (u[j] >= 0)
-            b |= __ldcg(&a.state[u[j]]) != TCMIS_REMOVED &&
-                 key_of(__ldcg(&a.prio[u[j]]), u[j]) > kv;
+          if (u[j] >= 0) {
+            const uint32_t qu = __ldcg(&a.q[u[j]]);
+            b |= qu != qv ? qu > qv : key_of(__ldcg(&a.prio[u[j]]), u[j]) > kv;
+          }
         blocked = group_any(b, gmask) != 0;
       }
       if (!blocked) {
@@ -177,10 +180,10 @@ __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
         const int32_t v = __ldcg(&in[q]);
         const uint8_t d = __ldcg(&a.next[v]);
         if (d == 2) {
-          mark_removed(v, a.state);
+          mark_removed(v, a.state, a.q);
           ++rem;
         } else if (d == 0) {
-          if (a.fresh) a.prio[v] = fresh_prio(v, fresh_m);
+          if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m);
           out[atomicAdd(tail, 1)] = v;
         }
       }
@@ -205,10 +208,10 @@ __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
         }
         if (gl == 0) {
           if (hit) {
-            mark_removed(v, a.state);
+            mark_removed(v, a.state, a.q);
             ++rem;
           } else {
-            if (a.fresh) a.prio[v] = fresh_prio(v, fresh_m);
+            if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m);
             out[atomicAdd(tail, 1)] = v;
           }
         }

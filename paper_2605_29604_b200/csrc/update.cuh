@@ -44,6 +44,7 @@ struct UpdateArgs {
   const int32_t *nbr;
   int64_t vnnz;            // nnz, negated if nbr is not 16-byte aligned (scan.cuh)
   uint32_t *prio;
+  uint16_t *q;
   uint8_t *state;
   const uint8_t *next;
   Ctrl *ctrl;
@@ -106,12 +107,12 @@ __global__ void __launch_bounds__(kBlock) k_update(UpdateArgs a) {
       const int32_t v = vs[j];
       if (v < 0 || ds[j] == 1) continue;  // candidates were settled by k_select
       if (ds[j] == 2) {
-        mark_removed(v, a.state);
+        mark_removed(v, a.state, a.q);
         publish(a.pub, v);
         ++rem;
       } else {
         ++mine;
-        if (a.fresh) a.prio[v] = fresh_prio(v, fresh_m);
+        if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m);
       }
     }
     int pos, total;
@@ -168,12 +169,12 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
       for (int j = 0; j < kPullK; ++j)
         if (u[j] >= 0) hit |= next[u[j]] == 1;
       if (hit) {
-        mark_removed(v, a.state);
+        mark_removed(v, a.state, a.q);
         publish(a.pub, v);
         ++rem;
       } else if (e - s <= kPullK) {
         survive = true;
-        if (a.fresh) a.prio[v] = fresh_prio(v, fresh_m);
+        if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m);
       } else {
         undecided = true;
       }
@@ -230,13 +231,13 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
         if (u[j] >= 0) hit |= next[u[j]] == 1;
       hi = w;
       if (hit) {
-        mark_removed(v, a.state);
+        mark_removed(v, a.state, a.q);
         publish(a.pub, v);
         ++rem;
         mode = kFetch;
       } else if (hi <= s) {
         survive = true;
-        if (a.fresh) a.prio[v] = fresh_prio(v, fresh_m);
+        if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m);
         mode = kFetch;
       } else if (e - hi >= kThreadMax) {
         defer = true;
@@ -288,11 +289,11 @@ __global__ void __launch_bounds__(kBlock)
     }
     if (lane == 0) {
       if (hit) {
-        mark_removed(v, a.state);
+        mark_removed(v, a.state, a.q);
         publish(a.pub, v);
         ++rem;
       } else {
-        if (a.fresh) a.prio[v] = fresh_prio(v, fresh_m);
+        if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m);
         out[atomicAdd(&ctrl->wl_count[out_slot], 1)] = v;
       }
     }
