@@ -84,6 +84,7 @@ struct Workspace {
   int64_t *mis_count = nullptr;
   Ctrl *ctrl = nullptr;        // device
   Ctrl *h_ctrl = nullptr;      // pinned host mirror
+  int64_t *h_misc = nullptr;   // pinned: [0] MIS count, [1] h3 tiles evaluated
   DevRound *rounds = nullptr;  // device, capacity round_cap
   DevRound *h_rounds = nullptr;
   int32_t round_cap = 0;

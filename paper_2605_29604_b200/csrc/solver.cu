@@ -282,6 +282,7 @@ void free_workspace(Workspace &ws) {
   dev_free(ws.mis_count);
   dev_free(ws.ctrl);
   cudaFreeHost(ws.h_ctrl);
+  cudaFreeHost(ws.h_misc);
   dev_free(ws.rounds);
   cudaFreeHost(ws.h_rounds);
   dev_free(ws.cub_tmp);
@@ -362,6 +363,7 @@ int ensure_workspace(tcmis_graph *g) {
     if (int rc = dev_alloc(&ws.bar, 2)) return rc;
     TCMIS_CUDA(cudaMemsetAsync(ws.bar, 0, 2 * sizeof(unsigned), g->ctx->stream));
     TCMIS_CUDA(cudaMallocHost((void **)&ws.h_ctrl, sizeof(Ctrl)));
+    TCMIS_CUDA(cudaMallocHost((void **)&ws.h_misc, 2 * sizeof(int64_t)));
     ws.round_cap = 4096;
     if (int rc = dev_alloc(&ws.rounds, (size_t)ws.round_cap)) return rc;
     TCMIS_CUDA(cudaMallocHost((void **)&ws.h_rounds, sizeof(DevRound) * ws.round_cap));
@@ -835,14 +837,47 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   std::vector<uint8_t> h_next, h_state, h_cand;
   std::vector<float> t1, t2, t3;  // per-round phase times (TCMIS_F_TIMING)
   bool step = cfg->observer || timing || (cfg->flags & TCMIS_F_HOST_LOOP);
+  int64_t h_mis_count = 0;
+  unsigned long long h3_eval = 0;
+  // ascending MIS ids (engine.cpp:293 sorts; ordered compaction needs no sort)
+  // and h3's collapsed tile counter, enqueued behind the rounds
+  auto enqueue_finish = [&]() -> int {
+    thrust::counting_iterator<int32_t> ids(0);
+    size_t bytes = ws.cub_bytes;
+    TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
+                                     (int)g->n, IsInMIS{ws.state}, st));
+    ctx->launches += 1;
+    TCMIS_CUDA(cudaMemcpyAsync(&ws.h_misc[0], ws.mis_count, sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, st));
+    if (seg_mode == 2) {
+      TCMIS_CUDA(cudaMemsetAsync(&ws.ctrl->eval, 0, sizeof(unsigned long long), st));
+      k_seg_total<<<grid_for(ctx, nseg, 256, 4), 256, 0, st>>>(ws.segflag, g->d_rowtiles, nseg,
+                                                               ws.ctrl);
+      TCMIS_LAUNCHED(ctx);
+      TCMIS_CUDA(cudaMemcpyAsync(&ws.h_misc[1], &ws.ctrl->eval, sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, st));
+    }
+    return 0;
+  };
+  auto read_finish = [&]() {  // after the stream synchronisation
+    h_mis_count = ws.h_misc[0];
+    h3_eval = seg_mode == 2 ? (unsigned long long)ws.h_misc[1] : 0ull;
+  };
+  bool finished = false;
   if (!step) {
     // the whole round loop is one CUDA graph: a conditional WHILE node whose
-    // body is {k_select, k_update}; k_update's last block writes the loop
-    // condition (alive > 0), so no host round trip happens between rounds.
+    // body is {select, exclusion, update}; k_round_end's last block writes the
+    // loop condition, so no host round trip happens between rounds.  The
+    // statistics, the MIS compaction and every read-back are enqueued behind
+    // it and waited for once.
     if (int rc = ensure_round_graph(g, a)) return rc;
     TCMIS_CUDA(cudaGraphLaunch(ws.exec, st));
     ctx->launches += launches_per_round(a);  // per round, counted below
     TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    const int pre = std::min(ws.round_cap, 64);
+    TCMIS_CUDA(cudaMemcpyAsync(ws.h_rounds, ws.rounds, sizeof(DevRound) * pre,
+                               cudaMemcpyDeviceToHost, st));
+    if (int rc = enqueue_finish()) return rc;
     TCMIS_CUDA(cudaStreamSynchronize(st));
     if (ws.h_ctrl->overflow) {
       // more rounds than the on-device ring holds: redo step-wise, draining
@@ -859,9 +894,12 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       const int rr = ws.h_ctrl->round - 1;
       const int mr = ws.h_ctrl->main_rounds;
       ctx->launches += launches_per_round(a) * ((int64_t)mr - 1) + (rr > mr ? 1 : 0);
-      rounds_h.resize(rr);
-      TCMIS_CUDA(cudaMemcpyAsync(rounds_h.data(), ws.rounds, sizeof(DevRound) * rr,
-                                 cudaMemcpyDeviceToHost, st));
+      if (rr > pre)
+        TCMIS_CUDA(cudaMemcpy(ws.h_rounds + pre, ws.rounds + pre, sizeof(DevRound) * (rr - pre),
+                              cudaMemcpyDeviceToHost));
+      rounds_h.assign(ws.h_rounds, ws.h_rounds + rr);
+      read_finish();
+      finished = true;
     }
   }
   if (step) {
@@ -914,27 +952,10 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     }
   }
   const int rounds_run = (int)rounds_h.size();
-  // ascending MIS ids (engine.cpp:293 sorts; ordered compaction needs no sort)
-  {
-    thrust::counting_iterator<int32_t> ids(0);
-    size_t bytes = ws.cub_bytes;
-    TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
-                                     (int)g->n, IsInMIS{ws.state}, st));
-    ctx->launches += 1;
-  }
-  int64_t h_mis_count = 0;
-  TCMIS_CUDA(cudaMemcpyAsync(&h_mis_count, ws.mis_count, sizeof(int64_t),
-                             cudaMemcpyDeviceToHost, st));
-  unsigned long long h3_eval = 0;
-  if (seg_mode == 2) {
-    TCMIS_CUDA(cudaMemsetAsync(&ws.ctrl->eval, 0, sizeof(unsigned long long), st));
-    k_seg_total<<<grid_for(ctx, nseg, 256, 4), 256, 0, st>>>(ws.segflag, g->d_rowtiles, nseg,
-                                                             ws.ctrl);
-    TCMIS_LAUNCHED(ctx);
-    TCMIS_CUDA(cudaMemcpyAsync(&h3_eval, &ws.ctrl->eval, sizeof(h3_eval),
-                               cudaMemcpyDeviceToHost, st));
-  }
+  if (!finished)
+    if (int rc = enqueue_finish()) return rc;
   TCMIS_CUDA(cudaStreamSynchronize(st));
+  if (!finished) read_finish();
   *mis_count_out = h_mis_count;
   if (timing) {
     // Phase 1 = the select kernels, Phase 2 = the pull-form exclusion

@@ -154,19 +154,31 @@ __global__ void __launch_bounds__(256)
 //  k_count_light  one warp per block row with <= kHashMax entries (88 % of
 //                 R-MAT s22's block rows): a 1024-slot open-addressing set
 //                 in shared memory (atomicCAS), cleared after each row.
-//  k_count_heavy  the rest, one CTA per (block row, window of kBmBits block
-//                 columns) from a dynamic work counter: a 32 KB shared
-//                 bitmap, atomicOr's old value tells a first occurrence.
+//  k_count_mid    <= kMidMax entries: one 128-thread CTA per row (dynamic
+//                 work counter), a 4096-slot shared set.
+//  k_count_big    the rest: one 512-thread CTA per row, 128 KB of dynamic
+//                 shared memory used as a set sized to the row (<= kBigHashMax
+//                 entries) or, for the hub rows beyond, as a 2^20-bit bitmap
+//                 swept window by window with per-row cursors (the rows are
+//                 sorted, so a window's entries are a prefix of what is left).
+//  The first version had only the light set and a bitmap CTA per (block row,
+//  2^18-column window) that located each window by binary search in all T
+//  rows: 202 ms at R-MAT s26 (half the block rows exceed 512 entries there).
 constexpr int kLightBlock = 256;
 constexpr int kHashSlots = 1024;
 constexpr int64_t kHashMax = 512;
-constexpr int kHeavyBlock = 512;
-constexpr int64_t kBmBits = 1 << 18;
+constexpr int kMidBlock = 128;
+constexpr int kMidSlots = 4096;
+constexpr int64_t kMidMax = 2048;
+constexpr int kBigBlock = 512;
+constexpr int kBigWords = 32768;          // 128 KB of dynamic shared memory
+constexpr int64_t kBigHashMax = 16384;    // set of <= 32768 slots
+constexpr int64_t kBigBits = 32ll * kBigWords;
 
 __global__ void __launch_bounds__(kLightBlock)
     k_count_light(int32_t n, int T, int32_t nb, const int64_t *__restrict__ off,
                   const int32_t *__restrict__ nbr, int32_t *__restrict__ rowtiles,
-                  int32_t *__restrict__ heavy, int32_t *__restrict__ heavy_count) {
+                  int32_t *__restrict__ lists, int32_t *__restrict__ counts) {
   __shared__ __align__(16) uint32_t tab[kLightBlock / 32][kHashSlots];
   const int lane = threadIdx.x & 31;
   uint32_t *t = tab[threadIdx.x >> 5];
@@ -178,8 +190,11 @@ __global__ void __launch_bounds__(kLightBlock)
        b += ((int64_t)gridDim.x * kLightBlock) >> 5) {
     const int64_t r0 = b * T, r1 = min((int64_t)n, r0 + T);
     const int64_t s = off[r0], e = off[r1];
-    if (e - s > kHashMax) {
-      if (lane == 0) heavy[atomicAdd(heavy_count, 1)] = (int32_t)b;
+    if (e - s > kHashMax) {  // mid rows from the front of `lists`, big rows from the back
+      if (lane == 0) {
+        if (e - s <= kMidMax) lists[atomicAdd(&counts[0], 1)] = (int32_t)b;
+        else lists[nb - 1 - atomicAdd(&counts[1], 1)] = (int32_t)b;
+      }
       continue;
     }
     int cnt = 0;
@@ -215,73 +230,134 @@ __global__ void __launch_bounds__(kLightBlock)
   }
 }
 
-__global__ void __launch_bounds__(kHeavyBlock)
-    k_count_heavy(int32_t n, int T, int32_t nb, const int64_t *__restrict__ off,
-                  const int32_t *__restrict__ nbr, int32_t *__restrict__ rowtiles,
-                  const int32_t *__restrict__ heavy, const int32_t *__restrict__ heavy_count,
-                  int32_t windows, unsigned long long *__restrict__ next_item) {
-  __shared__ __align__(16) uint32_t bm[kBmBits / 32];
-  __shared__ int64_t s_lo[64], s_hi[64];
-  __shared__ unsigned long long s_item;
-  __shared__ int s_red[kHeavyBlock / 32];
-  uint4 *bm4 = reinterpret_cast<uint4 *>(bm);
-  for (int i = threadIdx.x; i < kBmBits / 128; i += kHeavyBlock) bm4[i] = make_uint4(0, 0, 0, 0);
-  const unsigned long long items = (unsigned long long)*heavy_count * (unsigned)windows;
+// CTA-wide insert of block columns [s, e) into a shared set of `slots`
+// (power of two) slots; returns the CTA's count of first insertions (valid in
+// every thread) and leaves the set cleared.
+__device__ __forceinline__ int cta_hash_count(uint32_t *tab, int slots, const int32_t *__restrict__ nbr,
+                                              int64_t s, int64_t e, uint32_t uT, int *s_red) {
+  const int shift = 32 - (__ffs(slots) - 1);
+  int cnt = 0;
+  for (int64_t p = s + threadIdx.x; p < e; p += blockDim.x) {
+    const uint32_t c = (uint32_t)__ldg(&nbr[p]) / uT + 1u;
+    uint32_t h = (c * 0x9E3779B1u) >> shift;
+    for (;;) {
+      const uint32_t old = atomicCAS(&tab[h], 0u, c);
+      if (old == 0u) {
+        ++cnt;
+        break;
+      }
+      if (old == c) break;
+      h = (h + 1) & (slots - 1);
+    }
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  int total = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) total += s_red[w];
+  uint4 *t4 = reinterpret_cast<uint4 *>(tab);
+  for (int i = threadIdx.x; i < slots / 4; i += blockDim.x) t4[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  return total;
+}
+
+__global__ void __launch_bounds__(kMidBlock)
+    k_count_mid(int32_t n, int T, const int64_t *__restrict__ off, const int32_t *__restrict__ nbr,
+                int32_t *__restrict__ rowtiles, const int32_t *__restrict__ list,
+                const int32_t *__restrict__ count, unsigned *__restrict__ next_item) {
+  __shared__ __align__(16) uint32_t tab[kMidSlots];
+  __shared__ int s_red[kMidBlock / 32];
+  __shared__ unsigned s_item;
+  uint4 *t4 = reinterpret_cast<uint4 *>(tab);
+  for (int i = threadIdx.x; i < kMidSlots / 4; i += kMidBlock) t4[i] = make_uint4(0, 0, 0, 0);
+  const unsigned items = (unsigned)*count;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_item = atomicAdd(next_item, 1u);
+    __syncthreads();
+    const unsigned it = s_item;
+    if (it >= items) break;
+    const int32_t b = list[it];
+    const int64_t r0 = (int64_t)b * T, r1 = min((int64_t)n, r0 + T);
+    const int64_t s = off[r0], e = off[r1];
+    int slots = 1024;
+    while (slots < 2 * (e - s) && slots < kMidSlots) slots <<= 1;
+    const int total = cta_hash_count(tab, slots, nbr, s, e, (uint32_t)T, s_red);
+    if (threadIdx.x == 0) rowtiles[b] = total;
+  }
+}
+
+__global__ void __launch_bounds__(kBigBlock)
+    k_count_big(int32_t n, int T, int32_t nb, const int64_t *__restrict__ off,
+                const int32_t *__restrict__ nbr, int32_t *__restrict__ rowtiles,
+                const int32_t *__restrict__ list_end, const int32_t *__restrict__ count,
+                unsigned *__restrict__ next_item) {
+  extern __shared__ __align__(16) uint32_t big[];  // kBigWords
+  __shared__ int s_red[kBigBlock / 32];
+  __shared__ int64_t s_cur[64], s_end[64];
+  __shared__ unsigned s_item;
+  __shared__ int s_adv;
+  uint4 *b4 = reinterpret_cast<uint4 *>(big);
+  for (int i = threadIdx.x; i < kBigWords / 4; i += kBigBlock) b4[i] = make_uint4(0, 0, 0, 0);
+  const unsigned items = (unsigned)*count;
   const uint32_t uT = (uint32_t)T;
   for (;;) {
     __syncthreads();
-    if (threadIdx.x == 0) s_item = atomicAdd(next_item, 1ull);
+    if (threadIdx.x == 0) s_item = atomicAdd(next_item, 1u);
     __syncthreads();
-    const unsigned long long it = s_item;
+    const unsigned it = s_item;
     if (it >= items) break;
-    const int32_t b = heavy[it / windows];
-    const int64_t c0 = (int64_t)(it % windows) * kBmBits;
-    const int64_t c1 = min((int64_t)nb, c0 + kBmBits);
+    const int32_t b = list_end[-(int64_t)it];
     const int64_t r0 = (int64_t)b * T;
     const int rows = (int)min((int64_t)T, (int64_t)n - r0);
-    int nseg;
-    if (windows == 1) {  // the whole block row is one contiguous range
-      if (threadIdx.x == 0) {
-        s_lo[0] = off[r0];
-        s_hi[0] = off[r0 + rows];
-      }
-      nseg = 1;
-    } else {
-      if (threadIdx.x < rows) {
-        const int64_t rs = off[r0 + threadIdx.x], re = off[r0 + threadIdx.x + 1];
-        s_lo[threadIdx.x] = lower_bound_i32(nbr, rs, re, c0 * T);
-        s_hi[threadIdx.x] = lower_bound_i32(nbr, rs, re, c1 * T);
-      }
-      nseg = rows;
+    const int64_t s = off[r0], e = off[r0 + rows];
+    if (e - s <= kBigHashMax) {
+      int slots = 1024;
+      while (slots < 2 * (e - s) && slots < kBigWords) slots <<= 1;
+      const int total = cta_hash_count(big, slots, nbr, s, e, uT, s_red);
+      if (threadIdx.x == 0) rowtiles[b] = total;
+      continue;
+    }
+    // hub rows: windows of kBigBits block columns; row k's entries of window
+    // w are the next ones after its cursor (sorted rows)
+    if (threadIdx.x < rows) {
+      s_cur[threadIdx.x] = off[r0 + threadIdx.x];
+      s_end[threadIdx.x] = off[r0 + threadIdx.x + 1];
     }
     __syncthreads();
     int cnt = 0;
-    for (int k = 0; k < nseg; ++k) {
-      const int64_t lo = s_lo[k], hi = s_hi[k];
-      for (int64_t base = lo; base < hi; base += 4 * kHeavyBlock) {
-        uint32_t c[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int64_t p = base + threadIdx.x + (int64_t)kHeavyBlock * j;
-          c[j] = p < hi ? (uint32_t)((uint32_t)__ldg(&nbr[p]) / uT - (uint32_t)c0) : 0xffffffffu;
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (c[j] == 0xffffffffu) continue;
-          const uint32_t bit = 1u << (c[j] & 31);
-          cnt += (atomicOr(&bm[c[j] >> 5], bit) & bit) ? 0 : 1;
+    const int64_t windows = ((int64_t)nb + kBigBits - 1) / kBigBits;
+    for (int64_t w = 0; w < windows; ++w) {
+      const uint32_t wlo = (uint32_t)(w * kBigBits);
+      for (int k = 0; k < rows; ++k) {
+        for (;;) {
+          const int64_t p = s_cur[k] + threadIdx.x;
+          bool in = false;
+          if (p < s_end[k]) {
+            const uint32_t c = (uint32_t)__ldg(&nbr[p]) / uT;
+            if ((int64_t)c < (int64_t)wlo + kBigBits) {
+              in = true;
+              const uint32_t bit = 1u << ((c - wlo) & 31u);
+              cnt += (atomicOr(&big[(c - wlo) >> 5], bit) & bit) ? 0 : 1;
+            }
+          }
+          const int adv = __syncthreads_count(in);
+          if (threadIdx.x == 0) s_cur[k] += adv;
+          __syncthreads();
+          if (adv < kBigBlock) break;
         }
       }
+      for (int i = threadIdx.x; i < kBigWords / 4; i += kBigBlock) b4[i] = make_uint4(0, 0, 0, 0);
+      __syncthreads();
     }
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = cnt;
     __syncthreads();
-    if (threadIdx.x < 32) {
-      int v = threadIdx.x < kHeavyBlock / 32 ? s_red[threadIdx.x] : 0;
-      v = __reduce_add_sync(0xffffffffu, v);
-      if (threadIdx.x == 0 && v) atomicAdd(&rowtiles[b], v);
+    if (threadIdx.x == 0) {
+      int total = 0;
+      for (int i = 0; i < kBigBlock / 32; ++i) total += s_red[i];
+      rowtiles[b] = total;
     }
-    for (int i = threadIdx.x; i < kBmBits / 128; i += kHeavyBlock) bm4[i] = make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -352,24 +428,30 @@ int build_tile_counts(tcmis_graph *g, int T) {
   if (int rc = dev_alloc(&g->d_rowtiles, (size_t)nb + 1)) return rc;
   TCMIS_CUDA(cudaMemsetAsync(g->d_rowtiles, 0, sizeof(int32_t) * ((size_t)nb + 1), st));
   if (nb > 0) {
-    int32_t *heavy = nullptr, *cnt = nullptr;
-    if (int rc = dev_alloc(&heavy, (size_t)nb)) return rc;
-    unsigned long long *next_item = nullptr;
-    if (int rc = dev_alloc(&cnt, 1)) return rc;
-    if (int rc = dev_alloc(&next_item, 1)) return rc;
-    TCMIS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t), st));
-    TCMIS_CUDA(cudaMemsetAsync(next_item, 0, sizeof(unsigned long long), st));
+    // lists: mid rows from the front, big rows from the back; counts[0..1]
+    // list sizes, counts[2..3] the dynamic work counters
+    int32_t *lists = nullptr, *cnt = nullptr;
+    if (int rc = dev_alloc(&lists, (size_t)nb)) return rc;
+    if (int rc = dev_alloc(&cnt, 4)) return rc;
+    TCMIS_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(int32_t), st));
     k_count_light<<<grid_for(ctx, 32ll * nb, kLightBlock, 8), kLightBlock, 0, st>>>(
-        g->n, T, nb, g->d_off, g->d_nbr, g->d_rowtiles, heavy, cnt);
+        g->n, T, nb, g->d_off, g->d_nbr, g->d_rowtiles, lists, cnt);
     TCMIS_LAUNCHED(ctx);
-    const int32_t windows = (int32_t)(((int64_t)nb + kBmBits - 1) / kBmBits);
-    k_count_heavy<<<ctx->num_sms * 4, kHeavyBlock, 0, st>>>(
-        g->n, T, nb, g->d_off, g->d_nbr, g->d_rowtiles, heavy, cnt, windows,
-        next_item);
+    int mid_per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mid_per_sm, k_count_mid, kMidBlock, 0);
+    k_count_mid<<<ctx->num_sms * std::max(1, mid_per_sm), kMidBlock, 0, st>>>(
+        g->n, T, g->d_off, g->d_nbr, g->d_rowtiles, lists, cnt,
+        reinterpret_cast<unsigned *>(cnt + 2));
     TCMIS_LAUNCHED(ctx);
-    dev_free(heavy);
+    const size_t big_smem = sizeof(uint32_t) * kBigWords;
+    TCMIS_CUDA(cudaFuncSetAttribute(k_count_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)big_smem));
+    k_count_big<<<ctx->num_sms, kBigBlock, big_smem, st>>>(
+        g->n, T, nb, g->d_off, g->d_nbr, g->d_rowtiles, lists + nb - 1, cnt + 1,
+        reinterpret_cast<unsigned *>(cnt + 3));
+    TCMIS_LAUNCHED(ctx);
+    dev_free(lists);
     dev_free(cnt);
-    dev_free(next_item);
     unsigned long long *d_total = nullptr;
     if (int rc = dev_alloc(&d_total, 1)) return rc;
     cudaMemsetAsync(d_total, 0, 8, st);

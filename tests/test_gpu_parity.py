@@ -71,6 +71,28 @@ def test_tile_graph_export_matches_oracle(ctx, T):
     assert np.array_equal(a.row_bits, rb) and np.array_equal(a.block_row_offsets, bro)
 
 
+@pytest.mark.parametrize("T", [1, 2, 16])
+def test_tile_counts_all_row_classes(ctx, T):
+    """tile_graph's per-block-row tile counts (tiling.cpp:44-84) through every
+    K1 count path: light (<= 512 entries), mid (<= 2048), big (shared set,
+    <= 16384) and hub rows swept in several 2^20-column windows (a 1.5M-leaf
+    star at T = 1 and 2 has > 2^20 block columns)."""
+    rng = np.random.default_rng(T)
+    n = 1_500_000
+    leaves = np.arange(1, n, dtype=np.int32)
+    extra = rng.integers(0, n, size=(400_000, 2), dtype=np.int32)
+    mids = np.stack([np.repeat(np.arange(2, 40, dtype=np.int32), 1500),
+                     rng.integers(0, n, size=38 * 1500, dtype=np.int32)], 1)
+    e = np.concatenate([np.stack([np.zeros(n - 1, np.int32), leaves], 1), extra, mids])
+    g = O.graph_from_edges(n, e)
+    dg = tc.DeviceGraph.upload(as_tc(g), ctx)
+    want = O.tile_row_counts(g, T)
+    assert dg.tile(T) == int(want.sum())
+    exp = O.solve(g, "h2", 1, tile_dim=T)
+    got = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=1, tile_dim=T))
+    assert rounds_tuple(got.iterations) == oracle_tuple(exp)
+
+
 def test_tile_graph_hub_rows_split(ctx):
     # a star: one row with many block columns -> multiple work items
     n = 20000
