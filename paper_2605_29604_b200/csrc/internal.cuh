@@ -59,7 +59,7 @@ struct Ctrl {
   int32_t pull_count;  // entries of the pull long-row list this round
   int32_t check_unused; // (was the select kernels' pull check list)
   int32_t main_rounds; // rounds run by the per-round kernels (the rest ran in k_tail)
-  int32_t tail_check[2]; // k_tail pull check-list length, by round parity
+  int32_t tail_cnt[3];   // k_tail list lengths, by round mod 3 (tail.cuh)
   int32_t sel_undec;   // rows k_probe_select left to the k_select engine
   int32_t pull_undec;  // rows k_probe_pull left to the k_update_pull engine
 };
@@ -71,6 +71,7 @@ struct Workspace {
   uint16_t *q = nullptr;          // q_of(prio) (common.cuh), 0 once removed
   uint8_t *state = nullptr;
   uint8_t *next = nullptr;
+  uint8_t *xm = nullptr;          // k_tail exclusion planes: [0, n_cap) even, [n_cap, 2 n_cap) odd rounds
   int32_t *wl[2] = {nullptr, nullptr};
   uint8_t *segflag = nullptr;
   int32_t *mis = nullptr;
@@ -81,6 +82,7 @@ struct Workspace {
   int32_t *undec_pull = nullptr;  // probe leftovers for the pull engine
   uint32_t *segmark = nullptr;    // tail rounds: round that last counted a block column
   unsigned *bar = nullptr;        // grid barrier of k_tail
+  unsigned *blockcnt = nullptr;   // k_tail's fused MIS compaction: per-block counts
   int64_t *mis_count = nullptr;
   Ctrl *ctrl = nullptr;        // device
   Ctrl *h_ctrl = nullptr;      // pinned host mirror
@@ -234,7 +236,10 @@ int launch_select(tcmis_graph *g, const RoundArgs &a);
 int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle cond, int use_cond);
 int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
                       uint32_t *p_out, uint16_t *q_out, uint8_t *state, uint8_t *next,
-                      uint8_t *segflag = nullptr, int T = 1);
+                      uint8_t *segflag = nullptr, int T = 1, uint8_t *xm0 = nullptr,
+                      uint8_t *xm1 = nullptr);
+// offset of k_tail's odd exclusion plane in Workspace::xm (16-byte aligned)
+inline size_t xm_stride(const Workspace &ws) { return (ws.n_cap + 15) / 16 * 16; }
 double avg_degree(const tcmis_graph *g);
 
 // workspace management (solver.cu)

@@ -57,7 +57,8 @@ constexpr int kPrioV = 4;
 __global__ void __launch_bounds__(256)
     k_priorities(int32_t n, const int64_t *__restrict__ off, int aligned, int mode,
                  uint64_t mseed, double avg, double scale, uint32_t *__restrict__ p_out,
-                 uint16_t *__restrict__ q_out, int qshift, uint8_t *__restrict__ state, uint8_t *__restrict__ next,
+                 uint16_t *__restrict__ q_out, int qshift, uint8_t *__restrict__ state,
+                 uint8_t *__restrict__ next, uint8_t *__restrict__ xm0, uint8_t *__restrict__ xm1,
                  uint8_t *__restrict__ segflag, int T, int tshift) {
   const int32_t quads = (int32_t)(((int64_t)n + kPrioV - 1) / kPrioV);
   for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < quads;
@@ -106,12 +107,17 @@ __global__ void __launch_bounds__(256)
                        (uint32_t)q_of(pv[2], qshift) | ((uint32_t)q_of(pv[3], qshift) << 16));
       if (state) *reinterpret_cast<uint32_t *>(state + v0) = st4;
       if (next) *reinterpret_cast<uint32_t *>(next + v0) = nx4;
+      if (xm0) {  // k_tail's exclusion planes start clear
+        *reinterpret_cast<uint32_t *>(xm0 + v0) = 0u;
+        *reinterpret_cast<uint32_t *>(xm1 + v0) = 0u;
+      }
     } else {
       for (int j = 0; j < kPrioV && v0 + j < n; ++j) {
         if (p_out) p_out[v0 + j] = pv[j];
         if (q_out) q_out[v0 + j] = q_of(pv[j], qshift);
         if (state) state[v0 + j] = (uint8_t)(st4 >> (8 * j));
         if (next) next[v0 + j] = (uint8_t)(nx4 >> (8 * j));
+        if (xm0) xm0[v0 + j] = xm1[v0 + j] = 0;
       }
     }
   }
@@ -268,6 +274,7 @@ void free_workspace(Workspace &ws) {
   dev_free(ws.q);
   dev_free(ws.state);
   dev_free(ws.next);
+  dev_free(ws.xm);
   dev_free(ws.wl[0]);
   dev_free(ws.wl[1]);
   dev_free(ws.segflag);
@@ -279,6 +286,7 @@ void free_workspace(Workspace &ws) {
   dev_free(ws.undec_pull);
   dev_free(ws.segmark);
   dev_free(ws.bar);
+  dev_free(ws.blockcnt);
   dev_free(ws.mis_count);
   dev_free(ws.ctrl);
   cudaFreeHost(ws.h_ctrl);
@@ -320,6 +328,7 @@ int ensure_workspace(tcmis_graph *g) {
   dev_free(ws.q);
     dev_free(ws.state);
     dev_free(ws.next);
+  dev_free(ws.xm);
     dev_free(ws.wl[0]);
     dev_free(ws.wl[1]);
     dev_free(ws.mis);
@@ -334,8 +343,9 @@ int ensure_workspace(tcmis_graph *g) {
     ws.n_cap = 0;
     if (int rc = dev_alloc(&ws.prio, n)) return rc;
     if (int rc = dev_alloc(&ws.q, n + 8)) return rc;
-    if (int rc = dev_alloc(&ws.state, n)) return rc;
+    if (int rc = dev_alloc(&ws.state, n + 16)) return rc;  // uint4 reads past n (k_tail)
     if (int rc = dev_alloc(&ws.next, n)) return rc;
+    if (int rc = dev_alloc(&ws.xm, 2 * ((n + 15) / 16 * 16) + 32)) return rc;
     if (int rc = dev_alloc(&ws.wl[0], n)) return rc;
     if (int rc = dev_alloc(&ws.wl[1], n)) return rc;
     if (int rc = dev_alloc(&ws.mis, n)) return rc;
@@ -361,6 +371,7 @@ int ensure_workspace(tcmis_graph *g) {
     if (int rc = dev_alloc(&ws.ctrl, 1)) return rc;
     if (int rc = dev_alloc(&ws.mis_count, 1)) return rc;
     if (int rc = dev_alloc(&ws.bar, 2)) return rc;
+    if (int rc = dev_alloc(&ws.blockcnt, 4096)) return rc;
     TCMIS_CUDA(cudaMemsetAsync(ws.bar, 0, 2 * sizeof(unsigned), g->ctx->stream));
     TCMIS_CUDA(cudaMallocHost((void **)&ws.h_ctrl, sizeof(Ctrl)));
     TCMIS_CUDA(cudaMallocHost((void **)&ws.h_misc, 2 * sizeof(int64_t)));
@@ -426,7 +437,7 @@ int q_shift(int heuristic, int scale_bits) {
 
 int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
                       uint32_t *p_out, uint16_t *q_out, uint8_t *state, uint8_t *next,
-                      uint8_t *segflag, int T) {
+                      uint8_t *segflag, int T, uint8_t *xm0, uint8_t *xm1) {
   tcmis_ctx *ctx = g->ctx;
   int mode = 1;
   uint64_t mseed = mix64(seed);
@@ -445,7 +456,8 @@ int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bi
               (k_priorities<<<grid, 256, 0, ctx->stream>>>(g->n, off, aligned, mode, mseed,
                                                           mode ? avg_degree(g) : 0.0, scale,
                                                           p_out, q_out, q_shift(heuristic, scale_bits),
-                                                          state, next, segflag, T, tshift)));
+                                                          state, next, xm0, xm1, segflag, T,
+                                                          tshift)));
   TCMIS_LAUNCHED(ctx);
   return 0;
 }
@@ -539,6 +551,8 @@ TailArgs tail_args(tcmis_graph *g, const RoundArgs &a) {
   t.prio = ws.prio;
   t.q = ws.q;
   t.next = ws.next;
+  t.xm0 = ws.xm;
+  t.xm1 = ws.xm + xm_stride(ws);
   t.state = ws.state;
   t.segflag = ws.segflag;
   t.segmark = ws.segmark;
@@ -547,15 +561,16 @@ TailArgs tail_args(tcmis_graph *g, const RoundArgs &a) {
   t.total_tiles = a.total_tiles;
   t.seg_mode = a.seg_mode;
   t.T = a.T;
-  t.push = a.pull ? 0 : 1;
-  t.fresh = a.fresh;
-  t.seed = a.seed;
   t.ctrl = ws.ctrl;
   t.wl0 = ws.wl[0];
   t.wl1 = ws.wl[1];
-  t.check = ws.check;
   t.rounds = ws.rounds;
   t.bar = ws.bar;
+  t.compact = 1;
+  t.n = a.n;
+  t.mis = ws.mis;
+  t.mis_count = ws.mis_count;
+  t.blockcnt = ws.blockcnt;
   return t;
 }
 
@@ -774,7 +789,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
   uint8_t *seg0 = seg_mode ? ws.segflag : nullptr;
   if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio, ws.q, ws.state,
-                                 ws.next, seg0, T > 0 ? T : 1))
+                                 ws.next, seg0, T > 0 ? T : 1, ws.xm, ws.xm + xm_stride(ws)))
     return rc;
   Ctrl c0{};
   c0.round = 1;
@@ -783,6 +798,8 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   c0.sel = (unsigned long long)(g->n - g->nz_count);  // isolated: round-1 candidates
   *ws.h_ctrl = c0;
   TCMIS_CUDA(cudaMemcpyAsync(ws.ctrl, ws.h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+  // k_tail accumulates its rounds' counters into the ring (tail.cuh)
+  TCMIS_CUDA(cudaMemsetAsync(ws.rounds, 0, sizeof(DevRound) * ws.round_cap, st));
 
   RoundArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -825,7 +842,9 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   // small late rounds run in the persistent k_tail (not with the per-round
   // observer hook, which needs every round's snapshot)
   a.tail_thr = 0;
-  if (!cfg->observer) {
+  // (luby-fresh redraws every survivor's priority between rounds, which the
+  // tail's one-barrier rounds cannot order: it keeps the per-round kernels)
+  if (!cfg->observer && !fresh) {
     a.tail_thr = 1 << 16;
     if (const char *env = std::getenv("TCMIS_TAIL_THRESHOLD")) a.tail_thr = std::atoi(env);
     a.tail_grid = tail_grid(ctx);
@@ -841,12 +860,15 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   unsigned long long h3_eval = 0;
   // ascending MIS ids (engine.cpp:293 sorts; ordered compaction needs no sort)
   // and h3's collapsed tile counter, enqueued behind the rounds
+  bool tail_compacted = false;  // k_tail ends with the MIS compaction (tail.cuh)
   auto enqueue_finish = [&]() -> int {
-    thrust::counting_iterator<int32_t> ids(0);
-    size_t bytes = ws.cub_bytes;
-    TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
-                                     (int)g->n, IsInMIS{ws.state}, st));
-    ctx->launches += 1;
+    if (!tail_compacted) {
+      thrust::counting_iterator<int32_t> ids(0);
+      size_t bytes = ws.cub_bytes;
+      TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
+                                       (int)g->n, IsInMIS{ws.state}, st));
+      ctx->launches += 1;
+    }
     TCMIS_CUDA(cudaMemcpyAsync(&ws.h_misc[0], ws.mis_count, sizeof(int64_t),
                                cudaMemcpyDeviceToHost, st));
     if (seg_mode == 2) {
@@ -872,6 +894,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     // it and waited for once.
     if (int rc = ensure_round_graph(g, a)) return rc;
     TCMIS_CUDA(cudaGraphLaunch(ws.exec, st));
+    tail_compacted = a.tail_thr > 0;
     ctx->launches += launches_per_round(a);  // per round, counted below
     TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
     const int pre = std::min(ws.round_cap, 64);
@@ -884,12 +907,16 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       // the statistics every round (pathological inputs such as long paths)
       step = true;
       a.tail_thr = 0;
+      tail_compacted = false;
       if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
       if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio, ws.q,
-                                     ws.state, ws.next, seg0, T > 0 ? T : 1))
+                                     ws.state, ws.next, seg0, T > 0 ? T : 1, ws.xm,
+                                     ws.xm + xm_stride(ws)))
         return rc;
       *ws.h_ctrl = c0;
       TCMIS_CUDA(cudaMemcpyAsync(ws.ctrl, ws.h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+      // k_tail accumulates its rounds' counters into the ring (tail.cuh)
+      TCMIS_CUDA(cudaMemsetAsync(ws.rounds, 0, sizeof(DevRound) * ws.round_cap, st));
     } else {
       const int rr = ws.h_ctrl->round - 1;
       const int mr = ws.h_ctrl->main_rounds;
@@ -936,6 +963,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       if (a.tail_thr > 0 && ws.h_ctrl->alive <= a.tail_thr) {
         ctx->rec_round = round + 1;
         if (int rc = launch_tail(g, a)) return rc;
+        tail_compacted = true;
         TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
         TCMIS_CUDA(cudaStreamSynchronize(st));
         const int rr = ws.h_ctrl->round - 1;
@@ -1124,6 +1152,23 @@ int neighbor_count_impl(tcmis_graph *g, const uint8_t *c, int32_t *nc, int T, in
 }
 
 }  // namespace tcmis_b200
+
+#ifdef TCMIS_TAIL_PROF
+extern "C" __attribute__((visibility("default"))) int tcmis_debug_tail_prof(
+    unsigned long long *out, int cap) {
+  int n = 0;
+  cudaMemcpyFromSymbol(&n, tcmis_b200::g_tail_prof_n, sizeof(int));
+  n = n < cap / 2 ? n : cap / 2;
+  cudaMemcpyFromSymbol(out, tcmis_b200::g_tail_prof, sizeof(unsigned long long) * 2 * n);
+  int z = 0;
+  cudaMemcpyToSymbol(tcmis_b200::g_tail_prof_n, &z, sizeof(int));
+  return n;
+}
+extern "C" __attribute__((visibility("default"))) int tcmis_debug_tail_blk(
+    unsigned long long *out) {
+  return (int)cudaMemcpyFromSymbol(out, tcmis_b200::g_tail_blk, sizeof(unsigned long long) * 3 * 1024);
+}
+#endif
 
 namespace tcmis_b200 {
 

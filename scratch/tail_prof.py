@@ -1,0 +1,28 @@
+# k_tail phase timeline (build with -DTCMIS_TAIL_PROF); box only
+import ctypes as C, sys; sys.path.insert(0, '.')
+import paper_2605_29604_b200 as tc
+import bench
+L = tc.load()
+ctx = tc.Context(0)
+TAG = {1: "start", 2: "pass", 3: "barrier", 4: "compact0", 5: "count", 6: "countbar", 7: "compact1"}
+buf = (C.c_ulonglong * 256)()
+for cfg in sys.argv[1:]:
+    dg = bench.make_device_graph(tc, cfg, ctx)
+    dg.tile(16)
+    for i in range(3):
+        L.tcmis_debug_tail_prof(buf, 256)
+        tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2))
+        ctx.synchronize()
+        n = L.tcmis_debug_tail_prof(buf, 256)
+        t0 = buf[0]
+        print(cfg, i, " ".join(f"{TAG[buf[2*k+1] >> 32]}({buf[2*k+1] & 0xffffffff})@{(buf[2*k]-t0)/1000:.1f}" for k in range(n)), flush=True)
+    dg.close()
+# per-block view of the first tail round (last solve of the last config)
+import numpy as np
+blk = (C.c_ulonglong * (3 * 1024))()
+L.tcmis_debug_tail_blk(blk)
+a = np.frombuffer(blk, dtype=np.uint64).reshape(3, 1024)[:, :148].astype(np.int64)
+t0 = a[0].min()
+print("short-pass end us: min %.1f med %.1f max %.1f" % ((a[0].min()-t0)/1e3, (np.median(a[0])-t0)/1e3, (a[0].max()-t0)/1e3))
+print("long-pass end us: min %.1f med %.1f max %.1f" % ((a[1].min()-t0)/1e3, (np.median(a[1])-t0)/1e3, (a[1].max()-t0)/1e3))
+print("nlong per block: min %d med %d max %d sum %d" % (a[2].min(), np.median(a[2]), a[2].max(), a[2].sum()))
