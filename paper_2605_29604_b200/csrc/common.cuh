@@ -8,6 +8,10 @@ namespace tcmis_b200 {
 constexpr int kBlock = 256;    // threads per block of the round kernels
 constexpr int kStep = 4;       // row entries per thread-level step
 constexpr int kThreadMax = 32; // entries a thread examines before handing a row to a warp
+#ifndef TCMIS_WARP_U
+#define TCMIS_WARP_U 8
+#endif
+constexpr int kWarpU = TCMIS_WARP_U;  // independent loads per lane per step of a warp-wide row scan
 
 // Loads of the CSR (offsets, neighbour ids): read once per phase, so they are
 // marked evict-first (ld.global.cs) and do not push the randomly gathered
@@ -115,12 +119,33 @@ __device__ __forceinline__ uint64_t key_of(uint32_t p, int32_t v) {
 // above v's.  Candidates of the running round turn InMIS while the select
 // kernels run but keep their q (only removals, written by the update kernels
 // after the select kernels, zero it).
+// The gathers of q[u] carry an L2 evict_last policy (createpolicy, folded
+// into the load's memory descriptor) so the CSR streaming past them (marked
+// evict-first, ld_stream) does not push the gathered vector out of L2.
+#ifndef TCMIS_GATHER_HINT
+#define TCMIS_GATHER_HINT 1
+#endif
+__device__ __forceinline__ uint32_t ld_gather_q(const uint16_t *p) {
+#if TCMIS_GATHER_HINT
+  uint16_t r;
+  asm("{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n"
+      " ld.global.nc.L2::cache_hint.u16 %0, [%1], pol;\n}"
+      : "=h"(r)
+      : "l"(p));
+  return r;
+#else
+  return __ldg(p);
+#endif
+}
+
+// v's own p is needed only when q ties, so it is loaded then (saves a 4-byte
+// stream of p per visited vertex)
 __device__ __forceinline__ bool blocks(const uint16_t *__restrict__ q,
                                        const uint32_t *__restrict__ prio, int32_t u,
-                                       uint32_t qv, uint64_t kv) {
-  const uint32_t qu = __ldg(&q[u]);
+                                       uint32_t qv, int32_t v) {
+  const uint32_t qu = ld_gather_q(&q[u]);
   if (qu != qv) return qu > qv;  // qu == 0 (removed) never blocks: qv >= 1
-  return key_of(__ldg(&prio[u]), u) > kv;
+  return key_of(__ldg(&prio[u]), u) > key_of(__ldg(&prio[v]), v);
 }
 
 __device__ __forceinline__ uint32_t fresh_prio(int32_t v, uint64_t fresh_m) {

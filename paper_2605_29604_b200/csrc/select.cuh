@@ -93,14 +93,13 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
     if (i < cnt) {
       v = (round == 1 && a.nz_identity) ? (int32_t)i : __ldg(&wl[i]);
       const int64_t s = ld_stream(&a.off[v]), e = ld_stream(&a.off[v + 1]);
-      const uint64_t kv = key_of(__ldg(&prio[v]), v);
       const uint32_t qv = __ldg(&q[v]);
       int32_t u[8];
       load_tail8(nbr, a.vnnz, s, e, u);
       bool blocked = false;
 #pragma unroll
       for (int j = 0; j < kProbeK; ++j)
-        if (u[j] >= 0) blocked |= blocks(q, prio, u[j], qv, kv);
+        if (u[j] >= 0) blocked |= blocks(q, prio, u[j], qv, v);
       if (blocked) {
         // a non-candidate: the pull exclusion finds it on the worklist
       } else if (e - s <= kProbeK) {
@@ -138,7 +137,6 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
   int mode = kFetch;
   int32_t v = 0;
   int64_t s = 0, e = 0, hi = 0;
-  uint64_t kv = 0;
   uint32_t qv = 0;
   auto fetch = [&]() {
     i += stride;
@@ -146,7 +144,6 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
       v = __ldg(&a.undecided[i]);
       s = __ldg(&a.off[v]);
       e = __ldg(&a.off[v + 1]);
-      kv = key_of(__ldg(&prio[v]), v);
       qv = __ldg(&q[v]);
       hi = e - kProbeK;  // the probe examined the last kProbeK entries
       mode = kScan;
@@ -163,7 +160,7 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
       bool blocked = false;
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (u[j] >= 0) blocked |= blocks(q, prio, u[j], qv, kv);
+        if (u[j] >= 0) blocked |= blocks(q, prio, u[j], qv, v);
       hi = w;
       if (blocked) {
         mode = kFetch;
@@ -204,25 +201,24 @@ __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
        q += ((int64_t)gridDim.x * kBlock) >> 5) {
     const int32_t v = a.long_list[q];
     const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
-    const uint64_t kv = key_of(__ldg(&prio[v]), v);
     const uint32_t qv = __ldg(&a.q[v]);
     // the thread stage examined at least the last kThreadMax - 3 entries (its
     // first window may be short); rescanning an entry is harmless
     int64_t hi = e - (kThreadMax - 3);
     bool blocked = false;
     while (!blocked && hi > s) {
-      int32_t u[4];
+      int32_t u[kWarpU];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < kWarpU; ++j) {
         const int64_t idx = hi - 1 - lane - 32 * j;
-        u[j] = idx >= s ? __ldg(&nbr[idx]) : -1;
+        u[j] = idx >= s ? ld_stream(&nbr[idx]) : -1;
       }
       bool b = false;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (u[j] >= 0) b |= blocks(a.q, prio, u[j], qv, kv);
+      for (int j = 0; j < kWarpU; ++j)
+        if (u[j] >= 0) b |= blocks(a.q, prio, u[j], qv, v);
       blocked = __any_sync(0xffffffffu, b);
-      hi -= 128;
+      hi -= 32 * kWarpU;
     }
     if (!blocked) {
       if (lane == 0) {

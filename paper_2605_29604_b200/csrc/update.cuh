@@ -274,18 +274,18 @@ __global__ void __launch_bounds__(kBlock)
     int64_t hi = e - kThreadMax;
     bool hit = false;
     while (!hit && hi > s) {
-      int32_t u[4];
+      int32_t u[kWarpU];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < kWarpU; ++j) {
         const int64_t idx = hi - 1 - lane - 32 * j;
-        u[j] = idx >= s ? __ldg(&nbr[idx]) : -1;
+        u[j] = idx >= s ? ld_stream(&nbr[idx]) : -1;
       }
       bool b = false;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < kWarpU; ++j)
         if (u[j] >= 0) b |= next[u[j]] == 1;
       hit = __any_sync(0xffffffffu, b);
-      hi -= 128;
+      hi -= 32 * kWarpU;
     }
     if (lane == 0) {
       if (hit) {
