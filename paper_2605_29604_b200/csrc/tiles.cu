@@ -154,31 +154,77 @@ __global__ void __launch_bounds__(256)
 //  k_count_light  one warp per block row with <= kHashMax entries (88 % of
 //                 R-MAT s22's block rows): a 1024-slot open-addressing set
 //                 in shared memory (atomicCAS), cleared after each row.
-//  k_count_mid    <= kMidMax entries: one 128-thread CTA per row (dynamic
-//                 work counter), a 4096-slot shared set.
-//  k_count_big    the rest: one 512-thread CTA per row, 128 KB of dynamic
+//  k_count_mid    <= kMidMax entries: one 256-thread CTA per row (dynamic
+//                 work counter), an 8192-slot shared set -- or, when the
+//                 graph has at most 2^18 block columns, every non-light row
+//                 on an exact 2^18-bit shared bitmap.
+//  k_count_big    the rest: one 512-thread CTA per row, 64 KB of dynamic
 //                 shared memory used as a set sized to the row (<= kBigHashMax
-//                 entries) or, for the hub rows beyond, as a 2^20-bit bitmap
-//                 swept window by window with per-row cursors (the rows are
-//                 sorted, so a window's entries are a prefix of what is left).
+//                 entries) or, for the hub rows beyond, as a 2^19-bit bitmap
+//                 swept window by window (one binary search per row and
+//                 window: the rows are sorted).
 //  The first version had only the light set and a bitmap CTA per (block row,
 //  2^18-column window) that located each window by binary search in all T
 //  rows: 202 ms at R-MAT s26 (half the block rows exceed 512 entries there).
 constexpr int kLightBlock = 256;
 constexpr int kHashSlots = 1024;
 constexpr int64_t kHashMax = 512;
-constexpr int kMidBlock = 128;
-constexpr int kMidSlots = 4096;
-constexpr int64_t kMidMax = 2048;
+constexpr int kMidBlock = 256;
+constexpr int kMidSlots = 8192;           // 32 KB: 7 CTAs per SM
+constexpr int64_t kMidMax = 4096;
 constexpr int kBigBlock = 512;
-constexpr int kBigWords = 32768;          // 128 KB of dynamic shared memory
-constexpr int64_t kBigHashMax = 16384;    // set of <= 32768 slots
+constexpr int kBigWords = 16384;          // 64 KB of dynamic shared memory: 3 CTAs per SM
+constexpr int64_t kBigHashMax = 8192;     // set of <= 16384 slots
 constexpr int64_t kBigBits = 32ll * kBigWords;
+// hub block rows (R-MAT s22's block row 0 holds ~1M entries): one CTA per
+// row serialised the whole count behind it (0.5-1.1 ms); they are counted by
+// kHubCTAs CTAs each on a global bitmap (L2 atomics), kHubBatch rows at a time
+constexpr int64_t kHubMin = 65536;
+constexpr int kHubCTAs = 64;
+constexpr int kHubBatch = 64;
+
+__global__ void __launch_bounds__(256)
+    k_count_hub(int32_t n, int T, int32_t nb, const int64_t *__restrict__ off,
+                const int32_t *__restrict__ nbr, int32_t *__restrict__ rowtiles,
+                const int32_t *__restrict__ hubs, int first, uint32_t *__restrict__ bitmaps) {
+  __shared__ int s_red[8];
+  const int h = blockIdx.y;
+  const int32_t b = hubs[first + h];
+  const int64_t r0 = (int64_t)b * T, r1 = min((int64_t)n, r0 + T);
+  const int64_t s = off[r0], e = off[r1];
+  uint32_t *bm = bitmaps + (size_t)h * (((size_t)nb + 31) / 32);
+  const uint32_t uT = (uint32_t)T;
+  int cnt = 0;
+  const int64_t stride = (int64_t)gridDim.x * 256 * 4;
+  for (int64_t base = s + (int64_t)blockIdx.x * 256 * 4; base < e; base += stride) {
+    uint32_t c[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t p = base + threadIdx.x + 256ll * j;
+      c[j] = p < e ? (uint32_t)__ldg(&nbr[p]) / uT : 0xffffffffu;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (c[j] == 0xffffffffu) continue;
+      const uint32_t bit = 1u << (c[j] & 31u);
+      cnt += (atomicOr(&bm[c[j] >> 5], bit) & bit) ? 0 : 1;
+    }
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int i = 0; i < 8; ++i) t += s_red[i];
+    if (t) atomicAdd(&rowtiles[b], t);
+  }
+}
 
 __global__ void __launch_bounds__(kLightBlock)
     k_count_light(int32_t n, int T, int32_t nb, const int64_t *__restrict__ off,
                   const int32_t *__restrict__ nbr, int32_t *__restrict__ rowtiles,
-                  int32_t *__restrict__ lists, int32_t *__restrict__ counts) {
+                  int32_t *__restrict__ lists, int32_t *__restrict__ counts, int bitmap,
+                  int32_t *__restrict__ hubs) {
   __shared__ __align__(16) uint32_t tab[kLightBlock / 32][kHashSlots];
   const int lane = threadIdx.x & 31;
   uint32_t *t = tab[threadIdx.x >> 5];
@@ -192,7 +238,8 @@ __global__ void __launch_bounds__(kLightBlock)
     const int64_t s = off[r0], e = off[r1];
     if (e - s > kHashMax) {  // mid rows from the front of `lists`, big rows from the back
       if (lane == 0) {
-        if (e - s <= kMidMax) lists[atomicAdd(&counts[0], 1)] = (int32_t)b;
+        if (e - s > kHubMin) hubs[atomicAdd(&counts[4], 1)] = (int32_t)b;
+        else if (bitmap || e - s <= kMidMax) lists[atomicAdd(&counts[0], 1)] = (int32_t)b;
         else lists[nb - 1 - atomicAdd(&counts[1], 1)] = (int32_t)b;
       }
       continue;
@@ -237,17 +284,27 @@ __device__ __forceinline__ int cta_hash_count(uint32_t *tab, int slots, const in
                                               int64_t s, int64_t e, uint32_t uT, int *s_red) {
   const int shift = 32 - (__ffs(slots) - 1);
   int cnt = 0;
-  for (int64_t p = s + threadIdx.x; p < e; p += blockDim.x) {
-    const uint32_t c = (uint32_t)__ldg(&nbr[p]) / uT + 1u;
-    uint32_t h = (c * 0x9E3779B1u) >> shift;
-    for (;;) {
-      const uint32_t old = atomicCAS(&tab[h], 0u, c);
-      if (old == 0u) {
-        ++cnt;
-        break;
+  for (int64_t base = s; base < e; base += 4 * (int64_t)blockDim.x) {
+    uint32_t cc[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {  // 4 independent loads in flight per thread
+      const int64_t p = base + threadIdx.x + (int64_t)blockDim.x * j;
+      cc[j] = p < e ? (uint32_t)__ldg(&nbr[p]) / uT + 1u : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t c = cc[j];
+      if (!c) continue;
+      uint32_t h = (c * 0x9E3779B1u) >> shift;
+      for (;;) {
+        const uint32_t old = atomicCAS(&tab[h], 0u, c);
+        if (old == 0u) {
+          ++cnt;
+          break;
+        }
+        if (old == c) break;
+        h = (h + 1) & (slots - 1);
       }
-      if (old == c) break;
-      h = (h + 1) & (slots - 1);
     }
   }
   cnt = __reduce_add_sync(0xffffffffu, cnt);
@@ -264,7 +321,7 @@ __device__ __forceinline__ int cta_hash_count(uint32_t *tab, int slots, const in
 __global__ void __launch_bounds__(kMidBlock)
     k_count_mid(int32_t n, int T, const int64_t *__restrict__ off, const int32_t *__restrict__ nbr,
                 int32_t *__restrict__ rowtiles, const int32_t *__restrict__ list,
-                const int32_t *__restrict__ count, unsigned *__restrict__ next_item) {
+                const int32_t *__restrict__ count, unsigned *__restrict__ next_item, int bitmap) {
   __shared__ __align__(16) uint32_t tab[kMidSlots];
   __shared__ int s_red[kMidBlock / 32];
   __shared__ unsigned s_item;
@@ -280,9 +337,35 @@ __global__ void __launch_bounds__(kMidBlock)
     const int32_t b = list[it];
     const int64_t r0 = (int64_t)b * T, r1 = min((int64_t)n, r0 + T);
     const int64_t s = off[r0], e = off[r1];
-    int slots = 1024;
-    while (slots < 2 * (e - s) && slots < kMidSlots) slots <<= 1;
-    const int total = cta_hash_count(tab, slots, nbr, s, e, (uint32_t)T, s_red);
+    int total;
+    if (bitmap) {  // every block column has its own bit (nb <= 32 * kMidSlots)
+      int cnt = 0;
+      for (int64_t base = s; base < e; base += 4 * kMidBlock) {
+        uint32_t c[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {  // 4 independent loads in flight per thread
+          const int64_t p = base + threadIdx.x + (int64_t)kMidBlock * j;
+          c[j] = p < e ? (uint32_t)__ldg(&nbr[p]) / (uint32_t)T : 0xffffffffu;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (c[j] == 0xffffffffu) continue;
+          const uint32_t bit = 1u << (c[j] & 31u);
+          cnt += (atomicOr(&tab[c[j] >> 5], bit) & bit) ? 0 : 1;
+        }
+      }
+      cnt = __reduce_add_sync(0xffffffffu, cnt);
+      if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = cnt;
+      __syncthreads();
+      total = 0;
+      for (int w = 0; w < kMidBlock / 32; ++w) total += s_red[w];
+      for (int i = threadIdx.x; i < kMidSlots / 4; i += kMidBlock) t4[i] = make_uint4(0, 0, 0, 0);
+      __syncthreads();
+    } else {
+      int slots = 1024;
+      while (slots < 2 * (e - s) && slots < kMidSlots) slots <<= 1;
+      total = cta_hash_count(tab, slots, nbr, s, e, (uint32_t)T, s_red);
+    }
     if (threadIdx.x == 0) rowtiles[b] = total;
   }
 }
@@ -296,7 +379,6 @@ __global__ void __launch_bounds__(kBigBlock)
   __shared__ int s_red[kBigBlock / 32];
   __shared__ int64_t s_cur[64], s_end[64];
   __shared__ unsigned s_item;
-  __shared__ int s_adv;
   uint4 *b4 = reinterpret_cast<uint4 *>(big);
   for (int i = threadIdx.x; i < kBigWords / 4; i += kBigBlock) b4[i] = make_uint4(0, 0, 0, 0);
   const unsigned items = (unsigned)*count;
@@ -318,35 +400,29 @@ __global__ void __launch_bounds__(kBigBlock)
       if (threadIdx.x == 0) rowtiles[b] = total;
       continue;
     }
-    // hub rows: windows of kBigBits block columns; row k's entries of window
-    // w are the next ones after its cursor (sorted rows)
-    if (threadIdx.x < rows) {
-      s_cur[threadIdx.x] = off[r0 + threadIdx.x];
-      s_end[threadIdx.x] = off[r0 + threadIdx.x + 1];
-    }
-    __syncthreads();
+    // hub rows: windows of kBigBits block columns.  Row k's entries of window
+    // w are [lower_bound(k, w), lower_bound(k, w + 1)) (sorted rows): one
+    // binary search per row and window, then plain strided passes (the first
+    // version advanced per-row cursors chunk by chunk with two block barriers
+    // per 512 entries: 0.6 ms for the 162k-entry hub row of R-MAT s22)
     int cnt = 0;
     const int64_t windows = ((int64_t)nb + kBigBits - 1) / kBigBits;
     for (int64_t w = 0; w < windows; ++w) {
-      const uint32_t wlo = (uint32_t)(w * kBigBits);
+      const int64_t wlo = w * kBigBits;
+      if (threadIdx.x < rows) {
+        const int64_t rs = off[r0 + threadIdx.x], re = off[r0 + threadIdx.x + 1];
+        s_cur[threadIdx.x] = w == 0 ? rs : lower_bound_i32(nbr, rs, re, wlo * T);
+        s_end[threadIdx.x] = w + 1 == windows ? re : lower_bound_i32(nbr, rs, re, (wlo + kBigBits) * T);
+      }
+      __syncthreads();
       for (int k = 0; k < rows; ++k) {
-        for (;;) {
-          const int64_t p = s_cur[k] + threadIdx.x;
-          bool in = false;
-          if (p < s_end[k]) {
-            const uint32_t c = (uint32_t)__ldg(&nbr[p]) / uT;
-            if ((int64_t)c < (int64_t)wlo + kBigBits) {
-              in = true;
-              const uint32_t bit = 1u << ((c - wlo) & 31u);
-              cnt += (atomicOr(&big[(c - wlo) >> 5], bit) & bit) ? 0 : 1;
-            }
-          }
-          const int adv = __syncthreads_count(in);
-          if (threadIdx.x == 0) s_cur[k] += adv;
-          __syncthreads();
-          if (adv < kBigBlock) break;
+        for (int64_t p = s_cur[k] + threadIdx.x; p < s_end[k]; p += kBigBlock) {
+          const uint32_t c = (uint32_t)__ldg(&nbr[p]) / uT - (uint32_t)wlo;
+          const uint32_t bit = 1u << (c & 31u);
+          cnt += (atomicOr(&big[c >> 5], bit) & bit) ? 0 : 1;
         }
       }
+      __syncthreads();
       for (int i = threadIdx.x; i < kBigWords / 4; i += kBigBlock) b4[i] = make_uint4(0, 0, 0, 0);
       __syncthreads();
     }
@@ -430,27 +506,52 @@ int build_tile_counts(tcmis_graph *g, int T) {
   if (nb > 0) {
     // lists: mid rows from the front, big rows from the back; counts[0..1]
     // list sizes, counts[2..3] the dynamic work counters
-    int32_t *lists = nullptr, *cnt = nullptr;
+    // few enough block columns for one shared bitmap (R-MAT s22: nb = 2^18):
+    // every non-light row goes to k_count_mid's exact bitmap, no hashing
+    const int bitmap = (int64_t)nb <= 32ll * kMidSlots ? 1 : 0;
+    int32_t *lists = nullptr, *cnt = nullptr, *hubs = nullptr;
     if (int rc = dev_alloc(&lists, (size_t)nb)) return rc;
-    if (int rc = dev_alloc(&cnt, 4)) return rc;
-    TCMIS_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(int32_t), st));
+    if (int rc = dev_alloc(&hubs, (size_t)nb)) return rc;
+    if (int rc = dev_alloc(&cnt, 8)) return rc;
+    TCMIS_CUDA(cudaMemsetAsync(cnt, 0, 8 * sizeof(int32_t), st));
     k_count_light<<<grid_for(ctx, 32ll * nb, kLightBlock, 8), kLightBlock, 0, st>>>(
-        g->n, T, nb, g->d_off, g->d_nbr, g->d_rowtiles, lists, cnt);
+        g->n, T, nb, g->d_off, g->d_nbr, g->d_rowtiles, lists, cnt, bitmap, hubs);
     TCMIS_LAUNCHED(ctx);
+    int32_t nhub = 0;
+    TCMIS_CUDA(cudaMemcpyAsync(&nhub, cnt + 4, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    TCMIS_CUDA(cudaStreamSynchronize(st));
+    if (nhub > 0) {
+      // rowtiles[hub] was never written by k_count_light: start from 0
+      const size_t words = ((size_t)nb + 31) / 32;
+      uint32_t *bms = nullptr;
+      const int batch = std::min(nhub, kHubBatch);
+      if (int rc = dev_alloc(&bms, words * batch)) return rc;
+      for (int first = 0; first < nhub; first += kHubBatch) {
+        const int nh = std::min(kHubBatch, nhub - first);
+        TCMIS_CUDA(cudaMemsetAsync(bms, 0, 4 * words * nh, st));
+        k_count_hub<<<dim3(kHubCTAs, nh), 256, 0, st>>>(g->n, T, nb, g->d_off, g->d_nbr,
+                                                        g->d_rowtiles, hubs, first, bms);
+        TCMIS_LAUNCHED(ctx);
+      }
+      dev_free(bms);
+    }
     int mid_per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mid_per_sm, k_count_mid, kMidBlock, 0);
     k_count_mid<<<ctx->num_sms * std::max(1, mid_per_sm), kMidBlock, 0, st>>>(
         g->n, T, g->d_off, g->d_nbr, g->d_rowtiles, lists, cnt,
-        reinterpret_cast<unsigned *>(cnt + 2));
+        reinterpret_cast<unsigned *>(cnt + 2), bitmap);
     TCMIS_LAUNCHED(ctx);
     const size_t big_smem = sizeof(uint32_t) * kBigWords;
     TCMIS_CUDA(cudaFuncSetAttribute(k_count_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)big_smem));
-    k_count_big<<<ctx->num_sms, kBigBlock, big_smem, st>>>(
+    int big_per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&big_per_sm, k_count_big, kBigBlock, big_smem);
+    k_count_big<<<ctx->num_sms * std::max(1, big_per_sm), kBigBlock, big_smem, st>>>(
         g->n, T, nb, g->d_off, g->d_nbr, g->d_rowtiles, lists + nb - 1, cnt + 1,
         reinterpret_cast<unsigned *>(cnt + 3));
     TCMIS_LAUNCHED(ctx);
     dev_free(lists);
+    dev_free(hubs);
     dev_free(cnt);
     unsigned long long *d_total = nullptr;
     if (int rc = dev_alloc(&d_total, 1)) return rc;
