@@ -16,7 +16,9 @@
 
 #include <cstdint>
 #include <functional>
+#include <optional>
 #include <span>
+#include <utility>
 #include <string>
 #include <utility>
 #include <vector>
@@ -230,6 +232,24 @@ MISResult run_luby_reference(const Graph &g, std::uint64_t seed, LubyMode mode,
                              int scale_bits = kDefaultScaleBits, int workers = 1);
 
 MISResult run_mis(const Graph &g, const EngineConfig &config);
+
+// ------------------------------------------------------------- validate.hpp
+// validate.hpp:12-31 check_independence / check_maximality, evaluated on the
+// device (tcmis_validate); same witnesses and exception types.
+struct IndependenceReport {
+  bool independent = false;
+  std::optional<std::pair<VertexId, VertexId>> violating_edge;
+};
+
+IndependenceReport check_independence(const Graph &g, std::span<const VertexId> set);
+
+struct MaximalityReport {
+  bool maximal = false;
+  std::optional<VertexId> addable_vertex;
+};
+
+/// Requires an independent input set; throws std::invalid_argument otherwise.
+MaximalityReport check_maximality(const Graph &g, std::span<const VertexId> set);
 
 }  // namespace b200
 }  // namespace tcmis

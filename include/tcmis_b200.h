@@ -158,6 +158,15 @@ int tcmis_graph_export_tiles(tcmis_graph *g, int32_t tile_dim, int32_t *tile_row
 int tcmis_graph_tile_store(tcmis_graph *g, int32_t tile_dim, int64_t *tile_count,
                            int64_t *block_row_offsets, int32_t *tile_col, void *payload);
 
+/* validate.cpp:45-75 check_independence + check_maximality on the device, in
+ * one pass, with the reference's witnesses: *independent (else the violating
+ * edge (u, v), u < v, of the smallest offending vertex) and *maximal (else
+ * the smallest addable vertex; meaningful only for an independent set).  An id
+ * outside [0, n) -> TCMIS_E_INVALID_ARGUMENT (validate.cpp:12-22). */
+int tcmis_validate(tcmis_graph *g, const int32_t *set, int64_t count, int32_t *independent,
+                   int32_t *violating_u, int32_t *violating_v, int32_t *maximal,
+                   int32_t *addable_vertex);
+
 /* priorities.cpp:33-67 (h1_random / h2_degree_aware) on the device; p_out is
  * a host buffer of n entries. */
 int tcmis_priorities(tcmis_graph *g, int32_t heuristic, uint64_t seed, int32_t scale_bits,

@@ -120,6 +120,10 @@ def lib():
             fn.argtypes = args
         L.orc_rgg_radius.restype = C.c_uint64
         L.orc_rgg_radius.argtypes = [C.c_int32, C.c_double]
+        L.orc_check_independence.argtypes = [C.c_int32, i64p, i32p, i32p, C.c_int64,
+                                             C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        L.orc_check_maximality.argtypes = [C.c_int32, i64p, i32p, i32p, C.c_int64,
+                                           C.POINTER(C.c_int32)]
         L.orc_graph_free.argtypes = [C.POINTER(OrcGraph)]
         L.orc_checksum_bytes.restype = C.c_uint64
         L.orc_checksum_bytes.argtypes = [C.c_void_p, C.c_int64]
@@ -190,6 +194,10 @@ def ref():
         R.ref_sequential_greedy.argtypes = [C.c_void_p, u32p, u8p]
         R.ref_compute_max_np.argtypes = [C.c_void_p, u32p, u8p, u64p]
         R.ref_h3_resolution.argtypes = [C.c_void_p, u32p, u8p, u8p]
+        R.ref_check_independence.argtypes = [C.c_void_p, i32p, C.c_int64, C.POINTER(C.c_int32),
+                                             C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        R.ref_check_maximality.argtypes = [C.c_void_p, i32p, C.c_int64, C.POINTER(C.c_int32),
+                                           C.POINTER(C.c_int32)]
         _ref = R
     return _ref
 
@@ -428,3 +436,50 @@ def _ref_exc(code: int) -> Exception:
     msg = ref().ref_last_error().decode()
     return {1: ValueError, 2: RuntimeError, 3: AssertionError, 5: IndexError}.get(
         code, RuntimeError)(msg)
+
+
+# ------------------------------------------------------------- validation
+
+def check_independence(g: Graph, mis_set):
+    """validate.cpp:45-56 (C restatement): (independent, edge or None)."""
+    st = np.ascontiguousarray(mis_set, np.int32)
+    u, v = C.c_int32(0), C.c_int32(0)
+    r = lib().orc_check_independence(g.n, g.off, g.nbr if g.nbr.size else np.zeros(1, np.int32),
+                                     st if st.size else np.zeros(1, np.int32), st.size,
+                                     C.byref(u), C.byref(v))
+    if r < 0:
+        raise ValueError("set contains a vertex id outside [0, n)")
+    return bool(r), (None if r else (u.value, v.value))
+
+
+def check_maximality(g: Graph, mis_set):
+    st = np.ascontiguousarray(mis_set, np.int32)
+    a = C.c_int32(0)
+    r = lib().orc_check_maximality(g.n, g.off, g.nbr if g.nbr.size else np.zeros(1, np.int32),
+                                   st if st.size else np.zeros(1, np.int32), st.size, C.byref(a))
+    if r == -1:
+        raise ValueError("set contains a vertex id outside [0, n)")
+    if r == -2:
+        raise ValueError("maximality is defined on independent sets")
+    return bool(r), (None if r else a.value)
+
+
+def ref_check_independence(rg, mis_set):
+    """The reference's own check_independence (validate.cpp:45-56)."""
+    st = np.ascontiguousarray(mis_set, np.int32)
+    ind, u, v = C.c_int32(0), C.c_int32(0), C.c_int32(0)
+    rc = ref().ref_check_independence(rg.h, st if st.size else np.zeros(1, np.int32), st.size,
+                                      C.byref(ind), C.byref(u), C.byref(v))
+    if rc:
+        raise _ref_exc(rc)
+    return bool(ind.value), (None if ind.value else (u.value, v.value))
+
+
+def ref_check_maximality(rg, mis_set):
+    st = np.ascontiguousarray(mis_set, np.int32)
+    mx, a = C.c_int32(0), C.c_int32(0)
+    rc = ref().ref_check_maximality(rg.h, st if st.size else np.zeros(1, np.int32), st.size,
+                                    C.byref(mx), C.byref(a))
+    if rc:
+        raise _ref_exc(rc)
+    return bool(mx.value), (None if mx.value else a.value)

@@ -18,6 +18,7 @@
 #include "tcmis/priorities.hpp"
 #include "tcmis/spmv.hpp"
 #include "tcmis/tiling.hpp"
+#include "tcmis/validate.hpp"
 
 namespace {
 
@@ -286,6 +287,36 @@ int ref_h3_resolution(void* g, const uint32_t* p, const uint8_t* states, uint8_t
   auto r = tcmis::run_h3_resolution(*gr, pv, st, 1);
   std::memcpy(c, r.data(), r.size());
   return 0;
+}
+
+// validate.cpp:45-75 -- the reference's own validators (pins the oracle's)
+int ref_check_independence(void* gh, const int32_t* set, int64_t cnt, int32_t* independent,
+                           int32_t* wu, int32_t* wv) {
+  try {
+    const auto& g = *static_cast<tcmis::Graph*>(gh);
+    auto r = tcmis::check_independence(g, std::span<const tcmis::VertexId>(set, (size_t)cnt));
+    *independent = r.independent ? 1 : 0;
+    if (r.violating_edge) {
+      *wu = r.violating_edge->first;
+      *wv = r.violating_edge->second;
+    }
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+int ref_check_maximality(void* gh, const int32_t* set, int64_t cnt, int32_t* maximal,
+                         int32_t* addable) {
+  try {
+    const auto& g = *static_cast<tcmis::Graph*>(gh);
+    auto r = tcmis::check_maximality(g, std::span<const tcmis::VertexId>(set, (size_t)cnt));
+    *maximal = r.maximal ? 1 : 0;
+    if (r.addable_vertex) *addable = *r.addable_vertex;
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
 }
 
 }  // extern "C"

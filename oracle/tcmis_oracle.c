@@ -623,3 +623,59 @@ uint64_t orc_checksum_bytes(const void *data, int64_t len) {
   }
   return h;
 }
+
+/* ------------------------------------------------------------ validation */
+
+/* validate.cpp:45-56 check_independence: the first v (ascending) in the set
+ * with a neighbour u in the set gives the witness (min, max).  Returns 1
+ * independent, 0 not (witness in *wu, *wv), -1 an id outside [0, n). */
+int orc_check_independence(int32_t n, const int64_t *off, const int32_t *nbr, const int32_t *set,
+                           int64_t cnt, int32_t *wu, int32_t *wv) {
+  uint8_t *in = (uint8_t *)calloc((size_t)(n > 0 ? n : 1), 1);
+  for (int64_t i = 0; i < cnt; ++i) {
+    if (set[i] < 0 || set[i] >= n) {
+      free(in);
+      return -1;
+    }
+    in[set[i]] = 1;
+  }
+  for (int32_t v = 0; v < n; ++v) {
+    if (!in[v]) continue;
+    for (int64_t e = off[v]; e < off[v + 1]; ++e) {
+      const int32_t u = nbr[e];
+      if (in[u]) {
+        *wu = u < v ? u : v;
+        *wv = u < v ? v : u;
+        free(in);
+        return 0;
+      }
+    }
+  }
+  free(in);
+  return 1;
+}
+
+/* validate.cpp:58-75 check_maximality (independent input): the first v not
+ * in the set without a neighbour in the set is addable.  Returns 1 maximal,
+ * 0 not (*addable), -1 bad id, -2 the set is not independent. */
+int orc_check_maximality(int32_t n, const int64_t *off, const int32_t *nbr, const int32_t *set,
+                         int64_t cnt, int32_t *addable) {
+  int32_t a, b;
+  const int ind = orc_check_independence(n, off, nbr, set, cnt, &a, &b);
+  if (ind < 0) return -1;
+  if (ind == 0) return -2;
+  uint8_t *in = (uint8_t *)calloc((size_t)(n > 0 ? n : 1), 1);
+  for (int64_t i = 0; i < cnt; ++i) in[set[i]] = 1;
+  for (int32_t v = 0; v < n; ++v) {
+    if (in[v]) continue;
+    int blocked = 0;
+    for (int64_t e = off[v]; e < off[v + 1] && !blocked; ++e) blocked = in[nbr[e]];
+    if (!blocked) {
+      *addable = v;
+      free(in);
+      return 0;
+    }
+  }
+  free(in);
+  return 1;
+}

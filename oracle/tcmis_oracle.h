@@ -108,4 +108,9 @@ uint64_t orc_checksum_bytes(const void *data, int64_t len);
 #ifdef __cplusplus
 }
 #endif
+int orc_check_independence(int32_t n, const int64_t *off, const int32_t *nbr, const int32_t *set,
+                           int64_t cnt, int32_t *wu, int32_t *wv);
+int orc_check_maximality(int32_t n, const int64_t *off, const int32_t *nbr, const int32_t *set,
+                         int64_t cnt, int32_t *addable);
+
 #endif

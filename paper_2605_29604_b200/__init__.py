@@ -133,6 +133,7 @@ def load():
         "tcmis_graph_set_tiling": (C.c_int, [vp, i32, vp, i32]),
         "tcmis_graph_export_tiles": (C.c_int, [vp, i32, vp, vp, vp, vp]),
         "tcmis_graph_tile_store": (C.c_int, [vp, i32, P(i64), vp, vp, vp]),
+        "tcmis_validate": (C.c_int, [vp, vp, i64, P(i32), P(i32), P(i32), P(i32), P(i32)]),
         "tcmis_priorities": (C.c_int, [vp, i32, u64, i32, vp]),
         "tcmis_solve": (C.c_int, [vp, P(_Config), vp, vp, P(i64), P(_Stats), i32, P(i32)]),
         "tcmis_solve_device": (C.c_int, [vp, P(_Config), P(vp), P(i64), P(vp), P(_Stats), i32,
@@ -522,6 +523,29 @@ def tile_graph(g, tile_dim: int = 16, ctx: Optional[Context] = None) -> TiledAdj
                                            _ptr(bro)))
     return TiledAdjacency(tile_dim, dg.n, nb * tile_dim, tr[:cnt], tc[:cnt], rb[:cnt * tile_dim],
                           bro)
+
+
+def _check_set(g, mis_set, ctx=None):
+    dg = _as_device(g, ctx)
+    st = np.ascontiguousarray(mis_set, np.int32)
+    r = [C.c_int32(0) for _ in range(5)]
+    _check(load().tcmis_validate(dg.h, _ptr(st), st.size, *[C.byref(x) for x in r]))
+    return [x.value for x in r]
+
+
+def check_independence(g, mis_set, ctx: Optional[Context] = None):
+    """validate.cpp:45-56 on the device: (independent, violating_edge or None)."""
+    ind, u, v, _, _ = _check_set(g, mis_set, ctx)
+    return bool(ind), (None if ind else (u, v))
+
+
+def check_maximality(g, mis_set, ctx: Optional[Context] = None):
+    """validate.cpp:58-75 on the device: (maximal, addable_vertex or None);
+    ValueError for a set that is not independent."""
+    ind, _, _, mx, a = _check_set(g, mis_set, ctx)
+    if not ind:
+        raise ValueError("maximality is defined on independent sets")
+    return bool(mx), (None if mx else a)
 
 
 def tile_store(g, tile_dim: int = 16, ctx: Optional[Context] = None):

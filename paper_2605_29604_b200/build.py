@@ -29,7 +29,8 @@ NVCC_FLAGS = ARCH + [
     "-Xcompiler", "-fPIC,-fvisibility=hidden,-ffp-contract=off",
     "-I", INC, "-I", CSRC,
 ] + os.environ.get("TCMIS_NVCC_EXTRA", "").split()
-CU_SOURCES = ["capi.cu", "solver.cu", "tiles.cu", "gen.cu", "tiled_spmv.cu", "dist.cu"]
+CU_SOURCES = ["capi.cu", "solver.cu", "tiles.cu", "gen.cu", "tiled_spmv.cu", "dist.cu",
+              "validate.cu"]
 CXX_SOURCES = ["engine.cpp"]
 
 

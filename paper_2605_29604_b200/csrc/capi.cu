@@ -47,6 +47,8 @@ int gen_gnp_host(int32_t n, double avg_degree, uint64_t seed, int64_t **offsets,
                  int32_t **neighbors, int64_t *nnz_out);
 int h1_impl(tcmis_ctx *ctx, int32_t n, uint64_t seed, uint32_t *p_out);
 int partition_device(tcmis_graph *full, int32_t lo, int32_t hi, tcmis_graph **out);
+int validate_impl(tcmis_graph *g, const int32_t *set, int64_t cnt, int32_t *independent,
+                  int32_t *wu, int32_t *wv, int32_t *maximal, int32_t *addable);
 int upload_partition(tcmis_ctx *ctx, int32_t n, int32_t lo, int32_t hi, const int64_t *full,
                      const int32_t *rows, tcmis_graph **out);
 int dist_begin(tcmis_graph *g, const tcmis_config *cfg);
@@ -311,6 +313,17 @@ TCMIS_API int tcmis_graph_tile_store(tcmis_graph *g, int32_t T, int64_t *tile_co
                                cudaMemcpyDeviceToHost, st));
   TCMIS_CUDA(cudaStreamSynchronize(st));
   return 0;
+}
+
+TCMIS_API int tcmis_validate(tcmis_graph *g, const int32_t *set, int64_t count,
+                             int32_t *independent, int32_t *violating_u, int32_t *violating_v,
+                             int32_t *maximal, int32_t *addable_vertex) {
+  NEED(g && independent && violating_u && violating_v && maximal && addable_vertex,
+       "null handle");
+  NEED(count >= 0 && (count == 0 || set), "null set");
+  ENTER(g->ctx);
+  return validate_impl(g, set, count, independent, violating_u, violating_v, maximal,
+                       addable_vertex);
 }
 
 TCMIS_API int tcmis_priorities(tcmis_graph *g, int32_t heuristic, uint64_t seed,

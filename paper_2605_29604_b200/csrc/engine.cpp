@@ -272,6 +272,45 @@ std::vector<std::int32_t> csr_neighbor_count_oracle(const Graph &g,
   return nc;
 }
 
+// --------------------------------------------------------------- validate
+
+namespace {
+struct SetCheck {
+  std::int32_t independent = 0, u = 0, v = 0, maximal = 0, addable = 0;
+};
+SetCheck check_set(const Graph &g, std::span<const VertexId> set) {
+  SetCheck r;
+  if (g.n == 0) {  // membership() still rejects any id (validate.cpp:12-22)
+    if (!set.empty())
+      throw std::invalid_argument("set contains vertex id " + std::to_string(set[0]) +
+                                  " outside [0, n)");
+    r.independent = r.maximal = 1;
+    return r;
+  }
+  DeviceGraph dg(g);
+  check(tcmis_validate(dg.h, set.data(), static_cast<std::int64_t>(set.size()), &r.independent,
+                       &r.u, &r.v, &r.maximal, &r.addable));
+  return r;
+}
+}  // namespace
+
+IndependenceReport check_independence(const Graph &g, std::span<const VertexId> set) {
+  const SetCheck c = check_set(g, set);
+  IndependenceReport r;
+  r.independent = c.independent != 0;
+  if (!r.independent) r.violating_edge = std::pair<VertexId, VertexId>{c.u, c.v};
+  return r;
+}
+
+MaximalityReport check_maximality(const Graph &g, std::span<const VertexId> set) {
+  const SetCheck c = check_set(g, set);
+  if (!c.independent) throw std::invalid_argument("maximality is defined on independent sets");
+  MaximalityReport r;
+  r.maximal = c.maximal != 0;
+  if (!r.maximal) r.addable_vertex = c.addable;
+  return r;
+}
+
 // ----------------------------------------------------------------- engine
 
 const char *heuristic_name(Heuristic h) {

@@ -11,6 +11,7 @@
 
 #include "tcmis/engine.hpp"
 #include "tcmis/tiling.hpp"
+#include "tcmis/validate.hpp"
 
 using namespace tcmis;
 
@@ -82,6 +83,21 @@ int main(int argc, char **argv) {
   std::printf("{\"tiles8\": %lld, \"t8_rounds\": %zu, \"t8_eval1\": %lld}\n",
               (long long)t8.tile_count(), r8.iterations.size(),
               (long long)(r8.iterations.empty() ? 0 : r8.iterations[0].tiles_evaluated));
+  // validate.hpp on the device: the H2 result, and the result minus its
+  // first vertex (no longer maximal)
+  {
+    EngineConfig c2;
+    c2.heuristic = Heuristic::H2;
+    MISResult r2 = run_mis(g, c2);
+    IndependenceReport ir = check_independence(g, r2.mis);
+    MaximalityReport mr = check_maximality(g, r2.mis);
+    std::span<const VertexId> tail(r2.mis.data() + 1, r2.mis.size() - 1);
+    MaximalityReport mr2 = check_maximality(g, tail);
+    std::printf("{\"valid_ind\": %d, \"valid_max\": %d, \"minus_first_max\": %d, "
+                "\"addable\": %d}\n",
+                ir.independent ? 1 : 0, mr.maximal ? 1 : 0, mr2.maximal ? 1 : 0,
+                mr2.addable_vertex ? (int)*mr2.addable_vertex : -1);
+  }
   // reference error behaviour
   EngineConfig bad;
   bad.tile_dim = 0;

@@ -58,6 +58,12 @@ def test_cpp_dropin_matches_reference(dropin, kind, args):
         want_obs = {"h1": exp.n_rounds, "h2": exp.n_rounds, "h3": 1, "luby-fresh": 0,
                     "luby-perm": 0}[r["heuristic"]]
         assert r["observed"] == want_obs
+    val = [x for x in lines if "valid_ind" in x][0]
+    exp2 = O.solve(g, "h2", 1, tile_dim=16)
+    mis2 = np.flatnonzero(exp2.state == 1)
+    assert (val["valid_ind"], val["valid_max"]) == (1, 1)
+    want = O.check_maximality(g, mis2[1:])
+    assert (bool(val["minus_first_max"]), val["addable"]) == (want[0], -1 if want[1] is None else want[1])
     t8 = [x for x in lines if "tiles8" in x][0]
     assert t8["tiles8"] == int(O.tile_row_counts(g, 8).sum())
     e8 = O.solve(g, "h2", 1, tile_dim=8)

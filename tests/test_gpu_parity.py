@@ -467,3 +467,36 @@ def test_tile_kernels_match_tiled_spmv(ctx, excl, T):
             assert rc == 0, L.tcmis_last_error()
             assert np.array_equal(got, nc)
             assert (gev.value, gsk.value) == (ev.value, sk.value)
+
+
+@pytest.mark.parametrize("spec", [("rmat", 12, 16, 3), ("gnp_avg", 3000, 8.0, 2), ("grid", 40),
+                                  ("rgg", 5000, 3.0, 1), ("petersen",)])
+def test_device_validator_matches_oracle(ctx, spec):
+    """check_independence / check_maximality on the device give
+    the reference's answers and witnesses (oracle pinned to the reference in
+    tests/test_oracle.py)."""
+    g = O.gen(*spec)
+    dg = tc.DeviceGraph.upload(as_tc(g), ctx)
+    rng = np.random.default_rng(3)
+    s = O.solve(g, "h2", 1, tile_dim=16)
+    mis = np.flatnonzero(s.state == 1).astype(np.int32)
+    sets = [mis, mis[: max(0, mis.size - 3)], np.zeros(0, np.int32),
+            np.concatenate([mis, rng.integers(0, g.n, 5).astype(np.int32)])]
+    for st in sets:
+        assert tc.check_independence(dg, st) == O.check_independence(g, st)
+        if O.check_independence(g, st)[0]:
+            assert tc.check_maximality(dg, st) == O.check_maximality(g, st)
+        else:
+            with pytest.raises(ValueError):
+                tc.check_maximality(dg, st)
+    with pytest.raises(ValueError):
+        tc.check_independence(dg, np.array([g.n], np.int32))
+
+
+def test_device_validator_on_rmat22(ctx):
+    """The s22 solve validated on the device (independent and maximal)."""
+    dg = tc.DeviceGraph.rmat(22, 16, 1, ctx)
+    res = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2))
+    assert tc.check_independence(dg, res.mis) == (True, None)
+    assert tc.check_maximality(dg, res.mis) == (True, None)
+    assert tc.check_maximality(dg, res.mis[1:])[0] is False

@@ -200,3 +200,42 @@ def test_oracle_against_large_golden(name):
     if name not in golden_names(large=True):
         pytest.skip("large fixture not generated")
     test_oracle_against_golden_fixtures(name)
+
+
+def _sets_for(g, rng):
+    """independent+maximal (an MIS), independent non-maximal, dependent sets"""
+    s = O.solve(g, "h2", 1, tile_dim=16)
+    mis = np.flatnonzero(s.state == 1).astype(np.int32)
+    out = [mis, mis[: max(0, mis.size - 3)], np.zeros(0, np.int32)]
+    if g.nbr.size:
+        v = int(rng.integers(0, g.n))
+        while g.off[v + 1] == g.off[v]:
+            v = int(rng.integers(0, g.n))
+        out.append(np.array([v, g.nbr[g.off[v]]], np.int32))
+        out.append(np.concatenate([mis, rng.integers(0, g.n, 5).astype(np.int32)]))
+    return out
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("spec", [("rmat", 10, 16, 3), ("gnp_avg", 500, 6.0, 2), ("grid", 12),
+                                  ("petersen",)])
+def test_validate_restatement_matches_reference(spec):
+    """check_independence / check_maximality (validate.cpp:45-75): the C
+    restatement gives the reference's answers and witnesses."""
+    g = O.gen(*spec)
+    rg = O.RefGraph.from_csr(g)
+    rng = np.random.default_rng(7)
+    for st in _sets_for(g, rng):
+        assert O.check_independence(g, st) == O.ref_check_independence(rg, st)
+        ind = O.check_independence(g, st)[0]
+        if ind:
+            assert O.check_maximality(g, st) == O.ref_check_maximality(rg, st)
+        else:
+            with pytest.raises(ValueError):
+                O.check_maximality(g, st)
+            with pytest.raises(ValueError):
+                O.ref_check_maximality(rg, st)
+    with pytest.raises(ValueError):
+        O.check_independence(g, np.array([g.n], np.int32))
+    with pytest.raises(ValueError):
+        O.ref_check_independence(rg, np.array([g.n], np.int32))
