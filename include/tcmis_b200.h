@@ -259,6 +259,11 @@ int tcmis_tiled_spmv(tcmis_graph *g, int32_t tile_dim, const uint8_t *candidates
 int tcmis_gen_rmat(tcmis_ctx *ctx, int32_t scale, int32_t edge_factor, uint64_t seed,
                    tcmis_graph **out);
 int tcmis_gen_grid(tcmis_ctx *ctx, int32_t side, tcmis_graph **out);
+/* graph.cpp:14-41 graph_from_edges on the device: the m edges
+ * (u[i], v[i]) symmetrised, self-loops dropped, duplicates merged, rows
+ * sorted; an endpoint outside [0, n) -> TCMIS_E_OUT_OF_RANGE. */
+int tcmis_graph_from_edges(tcmis_ctx *ctx, int32_t n, int64_t m, const int32_t *u,
+                           const int32_t *v, tcmis_graph **out);
 int tcmis_gen_rgg(tcmis_ctx *ctx, int32_t n, uint64_t radius, uint64_t seed,
                   tcmis_graph **out);
 /* Host-side G(n,p) (generate.cpp:30-66): serial by definition (one RNG

@@ -143,6 +143,7 @@ def load():
         "tcmis_tiled_spmv": (C.c_int, [vp, i32, vp, i32, vp, P(i64), P(i64)]),
         "tcmis_gen_rmat": (C.c_int, [vp, i32, i32, u64, P(vp)]),
         "tcmis_gen_grid": (C.c_int, [vp, i32, P(vp)]),
+        "tcmis_graph_from_edges": (C.c_int, [vp, i32, i64, vp, vp, P(vp)]),
         "tcmis_gen_rgg": (C.c_int, [vp, i32, u64, u64, P(vp)]),
         "tcmis_gen_gnp_host": (C.c_int, [i32, C.c_double, u64, P(P(i64)), P(P(i32)), P(i64)]),
         "tcmis_free": (None, [vp]),
@@ -343,6 +344,17 @@ class DeviceGraph:
         h = C.c_void_p()
         _check(load().tcmis_gen_rmat(ctx.h, scale, edge_factor, seed, C.byref(h)))
         return cls(h, ctx)
+
+    @classmethod
+    def from_edges(cls, n: int, edges, ctx: Optional[Context] = None) -> "DeviceGraph":
+        """graph_from_edges (graph.cpp:14-41) normalised on the device."""
+        ctx = ctx or default_context()
+        e = np.asarray(edges, dtype=np.int32).reshape(-1, 2)
+        eu, ev = np.ascontiguousarray(e[:, 0]), np.ascontiguousarray(e[:, 1])
+        h = C.c_void_p()
+        _check(load().tcmis_graph_from_edges(ctx.h, int(n), int(e.shape[0]), _ptr(eu), _ptr(ev),
+                                             C.byref(h)))
+        return cls(h, ctx, keepalive=(eu, ev))
 
     @classmethod
     def grid(cls, side: int, ctx: Optional[Context] = None) -> "DeviceGraph":

@@ -42,6 +42,8 @@ int neighbor_count_impl(tcmis_graph *g, const uint8_t *c, int32_t *nc, int T, in
                         int64_t *sk);
 int gen_rmat(tcmis_ctx *ctx, int32_t scale, int32_t ef, uint64_t seed, tcmis_graph **out);
 int gen_grid(tcmis_ctx *ctx, int32_t side, tcmis_graph **out);
+int gen_from_edges(tcmis_ctx *ctx, int32_t n, int64_t m, const int32_t *u, const int32_t *v,
+                   tcmis_graph **out);
 int gen_rgg(tcmis_ctx *ctx, int32_t n, uint64_t R, uint64_t seed, tcmis_graph **out);
 int gen_gnp_host(int32_t n, double avg_degree, uint64_t seed, int64_t **offsets,
                  int32_t **neighbors, int64_t *nnz_out);
@@ -482,6 +484,13 @@ TCMIS_API int tcmis_gen_rmat(tcmis_ctx *ctx, int32_t scale, int32_t ef, uint64_t
   NEED(ctx && out, "null handle");
   ENTER(ctx);
   return gen_rmat(ctx, scale, ef, seed, out);
+}
+
+TCMIS_API int tcmis_graph_from_edges(tcmis_ctx *ctx, int32_t n, int64_t m, const int32_t *u,
+                                     const int32_t *v, tcmis_graph **out) {
+  NEED(ctx && out && (m == 0 || (u && v)), "null handle");
+  ENTER(ctx);
+  return gen_from_edges(ctx, n, m, u, v, out);
 }
 
 TCMIS_API int tcmis_gen_grid(tcmis_ctx *ctx, int32_t side, tcmis_graph **out) {

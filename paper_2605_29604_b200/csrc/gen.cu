@@ -246,6 +246,98 @@ int gen_rmat(tcmis_ctx *ctx, int32_t scale, int32_t ef, uint64_t seed, tcmis_gra
   return wrap_owned(ctx, n, m, o, q, out);
 }
 
+namespace {
+
+// graph.cpp:14-41 graph_from_edges, step 1: both directions of every edge as
+// a (u << bits | v) key; self-loops become the sentinel (all ones), which
+// sorts last and is dropped after the unique pass
+__global__ void k_edge_keys(int bits, int32_t n, int64_t m, const int32_t *__restrict__ eu,
+                            const int32_t *__restrict__ ev,
+                            unsigned long long *__restrict__ keys, int *__restrict__ bad) {
+  const unsigned long long sentinel = (bits >= 32) ? ~0ull : ((1ull << (2 * bits)) - 1);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = eu[e], v = ev[e];
+    if (u < 0 || u >= n || v < 0 || v >= n) {
+      atomicExch(bad, 1);
+      keys[2 * e] = keys[2 * e + 1] = sentinel;
+    } else if (u == v) {
+      keys[2 * e] = keys[2 * e + 1] = sentinel;
+    } else {
+      keys[2 * e] = ((unsigned long long)u << bits) | (unsigned)v;
+      keys[2 * e + 1] = ((unsigned long long)v << bits) | (unsigned)u;
+    }
+  }
+}
+
+}  // namespace
+
+// graph_from_edges (graph.cpp:14-41: symmetrise, drop
+// self-loops, dedup, CSR with sorted rows) on the device -- radix sort +
+// unique over 2*ceil(log2 n)-bit keys, the same pipeline as the R-MAT
+// generator.  An endpoint outside [0, n) -> std::out_of_range (graph.cpp:23-24).
+int gen_from_edges(tcmis_ctx *ctx, int32_t n, int64_t m, const int32_t *h_u, const int32_t *h_v,
+                   tcmis_graph **out) {
+  if (n < 0 || m < 0) return set_error(TCMIS_E_INVALID_ARGUMENT, "negative size");
+  cudaStream_t st = ctx->stream;
+  int bits = 1;
+  while (bits < 31 && (1ll << bits) < (int64_t)n) ++bits;
+  const int64_t nk = 2 * m;
+  DevBuf<int32_t> du, dv;
+  DevBuf<unsigned long long> a, b;
+  DevBuf<int> bad;
+  if (int rc = du.alloc((size_t)m)) return rc;
+  if (int rc = dv.alloc((size_t)m)) return rc;
+  if (int rc = a.alloc((size_t)nk)) return rc;
+  if (int rc = b.alloc((size_t)nk)) return rc;
+  if (int rc = bad.alloc(1)) return rc;
+  TCMIS_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+  if (m) {
+    TCMIS_CUDA(cudaMemcpyAsync(du.p, h_u, 4ull * m, cudaMemcpyHostToDevice, st));
+    TCMIS_CUDA(cudaMemcpyAsync(dv.p, h_v, 4ull * m, cudaMemcpyHostToDevice, st));
+    k_edge_keys<<<grid_for(ctx, m, 256, 16), 256, 0, st>>>(bits, n, m, du.p, dv.p, a.p, bad.p);
+    TCMIS_LAUNCHED(ctx);
+  }
+  int h_bad = 0;
+  TCMIS_CUDA(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  if (h_bad) return set_error(TCMIS_E_OUT_OF_RANGE, "edge endpoint outside [0, n)");
+  int64_t mm = 0;
+  if (nk) {
+    size_t bytes = 0;
+    TCMIS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, a.p, b.p, nk, 0, 2 * bits, st));
+    DevBuf<char> tmp;
+    if (int rc = tmp.alloc(bytes)) return rc;
+    TCMIS_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, bytes, a.p, b.p, nk, 0, 2 * bits, st));
+    DevBuf<int64_t> d_m;
+    if (int rc = d_m.alloc(1)) return rc;
+    size_t ub = 0;
+    TCMIS_CUDA(cub::DeviceSelect::Unique(nullptr, ub, b.p, a.p, d_m.p, nk, st));
+    DevBuf<char> tmp2;
+    if (int rc = tmp2.alloc(ub)) return rc;
+    TCMIS_CUDA(cub::DeviceSelect::Unique(tmp2.p, ub, b.p, a.p, d_m.p, nk, st));
+    ctx->launches += 2;
+    TCMIS_CUDA(cudaMemcpyAsync(&mm, d_m.p, 8, cudaMemcpyDeviceToHost, st));
+    TCMIS_CUDA(cudaStreamSynchronize(st));
+    if (mm > 0) {
+      unsigned long long last = 0;
+      TCMIS_CUDA(cudaMemcpy(&last, a.p + (mm - 1), 8, cudaMemcpyDeviceToHost));
+      const unsigned long long sentinel = (1ull << (2 * bits)) - 1;
+      if (last == sentinel) --mm;
+    }
+  }
+  DevBuf<int64_t> off;
+  DevBuf<int32_t> nbr;
+  if (int rc = off.alloc((size_t)n + 1)) return rc;
+  if (int rc = nbr.alloc((size_t)mm)) return rc;
+  k_keys_to_csr<<<grid_for(ctx, mm + 1, 256, 16), 256, 0, st>>>(bits, n, mm, a.p, off.p, nbr.p);
+  TCMIS_LAUNCHED(ctx);
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  int64_t *o = off.release();
+  int32_t *q = nbr.release();
+  return wrap_owned(ctx, n, mm, o, q, out);
+}
+
 int gen_grid(tcmis_ctx *ctx, int32_t side, tcmis_graph **out) {
   if (side < 0 || (int64_t)side * side > 0x7fffffffLL)
     return set_error(TCMIS_E_INVALID_ARGUMENT, "grid side out of range");

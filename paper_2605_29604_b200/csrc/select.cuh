@@ -37,6 +37,7 @@ namespace tcmis_b200 {
 #define TCMIS_SEL_MINB 8
 #endif
 
+
 struct SelectArgs {
   int32_t n1;              // round-1 list length (non-isolated vertices)
   const int32_t *nz;       // round-1 list
@@ -155,11 +156,19 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
   while (__any_sync(0xffffffffu, mode != kDone)) {
     bool defer = false;
     if (mode == kScan) {
-      int32_t u[4];
-      const int64_t w = load_window_down(nbr, a.vnnz, s, hi, u);
+      // two 16-byte windows per step: 8 entries and their q gathers in flight
+      int32_t u[8];
+      int64_t w = load_window_down(nbr, a.vnnz, s, hi, u);
+#if TCMIS_SEL_WIN2
+      if (w > s) w = load_window_down(nbr, a.vnnz, s, w, u + 4);
+      else u[4] = u[5] = u[6] = u[7] = -1;
+      constexpr int kU = 8;
+#else
+      constexpr int kU = 4;
+#endif
       bool blocked = false;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < kU; ++j)
         if (u[j] >= 0) blocked |= blocks(q, prio, u[j], qv, v);
       hi = w;
       if (blocked) {

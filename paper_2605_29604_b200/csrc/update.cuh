@@ -223,11 +223,18 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
   while (__any_sync(0xffffffffu, mode != kDone)) {
     bool survive = false, defer = false;
     if (mode == kScan) {
-      int32_t u[4];
-      const int64_t w = load_window_down(nbr, a.vnnz, s, hi, u);
+      int32_t u[8];
+      int64_t w = load_window_down(nbr, a.vnnz, s, hi, u);
+#if TCMIS_SEL_WIN2
+      if (w > s) w = load_window_down(nbr, a.vnnz, s, w, u + 4);
+      else u[4] = u[5] = u[6] = u[7] = -1;
+      constexpr int kU = 8;
+#else
+      constexpr int kU = 4;
+#endif
       bool hit = false;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < kU; ++j)
         if (u[j] >= 0) hit |= next[u[j]] == 1;
       hi = w;
       if (hit) {

@@ -500,3 +500,23 @@ def test_device_validator_on_rmat22(ctx):
     assert tc.check_independence(dg, res.mis) == (True, None)
     assert tc.check_maximality(dg, res.mis) == (True, None)
     assert tc.check_maximality(dg, res.mis[1:])[0] is False
+
+
+def test_graph_from_edges_on_device(ctx):
+    """graph_from_edges (graph.cpp:14-41) normalised on the
+    device -- symmetrised, loops dropped, duplicates merged, rows sorted --
+    equals the reference restatement; out-of-range endpoints raise."""
+    rng = np.random.default_rng(11)
+    for n, m in ((1, 3), (7, 0), (1000, 5000), (70_000, 400_000), (1 << 17, 300_000)):
+        e = rng.integers(0, n, size=(m, 2), dtype=np.int32)
+        if m:
+            e[: m // 10, 1] = e[: m // 10, 0]                         # self-loops
+            e = np.concatenate([e, np.ascontiguousarray(e[m // 10: m // 5, ::-1])])  # reversed dups
+        dg = tc.DeviceGraph.from_edges(n, e, ctx)
+        want = O.graph_from_edges(n, e)
+        h = dg.download()
+        assert h.n == want.n
+        assert np.array_equal(h.offsets, want.off)
+        assert np.array_equal(h.neighbors, want.nbr)
+    with pytest.raises(IndexError):
+        tc.DeviceGraph.from_edges(10, np.array([[0, 10]], np.int32), ctx)
