@@ -16,6 +16,7 @@
 
 #include <cstdint>
 #include <functional>
+#include <iosfwd>
 #include <optional>
 #include <span>
 #include <utility>
@@ -114,6 +115,28 @@ struct TiledAdjacency {
 // K1 on the GPU (warp-per-block-row merge, tiles.cu); std::invalid_argument
 // unless 1 <= tile_dim <= 64.
 TiledAdjacency tile_graph(const Graph &g, int tile_dim);
+
+/// tiling.hpp:69 -- inverse of tile_graph: the source graph back from its tiles.
+Graph tiled_to_csr_roundtrip(const TiledAdjacency &a);
+
+/// tiling.hpp:71-78
+struct TileStats {
+  std::int64_t tile_count = 0;
+  std::int64_t total_nonzeros = 0;
+  std::vector<std::int64_t> occupancy_histogram;  // index = non-zeros per tile
+  double density = 0.0;                           // tile_count*T^2 / n_padded^2
+};
+TileStats tile_stats(const TiledAdjacency &a);
+
+/// tiling.hpp:80-86 -- the binary cache "TCMISTIL" (little endian): 8-byte
+/// magic, u32 version 1, u32 tile_dim, u64 n, u64 tile_count, then per tile
+/// u32 block_row, u32 block_col and ceil(T*T/8) payload bytes, row-major,
+/// bit k = entry (k/T, k%T), LSB-first.  read_tiled throws std::runtime_error
+/// on a bad magic / version / truncated or unsorted file.
+void write_tiled(std::ostream &out, const TiledAdjacency &a);
+TiledAdjacency read_tiled(std::istream &in);
+std::int64_t tiled_bytes_estimate(const TiledAdjacency &a);
+std::int64_t csr_bytes_estimate(const Graph &g);
 
 struct TiledVector {
   int tile_dim = 16;

@@ -198,6 +198,7 @@ def ref():
                                              C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         R.ref_check_maximality.argtypes = [C.c_void_p, i32p, C.c_int64, C.POINTER(C.c_int32),
                                            C.POINTER(C.c_int32)]
+        R.ref_write_tiled.argtypes = [C.c_void_p, C.c_int32, C.c_char_p]
         _ref = R
     return _ref
 
@@ -483,3 +484,10 @@ def ref_check_maximality(rg, mis_set):
     if rc:
         raise _ref_exc(rc)
     return bool(mx.value), (None if mx.value else a.value)
+
+
+def ref_write_tiled(rg, tile_dim: int, path: str) -> None:
+    """The reference's write_tiled(tile_graph(g, T)) into `path`."""
+    rc = ref().ref_write_tiled(rg.h, tile_dim, path.encode())
+    if rc:
+        raise _ref_exc(rc)

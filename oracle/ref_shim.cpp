@@ -6,6 +6,7 @@
 // cpu_baseline leg of bench.py call the reference exactly as a C++ user would
 // (tcmis::run_mis & co.).  No reference source is copied into this repo.
 #include <chrono>
+#include <fstream>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -313,6 +314,19 @@ int ref_check_maximality(void* gh, const int32_t* set, int64_t cnt, int32_t* max
     auto r = tcmis::check_maximality(g, std::span<const tcmis::VertexId>(set, (size_t)cnt));
     *maximal = r.maximal ? 1 : 0;
     if (r.addable_vertex) *addable = *r.addable_vertex;
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+// tiling.cpp write_tiled of tile_graph(g, T) into `path` (format pin)
+int ref_write_tiled(void* gh, int32_t T, const char* path) {
+  try {
+    const auto& g = *static_cast<tcmis::Graph*>(gh);
+    auto a = tcmis::tile_graph(g, T);
+    std::ofstream f(path, std::ios::binary);
+    tcmis::write_tiled(f, a);
     return 0;
   } catch (...) {
     return code_of(std::current_exception());

@@ -16,6 +16,10 @@ constexpr int kThreadMax = 32; // entries a thread examines before handing a row
 #define TCMIS_WARP_U 8
 #endif
 constexpr int kWarpU = TCMIS_WARP_U;  // independent loads per lane per step of a warp-wide row scan
+#ifndef TCMIS_BLOCK_ROW
+#define TCMIS_BLOCK_ROW 65536
+#endif
+constexpr int64_t kBlockRow = TCMIS_BLOCK_ROW;  // long-row lists: rows beyond this are scanned block-wide
 
 // Loads of the CSR (offsets, neighbour ids): read once per phase, so they are
 // marked evict-first (ld.global.cs) and do not push the randomly gathered

@@ -7,6 +7,10 @@
 #include <cmath>
 #include <memory>
 #include <mutex>
+#include <bit>
+#include <istream>
+#include <ostream>
+#include <cstring>
 #include <stdexcept>
 
 #include "tcmis/tcmis.hpp"
@@ -211,6 +215,135 @@ TiledAdjacency tile_graph(const Graph &g, int tile_dim) {
   check(tcmis_graph_export_tiles(dg.h, tile_dim, a.tile_row.data(), a.tile_col.data(),
                                  a.row_bits.data(), a.block_row_offsets.data()));
   return a;
+}
+
+// ------------------------------------------------- tile persistence (f3)
+// Host-side utilities over the tiles tile_graph() exported from the device:
+// the reference's binary cache format (tiling.hpp:80-86), its roundtrip and
+// its statistics (tiling.cpp:103-228), restated from the header contract.
+
+Graph tiled_to_csr_roundtrip(const TiledAdjacency &a) {
+  std::vector<std::pair<VertexId, VertexId>> edges;
+  const int T = a.tile_dim;
+  for (std::int64_t t = 0; t < a.tile_count(); ++t) {
+    const VertexId r0 = a.tile_row[t] * T, c0 = a.tile_col[t] * T;
+    for (int i = 0; i < T; ++i)
+      for (std::uint64_t w = a.row_bits[t * T + i]; w; w &= w - 1) {
+        const VertexId v = r0 + i, u = c0 + std::countr_zero(w);
+        if (v < u) edges.emplace_back(v, u);  // the symmetric copy is the other tile's
+      }
+  }
+  return graph_from_edges(a.n, edges);
+}
+
+TileStats tile_stats(const TiledAdjacency &a) {
+  TileStats st;
+  const int T = a.tile_dim;
+  st.tile_count = a.tile_count();
+  st.occupancy_histogram.assign(static_cast<std::size_t>(T) * T + 1, 0);
+  for (std::int64_t t = 0; t < st.tile_count; ++t) {
+    std::int64_t nz = 0;
+    for (int i = 0; i < T; ++i) nz += std::popcount(a.row_bits[t * T + i]);
+    st.total_nonzeros += nz;
+    ++st.occupancy_histogram[static_cast<std::size_t>(nz)];
+  }
+  const double np = static_cast<double>(a.n_padded);
+  st.density = np > 0 ? static_cast<double>(st.tile_count) * T * T / (np * np) : 0.0;
+  return st;
+}
+
+namespace {
+constexpr char kTiledMagic[8] = {'T', 'C', 'M', 'I', 'S', 'T', 'I', 'L'};
+constexpr std::uint32_t kTiledVersion = 1;
+
+template <typename U>
+void put_le(std::ostream &out, U x) {
+  unsigned char b[sizeof(U)];
+  for (std::size_t i = 0; i < sizeof(U); ++i) b[i] = static_cast<unsigned char>(x >> (8 * i));
+  out.write(reinterpret_cast<const char *>(b), sizeof(U));
+}
+
+template <typename U>
+U get_le(std::istream &in) {
+  unsigned char b[sizeof(U)];
+  if (!in.read(reinterpret_cast<char *>(b), sizeof(U)))
+    throw std::runtime_error("truncated tiled file");
+  U x = 0;
+  for (std::size_t i = 0; i < sizeof(U); ++i) x |= static_cast<U>(b[i]) << (8 * i);
+  return x;
+}
+}  // namespace
+
+void write_tiled(std::ostream &out, const TiledAdjacency &a) {
+  const int T = a.tile_dim;
+  out.write(kTiledMagic, sizeof(kTiledMagic));
+  put_le<std::uint32_t>(out, kTiledVersion);
+  put_le<std::uint32_t>(out, static_cast<std::uint32_t>(T));
+  put_le<std::uint64_t>(out, static_cast<std::uint64_t>(a.n));
+  put_le<std::uint64_t>(out, static_cast<std::uint64_t>(a.tile_count()));
+  std::vector<unsigned char> pay(static_cast<std::size_t>((T * T + 7) / 8));
+  for (std::int64_t t = 0; t < a.tile_count(); ++t) {
+    put_le<std::uint32_t>(out, static_cast<std::uint32_t>(a.tile_row[t]));
+    put_le<std::uint32_t>(out, static_cast<std::uint32_t>(a.tile_col[t]));
+    std::fill(pay.begin(), pay.end(), 0);
+    for (int i = 0; i < T; ++i)
+      for (std::uint64_t w = a.row_bits[t * T + i]; w; w &= w - 1) {
+        const int k = i * T + std::countr_zero(w);
+        pay[k >> 3] |= static_cast<unsigned char>(1u << (k & 7));
+      }
+    out.write(reinterpret_cast<const char *>(pay.data()), static_cast<std::streamsize>(pay.size()));
+  }
+  if (!out) throw std::runtime_error("failed writing tiled file");
+}
+
+TiledAdjacency read_tiled(std::istream &in) {
+  char magic[8];
+  if (!in.read(magic, sizeof(magic)) || std::memcmp(magic, kTiledMagic, sizeof(magic)) != 0)
+    throw std::runtime_error("not a tiled adjacency file");
+  if (get_le<std::uint32_t>(in) != kTiledVersion)
+    throw std::runtime_error("unsupported tiled file version");
+  const int T = static_cast<int>(get_le<std::uint32_t>(in));
+  check_tile_dim(T);
+  TiledAdjacency a;
+  a.tile_dim = T;
+  a.n = static_cast<VertexId>(get_le<std::uint64_t>(in));
+  const std::uint64_t tiles = get_le<std::uint64_t>(in);
+  const std::int32_t nb = static_cast<std::int32_t>((static_cast<std::int64_t>(a.n) + T - 1) / T);
+  a.n_padded = nb * T;
+  a.block_row_offsets.assign(static_cast<std::size_t>(nb) + 1, 0);
+  std::vector<unsigned char> pay(static_cast<std::size_t>((T * T + 7) / 8));
+  std::int32_t pr = -1, pc = -1;
+  for (std::uint64_t t = 0; t < tiles; ++t) {
+    const auto br = static_cast<std::int32_t>(get_le<std::uint32_t>(in));
+    const auto bc = static_cast<std::int32_t>(get_le<std::uint32_t>(in));
+    if (br < 0 || bc < 0 || br >= nb || bc >= nb)
+      throw std::runtime_error("tile coordinates out of range");
+    if (br < pr || (br == pr && bc <= pc))
+      throw std::runtime_error("tiles not sorted by (block_row, block_col)");
+    pr = br;
+    pc = bc;
+    if (!in.read(reinterpret_cast<char *>(pay.data()), static_cast<std::streamsize>(pay.size())))
+      throw std::runtime_error("truncated tiled file");
+    a.tile_row.push_back(br);
+    a.tile_col.push_back(bc);
+    const std::size_t base = a.row_bits.size();
+    a.row_bits.resize(base + static_cast<std::size_t>(T), 0);
+    for (int k = 0; k < T * T; ++k)
+      if ((pay[k >> 3] >> (k & 7)) & 1u) a.row_bits[base + k / T] |= std::uint64_t{1} << (k % T);
+    a.block_row_offsets[static_cast<std::size_t>(br) + 1] = static_cast<std::int64_t>(t) + 1;
+  }
+  for (std::int32_t b = 0; b < nb; ++b)  // block rows without tiles
+    a.block_row_offsets[b + 1] = std::max(a.block_row_offsets[b + 1], a.block_row_offsets[b]);
+  return a;
+}
+
+std::int64_t tiled_bytes_estimate(const TiledAdjacency &a) {
+  return 24 + a.tile_count() * (8 + (a.tile_dim * a.tile_dim + 7) / 8);
+}
+
+std::int64_t csr_bytes_estimate(const Graph &g) {
+  return static_cast<std::int64_t>((static_cast<std::size_t>(g.n) + 1) * sizeof(EdgeIndex) +
+                                   g.neighbors.size() * sizeof(VertexId));
 }
 
 TiledVector pack_vector(std::span<const std::uint8_t> values, int tile_dim) {

@@ -62,6 +62,8 @@ struct Ctrl {
   int32_t tail_cnt[3];   // k_tail list lengths, by round mod 3 (tail.cuh)
   int32_t sel_undec;   // rows k_probe_select left to the k_select engine
   int32_t pull_undec;  // rows k_probe_pull left to the k_update_pull engine
+  int32_t sel_vlong;   // select rows longer than kBlockRow (block-wide in k_select_long)
+  int32_t pull_vlong;  // pull rows longer than kBlockRow (block-wide in k_round_end)
 };
 
 struct Workspace {
@@ -77,6 +79,8 @@ struct Workspace {
   int32_t *mis = nullptr;
   int32_t *long_list = nullptr;   // select: rows that outlived the thread probe
   int32_t *long_list2 = nullptr;  // pull exclusion: same, for k_round_end
+  int32_t *vlong = nullptr;       // rows beyond kBlockRow: [0, cap) select, [cap, 2 cap) pull
+  int64_t vlong_cap = 0;
   int32_t *check = nullptr;       // pull exclusion: this round's non-candidates
   int32_t *undec_sel = nullptr;   // probe leftovers for the select engine
   int32_t *undec_pull = nullptr;  // probe leftovers for the pull engine

@@ -55,6 +55,7 @@ struct SelectArgs {
   Ctrl *ctrl;
   const int32_t *wl0, *wl1;
   int32_t *long_list;      // rows outliving the thread probe (ctrl->long_count)
+  int32_t *vlong;          // ... longer than kBlockRow (ctrl->sel_vlong)
   int32_t *undecided;      // rows the probe could not settle (ctrl->sel_undec)
   Publish pub;             // multi-GPU: this round's candidates of the own range
 };
@@ -192,7 +193,9 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
       hi = p;
       if (hi >= e) mode = kFetch;
     }
-    warp_append(defer, v, a.long_list, &ctrl->long_count);
+    const bool vl = defer && e - s > kBlockRow;
+    warp_append(defer && !vl, v, a.long_list, &ctrl->long_count);
+    warp_append(vl, v, a.vlong, &ctrl->sel_vlong);
     if (mode == kFetch) fetch();
   }
   block_add3(sel, 0, 0, ctrl);
@@ -200,12 +203,13 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
 
 __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
   Ctrl *ctrl = a.ctrl;
-  const int cnt = ctrl->long_count;
-  if ((int64_t)blockIdx.x * (kBlock / 32) >= cnt) return;
+  const int cnt = ctrl->long_count, nvl = ctrl->sel_vlong;
+  if ((int64_t)blockIdx.x * (kBlock / 32) >= cnt && blockIdx.x >= nvl) return;
   const int lane = threadIdx.x & 31;
   const int32_t *__restrict__ nbr = a.nbr;
   const uint32_t *__restrict__ prio = a.prio;
   unsigned long long sel = 0;
+  // one warp per row; rows longer than kBlockRow by the whole block below
   for (int64_t q = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5; q < cnt;
        q += ((int64_t)gridDim.x * kBlock) >> 5) {
     const int32_t v = a.long_list[q];
@@ -237,6 +241,32 @@ __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
       }
       if (a.push)
         for (int64_t idx = s + lane; idx < e; idx += 32) exclude(a.next, __ldg(&nbr[idx]));
+    }
+  }
+  for (int64_t q = blockIdx.x; q < nvl; q += gridDim.x) {
+    const int32_t v = a.vlong[q];
+    const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
+    const uint32_t qv = __ldg(&a.q[v]);
+    int64_t hi = e - (kThreadMax - 3);
+    bool blocked = false;
+    while (!blocked && hi > s) {
+      bool b = false;
+#pragma unroll
+      for (int j = 0; j < kWarpU; ++j) {
+        const int64_t idx = hi - 1 - threadIdx.x - (int64_t)kBlock * j;
+        if (idx >= s) b |= blocks(a.q, prio, ld_stream(&nbr[idx]), qv, v);
+      }
+      blocked = __syncthreads_or(b) != 0;
+      hi -= (int64_t)kBlock * kWarpU;
+    }
+    if (!blocked) {
+      if (threadIdx.x == 0) {
+        mark_candidate(v, a.next, a.state, a.segflag, a.T);
+        publish(a.pub, v);
+        ++sel;
+      }
+      if (a.push)
+        for (int64_t idx = s + threadIdx.x; idx < e; idx += kBlock) exclude(a.next, __ldg(&nbr[idx]));
     }
   }
   block_add3(sel, 0, 0, ctrl);

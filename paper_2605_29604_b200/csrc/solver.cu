@@ -281,6 +281,7 @@ void free_workspace(Workspace &ws) {
   dev_free(ws.mis);
   dev_free(ws.long_list);
   dev_free(ws.long_list2);
+  dev_free(ws.vlong);
   dev_free(ws.check);
   dev_free(ws.undec_sel);
   dev_free(ws.undec_pull);
@@ -328,7 +329,7 @@ int ensure_workspace(tcmis_graph *g) {
   dev_free(ws.q);
     dev_free(ws.state);
     dev_free(ws.next);
-  dev_free(ws.xm);
+    dev_free(ws.xm);
     dev_free(ws.wl[0]);
     dev_free(ws.wl[1]);
     dev_free(ws.mis);
@@ -359,6 +360,20 @@ int ensure_workspace(tcmis_graph *g) {
     if (int rc = dev_alloc(&ws.tile_hit, n / 16 + 2)) return rc;
     TCMIS_CUDA(cudaMemsetAsync(ws.next, 0, n, g->ctx->stream));
     ws.n_cap = n;
+  }
+  {  // at most nnz / kBlockRow rows are longer than kBlockRow (per graph)
+    const int64_t need = std::min<int64_t>((int64_t)n, g->nnz / kBlockRow + 1);
+    if (ws.vlong_cap < need) {
+      if (ws.exec) {  // the cached round graph points at the old lists
+        cudaGraphExecDestroy(ws.exec);
+        ws.exec = nullptr;
+      }
+      dev_free(ws.vlong);
+      ws.vlong = nullptr;
+      ws.vlong_cap = 0;
+      if (int rc = dev_alloc(&ws.vlong, 2 * (size_t)need)) return rc;
+      ws.vlong_cap = need;
+    }
   }
   // segment flags for any tile_dim >= 1
   if (ws.seg_cap < n) {
@@ -504,6 +519,7 @@ SelectArgs select_args(tcmis_graph *g, const RoundArgs &a) {
   s.wl0 = ws.wl[0];
   s.wl1 = ws.wl[1];
   s.long_list = ws.long_list;
+  s.vlong = ws.vlong;
   s.undecided = ws.undec_sel;
   s.pub = Publish{a.pub_cand, a.pub_lo};
   if (a.tile) s.pub = Publish{ws.cbits, 0};  // the candidate segments of the tile kernels
@@ -530,6 +546,7 @@ UpdateArgs update_args(tcmis_graph *g, const RoundArgs &a) {
   u.nz = a.nz;
   u.nz_identity = a.nz_count == a.n ? 1 : 0;
   u.long_list = ws.long_list2;
+  u.vlong = ws.vlong + ws.vlong_cap;
   u.undecided = ws.undec_pull;
   u.pub = Publish{a.pub_dead, a.pub_lo};
   u.segflag = ws.segflag;

@@ -55,6 +55,7 @@ struct UpdateArgs {
   const int32_t *nz;
   int nz_identity;
   int32_t *long_list;      // pull: rows outliving the thread probe (ctrl->pull_count)
+  int32_t *vlong;          // ... longer than kBlockRow (ctrl->pull_vlong)
   int32_t *undecided;      // pull: rows the probe could not settle (ctrl->pull_undec)
   Publish pub;             // multi-GPU: this round's removals of the own range
   const uint32_t *tile_hit;  // tile exclusion: per T=16 block row, rows with a candidate nbr
@@ -252,7 +253,9 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
       }
     }
     warp_emit(wo, survive, v, out, tail);
-    warp_append(defer, v, a.long_list, &ctrl->pull_count);
+    const bool vl = defer && e - s > kBlockRow;
+    warp_append(defer && !vl, v, a.long_list, &ctrl->pull_count);
+    warp_append(vl, v, a.vlong, &ctrl->pull_vlong);
     if (mode == kFetch) fetch();
   }
   warp_flush(wo, out, tail);
@@ -272,8 +275,20 @@ __global__ void __launch_bounds__(kBlock)
   const int32_t *__restrict__ nbr = a.nbr;
   const uint8_t *__restrict__ next = a.next;
   unsigned long long rem = 0, ev = 0;
-  // pull rows longer than the thread probe: one warp per row
+  // pull rows longer than the thread probe: one warp per row, rows longer
+  // than kBlockRow by the whole block (a survivor must scan its entire row,
+  // and one warp walks 256 entries per dependent step)
   const int nl = ctrl->pull_count;
+  auto decide = [&](int32_t v, bool hit) {
+    if (hit) {
+      mark_removed(v, a.state, a.q);
+      publish(a.pub, v);
+      ++rem;
+    } else {
+      if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m);
+      out[atomicAdd(&ctrl->wl_count[out_slot], 1)] = v;
+    }
+  };
   for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nl;
        q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int32_t v = a.long_list[q];
@@ -294,16 +309,25 @@ __global__ void __launch_bounds__(kBlock)
       hit = __any_sync(0xffffffffu, b);
       hi -= 32 * kWarpU;
     }
-    if (lane == 0) {
-      if (hit) {
-        mark_removed(v, a.state, a.q);
-        publish(a.pub, v);
-        ++rem;
-      } else {
-        if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m);
-        out[atomicAdd(&ctrl->wl_count[out_slot], 1)] = v;
+    if (lane == 0) decide(v, hit);
+  }
+  const int nvl = ctrl->pull_vlong;
+  for (int64_t q = blockIdx.x; q < nvl; q += gridDim.x) {
+    const int32_t v = a.vlong[q];
+    const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
+    int64_t hi = e - kThreadMax;
+    bool hit = false;
+    while (!hit && hi > s) {
+      bool b = false;
+#pragma unroll
+      for (int j = 0; j < kWarpU; ++j) {
+        const int64_t idx = hi - 1 - threadIdx.x - (int64_t)kBlock * j;
+        if (idx >= s) b |= next[ld_stream(&nbr[idx])] == 1;
       }
+      hit = __syncthreads_or(b) != 0;
+      hi -= (int64_t)kBlock * kWarpU;
     }
+    if (threadIdx.x == 0) decide(v, hit);
   }
   if (a.seg_mode == 1) {  // spmv.cpp:37-46, per block column (A is symmetric)
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < a.nseg;
@@ -343,6 +367,8 @@ __global__ void __launch_bounds__(kBlock)
     vc->wl_count[round & 1] = 0;
     vc->long_count = 0;
     vc->pull_count = 0;
+    vc->sel_vlong = 0;
+    vc->pull_vlong = 0;
     vc->sel_undec = 0;
     vc->pull_undec = 0;
     vc->main_rounds = vc->main_rounds + 1;

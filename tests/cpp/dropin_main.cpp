@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <fstream>
 #include <stdexcept>
+#include <sstream>
 #include <string>
 
 #include "tcmis/engine.hpp"
@@ -83,6 +84,32 @@ int main(int argc, char **argv) {
   std::printf("{\"tiles8\": %lld, \"t8_rounds\": %zu, \"t8_eval1\": %lld}\n",
               (long long)t8.tile_count(), r8.iterations.size(),
               (long long)(r8.iterations.empty() ? 0 : r8.iterations[0].tiles_evaluated));
+  // tiling.hpp persistence: binary cache write -> read,
+  // roundtrip to CSR, statistics
+  {
+    TiledAdjacency t16 = tile_graph(g, 16);
+    const std::string path = std::string(argv[1]) + ".t16";
+    {
+      std::ofstream f(path, std::ios::binary);
+      write_tiled(f, t16);
+    }
+    std::ifstream f(path, std::ios::binary);
+    TiledAdjacency back = read_tiled(f);
+    const bool same = back.tile_row == t16.tile_row && back.tile_col == t16.tile_col &&
+                      back.row_bits == t16.row_bits &&
+                      back.block_row_offsets == t16.block_row_offsets && back.n == t16.n;
+    Graph rt = tiled_to_csr_roundtrip(t16);
+    const bool rt_ok = rt.offsets == g.offsets && rt.neighbors == g.neighbors;
+    TileStats ts = tile_stats(t16);
+    std::printf("{\"tiled_io\": %d, \"roundtrip\": %d, \"nonzeros\": %lld, \"hist0\": %lld, "
+                "\"bytes_est\": %lld, \"csr_est\": %lld}\n",
+                same ? 1 : 0, rt_ok ? 1 : 0, (long long)ts.total_nonzeros,
+                (long long)ts.occupancy_histogram[0], (long long)tiled_bytes_estimate(t16),
+                (long long)csr_bytes_estimate(g));
+    std::stringstream bad("NOTTILED........");
+    std::printf("{\"bad_magic\": \"%s\"}\n",
+                throws<std::runtime_error>([&] { read_tiled(bad); }));
+  }
   // validate.hpp on the device: the H2 result, and the result minus its
   // first vertex (no longer maximal)
   {

@@ -58,6 +58,16 @@ def test_cpp_dropin_matches_reference(dropin, kind, args):
         want_obs = {"h1": exp.n_rounds, "h2": exp.n_rounds, "h3": 1, "luby-fresh": 0,
                     "luby-perm": 0}[r["heuristic"]]
         assert r["observed"] == want_obs
+    tio = [x for x in lines if "tiled_io" in x][0]
+    assert (tio["tiled_io"], tio["roundtrip"]) == (1, 1)
+    assert tio["nonzeros"] == g.nbr.size
+    assert tio["csr_est"] == 8 * (g.n + 1) + 4 * g.nbr.size
+    assert [x for x in lines if "bad_magic" in x][0]["bad_magic"] == "yes"
+    if O.ref_available():  # byte-identical to the reference's own cache file
+        ref_path = path + ".ref.t16"
+        O.ref_write_tiled(O.RefGraph.from_csr(g), 16, ref_path)
+        with open(path + ".t16", "rb") as a, open(ref_path, "rb") as b:
+            assert a.read() == b.read()
     val = [x for x in lines if "valid_ind" in x][0]
     exp2 = O.solve(g, "h2", 1, tile_dim=16)
     mis2 = np.flatnonzero(exp2.state == 1)
