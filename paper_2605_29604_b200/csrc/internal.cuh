@@ -66,6 +66,14 @@ struct Ctrl {
   int32_t pull_vlong;  // pull rows longer than kBlockRow (block-wide in k_round_end)
 };
 
+// What the whole-solve graph leaves in mapped pinned host memory (k_pack):
+// the host reads it after one stream synchronisation, no copies.
+struct HostRes {
+  Ctrl ctrl;
+  long long mis_count;
+  DevRound rounds[64];
+};
+
 struct Workspace {
   size_t n_cap = 0;
   size_t seg_cap = 0;
@@ -91,6 +99,8 @@ struct Workspace {
   Ctrl *ctrl = nullptr;        // device
   Ctrl *h_ctrl = nullptr;      // pinned host mirror
   int64_t *h_misc = nullptr;   // pinned: [0] MIS count, [1] h3 tiles evaluated
+  HostRes *h_res = nullptr;    // mapped pinned (cudaHostAllocMapped)
+  HostRes *d_res = nullptr;    // its device alias
   DevRound *rounds = nullptr;  // device, capacity round_cap
   DevRound *h_rounds = nullptr;
   int32_t round_cap = 0;
@@ -99,7 +109,7 @@ struct Workspace {
   cudaGraphExec_t exec = nullptr;  // cached WHILE{select; update} graph
   uint32_t *cbits = nullptr;      // tile exclusion: this round's candidates, bit per vertex
   uint32_t *tile_hit = nullptr;   // tile exclusion: per T=16 block row, rows with a candidate nbr
-  alignas(8) unsigned char graph_key[256] = {};
+  alignas(8) unsigned char graph_key[512] = {};
 };
 
 }  // namespace tcmis_b200
@@ -241,7 +251,8 @@ int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle
 int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
                       uint32_t *p_out, uint16_t *q_out, uint8_t *state, uint8_t *next,
                       uint8_t *segflag = nullptr, int T = 1, uint8_t *xm0 = nullptr,
-                      uint8_t *xm1 = nullptr);
+                      uint8_t *xm1 = nullptr, Ctrl *ctrl = nullptr, const Ctrl *ctrl0 = nullptr,
+                      DevRound *rounds = nullptr, int32_t nrounds = 0);
 // offset of k_tail's odd exclusion plane in Workspace::xm (16-byte aligned)
 inline size_t xm_stride(const Workspace &ws) { return (ws.n_cap + 15) / 16 * 16; }
 double avg_degree(const tcmis_graph *g);

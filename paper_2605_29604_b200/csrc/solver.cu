@@ -59,7 +59,15 @@ __global__ void __launch_bounds__(256)
                  uint64_t mseed, double avg, double scale, uint32_t *__restrict__ p_out,
                  uint16_t *__restrict__ q_out, int qshift, uint8_t *__restrict__ state,
                  uint8_t *__restrict__ next, uint8_t *__restrict__ xm0, uint8_t *__restrict__ xm1,
-                 uint8_t *__restrict__ segflag, int T, int tshift) {
+                 uint8_t *__restrict__ segflag, int T, int tshift, Ctrl *ctrl, Ctrl ctrl0,
+                 DevRound *rounds, int32_t nrounds) {
+  // the solve's control block and (for k_tail, which accumulates into it)
+  // the zeroed statistics ring: no separate copy / memset on the stream
+  if (ctrl && blockIdx.x == 0 && threadIdx.x == 0) *ctrl = ctrl0;
+  if (rounds)
+    for (int32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nrounds;
+         r += gridDim.x * blockDim.x)
+      rounds[r] = DevRound{0, 0, 0, 0, 0};
   const int32_t quads = (int32_t)(((int64_t)n + kPrioV - 1) / kPrioV);
   for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < quads;
        q += gridDim.x * blockDim.x) {
@@ -171,6 +179,18 @@ struct HasEdges {
 };
 
 // ----------------------------------------------------------------- rounds
+
+// The whole-solve graph's last node: control block, MIS count and the first
+// 64 rounds' statistics into mapped host memory (HostRes).
+__global__ void k_pack(const Ctrl *__restrict__ ctrl, const int64_t *__restrict__ mis_count,
+                       const DevRound *__restrict__ rounds, int32_t cap, HostRes *out) {
+  if (threadIdx.x == 0) {
+    out->ctrl = *ctrl;
+    out->mis_count = (long long)*mis_count;
+  }
+  for (int r = threadIdx.x; r < 64 && r < cap; r += blockDim.x) out->rounds[r] = rounds[r];
+  __threadfence_system();
+}
 
 // h3: tile counters of the single collapsed iteration (segments that hold
 // any MIS vertex).
@@ -292,6 +312,7 @@ void free_workspace(Workspace &ws) {
   dev_free(ws.ctrl);
   cudaFreeHost(ws.h_ctrl);
   cudaFreeHost(ws.h_misc);
+  cudaFreeHost(ws.h_res);
   dev_free(ws.rounds);
   cudaFreeHost(ws.h_rounds);
   dev_free(ws.cub_tmp);
@@ -390,6 +411,8 @@ int ensure_workspace(tcmis_graph *g) {
     TCMIS_CUDA(cudaMemsetAsync(ws.bar, 0, 2 * sizeof(unsigned), g->ctx->stream));
     TCMIS_CUDA(cudaMallocHost((void **)&ws.h_ctrl, sizeof(Ctrl)));
     TCMIS_CUDA(cudaMallocHost((void **)&ws.h_misc, 2 * sizeof(int64_t)));
+    TCMIS_CUDA(cudaHostAlloc((void **)&ws.h_res, sizeof(HostRes), cudaHostAllocMapped));
+    TCMIS_CUDA(cudaHostGetDevicePointer((void **)&ws.d_res, ws.h_res, 0));
     ws.round_cap = 4096;
     if (int rc = dev_alloc(&ws.rounds, (size_t)ws.round_cap)) return rc;
     TCMIS_CUDA(cudaMallocHost((void **)&ws.h_rounds, sizeof(DevRound) * ws.round_cap));
@@ -452,7 +475,8 @@ int q_shift(int heuristic, int scale_bits) {
 
 int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
                       uint32_t *p_out, uint16_t *q_out, uint8_t *state, uint8_t *next,
-                      uint8_t *segflag, int T, uint8_t *xm0, uint8_t *xm1) {
+                      uint8_t *segflag, int T, uint8_t *xm0, uint8_t *xm1, Ctrl *ctrl,
+                      const Ctrl *ctrl0, DevRound *rounds, int32_t nrounds) {
   tcmis_ctx *ctx = g->ctx;
   int mode = 1;
   uint64_t mseed = mix64(seed);
@@ -472,7 +496,8 @@ int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bi
                                                           mode ? avg_degree(g) : 0.0, scale,
                                                           p_out, q_out, q_shift(heuristic, scale_bits),
                                                           state, next, xm0, xm1, segflag, T,
-                                                          tshift)));
+                                                          tshift, ctrl, ctrl0 ? *ctrl0 : Ctrl{},
+                                                          rounds, nrounds)));
   TCMIS_LAUNCHED(ctx);
   return 0;
 }
@@ -664,53 +689,128 @@ int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle
 
 inline int launches_per_round(const RoundArgs &a) { return (a.pull || a.tile) ? 6 : 5; }
 
-// Instantiate (once per distinct argument set) the graph
-//   WHILE(cond) { k_select ; k_update }
+// The parameters of a solve's first kernels (segment-flag clear,
+// k_priorities with the control-block init), part of the graph's cache key.
+struct SolvePre {
+  int H;
+  uint64_t seed;
+  int scale_bits;
+  int T;
+  int seg_mode;
+  int32_t nseg;
+  Ctrl c0;
+};
+
+// Instantiate (once per distinct argument set) the whole-solve graph
+//   memset(segflag) -> k_priorities -> WHILE(cond) { select ; exclusion ; update }
+//     -> k_tail (rounds <= tail_thr + MIS compaction) | cub compaction
+//     -> [h3: tile total] -> k_pack (results into mapped host memory)
 // over this workspace's buffers.
-int ensure_round_graph(tcmis_graph *g, const RoundArgs &a) {
+int ensure_solve_graph(tcmis_graph *g, const RoundArgs &a, const SolvePre &pre) {
   Workspace &ws = g->ws;
-  static_assert(sizeof(RoundArgs) <= sizeof(ws.graph_key), "graph key too small");
-  if (ws.exec && std::memcmp(ws.graph_key, &a, sizeof(a)) == 0) return 0;
+  static_assert(sizeof(RoundArgs) + sizeof(SolvePre) <= sizeof(ws.graph_key), "graph key too small");
+  unsigned char key[sizeof(ws.graph_key)] = {};
+  std::memcpy(key, &a, sizeof(a));
+  std::memcpy(key + sizeof(a), &pre, sizeof(pre));
+  if (ws.exec && std::memcmp(ws.graph_key, key, sizeof(key)) == 0) return 0;
   if (ws.exec) {
     cudaGraphExecDestroy(ws.exec);
     ws.exec = nullptr;
   }
-  cudaStream_t st = g->ctx->stream;
+  tcmis_ctx *ctx = g->ctx;
+  const int64_t launches0 = ctx->launches;  // capture is not execution
+  cudaStream_t st = ctx->stream;
   cudaGraph_t graph = nullptr;
   TCMIS_CUDA(cudaGraphCreate(&graph, 0));
-  cudaGraphConditionalHandle cond;
-  TCMIS_CUDA(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
-  cudaGraphNodeParams p{};
-  p.type = cudaGraphNodeTypeConditional;
-  p.conditional.handle = cond;
-  p.conditional.type = cudaGraphCondTypeWhile;
-  p.conditional.size = 1;
-  cudaGraphNode_t node;
-  TCMIS_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &p));
-  cudaGraph_t body = p.conditional.phGraph_out[0];
-  TCMIS_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0,
-                                           cudaStreamCaptureModeRelaxed));
-  int rc = launch_select(g, a);
-  if (!rc) rc = launch_update(g, a, cond, 1);
+  int rc = 0;
+  cudaError_t e = cudaSuccess;
   cudaGraph_t captured = nullptr;
-  cudaError_t e = cudaStreamEndCapture(st, &captured);
-  if (!rc && e != cudaSuccess) rc = cuda_error(e, "cudaStreamEndCapture");
-  // then the persistent tail kernel finishes the small rounds
-  if (!rc && a.tail_thr > 0) {
-    e = cudaStreamBeginCaptureToGraph(st, graph, &node, nullptr, 1, cudaStreamCaptureModeRelaxed);
-    if (e != cudaSuccess) rc = cuda_error(e, "cudaStreamBeginCaptureToGraph(tail)");
-    if (!rc) rc = launch_tail(g, a);
+  // 1. the first kernels
+  e = cudaStreamBeginCaptureToGraph(st, graph, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+  if (e != cudaSuccess) rc = cuda_error(e, "cudaStreamBeginCaptureToGraph(pre)");
+  if (!rc) {
+    if (pre.seg_mode) {
+      e = cudaMemsetAsync(ws.segflag, 0, (size_t)pre.nseg, st);
+      if (e != cudaSuccess) rc = cuda_error(e, "memset(segflag)");
+    }
+    if (!rc)
+      rc = launch_priorities(g, pre.H, pre.seed, pre.scale_bits, ws.prio, ws.q, ws.state, ws.next,
+                             pre.seg_mode ? ws.segflag : nullptr, pre.T, ws.xm,
+                             ws.xm + xm_stride(ws), ws.ctrl, &pre.c0, ws.rounds, ws.round_cap);
     e = cudaStreamEndCapture(st, &captured);
-    if (!rc && e != cudaSuccess) rc = cuda_error(e, "cudaStreamEndCapture(tail)");
-    g->ctx->launches--;
+    if (!rc && e != cudaSuccess) rc = cuda_error(e, "cudaStreamEndCapture(pre)");
+  }
+  // the pre-part's leaf (k_priorities) is the node without dependents
+  cudaGraphNode_t leaf = nullptr;
+  if (!rc) {
+    size_t nn = 0;
+    cudaGraphGetNodes(graph, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    cudaGraphGetNodes(graph, nodes.data(), &nn);
+    for (cudaGraphNode_t nd : nodes) {
+      size_t nd_out = 0;
+      cudaGraphNodeGetDependentNodes(nd, nullptr, &nd_out);
+      if (nd_out == 0) leaf = nd;
+    }
+    if (!leaf) rc = set_error(TCMIS_E_CUDA, "solve graph: no leaf after the first kernels");
+  }
+  // 2. WHILE(cond) { select ; exclusion ; update }
+  cudaGraphConditionalHandle cond;
+  cudaGraphNode_t node = nullptr;
+  if (!rc) {
+    e = cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams p{};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = cond;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    if (e == cudaSuccess) e = cudaGraphAddNode(&node, graph, &leaf, 1, &p);
+    if (e != cudaSuccess) rc = cuda_error(e, "solve graph: WHILE node");
+    cudaGraph_t body = p.conditional.phGraph_out[0];
+    if (!rc) {
+      e = cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0,
+                                        cudaStreamCaptureModeRelaxed);
+      if (e != cudaSuccess) rc = cuda_error(e, "cudaStreamBeginCaptureToGraph(body)");
+    }
+    if (!rc) {
+      rc = launch_select(g, a);
+      if (!rc) rc = launch_update(g, a, cond, 1);
+      e = cudaStreamEndCapture(st, &captured);
+      if (!rc && e != cudaSuccess) rc = cuda_error(e, "cudaStreamEndCapture(body)");
+    }
+  }
+  // 3. tail + compaction, h3's tile total, and the result pack
+  if (!rc) {
+    e = cudaStreamBeginCaptureToGraph(st, graph, &node, nullptr, 1, cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) rc = cuda_error(e, "cudaStreamBeginCaptureToGraph(post)");
+    if (!rc) {
+      if (a.tail_thr > 0) {
+        rc = launch_tail(g, a);
+      } else {
+        thrust::counting_iterator<int32_t> ids(0);
+        size_t bytes = ws.cub_bytes;
+        e = cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count, (int)g->n,
+                                  IsInMIS{ws.state}, st);
+        if (e != cudaSuccess) rc = cuda_error(e, "MIS compaction");
+      }
+      if (!rc && pre.seg_mode == 2) {
+        cudaMemsetAsync(&ws.ctrl->eval, 0, sizeof(unsigned long long), st);
+        k_seg_total<<<grid_for(ctx, pre.nseg, 256, 4), 256, 0, st>>>(ws.segflag, g->d_rowtiles,
+                                                                     pre.nseg, ws.ctrl);
+      }
+      if (!rc)
+        k_pack<<<1, 64, 0, st>>>(ws.ctrl, ws.mis_count, ws.rounds, ws.round_cap, ws.d_res);
+      e = cudaStreamEndCapture(st, &captured);
+      if (!rc && e != cudaSuccess) rc = cuda_error(e, "cudaStreamEndCapture(post)");
+    }
   }
   if (!rc) {
     e = cudaGraphInstantiate(&ws.exec, graph, 0);
     if (e != cudaSuccess) rc = cuda_error(e, "cudaGraphInstantiate");
   }
   cudaGraphDestroy(graph);
-  g->ctx->launches -= launches_per_round(a);  // capture is not execution
-  if (!rc) std::memcpy(ws.graph_key, &a, sizeof(a));
+  ctx->launches = launches0;
+  if (!rc) std::memcpy(ws.graph_key, key, sizeof(key));
   return rc;
 }
 
@@ -803,20 +903,24 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   cfg = &cfg_local;
 
   if (timing) timeline_begin(ctx);
-  if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
   uint8_t *seg0 = seg_mode ? ws.segflag : nullptr;
-  if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio, ws.q, ws.state,
-                                 ws.next, seg0, T > 0 ? T : 1, ws.xm, ws.xm + xm_stride(ws)))
-    return rc;
   Ctrl c0{};
   c0.round = 1;
   c0.alive = g->n;
   c0.max_rounds = ws.round_cap;
   c0.sel = (unsigned long long)(g->n - g->nz_count);  // isolated: round-1 candidates
   *ws.h_ctrl = c0;
-  TCMIS_CUDA(cudaMemcpyAsync(ws.ctrl, ws.h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
-  // k_tail accumulates its rounds' counters into the ring (tail.cuh)
-  TCMIS_CUDA(cudaMemsetAsync(ws.rounds, 0, sizeof(DevRound) * ws.round_cap, st));
+  bool step = cfg->observer || timing || (cfg->flags & TCMIS_F_HOST_LOOP);
+  // the solve's first kernels: segment flags cleared, priorities, states, and
+  // the control block + zeroed statistics ring (k_tail accumulates into it)
+  auto launch_pre = [&]() -> int {
+    if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
+    return launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio, ws.q, ws.state, ws.next,
+                             seg0, T > 0 ? T : 1, ws.xm, ws.xm + xm_stride(ws), ws.ctrl, &c0,
+                             ws.rounds, ws.round_cap);
+  };
+  if (step)
+    if (int rc = launch_pre()) return rc;
 
   RoundArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -872,7 +976,6 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   std::vector<DevRound> rounds_h;
   std::vector<uint8_t> h_next, h_state, h_cand;
   std::vector<float> t1, t2, t3;  // per-round phase times (TCMIS_F_TIMING)
-  bool step = cfg->observer || timing || (cfg->flags & TCMIS_F_HOST_LOOP);
   int64_t h_mis_count = 0;
   unsigned long long h3_eval = 0;
   // ascending MIS ids (engine.cpp:293 sorts; ordered compaction needs no sort)
@@ -904,45 +1007,47 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   };
   bool finished = false;
   if (!step) {
-    // the whole round loop is one CUDA graph: a conditional WHILE node whose
-    // body is {select, exclusion, update}; k_round_end's last block writes the
-    // loop condition, so no host round trip happens between rounds.  The
-    // statistics, the MIS compaction and every read-back are enqueued behind
-    // it and waited for once.
-    if (int rc = ensure_round_graph(g, a)) return rc;
+    // the whole solve is one CUDA graph (ensure_solve_graph): priorities,
+    // a conditional WHILE node over {select, exclusion, update} whose loop
+    // condition k_round_end sets on the device, the persistent tail with the
+    // fused MIS compaction, and k_pack, which leaves the control block, the
+    // MIS count and the statistics in mapped host memory -- one launch, one
+    // synchronisation, no copies.
+    SolvePre pre{};
+    pre.H = H;
+    pre.seed = cfg->seed;
+    pre.scale_bits = cfg->scale_bits;
+    pre.T = T > 0 ? T : 1;
+    pre.seg_mode = seg_mode;
+    pre.nseg = nseg;
+    pre.c0 = c0;
+    if (int rc = ensure_solve_graph(g, a, pre)) return rc;
     TCMIS_CUDA(cudaGraphLaunch(ws.exec, st));
-    tail_compacted = a.tail_thr > 0;
-    ctx->launches += launches_per_round(a);  // per round, counted below
-    TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
-    const int pre = std::min(ws.round_cap, 64);
-    TCMIS_CUDA(cudaMemcpyAsync(ws.h_rounds, ws.rounds, sizeof(DevRound) * pre,
-                               cudaMemcpyDeviceToHost, st));
-    if (int rc = enqueue_finish()) return rc;
     TCMIS_CUDA(cudaStreamSynchronize(st));
-    if (ws.h_ctrl->overflow) {
+    const HostRes &hr = *ws.h_res;
+    *ws.h_ctrl = hr.ctrl;
+    if (hr.ctrl.overflow) {
       // more rounds than the on-device ring holds: redo step-wise, draining
       // the statistics every round (pathological inputs such as long paths)
       step = true;
       a.tail_thr = 0;
       tail_compacted = false;
-      if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
-      if (int rc = launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio, ws.q,
-                                     ws.state, ws.next, seg0, T > 0 ? T : 1, ws.xm,
-                                     ws.xm + xm_stride(ws)))
-        return rc;
       *ws.h_ctrl = c0;
-      TCMIS_CUDA(cudaMemcpyAsync(ws.ctrl, ws.h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
-      // k_tail accumulates its rounds' counters into the ring (tail.cuh)
-      TCMIS_CUDA(cudaMemsetAsync(ws.rounds, 0, sizeof(DevRound) * ws.round_cap, st));
+      if (int rc = launch_pre()) return rc;
     } else {
-      const int rr = ws.h_ctrl->round - 1;
-      const int mr = ws.h_ctrl->main_rounds;
-      ctx->launches += launches_per_round(a) * ((int64_t)mr - 1) + (rr > mr ? 1 : 0);
-      if (rr > pre)
-        TCMIS_CUDA(cudaMemcpy(ws.h_rounds + pre, ws.rounds + pre, sizeof(DevRound) * (rr - pre),
-                              cudaMemcpyDeviceToHost));
-      rounds_h.assign(ws.h_rounds, ws.h_rounds + rr);
-      read_finish();
+      const int rr = hr.ctrl.round - 1;
+      const int mr = hr.ctrl.main_rounds;
+      ctx->launches += 2 + launches_per_round(a) * (int64_t)mr + (seg_mode == 2 ? 1 : 0) +
+                       (a.tail_thr > 0 ? 1 : 1);
+      const int pre_n = std::min(rr, std::min(ws.round_cap, 64));
+      rounds_h.assign(hr.rounds, hr.rounds + pre_n);
+      if (rr > pre_n) {
+        rounds_h.resize(rr);
+        TCMIS_CUDA(cudaMemcpy(rounds_h.data() + pre_n, ws.rounds + pre_n,
+                              sizeof(DevRound) * (rr - pre_n), cudaMemcpyDeviceToHost));
+      }
+      h_mis_count = hr.mis_count;
+      h3_eval = seg_mode == 2 ? hr.ctrl.eval : 0ull;
       finished = true;
     }
   }
