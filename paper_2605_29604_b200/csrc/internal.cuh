@@ -57,7 +57,6 @@ struct Ctrl {
   int32_t overflow;    // set when rounds exceeded max_rounds
   int32_t long_count;  // entries of the select long-row list this round
   int32_t pull_count;  // entries of the pull long-row list this round
-  int32_t check_unused; // (was the select kernels' pull check list)
   int32_t main_rounds; // rounds run by the per-round kernels (the rest ran in k_tail)
   int32_t tail_cnt[3];   // k_tail list lengths, by round mod 3 (tail.cuh)
   int32_t sel_undec;   // rows k_probe_select left to the k_select engine
@@ -89,7 +88,6 @@ struct Workspace {
   int32_t *long_list2 = nullptr;  // pull exclusion: same, for k_round_end
   int32_t *vlong = nullptr;       // rows beyond kBlockRow: [0, cap) select, [cap, 2 cap) pull
   int64_t vlong_cap = 0;
-  int32_t *check = nullptr;       // pull exclusion: this round's non-candidates
   int32_t *undec_sel = nullptr;   // probe leftovers for the select engine
   int32_t *undec_pull = nullptr;  // probe leftovers for the pull engine
   uint32_t *segmark = nullptr;    // tail rounds: round that last counted a block column

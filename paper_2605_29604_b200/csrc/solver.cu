@@ -302,7 +302,6 @@ void free_workspace(Workspace &ws) {
   dev_free(ws.long_list);
   dev_free(ws.long_list2);
   dev_free(ws.vlong);
-  dev_free(ws.check);
   dev_free(ws.undec_sel);
   dev_free(ws.undec_pull);
   dev_free(ws.segmark);
@@ -356,7 +355,6 @@ int ensure_workspace(tcmis_graph *g) {
     dev_free(ws.mis);
     dev_free(ws.long_list);
     dev_free(ws.long_list2);
-    dev_free(ws.check);
     dev_free(ws.undec_sel);
     dev_free(ws.undec_pull);
     dev_free(ws.segmark);
@@ -373,7 +371,6 @@ int ensure_workspace(tcmis_graph *g) {
     if (int rc = dev_alloc(&ws.mis, n)) return rc;
     if (int rc = dev_alloc(&ws.long_list, n)) return rc;
     if (int rc = dev_alloc(&ws.long_list2, n)) return rc;
-    if (int rc = dev_alloc(&ws.check, n)) return rc;
     if (int rc = dev_alloc(&ws.undec_sel, n)) return rc;
     if (int rc = dev_alloc(&ws.undec_pull, n)) return rc;
     if (int rc = dev_alloc(&ws.segmark, n)) return rc;
@@ -613,12 +610,14 @@ TailArgs tail_args(tcmis_graph *g, const RoundArgs &a) {
   t.mis = ws.mis;
   t.mis_count = ws.mis_count;
   t.blockcnt = ws.blockcnt;
+  t.pack = nullptr;
   return t;
 }
 
 // cooperative launch: the grid barriers of k_tail need every block resident
-int launch_tail(tcmis_graph *g, const RoundArgs &a) {
+int launch_tail(tcmis_graph *g, const RoundArgs &a, HostRes *pack = nullptr) {
   TailArgs t = tail_args(g, a);
+  t.pack = pack;
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(a.tail_grid);
   lc.blockDim = dim3(kTailBlock);
@@ -784,8 +783,9 @@ int ensure_solve_graph(tcmis_graph *g, const RoundArgs &a, const SolvePre &pre) 
     e = cudaStreamBeginCaptureToGraph(st, graph, &node, nullptr, 1, cudaStreamCaptureModeRelaxed);
     if (e != cudaSuccess) rc = cuda_error(e, "cudaStreamBeginCaptureToGraph(post)");
     if (!rc) {
+      const bool tail_packs = a.tail_thr > 0 && pre.seg_mode != 2;
       if (a.tail_thr > 0) {
-        rc = launch_tail(g, a);
+        rc = launch_tail(g, a, tail_packs ? ws.d_res : nullptr);
       } else {
         thrust::counting_iterator<int32_t> ids(0);
         size_t bytes = ws.cub_bytes;
@@ -798,7 +798,7 @@ int ensure_solve_graph(tcmis_graph *g, const RoundArgs &a, const SolvePre &pre) 
         k_seg_total<<<grid_for(ctx, pre.nseg, 256, 4), 256, 0, st>>>(ws.segflag, g->d_rowtiles,
                                                                      pre.nseg, ws.ctrl);
       }
-      if (!rc)
+      if (!rc && !tail_packs)
         k_pack<<<1, 64, 0, st>>>(ws.ctrl, ws.mis_count, ws.rounds, ws.round_cap, ws.d_res);
       e = cudaStreamEndCapture(st, &captured);
       if (!rc && e != cudaSuccess) rc = cuda_error(e, "cudaStreamEndCapture(post)");
@@ -1037,8 +1037,11 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     } else {
       const int rr = hr.ctrl.round - 1;
       const int mr = hr.ctrl.main_rounds;
+      // k_priorities, the rounds, the tail (or cub's compaction), and k_pack
+      // unless the tail packed (h3 adds k_seg_total)
+      const bool tail_packs = a.tail_thr > 0 && seg_mode != 2;
       ctx->launches += 2 + launches_per_round(a) * (int64_t)mr + (seg_mode == 2 ? 1 : 0) +
-                       (a.tail_thr > 0 ? 1 : 1);
+                       (tail_packs ? 0 : 1);
       const int pre_n = std::min(rr, std::min(ws.round_cap, 64));
       rounds_h.assign(hr.rounds, hr.rounds + pre_n);
       if (rr > pre_n) {

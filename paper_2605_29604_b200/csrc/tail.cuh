@@ -101,6 +101,7 @@ struct TailArgs {
   int32_t *mis;
   int64_t *mis_count;
   unsigned *blockcnt;       // gridDim.x per-block counts
+  HostRes *pack;            // non-null: also leave the solve's results in mapped host memory
 };
 
 __device__ __forceinline__ void grid_barrier(unsigned *bar) {
@@ -297,7 +298,22 @@ __device__ void compact_mis(const TailArgs &a) {
     base += s_woff[kTailBlock / 32];
     __syncthreads();  // stage / s_woff reuse
   }
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *a.mis_count = base;
+  if (blockIdx.x == gridDim.x - 1) {
+    if (threadIdx.x == 0) *a.mis_count = base;
+    if (a.pack) {  // k_pack's job, done here: one graph node less
+      // word copies through L2 (ld.global.cg): written by other blocks
+      const int32_t cap = __ldcg(&a.ctrl->max_rounds);
+      const int nr = (int)(sizeof(DevRound) / 4) * (cap < 64 ? cap : 64);
+      const uint32_t *rs = reinterpret_cast<const uint32_t *>(a.rounds);
+      uint32_t *rd = reinterpret_cast<uint32_t *>(a.pack->rounds);
+      for (int i = threadIdx.x; i < nr; i += kTailBlock) rd[i] = __ldcg(rs + i);
+      const uint32_t *cs = reinterpret_cast<const uint32_t *>(a.ctrl);
+      uint32_t *cd = reinterpret_cast<uint32_t *>(&a.pack->ctrl);
+      for (int i = threadIdx.x; i < (int)(sizeof(Ctrl) / 4); i += kTailBlock) cd[i] = __ldcg(cs + i);
+      if (threadIdx.x == 0) a.pack->mis_count = (long long)base;
+      __threadfence_system();
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
