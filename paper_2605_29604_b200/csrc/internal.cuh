@@ -248,9 +248,9 @@ int launch_select(tcmis_graph *g, const RoundArgs &a);
 int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle cond, int use_cond);
 int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
                       uint32_t *p_out, uint16_t *q_out, uint8_t *state, uint8_t *next,
-                      uint8_t *segflag = nullptr, int T = 1, uint8_t *xm0 = nullptr,
-                      uint8_t *xm1 = nullptr, Ctrl *ctrl = nullptr, const Ctrl *ctrl0 = nullptr,
-                      DevRound *rounds = nullptr, int32_t nrounds = 0);
+                      uint8_t *segflag = nullptr, int T = 1, Ctrl *ctrl = nullptr,
+                      const Ctrl *ctrl0 = nullptr, DevRound *rounds = nullptr,
+                      int32_t nrounds = 0);
 // offset of k_tail's odd exclusion plane in Workspace::xm (16-byte aligned)
 inline size_t xm_stride(const Workspace &ws) { return (ws.n_cap + 15) / 16 * 16; }
 double avg_degree(const tcmis_graph *g);

@@ -58,8 +58,8 @@ __global__ void __launch_bounds__(256)
     k_priorities(int32_t n, const int64_t *__restrict__ off, int aligned, int mode,
                  uint64_t mseed, double avg, double scale, uint32_t *__restrict__ p_out,
                  uint16_t *__restrict__ q_out, int qshift, uint8_t *__restrict__ state,
-                 uint8_t *__restrict__ next, uint8_t *__restrict__ xm0, uint8_t *__restrict__ xm1,
-                 uint8_t *__restrict__ segflag, int T, int tshift, Ctrl *ctrl, Ctrl ctrl0,
+                 uint8_t *__restrict__ next, uint8_t *__restrict__ segflag, int T, int tshift,
+                 Ctrl *ctrl, Ctrl ctrl0,
                  DevRound *rounds, int32_t nrounds) {
   // the solve's control block and (for k_tail, which accumulates into it)
   // the zeroed statistics ring: no separate copy / memset on the stream
@@ -115,17 +115,12 @@ __global__ void __launch_bounds__(256)
                        (uint32_t)q_of(pv[2], qshift) | ((uint32_t)q_of(pv[3], qshift) << 16));
       if (state) *reinterpret_cast<uint32_t *>(state + v0) = st4;
       if (next) *reinterpret_cast<uint32_t *>(next + v0) = nx4;
-      if (xm0) {  // k_tail's exclusion planes start clear
-        *reinterpret_cast<uint32_t *>(xm0 + v0) = 0u;
-        *reinterpret_cast<uint32_t *>(xm1 + v0) = 0u;
-      }
     } else {
       for (int j = 0; j < kPrioV && v0 + j < n; ++j) {
         if (p_out) p_out[v0 + j] = pv[j];
         if (q_out) q_out[v0 + j] = q_of(pv[j], qshift);
         if (state) state[v0 + j] = (uint8_t)(st4 >> (8 * j));
         if (next) next[v0 + j] = (uint8_t)(nx4 >> (8 * j));
-        if (xm0) xm0[v0 + j] = xm1[v0 + j] = 0;
       }
     }
   }
@@ -472,8 +467,8 @@ int q_shift(int heuristic, int scale_bits) {
 
 int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
                       uint32_t *p_out, uint16_t *q_out, uint8_t *state, uint8_t *next,
-                      uint8_t *segflag, int T, uint8_t *xm0, uint8_t *xm1, Ctrl *ctrl,
-                      const Ctrl *ctrl0, DevRound *rounds, int32_t nrounds) {
+                      uint8_t *segflag, int T, Ctrl *ctrl, const Ctrl *ctrl0, DevRound *rounds,
+                      int32_t nrounds) {
   tcmis_ctx *ctx = g->ctx;
   int mode = 1;
   uint64_t mseed = mix64(seed);
@@ -492,8 +487,8 @@ int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bi
               (k_priorities<<<grid, 256, 0, ctx->stream>>>(g->n, off, aligned, mode, mseed,
                                                           mode ? avg_degree(g) : 0.0, scale,
                                                           p_out, q_out, q_shift(heuristic, scale_bits),
-                                                          state, next, xm0, xm1, segflag, T,
-                                                          tshift, ctrl, ctrl0 ? *ctrl0 : Ctrl{},
+                                                          state, next, segflag, T, tshift, ctrl,
+                                                          ctrl0 ? *ctrl0 : Ctrl{},
                                                           rounds, nrounds)));
   TCMIS_LAUNCHED(ctx);
   return 0;
@@ -734,8 +729,8 @@ int ensure_solve_graph(tcmis_graph *g, const RoundArgs &a, const SolvePre &pre) 
     }
     if (!rc)
       rc = launch_priorities(g, pre.H, pre.seed, pre.scale_bits, ws.prio, ws.q, ws.state, ws.next,
-                             pre.seg_mode ? ws.segflag : nullptr, pre.T, ws.xm,
-                             ws.xm + xm_stride(ws), ws.ctrl, &pre.c0, ws.rounds, ws.round_cap);
+                             pre.seg_mode ? ws.segflag : nullptr, pre.T, ws.ctrl, &pre.c0,
+                             ws.rounds, ws.round_cap);
     e = cudaStreamEndCapture(st, &captured);
     if (!rc && e != cudaSuccess) rc = cuda_error(e, "cudaStreamEndCapture(pre)");
   }
@@ -916,8 +911,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   auto launch_pre = [&]() -> int {
     if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
     return launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio, ws.q, ws.state, ws.next,
-                             seg0, T > 0 ? T : 1, ws.xm, ws.xm + xm_stride(ws), ws.ctrl, &c0,
-                             ws.rounds, ws.round_cap);
+                             seg0, T > 0 ? T : 1, ws.ctrl, &c0, ws.rounds, ws.round_cap);
   };
   if (step)
     if (int rc = launch_pre()) return rc;

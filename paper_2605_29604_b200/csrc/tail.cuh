@@ -20,8 +20,8 @@
 //     never touch the plane round r reads for round r-1's removals -- the
 //     snapshot of the reference's bulk-synchronous round is kept, and round
 //     count and every statistic equal the reference's.  A stale mark from
-//     round r-2 sits only on vertices that died then (q = 0), and
-//     k_priorities clears both planes at the start of every solve;
+//     round r-2 (or an earlier solve) sits only on dead vertices (q = 0); the
+//     kernel clears both planes of the vertices alive at its start;
 //   * L_{r+1} = round r's non-candidates.
 //
 // Round r's IterationStats are complete after round r+1's pass (its removed /
@@ -64,7 +64,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #endif
 
-constexpr int kGroup = 8;             // lanes per vertex in the tail kernel
+#ifndef TCMIS_TAIL_GROUP
+#define TCMIS_TAIL_GROUP 8
+#endif
+constexpr int kGroup = TCMIS_TAIL_GROUP;  // lanes per vertex in the tail kernel
 #ifndef TCMIS_TAIL_UNROLL
 #define TCMIS_TAIL_UNROLL 16
 #endif
@@ -316,7 +319,10 @@ __device__ void compact_mis(const TailArgs &a) {
   }
 }
 
-__global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
+#ifndef TCMIS_TAIL_MINB
+#define TCMIS_TAIL_MINB 1
+#endif
+__global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a) {
   __shared__ int32_t s_long[kTailLongCap];
   __shared__ int s_nlong;
   __shared__ unsigned long long s_acc[4];
@@ -333,6 +339,18 @@ __global__ void __launch_bounds__(kTailBlock) k_tail(TailArgs a) {
   const int r0 = *(volatile int *)&ctrl->round;
   const int64_t cnt0 = *(volatile int *)&ctrl->wl_count[r0 & 1];
   TAIL_MARK(1, cnt0);
+  if (cnt0 > 0) {
+    // the exclusion planes of the vertices alive at the tail's start (every
+    // list below is a subset): stale marks elsewhere sit on dead vertices
+    const int32_t *in0 = (r0 & 1) ? a.wl1 : a.wl0;
+    for (int64_t i = (int64_t)blockIdx.x * kTailBlock + threadIdx.x; i < cnt0;
+         i += (int64_t)gridDim.x * kTailBlock) {
+      const int32_t v = __ldcg(&in0[i]);
+      a.xm0[v] = 0;
+      a.xm1[v] = 0;
+    }
+    grid_barrier(a.bar);
+  }
   for (int round = r0; cnt0 > 0; ++round) {
     const bool first = round == r0;
     const int64_t cnt = first ? cnt0 : (int64_t) * (volatile int *)&ctrl->tail_cnt[round % 3];
