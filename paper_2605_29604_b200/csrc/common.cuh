@@ -78,11 +78,17 @@ __device__ __forceinline__ void block_add3(unsigned long long a, unsigned long l
 // every neighbour of a candidate leaves in the same round, so no alive vertex
 // ever reads it again.  next[v] = 1 is what neighbours test this round (and
 // it is never cleared: see update.cuh).
+// block column of v for tile dimension T (uniform): a shift for the usual
+// power-of-two T instead of a ~20-instruction integer division
+__device__ __forceinline__ int32_t seg_of(int32_t v, int T) {
+  return (T & (T - 1)) == 0 ? (v >> (__ffs(T) - 1)) : v / T;
+}
+
 __device__ __forceinline__ void mark_candidate(int32_t v, uint8_t *next, uint8_t *state,
                                                uint8_t *segflag, int T) {
   next[v] = 1;
   state[v] = TCMIS_IN_MIS;
-  if (segflag) segflag[v / T] = 1;
+  if (segflag) segflag[seg_of(v, T)] = 1;
 }
 
 // Multi-GPU: a rank publishes its own range's decisions as a bitmap slice

@@ -103,4 +103,44 @@ __device__ __forceinline__ void load_tail8(const int32_t *__restrict__ nbr, int6
   for (int j = 0; j < 8; ++j) u[j] = e - 1 - j >= s ? t[j] : -1;
 }
 
+// The last <= 4 entries of a row [s, e): u[0] = nbr[e-1], u[1] = nbr[e-2],
+// ... (-1 outside [s, e)).  The aligned 16-byte window holding e-1 supplies
+// r+1 of them (r = (e-1) mod 4); the window before it is loaded only when
+// the row reaches back into it.  Used by the straight-line probes, which
+// examine 4 entries (a smaller instruction footprint than load_tail8: the
+// grid's round-1 probe is issue-bound).
+__device__ __forceinline__ void load_tail4(const int32_t *__restrict__ nbr, int64_t nnz,
+                                           int64_t s, int64_t e, int32_t u[4]) {
+  const int64_t w1 = (e - 1) & ~(int64_t)3;
+  const int r = (int)((e - 1) - w1);
+  const bool need0 = r < 3 && s < w1;  // entries e-2..e-4 reach below w1
+  int4 a = make_int4(-1, -1, -1, -1), b;
+  if (w1 + 4 <= nnz) {
+    b = ld_stream(reinterpret_cast<const int4 *>(nbr + w1));
+    if (need0) a = ld_stream(reinterpret_cast<const int4 *>(nbr + w1 - 4));
+  } else {
+    const int64_t lim = nnz < 0 ? -nnz : nnz;
+    int32_t t[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t p = w1 - 4 + j;
+      t[j] = (p >= 0 && p < lim) ? __ldg(&nbr[p]) : -1;
+    }
+    a = make_int4(t[0], t[1], t[2], t[3]);
+    b = make_int4(t[4], t[5], t[6], t[7]);
+  }
+  const int32_t c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  int32_t t0, t1, t2, t3;
+  switch (r) {
+    case 0: t0 = c[4]; t1 = c[3]; t2 = c[2]; t3 = c[1]; break;
+    case 1: t0 = c[5]; t1 = c[4]; t2 = c[3]; t3 = c[2]; break;
+    case 2: t0 = c[6]; t1 = c[5]; t2 = c[4]; t3 = c[3]; break;
+    default: t0 = c[7]; t1 = c[6]; t2 = c[5]; t3 = c[4]; break;
+  }
+  u[0] = e - 1 >= s ? t0 : -1;
+  u[1] = e - 2 >= s ? t1 : -1;
+  u[2] = e - 3 >= s ? t2 : -1;
+  u[3] = e - 4 >= s ? t3 : -1;
+}
+
 }  // namespace tcmis_b200

@@ -96,8 +96,8 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
       v = (round == 1 && a.nz_identity) ? (int32_t)i : __ldg(&wl[i]);
       const int64_t s = ld_stream(&a.off[v]), e = ld_stream(&a.off[v + 1]);
       const uint32_t qv = __ldg(&q[v]);
-      int32_t u[8];
-      load_tail8(nbr, a.vnnz, s, e, u);
+      int32_t u[4];
+      load_tail4(nbr, a.vnnz, s, e, u);
       bool blocked = false;
 #pragma unroll
       for (int j = 0; j < kProbeK; ++j)

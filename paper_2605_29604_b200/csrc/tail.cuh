@@ -138,7 +138,7 @@ __device__ __forceinline__ void tail_candidate(const TailArgs &a, int32_t v, int
   a.next[v] = 1;
   a.state[v] = TCMIS_IN_MIS;
   ++sel;
-  const int32_t sb = v / a.T;
+  const int32_t sb = seg_of(v, a.T);
   if (a.seg_mode == 2) {
     a.segflag[sb] = 1;
   } else if (a.seg_mode == 1) {

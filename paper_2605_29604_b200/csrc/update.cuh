@@ -163,8 +163,8 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
     }
     if (i < cnt && a.state[v] == TCMIS_ALIVE) {
       const int64_t s = ld_stream(&a.off[v]), e = ld_stream(&a.off[v + 1]);
-      int32_t u[8];
-      load_tail8(a.nbr, a.vnnz, s, e, u);
+      int32_t u[4];
+      load_tail4(a.nbr, a.vnnz, s, e, u);
       bool hit = false;
 #pragma unroll
       for (int j = 0; j < kPullK; ++j)
