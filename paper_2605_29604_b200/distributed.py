@@ -199,24 +199,51 @@ def solve_partitioned(rank_obj, rank_lo: list[int], rank: int, world: int, dist,
     gathered = rank_obj.words_tensor(maxw * world)
     rounds = []
     cap = max_rounds or max(n, 1)
+    def enqueue_round():
+        rank_obj.select(mine)
+        _all_gather(dist, gathered, mine)
+        rank_obj.apply(gathered, rank_lo, rank, maxw, 0)
+        counts = rank_obj.update(mine)
+        _all_gather(dist, gathered, mine)
+        rank_obj.apply(gathered, rank_lo, rank, maxw, 1)
+        t = (counts.clone() if torch.is_tensor(counts)
+             else torch.tensor(counts, dtype=torch.int64, device=mine.device))
+        _all_reduce(dist, t)
+        return t
+
     with rank_obj.collective_stream():
-        for it in range(1, cap + 1):
-            rank_obj.select(mine)
-            _all_gather(dist, gathered, mine)
-            rank_obj.apply(gathered, rank_lo, rank, maxw, 0)
-            counts = rank_obj.update(mine)
-            _all_gather(dist, gathered, mine)
-            rank_obj.apply(gathered, rank_lo, rank, maxw, 1)
-            t = (counts.clone() if torch.is_tensor(counts)
-                 else torch.tensor(counts, dtype=torch.int64, device=mine.device))
-            _all_reduce(dist, t)
-            # the round's only host synchronisation: the termination test
-            sel, rem, alive, ev, sk = (int(x) for x in t.cpu().tolist())
-            rounds.append(RoundStats(it, sel, rem, alive, ev, sk))
-            if alive == 0:
-                break
+        if not mine.is_cuda:
+            for it in range(1, cap + 1):
+                sel, rem, alive, ev, sk = (int(x) for x in enqueue_round().tolist())
+                rounds.append(RoundStats(it, sel, rem, alive, ev, sk))
+                if alive == 0:
+                    break
+            else:
+                raise RuntimeError("iteration cap exceeded; engine livelock")  # engine.cpp:248-249
         else:
-            raise RuntimeError("iteration cap exceeded; engine livelock")  # engine.cpp:248-249
+            # the termination test lags one round: round it+1 is enqueued
+            # before round it's all-reduced counters reach the host, so the host
+            # never drains the stream between rounds.  After the last round
+            # (alive == 0) the extra round runs on empty worklists (no-op).
+            host = [torch.empty(5, dtype=torch.int64).pin_memory() for _ in range(2)]
+            done = [torch.cuda.Event() for _ in range(2)]
+
+            def launch(it):
+                t = enqueue_round()
+                host[it % 2].copy_(t, non_blocking=True)
+                done[it % 2].record()
+
+            launch(1)
+            for it in range(1, cap + 1):
+                if it < cap:
+                    launch(it + 1)
+                done[it % 2].synchronize()
+                sel, rem, alive, ev, sk = (int(x) for x in host[it % 2].tolist())
+                rounds.append(RoundStats(it, sel, rem, alive, ev, sk))
+                if alive == 0:
+                    break
+            else:
+                raise RuntimeError("iteration cap exceeded; engine livelock")  # engine.cpp:248-249
         if heuristic == "h3":
             ev, tot = rank_obj.h3_tiles()
             t = torch.tensor([ev, tot], dtype=torch.int64, device=mine.device)

@@ -32,3 +32,30 @@ def test_partitioned_device_side(world, spec, heuristic):
         want = [w[:3] + (0, 0) for w in want]
     assert got == want
     assert np.array_equal(state == 1, exp.state == 1)
+
+
+@pytest.mark.parametrize("heuristic", ["h2", "h3", "luby-perm"])
+def test_partitioned_protocol_nccl_world1(heuristic):
+    """The multi-process protocol itself (solve_partitioned: NCCL collectives
+    on the engine stream, the one-round-lagged termination test) on a
+    one-rank NCCL group -- the only NCCL group one GPU can form."""
+    import torch
+    import torch.distributed as dist
+    g = O.gen("rmat", 13, 16, 5)
+    rank_lo = D.partition_rows(g.off, 1, 16)
+    dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1)
+    try:
+        torch.cuda.set_device(0)
+        me = D.GpuRank(tc.Context(0), g.n, 0, g.n, g.off, g.nbr, "cuda:0")
+        res = D.solve_partitioned(me, rank_lo, 0, 1, dist, heuristic=heuristic)
+    finally:
+        dist.destroy_process_group()
+    exp = O.solve(g, heuristic, 1, tile_dim=16)
+    got = [(r.candidates_selected, r.vertices_removed, r.alive_remaining, r.tiles_evaluated,
+            r.tiles_skipped) for r in res.rounds]
+    want = [(r["sel"], r["rem"], r["alive"], r["tiles_eval"], r["tiles_skip"])
+            for r in exp.rounds]
+    if heuristic == "luby-perm":
+        want = [w[:3] + (0, 0) for w in want]
+    assert got == want
+    assert np.array_equal(res.own_state == 1, exp.state == 1)
