@@ -7,7 +7,10 @@ namespace tcmis_b200 {
 
 constexpr int kBlock = 256;    // threads per block of the round kernels
 constexpr int kStep = 4;       // row entries per thread-level step
-constexpr int kThreadMax = 32; // entries a thread examines before handing a row to a warp
+#ifndef TCMIS_THREAD_MAX
+#define TCMIS_THREAD_MAX 64
+#endif
+constexpr int kThreadMax = TCMIS_THREAD_MAX;  // entries a thread examines before handing a row to a warp
 // the per-lane scan engines read two 16-byte windows (8 entries) per step
 #ifndef TCMIS_SEL_WIN2
 #define TCMIS_SEL_WIN2 1
