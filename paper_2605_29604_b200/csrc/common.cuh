@@ -23,6 +23,12 @@ constexpr int kWarpU = TCMIS_WARP_U;  // independent loads per lane per step of 
 #define TCMIS_BLOCK_ROW 65536
 #endif
 constexpr int64_t kBlockRow = TCMIS_BLOCK_ROW;  // long-row lists: rows beyond this are scanned block-wide
+// pull exclusion: rows that outlive the engine are cut into chunks of this
+// many entries, which k_round_end's warps take independently (update.cuh)
+#ifndef TCMIS_PULL_CHUNK
+#define TCMIS_PULL_CHUNK 2048
+#endif
+constexpr int kPullChunk = TCMIS_PULL_CHUNK;
 
 // Loads of the CSR (offsets, neighbour ids): read once per phase, so they are
 // marked evict-first (ld.global.cs) and do not push the randomly gathered
@@ -227,6 +233,23 @@ __device__ __forceinline__ void warp_append(bool have, int32_t v, int32_t *out, 
   if (lane == leader) pos = atomicAdd(tail, __popc(m));
   pos = __shfl_sync(0xffffffffu, pos, leader);
   if (have) out[pos + __popc(m & ((1u << lane) - 1u))] = v;
+}
+
+// Per-lane reservation of `cnt` (>= 0) consecutive slots at *tail, one atomic
+// per warp; returns the lane's first slot.  Warp-uniform call.
+__device__ __forceinline__ int warp_reserve(int cnt, int *tail) {
+  const int lane = threadIdx.x & 31;
+  int x = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, x, 31);
+  int base = 0;
+  if (lane == 31 && total) base = atomicAdd(tail, total);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  return base + x - cnt;
 }
 
 }  // namespace tcmis_b200

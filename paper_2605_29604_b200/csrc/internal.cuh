@@ -62,7 +62,17 @@ struct Ctrl {
   int32_t sel_undec;   // rows k_probe_select left to the k_select engine
   int32_t pull_undec;  // rows k_probe_pull left to the k_update_pull engine
   int32_t sel_vlong;   // select rows longer than kBlockRow (block-wide in k_select_long)
-  int32_t pull_vlong;  // pull rows longer than kBlockRow (block-wide in k_round_end)
+  int32_t pull_items;  // chunks of the pull long rows (k_round_end work items)
+};
+
+// A pull row that outlived k_update_pull's engine (update.cuh): entries
+// [lo, hi) are still to be scanned, as chunks first .. first + chunks - 1 of
+// the round's item list; `left` counts the chunks not yet finished and `hit`
+// is set by any chunk that finds a candidate neighbour.
+struct PullRow {
+  int64_t lo, hi;
+  int32_t v, first;
+  int32_t left, hit;
 };
 
 // What the whole-solve graph leaves in mapped pinned host memory (k_pack):
@@ -85,8 +95,10 @@ struct Workspace {
   uint8_t *segflag = nullptr;
   int32_t *mis = nullptr;
   int32_t *long_list = nullptr;   // select: rows that outlived the thread probe
-  int32_t *long_list2 = nullptr;  // pull exclusion: same, for k_round_end
-  int32_t *vlong = nullptr;       // rows beyond kBlockRow: [0, cap) select, [cap, 2 cap) pull
+  PullRow *prow = nullptr;        // pull exclusion: rows that outlived the engine
+  int32_t *pitems = nullptr;      // ... their chunks (row index per item), for k_round_end
+  int64_t prow_cap = 0;
+  int32_t *vlong = nullptr;       // select rows beyond kBlockRow (k_select_long, block-wide)
   int64_t vlong_cap = 0;
   int32_t *undec_sel = nullptr;   // probe leftovers for the select engine
   int32_t *undec_pull = nullptr;  // probe leftovers for the pull engine

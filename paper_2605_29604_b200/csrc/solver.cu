@@ -295,7 +295,8 @@ void free_workspace(Workspace &ws) {
   dev_free(ws.segflag);
   dev_free(ws.mis);
   dev_free(ws.long_list);
-  dev_free(ws.long_list2);
+  dev_free(ws.prow);
+  dev_free(ws.pitems);
   dev_free(ws.vlong);
   dev_free(ws.undec_sel);
   dev_free(ws.undec_pull);
@@ -349,7 +350,6 @@ int ensure_workspace(tcmis_graph *g) {
     dev_free(ws.wl[1]);
     dev_free(ws.mis);
     dev_free(ws.long_list);
-    dev_free(ws.long_list2);
     dev_free(ws.undec_sel);
     dev_free(ws.undec_pull);
     dev_free(ws.segmark);
@@ -365,7 +365,6 @@ int ensure_workspace(tcmis_graph *g) {
     if (int rc = dev_alloc(&ws.wl[1], n)) return rc;
     if (int rc = dev_alloc(&ws.mis, n)) return rc;
     if (int rc = dev_alloc(&ws.long_list, n)) return rc;
-    if (int rc = dev_alloc(&ws.long_list2, n)) return rc;
     if (int rc = dev_alloc(&ws.undec_sel, n)) return rc;
     if (int rc = dev_alloc(&ws.undec_pull, n)) return rc;
     if (int rc = dev_alloc(&ws.segmark, n)) return rc;
@@ -384,8 +383,26 @@ int ensure_workspace(tcmis_graph *g) {
       dev_free(ws.vlong);
       ws.vlong = nullptr;
       ws.vlong_cap = 0;
-      if (int rc = dev_alloc(&ws.vlong, 2 * (size_t)need)) return rc;
+      if (int rc = dev_alloc(&ws.vlong, (size_t)need)) return rc;
       ws.vlong_cap = need;
+    }
+  }
+  {  // pull rows that outlive the engine are longer than kThreadMax; their
+     // chunks number at most rows + nnz / kPullChunk (per graph)
+    const int64_t rows = std::min<int64_t>((int64_t)n, g->nnz / kThreadMax + 1);
+    if (ws.prow_cap < rows) {
+      if (ws.exec) {
+        cudaGraphExecDestroy(ws.exec);
+        ws.exec = nullptr;
+      }
+      dev_free(ws.prow);
+      dev_free(ws.pitems);
+      ws.prow = nullptr;
+      ws.pitems = nullptr;
+      ws.prow_cap = 0;
+      if (int rc = dev_alloc(&ws.prow, (size_t)rows)) return rc;
+      if (int rc = dev_alloc(&ws.pitems, (size_t)(rows + g->nnz / kPullChunk + 1))) return rc;
+      ws.prow_cap = rows;
     }
   }
   // segment flags for any tile_dim >= 1
@@ -562,8 +579,8 @@ UpdateArgs update_args(tcmis_graph *g, const RoundArgs &a) {
   u.n1 = a.nz_count;
   u.nz = a.nz;
   u.nz_identity = a.nz_count == a.n ? 1 : 0;
-  u.long_list = ws.long_list2;
-  u.vlong = ws.vlong + ws.vlong_cap;
+  u.prow = ws.prow;
+  u.pitems = ws.pitems;
   u.undecided = ws.undec_pull;
   u.pub = Publish{a.pub_dead, a.pub_lo};
   u.segflag = ws.segflag;

@@ -21,8 +21,11 @@
 //         scanned from the end for next[u] == 1, stopping at the first hit
 //         (R-MAT s22 round 1: 5.3M entries examined instead of 7.1M push
 //         stores concentrated on hub lines).  Rows the probe cannot settle go
-//         to k_update_pull; rows still unsettled after kThreadMax entries go
-//         to a list that k_round_end scans warp-wide.  (A first version had
+//         to k_update_pull; rows still unsettled after kThreadMax entries are
+//         cut into chunks of kPullChunk entries that k_round_end's warps scan
+//         independently, so one long surviving row no longer sets the
+//         kernel's duration (a row of 64k entries was 256 dependent warp
+//         steps; R-MAT s26 round 1).  (A first version had
 //         the select kernels emit a non-candidate list: on the grid that
 //         emission alone cost as much as the select, ncu round 1.)
 // k_round_end then also folds the tile counters, elects the last block, and
@@ -54,8 +57,8 @@ struct UpdateArgs {
   int32_t n1;              // round-1 list (non-isolated vertices) for the pull probe
   const int32_t *nz;
   int nz_identity;
-  int32_t *long_list;      // pull: rows outliving the thread probe (ctrl->pull_count)
-  int32_t *vlong;          // ... longer than kBlockRow (ctrl->pull_vlong)
+  PullRow *prow;           // pull: rows outliving the engine (ctrl->pull_count)
+  int32_t *pitems;         // ... their chunks, row index per item (ctrl->pull_items)
   int32_t *undecided;      // pull: rows the probe could not settle (ctrl->pull_undec)
   Publish pub;             // multi-GPU: this round's removals of the own range
   const uint32_t *tile_hit;  // tile exclusion: per T=16 block row, rows with a candidate nbr
@@ -253,9 +256,15 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
       }
     }
     warp_emit(wo, survive, v, out, tail);
-    const bool vl = defer && e - s > kBlockRow;
-    warp_append(defer && !vl, v, a.long_list, &ctrl->pull_count);
-    warp_append(vl, v, a.vlong, &ctrl->pull_vlong);
+    if (__any_sync(0xffffffffu, defer)) {  // entries [s, hi) are left
+      const int nch = defer ? (int)((hi - s + kPullChunk - 1) / kPullChunk) : 0;
+      const int slot = warp_reserve(defer ? 1 : 0, &ctrl->pull_count);
+      const int first = warp_reserve(nch, &ctrl->pull_items);
+      if (defer) {
+        a.prow[slot] = PullRow{s, hi, v, first, nch, 0};
+        for (int c = 0; c < nch; ++c) a.pitems[first + c] = slot;
+      }
+    }
     if (mode == kFetch) fetch();
   }
   warp_flush(wo, out, tail);
@@ -275,10 +284,10 @@ __global__ void __launch_bounds__(kBlock)
   const int32_t *__restrict__ nbr = a.nbr;
   const uint8_t *__restrict__ next = a.next;
   unsigned long long rem = 0, ev = 0;
-  // pull rows longer than the thread probe: one warp per row, rows longer
-  // than kBlockRow by the whole block (a survivor must scan its entire row,
-  // and one warp walks 256 entries per dependent step)
-  const int nl = ctrl->pull_count;
+  // pull rows that outlived the engine, one chunk of kPullChunk entries per
+  // warp (chunk c covers [hi - (c+1) kPullChunk, hi - c kPullChunk) of the
+  // row); a chunk stops at its first candidate neighbour or once another
+  // chunk of the row has found one, and the last chunk to finish decides
   auto decide = [&](int32_t v, bool hit) {
     if (hit) {
       mark_removed(v, a.state, a.q);
@@ -289,45 +298,40 @@ __global__ void __launch_bounds__(kBlock)
       out[atomicAdd(&ctrl->wl_count[out_slot], 1)] = v;
     }
   };
-  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nl;
-       q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int32_t v = a.long_list[q];
-    const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
-    int64_t hi = e - kThreadMax;
-    bool hit = false;
-    while (!hit && hi > s) {
+  const int ni = ctrl->pull_items;
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < ni;
+       it += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int32_t slot = __ldcg(&a.pitems[it]);
+    PullRow *row = &a.prow[slot];
+    const int64_t lo0 = __ldcg(&row->lo), hi0 = __ldcg(&row->hi);
+    const int32_t v = __ldcg(&row->v), first = __ldcg(&row->first);
+    int64_t hi = hi0 - (int64_t)(it - first) * kPullChunk;
+    const int64_t lo = hi - kPullChunk > lo0 ? hi - kPullChunk : lo0;
+    bool hit = false, other = false;
+    while (!hit && !other && hi > lo) {
       int32_t u[kWarpU];
 #pragma unroll
       for (int j = 0; j < kWarpU; ++j) {
         const int64_t idx = hi - 1 - lane - 32 * j;
-        u[j] = idx >= s ? ld_stream(&nbr[idx]) : -1;
+        u[j] = idx >= lo ? ld_stream(&nbr[idx]) : -1;
       }
+      other = __ldcg(&row->hit) != 0;  // in flight with the row loads
       bool b = false;
 #pragma unroll
       for (int j = 0; j < kWarpU; ++j)
         if (u[j] >= 0) b |= next[u[j]] == 1;
       hit = __any_sync(0xffffffffu, b);
+      other = __shfl_sync(0xffffffffu, other, 0);
       hi -= 32 * kWarpU;
     }
-    if (lane == 0) decide(v, hit);
-  }
-  const int nvl = ctrl->pull_vlong;
-  for (int64_t q = blockIdx.x; q < nvl; q += gridDim.x) {
-    const int32_t v = a.vlong[q];
-    const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
-    int64_t hi = e - kThreadMax;
-    bool hit = false;
-    while (!hit && hi > s) {
-      bool b = false;
-#pragma unroll
-      for (int j = 0; j < kWarpU; ++j) {
-        const int64_t idx = hi - 1 - threadIdx.x - (int64_t)kBlock * j;
-        if (idx >= s) b |= next[ld_stream(&nbr[idx])] == 1;
+    if (lane == 0) {
+      if (hit) atomicExch(&row->hit, 1);
+      __threadfence();
+      if (atomicSub(&row->left, 1) == 1) {
+        __threadfence();
+        decide(v, atomicAdd(&row->hit, 0) != 0);
       }
-      hit = __syncthreads_or(b) != 0;
-      hi -= (int64_t)kBlock * kWarpU;
     }
-    if (threadIdx.x == 0) decide(v, hit);
   }
   if (a.seg_mode == 1) {  // spmv.cpp:37-46, per block column (A is symmetric)
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < a.nseg;
@@ -368,7 +372,7 @@ __global__ void __launch_bounds__(kBlock)
     vc->long_count = 0;
     vc->pull_count = 0;
     vc->sel_vlong = 0;
-    vc->pull_vlong = 0;
+    vc->pull_items = 0;
     vc->sel_undec = 0;
     vc->pull_undec = 0;
     vc->main_rounds = vc->main_rounds + 1;
