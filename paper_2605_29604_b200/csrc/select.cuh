@@ -6,22 +6,22 @@
 // above key[v]", and a single higher neighbour settles the answer, so the
 // scan exits early.  Any scan order gives the same set.
 //
-// Cost model (DESIGN.md "K3"): at R-MAT s22 round 1 only 9.5M of the 128M
+// Cost model (DESIGN.md §5): at R-MAT s22 round 1 only 9.5M of the 128M
 // adjacency entries must be examined (scanning each row from its end: the
-// high ids there are the low-degree, high-priority vertices), and 99.9 % of
-// the vertices are settled within their last 32 entries.  The kernel is
-// bound by memory latency and L1 wavefronts of the random key gathers, not by
-// HBM bytes.  Layout of the work:
+// high ids there are the low-degree, high-priority vertices), and 84 % of the
+// vertices are settled by their last 4 entries.  The kernels are bound by
+// memory latency of the random q gathers, not by HBM bytes.  Layout:
 //
-//  k_select       one thread per worklist vertex, as a per-thread state
-//                 machine: every loop iteration each lane does ONE unit --
-//                 probe the next kStep entries of its row (from the end), or
-//                 push to kStep neighbours, or fetch its next vertex -- so a
-//                 lane never idles behind the slowest vertex of its warp.  A
-//                 vertex unsettled after kThreadMax entries goes to a global
-//                 list for k_select_long.
-//  k_select_long  one warp per listed vertex over the whole grid: 128 entries
-//                 per step (4 independent loads per lane), early exit.
+//  k_probe_select one thread per worklist vertex, straight-line: the last 4
+//                 entries; settles short rows and blocked vertices.
+//  k_select       the probe's undecided rows, one lane per row as a per-lane
+//                 state machine: every loop iteration each lane scans the
+//                 next 8 entries of its row (two 16-byte windows, from the
+//                 end) or fetches its next row, so a lane never idles behind
+//                 the slowest row of its warp.  A row unsettled after
+//                 kThreadMax entries goes to a list for k_select_long.
+//  k_select_long  one warp per listed row: 256 entries per step (8 loads per
+//                 lane), early exit; rows beyond kBlockRow entries block-wide.
 //
 // Outputs: candidates get next = 1 and state = InMIS; in push mode their
 // neighbours get next = 2; in pull mode nothing else (the pull kernels walk
