@@ -30,6 +30,21 @@ constexpr int64_t kBlockRow = TCMIS_BLOCK_ROW;  // long-row lists: rows beyond t
 #endif
 constexpr int kPullChunk = TCMIS_PULL_CHUNK;
 
+// Programmatic dependent launch (TCMIS_PDL): the round kernels are launched
+// with programmatic stream serialisation, let their successor launch at once
+// and wait for their predecessor's completion before touching memory, so a
+// kernel boundary costs no launch latency.  Without the launch attribute both
+// instructions are no-ops.
+#ifndef TCMIS_PDL
+#define TCMIS_PDL 0
+#endif
+__device__ __forceinline__ void pdl_entry() {
+#if TCMIS_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 // Loads of the CSR (offsets, neighbour ids): read once per phase, so they are
 // marked evict-first (ld.global.cs) and do not push the randomly gathered
 // priority / state / decision vectors out of L2.

@@ -73,6 +73,7 @@ constexpr int kProbeK = 4;  // row entries the straight-line probe examines
 // This settles 84 % of R-MAT s22's round-1 vertices and every vertex of
 // rows <= kProbeK (the whole grid, most of the RGG).
 __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
+  pdl_entry();
   __shared__ int32_t s_und[kBlock / 32][64];
   Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
 // machine (scan down in 16-byte windows from e - kProbeK; push up), so a
 // lane never idles behind another lane's longer row.
 __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a) {
+  pdl_entry();
   Ctrl *ctrl = a.ctrl;
   const int64_t cnt = ctrl->sel_undec;
   if ((int64_t)blockIdx.x * kBlock >= cnt) return;
@@ -202,6 +204,7 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
 }
 
 __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
+  pdl_entry();
   Ctrl *ctrl = a.ctrl;
   const int cnt = ctrl->long_count, nvl = ctrl->sel_vlong;
   if ((int64_t)blockIdx.x * (kBlock / 32) >= cnt && blockIdx.x >= nvl) return;

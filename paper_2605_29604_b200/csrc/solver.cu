@@ -655,17 +655,38 @@ int tail_grid(tcmis_ctx *ctx) {
   return ctx->num_sms * ctx->tail_blocks_per_sm;
 }
 
+// Round kernels (those starting with pdl_entry(), common.cuh) are launched
+// with programmatic stream serialisation when TCMIS_PDL is set.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_round_kernel(void (*k)(KArgs...), int grid, cudaStream_t st, Args... args) {
+#if TCMIS_PDL
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(kBlock);
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, k, args...);
+#else
+  k<<<grid, kBlock, 0, st>>>(args...);
+  return cudaSuccess;
+#endif
+}
+
 int launch_select(tcmis_graph *g, const RoundArgs &a) {
   tcmis_ctx *ctx = g->ctx;
   cudaStream_t st = ctx->stream;
   const SelectArgs s = select_args(g, a);
   if (a.tile)
     TCMIS_CUDA(cudaMemsetAsync(g->ws.cbits, 0, 4 * ((size_t)a.n / 32 + 1), st));
-  TCMIS_TIMED(ctx, "k_probe_select", (k_probe_select<<<a.sel_grid, kBlock, 0, st>>>(s)));
+  TCMIS_TIMED(ctx, "k_probe_select", (launch_round_kernel(k_probe_select, a.sel_grid, st, s)));
   TCMIS_LAUNCHED(ctx);
-  TCMIS_TIMED(ctx, "k_select", (k_select<<<a.sel_grid, kBlock, 0, st>>>(s)));
+  TCMIS_TIMED(ctx, "k_select", (launch_round_kernel(k_select, a.sel_grid, st, s)));
   TCMIS_LAUNCHED(ctx);
-  TCMIS_TIMED(ctx, "k_select_long", (k_select_long<<<a.sel_grid, kBlock, 0, st>>>(s)));
+  TCMIS_TIMED(ctx, "k_select_long", (launch_round_kernel(k_select_long, a.sel_grid, st, s)));
   TCMIS_LAUNCHED(ctx);
   return 0;
 }
@@ -676,9 +697,9 @@ int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle
   cudaStream_t st = ctx->stream;
   const UpdateArgs u = update_args(g, a);
   if (a.pull) {
-    TCMIS_TIMED(ctx, "k_probe_pull", (k_probe_pull<<<a.sel_grid, kBlock, 0, st>>>(u)));
+    TCMIS_TIMED(ctx, "k_probe_pull", (launch_round_kernel(k_probe_pull, a.sel_grid, st, u)));
     TCMIS_LAUNCHED(ctx);
-    TCMIS_TIMED(ctx, "k_update_pull", (k_update_pull<<<a.sel_grid, kBlock, 0, st>>>(u)));
+    TCMIS_TIMED(ctx, "k_update_pull", (launch_round_kernel(k_update_pull, a.sel_grid, st, u)));
   } else if (a.tile) {
     TCMIS_CUDA(cudaMemsetAsync(g->ws.tile_hit, 0, 4 * ((size_t)a.nb16 + 1), st));
     TileExclArgs t{a.store_tiles, a.trow, a.tcol, a.tbits, g->ws.cbits, g->ws.tile_hit};
@@ -688,12 +709,12 @@ int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle
     else
       TCMIS_TIMED(ctx, "k_tile_excl_bits", (k_tile_excl_bits<<<grid, 256, 0, st>>>(t)));
     TCMIS_LAUNCHED(ctx);
-    TCMIS_TIMED(ctx, "k_update", (k_update<<<a.upd_grid, kBlock, 0, st>>>(u)));
+    TCMIS_TIMED(ctx, "k_update", (launch_round_kernel(k_update, a.upd_grid, st, u)));
   } else {
-    TCMIS_TIMED(ctx, "k_update", (k_update<<<a.upd_grid, kBlock, 0, st>>>(u)));
+    TCMIS_TIMED(ctx, "k_update", (launch_round_kernel(k_update, a.upd_grid, st, u)));
   }
   TCMIS_LAUNCHED(ctx);
-  TCMIS_TIMED(ctx, "k_round_end", (k_round_end<<<a.upd_grid, kBlock, 0, st>>>(u, cond, use_cond)));
+  TCMIS_TIMED(ctx, "k_round_end", (launch_round_kernel(k_round_end, a.upd_grid, st, u, cond, use_cond)));
   TCMIS_LAUNCHED(ctx);
   return 0;
 }

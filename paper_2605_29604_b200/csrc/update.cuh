@@ -74,6 +74,7 @@ struct UpdateArgs {
 // ---------------------------------------------------------------- push
 
 __global__ void __launch_bounds__(kBlock) k_update(UpdateArgs a) {
+  pdl_entry();
   using BlockScan = cub::BlockScan<int, kBlock>;
   __shared__ typename BlockScan::TempStorage scan_tmp;
   __shared__ int s_base;
@@ -142,6 +143,7 @@ constexpr int kPullK = 4;  // row entries the straight-line pull probe examines
 // Straight-line: the last <= 8 row entries with two aligned 16-byte loads,
 // candidate flags of the last kPullK.
 __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
+  pdl_entry();
   __shared__ int32_t s_srv[kBlock / 32][64];
   __shared__ int32_t s_und[kBlock / 32][64];
   Ctrl *ctrl = a.ctrl;
@@ -194,6 +196,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
 // Pull engine over the probe's undecided rows (per-lane state machine,
 // 16-byte windows downward from e - kPullK).
 __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
+  pdl_entry();
   __shared__ int32_t s_buf[kBlock / 32][64];
   Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
@@ -275,6 +278,7 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
 
 __global__ void __launch_bounds__(kBlock)
     k_round_end(UpdateArgs a, cudaGraphConditionalHandle cond, int use_cond) {
+  pdl_entry();
   Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
   int32_t *out = (round & 1) ? a.wl0 : a.wl1;
@@ -334,8 +338,32 @@ __global__ void __launch_bounds__(kBlock)
     }
   }
   if (a.seg_mode == 1) {  // spmv.cpp:37-46, per block column (A is symmetric)
-    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < a.nseg;
-         b += (int64_t)gridDim.x * blockDim.x) {
+    // 16 flags per thread with one 16-byte load (the sweep is one pass, not a
+    // grid-stride chain of byte loads); tile counts only for the set flags
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    int64_t head = 0;
+    if ((((uintptr_t)a.segflag | (uintptr_t)a.rowtiles) & 15) == 0) {
+      const int64_t nv = a.nseg / 16;
+      for (int64_t c = gt; c < nv; c += gs) {
+        uint4 *fp = reinterpret_cast<uint4 *>(a.segflag + 16 * c);
+        const uint4 f = *fp;
+        if (!(f.x | f.y | f.z | f.w)) continue;
+        const uint32_t w[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (!w[k]) continue;
+          const int4 t = __ldg(reinterpret_cast<const int4 *>(a.rowtiles + 16 * c + 4 * k));
+          if (w[k] & 0xffu) ev += (unsigned long long)t.x;
+          if (w[k] & 0xff00u) ev += (unsigned long long)t.y;
+          if (w[k] & 0xff0000u) ev += (unsigned long long)t.z;
+          if (w[k] & 0xff000000u) ev += (unsigned long long)t.w;
+        }
+        *fp = make_uint4(0, 0, 0, 0);
+      }
+      head = nv * 16;
+    }
+    for (int64_t b = head + gt; b < a.nseg; b += gs) {
       if (a.segflag[b]) {
         ev += (unsigned long long)a.rowtiles[b];
         a.segflag[b] = 0;
