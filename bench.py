@@ -480,6 +480,7 @@ def run_partitioned(args, rank: int, world: int, local: int) -> dict | None:
     log(f"[bench:rank{rank}] {args.config}: n={n} m={m} rows [{rank_lo[rank]}, "
         f"{rank_lo[rank + 1]}) (setup {time.time() - t0:.1f}s)")
     single = None
+    solve_bytes = None
     if rank == 0 and not args.no_single:
         # the same graph solved by one GPU (this rank's, alone), device-resident,
         # timed exactly like the N = 1 line (tcmis_solve_device, CUDA events)
@@ -512,6 +513,11 @@ def run_partitioned(args, rank: int, world: int, local: int) -> dict | None:
         single = {"ms": round(med, 4), "value": round(m / (med * 1e-3) / 1e9, 4),
                   "iterations": nit1, "mis_size": cnt1,
                   "note": "rank 0 alone, before partitioning; median of 5 device-resident solves"}
+        # SURVEY 8(d) algorithmic bytes of the whole solve, from the trajectory
+        # (identical for every world size), outside every timed region
+        traj = trajectory_terms(tc, full, cfg1)
+        solve_bytes = 13 * n + sum(12 * A + 4 * nA + 8 * NC + 4 * nNC + 2 * A
+                                   for A, nA, NC, nNC in traj)
     me = D.GpuRank(ctx, n, rank_lo[rank], rank_lo[rank + 1], None, None, device, full=full)
     full.close()
     stream = torch.cuda.ExternalStream(ctx.stream, device=device)
@@ -562,9 +568,12 @@ def run_partitioned(args, rank: int, world: int, local: int) -> dict | None:
             t_a = time.perf_counter()
             rk = D.GpuRank(ctx, n, rank_lo[rank], rank_lo[rank + 1], h_off, None, device,
                            rows=own_rows)
-            D.solve_partitioned(rk, rank_lo, rank, world, dist, heuristic=args.heuristic,
-                                seed=1, tile_dim=16)
+            r2 = D.solve_partitioned(rk, rank_lo, rank, world, dist, heuristic=args.heuristic,
+                                     seed=1, tile_dim=16, max_rounds=len(res.rounds) + 1)
             rk.close()
+            if [tuple(vars(x).values()) for x in r2.rounds] != [tuple(vars(x).values())
+                                                                for x in res.rounds]:
+                raise RuntimeError(f"e2e partitioned solve diverged: {r2.rounds} vs {res.rounds}")
             torch.cuda.synchronize()
             t_b = time.perf_counter()
             if k:
@@ -600,6 +609,21 @@ def run_partitioned(args, rank: int, world: int, local: int) -> dict | None:
         "single_gpu_same_graph": single,
         "roofline": None, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
     }
+    if single is not None:
+        single["matches_partitioned"] = (single["iterations"] == len(res.rounds)
+                                         and single["mis_size"] == mis_size)
+    if solve_bytes is not None:
+        hbm, peak_kind = peaks()
+        ach = solve_bytes / (ms_per_step * 1e-3) / 1e9
+        line["roofline"] = {
+            "kernel": "whole partitioned solve (all ranks' round kernels, collectives included)",
+            "bound": "hbm", "achieved": round(ach, 1), "peak": round(hbm * world, 1),
+            "peak_kind": f"{peak_kind} x {world} GPUs", "unit": "GB/s",
+            "frac": round(ach / (hbm * world), 4), "traffic": None,
+            "algorithmic_bytes": int(solve_bytes),
+            "definition": "SURVEY 8(d) algorithmic bytes of the solve (init + every round's "
+                          "phases, from the trajectory) / max-over-ranks CUDA-event time, "
+                          "against the aggregate HBM peak of the N GPUs"}
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sampled(tc, ctx, args)
     dist.barrier()
@@ -741,6 +765,8 @@ def run_reference(args) -> dict | None:
 def main():
     import faulthandler
     faulthandler.enable()
+    if os.environ.get("TCMIS_BENCH_HANG_DUMP"):  # debugging: stacks of a stuck run
+        faulthandler.dump_traceback_later(float(os.environ["TCMIS_BENCH_HANG_DUMP"]), repeat=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)

@@ -113,13 +113,19 @@ class GpuRank:
         self.g = tc.DeviceGraph(h, ctx)
         self.n, self.lo, self.hi = n, lo, hi
         self.stream = torch.cuda.ExternalStream(ctx.stream, device=device)
-        self.counts = torch.zeros(5, dtype=torch.int64, device=device)
+        with torch.cuda.stream(self.stream):
+            self.counts = torch.zeros(5, dtype=torch.int64, device=device)
 
     def close(self):
         self.g.close()
 
     def words_tensor(self, words: int):
-        return self.torch.zeros(words, dtype=self.torch.int32, device=self.device)
+        # allocated and zero-filled on the engine stream (a non-blocking
+        # stream): a fill queued on torch's default stream would be unordered
+        # with the engine's kernels, and the caching allocator would hand the
+        # block to the next solve while the engine stream still uses it
+        with self.torch.cuda.stream(self.stream):
+            return self.torch.zeros(words, dtype=self.torch.int32, device=self.device)
 
     def begin(self, heuristic: str, seed: int, tile_dim: int, scale_bits: int):
         cfg = self.tc.EngineConfig(heuristic=HEURISTICS[heuristic], seed=seed,
@@ -243,7 +249,8 @@ def solve_partitioned(rank_obj, rank_lo: list[int], rank: int, world: int, dist,
                 if alive == 0:
                     break
             else:
-                raise RuntimeError("iteration cap exceeded; engine livelock")  # engine.cpp:248-249
+                raise RuntimeError("iteration cap exceeded; engine livelock "  # engine.cpp:248-249
+                                   f"(rounds {[tuple(vars(r).values()) for r in rounds[:8]]})")
         if heuristic == "h3":
             ev, tot = rank_obj.h3_tiles()
             t = torch.tensor([ev, tot], dtype=torch.int64, device=mine.device)
@@ -277,6 +284,7 @@ def solve_partitioned_local(ranks: list, rank_lo: list[int], heuristic: str = "h
             r.select(m)
         torch.cuda.synchronize()
         gathered.copy_(torch.cat(mine))
+        torch.cuda.synchronize()  # the copy ran on torch's stream, apply on the engine's
         for k, r in enumerate(ranks):
             r.apply(gathered, rank_lo, k, maxw, 0)
         for r, m in zip(ranks, mine):
@@ -284,6 +292,7 @@ def solve_partitioned_local(ranks: list, rank_lo: list[int], heuristic: str = "h
         torch.cuda.synchronize()
         counts = sum(r.counts.cpu() for r in ranks)
         gathered.copy_(torch.cat(mine))
+        torch.cuda.synchronize()
         for k, r in enumerate(ranks):
             r.apply(gathered, rank_lo, k, maxw, 1)
         sel, rem, alive, ev, sk = (int(x) for x in counts)
