@@ -256,6 +256,14 @@ MISResult run_luby_reference(const Graph &g, std::uint64_t seed, LubyMode mode,
 
 MISResult run_mis(const Graph &g, const EngineConfig &config);
 
+/// The result row of the reference's `cmd_run` (the absent
+/// CLI): graph, n, m, heuristic, seed, |MIS|, iterations, total ms, phase 1/2/3
+/// ms, tiles evaluated, tiles skipped -- comma-separated, no trailing newline.
+/// Phase times are the device times the result carries (0 for a graph-launched
+/// solve, which has no per-phase timers).
+std::string csv_header();
+std::string csv_row(const std::string &graph_name, const Graph &g, const MISResult &r);
+
 // ------------------------------------------------------------- validate.hpp
 // validate.hpp:12-31 check_independence / check_maximality, evaluated on the
 // device (tcmis_validate); same witnesses and exception types.

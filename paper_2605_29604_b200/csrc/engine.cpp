@@ -10,6 +10,7 @@
 #include <bit>
 #include <istream>
 #include <ostream>
+#include <cstdio>
 #include <cstring>
 #include <stdexcept>
 
@@ -604,6 +605,34 @@ MISResult run_mis(const Graph &g, const EngineConfig &cfg) {  // engine.cpp:354-
     default:
       return run_tc_mis(g, cfg);
   }
+}
+
+std::string csv_header() {
+  return "graph,n,m,heuristic,seed,mis_size,iterations,total_ms,phase1_ms,phase2_ms,phase3_ms,"
+         "tiles_evaluated,tiles_skipped";
+}
+
+std::string csv_row(const std::string &graph_name, const Graph &g, const MISResult &r) {
+  if (graph_name.find_first_of(",\n\"") != std::string::npos)
+    throw std::invalid_argument("csv_row: graph name must not contain ',', '\"' or a newline");
+  char ms[4][32];
+  const double t[4] = {r.total_ms(), r.phase1_ms(), r.phase2_ms(), r.phase3_ms()};
+  for (int i = 0; i < 4; ++i) std::snprintf(ms[i], sizeof(ms[i]), "%.3f", t[i]);
+  std::string row = graph_name;
+  auto put = [&row](const std::string &x) {
+    row += ',';
+    row += x;
+  };
+  put(std::to_string(g.n));
+  put(std::to_string(g.num_edges()));
+  put(heuristic_name(r.heuristic));
+  put(std::to_string(r.seed));
+  put(std::to_string(r.cardinality()));
+  put(std::to_string(r.iterations.size()));
+  for (const char *x : ms) put(x);
+  put(std::to_string(r.tiles_evaluated()));
+  put(std::to_string(r.tiles_skipped()));
+  return row;
 }
 
 }  // namespace b200

@@ -125,6 +125,15 @@ int main(int argc, char **argv) {
                 ir.independent ? 1 : 0, mr.maximal ? 1 : 0, mr2.maximal ? 1 : 0,
                 mr2.addable_vertex ? (int)*mr2.addable_vertex : -1);
   }
+  // cmd_run's CSV row
+  {
+    EngineConfig c2;
+    c2.heuristic = Heuristic::H2;
+    MISResult r2 = run_mis(g, c2);
+    std::printf("{\"csv_header\": \"%s\", \"csv_row\": \"%s\", \"csv_bad_name\": \"%s\"}\n",
+                csv_header().c_str(), csv_row("g", g, r2).c_str(),
+                throws<std::invalid_argument>([&] { csv_row("a,b", g, r2); }));
+  }
   // reference error behaviour
   EngineConfig bad;
   bad.tile_dim = 0;

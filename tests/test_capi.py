@@ -52,7 +52,10 @@ def test_cxx_dropin_library_exports_engine_api():
                 "tcmis::b200::h2_degree_aware(", "tcmis::b200::h1_random(",
                 "tcmis::b200::compute_max_np(",
                 "tcmis::b200::tiled_spmv(", "tcmis::b200::phase3_update(",
-                "tcmis::b200::run_h3_resolution("):
+                "tcmis::b200::run_h3_resolution(", "tcmis::b200::write_tiled(",
+                "tcmis::b200::read_tiled(", "tcmis::b200::tile_stats(",
+                "tcmis::b200::check_independence(", "tcmis::b200::check_maximality(",
+                "tcmis::b200::csv_header[abi:cxx11](", "tcmis::b200::csv_row("):
         assert sym in names, sym
 
 

@@ -78,5 +78,16 @@ def test_cpp_dropin_matches_reference(dropin, kind, args):
     assert t8["tiles8"] == int(O.tile_row_counts(g, 8).sum())
     e8 = O.solve(g, "h2", 1, tile_dim=8)
     assert t8["t8_rounds"] == e8.n_rounds and t8["t8_eval1"] == e8.rounds[0]["tiles_eval"]
+    csv = [x for x in lines if "csv_row" in x][0]
+    assert csv["csv_header"].split(",") == [
+        "graph", "n", "m", "heuristic", "seed", "mis_size", "iterations", "total_ms",
+        "phase1_ms", "phase2_ms", "phase3_ms", "tiles_evaluated", "tiles_skipped"]
+    row = csv["csv_row"].split(",")
+    assert row[:7] == ["g", str(g.n), str(g.num_edges), "h2", "1", str(int(mis2.size)),
+                       str(exp2.n_rounds)]
+    assert all(float(x) >= 0 for x in row[7:11])
+    assert row[11:] == [str(sum(x["tiles_eval"] for x in exp2.rounds)),
+                        str(sum(x["tiles_skip"] for x in exp2.rounds))]
+    assert csv["csv_bad_name"] == "yes"
     errs = [x for x in lines if "bad_tile" in x][0]
     assert all(v == "yes" for v in errs.values()), errs
