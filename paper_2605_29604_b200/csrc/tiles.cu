@@ -176,6 +176,7 @@ constexpr int kBigBlock = 512;
 constexpr int kBigWords = 16384;          // 64 KB of dynamic shared memory: 3 CTAs per SM
 constexpr int64_t kBigHashMax = 8192;     // set of <= 16384 slots
 constexpr int64_t kBigBits = 32ll * kBigWords;
+constexpr int kBigGroup = 8;              // windows whose row boundaries are searched together
 // hub block rows (R-MAT s22's block row 0 holds ~1M entries): one CTA per
 // row serialised the whole count behind it (0.5-1.1 ms); they are counted by
 // kHubCTAs CTAs each on a global bitmap (L2 atomics), kHubBatch rows at a time
@@ -377,7 +378,8 @@ __global__ void __launch_bounds__(kBigBlock)
                 unsigned *__restrict__ next_item) {
   extern __shared__ __align__(16) uint32_t big[];  // kBigWords
   __shared__ int s_red[kBigBlock / 32];
-  __shared__ int64_t s_cur[64], s_end[64];
+  __shared__ int64_t s_bound[64][kBigGroup + 1];
+  __shared__ int64_t s_pre[65];
   __shared__ unsigned s_item;
   uint4 *b4 = reinterpret_cast<uint4 *>(big);
   for (int i = threadIdx.x; i < kBigWords / 4; i += kBigBlock) b4[i] = make_uint4(0, 0, 0, 0);
@@ -400,31 +402,77 @@ __global__ void __launch_bounds__(kBigBlock)
       if (threadIdx.x == 0) rowtiles[b] = total;
       continue;
     }
-    // hub rows: windows of kBigBits block columns.  Row k's entries of window
-    // w are [lower_bound(k, w), lower_bound(k, w + 1)) (sorted rows): one
-    // binary search per row and window, then plain strided passes (the first
-    // version advanced per-row cursors chunk by chunk with two block barriers
-    // per 512 entries: 0.6 ms for the 162k-entry hub row of R-MAT s22)
+    // rows beyond the set: windows of kBigBits block columns.  Row k's
+    // entries of window w are [lower_bound(k, w), lower_bound(k, w + 1))
+    // (sorted rows).  The boundaries of kBigGroup windows are searched at
+    // once, one thread per (row, boundary), and each window is then ONE flat
+    // pass over the concatenated row segments.  (The previous version ran the
+    // T searches of a window and then T per-row loops one after another: a
+    // chain of dependent loads per window, 13.7 of the 23.5 ms of R-MAT s26's
+    // tile count.)
     int cnt = 0;
     const int64_t windows = ((int64_t)nb + kBigBits - 1) / kBigBits;
-    for (int64_t w = 0; w < windows; ++w) {
-      const int64_t wlo = w * kBigBits;
-      if (threadIdx.x < rows) {
-        const int64_t rs = off[r0 + threadIdx.x], re = off[r0 + threadIdx.x + 1];
-        s_cur[threadIdx.x] = w == 0 ? rs : lower_bound_i32(nbr, rs, re, wlo * T);
-        s_end[threadIdx.x] = w + 1 == windows ? re : lower_bound_i32(nbr, rs, re, (wlo + kBigBits) * T);
+    for (int64_t w0 = 0; w0 < windows; w0 += kBigGroup) {
+      const int gw = (int)min((int64_t)kBigGroup, windows - w0);
+      for (int i = threadIdx.x; i < rows * (gw + 1); i += kBigBlock) {
+        const int k = i / (gw + 1), jb = i % (gw + 1);
+        const int64_t wb = w0 + jb;
+        const int64_t rs = off[r0 + k], re = off[r0 + k + 1];
+        s_bound[k][jb] = wb == 0 ? rs
+                         : wb >= windows ? re
+                                         : lower_bound_i32(nbr, rs, re, wb * kBigBits * T);
       }
       __syncthreads();
-      for (int k = 0; k < rows; ++k) {
-        for (int64_t p = s_cur[k] + threadIdx.x; p < s_end[k]; p += kBigBlock) {
-          const uint32_t c = (uint32_t)__ldg(&nbr[p]) / uT - (uint32_t)wlo;
-          const uint32_t bit = 1u << (c & 31u);
-          cnt += (atomicOr(&big[c >> 5], bit) & bit) ? 0 : 1;
+      for (int jw = 0; jw < gw; ++jw) {
+        const uint32_t wlo = (uint32_t)((w0 + jw) * kBigBits);
+        if (threadIdx.x < 32) {  // segment prefix over the rows (rows <= 64)
+          const int k0 = threadIdx.x, k1 = threadIdx.x + 32;
+          const int64_t l0 = k0 < rows ? s_bound[k0][jw + 1] - s_bound[k0][jw] : 0;
+          const int64_t l1 = k1 < rows ? s_bound[k1][jw + 1] - s_bound[k1][jw] : 0;
+          int64_t x0 = l0, x1 = l1;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const int64_t y0 = __shfl_up_sync(0xffffffffu, x0, d);
+            const int64_t y1 = __shfl_up_sync(0xffffffffu, x1, d);
+            if (k0 >= d) {
+              x0 += y0;
+              x1 += y1;
+            }
+          }
+          const int64_t tot0 = __shfl_sync(0xffffffffu, x0, 31);
+          s_pre[k0] = x0 - l0;
+          s_pre[k1] = tot0 + x1 - l1;
+          if (k0 == 31) s_pre[64] = tot0 + x1;
         }
+        __syncthreads();
+        const int64_t total = s_pre[64];
+        for (int64_t q0 = threadIdx.x; q0 < total; q0 += 4 * kBigBlock) {
+          uint32_t c[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int64_t q = q0 + (int64_t)kBigBlock * j;
+            c[j] = 0xffffffffu;
+            if (q < total) {
+              int lo = 0, hi = rows - 1;  // last row with s_pre[k] <= q
+              while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_pre[mid] <= q) lo = mid;
+                else hi = mid - 1;
+              }
+              c[j] = (uint32_t)__ldg(&nbr[s_bound[lo][jw] + (q - s_pre[lo])]) / uT - wlo;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (c[j] == 0xffffffffu) continue;
+            const uint32_t bit = 1u << (c[j] & 31u);
+            cnt += (atomicOr(&big[c[j] >> 5], bit) & bit) ? 0 : 1;
+          }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kBigWords / 4; i += kBigBlock) b4[i] = make_uint4(0, 0, 0, 0);
+        __syncthreads();
       }
-      __syncthreads();
-      for (int i = threadIdx.x; i < kBigWords / 4; i += kBigBlock) b4[i] = make_uint4(0, 0, 0, 0);
-      __syncthreads();
     }
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = cnt;

@@ -83,11 +83,18 @@ def test_tile_counts_all_row_classes(ctx, T):
     extra = rng.integers(0, n, size=(400_000, 2), dtype=np.int32)
     mids = np.stack([np.repeat(np.arange(2, 40, dtype=np.int32), 1500),
                      rng.integers(0, n, size=38 * 1500, dtype=np.int32)], 1)
-    e = np.concatenate([np.stack([np.zeros(n - 1, np.int32), leaves], 1), extra, mids])
+    # vertices 5 and 6: ~20k random neighbours each, so at T = 1, 2 they are big
+    # rows (8192 < entries <= 65536) swept in several 2^19-column windows
+    wide = np.stack([np.repeat(np.array([5, 6], np.int32), 20_000),
+                     rng.integers(0, n, size=40_000, dtype=np.int32)], 1)
+    e = np.concatenate([np.stack([np.zeros(n - 1, np.int32), leaves], 1), extra, mids, wide])
     g = O.graph_from_edges(n, e)
     dg = tc.DeviceGraph.upload(as_tc(g), ctx)
     want = O.tile_row_counts(g, T)
     assert dg.tile(T) == int(want.sum())
+    # per block row, through the reference-layout export (same K1 counts)
+    a = tc.tile_graph(as_tc(g), T, ctx)
+    assert np.array_equal(np.diff(a.block_row_offsets), want)
     exp = O.solve(g, "h2", 1, tile_dim=T)
     got = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=1, tile_dim=T))
     assert rounds_tuple(got.iterations) == oracle_tuple(exp)
