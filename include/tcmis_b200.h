@@ -125,6 +125,14 @@ int32_t tcmis_ctx_timeline(tcmis_ctx *ctx, tcmis_kernel_time *out, int32_t cap);
  * context stream); wrap_device borrows device arrays the caller keeps alive. */
 int tcmis_graph_upload(tcmis_ctx *ctx, int32_t n, const int64_t *offsets,
                        const int32_t *neighbors, tcmis_graph **out);
+/* upload + tcmis_graph_tile(tile_dim) in one call, the tile count overlapping
+ * the upload: neighbour ids go up in chunks of block rows while the light
+ * block rows of the chunks already resident are counted on a side stream
+ * (the drop-in path of run_mis / run_tc_mis(g, cfg), engine.cpp:297-299).
+ * *tile_count (may be NULL) = TiledAdjacency::tile_count(). */
+int tcmis_graph_upload_tiled(tcmis_ctx *ctx, int32_t n, const int64_t *offsets,
+                             const int32_t *neighbors, int32_t tile_dim, tcmis_graph **out,
+                             int64_t *tile_count);
 int tcmis_graph_wrap_device(tcmis_ctx *ctx, int32_t n, int64_t nnz, const int64_t *d_offsets,
                             const int32_t *d_neighbors, tcmis_graph **out);
 void tcmis_graph_destroy(tcmis_graph *g);

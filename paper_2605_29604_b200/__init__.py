@@ -122,6 +122,7 @@ def load():
         "tcmis_ctx_synchronize": (C.c_int, [vp]),
         "tcmis_ctx_launches": (i64, [vp]),
         "tcmis_graph_upload": (C.c_int, [vp, i32, vp, vp, P(vp)]),
+        "tcmis_graph_upload_tiled": (C.c_int, [vp, i32, vp, vp, i32, P(vp), P(i64)]),
         "tcmis_graph_wrap_device": (C.c_int, [vp, i32, i64, vp, vp, P(vp)]),
         "tcmis_graph_destroy": (None, [vp]),
         "tcmis_graph_n": (i32, [vp]),
@@ -321,11 +322,19 @@ class DeviceGraph:
         self._keep = keepalive
 
     @classmethod
-    def upload(cls, g: Graph, ctx: Optional[Context] = None) -> "DeviceGraph":
+    def upload(cls, g: Graph, ctx: Optional[Context] = None,
+               tile_dim: Optional[int] = None) -> "DeviceGraph":
+        """Host CSR -> HBM.  With tile_dim, the K1 tile count of that tiling
+        runs overlapped with the upload (tcmis_graph_upload_tiled)."""
         ctx = ctx or default_context()
         h = C.c_void_p()
-        _check(load().tcmis_graph_upload(ctx.h, int(g.n), _ptr(g.offsets), _ptr(g.neighbors),
-                                         C.byref(h)))
+        if tile_dim is None:
+            _check(load().tcmis_graph_upload(ctx.h, int(g.n), _ptr(g.offsets),
+                                             _ptr(g.neighbors), C.byref(h)))
+        else:
+            _check(load().tcmis_graph_upload_tiled(ctx.h, int(g.n), _ptr(g.offsets),
+                                                   _ptr(g.neighbors), int(tile_dim),
+                                                   C.byref(h), None))
         return cls(h, ctx)
 
     @classmethod

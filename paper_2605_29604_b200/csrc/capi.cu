@@ -153,6 +153,10 @@ TCMIS_API void tcmis_ctx_destroy(tcmis_ctx *ctx) {
   for (auto &ev : ctx->ev) cudaEventDestroy(ev);
   for (auto &ev : ctx->event_pool) cudaEventDestroy(ev);
   cudaStreamDestroy(ctx->stream);
+  if (ctx->side) {
+    cudaStreamDestroy(ctx->side);
+    for (cudaEvent_t e : ctx->side_ev) cudaEventDestroy(e);
+  }
   delete ctx;
 }
 
@@ -167,6 +171,27 @@ TCMIS_API int32_t tcmis_ctx_timeline(tcmis_ctx *ctx, tcmis_kernel_time *out, int
 TCMIS_API int tcmis_ctx_synchronize(tcmis_ctx *ctx) {
   NEED(ctx, "null context");
   TCMIS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+TCMIS_API int tcmis_graph_upload_tiled(tcmis_ctx *ctx, int32_t n, const int64_t *offsets,
+                                       const int32_t *neighbors, int32_t tile_dim,
+                                       tcmis_graph **out, int64_t *tile_count) {
+  NEED(ctx && out, "null handle");
+  NEED(n >= 0, "vertex count must be non-negative");
+  NEED(n == 0 || offsets, "null offsets");
+  *out = nullptr;
+  const int64_t nnz = offsets ? offsets[n] : 0;
+  NEED(nnz >= 0, "negative edge count");
+  NEED(nnz == 0 || neighbors, "null neighbors");
+  ENTER(ctx);
+  tcmis_graph *g = nullptr;
+  if (int rc = upload_tiled(ctx, n, offsets, neighbors, tile_dim, &g)) {
+    if (g) tcmis_graph_destroy(g);
+    return rc;
+  }
+  *out = g;
+  if (tile_count) *tile_count = g->tile_total;
   return 0;
 }
 

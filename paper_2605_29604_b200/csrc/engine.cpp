@@ -51,6 +51,13 @@ struct DeviceGraph {
     check(tcmis_graph_upload(context(), g.n, g.offsets.empty() ? nullptr : g.offsets.data(),
                              g.neighbors.empty() ? nullptr : g.neighbors.data(), &h));
   }
+  // upload with the K1 tile count of tile_dim overlapped (tcmis_graph_upload_tiled)
+  DeviceGraph(const Graph &g, int tile_dim) {
+    check(tcmis_graph_upload_tiled(context(), g.n,
+                                   g.offsets.empty() ? nullptr : g.offsets.data(),
+                                   g.neighbors.empty() ? nullptr : g.neighbors.data(), tile_dim,
+                                   &h, nullptr));
+  }
   ~DeviceGraph() { tcmis_graph_destroy(h); }
   DeviceGraph(const DeviceGraph &) = delete;
   DeviceGraph &operator=(const DeviceGraph &) = delete;
@@ -575,8 +582,8 @@ MISResult run_tc_mis(const Graph &g, const EngineConfig &cfg) {
   if (cfg.heuristic != Heuristic::H1 && cfg.heuristic != Heuristic::H2 &&
       cfg.heuristic != Heuristic::H3)
     throw std::invalid_argument("tiled engine only runs h1/h2/h3; use run_luby_reference");
-  DeviceGraph dg(g);
-  return solve(dg.h, g.n, cfg, cfg.heuristic);  // tiling derived on the device
+  DeviceGraph dg(g, cfg.tile_dim);  // tile_graph on the device, overlapped with the upload
+  return solve(dg.h, g.n, cfg, cfg.heuristic);
 }
 
 MISResult run_luby_reference(const Graph &g, std::uint64_t seed, LubyMode mode, int scale_bits,

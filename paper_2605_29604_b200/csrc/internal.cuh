@@ -144,6 +144,9 @@ struct tcmis_ctx {
   int tail_blocks_per_sm = 0;  // co-resident k_tail blocks per SM (occupancy)
   int64_t launches = 0;
   cudaEvent_t ev[8] = {};
+  // side stream + events of upload_tiled (K1 counting overlapped with the upload)
+  cudaStream_t side = nullptr;
+  cudaEvent_t side_ev[9] = {};  // one per upload chunk (8) + the join
   // the largest solve workspace of a destroyed graph, adopted by the next
   // graph that fits (upload -> solve -> destroy loops re-use buffers, pinned
   // staging and the instantiated round graph)
@@ -274,6 +277,10 @@ void free_workspace(Workspace &ws);
 
 // tiling (tiles.cu)
 int build_tile_counts(tcmis_graph *g, int T);
+int wrap_owned(tcmis_ctx *ctx, int32_t n, int64_t nnz, int64_t *d_off, int32_t *d_nbr,
+               tcmis_graph **out);
+int upload_tiled(tcmis_ctx *ctx, int32_t n, const int64_t *off, const int32_t *nbr, int T,
+                 tcmis_graph **out);
 int export_tiles(tcmis_graph *g, int T, int32_t *tile_row, int32_t *tile_col,
                  uint64_t *row_bits, int64_t *bro);
 int build_tile_store(tcmis_graph *g, int T);

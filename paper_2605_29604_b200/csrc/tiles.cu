@@ -176,7 +176,8 @@ constexpr int kBigBlock = 512;
 constexpr int kBigWords = 16384;          // 64 KB of dynamic shared memory: 3 CTAs per SM
 constexpr int64_t kBigHashMax = 8192;     // set of <= 16384 slots
 constexpr int64_t kBigBits = 32ll * kBigWords;
-constexpr int kBigGroup = 8;              // windows whose row boundaries are searched together
+constexpr int kBigGroup = 8;
+constexpr int kUploadChunks = 8;          // upload_tiled: chunks of the neighbour-id upload              // windows whose row boundaries are searched together
 // hub block rows (R-MAT s22's block row 0 holds ~1M entries): one CTA per
 // row serialised the whole count behind it (0.5-1.1 ms); they are counted by
 // kHubCTAs CTAs each on a global bitmap (L2 atomics), kHubBatch rows at a time
@@ -222,10 +223,10 @@ __global__ void __launch_bounds__(256)
 }
 
 __global__ void __launch_bounds__(kLightBlock)
-    k_count_light(int32_t n, int T, int32_t nb, const int64_t *__restrict__ off,
-                  const int32_t *__restrict__ nbr, int32_t *__restrict__ rowtiles,
-                  int32_t *__restrict__ lists, int32_t *__restrict__ counts, int bitmap,
-                  int32_t *__restrict__ hubs) {
+    k_count_light(int32_t n, int T, int32_t nb, int32_t b_lo, int32_t b_hi,
+                  const int64_t *__restrict__ off, const int32_t *__restrict__ nbr,
+                  int32_t *__restrict__ rowtiles, int32_t *__restrict__ lists,
+                  int32_t *__restrict__ counts, int bitmap, int32_t *__restrict__ hubs) {
   __shared__ __align__(16) uint32_t tab[kLightBlock / 32][kHashSlots];
   const int lane = threadIdx.x & 31;
   uint32_t *t = tab[threadIdx.x >> 5];
@@ -233,7 +234,7 @@ __global__ void __launch_bounds__(kLightBlock)
   for (int i = lane; i < kHashSlots / 4; i += 32) t4[i] = make_uint4(0, 0, 0, 0);
   __syncwarp();
   const uint32_t uT = (uint32_t)T;
-  for (int64_t b = ((int64_t)blockIdx.x * kLightBlock + threadIdx.x) >> 5; b < nb;
+  for (int64_t b = b_lo + (((int64_t)blockIdx.x * kLightBlock + threadIdx.x) >> 5); b < b_hi;
        b += ((int64_t)gridDim.x * kLightBlock) >> 5) {
     const int64_t r0 = b * T, r1 = min((int64_t)n, r0 + T);
     const int64_t s = off[r0], e = off[r1];
@@ -537,74 +538,133 @@ int plan_items(tcmis_graph *g, int T, int32_t nb, Items &it) {
 
 }  // namespace
 
-int build_tile_counts(tcmis_graph *g, int T) {
+// K1 in three steps, so the light pass can run block-row range by range
+// while the neighbour ids are still arriving (upload_tiled).
+struct K1Plan {
+  int T = 0;
+  int32_t nb = 0;
+  int bitmap = 0;
+  int32_t *lists = nullptr, *cnt = nullptr, *hubs = nullptr;
+  uint32_t *bms = nullptr;  // hub bitmaps, kHubBatch of them
+};
+
+int k1_begin(tcmis_graph *g, int T, K1Plan &p) {
   if (T < 1 || T > 64)
     return set_error(TCMIS_E_INVALID_ARGUMENT,
                      "tile_dim must be in [1, 64], got " + std::to_string(T));
-  tcmis_ctx *ctx = g->ctx;
-  cudaStream_t st = ctx->stream;
+  cudaStream_t st = g->ctx->stream;
   const int32_t nb = (int32_t)(((int64_t)g->n + T - 1) / T);
   dev_free(g->d_rowtiles);
   g->d_rowtiles = nullptr;
   g->tile_T = 0;
   g->tile_nb = nb;
   g->tile_total = 0;
+  p = K1Plan{};
+  p.T = T;
+  p.nb = nb;
   if (int rc = dev_alloc(&g->d_rowtiles, (size_t)nb + 1)) return rc;
   TCMIS_CUDA(cudaMemsetAsync(g->d_rowtiles, 0, sizeof(int32_t) * ((size_t)nb + 1), st));
-  if (nb > 0) {
-    // lists: mid rows from the front, big rows from the back; counts[0..1]
-    // list sizes, counts[2..3] the dynamic work counters
-    // few enough block columns for one shared bitmap (R-MAT s22: nb = 2^18):
-    // every non-light row goes to k_count_mid's exact bitmap, no hashing
-    const int bitmap = (int64_t)nb <= 32ll * kMidSlots ? 1 : 0;
-    int32_t *lists = nullptr, *cnt = nullptr, *hubs = nullptr;
-    if (int rc = dev_alloc(&lists, (size_t)nb)) return rc;
-    if (int rc = dev_alloc(&hubs, (size_t)nb)) return rc;
-    if (int rc = dev_alloc(&cnt, 8)) return rc;
-    TCMIS_CUDA(cudaMemsetAsync(cnt, 0, 8 * sizeof(int32_t), st));
-    k_count_light<<<grid_for(ctx, 32ll * nb, kLightBlock, 8), kLightBlock, 0, st>>>(
-        g->n, T, nb, g->d_off, g->d_nbr, g->d_rowtiles, lists, cnt, bitmap, hubs);
-    TCMIS_LAUNCHED(ctx);
-    int32_t nhub = 0;
-    TCMIS_CUDA(cudaMemcpyAsync(&nhub, cnt + 4, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    TCMIS_CUDA(cudaStreamSynchronize(st));
-    if (nhub > 0) {
-      // rowtiles[hub] was never written by k_count_light: start from 0
-      const size_t words = ((size_t)nb + 31) / 32;
-      uint32_t *bms = nullptr;
-      const int batch = std::min(nhub, kHubBatch);
-      if (int rc = dev_alloc(&bms, words * batch)) return rc;
-      for (int first = 0; first < nhub; first += kHubBatch) {
-        const int nh = std::min(kHubBatch, nhub - first);
-        TCMIS_CUDA(cudaMemsetAsync(bms, 0, 4 * words * nh, st));
-        k_count_hub<<<dim3(kHubCTAs, nh), 256, 0, st>>>(g->n, T, nb, g->d_off, g->d_nbr,
-                                                        g->d_rowtiles, hubs, first, bms);
-        TCMIS_LAUNCHED(ctx);
-      }
-      dev_free(bms);
+  if (nb == 0) return 0;
+  // lists: mid rows from the front, big rows from the back; cnt[0..1] list
+  // sizes, cnt[2..3] the dynamic work counters, cnt[4] the hub count.  Few
+  // enough block columns for one shared bitmap (R-MAT s22: nb = 2^18): every
+  // non-light row goes to k_count_mid's exact bitmap, no hashing.
+  p.bitmap = (int64_t)nb <= 32ll * kMidSlots ? 1 : 0;
+  if (int rc = dev_alloc(&p.lists, (size_t)nb)) return rc;
+  if (int rc = dev_alloc(&p.hubs, (size_t)nb)) return rc;
+  if (int rc = dev_alloc(&p.cnt, 8)) return rc;
+  TCMIS_CUDA(cudaMemsetAsync(p.cnt, 0, 8 * sizeof(int32_t), st));
+  return 0;
+}
+
+// light block rows of [b_lo, b_hi) counted, the rest listed (stream st)
+int k1_light(tcmis_graph *g, const K1Plan &p, int32_t b_lo, int32_t b_hi, cudaStream_t st) {
+  tcmis_ctx *ctx = g->ctx;
+  if (b_hi <= b_lo) return 0;
+  k_count_light<<<grid_for(ctx, 32ll * (b_hi - b_lo), kLightBlock, 8), kLightBlock, 0, st>>>(
+      g->n, p.T, p.nb, b_lo, b_hi, g->d_off, g->d_nbr, g->d_rowtiles, p.lists, p.cnt, p.bitmap,
+      p.hubs);
+  TCMIS_LAUNCHED(ctx);
+  return 0;
+}
+
+// The heavy rows k_count_light listed: hubs [hub_lo, hub_hi), mid rows
+// [mid_lo, mid_hi) of the front list and big rows [big_lo, big_hi) of the
+// back list, on stream st.  The work counters are set to the range starts so
+// the list can be processed in instalments as the light pass extends it.
+int k1_heavy(tcmis_graph *g, K1Plan &p, int32_t hub_lo, int32_t hub_hi, int32_t mid_lo,
+             int32_t mid_hi, int32_t big_lo, int32_t big_hi, cudaStream_t st) {
+  tcmis_ctx *ctx = g->ctx;
+  const int T = p.T;
+  const int32_t nb = p.nb;
+  if (hub_hi > hub_lo) {
+    // rowtiles[hub] was never written by k_count_light: start from 0
+    const size_t words = ((size_t)nb + 31) / 32;
+    if (!p.bms) {
+      if (int rc = dev_alloc(&p.bms, words * kHubBatch)) return rc;
     }
+    for (int first = hub_lo; first < hub_hi; first += kHubBatch) {
+      const int nh = std::min(kHubBatch, hub_hi - first);
+      TCMIS_CUDA(cudaMemsetAsync(p.bms, 0, 4 * words * nh, st));
+      k_count_hub<<<dim3(kHubCTAs, nh), 256, 0, st>>>(g->n, T, nb, g->d_off, g->d_nbr,
+                                                      g->d_rowtiles, p.hubs, first, p.bms);
+      TCMIS_LAUNCHED(ctx);
+    }
+  }
+  const int32_t starts[2] = {mid_lo, big_lo};
+  TCMIS_CUDA(cudaMemcpyAsync(p.cnt + 2, starts, sizeof(starts), cudaMemcpyHostToDevice, st));
+  if (mid_hi > mid_lo) {
     int mid_per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mid_per_sm, k_count_mid, kMidBlock, 0);
-    k_count_mid<<<ctx->num_sms * std::max(1, mid_per_sm), kMidBlock, 0, st>>>(
-        g->n, T, g->d_off, g->d_nbr, g->d_rowtiles, lists, cnt,
-        reinterpret_cast<unsigned *>(cnt + 2), bitmap);
+    const int64_t grid = std::min<int64_t>((int64_t)ctx->num_sms * std::max(1, mid_per_sm),
+                                           mid_hi - mid_lo);
+    k_count_mid<<<(int)grid, kMidBlock, 0, st>>>(g->n, T, g->d_off, g->d_nbr, g->d_rowtiles,
+                                                 p.lists, p.cnt,
+                                                 reinterpret_cast<unsigned *>(p.cnt + 2), p.bitmap);
     TCMIS_LAUNCHED(ctx);
+  }
+  if (big_hi > big_lo) {
     const size_t big_smem = sizeof(uint32_t) * kBigWords;
     TCMIS_CUDA(cudaFuncSetAttribute(k_count_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)big_smem));
     int big_per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&big_per_sm, k_count_big, kBigBlock, big_smem);
-    k_count_big<<<ctx->num_sms * std::max(1, big_per_sm), kBigBlock, big_smem, st>>>(
-        g->n, T, nb, g->d_off, g->d_nbr, g->d_rowtiles, lists + nb - 1, cnt + 1,
-        reinterpret_cast<unsigned *>(cnt + 3));
+    const int64_t grid = std::min<int64_t>((int64_t)ctx->num_sms * std::max(1, big_per_sm),
+                                           big_hi - big_lo);
+    k_count_big<<<(int)grid, kBigBlock, big_smem, st>>>(
+        g->n, T, nb, g->d_off, g->d_nbr, g->d_rowtiles, p.lists + nb - 1, p.cnt + 1,
+        reinterpret_cast<unsigned *>(p.cnt + 3));
     TCMIS_LAUNCHED(ctx);
-    dev_free(lists);
-    dev_free(hubs);
-    dev_free(cnt);
+  }
+  return 0;
+}
+
+// list sizes after the light passes so far: hub, mid, big (host sync of st)
+int k1_lists(K1Plan &p, cudaStream_t st, int32_t *hub, int32_t *mid, int32_t *big) {
+  int32_t c[5] = {0, 0, 0, 0, 0};
+  TCMIS_CUDA(cudaMemcpyAsync(c, p.cnt, sizeof(c), cudaMemcpyDeviceToHost, st));
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  *mid = c[0];
+  *big = c[1];
+  *hub = c[4];
+  return 0;
+}
+
+// the tile total, buffers released (context stream; after every pass)
+int k1_total(tcmis_graph *g, K1Plan &p) {
+  tcmis_ctx *ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  if (p.nb > 0) {
+    dev_free(p.bms);
+    dev_free(p.lists);
+    dev_free(p.hubs);
+    dev_free(p.cnt);
+    p.bms = nullptr;
+    p.lists = p.hubs = p.cnt = nullptr;
     unsigned long long *d_total = nullptr;
     if (int rc = dev_alloc(&d_total, 1)) return rc;
     cudaMemsetAsync(d_total, 0, 8, st);
-    k_sum_rowtiles<<<grid_for(ctx, nb, 256, 4), 256, 0, st>>>(g->d_rowtiles, nb, d_total);
+    k_sum_rowtiles<<<grid_for(ctx, p.nb, 256, 4), 256, 0, st>>>(g->d_rowtiles, p.nb, d_total);
     ctx->launches++;
     unsigned long long total = 0;
     cudaMemcpyAsync(&total, d_total, 8, cudaMemcpyDeviceToHost, st);
@@ -613,7 +673,105 @@ int build_tile_counts(tcmis_graph *g, int T) {
     if (e != cudaSuccess) return cuda_error(e, "tile counts");
     g->tile_total = (int64_t)total;
   }
-  g->tile_T = T;
+  g->tile_T = p.T;
+  return 0;
+}
+
+int build_tile_counts(tcmis_graph *g, int T) {
+  K1Plan p;
+  cudaStream_t st = g->ctx->stream;
+  if (int rc = k1_begin(g, T, p)) return rc;
+  if (p.nb > 0) {
+    if (int rc = k1_light(g, p, 0, p.nb, st)) return rc;
+    int32_t hub = 0, mid = 0, big = 0;
+    if (int rc = k1_lists(p, st, &hub, &mid, &big)) return rc;
+    if (int rc = k1_heavy(g, p, 0, hub, 0, mid, 0, big, st)) return rc;
+  }
+  return k1_total(g, p);
+}
+
+// Host CSR -> device graph with the K1 counts of tile_dim T, the count
+// overlapping the upload: the neighbour ids go up in chunks of block rows on
+// the context stream (copy engine) and a side stream counts each chunk's
+// light rows as soon as it has landed; the hub / mid / big rows follow the
+// last chunk.  The drop-in path's upload + tile_graph in one call.
+int upload_tiled(tcmis_ctx *ctx, int32_t n, const int64_t *off, const int32_t *nbr, int T,
+                 tcmis_graph **out) {
+  *out = nullptr;
+  if (T < 1 || T > 64)
+    return set_error(TCMIS_E_INVALID_ARGUMENT,
+                     "tile_dim must be in [1, 64], got " + std::to_string(T));
+  cudaStream_t st = ctx->stream;
+  const int64_t nnz = off ? off[n] : 0;
+  int64_t *d_off = nullptr;
+  int32_t *d_nbr = nullptr;
+  if (int rc = dev_alloc(&d_off, (size_t)n + 1)) return rc;
+  if (int rc = dev_alloc(&d_nbr, (size_t)nnz)) {
+    dev_free(d_off);
+    return rc;
+  }
+  if (off) TCMIS_CUDA(cudaMemcpyAsync(d_off, off, 8ull * (n + 1), cudaMemcpyHostToDevice, st));
+  else TCMIS_CUDA(cudaMemsetAsync(d_off, 0, 8, st));
+  tcmis_graph *g = nullptr;
+  if (int rc = wrap_owned(ctx, n, nnz, d_off, d_nbr, &g)) return rc;
+  *out = g;
+  K1Plan p;
+  if (int rc = k1_begin(g, T, p)) return rc;
+  if (p.nb > 0) {  // hub bitmaps up front: the side stream must not allocate
+    if (int rc = dev_alloc(&p.bms, (((size_t)p.nb + 31) / 32) * kHubBatch)) return rc;
+  }
+  if (!ctx->side) {
+    TCMIS_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    for (cudaEvent_t &e : ctx->side_ev)
+      TCMIS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  // ~16M ids per chunk, at most 8 chunks, cut at block-row boundaries.  All
+  // copies are enqueued first (copy engine, context stream); the side stream
+  // then counts chunk by chunk -- light rows, then the heavy rows the light
+  // pass listed -- each chunk as soon as its ids have landed.
+  const int K = (int)std::min<int64_t>(kUploadChunks, std::max<int64_t>(1, nnz >> 24));
+  std::vector<int32_t> bnd{0};
+  for (int c = 1; c <= K && p.nb > 0; ++c) {
+    int32_t b_c = p.nb;
+    if (c < K) {
+      const int64_t want = nnz * c / K;
+      int32_t lo = bnd.back(), hi = p.nb;  // first block row whose first entry >= want
+      while (lo < hi) {
+        const int32_t mid = lo + (hi - lo) / 2;
+        if (off[std::min<int64_t>(n, (int64_t)mid * T)] < want) lo = mid + 1;
+        else hi = mid;
+      }
+      b_c = lo;
+    }
+    if (b_c > bnd.back()) bnd.push_back(b_c);
+  }
+  const int chunks = (int)bnd.size() - 1;
+  for (int c = 0; c < chunks; ++c) {
+    const int64_t e0 = off[(int64_t)bnd[c] * T];
+    const int64_t e1 = off[std::min<int64_t>(n, (int64_t)bnd[c + 1] * T)];
+    if (e1 > e0)
+      TCMIS_CUDA(cudaMemcpyAsync(d_nbr + e0, nbr + e0, 4ull * (e1 - e0), cudaMemcpyHostToDevice, st));
+    TCMIS_CUDA(cudaEventRecord(ctx->side_ev[c], st));
+  }
+  if (p.nb == 0 && nnz)
+    TCMIS_CUDA(cudaMemcpyAsync(d_nbr, nbr, 4ull * nnz, cudaMemcpyHostToDevice, st));
+  int32_t hub0 = 0, mid0 = 0, big0 = 0;
+  for (int c = 0; c < chunks; ++c) {
+    TCMIS_CUDA(cudaStreamWaitEvent(ctx->side, ctx->side_ev[c], 0));
+    if (int rc = k1_light(g, p, bnd[c], bnd[c + 1], ctx->side)) return rc;
+    int32_t hub = 0, mid = 0, big = 0;
+    if (int rc = k1_lists(p, ctx->side, &hub, &mid, &big)) return rc;
+    if (int rc = k1_heavy(g, p, hub0, hub, mid0, mid, big0, big, ctx->side)) return rc;
+    hub0 = hub;
+    mid0 = mid;
+    big0 = big;
+  }
+  if (chunks > 0) {
+    TCMIS_CUDA(cudaEventRecord(ctx->side_ev[kUploadChunks], ctx->side));
+    TCMIS_CUDA(cudaStreamWaitEvent(st, ctx->side_ev[kUploadChunks], 0));
+  }
+  if (int rc = k1_total(g, p)) return rc;
+  TCMIS_CUDA(cudaStreamSynchronize(st));
   return 0;
 }
 

@@ -527,3 +527,34 @@ def test_graph_from_edges_on_device(ctx):
         assert np.array_equal(h.neighbors, want.nbr)
     with pytest.raises(IndexError):
         tc.DeviceGraph.from_edges(10, np.array([[0, 10]], np.int32), ctx)
+
+
+@pytest.mark.parametrize("scale,T", [(21, 16), (14, 16), (14, 8), (14, 1)])
+def test_upload_tiled_counts(ctx, scale, T):
+    """tcmis_graph_upload_tiled: the K1 count overlapped with a chunked upload
+    (3 chunks of block rows at s21, one at s14) gives tile_graph's tiles per
+    block row (tiling.cpp:44-84), and the solve's tile counters follow."""
+    g = O.gen("rmat", scale, 16, 1)
+    want = O.tile_row_counts(g, T)
+    dg = tc.DeviceGraph.upload(as_tc(g), ctx, tile_dim=T)
+    a = tc.tile_graph(dg, T)  # cached counts of the upload: no recount
+    assert np.array_equal(np.diff(a.block_row_offsets), want)
+    exp = O.solve(g, "h2", 1, tile_dim=T)
+    got = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=1, tile_dim=T))
+    assert rounds_tuple(got.iterations) == oracle_tuple(exp)
+    dg.close()
+
+
+def test_upload_tiled_edge_cases(ctx):
+    empty = tc.DeviceGraph.upload(tc.Graph(0, np.zeros(1, np.int64), np.zeros(0, np.int32)),
+                                  ctx, tile_dim=16)
+    assert empty.tile(16) == 0
+    iso = tc.DeviceGraph.upload(tc.Graph(100, np.zeros(101, np.int64), np.zeros(0, np.int32)),
+                                ctx, tile_dim=16)
+    assert iso.tile(16) == 0
+    r = tc.run_mis(iso, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=1, tile_dim=16))
+    assert len(r.mis) == 100
+    g = O.gen("petersen")
+    for bad in (0, 65):
+        with pytest.raises(Exception):
+            tc.DeviceGraph.upload(as_tc(g), ctx, tile_dim=bad)
