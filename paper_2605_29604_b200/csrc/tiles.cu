@@ -734,7 +734,10 @@ int upload_tiled(tcmis_ctx *ctx, int32_t n, const int64_t *off, const int32_t *n
   for (int c = 1; c <= K && p.nb > 0; ++c) {
     int32_t b_c = p.nb;
     if (c < K) {
-      const int64_t want = nnz * c / K;
+      // shrinking chunks (boundary at 1 - (1 - c/K)^2 of the ids): the count of
+      // the last chunk, which nothing overlaps, is the smallest
+      const double f = 1.0 - (1.0 - (double)c / K) * (1.0 - (double)c / K);
+      const int64_t want = (int64_t)(f * (double)nnz);
       int32_t lo = bnd.back(), hi = p.nb;  // first block row whose first entry >= want
       while (lo < hi) {
         const int32_t mid = lo + (hi - lo) / 2;
