@@ -15,6 +15,11 @@ constexpr int kThreadMax = TCMIS_THREAD_MAX;  // entries a thread examines befor
 #ifndef TCMIS_SEL_WIN2
 #define TCMIS_SEL_WIN2 1
 #endif
+// 16-byte windows per step of the per-lane scan engines (k_select, k_update_pull)
+#ifndef TCMIS_SEL_WIN
+#define TCMIS_SEL_WIN (TCMIS_SEL_WIN2 ? 2 : 1)
+#endif
+constexpr int kSelWin = TCMIS_SEL_WIN;
 #ifndef TCMIS_WARP_U
 #define TCMIS_WARP_U 8
 #endif

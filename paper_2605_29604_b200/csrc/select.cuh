@@ -127,6 +127,12 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
 // Engine: the probe's undecided rows, one lane per row as a per-lane state
 // machine (scan down in 16-byte windows from e - kProbeK; push up), so a
 // lane never idles behind another lane's longer row.
+// kWin 16-byte windows per step.  Four on graphs whose q vector outgrows a
+// good part of L2 (more gathers in flight per lane against the misses: R-MAT
+// s26 round 1 1.07 -> 0.93 ms); two elsewhere (s22: 57 / 55 / 61 us for two /
+// three / four, and the pull engine is best at two everywhere).
+constexpr int32_t kSelWideN = 1 << 25;
+template <int kWin>
 __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a) {
   pdl_entry();
   Ctrl *ctrl = a.ctrl;
@@ -159,16 +165,19 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
   while (__any_sync(0xffffffffu, mode != kDone)) {
     bool defer = false;
     if (mode == kScan) {
-      // two 16-byte windows per step: 8 entries and their q gathers in flight
-      int32_t u[8];
+      // kWin 16-byte windows per step: 4 kWin entries and their q gathers in flight
+      constexpr int kU = 4 * kWin;
+      int32_t u[kU];
       int64_t w = load_window_down(nbr, a.vnnz, s, hi, u);
-#if TCMIS_SEL_WIN2
-      if (w > s) w = load_window_down(nbr, a.vnnz, s, w, u + 4);
-      else u[4] = u[5] = u[6] = u[7] = -1;
-      constexpr int kU = 8;
-#else
-      constexpr int kU = 4;
-#endif
+#pragma unroll
+      for (int k = 1; k < kWin; ++k) {
+        if (w > s) {
+          w = load_window_down(nbr, a.vnnz, s, w, u + 4 * k);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) u[4 * k + j] = -1;
+        }
+      }
       bool blocked = false;
 #pragma unroll
       for (int j = 0; j < kU; ++j)

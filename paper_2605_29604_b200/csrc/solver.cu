@@ -684,7 +684,9 @@ int launch_select(tcmis_graph *g, const RoundArgs &a) {
     TCMIS_CUDA(cudaMemsetAsync(g->ws.cbits, 0, 4 * ((size_t)a.n / 32 + 1), st));
   TCMIS_TIMED(ctx, "k_probe_select", (launch_round_kernel(k_probe_select, a.sel_grid, st, s)));
   TCMIS_LAUNCHED(ctx);
-  TCMIS_TIMED(ctx, "k_select", (launch_round_kernel(k_select, a.sel_grid, st, s)));
+  TCMIS_TIMED(ctx, "k_select",
+              (launch_round_kernel(a.n >= kSelWideN ? k_select<4> : k_select<kSelWin>,
+                                   a.sel_grid, st, s)));
   TCMIS_LAUNCHED(ctx);
   TCMIS_TIMED(ctx, "k_select_long", (launch_round_kernel(k_select_long, a.sel_grid, st, s)));
   TCMIS_LAUNCHED(ctx);

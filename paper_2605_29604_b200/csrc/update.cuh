@@ -230,15 +230,18 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
   while (__any_sync(0xffffffffu, mode != kDone)) {
     bool survive = false, defer = false;
     if (mode == kScan) {
-      int32_t u[8];
+      constexpr int kU = 4 * kSelWin;
+      int32_t u[kU];
       int64_t w = load_window_down(nbr, a.vnnz, s, hi, u);
-#if TCMIS_SEL_WIN2
-      if (w > s) w = load_window_down(nbr, a.vnnz, s, w, u + 4);
-      else u[4] = u[5] = u[6] = u[7] = -1;
-      constexpr int kU = 8;
-#else
-      constexpr int kU = 4;
-#endif
+#pragma unroll
+      for (int k = 1; k < kSelWin; ++k) {
+        if (w > s) {
+          w = load_window_down(nbr, a.vnnz, s, w, u + 4 * k);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) u[4 * k + j] = -1;
+        }
+      }
       bool hit = false;
 #pragma unroll
       for (int j = 0; j < kU; ++j)
