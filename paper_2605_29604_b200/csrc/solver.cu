@@ -91,18 +91,26 @@ __global__ void __launch_bounds__(256)
     uint64_t x = mseed + (uint64_t)(v0 + 1) * kGolden;  // vertex_hash, priorities.cpp:21-23
 #pragma unroll
     for (int j = 0; j < kPrioV; ++j, x += kGolden) {
-      const uint64_t h = mix64(x);
       const int32_t deg = (int32_t)(o[j + 1] - o[j]);
-      if (mode == 0) {
-        pv[j] = (uint32_t)(h >> 32);
-      } else {
-        const double eps = (double)(h >> 11) * 0x1.0p-53;  // hash_to_unit, priorities.cpp:25-27
-        pv[j] = h2_value(avg, deg, eps, scale);
-      }
       // an isolated vertex has no alive neighbour: it is a round-1 candidate
       // (engine.cpp:94-99 leaves max_np at kNoNeighborKey) and round 1's
       // select never has to visit it
       const bool iso = next && deg == 0 && v0 + j < n;
+      if (iso) {
+        // nobody's neighbour, so its key is never compared: no hash or FP64
+        // work (the kernel is instruction-bound; R-MAT's isolated vertices
+        // fill whole warps at the high ids).  tcmis_priorities (next == null)
+        // still computes every p.
+        pv[j] = 0;
+      } else {
+        const uint64_t h = mix64(x);
+        if (mode == 0) {
+          pv[j] = (uint32_t)(h >> 32);
+        } else {
+          const double eps = (double)(h >> 11) * 0x1.0p-53;  // hash_to_unit, priorities.cpp:25-27
+          pv[j] = h2_value(avg, deg, eps, scale);
+        }
+      }
       st4 |= (uint32_t)(iso ? TCMIS_IN_MIS : TCMIS_ALIVE) << (8 * j);
       nx4 |= (uint32_t)(iso ? 1 : 0) << (8 * j);
       if (iso && segflag) segflag[tshift >= 0 ? (v0 + j) >> tshift : (v0 + j) / T] = 1;
