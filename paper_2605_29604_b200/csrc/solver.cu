@@ -719,9 +719,14 @@ int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle
     else
       TCMIS_TIMED(ctx, "k_tile_excl_bits", (k_tile_excl_bits<<<grid, 256, 0, st>>>(t)));
     TCMIS_LAUNCHED(ctx);
-    TCMIS_TIMED(ctx, "k_update", (launch_round_kernel(k_update, a.upd_grid, st, u)));
+    TCMIS_TIMED(ctx, "k_update",
+                (launch_round_kernel(k_update<false>, a.upd_grid, st, u, cond, 0)));
   } else {
-    TCMIS_TIMED(ctx, "k_update", (launch_round_kernel(k_update, a.upd_grid, st, u)));
+    // push: the update kernel ends the round itself
+    TCMIS_TIMED(ctx, "k_update",
+                (launch_round_kernel(k_update<true>, a.upd_grid, st, u, cond, use_cond)));
+    TCMIS_LAUNCHED(ctx);
+    return 0;
   }
   TCMIS_LAUNCHED(ctx);
   TCMIS_TIMED(ctx, "k_round_end", (launch_round_kernel(k_round_end, a.upd_grid, st, u, cond, use_cond)));
@@ -729,7 +734,7 @@ int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle
   return 0;
 }
 
-inline int launches_per_round(const RoundArgs &a) { return (a.pull || a.tile) ? 6 : 5; }
+inline int launches_per_round(const RoundArgs &a) { return (a.pull || a.tile) ? 6 : 4; }
 
 // The parameters of a solve's first kernels (segment-flag clear,
 // k_priorities with the control-block init), part of the graph's cache key.

@@ -71,9 +71,95 @@ struct UpdateArgs {
   int32_t tail_thr;        // the WHILE loop continues while alive > tail_thr
 };
 
+// The end of a round, run by every block of the round's last kernel: the
+// segment flags swept into the tile counters, the block's counts added, and
+// the last block to arrive publishes the round's DevRound, resets the
+// per-round counters and sets the graph's loop condition.
+__device__ __forceinline__ void round_end_tail(const UpdateArgs &a, unsigned long long rem,
+                                               cudaGraphConditionalHandle cond, int use_cond) {
+  Ctrl *ctrl = a.ctrl;
+  const int round = ctrl->round;
+  const int out_slot = (round + 1) & 1;
+  unsigned long long ev = 0;
+  if (a.seg_mode == 1) {  // spmv.cpp:37-46, per block column (A is symmetric)
+    // 16 flags per thread with one 16-byte load (the sweep is one pass, not a
+    // grid-stride chain of byte loads); tile counts only for the set flags
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    int64_t head = 0;
+    if ((((uintptr_t)a.segflag | (uintptr_t)a.rowtiles) & 15) == 0) {
+      const int64_t nv = a.nseg / 16;
+      for (int64_t c = gt; c < nv; c += gs) {
+        uint4 *fp = reinterpret_cast<uint4 *>(a.segflag + 16 * c);
+        const uint4 f = *fp;
+        if (!(f.x | f.y | f.z | f.w)) continue;
+        const uint32_t w[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (!w[k]) continue;
+          const int4 t = __ldg(reinterpret_cast<const int4 *>(a.rowtiles + 16 * c + 4 * k));
+          if (w[k] & 0xffu) ev += (unsigned long long)t.x;
+          if (w[k] & 0xff00u) ev += (unsigned long long)t.y;
+          if (w[k] & 0xff0000u) ev += (unsigned long long)t.z;
+          if (w[k] & 0xff000000u) ev += (unsigned long long)t.w;
+        }
+        *fp = make_uint4(0, 0, 0, 0);
+      }
+      head = nv * 16;
+    }
+    for (int64_t b = head + gt; b < a.nseg; b += gs) {
+      if (a.segflag[b]) {
+        ev += (unsigned long long)a.rowtiles[b];
+        a.segflag[b] = 0;
+      }
+    }
+  }
+  block_add3(0, rem, ev, ctrl);
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&ctrl->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    volatile Ctrl *vc = ctrl;
+    const int32_t alive = vc->wl_count[out_slot];
+    DevRound r;
+    r.sel = vc->sel;
+    r.rem = vc->rem;
+    r.alive = (unsigned long long)alive;
+    r.eval = a.seg_mode == 1 ? vc->eval : 0;
+    r.skip = a.seg_mode == 1 ? (unsigned long long)a.total_tiles - vc->eval : 0;
+    // a ring: the host loop drains one slot per round; the graph loop flags
+    // the (pathological, > max_rounds) case and the host re-runs step-wise
+    a.rounds[(round - 1) % vc->max_rounds] = r;
+    if (round > vc->max_rounds) vc->overflow = 1;
+    vc->alive = alive;
+    vc->sel = 0;
+    vc->rem = 0;
+    vc->eval = 0;
+    vc->ticket = 0;
+    vc->wl_count[round & 1] = 0;
+    vc->long_count = 0;
+    vc->pull_count = 0;
+    vc->sel_vlong = 0;
+    vc->pull_items = 0;
+    vc->sel_undec = 0;
+    vc->pull_undec = 0;
+    vc->main_rounds = vc->main_rounds + 1;
+    vc->round = round + 1;
+    if (use_cond) cudaGraphSetConditional(cond, alive > a.tail_thr ? 1u : 0u);
+  }
+}
+
 // ---------------------------------------------------------------- push
 
-__global__ void __launch_bounds__(kBlock) k_update(UpdateArgs a) {
+// kEnd: the push round's last kernel also ends the round (round_end_tail),
+// so the push form runs no separate k_round_end.
+template <bool kEnd>
+__global__ void __launch_bounds__(kBlock)
+    k_update(UpdateArgs a, cudaGraphConditionalHandle cond, int use_cond) {
   pdl_entry();
   using BlockScan = cub::BlockScan<int, kBlock>;
   __shared__ typename BlockScan::TempStorage scan_tmp;
@@ -82,7 +168,7 @@ __global__ void __launch_bounds__(kBlock) k_update(UpdateArgs a) {
   const int round = ctrl->round;
   const int64_t cnt = round == 1 ? a.n : ctrl->wl_count[round & 1];
   constexpr int64_t kChunk = (int64_t)kBlock * kUpdItems;
-  if ((int64_t)blockIdx.x * kChunk >= cnt) return;
+  if (!kEnd && (int64_t)blockIdx.x * kChunk >= cnt) return;  // kEnd: every block ends the round
   const int32_t *in = (round & 1) ? a.wl1 : a.wl0;
   int32_t *out = (round & 1) ? a.wl0 : a.wl1;
   const int out_slot = (round + 1) & 1;
@@ -130,7 +216,8 @@ __global__ void __launch_bounds__(kBlock) k_update(UpdateArgs a) {
       if (vs[j] >= 0 && ds[j] == 0) out[pos++] = vs[j];
     __syncthreads();  // scan_tmp / s_base reuse
   }
-  block_add3(0, rem, 0, ctrl);
+  if (kEnd) round_end_tail(a, rem, cond, use_cond);
+  else block_add3(0, rem, 0, ctrl);
 }
 
 // ---------------------------------------------------------------- pull
@@ -290,7 +377,7 @@ __global__ void __launch_bounds__(kBlock)
   const uint64_t fresh_m = a.fresh ? mix64(combine_seed(a.seed, (uint64_t)round + 1)) : 0;
   const int32_t *__restrict__ nbr = a.nbr;
   const uint8_t *__restrict__ next = a.next;
-  unsigned long long rem = 0, ev = 0;
+  unsigned long long rem = 0;
   // pull rows that outlived the engine, one chunk of kPullChunk entries per
   // warp (chunk c covers [hi - (c+1) kPullChunk, hi - c kPullChunk) of the
   // row); a chunk stops at its first candidate neighbour or once another
@@ -340,76 +427,7 @@ __global__ void __launch_bounds__(kBlock)
       }
     }
   }
-  if (a.seg_mode == 1) {  // spmv.cpp:37-46, per block column (A is symmetric)
-    // 16 flags per thread with one 16-byte load (the sweep is one pass, not a
-    // grid-stride chain of byte loads); tile counts only for the set flags
-    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
-    int64_t head = 0;
-    if ((((uintptr_t)a.segflag | (uintptr_t)a.rowtiles) & 15) == 0) {
-      const int64_t nv = a.nseg / 16;
-      for (int64_t c = gt; c < nv; c += gs) {
-        uint4 *fp = reinterpret_cast<uint4 *>(a.segflag + 16 * c);
-        const uint4 f = *fp;
-        if (!(f.x | f.y | f.z | f.w)) continue;
-        const uint32_t w[4] = {f.x, f.y, f.z, f.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (!w[k]) continue;
-          const int4 t = __ldg(reinterpret_cast<const int4 *>(a.rowtiles + 16 * c + 4 * k));
-          if (w[k] & 0xffu) ev += (unsigned long long)t.x;
-          if (w[k] & 0xff00u) ev += (unsigned long long)t.y;
-          if (w[k] & 0xff0000u) ev += (unsigned long long)t.z;
-          if (w[k] & 0xff000000u) ev += (unsigned long long)t.w;
-        }
-        *fp = make_uint4(0, 0, 0, 0);
-      }
-      head = nv * 16;
-    }
-    for (int64_t b = head + gt; b < a.nseg; b += gs) {
-      if (a.segflag[b]) {
-        ev += (unsigned long long)a.rowtiles[b];
-        a.segflag[b] = 0;
-      }
-    }
-  }
-  block_add3(0, rem, ev, ctrl);
-  __shared__ bool last;
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(&ctrl->ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    volatile Ctrl *vc = ctrl;
-    const int32_t alive = vc->wl_count[out_slot];
-    DevRound r;
-    r.sel = vc->sel;
-    r.rem = vc->rem;
-    r.alive = (unsigned long long)alive;
-    r.eval = a.seg_mode == 1 ? vc->eval : 0;
-    r.skip = a.seg_mode == 1 ? (unsigned long long)a.total_tiles - vc->eval : 0;
-    // a ring: the host loop drains one slot per round; the graph loop flags
-    // the (pathological, > max_rounds) case and the host re-runs step-wise
-    a.rounds[(round - 1) % vc->max_rounds] = r;
-    if (round > vc->max_rounds) vc->overflow = 1;
-    vc->alive = alive;
-    vc->sel = 0;
-    vc->rem = 0;
-    vc->eval = 0;
-    vc->ticket = 0;
-    vc->wl_count[round & 1] = 0;
-    vc->long_count = 0;
-    vc->pull_count = 0;
-    vc->sel_vlong = 0;
-    vc->pull_items = 0;
-    vc->sel_undec = 0;
-    vc->pull_undec = 0;
-    vc->main_rounds = vc->main_rounds + 1;
-    vc->round = round + 1;
-    if (use_cond) cudaGraphSetConditional(cond, alive > a.tail_thr ? 1u : 0u);
-  }
+  round_end_tail(a, rem, cond, use_cond);
 }
 
 }  // namespace tcmis_b200
