@@ -257,11 +257,18 @@ __device__ void compact_mis(const TailArgs &a) {
   __shared__ int s_woff[kTailBlock / 32 + 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t v_lo = u0 * 16, v_hi = min((int64_t)a.n, u1 * 16);
-  for (int64_t t0 = v_lo; t0 < v_hi; t0 += 256ll * (kTailBlock / 32)) {
+  constexpr int64_t kStep = 256ll * (kTailBlock / 32);
+  // the next tile's 8 states per lane are loaded before this tile's barriers
+  uint2 xn = make_uint2(0, 0);
+  if (v_lo + (int64_t)w * 256 + lane * 8 < v_hi)
+    xn = __ldcg(reinterpret_cast<const uint2 *>(a.state + v_lo + (int64_t)w * 256 + lane * 8));
+  for (int64_t t0 = v_lo; t0 < v_hi; t0 += kStep) {
     const int64_t v0 = t0 + (int64_t)w * 256 + lane * 8;
+    const uint2 x = xn;
+    if (v0 + kStep < v_hi)
+      xn = __ldcg(reinterpret_cast<const uint2 *>(a.state + v0 + kStep));
     uint32_t m = 0;
     if (v0 < v_hi) {
-      const uint2 x = __ldcg(reinterpret_cast<const uint2 *>(a.state + v0));
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if (((x.x >> (8 * j)) & 0xffu) == TCMIS_IN_MIS) m |= 1u << j;
@@ -286,14 +293,17 @@ __device__ void compact_mis(const TailArgs &a) {
       stage[w][k++] = (int32_t)(v0 + bit);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {  // exclusive scan of the 32 warp counts
-      int acc = 0;
-      for (int i = 0; i < kTailBlock / 32; ++i) {
-        const int t = s_woff[i];
-        s_woff[i] = acc;
-        acc += t;
+    if (w == 0) {  // exclusive scan of the 32 warp counts, by shuffles
+      static_assert(kTailBlock / 32 == 32, "one warp count per lane");
+      const int t = s_woff[lane];
+      int sc = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, sc, o);
+        if (lane >= o) sc += y;
       }
-      s_woff[kTailBlock / 32] = acc;
+      s_woff[lane] = sc - t;
+      if (lane == 31) s_woff[32] = sc;
     }
     __syncthreads();
     const int wc = (w + 1 < kTailBlock / 32 ? s_woff[w + 1] : s_woff[kTailBlock / 32]) - s_woff[w];
