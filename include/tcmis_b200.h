@@ -150,9 +150,12 @@ int tcmis_graph_download(tcmis_graph *g, int64_t *offsets, int32_t *neighbors);
  * graph.  *tile_count receives TiledAdjacency::tile_count(). */
 int tcmis_graph_tile(tcmis_graph *g, int32_t tile_dim, int64_t *tile_count);
 /* Same, from a TiledAdjacency the caller already holds (the prebuilt-tiles
- * overload engine.hpp:111-112): block_row_offsets has n_block_rows+1 entries. */
+ * overload engine.hpp:111-112): block_row_offsets has n_block_rows+1 entries,
+ * tile_col tile_count entries.  The tile counters of the solve are taken on
+ * exactly this tile set (tiles per block column, spmv.cpp:37-46), whatever
+ * tiling produced it; a column outside [0, n_block_rows) is rejected. */
 int tcmis_graph_set_tiling(tcmis_graph *g, int32_t tile_dim, const int64_t *block_row_offsets,
-                           int32_t n_block_rows);
+                           int32_t n_block_rows, const int32_t *tile_col, int64_t tile_count);
 /* Full tile materialisation in the reference layout (tile_row, tile_col,
  * T u64 row words per tile, block_row_offsets[nb+1]); host buffers sized from
  * tcmis_graph_tile()'s count. */

@@ -307,10 +307,16 @@ class Solve:
 
 
 def luby_rounds(g: Graph, p, fresh: bool = False, seed: int = 1, T: int | None = None,
-                max_rounds: int = 4096) -> Solve:
-    """Round-by-round oracle (engine.cpp:231-295 / 301-352)."""
+                max_rounds: int = 4096, col_counts=None) -> Solve:
+    """Round-by-round oracle (engine.cpp:231-295 / 301-352).  The tile
+    counters count, per round, the tiles whose block column holds a candidate
+    (spmv.cpp:37-46): `col_counts` = tiles per block column of the tiling
+    (default tile_graph(g, T)'s, where columns and rows count alike)."""
     L = lib()
-    rt = tile_row_counts(g, T) if T else None
+    rt = None
+    if T:
+        rt = (tile_row_counts(g, T) if col_counts is None
+              else np.ascontiguousarray(col_counts, np.int64))
     st = np.zeros(max(g.n, 1), np.uint8)
     rounds = (OrcRound * max_rounds)()
     nbr = g.nbr if g.nbr.size else np.zeros(1, np.int32)

@@ -131,7 +131,7 @@ def load():
         "tcmis_graph_device_neighbors": (vp, [vp]),
         "tcmis_graph_download": (C.c_int, [vp, vp, vp]),
         "tcmis_graph_tile": (C.c_int, [vp, i32, P(i64)]),
-        "tcmis_graph_set_tiling": (C.c_int, [vp, i32, vp, i32]),
+        "tcmis_graph_set_tiling": (C.c_int, [vp, i32, vp, i32, vp, i64]),
         "tcmis_graph_export_tiles": (C.c_int, [vp, i32, vp, vp, vp, vp]),
         "tcmis_graph_tile_store": (C.c_int, [vp, i32, P(i64), vp, vp, vp]),
         "tcmis_validate": (C.c_int, [vp, vp, i64, P(i32), P(i32), P(i32), P(i32), P(i32)]),
@@ -507,8 +507,9 @@ def run_tc_mis(g, tiled=None, config: Optional[EngineConfig] = None,
         if tiled.tile_dim != cfg.tile_dim:  # spmv.cpp:22-24, raised in round 1
             raise ValueError("tiled adjacency and vector disagree on tile layout")
         bro = np.ascontiguousarray(tiled.block_row_offsets, np.int64)
+        tcol = np.ascontiguousarray(tiled.tile_col, np.int32)
         _check(load().tcmis_graph_set_tiling(dg.h, int(tiled.tile_dim), _ptr(bro),
-                                             int(bro.size - 1)))
+                                             int(bro.size - 1), _ptr(tcol), int(tcol.size)))
     return _solve(dg, cfg)
 
 

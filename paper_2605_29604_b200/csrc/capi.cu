@@ -253,6 +253,7 @@ TCMIS_API void tcmis_graph_destroy(tcmis_graph *g) {
   dev_free(g->d_rowtiles);
   dev_free(g->d_nz);
   dev_free(g->d_off_full);
+  free_dist(g);
   free_tile_store(g);
   Workspace &sp = g->ctx->spare;
   if (g->ws.ctrl && g->ws.n_cap >= sp.n_cap) {
@@ -294,22 +295,35 @@ TCMIS_API int tcmis_graph_tile(tcmis_graph *g, int32_t tile_dim, int64_t *tile_c
 }
 
 TCMIS_API int tcmis_graph_set_tiling(tcmis_graph *g, int32_t T, const int64_t *bro,
-                                     int32_t nb) {
+                                     int32_t nb, const int32_t *tile_col, int64_t tile_count) {
   NEED(g, "null graph");
+  ENTER(g->ctx);
   if (T < 1 || T > 64)
     return set_error(TCMIS_E_INVALID_ARGUMENT,
                      "tile_dim must be in [1, 64], got " + std::to_string(T));
   NEED(nb == (int32_t)(((int64_t)g->n + T - 1) / T), "tiled adjacency built for a different graph");
   NEED(nb == 0 || bro, "null block_row_offsets");
-  std::vector<int32_t> rt((size_t)nb + 1, 0);
-  for (int32_t b = 0; b < nb; ++b) rt[b] = (int32_t)(bro[b + 1] - bro[b]);
+  NEED(tile_count == 0 || tile_col, "null tile_col");
+  NEED(nb == 0 || bro[nb] - bro[0] == tile_count, "block_row_offsets disagree with tile_count");
+  // The counters of tiled_spmv (spmv.cpp:37-46) are defined on THIS tiling:
+  // a tile is evaluated iff the segment of its block column holds a
+  // candidate, so the device keeps tiles per block column, counted from the
+  // caller's tile_col (any tile set, not only tile_graph(g)'s symmetric one).
+  std::vector<int32_t> ct((size_t)nb + 1, 0);
+  for (int64_t t = 0; t < tile_count; ++t) {
+    const int32_t c = tile_col[t];
+    if (c < 0 || c >= nb) return set_error(TCMIS_E_INVALID_ARGUMENT, "tile column out of range");
+    ++ct[(size_t)c];
+  }
   dev_free(g->d_rowtiles);
   g->d_rowtiles = nullptr;
   g->tile_T = 0;
   if (int rc = dev_alloc(&g->d_rowtiles, (size_t)nb + 1)) return rc;
-  TCMIS_CUDA(cudaMemcpy(g->d_rowtiles, rt.data(), 4ull * (nb + 1), cudaMemcpyHostToDevice));
+  TCMIS_CUDA(cudaMemcpyAsync(g->d_rowtiles, ct.data(), 4ull * (nb + 1), cudaMemcpyHostToDevice,
+                             g->ctx->stream));
+  TCMIS_CUDA(cudaStreamSynchronize(g->ctx->stream));
   g->tile_nb = nb;
-  g->tile_total = nb ? bro[nb] - bro[0] : 0;
+  g->tile_total = tile_count;
   g->tile_T = T;
   return 0;
 }

@@ -108,12 +108,17 @@ struct DistState {
   int32_t *d_rank_lo = nullptr;      // ... and its device mirror (uploaded once)
 };
 
+// owned by the graph (created on first use, freed by tcmis_graph_destroy)
 static DistState &dist_state(tcmis_graph *g) {
-  static thread_local std::vector<std::pair<tcmis_graph *, DistState>> states;
-  for (auto &p : states)
-    if (p.first == g) return p.second;
-  states.emplace_back(g, DistState{});
-  return states.back().second;
+  if (!g->dist) g->dist = new DistState{};
+  return *g->dist;
+}
+
+void free_dist(tcmis_graph *g) {
+  if (!g->dist) return;
+  dev_free(g->dist->d_rank_lo);
+  delete g->dist;
+  g->dist = nullptr;
 }
 
 int dist_begin(tcmis_graph *g, const tcmis_config *cfg) {

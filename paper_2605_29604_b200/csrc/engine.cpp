@@ -36,24 +36,58 @@ void check(int code) {
   if (code != TCMIS_OK) raise(code);
 }
 
-tcmis_ctx *context() {
-  static std::once_flag once;
-  static tcmis_ctx *ctx = nullptr;
-  static int status = TCMIS_OK;
-  std::call_once(once, [] { status = tcmis_ctx_create(0, &ctx); });
-  if (status != TCMIS_OK) raise(status);
-  return ctx;
-}
+// Device contexts of the drop-in calls.  A context (one stream, one spare
+// workspace, the cached round graph) is not re-entrant, while the reference's
+// free functions may run concurrently on different graphs; so every call
+// leases a context of its own for its whole duration from a process-wide
+// pool (created on first use, returned when the call ends, never destroyed:
+// the CUDA runtime may already be gone at exit).  One thread at a time re-uses
+// the same warm context.
+class ContextLease {
+ public:
+  ContextLease() {
+    {
+      std::lock_guard<std::mutex> lk(mu());
+      if (!pool().empty()) {
+        ctx_ = pool().back();
+        pool().pop_back();
+        return;
+      }
+    }
+    check(tcmis_ctx_create(0, &ctx_));
+  }
+  ~ContextLease() {
+    std::lock_guard<std::mutex> lk(mu());
+    pool().push_back(ctx_);
+  }
+  ContextLease(const ContextLease &) = delete;
+  ContextLease &operator=(const ContextLease &) = delete;
+  tcmis_ctx *get() const { return ctx_; }
 
+ private:
+  static std::mutex &mu() {
+    static std::mutex m;
+    return m;
+  }
+  static std::vector<tcmis_ctx *> &pool() {
+    static auto *p = new std::vector<tcmis_ctx *>();
+    return *p;
+  }
+  tcmis_ctx *ctx_ = nullptr;
+};
+
+// A graph uploaded for one call, on a context leased for that call (the
+// lease is declared first, so it outlives the graph).
 struct DeviceGraph {
+  ContextLease lease;
   tcmis_graph *h = nullptr;
   explicit DeviceGraph(const Graph &g) {
-    check(tcmis_graph_upload(context(), g.n, g.offsets.empty() ? nullptr : g.offsets.data(),
+    check(tcmis_graph_upload(lease.get(), g.n, g.offsets.empty() ? nullptr : g.offsets.data(),
                              g.neighbors.empty() ? nullptr : g.neighbors.data(), &h));
   }
   // upload with the K1 tile count of tile_dim overlapped (tcmis_graph_upload_tiled)
   DeviceGraph(const Graph &g, int tile_dim) {
-    check(tcmis_graph_upload_tiled(context(), g.n,
+    check(tcmis_graph_upload_tiled(lease.get(), g.n,
                                    g.offsets.empty() ? nullptr : g.offsets.data(),
                                    g.neighbors.empty() ? nullptr : g.neighbors.data(), tile_dim,
                                    &h, nullptr));
@@ -101,8 +135,13 @@ MISResult solve(tcmis_graph *g, VertexId n, const EngineConfig &cfg, Heuristic h
   int32_t nit = 0;
   check(tcmis_solve(g, &c, nullptr, mis.data(), &cnt, st.data(), static_cast<int32_t>(st.size()),
                     &nit));
-  if (nit > static_cast<int32_t>(st.size())) {  // pathological round counts: ask again
+  if (nit > static_cast<int32_t>(st.size())) {
+    // pathological round counts: ask again for all the statistics (the solve
+    // is deterministic); the hook already saw every iteration once
+    // (engine.cpp:275-278), so the second run goes without it
     st.resize(static_cast<std::size_t>(nit));
+    c.observer = nullptr;
+    c.observer_user = nullptr;
     check(tcmis_solve(g, &c, nullptr, mis.data(), &cnt, st.data(), nit, &nit));
   }
   r.mis.assign(mis.begin(), mis.begin() + cnt);
@@ -177,7 +216,8 @@ PriorityVector h1_random(VertexId n, std::uint64_t seed) {
   PriorityVector pv;
   pv.seed = seed;
   pv.p.resize(static_cast<std::size_t>(n));
-  check(tcmis_h1_random(context(), n, seed, pv.p.data()));
+  ContextLease lease;
+  check(tcmis_h1_random(lease.get(), n, seed, pv.p.data()));
   return pv;
 }
 
@@ -386,7 +426,8 @@ std::vector<std::int32_t> tiled_spmv(const TiledAdjacency &a, const TiledVector 
     // K4b on the CUDA cores (it beats the tensor-core form at
     // every measured tile density); an all-zero segment contributes nothing,
     // so without skipping every tile merely counts as evaluated
-    check(tcmis_tiled_spmv_tiles(context(), a.n, a.tile_dim, a.tile_count(), a.tile_col.data(),
+    ContextLease lease;
+    check(tcmis_tiled_spmv_tiles(lease.get(), a.n, a.tile_dim, a.tile_count(), a.tile_col.data(),
                                  a.row_bits.data(), a.block_row_offsets.data(),
                                  c.segment_bits.data(), TCMIS_EXCL_TILE_BITS, nc.data(), &ev,
                                  &sk));
@@ -569,7 +610,7 @@ MISResult run_tc_mis(const Graph &g, const TiledAdjacency &tiled, const EngineCo
     throw std::invalid_argument("tiled adjacency and vector disagree on tile layout");
   DeviceGraph dg(g);
   check(tcmis_graph_set_tiling(dg.h, tiled.tile_dim, tiled.block_row_offsets.data(),
-                               tiled.n_block_rows()));
+                               tiled.n_block_rows(), tiled.tile_col.data(), tiled.tile_count()));
   return solve(dg.h, g.n, cfg, cfg.heuristic);
 }
 

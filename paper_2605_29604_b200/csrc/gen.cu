@@ -5,7 +5,7 @@
 // so sample e, level l uses draw e*scale + l and every sample is independent.
 // Normalisation (graph.cpp:14-41: drop loops, add reverse edges, sort, dedupe)
 // is a radix sort + unique over (u << scale | v) keys.  The result is bit-
-// identical to tcmis::rmat_graph (pinned by tests/test_gpu_generators.py).
+// identical to tcmis::rmat_graph (pinned by tests/test_gpu_parity.py::test_gpu_rmat_bit_identical).
 //
 // Grid and RGG have no reference generator; their definitions are DESIGN.md's
 // (and oracle/tcmis_oracle.c's).  G(n,p) is inherently serial (one RNG stream

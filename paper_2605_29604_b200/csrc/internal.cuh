@@ -83,6 +83,8 @@ struct HostRes {
   DevRound rounds[64];
 };
 
+struct DistState;
+
 struct Workspace {
   size_t n_cap = 0;
   size_t seg_cap = 0;
@@ -183,6 +185,7 @@ struct tcmis_graph {
   int32_t part_lo = 0, part_hi = -1;  // part_hi < 0: not partitioned
   int64_t *d_off_full = nullptr;
   int64_t nnz_global = -1;
+  tcmis_b200::DistState *dist = nullptr;  // partitioned-solve state (dist.cu), freed with the graph
   tcmis_b200::Workspace ws;
 };
 
@@ -274,6 +277,9 @@ double avg_degree(const tcmis_graph *g);
 int ensure_workspace(tcmis_graph *g);
 int ensure_cub(tcmis_graph *g, size_t bytes);
 void free_workspace(Workspace &ws);
+
+// partitioned-solve state (dist.cu)
+void free_dist(tcmis_graph *g);
 
 // tiling (tiles.cu)
 int build_tile_counts(tcmis_graph *g, int T);

@@ -43,7 +43,9 @@ def partition_rows(offsets: np.ndarray, world: int, tile_dim: int = 16) -> list[
     for r in range(1, world):
         target = total * r // world
         v = int(np.searchsorted(offsets, target, side="left"))
-        v = min(n, max(lo[-1], (v + align // 2) // align * align))
+        # boundaries stay aligned: the last one at or below n is n // align *
+        # align (n itself need not be aligned; a trailing rank may be empty)
+        v = min(n // align * align, max(lo[-1], (v + align // 2) // align * align))
         lo.append(v)
     lo.append(n)
     return lo
@@ -195,7 +197,8 @@ def solve_partitioned(rank_obj, rank_lo: list[int], rank: int, world: int, dist,
     the tests) and `dist` is torch.distributed (NCCL on GPUs, gloo on CPU)."""
     import torch
     n = rank_lo[-1]
-    if any((rank_lo[r] % 64) or (rank_lo[r] % tile_dim) for r in range(world)):
+    if any(((rank_lo[r] % 64) or (rank_lo[r] % tile_dim)) and rank_lo[r] != n
+           for r in range(world)):
         raise ValueError("partition boundaries must be multiples of 64 and of tile_dim")
     if heuristic not in HEURISTICS:
         raise ValueError(f"partitioned solve runs {sorted(HEURISTICS)}, not {heuristic!r}")

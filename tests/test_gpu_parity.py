@@ -226,6 +226,32 @@ def test_prebuilt_tiles_overload(ctx):
         tc.run_tc_mis(as_tc(g), a, tc.EngineConfig(heuristic=tc.Heuristic.H2, tile_dim=16))
 
 
+def test_prebuilt_tiles_any_tile_set(ctx):
+    # the counters are taken on the GIVEN tiling (spmv.cpp:37-46), also when it
+    # is not tile_graph(g)'s symmetric tile set: drop every third tile
+    g = O.gen("rmat", 10, 16, 3)
+    a = tc.tile_graph(as_tc(g), 8, ctx)
+    keep = np.arange(a.tile_count()) % 3 != 0
+    tr, tcol = a.tile_row[keep], a.tile_col[keep]
+    nb = a.block_row_offsets.size - 1
+    bro = np.zeros(nb + 1, np.int64)
+    np.add.at(bro, tr + 1, 1)
+    sub = tc.TiledAdjacency(tile_dim=8, n=a.n, n_padded=a.n_padded, tile_row=tr, tile_col=tcol,
+                            row_bits=a.row_bits.reshape(-1, 8)[keep].reshape(-1),
+                            block_row_offsets=np.cumsum(bro))
+    res = tc.run_tc_mis(as_tc(g), sub, tc.EngineConfig(heuristic=tc.Heuristic.H2, tile_dim=8))
+    p = O.priorities(g, "h2", 1)
+    exp = O.luby_rounds(g, p, T=8, col_counts=np.bincount(tcol, minlength=nb))
+    assert rounds_tuple(res.iterations) == oracle_tuple(exp)
+    assert sum(i.tiles_evaluated + i.tiles_skipped for i in res.iterations) == \
+        len(res.iterations) * int(keep.sum())
+    bad = tc.TiledAdjacency(tile_dim=8, n=a.n, n_padded=a.n_padded, tile_row=tr,
+                            tile_col=np.full_like(tcol, nb), row_bits=sub.row_bits,
+                            block_row_offsets=sub.block_row_offsets)
+    with pytest.raises(ValueError):
+        tc.run_tc_mis(as_tc(g), bad, tc.EngineConfig(heuristic=tc.Heuristic.H2, tile_dim=8))
+
+
 def test_edge_cases(ctx):
     for g in (O.graph_from_edges(1, np.zeros((0, 2), np.int32)),
               O.graph_from_edges(100, np.zeros((0, 2), np.int32)),

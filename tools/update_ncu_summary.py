@@ -1,5 +1,5 @@
 # profiles/ncu_summary.json from ncu launch lists (gpu__time_duration + dram
-# bytes) of scratch/ncu_target.py: per config, the round-1 launch of every
+# bytes) of tools/ncu_target.py: per config, the round-1 launch of every
 # kernel in the SECOND (warm) solve.  usage: update_ncu_summary.py CFG CSV [CFG CSV ...]
 import csv, json, os, re, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -9,7 +9,7 @@ try:
 except Exception:
     summ = {}
 summ["_doc"] = ("per config: ncu launch list (--metrics gpu__time_duration.sum,dram__bytes_read.sum,"
-                "dram__bytes_write.sum --clock-control none) of scratch/ncu_target.py; the round-1 "
+                "dram__bytes_write.sum --clock-control none) of tools/ncu_target.py; the round-1 "
                 "launch of each kernel in the second (warm) host-loop solve; dram_bytes = read + write "
                 "per launch (cold-cache, serialised by ncu)")
 args = sys.argv[1:]
