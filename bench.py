@@ -2,11 +2,14 @@
 """bench.py -- TC-MIS on B200: MIS time and Gedges/s (BASELINE.json metric).
 
 A "step" is one complete MIS solve (H2 priorities -> bulk-synchronous rounds
--> ascending MIS ids on the device) of the configured synthetic graph.
+-> ascending MIS ids back on the host) of the configured synthetic graph.
 
-  value  device-resident: the CSR is already in HBM (generated there); the
-         step is tcmis_solve_device() through the C-ABI, timed with CUDA
-         events on the engine's stream; L2 is flushed between steps.
+  value  the CSR is already in HBM (generated there); the step is
+         tcmis_solve() through the C-ABI up to the ascending MIS ids in a
+         pinned host buffer (SURVEY 8(d) "MIS time": priority init through
+         the MIS ids back on host), timed with CUDA events on the engine's
+         stream; L2 is flushed between steps.  `device_resident` times the
+         same solve with the ids left in HBM (tcmis_solve_device).
   e2e    the drop-in path: host CSR in pinned memory -> tcmis_graph_upload
          (H2D) -> tcmis_graph_tile -> tcmis_solve (D2H of the MIS ids and the
          per-iteration stats into host buffers) -> destroy, every step.
@@ -193,28 +196,42 @@ def run_ours(args) -> dict:
                                        C.byref(d_state), stats, 4096, C.byref(nit)))
         return cnt.value, nit.value
 
-    # ---- value: device-resident solves
-    for _ in range(args.warmup):
-        solve_device()
-    ctx.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    launches0 = ctx.launches()
-    with ClockSampler(local) as clk:
-        for k in range(args.steps):
+    h_mis = torch.empty(max(n, 1), dtype=torch.int32).pin_memory()  # the step's result buffer
+    h_stats = (tc._Stats * 4096)()
+
+    def solve_host():
+        cnt, nit = C.c_int64(0), C.c_int32(0)
+        tc._check(L.tcmis_solve(dg.h, C.byref(c_cfg), None, C.c_void_p(h_mis.data_ptr()),
+                                C.byref(cnt), h_stats, 4096, C.byref(nit)))
+        return cnt.value, nit.value
+
+    def timed(fn, steps):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        torch.cuda.synchronize()
+        out = None
+        for k in range(steps):
             with torch.cuda.stream(stream):
                 flush.zero_()
                 ev[k][0].record(stream)
-            mis_count, iters = solve_device()
+            out = fn()
             with torch.cuda.stream(stream):
                 ev[k][1].record(stream)
         ctx.synchronize()
         torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in ev], out
+
+    # ---- value: solves up to the MIS ids in pinned host memory
+    for _ in range(args.warmup):
+        solve_host()
+        solve_device()
+    ctx.synchronize()
+    if dist:
+        dist.barrier()
+    launches0 = ctx.launches()
+    with ClockSampler(local) as clk:
+        step_ms, (mis_count, iters) = timed(solve_host, args.steps)
     launches = ctx.launches() - launches0
-    step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
     if dist:
         t = torch.tensor([total_ms], device=f"cuda:{local}")
@@ -222,6 +239,15 @@ def run_ours(args) -> dict:
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     value = world * m / (ms_per_step * 1e-3) / 1e9  # replicas: every rank solves its graph
+    assert int(h_mis[:mis_count].diff().min()) > 0 if mis_count > 1 else True
+    # the same solve with the ids left in HBM (what the kernels alone take)
+    dev_ms, _ = timed(solve_device, args.steps)
+    dev_ms = sorted(dev_ms)[len(dev_ms) // 2]
+    device_resident = {"ms": round(dev_ms, 4), "value": round(m / (dev_ms * 1e-3) / 1e9, 4),
+                       "d2h_ms": round(ms_per_step - dev_ms, 4),
+                       "note": "median step of tcmis_solve_device (MIS ids stay in HBM); "
+                               "d2h_ms = value's step minus this (the 4|MIS|-byte id copy "
+                               "over PCIe and its synchronisation)"}
 
     # ---- kernel roofline: per-kernel CUDA events around every launch of a
     # step-wise solve (same kernels as the graph; TCMIS_F_TIMING)
@@ -253,6 +279,7 @@ def run_ours(args) -> dict:
                    "parallelism": "replicas" if world > 1 else "single",
                    "l2": "256 MB flush between steps; CSR > L2"},
         "mis_ms": round(ms_per_step, 4),
+        "device_resident": device_resident,
         "kernels_ms": [[k, r, round(ms, 4)] for k, r, ms in kernels],
         "roofline": roofline, "e2e": e2e, "clocks": clk.summary(),
         "gpu_launches": launches,
@@ -283,10 +310,12 @@ def timeline(tc, ctx):
 # also scans the pull exclusion's longest rows but is booked as Phase 3
 PHASE = {"k_probe_select": 1, "k_select": 1, "k_select_long": 1,
          "k_probe_pull": 2, "k_update_pull": 2, "k_tile_excl_bits": 2, "k_tile_excl_mma": 2,
-         "k_update": 3, "k_round_end": 3, "k_priorities": 0}
+         "k_update": 3, "k_round_end": 3, "k_priorities": 0, "k_tail": 4}
 PHASE_NAME = {0: "init (priorities, states)", 1: "Phase 1 candidate detection",
               2: "Phase 2 neighbour exclusion (SpMV)", 3: "Phase 3 state update + compaction",
-              12: "Phases 1+2 (push exclusion fused into candidate detection)"}
+              12: "Phases 1+2 (push exclusion fused into candidate detection)",
+              4: "Tail rounds (Phases 1-3 of every remaining round in one persistent kernel, "
+                 "+ MIS id compaction)"}
 
 
 def kernel_roofline(tc, dg, cfg, kernels, args, ms_per_step):
@@ -314,7 +343,7 @@ def kernel_roofline(tc, dg, cfg, kernels, args, ms_per_step):
             continue
         if push and ph in (1, 2):
             ph = 12
-        key = (ph, rnd if ph else 0)
+        key = (ph, rnd if ph else 0)  # k_tail: rnd = its first round
         e = acc.setdefault(key, {"ms": 0.0, "kernels": []})
         e["ms"] += ms
         e["kernels"].append(name)
@@ -327,13 +356,20 @@ def kernel_roofline(tc, dg, cfg, kernels, args, ms_per_step):
                 continue
             A, nnzA, NC, nnzNC = traj[rnd - 1]
             b1, b2, b3 = 12 * A + 4 * nnzA, 8 * NC + 4 * nnzNC, 2 * A
-            b = {1: b1, 2: b2, 3: b3, 12: b1 + b2}[ph]
+            if ph == 4:  # every round from rnd on, all three phases
+                b = sum(12 * A + 4 * nA + 8 * NC + 4 * nNC + 2 * A
+                        for A, nA, NC, nNC in traj[rnd - 1:])
+            else:
+                b = {1: b1, 2: b2, 3: b3, 12: b1 + b2}[ph]
         ach = b / (e["ms"] * 1e-3) / 1e9 if e["ms"] > 0 else 0.0
-        phases.append({"phase": PHASE_NAME[ph], "round": rnd, "kernels": e["kernels"],
+        phases.append({"phase": PHASE_NAME[ph], "round": rnd if ph != 4 else f"{rnd}-{len(traj)}",
+                       "kernels": e["kernels"],
                        "algorithmic_bytes": int(b), "ms": round(e["ms"], 4),
                        "achieved": round(ach, 1), "frac": round(ach / hbm, 4)})
     if not phases:
         return None
+    # the dominant phase-round by time (the tail counts as one: it is one
+    # launch over all the late rounds)
     dom = max(phases, key=lambda p: p["ms"])
     traffic = None
     try:
@@ -676,19 +712,62 @@ def ref_graph_for(name: str):
     raise ValueError(name)
 
 
-def ref_time(rg, heuristic: str, reps: int, cores: int):
-    """Time the reference's fastest identical-output CPU path on rg:
-    run_luby_reference(Permutation) -- same MIS and same round count as h2,
-    no 12 GB tiling."""
+def mem_available() -> int:
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def ref_tiling(rg, nnz: int):
+    """The reference's own tile_graph(g, 16) (tiling.cpp:44-84), timed as
+    preprocessing, when its 136 B/tile layout fits twice into the host's free
+    memory (tiles <= nnz); else None (s26 needs ~237 GB)."""
     import oracle as O
-    ts = []
-    for _ in range(reps):
-        if heuristic in ("h2", "h3", "luby-perm"):
-            _m, rr, ms = O.ref_run_luby(rg, 1, False, 20, cores)
-        else:
-            _m, rr, ms = O.ref_run_mis(rg, heuristic, 1, 16, cores)
-        ts.append(ms)
-    return ts, len(rr)
+    if 2 * 136 * nnz > mem_available():
+        return None
+    return O.RefTiled(rg, 16)
+
+
+def ref_paths(rg, heuristic: str, cores: int, tiled) -> dict:
+    """The reference's CPU paths that return the same MIS for `heuristic`
+    (h2, h3 and luby-perm give the identical MIS), each a callable
+    returning (rounds, wall ms).  The tiled ones run over the prebuilt tiling
+    (engine.hpp:111-112), so tile_graph is not inside their time."""
+    import oracle as O
+    P = {}
+    if heuristic in ("h2", "h3", "luby-perm"):
+        if tiled is not None:
+            for h in ("h2", "h3"):
+                P[f"run_tc_mis({h}, prebuilt tile_graph T=16)"] = (
+                    lambda h=h: O.ref_run_tc_mis_tiled(rg, tiled, h, 1, cores)[1:])
+        P["run_luby_reference(Permutation)"] = lambda: O.ref_run_luby(rg, 1, False, 20, cores)[1:]
+    elif heuristic == "luby-fresh":
+        P["run_luby_reference(Fresh)"] = lambda: O.ref_run_luby(rg, 1, True, 20, cores)[1:]
+    elif tiled is not None:
+        P["run_tc_mis(h1, prebuilt tile_graph T=16)"] = (
+            lambda: O.ref_run_tc_mis_tiled(rg, tiled, "h1", 1, cores)[1:])
+    else:
+        P["run_mis(h1) (tiles inside)"] = lambda: O.ref_run_mis(rg, "h1", 1, 16, cores)[1:]
+    return P
+
+
+def ref_select(paths: dict, reps: int = 3):
+    """Median of `reps` wall times per path; the fastest path
+    is the headline CPU number."""
+    med, rounds = {}, {}
+    for name, fn in paths.items():
+        ts = []
+        for _ in range(reps):
+            rr, ms = fn()
+            ts.append(ms)
+            rounds[name] = len(rr)
+        med[name] = sorted(ts)[len(ts) // 2]
+    best = min(med, key=med.get)
+    return best, med, rounds
 
 
 def cpu_baseline(dg, args) -> dict:
@@ -699,20 +778,23 @@ def cpu_baseline(dg, args) -> dict:
     h = dg.download()
     rg = O.RefGraph.from_csr(O.Graph(h.n, h.offsets, h.neighbors))
     cores = os.cpu_count() or 1
-    t0 = time.time()
-    ts, rounds = ref_time(rg, args.heuristic, 1, cores)
-    reps = 1
-    while time.time() - t0 < 10 and reps < 5:  # bounded sample: ~10-30 s of CPU work
-        t2, _ = ref_time(rg, args.heuristic, 1, cores)
-        ts += t2
-        reps += 1
-    ms = sorted(ts)[len(ts) // 2]
-    return {"value": round((h.neighbors.size // 2) / (ms * 1e-3) / 1e9, 5), "unit": "Gedges/s",
-            "cores": cores, "kind": "reference", "ms": round(ms, 2),
-            "sample": f"{reps} full solve(s) of the same graph by the reference's "
-                      f"run_luby_reference(Permutation) (identical MIS and round count to "
-                      f"{args.heuristic}), median, workers={cores}",
-            "cpu_model": cpu_model()}
+    tiled = ref_tiling(rg, int(h.neighbors.size))
+    best, med, rounds = ref_select(ref_paths(rg, args.heuristic, cores, tiled), 3)
+    ms = med[best]
+    m = h.neighbors.size // 2
+    out = {"value": round(m / (ms * 1e-3) / 1e9, 5), "unit": "Gedges/s",
+           "cores": cores, "kind": "reference", "ms": round(ms, 2), "path": best,
+           "paths_ms": {k: round(v, 2) for k, v in med.items()},
+           "tile_graph_ms": round(tiled.ms, 1) if tiled is not None else None,
+           "sample": f"the whole graph: each identical-output reference path run 3 times "
+                     f"(median), workers={cores}; value = the fastest ({best}); the tiled "
+                     f"paths over one prebuilt tile_graph(g, 16), timed separately "
+                     f"(tile_graph_ms)" + ("" if tiled is not None else
+                                           "; tiled paths skipped: tiles exceed host memory"),
+           "cpu_model": cpu_model()}
+    if tiled is not None:
+        tiled.close()
+    return out
 
 
 def cpu_model() -> str:
@@ -745,31 +827,44 @@ def run_reference(args) -> dict | None:
     g = rg.to_csr()
     log(f"[bench:reference] {args.config}{' (sample rmat%d)' % SAMPLE_SCALE if sampled else ''}: "
         f"n={g.n} m={g.num_edges} (reference generator {time.time() - t0:.1f}s)")
+    tiled = None if sampled else ref_tiling(rg, int(g.nbr.size))
+    if tiled is not None:
+        log(f"[bench:reference] tile_graph(g, 16): {tiled.tile_count()} tiles in {tiled.ms:.0f} ms")
+    # every identical-output path, median of 3; the fastest one is timed
+    paths = ref_paths(rg, args.heuristic, cores, tiled)
+    best, med, rounds = ref_select(paths, 3)
+    log(f"[bench:reference] paths (median of 3, ms): {med}; timing {best}")
     for _ in range(args.warmup):
-        ref_time(rg, args.heuristic, 1, cores)
-    ts, rounds = ref_time(rg, args.heuristic, args.steps, cores)
+        paths[best]()
+    ts = [paths[best]()[1] for _ in range(args.steps)]
     ms = sum(ts) / len(ts)
     value = g.num_edges / (ms * 1e-3) / 1e9
-    path = ("run_luby_reference(Permutation)" if args.heuristic in ("h2", "h3", "luby-perm")
-            else f"run_mis({args.heuristic})")
-    return {
+    line = {
         "impl": "reference", "metric": "Gedges/s (MIS solve, BASELINE config)",
         "value": round(value, 5), "unit": "Gedges/s", "n_gpus": 0, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "integer / f64 priority",
         "data": "synthetic (reference generators)",
         "config": {"workload": CONFIGS[args.config]["workload"], "graph": args.config,
-                   "n": g.n, "m": g.num_edges, "heuristic": args.heuristic, "iterations": rounds,
-                   "path": path},
+                   "n": g.n, "m": g.num_edges, "heuristic": args.heuristic, "seed": 1,
+                   "tile_dim": 16, "iterations": rounds[best], "path": best},
+        "paths_ms": {k: round(v, 2) for k, v in med.items()},
+        "tile_graph_ms": round(tiled.ms, 1) if tiled is not None else None,
         "cpu_baseline": {"value": round(value, 5), "unit": "Gedges/s", "cores": cores,
                          "kind": "reference", "cpu_model": cpu_model(),
                          "sample": (f"rmat_graph({SAMPLE_SCALE},16,1) as a bounded sample of "
                                     f"the s26 workload; " if sampled else "") +
                                    f"{args.steps} full solves of the whole graph by the "
-                                   f"unmodified reference ({path}), workers={cores}"},
+                                   f"unmodified reference's fastest identical-output path "
+                                   f"({best}; every path's median of 3 in paths_ms; tiled "
+                                   f"paths over a prebuilt tile_graph, tile_graph_ms apart), "
+                                   f"workers={cores}"},
         "e2e": {"value": round(value, 5), "unit": "Gedges/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    if tiled is not None:
+        tiled.close()
+    return line
 
 
 def main():

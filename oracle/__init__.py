@@ -422,6 +422,54 @@ def ref_run_mis(g: RefGraph, heuristic: str = "h3", seed: int = 1, tile_dim: int
     return member[:n], out, ms.value
 
 
+class RefTiled:
+    """A TiledAdjacency built by the compiled reference's tile_graph
+    (tiling.cpp:44-84); `ms` is its wall time."""
+
+    def __init__(self, g: RefGraph, tile_dim: int = 16):
+        R = ref()
+        ms = C.c_double(0)
+        self.h = R.ref_tile_graph(g.h, tile_dim, C.byref(ms))
+        if not self.h:
+            raise RuntimeError("reference tile_graph failed: " + R.ref_last_error().decode())
+        self.ms = ms.value
+        self.tile_dim = tile_dim
+
+    def tile_count(self) -> int:
+        return int(ref().ref_tiled_count(self.h))
+
+    def close(self):
+        if self.h and _ref is not None:
+            _ref.ref_tiled_free(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def ref_run_tc_mis_tiled(g: RefGraph, tiled: RefTiled, heuristic: str = "h3", seed: int = 1,
+                         workers: int = 0, scale_bits: int = 20, max_rounds: int = 4096):
+    """tcmis::run_tc_mis(g, tiled, cfg) (engine.cpp:231-295) over a prebuilt
+    tiling.  Returns (member u8[n], rounds, wall_ms)."""
+    R = ref()
+    n = R.ref_graph_n(g.h)
+    member = np.zeros(max(n, 1), np.uint8)
+    cnt = C.c_int64(0)
+    rounds = (RefRound * max_rounds)()
+    nr = C.c_int(0)
+    ms = C.c_double(0)
+    rc = R.ref_run_tc_mis_tiled(g.h, tiled.h, HEURISTICS[heuristic], seed, tiled.tile_dim,
+                                workers, scale_bits, member, C.byref(cnt), rounds, max_rounds,
+                                C.byref(nr), C.byref(ms))
+    if rc:
+        raise _ref_exc(rc)
+    out = [{f: getattr(rounds[i], f) for f, _ in RefRound._fields_} for i in range(nr.value)]
+    return member[:n], out, ms.value
+
+
 def ref_run_luby(g: RefGraph, seed: int = 1, fresh: bool = False, scale_bits: int = 20,
                  workers: int = 0, max_rounds: int = 4096):
     R = ref()

@@ -369,11 +369,17 @@ def test_golden_baseline_configs(ctx, name):
 
 
 def test_rmat26_golden_rounds(ctx):
-    """R-MAT s26 (~1.05B edges) on one GPU against the reference's rounds
-    (tests/golden/rmat26_ef16.json): n, m, max degree, the
-    T=16 tile count, |MIS|, the iteration count and every round's selected /
-    removed / alive, plus the round-1 trajectory terms."""
+    """R-MAT s26 (~1.05B edges) on one GPU against tests/golden/rmat26_ef16.json
+    (tests/golden/make_rmat26.py: the reference's run_luby_reference on the
+    bit-identical device-generated CSR, re-pinned by its sequential greedy
+    oracle; tile counters from the restatement): CSR checksums, the T=16 tile
+    count, and for h2, h3, h1 and luby-perm the membership checksum, |MIS|, the
+    iteration count and every round's selected / removed / alive / tiles
+    evaluated / skipped."""
     gd = golden("rmat26_ef16")
+    if "results" in gd:
+        _check_golden("rmat26_ef16", ctx)
+        return
     dg = tc.DeviceGraph.rmat(26, 16, 1, ctx)
     assert (dg.n, dg.num_edges()) == (gd["n"], gd["m"])
     assert dg.tile(16) == gd["tile_count"]
@@ -382,8 +388,6 @@ def test_rmat26_golden_rounds(ctx):
     assert res.cardinality() == exp["mis_size"]
     got = [[i.candidates_selected, i.vertices_removed, i.alive_remaining] for i in res.iterations]
     assert got == exp["rounds_sel_rem_alive"]
-    member = res.state == 1
-    assert int(member.sum()) == exp["mis_size"]
     dg.close()
 
 
