@@ -377,18 +377,10 @@ def test_rmat26_golden_rounds(ctx):
     iteration count and every round's selected / removed / alive / tiles
     evaluated / skipped."""
     gd = golden("rmat26_ef16")
-    if "results" in gd:
-        _check_golden("rmat26_ef16", ctx)
-        return
-    dg = tc.DeviceGraph.rmat(26, 16, 1, ctx)
-    assert (dg.n, dg.num_edges()) == (gd["n"], gd["m"])
-    assert dg.tile(16) == gd["tile_count"]
-    res = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=1, tile_dim=16))
-    exp = gd["h2_seed1"]
-    assert res.cardinality() == exp["mis_size"]
-    got = [[i.candidates_selected, i.vertices_removed, i.alive_remaining] for i in res.iterations]
-    assert got == exp["rounds_sel_rem_alive"]
-    dg.close()
+    # the fixture's H2 rounds are SURVEY Appendix A's (the reference's phase functions)
+    assert [r[:3] for r in gd["results"]["h2/seed1"]["rounds"]] == \
+        gd["survey_appendix_a"]["h2_seed1"]["rounds_sel_rem_alive"]
+    _check_golden("rmat26_ef16", ctx)
 
 
 def test_rmat22_properties(ctx):
