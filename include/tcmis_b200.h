@@ -90,6 +90,10 @@ typedef struct tcmis_config {
 
 #define TCMIS_F_TIMING 0x1u     /* record per-phase device times in the stats */
 #define TCMIS_F_HOST_LOOP 0x2u  /* drive rounds from the host (no CUDA-graph while loop) */
+/* test hook: start the solve from a control block that disagrees with the
+ * vertex states; the device's round invariant check must then fail the solve
+ * with TCMIS_E_LOGIC (the reference's logic_error, engine.cpp:152-153) */
+#define TCMIS_F_DEBUG_CORRUPT 0x100u
 
 /* Fill *cfg with the reference defaults (EngineConfig{}). */
 void tcmis_config_init(tcmis_config *cfg);

@@ -99,6 +99,7 @@ class _Config(C.Structure):
 
 F_TIMING = 0x1
 F_HOST_LOOP = 0x2
+F_DEBUG_CORRUPT = 0x100  # test hook (include/tcmis_b200.h)
 
 
 def load():
@@ -244,6 +245,7 @@ class EngineConfig:  # engine.hpp:53-65
     exclusion: Exclusion = Exclusion.AUTO
     timing: bool = False
     host_loop: bool = False
+    flags: int = 0  # extra TCMIS_F_* bits (test hooks)
 
     def _c(self) -> tuple:
         c = _Config()
@@ -254,7 +256,8 @@ class EngineConfig:  # engine.hpp:53-65
         c.scale_bits = int(self.scale_bits)
         c.workers = int(self.workers)
         c.exclusion = int(self.exclusion)
-        c.flags = (F_TIMING if self.timing else 0) | (F_HOST_LOOP if self.host_loop else 0)
+        c.flags = ((F_TIMING if self.timing else 0) | (F_HOST_LOOP if self.host_loop else 0)
+                   | int(self.flags))
         keep = None
         if self.iteration_observer is not None:
             obs = self.iteration_observer

@@ -65,6 +65,17 @@ __device__ __forceinline__ T ld_stream(const T *p) {
 #endif
 }
 
+// Phase timer of the reference (engine.cpp:253-284): block 0 stamps the
+// phase's start into the round's DevRound slot (internal.cuh)
+__device__ __forceinline__ void stamp_phase(DevRound *rounds, const Ctrl *ctrl, int round,
+                                            int k0, int k1) {
+  if (rounds && blockIdx.x == 0 && threadIdx.x == 0) {
+    DevRound *r = &rounds[(round - 1) % ctrl->max_rounds];
+    const unsigned long long t = gtimer_ns();
+    for (int k = k0; k <= k1; ++k) r->t[k] = t;
+  }
+}
+
 // per-thread work modes of the state-machine kernels
 enum : int { kFetch = 0, kScan = 1, kPush = 2, kDone = 3 };
 

@@ -176,9 +176,9 @@ int dist_apply(tcmis_graph *g, const uint32_t *d_gathered, const int32_t *h_rank
 
 // d_counts: DEVICE int64[5] = this rank's (selected, removed, alive,
 // tiles_evaluated, tiles_skipped) of the round, copied stream-ordered from
-// the DevRound k_round_end publishes (DevRound is 5 x u64 in that order).
+// the DevRound k_round_end publishes (its first 5 x u64, in that order).
 int dist_update(tcmis_graph *g, uint32_t *d_bits, int32_t words, int64_t *d_counts) {
-  static_assert(sizeof(DevRound) == 5 * sizeof(int64_t), "DevRound layout");
+  static_assert(offsetof(DevRound, skip) == 4 * sizeof(int64_t), "DevRound layout");
   DistState &d = dist_state(g);
   if (!d.active) return set_error(TCMIS_E_LOGIC, "tcmis_dist_begin first");
   cudaStream_t st = g->ctx->stream;
@@ -188,8 +188,8 @@ int dist_update(tcmis_graph *g, uint32_t *d_bits, int32_t words, int64_t *d_coun
   if (int rc = launch_update(g, d.a, 0, 0)) return rc;
   Workspace &ws = g->ws;
   const int32_t round = ++d.round;
-  TCMIS_CUDA(cudaMemcpyAsync(d_counts, ws.rounds + (round - 1) % ws.round_cap, sizeof(DevRound),
-                             cudaMemcpyDeviceToDevice, st));
+  TCMIS_CUDA(cudaMemcpyAsync(d_counts, ws.rounds + (round - 1) % ws.round_cap,
+                             5 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
   return 0;
 }
 

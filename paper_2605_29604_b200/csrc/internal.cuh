@@ -41,9 +41,19 @@ __host__ __device__ __forceinline__ uint64_t combine_seed(uint64_t seed, uint64_
   return mix64(seed + mix64(round + kGolden));
 }
 
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Per-round statistics as the device accumulates them.
 struct DevRound {
   unsigned long long sel, rem, alive, eval, skip;
+  // %globaltimer (ns) at the start of Phase 1, Phase 2, Phase 3 and at the
+  // round's end, stamped by the round's kernels (the reference's phase
+  // timers, engine.cpp:253-284); 0 where a phase has no kernel of its own
+  unsigned long long t[4];
 };
 
 // Device control block driving the round loop (one per solve workspace).
@@ -58,11 +68,12 @@ struct Ctrl {
   int32_t long_count;  // entries of the select long-row list this round
   int32_t pull_count;  // entries of the pull long-row list this round
   int32_t main_rounds; // rounds run by the per-round kernels (the rest ran in k_tail)
-  int32_t tail_cnt[3];   // k_tail list lengths, by round mod 3 (tail.cuh)
   int32_t sel_undec;   // rows k_probe_select left to the k_select engine
   int32_t pull_undec;  // rows k_probe_pull left to the k_update_pull engine
   int32_t sel_vlong;   // select rows longer than kBlockRow (block-wide in k_select_long)
   int32_t pull_items;  // chunks of the pull long rows (k_round_end work items)
+  int32_t corrupt;     // a round broke selected + removed + alive == alive before
+                       // (engine.cpp:138-141,152-153 logic_error): set on the device
 };
 
 // A pull row that outlived k_update_pull's engine (update.cuh): entries
@@ -92,7 +103,7 @@ struct Workspace {
   uint16_t *q = nullptr;          // q_of(prio) (common.cuh), 0 once removed
   uint8_t *state = nullptr;
   uint8_t *next = nullptr;
-  uint8_t *xm = nullptr;          // k_tail exclusion planes: [0, n_cap) even, [n_cap, 2 n_cap) odd rounds
+  uint16_t *xt = nullptr;         // k_tail round tags (tail.cuh), zeroed at allocation
   int32_t *wl[2] = {nullptr, nullptr};
   uint8_t *segflag = nullptr;
   int32_t *mis = nullptr;
@@ -106,7 +117,8 @@ struct Workspace {
   int32_t *undec_pull = nullptr;  // probe leftovers for the pull engine
   uint32_t *segmark = nullptr;    // tail rounds: round that last counted a block column
   unsigned *bar = nullptr;        // grid barrier of k_tail
-  unsigned *blockcnt = nullptr;   // k_tail's fused MIS compaction: per-block counts
+  unsigned *warpcnt = nullptr;    // k_tail's fused MIS compaction: 2 x kTailMaxWarps per-warp
+                                  // counts by solve parity, then tslot[2] (tag base, solve counter)
   int64_t *mis_count = nullptr;
   Ctrl *ctrl = nullptr;        // device
   Ctrl *h_ctrl = nullptr;      // pinned host mirror
@@ -269,10 +281,6 @@ int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bi
                       uint8_t *segflag = nullptr, int T = 1, Ctrl *ctrl = nullptr,
                       const Ctrl *ctrl0 = nullptr, DevRound *rounds = nullptr,
                       int32_t nrounds = 0);
-// offset of k_tail's odd exclusion plane in Workspace::xm (16-byte aligned)
-inline size_t xm_stride(const Workspace &ws) { return (ws.n_cap + 15) / 16 * 16; }
-double avg_degree(const tcmis_graph *g);
-
 // workspace management (solver.cu)
 int ensure_workspace(tcmis_graph *g);
 int ensure_cub(tcmis_graph *g, size_t bytes);

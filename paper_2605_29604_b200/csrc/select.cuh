@@ -58,6 +58,7 @@ struct SelectArgs {
   int32_t *vlong;          // ... longer than kBlockRow (ctrl->sel_vlong)
   int32_t *undecided;      // rows the probe could not settle (ctrl->sel_undec)
   Publish pub;             // multi-GPU: this round's candidates of the own range
+  DevRound *rounds;        // Phase 1 start stamp (null: none)
 };
 
 // push: every neighbour of a candidate is excluded this round (spmv.cpp:18-59
@@ -77,6 +78,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
   __shared__ int32_t s_und[kBlock / 32][64];
   Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
+  stamp_phase(a.rounds, ctrl, round, 0, 0);
   // round 1 visits only the non-isolated vertices (k_priorities already made
   // the isolated ones candidates)
   const int64_t cnt = round == 1 ? a.n1 : ctrl->wl_count[round & 1];

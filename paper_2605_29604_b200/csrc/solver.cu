@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256)
   if (rounds)
     for (int32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nrounds;
          r += gridDim.x * blockDim.x)
-      rounds[r] = DevRound{0, 0, 0, 0, 0};
+      rounds[r] = DevRound{};
   const int32_t quads = (int32_t)(((int64_t)n + kPrioV - 1) / kPrioV);
   for (int32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < quads;
        q += gridDim.x * blockDim.x) {
@@ -297,7 +297,7 @@ void free_workspace(Workspace &ws) {
   dev_free(ws.q);
   dev_free(ws.state);
   dev_free(ws.next);
-  dev_free(ws.xm);
+  dev_free(ws.xt);
   dev_free(ws.wl[0]);
   dev_free(ws.wl[1]);
   dev_free(ws.segflag);
@@ -310,7 +310,7 @@ void free_workspace(Workspace &ws) {
   dev_free(ws.undec_pull);
   dev_free(ws.segmark);
   dev_free(ws.bar);
-  dev_free(ws.blockcnt);
+  dev_free(ws.warpcnt);
   dev_free(ws.mis_count);
   dev_free(ws.ctrl);
   cudaFreeHost(ws.h_ctrl);
@@ -353,7 +353,7 @@ int ensure_workspace(tcmis_graph *g) {
   dev_free(ws.q);
     dev_free(ws.state);
     dev_free(ws.next);
-    dev_free(ws.xm);
+    dev_free(ws.xt);
     dev_free(ws.wl[0]);
     dev_free(ws.wl[1]);
     dev_free(ws.mis);
@@ -367,8 +367,9 @@ int ensure_workspace(tcmis_graph *g) {
     if (int rc = dev_alloc(&ws.prio, n)) return rc;
     if (int rc = dev_alloc(&ws.q, n + 8)) return rc;
     if (int rc = dev_alloc(&ws.state, n + 16)) return rc;  // uint4 reads past n (k_tail)
-    if (int rc = dev_alloc(&ws.next, n)) return rc;
-    if (int rc = dev_alloc(&ws.xm, 2 * ((n + 15) / 16 * 16) + 32)) return rc;
+    if (int rc = dev_alloc(&ws.next, n + 16)) return rc;  // uint4 reads past n (k_tail)
+    if (int rc = dev_alloc(&ws.xt, n)) return rc;
+    TCMIS_CUDA(cudaMemsetAsync(ws.xt, 0, sizeof(uint16_t) * n, g->ctx->stream));
     if (int rc = dev_alloc(&ws.wl[0], n)) return rc;
     if (int rc = dev_alloc(&ws.wl[1], n)) return rc;
     if (int rc = dev_alloc(&ws.mis, n)) return rc;
@@ -378,7 +379,7 @@ int ensure_workspace(tcmis_graph *g) {
     if (int rc = dev_alloc(&ws.segmark, n)) return rc;
     if (int rc = dev_alloc(&ws.cbits, n / 32 + 2)) return rc;
     if (int rc = dev_alloc(&ws.tile_hit, n / 16 + 2)) return rc;
-    TCMIS_CUDA(cudaMemsetAsync(ws.next, 0, n, g->ctx->stream));
+    TCMIS_CUDA(cudaMemsetAsync(ws.next, 0, n + 16, g->ctx->stream));
     ws.n_cap = n;
   }
   {  // at most nnz / kBlockRow rows are longer than kBlockRow (per graph)
@@ -423,9 +424,11 @@ int ensure_workspace(tcmis_graph *g) {
   if (!ws.ctrl) {
     if (int rc = dev_alloc(&ws.ctrl, 1)) return rc;
     if (int rc = dev_alloc(&ws.mis_count, 1)) return rc;
-    if (int rc = dev_alloc(&ws.bar, 2)) return rc;
-    if (int rc = dev_alloc(&ws.blockcnt, 4096)) return rc;
-    TCMIS_CUDA(cudaMemsetAsync(ws.bar, 0, 2 * sizeof(unsigned), g->ctx->stream));
+    if (int rc = dev_alloc(&ws.bar, 4)) return rc;
+    if (int rc = dev_alloc(&ws.warpcnt, 2 * (size_t)kTailMaxWarps + 2)) return rc;
+    TCMIS_CUDA(cudaMemsetAsync(ws.warpcnt, 0, sizeof(unsigned) * (2 * (size_t)kTailMaxWarps + 2),
+                               g->ctx->stream));
+    TCMIS_CUDA(cudaMemsetAsync(ws.bar, 0, 4 * sizeof(unsigned), g->ctx->stream));
     TCMIS_CUDA(cudaMallocHost((void **)&ws.h_ctrl, sizeof(Ctrl)));
     TCMIS_CUDA(cudaMallocHost((void **)&ws.h_misc, 2 * sizeof(int64_t)));
     TCMIS_CUDA(cudaHostAlloc((void **)&ws.h_res, sizeof(HostRes), cudaHostAllocMapped));
@@ -565,6 +568,7 @@ SelectArgs select_args(tcmis_graph *g, const RoundArgs &a) {
   s.undecided = ws.undec_sel;
   s.pub = Publish{a.pub_cand, a.pub_lo};
   if (a.tile) s.pub = Publish{ws.cbits, 0};  // the candidate segments of the tile kernels
+  s.rounds = ws.rounds;
   return s;
 }
 
@@ -607,11 +611,12 @@ TailArgs tail_args(tcmis_graph *g, const RoundArgs &a) {
   TailArgs t;
   t.off = a.off;
   t.nbr = a.nbr;
+  t.vnnz = a.vnnz;
   t.prio = ws.prio;
   t.q = ws.q;
   t.next = ws.next;
-  t.xm0 = ws.xm;
-  t.xm1 = ws.xm + xm_stride(ws);
+  t.xt = ws.xt;
+  t.tslot = ws.warpcnt + 2 * (size_t)kTailMaxWarps;
   t.state = ws.state;
   t.segflag = ws.segflag;
   t.segmark = ws.segmark;
@@ -625,11 +630,10 @@ TailArgs tail_args(tcmis_graph *g, const RoundArgs &a) {
   t.wl1 = ws.wl[1];
   t.rounds = ws.rounds;
   t.bar = ws.bar;
-  t.compact = 1;
   t.n = a.n;
   t.mis = ws.mis;
   t.mis_count = ws.mis_count;
-  t.blockcnt = ws.blockcnt;
+  t.warpcnt = ws.warpcnt;
   t.pack = nullptr;
   return t;
 }
@@ -641,6 +645,7 @@ int launch_tail(tcmis_graph *g, const RoundArgs &a, HostRes *pack = nullptr) {
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(a.tail_grid);
   lc.blockDim = dim3(kTailBlock);
+  lc.dynamicSmemBytes = kTailDynSmem;
   lc.stream = g->ctx->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -657,7 +662,8 @@ int launch_tail(tcmis_graph *g, const RoundArgs &a, HostRes *pack = nullptr) {
 int tail_grid(tcmis_ctx *ctx) {
   if (ctx->tail_blocks_per_sm == 0) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail, kTailBlock, 0);
+    cudaFuncSetAttribute(k_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailDynSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail, kTailBlock, kTailDynSmem);
     ctx->tail_blocks_per_sm = per_sm > 0 ? per_sm : 1;
   }
   return ctx->num_sms * ctx->tail_blocks_per_sm;
@@ -957,6 +963,9 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   c0.alive = g->n;
   c0.max_rounds = ws.round_cap;
   c0.sel = (unsigned long long)(g->n - g->nz_count);  // isolated: round-1 candidates
+  // test hook: a control block that disagrees with the states, which the
+  // round-end invariant check must report as the reference's logic_error
+  if (cfg->flags & TCMIS_F_DEBUG_CORRUPT) c0.alive += 1;
   *ws.h_ctrl = c0;
   bool step = cfg->observer || timing || (cfg->flags & TCMIS_F_HOST_LOOP);
   // the solve's first kernels: segment flags cleared, priorities, states, and
@@ -1016,6 +1025,9 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     a.tail_thr = 1 << 16;
     if (const char *env = std::getenv("TCMIS_TAIL_THRESHOLD")) a.tail_thr = std::atoi(env);
     a.tail_grid = tail_grid(ctx);
+    // k_tail keeps each block's share of its starting list in shared memory,
+    // one vertex per thread (tail.cuh): at most kTailBlock per block
+    a.tail_thr = (int32_t)std::min<int64_t>(a.tail_thr, (int64_t)a.tail_grid * kTailBlock);
   }
   if (seg_mode == 1 && a.tail_thr > 0)
     TCMIS_CUDA(cudaMemsetAsync(ws.segmark, 0, sizeof(uint32_t) * (size_t)nseg, st));
@@ -1157,6 +1169,38 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   TCMIS_CUDA(cudaStreamSynchronize(st));
   if (!finished) read_finish();
   *mis_count_out = h_mis_count;
+  {
+    const Ctrl &cf = finished ? ws.h_res->ctrl : *ws.h_ctrl;
+    int32_t corrupt = cf.corrupt;
+    if (!finished) {  // the host loop's last control block copy may predate the tail
+      Ctrl c{};
+      TCMIS_CUDA(cudaMemcpy(&c, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+      corrupt = c.corrupt;
+    }
+    if (corrupt)  // engine.cpp:152-153
+      return set_error(TCMIS_E_LOGIC,
+                       "candidate flagged on a non-alive vertex (a round's selected + removed + "
+                       "alive differs from its alive count before)");
+  }
+  if (!timing) {
+    // the phase stamps the round kernels left in the ring (%globaltimer):
+    // Phase 1 = select (push exclusion fused), Phase 2 = pull / tile
+    // exclusion, Phase 3 = update and round end; a k_tail round fuses all
+    // three and reports its pass + barrier as Phase 1
+    auto span_ms = [](unsigned long long a0, unsigned long long a1) {
+      return (a0 && a1 && a1 > a0) ? (float)((double)(a1 - a0) * 1e-6) : 0.f;
+    };
+    t1.assign(rounds_h.size(), 0.f);
+    t2.assign(rounds_h.size(), 0.f);
+    t3.assign(rounds_h.size(), 0.f);
+    for (size_t r = 0; r < rounds_h.size(); ++r) {
+      const DevRound &d = rounds_h[r];
+      const unsigned long long p2 = d.t[1] ? d.t[1] : d.t[2];
+      t1[r] = span_ms(d.t[0], p2 ? p2 : d.t[3]);
+      t2[r] = span_ms(d.t[1], d.t[2]);
+      t3[r] = span_ms(d.t[2], d.t[3]);
+    }
+  }
   if (timing) {
     // Phase 1 = the select kernels, Phase 2 = the pull-form exclusion
     // kernels (push-form exclusion is fused into Phase 1), Phase 3 = update;

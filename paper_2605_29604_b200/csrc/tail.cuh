@@ -7,34 +7,54 @@
 // list L_r does
 //
 //   * the Phase 3 of round r-1 (engine.cpp:121-160): L_r holds round r-1's
-//     non-candidates; a vertex whose decision byte says "excluded in round
-//     r-1" is Removed now (state, q = 0), the rest are alive in round r;
-//   * the Phase 1 of round r (engine.cpp:86-119) for the alive ones: a group
-//     of kGroup lanes scans the row from its end, kGroup*kTU entries per step,
-//     and stops at the first neighbour that is alive at the start of round r
-//     (q != 0 and not excluded in round r-1) with a higher key; rows longer
-//     than kTailLong are scanned by the whole block;
+//     non-candidates; a vertex tagged "excluded in round r-1" is Removed now
+//     (state, q = 0), the rest are alive in round r;
+//   * the Phase 1 of round r (engine.cpp:86-119) for the alive ones: a
+//     neighbour blocks v iff it is alive at the start of round r (q != 0 and
+//     not tagged for round r-1) and has a higher key;
 //   * the push form of Phase 2 (spmv.cpp:18-59, nc > 0) for round r's
-//     candidates: a blind store xm[r & 1][u] = 1 for every neighbour u.  The
-//     exclusion planes alternate with the round's parity, so round r's pushes
-//     never touch the plane round r reads for round r-1's removals -- the
-//     snapshot of the reference's bulk-synchronous round is kept, and round
-//     count and every statistic equal the reference's.  A stale mark from
-//     round r-2 (or an earlier solve) sits only on dead vertices (q = 0); the
-//     kernel clears both planes of the vertices alive at its start;
+//     candidates: xt[u] = tag(r) for every neighbour u alive at the round's
+//     start.  Round r reads only tag(r-1), so its own pushes never disturb the
+//     snapshot it reads -- the reference's bulk-synchronous round is kept, and
+//     the round count and every statistic equal the reference's;
 //   * L_{r+1} = round r's non-candidates.
 //
-// Round r's IterationStats are complete after round r+1's pass (its removed /
-// alive counts are counted there), so block 0 publishes round r-1 after
-// barrier r.  The solve's MIS-id compaction is fused at the end.  Data
-// written by other blocks in an earlier phase is read with ld.global.cg (L2).
-// (The first version ran S and U as separate phases, two barriers per round:
-// s22 rounds 2-4 took 75 us, ER rounds 2-6 65 us.)
+// Round tags.  xt is a u16 plane whose tags do not repeat across solves: the
+// solve's tags are tag(r) = base + 2 + (r - r0), and the next solve's base is
+// one past the last tag used, kept on the device (tslot[0]).  A vertex never
+// tagged holds 0 or an older solve's tag, so nothing has to be cleared before
+// the first round (the previous design cleared two byte planes of the
+// starting list and paid a grid barrier for it).  Once base passes kTagWrap
+// (every ~12k solves) the tags of the starting list are cleared and base
+// restarts at 0; a solve runs at most kMaxTailRounds tail rounds (beyond, it
+// flags the ring overflow and the host re-runs it step-wise).
+// A neighbour's tag is loaded only when its q is non-zero: most neighbours
+// of a late round's vertices left in round 1 (q = 0), and the tag plane is
+// cold in L2 (the first version loaded both together: s22's first tail round
+// took 29 us, mostly random DRAM sectors of a 4-byte tag plane).
+//
+// Block-resident lists.  The host caps the tail's starting list at 1024
+// vertices per block (tail_thr <= grid x 1024).  Block b takes a contiguous
+// slice of it, and from then on its survivors stay with it: the slice lives
+// in shared memory (id, row extent, q), entry k with thread k.  A round costs
+//   1. one THREAD per entry: its tag and the last kThrScan entries of its row
+//      are loaded together (the row extent is in shared memory), then their
+//      q / tag gathers -- two dependent round trips.  A blocker there (rows
+//      are scanned from the end, where R-MAT's low-degree, high-priority
+//      neighbours sit) settles a non-candidate; a row of <= kThrScan entries
+//      is settled either way, and a candidate pushes from its registers;
+//   2. rows left over: groups of kGroup lanes, kGroup*kTU entries per step
+//      (rows above kTailLong: the whole block);
+//   3. the survivors compacted in shared memory, and ONE grid barrier whose
+//      arrival atomic also sums the survivors (grid_barrier_sum): the release
+//      word says whether anyone is left, so no round trip decides the loop.
+// The per-round statistics are accumulated with fire-and-forget atomics and
+// published once, after the last round, by block 0.
 #pragma once
 
 #include <cub/cub.cuh>
 
-#include "common.cuh"
+#include "scan.cuh"
 
 namespace tcmis_b200 {
 
@@ -43,7 +63,7 @@ namespace tcmis_b200 {
 // into g_tail_prof (read back by tcmis_debug_tail_prof, solver.cu)
 __device__ unsigned long long g_tail_prof[256];
 __device__ int g_tail_prof_n;
-__device__ unsigned long long g_tail_blk[3][1024];  // first round: per block (t_short, t_long_end, nlong)
+__device__ unsigned long long g_tail_blk[3][1024];  // first round: per block (t_thread, t_end, ndeferred)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -67,25 +87,39 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef TCMIS_TAIL_GROUP
 #define TCMIS_TAIL_GROUP 8
 #endif
-constexpr int kGroup = TCMIS_TAIL_GROUP;  // lanes per vertex in the tail kernel
+constexpr int kGroup = TCMIS_TAIL_GROUP;  // lanes per deferred row
 #ifndef TCMIS_TAIL_UNROLL
 #define TCMIS_TAIL_UNROLL 16
 #endif
-constexpr int kTU = TCMIS_TAIL_UNROLL;  // independent loads per lane per step
-constexpr int kTailBlock = 1024;  // one block per SM: 148 arrivals per barrier
+constexpr int kTU = TCMIS_TAIL_UNROLL;  // independent loads per lane per group step
+constexpr int kTailBlock = 1024;        // one block per SM: 148 arrivals per barrier
+constexpr int kTailWarps = kTailBlock / 32;
+constexpr int kTailGroups = kTailBlock / kGroup;
+#ifndef TCMIS_TAIL_THR_SCAN
+#define TCMIS_TAIL_THR_SCAN 16
+#endif
+constexpr int kThrScan = TCMIS_TAIL_THR_SCAN;  // row entries a thread scans on its own
 #ifndef TCMIS_TAIL_LONG
 #define TCMIS_TAIL_LONG 512
 #endif
 constexpr int64_t kTailLong = TCMIS_TAIL_LONG;  // rows above this are scanned by a whole block
-constexpr int kTailLongCap = 256;               // per-block list of such rows per round
+constexpr int kTailLongCap = 256;               // per-block list of such rows per chunk
+constexpr int kMaxTailRounds = 4096;            // = the host's round ring (DevRound) capacity
+constexpr uint32_t kTagWrap = 0xFFFFu - kMaxTailRounds - 4;  // restart the round tags beyond this base
+constexpr int kCompactV = 512;                  // vertices per warp step of the MIS write pass
+constexpr int kTailMaxWarps = 32 * 2048;        // capacity of one per-warp count buffer
+// dynamic shared memory of k_tail: the write pass's per-warp staging
+constexpr size_t kTailDynSmem = sizeof(int32_t) * kTailWarps * kCompactV;
 
 struct TailArgs {
   const int64_t *off;
   const int32_t *nbr;
-  uint32_t *prio;
+  int64_t vnnz;             // nnz, negated if nbr is not 16-byte aligned (scan.cuh)
+  const uint32_t *prio;
   uint16_t *q;
-  uint8_t *next;
-  uint8_t *xm0, *xm1;       // exclusion planes by round parity
+  const uint8_t *next;      // next[v] == 1: candidate of a per-round kernel round (read-only here)
+  uint16_t *xt;             // round tags (see above)
+  uint32_t *tslot;          // [0] tag base, [1] solve counter: persist across solves
   uint8_t *state;
   uint8_t *segflag;         // byte flags (seg_mode 2)
   uint32_t *segmark;        // seg_mode 1: round that last counted the segment
@@ -97,46 +131,71 @@ struct TailArgs {
   Ctrl *ctrl;
   int32_t *wl0, *wl1;
   DevRound *rounds;
-  unsigned *bar;            // [0] arrivals, [1] generation
+  unsigned *bar;            // grid_barrier_sum: [0..1] arrivals | sum, [2] generation
   // the solve's final step, fused: ascending MIS ids (engine.cpp:293)
-  int compact;
   int32_t n;
   int32_t *mis;
   int64_t *mis_count;
-  unsigned *blockcnt;       // gridDim.x per-block counts
+  unsigned *warpcnt;        // 2 x kTailMaxWarps per-warp InMIS counts, by solve parity
   HostRes *pack;            // non-null: also leave the solve's results in mapped host memory
 };
 
-__device__ __forceinline__ void grid_barrier(unsigned *bar) {
+// Grid barrier whose arrival also sums one value per block: bar[0..1] is a
+// u64 word (arrivals << 40 | sum), bar[2] the generation word (gen << 1 |
+// "the sum was 0").  The last block to arrive resets the word and publishes
+// the next generation with the flag, so the waiting blocks learn the sum's
+// verdict from the very load that releases them.  Returns the flag.
+__device__ __forceinline__ bool grid_barrier_sum(unsigned *bar, unsigned x) {
+  __shared__ unsigned s_flag;
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned *gen = bar + 1;
+    unsigned long long *word = reinterpret_cast<unsigned long long *>(bar);
+    volatile unsigned *gen = bar + 2;
     const unsigned g = *gen;
     __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0;
+    const unsigned long long old = atomicAdd(word, (1ull << 40) | (unsigned long long)x);
+    unsigned res;
+    if ((unsigned)(old >> 40) == gridDim.x - 1) {
+      const unsigned long long sum = (old & ((1ull << 40) - 1)) + x;
+      *word = 0;
       __threadfence();
-      atomicAdd(bar + 1, 1u);
+      res = (((g >> 1) + 1u) << 1) | (sum == 0 ? 1u : 0u);
+      atomicExch(bar + 2, res);
     } else {
-      while (*gen == g) __nanosleep(64);
+      while (((res = *gen) >> 1) == (g >> 1)) __nanosleep(32);
     }
     __threadfence();
+    s_flag = res & 1u;
   }
   __syncthreads();
+  return s_flag != 0;
 }
 
-
-__device__ __forceinline__ uint8_t *xplane(const TailArgs &a, int r) {
-  return (r & 1) ? a.xm1 : a.xm0;
+// The compaction's range of warp gw: 16-vertex units, contiguous per warp.
+struct WarpRange {
+  int64_t lo, hi;  // vertices [lo, hi)
+  int32_t len;     // vertices per warp (a multiple of 16)
+};
+__device__ __forceinline__ WarpRange warp_range(int32_t n, int nwarps, int gw) {
+  const int64_t units = ((int64_t)n + 15) / 16;
+  const int64_t per = (units + nwarps - 1) / nwarps;
+  WarpRange r;
+  r.len = (int32_t)(per * 16);
+  r.lo = min((int64_t)n, (int64_t)gw * per * 16);
+  r.hi = min((int64_t)n, r.lo + per * 16);
+  return r;
 }
 
-// A candidate of the tail (mark_candidate + the tile counter of seg_mode 1:
-// exactly one candidate of the round counts its block column).
+// A candidate of the tail: InMIS, its compaction range counted, and the tile
+// counter of seg_mode 1 (exactly one candidate of the round counts its block
+// column).  next[] is not written: it keeps marking the per-round kernels'
+// candidates, which the compaction's count pass reads while the tail runs.
 __device__ __forceinline__ void tail_candidate(const TailArgs &a, int32_t v, int round,
+                                               unsigned *wcnt, int32_t wlen,
                                                unsigned long long &sel,
                                                unsigned long long &ev) {
-  a.next[v] = 1;
   a.state[v] = TCMIS_IN_MIS;
+  atomicAdd(&wcnt[v / wlen], 1u);
   ++sel;
   const int32_t sb = seg_of(v, a.T);
   if (a.seg_mode == 2) {
@@ -147,43 +206,22 @@ __device__ __forceinline__ void tail_candidate(const TailArgs &a, int32_t v, int
   }
 }
 
-// u blocks v in round r: alive at the start of round r (q != 0, not
-// excluded in round r-1), higher key; `alive` reports the first part
-__device__ __forceinline__ bool tail_blocks(const TailArgs &a, int32_t u, const uint8_t *dead,
-                                            uint32_t qv, uint64_t kv, bool &alive) {
+// u blocks v in round r: alive at the start of round r (q != 0, not tagged
+// for round r-1), higher key; `alive` reports the first part.  q[u] and the
+// tag are independent loads: one round trip for both.
+__device__ __forceinline__ bool tail_blocks(const TailArgs &a, int32_t u, uint32_t tprev,
+                                            bool first, uint32_t qv, int32_t v, bool &alive) {
   const uint32_t qu = __ldcg(&a.q[u]);
-  const uint8_t dx = __ldcg(&dead[u]);  // independent of qu: one round trip for both
-  alive = qu != 0 && !dx;
+  alive = false;
+  if (qu == 0) return false;
+  alive = first || __ldcg(&a.xt[u]) != (uint16_t)tprev;  // no tag is tag(r0 - 1)
   if (!alive) return false;
-  return qu != qv ? qu > qv : key_of(__ldcg(&a.prio[u]), u) > kv;
+  return qu != qv ? qu > qv : key_of(__ldg(&a.prio[u]), u) > key_of(__ldg(&a.prio[v]), v);
 }
 
-__device__ __forceinline__ bool tail_alive(const TailArgs &a, int32_t u, const uint8_t *dead) {
-  const uint32_t qu = __ldcg(&a.q[u]);
-  const uint8_t dx = __ldcg(&dead[u]);
-  return qu != 0 && !dx;
-}
-
-// the lanes of one group stay converged (same vertex, same trip count);
-// different groups of a warp may diverge, so the vote uses the group's mask
-__device__ __forceinline__ unsigned group_any(bool b, unsigned gmask) {
-  return __ballot_sync(gmask, b);
-}
-
-// A long row is handed to the block (list in shared memory, capacity
-// kTailLongCap; on overflow the group scans it itself).  Returns whether the
-// group should skip the row -- the same answer for all lanes of the group.
-__device__ __forceinline__ bool defer_long(int32_t v, int32_t *s_long, int *s_nlong, int gl,
-                                           unsigned gmask, int lane) {
-  int listed = 0;
-  if (gl == 0) {
-    const int k = atomicAdd(s_nlong, 1);
-    if (k < kTailLongCap) {
-      s_long[k] = v;
-      listed = 1;
-    }
-  }
-  return __shfl_sync(gmask, listed, lane & ~(kGroup - 1)) != 0;
+__device__ __forceinline__ bool tail_alive(const TailArgs &a, int32_t u, uint32_t tprev,
+                                           bool first) {
+  return __ldcg(&a.q[u]) != 0 && (first || __ldcg(&a.xt[u]) != (uint16_t)tprev);
 }
 
 __device__ __forceinline__ unsigned long long *slot_field(const TailArgs &a, int round, int f) {
@@ -191,91 +229,71 @@ __device__ __forceinline__ unsigned long long *slot_field(const TailArgs &a, int
   return f == 0 ? &r->sel : f == 1 ? &r->rem : f == 2 ? &r->alive : &r->eval;
 }
 
-// Ascending ids of the InMIS vertices (the reference sorts result.mis,
-// engine.cpp:293): block b owns a contiguous range of 16-vertex units and
-// walks it in tiles of kTailBlock units (one coalesced 16-byte state load per
-// thread): per-block counts -> grid barrier -> every block sums the counts
-// before it and writes its ids tile by tile (block scan of the per-thread
-// counts).  Replaces a separate cub::DeviceSelect (2 launches, 17 us at
-// R-MAT s22, 191 us at s26).
-__device__ __forceinline__ uint32_t in_mis_mask16(const TailArgs &a, int64_t u) {
-  const uint4 w = __ldcg(reinterpret_cast<const uint4 *>(a.state) + u);
+// 16 states (or decision bytes) -> bit j set iff byte j == val
+__device__ __forceinline__ uint32_t eq_mask16(uint4 w, uint32_t val) {
   const uint32_t x[4] = {w.x, w.y, w.z, w.w};
   uint32_t m = 0;
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t e = __vcmpeq4(x[k], val * 0x01010101u);  // 0xff per equal byte
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (((x[k] >> (8 * j)) & 0xffu) == TCMIS_IN_MIS) m |= 1u << (4 * k + j);
-  const int64_t left = (int64_t)a.n - 16 * u;  // padding bytes past n
-  if (left < 16) m &= (1u << left) - 1u;
+    for (int j = 0; j < 4; ++j) m |= ((e >> (8 * j + 7)) & 1u) << (4 * k + j);
+  }
   return m;
 }
 
-constexpr int kCU = 4;  // 16-vertex units per thread per tile (independent 16-B loads)
-
-__device__ void compact_mis(const TailArgs &a) {
+// Ascending ids of the InMIS vertices (the reference sorts result.mis,
+// engine.cpp:293).  Warp gw of the grid owns a contiguous vertex range; its
+// InMIS count is known without a pass at the end: the count pass at the
+// tail's start counted the per-round kernels' candidates (next == 1, which
+// the tail never writes) and every tail candidate added itself (atomic on its
+// range).  After the rounds' last grid barrier every block sums the counts
+// before it, and every warp writes its range's ids on its own: 16 states per
+// lane per step (16-byte loads, the next step's prefetched), ids staged in
+// the warp's shared-memory slice and copied out coalesced.  No block barrier
+// inside the write loop, no grid barrier at all (the previous version counted
+// per block at the end: a count pass plus a grid barrier, 6 us at s22).
+__device__ void compact_mis(const TailArgs &a, unsigned *wcnt, unsigned *wnext, int32_t *stage) {
   __shared__ unsigned long long s_base;
-  const int64_t units = ((int64_t)a.n + 15) / 16;
-  const int64_t per_block = (units + gridDim.x - 1) / gridDim.x;
-  const int64_t u0 = min(units, (int64_t)blockIdx.x * per_block);
-  const int64_t u1 = min(units, u0 + per_block);
-  constexpr int64_t kTile = (int64_t)kTailBlock * kCU;
-  int cnt = 0;
-  for (int64_t t0 = u0; t0 < u1; t0 += kTile) {
-    uint32_t m[kCU];
-#pragma unroll
-    for (int k = 0; k < kCU; ++k) {
-      const int64_t u = t0 + (int64_t)k * kTailBlock + threadIdx.x;
-      m[k] = u < u1 ? in_mis_mask16(a, u) : 0u;
-    }
-#pragma unroll
-    for (int k = 0; k < kCU; ++k) cnt += __popc(m[k]);
-  }
-  cnt = __reduce_add_sync(0xffffffffu, cnt);
-  if (threadIdx.x == 0) s_base = 0;
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&s_base, (unsigned long long)cnt);
-  __syncthreads();
-  if (threadIdx.x == 0) a.blockcnt[blockIdx.x] = (unsigned)s_base;
-  TAIL_MARK(5, 0);
-  grid_barrier(a.bar);
-  TAIL_MARK(6, 0);
-  unsigned long long before = 0;
-  for (int j = threadIdx.x; j < (int)blockIdx.x; j += kTailBlock) before += __ldcg(&a.blockcnt[j]);
-  before = __reduce_add_sync(0xffffffffu, (unsigned)before);
-  if (threadIdx.x == 0) s_base = 0;
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0 && before) atomicAdd(&s_base, before);
-  __syncthreads();
-  int64_t base = (int64_t)s_base;
-  // write pass: warp w of a tile owns 256 consecutive vertices (8 per lane,
-  // one 8-byte state load); the warp stages its ids in shared memory in order
-  // and copies them out coalesced (a thread writing its own run directly
-  // made every store instruction touch 32 sectors: 247 us at s26)
-  __shared__ int32_t stage[kTailBlock / 32][256];
-  __shared__ int s_woff[kTailBlock / 32 + 1];
+  __shared__ unsigned s_woff[kTailWarps + 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t v_lo = u0 * 16, v_hi = min((int64_t)a.n, u1 * 16);
-  constexpr int64_t kStep = 256ll * (kTailBlock / 32);
-  // the next tile's 8 states per lane are loaded before this tile's barriers
-  uint2 xn = make_uint2(0, 0);
-  if (v_lo + (int64_t)w * 256 + lane * 8 < v_hi)
-    xn = __ldcg(reinterpret_cast<const uint2 *>(a.state + v_lo + (int64_t)w * 256 + lane * 8));
-  for (int64_t t0 = v_lo; t0 < v_hi; t0 += kStep) {
-    const int64_t v0 = t0 + (int64_t)w * 256 + lane * 8;
-    const uint2 x = xn;
-    if (v0 + kStep < v_hi)
-      xn = __ldcg(reinterpret_cast<const uint2 *>(a.state + v0 + kStep));
-    uint32_t m = 0;
-    if (v0 < v_hi) {
+  const int nwarps = gridDim.x * kTailWarps;
+  const int gw = blockIdx.x * kTailWarps + w;
+  unsigned long long before = 0;
+  for (int j = threadIdx.x; j < blockIdx.x * kTailWarps; j += kTailBlock) before += __ldcg(&wcnt[j]);
+  for (int o = 16; o; o >>= 1) before += __shfl_down_sync(0xffffffffu, before, o);
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  if (lane == 0 && before) atomicAdd(&s_base, before);
+  if (w == 0) {  // exclusive scan of the block's 32 warp counts
+    static_assert(kTailWarps == 32, "one warp count per lane");
+    const unsigned t = __ldcg(&wcnt[blockIdx.x * kTailWarps + lane]);
+    unsigned sc = t;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (((x.x >> (8 * j)) & 0xffu) == TCMIS_IN_MIS) m |= 1u << j;
-        if (((x.y >> (8 * j)) & 0xffu) == TCMIS_IN_MIS) m |= 1u << (4 + j);
-      }
-      const int64_t left = v_hi - v0;
-      if (left < 8) m &= (1u << left) - 1u;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, sc, o);
+      if (lane >= o) sc += y;
+    }
+    s_woff[lane] = sc - t;
+    if (lane == 31) s_woff[32] = sc;
+  }
+  __syncthreads();
+  int64_t base = (int64_t)s_base + s_woff[w];
+  const WarpRange R = warp_range(a.n, nwarps, gw);
+  int32_t *stg = stage + w * kCompactV;
+  uint4 xn = make_uint4(0, 0, 0, 0);
+  if (R.lo + lane * 16 < R.hi)
+    xn = __ldcg(reinterpret_cast<const uint4 *>(a.state + R.lo + lane * 16));
+  for (int64_t t0 = R.lo; t0 < R.hi; t0 += kCompactV) {
+    const int64_t v0 = t0 + lane * 16;
+    const uint4 x = xn;
+    if (v0 + kCompactV < R.hi)
+      xn = __ldcg(reinterpret_cast<const uint4 *>(a.state + v0 + kCompactV));
+    uint32_t m = 0;
+    if (v0 < R.hi) {
+      m = eq_mask16(x, TCMIS_IN_MIS);
+      const int64_t left = R.hi - v0;
+      if (left < 16) m &= (1u << left) - 1u;
     }
     const int c = __popc(m);
     int incl = c;
@@ -284,48 +302,35 @@ __device__ void compact_mis(const TailArgs &a) {
       const int y = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += y;
     }
-    const int excl = incl - c;
-    if (lane == 31) s_woff[w] = incl;
-    int k = excl;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int k = incl - c;
     while (m) {
       const int bit = __ffs(m) - 1;
       m &= m - 1;
-      stage[w][k++] = (int32_t)(v0 + bit);
+      stg[k++] = (int32_t)(v0 + bit);
     }
-    __syncthreads();
-    if (w == 0) {  // exclusive scan of the 32 warp counts, by shuffles
-      static_assert(kTailBlock / 32 == 32, "one warp count per lane");
-      const int t = s_woff[lane];
-      int sc = t;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, sc, o);
-        if (lane >= o) sc += y;
-      }
-      s_woff[lane] = sc - t;
-      if (lane == 31) s_woff[32] = sc;
-    }
-    __syncthreads();
-    const int wc = (w + 1 < kTailBlock / 32 ? s_woff[w + 1] : s_woff[kTailBlock / 32]) - s_woff[w];
-    for (int i = lane; i < wc; i += 32) a.mis[base + s_woff[w] + i] = stage[w][i];
-    base += s_woff[kTailBlock / 32];
-    __syncthreads();  // stage / s_woff reuse
+    __syncwarp();
+    for (int i = lane; i < total; i += 32) a.mis[base + i] = stg[i];
+    base += total;
+    __syncwarp();
   }
-  if (blockIdx.x == gridDim.x - 1) {
-    if (threadIdx.x == 0) *a.mis_count = base;
-    if (a.pack) {  // k_pack's job, done here: one graph node less
-      // word copies through L2 (ld.global.cg): written by other blocks
-      const int32_t cap = __ldcg(&a.ctrl->max_rounds);
-      const int nr = (int)(sizeof(DevRound) / 4) * (cap < 64 ? cap : 64);
-      const uint32_t *rs = reinterpret_cast<const uint32_t *>(a.rounds);
-      uint32_t *rd = reinterpret_cast<uint32_t *>(a.pack->rounds);
-      for (int i = threadIdx.x; i < nr; i += kTailBlock) rd[i] = __ldcg(rs + i);
-      const uint32_t *cs = reinterpret_cast<const uint32_t *>(a.ctrl);
-      uint32_t *cd = reinterpret_cast<uint32_t *>(&a.pack->ctrl);
-      for (int i = threadIdx.x; i < (int)(sizeof(Ctrl) / 4); i += kTailBlock) cd[i] = __ldcg(cs + i);
-      if (threadIdx.x == 0) a.pack->mis_count = (long long)base;
-      __threadfence_system();
-    }
+  if (lane == 0) wnext[gw] = 0;  // the next solve's buffer (this one's is read by other blocks)
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    const long long total = (long long)s_base + s_woff[kTailWarps];
+    *a.mis_count = total;
+    if (a.pack) a.pack->mis_count = total;
+  }
+  if (a.pack && blockIdx.x == gridDim.x - 1) {  // k_pack's job, done here: one graph node less
+    // word copies through L2 (ld.global.cg): written by other blocks
+    const int32_t cap = __ldcg(&a.ctrl->max_rounds);
+    const int nr = (int)(sizeof(DevRound) / 4) * (cap < 64 ? cap : 64);
+    const uint32_t *rs = reinterpret_cast<const uint32_t *>(a.rounds);
+    uint32_t *rd = reinterpret_cast<uint32_t *>(a.pack->rounds);
+    for (int i = threadIdx.x; i < nr; i += kTailBlock) rd[i] = __ldcg(rs + i);
+    const uint32_t *cs = reinterpret_cast<const uint32_t *>(a.ctrl);
+    uint32_t *cd = reinterpret_cast<uint32_t *>(&a.pack->ctrl);
+    for (int i = threadIdx.x; i < (int)(sizeof(Ctrl) / 4); i += kTailBlock) cd[i] = __ldcg(cs + i);
+    __threadfence_system();
   }
 }
 
@@ -333,65 +338,175 @@ __device__ void compact_mis(const TailArgs &a) {
 #define TCMIS_TAIL_MINB 1
 #endif
 __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a) {
-  __shared__ int32_t s_long[kTailLongCap];
-  __shared__ int s_nlong;
+  extern __shared__ int32_t s_stage[];  // kTailDynSmem: compact_mis's staging
+  // the block's list: entry k = (id, row extent, q), handled by thread k
+  __shared__ int32_t s_v[kTailBlock];
+  __shared__ int64_t s_s[kTailBlock], s_e[kTailBlock];
+  __shared__ uint16_t s_q[kTailBlock];
+  __shared__ uint8_t s_keep[kTailBlock];  // the entry's verdict: 1 = non-candidate
+  __shared__ int16_t s_def[kTailBlock];   // entries left to the groups
+  __shared__ int16_t s_long[kTailLongCap];  // ... and to the whole block
+  __shared__ int s_nd, s_nlong, s_nl;
   __shared__ unsigned long long s_acc[4];
   Ctrl *ctrl = a.ctrl;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int gl = lane & (kGroup - 1);
-  const unsigned gmask = ((1u << kGroup) - 1u) << (lane & ~(kGroup - 1));
-  const int64_t gid = ((int64_t)blockIdx.x * kTailBlock + threadIdx.x) / kGroup;
-  const int64_t ngroups = ((int64_t)gridDim.x * kTailBlock) / kGroup;
-  constexpr int kW = kGroup * kTU;  // entries per group step: short rows settle in one step
-  if (threadIdx.x == 0) s_nlong = 0;
+  const unsigned gmask = (kGroup == 32 ? 0xffffffffu : ((1u << kGroup) - 1u)) << (lane & ~(kGroup - 1));
+  const int grp = threadIdx.x / kGroup;
+  constexpr int kW = kGroup * kTU;  // entries per group step
   if (threadIdx.x < 4) s_acc[threadIdx.x] = 0;
-  __syncthreads();
+  if (threadIdx.x == 0) {
+    s_nd = 0;
+    s_nlong = 0;
+    s_nl = 0;
+  }
+  const uint32_t base0 = __ldcg(&a.tslot[0]);
+  const uint32_t solve = __ldcg(&a.tslot[1]);
+  const int nwarps = gridDim.x * kTailWarps;
+  unsigned *wcnt = a.warpcnt + (solve & 1u) * kTailMaxWarps;
+  unsigned *wnext = a.warpcnt + ((solve + 1u) & 1u) * kTailMaxWarps;
+  const int32_t wlen = warp_range(a.n, nwarps, 0).len;
   const int r0 = *(volatile int *)&ctrl->round;
   const int64_t cnt0 = *(volatile int *)&ctrl->wl_count[r0 & 1];
   TAIL_MARK(1, cnt0);
-  if (cnt0 > 0) {
-    // the exclusion planes of the vertices alive at the tail's start (every
-    // list below is a subset): stale marks elsewhere sit on dead vertices
+  // the block's slice of the starting list (<= kTailBlock entries: host cap)
+  int nl = (int)(cnt0 * (blockIdx.x + 1) / gridDim.x - cnt0 * blockIdx.x / gridDim.x);
+  {
+    const int64_t lo = cnt0 * blockIdx.x / gridDim.x;
     const int32_t *in0 = (r0 & 1) ? a.wl1 : a.wl0;
-    for (int64_t i = (int64_t)blockIdx.x * kTailBlock + threadIdx.x; i < cnt0;
-         i += (int64_t)gridDim.x * kTailBlock) {
-      const int32_t v = __ldcg(&in0[i]);
-      a.xm0[v] = 0;
-      a.xm1[v] = 0;
+    if (threadIdx.x < nl) {
+      const int32_t v = __ldcg(&in0[lo + threadIdx.x]);
+      s_v[threadIdx.x] = v;
+      s_s[threadIdx.x] = __ldg(&a.off[v]);
+      s_e[threadIdx.x] = __ldg(&a.off[v + 1]);
+      s_q[threadIdx.x] = __ldcg(&a.q[v]);
     }
-    grid_barrier(a.bar);
   }
-  for (int round = r0; cnt0 > 0; ++round) {
+  {  // count pass: the per-round kernels' candidates in this warp's range
+    const WarpRange R = warp_range(a.n, nwarps, blockIdx.x * kTailWarps + w);
+    unsigned c = 0;
+#pragma unroll 4
+    for (int64_t v0 = R.lo + lane * 16; v0 < R.hi; v0 += 32 * 16) {
+      uint32_t m = eq_mask16(__ldcg(reinterpret_cast<const uint4 *>(a.next + v0)), 1u);
+      const int64_t left = R.hi - v0;
+      if (left < 16) m &= (1u << left) - 1u;
+      c += __popc(m);
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0 && c) atomicAdd(&wcnt[blockIdx.x * kTailWarps + w], c);
+  }
+  uint32_t base = base0;
+  if (base0 >= kTagWrap && cnt0 > 0) {
+    // once every ~4e9 rounds: clear the tags of the vertices alive at the
+    // start (every later list is a subset) and restart the tags at 1
+    __syncthreads();
+    if (threadIdx.x < nl) a.xt[s_v[threadIdx.x]] = 0;
+    base = 0;
+    grid_barrier_sum(a.bar, 1);
+  }
+  TAIL_MARK(8, 0);
+  int round = r0;
+  bool done = cnt0 == 0;
+  if (done) grid_barrier_sum(a.bar, 0);  // the count pass must be complete before the compaction
+  __syncthreads();                       // the list's shared-memory fill
+  for (; !done; ++round) {
+    if (round - r0 >= kMaxTailRounds) {  // uniform: the ring overflows, the host re-runs step-wise
+      if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->overflow = 1;
+      break;
+    }
     const bool first = round == r0;
-    const int64_t cnt = first ? cnt0 : (int64_t) * (volatile int *)&ctrl->tail_cnt[round % 3];
-    const int32_t *in = (round & 1) ? a.wl1 : a.wl0;
-    int32_t *out = (round & 1) ? a.wl0 : a.wl1;
-    int *out_cnt = &ctrl->tail_cnt[(round + 1) % 3];
-    const uint8_t *dead = xplane(a, round - 1);
-    uint8_t *push = xplane(a, round);
+    const uint32_t tprev = base + 1u + (uint32_t)(round - r0);  // tag(round - 1)
+    const uint32_t tcur = tprev + 1u;                           // tag(round)
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      a.rounds[(round - 1) % ctrl->max_rounds].t[0] = gtimer_ns();
     unsigned long long sel = 0, ev = 0, rem = 0, alive = 0;
-    for (int64_t i = gid; i < cnt; i += ngroups) {
-      const int32_t v = __ldcg(&in[i]);
-      if (!first && __ldcg(&dead[v])) {  // removed in round - 1
-        if (gl == 0) {
-          mark_removed(v, a.state, a.q);
-          ++rem;
+    const int k = threadIdx.x;
+    const bool have = k < nl;
+    int32_t v = -1;
+    int64_t s = 0, e = 0;
+    uint32_t qv = 0;
+    uint8_t keep = 0;
+    if (have) {
+      v = s_v[k];
+      s = s_s[k];
+      e = s_e[k];
+      qv = s_q[k];
+      // 1. the entry's tag and the last kThrScan row entries, loaded together
+      const uint32_t tv = first ? 0u : __ldcg(&a.xt[v]);  // loaded with the row entries
+      // the row's last kThrScan/4 aligned 16-byte windows (13-16 entries):
+      // one wavefront per lane and window instead of one per entry
+      int32_t u[kThrScan];
+      int64_t hi = e;
+#pragma unroll
+      for (int j = 0; j < kThrScan / 4; ++j) {
+        if (hi > s) {
+          hi = load_window_down(a.nbr, a.vnnz, s, hi, &u[4 * j]);
+        } else {
+          u[4 * j] = u[4 * j + 1] = u[4 * j + 2] = u[4 * j + 3] = -1;
         }
-        continue;
       }
-      if (gl == 0) ++alive;
-      const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
-      if (e - s > kTailLong && defer_long(v, s_long, &s_nlong, gl, gmask, lane)) continue;
-      const uint64_t kv = key_of(__ldcg(&a.prio[v]), v);
-      const uint32_t qv = __ldcg(&a.q[v]);
+      if (!first && tv == (uint16_t)tprev) {  // excluded in round - 1
+        mark_removed(v, a.state, a.q);
+        ++rem;
+      } else {
+        ++alive;
+        bool b = false;
+        uint32_t live = 0;
+#pragma unroll
+        for (int j = 0; j < kThrScan; ++j)
+          if (u[j] >= 0) {
+            bool al;
+            b |= tail_blocks(a, u[j], tprev, first, qv, v, al);
+            live |= (uint32_t)al << j;
+          }
+        if (b) {
+          keep = 1;
+        } else if (hi <= s) {  // the whole row was in the windows
+          tail_candidate(a, v, round, wcnt, wlen, sel, ev);
+#pragma unroll
+          for (int j = 0; j < kThrScan; ++j)
+            if ((live >> j) & 1u) a.xt[u[j]] = (uint16_t)tcur;
+        } else {
+          s_def[atomicAdd(&s_nd, 1)] = (int16_t)k;
+        }
+      }
+      s_keep[k] = keep;
+    }
+    __syncthreads();
+    TAIL_MARK(9, s_nd);
+#ifdef TCMIS_TAIL_PROF
+    if (first && threadIdx.x == 0) {
+      g_tail_blk[0][blockIdx.x] = gtimer();
+      g_tail_blk[2][blockIdx.x] = (unsigned long long)s_nd;
+    }
+#endif
+    // 2. the deferred rows: kGroup lanes each (the whole row again, from the
+    // end, so a row of <= kW entries pushes from registers)
+    const int nd = s_nd;
+    for (int d = grp; d < nd; d += kTailGroups) {
+      const int kd = s_def[d];
+      const int32_t dv = s_v[kd];
+      const int64_t ds = s_s[kd], de = s_e[kd];
+      if (de - ds > kTailLong) {
+        int listed = 0;
+        if (gl == 0) {
+          const int kk = atomicAdd(&s_nlong, 1);
+          if (kk < kTailLongCap) {
+            s_long[kk] = (int16_t)kd;
+            listed = 1;
+          }
+        }
+        if (__shfl_sync(gmask, listed, lane & ~(kGroup - 1))) continue;
+      }
+      const uint32_t dq = s_q[kd];
       bool blocked = false;
       int32_t u[kTU];
-      uint32_t live = 0;  // neighbours of the last chunk alive at the round's start
-      for (int64_t hi = e; hi > s && !blocked; hi -= kW) {
+      uint32_t live = 0;
+      for (int64_t top = de; top > ds && !blocked; top -= kW) {
 #pragma unroll
         for (int j = 0; j < kTU; ++j) {
-          const int64_t idx = hi - 1 - gl - kGroup * j;
-          u[j] = idx >= s ? __ldg(&a.nbr[idx]) : -1;
+          const int64_t idx = top - 1 - gl - kGroup * j;
+          u[j] = idx >= ds ? __ldg(&a.nbr[idx]) : -1;
         }
         bool b = false;
         live = 0;
@@ -399,81 +514,93 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
         for (int j = 0; j < kTU; ++j)
           if (u[j] >= 0) {
             bool al;
-            b |= tail_blocks(a, u[j], dead, qv, kv, al);
+            b |= tail_blocks(a, u[j], tprev, first, dq, dv, al);
             live |= (uint32_t)al << j;
           }
-        blocked = group_any(b, gmask) != 0;
+        blocked = __ballot_sync(gmask, b) != 0;
       }
       if (!blocked) {
-        if (gl == 0) tail_candidate(a, v, round, sel, ev);
-        // push to the neighbours alive at the round's start only: after round
-        // 1 most neighbours are dead, and every skipped byte store is a
-        // random partial-sector write saved (R-MAT s22 round 2: ~1.4M)
-        if (e - s <= kW) {  // the row was one chunk: its ids and flags are still here
+        if (gl == 0) tail_candidate(a, dv, round, wcnt, wlen, sel, ev);
+        if (de - ds <= kW) {
 #pragma unroll
           for (int j = 0; j < kTU; ++j)
-            if ((live >> j) & 1u) push[u[j]] = 1;
+            if ((live >> j) & 1u) a.xt[u[j]] = (uint16_t)tcur;
         } else {
-          for (int64_t hi = e; hi > s; hi -= kW) {
+          for (int64_t top = de; top > ds; top -= kW) {
 #pragma unroll
             for (int j = 0; j < kTU; ++j) {
-              const int64_t idx = hi - 1 - gl - kGroup * j;
-              u[j] = idx >= s ? __ldg(&a.nbr[idx]) : -1;
+              const int64_t idx = top - 1 - gl - kGroup * j;
+              u[j] = idx >= ds ? __ldg(&a.nbr[idx]) : -1;
             }
 #pragma unroll
             for (int j = 0; j < kTU; ++j)
-              if (u[j] >= 0 && tail_alive(a, u[j], dead)) push[u[j]] = 1;
+              if (u[j] >= 0 && tail_alive(a, u[j], tprev, first)) a.xt[u[j]] = (uint16_t)tcur;
           }
         }
       } else if (gl == 0) {
-        out[atomicAdd(out_cnt, 1)] = v;
+        s_keep[kd] = 1;
       }
     }
     __syncthreads();
+    TAIL_MARK(10, s_nlong);
+    // 3. rows above kTailLong: the whole block, kBU entries per thread and
+    // step (a row of <= kBU * kTailBlock entries pushes from registers)
     const int nlong = min(s_nlong, kTailLongCap);
-#ifdef TCMIS_TAIL_PROF
-    if (first && threadIdx.x == 0) {
-      g_tail_blk[0][blockIdx.x] = gtimer();
-      g_tail_blk[2][blockIdx.x] = (unsigned long long)s_nlong;
-    }
-#endif
-    for (int k = 0; k < nlong; ++k) {
-      const int32_t v = s_long[k];
-      const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
-      const uint64_t kv = key_of(__ldcg(&a.prio[v]), v);
-      const uint32_t qv = __ldcg(&a.q[v]);
+    for (int kk = 0; kk < nlong; ++kk) {
+      const int kd = s_long[kk];
+      const int32_t dv = s_v[kd];
+      const int64_t ds = s_s[kd], de = s_e[kd];
+      const uint32_t dq = s_q[kd];
+      constexpr int kBU = 8;
+      constexpr int64_t kBW = (int64_t)kBU * kTailBlock;
       bool blocked = false;
-      for (int64_t hi = e; hi > s && !blocked; hi -= 4 * kTailBlock) {
-        bool b = false;
+      int32_t x[kBU];
+      uint32_t live = 0;
+      for (int64_t top = de; top > ds && !blocked; top -= kBW) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int64_t idx = hi - 1 - threadIdx.x - (int64_t)kTailBlock * j;
-          bool al;
-          if (idx >= s) b |= tail_blocks(a, __ldg(&a.nbr[idx]), dead, qv, kv, al);
+        for (int j = 0; j < kBU; ++j) {
+          const int64_t idx = top - 1 - threadIdx.x - (int64_t)kTailBlock * j;
+          x[j] = idx >= ds ? __ldg(&a.nbr[idx]) : -1;
         }
+        bool b = false;
+        live = 0;
+#pragma unroll
+        for (int j = 0; j < kBU; ++j)
+          if (x[j] >= 0) {
+            bool al;
+            b |= tail_blocks(a, x[j], tprev, first, dq, dv, al);
+            live |= (uint32_t)al << j;
+          }
         blocked = __syncthreads_or(b) != 0;
       }
       if (!blocked) {
-        if (threadIdx.x == 0) tail_candidate(a, v, round, sel, ev);
-        for (int64_t base = s; base < e; base += 4 * kTailBlock) {
-          int32_t w[4];
+        if (threadIdx.x == 0) tail_candidate(a, dv, round, wcnt, wlen, sel, ev);
+        if (de - ds <= kBW) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int64_t idx = base + threadIdx.x + (int64_t)kTailBlock * j;
-            w[j] = idx < e ? __ldg(&a.nbr[idx]) : -1;
+          for (int j = 0; j < kBU; ++j)
+            if ((live >> j) & 1u) a.xt[x[j]] = (uint16_t)tcur;
+        } else {
+          for (int64_t top = de; top > ds; top -= kBW) {
+#pragma unroll
+            for (int j = 0; j < kBU; ++j) {
+              const int64_t idx = top - 1 - threadIdx.x - (int64_t)kTailBlock * j;
+              x[j] = idx >= ds ? __ldg(&a.nbr[idx]) : -1;
+            }
+#pragma unroll
+            for (int j = 0; j < kBU; ++j)
+              if (x[j] >= 0 && tail_alive(a, x[j], tprev, first)) a.xt[x[j]] = (uint16_t)tcur;
           }
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (w[j] >= 0 && tail_alive(a, w[j], dead)) push[w[j]] = 1;
         }
       } else if (threadIdx.x == 0) {
-        out[atomicAdd(out_cnt, 1)] = v;
+        s_keep[kd] = 1;
       }
     }
+    TAIL_MARK(11, 0);
 #ifdef TCMIS_TAIL_PROF
     if (first && threadIdx.x == 0) g_tail_blk[1][blockIdx.x] = gtimer();
 #endif
-    // round's counters -> the DevRound ring (round: sel, eval; round-1: rem, alive)
+    // 4. the round's counters: fire-and-forget atomics into the ring
+    // (round: sel, eval; round - 1: rem, alive)
     sel = __reduce_add_sync(0xffffffffu, (unsigned)sel);
     ev = __reduce_add_sync(0xffffffffu, (unsigned)ev);  // < 2^32 per warp
     rem = __reduce_add_sync(0xffffffffu, (unsigned)rem);
@@ -484,9 +611,8 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
       if (rem) atomicAdd(&s_acc[2], rem);
       if (alive) atomicAdd(&s_acc[3], alive);
     }
-    __syncthreads();
+    __syncthreads();  // s_keep, s_acc complete; the entry arrays are read no more
     if (threadIdx.x == 0) {
-      s_nlong = 0;
       if (s_acc[0]) atomicAdd(slot_field(a, round, 0), s_acc[0]);
       if (s_acc[1]) atomicAdd(slot_field(a, round, 3), s_acc[1]);
       if (!first) {
@@ -494,41 +620,63 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
         if (s_acc[3]) atomicAdd(slot_field(a, round - 1, 2), s_acc[3]);
       }
       s_acc[0] = s_acc[1] = s_acc[2] = s_acc[3] = 0;
+      s_nd = 0;
+      s_nlong = 0;
     }
-    TAIL_MARK(2, cnt);
-    grid_barrier(a.bar);
+    // 5. the block's survivors (round's non-candidates) stay with it
+    if (have && s_keep[k]) {
+      const int j = atomicAdd(&s_nl, 1);
+      s_v[j] = v;
+      s_s[j] = s;
+      s_e[j] = e;
+      s_q[j] = (uint16_t)qv;
+    }
+    __syncthreads();
+    nl = s_nl;
+    TAIL_MARK(2, nl);
+    done = grid_barrier_sum(a.bar, (unsigned)nl);
+    if (threadIdx.x == 0) s_nl = 0;
     TAIL_MARK(3, round);
-    // round - 1 is complete: publish it; stop when it left nobody alive
-    bool done = false;
-    if (!first) {
-      volatile DevRound *pr = &a.rounds[(round - 2) % ctrl->max_rounds];
-      const unsigned long long alive_prev = pr->alive;
-      done = alive_prev == 0;
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
-        volatile Ctrl *vc = ctrl;
-        const unsigned long long evp = pr->eval;
-        pr->eval = a.seg_mode == 1 ? evp : 0;
-        pr->skip = a.seg_mode == 1 ? (unsigned long long)a.total_tiles - evp : 0;
-        if (round - 1 > vc->max_rounds) vc->overflow = 1;
-        vc->alive = (int32_t)alive_prev;
-        vc->round = done ? round : round + 1;  // rounds run = round - 1 when done
-      }
-    }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      // ready the ring slot two rounds ahead and the list count read this round
-      volatile DevRound *z = &a.rounds[(round + 1) % ctrl->max_rounds];
-      z->sel = z->rem = z->alive = z->eval = z->skip = 0;
-      ctrl->tail_cnt[round % 3] = 0;
-      __threadfence();
+      const unsigned long long t = gtimer_ns();
+      DevRound *r = &a.rounds[(round - 1) % ctrl->max_rounds];
+      r->t[1] = r->t[2] = r->t[3] = t;
     }
-    if (done) break;
   }
-  if (a.compact) {
-    grid_barrier(a.bar);
-    TAIL_MARK(4, 0);
-    compact_mis(a);
-    TAIL_MARK(7, 0);
+  // every block has passed the last round's barrier: states and counts are
+  // final.  Pass `round - 1` was the last one run; it was a round of the
+  // reference iff it had an alive vertex, i.e. selected one (a pass of only
+  // removals closes round - 2).  Its non-candidates were 0, so the ring's
+  // zeroed rem / alive of that round are already right.  The last block
+  // publishes: it also packs the control block and the ring for the host
+  // (compact_mis), after its own writes.
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    a.tslot[0] = base + 2u + (uint32_t)(round - r0);  // one past every tag this solve used
+    a.tslot[1] = solve + 1u;
+    volatile Ctrl *vc = ctrl;
+    const int cap = vc->max_rounds;
+    int last = round - 1;  // last pass
+    if (last >= r0 && ((volatile DevRound *)&a.rounds[(last - 1) % cap])->sel == 0) --last;
+    unsigned long long before = (unsigned long long)vc->alive;  // alive at the start of r0
+    for (int r = r0; r <= last; ++r) {
+      volatile DevRound *pr = &a.rounds[(r - 1) % cap];
+      const unsigned long long evp = pr->eval;
+      pr->eval = a.seg_mode == 1 ? evp : 0;
+      pr->skip = a.seg_mode == 1 ? (unsigned long long)a.total_tiles - evp : 0;
+      // engine.cpp:138-160 invariant, as in round_end_tail (update.cuh)
+      if (before != pr->sel + pr->rem + pr->alive) vc->corrupt = 1;
+      before = pr->alive;
+    }
+    if (last >= r0) {
+      if (last > cap) vc->overflow = 1;
+      vc->alive = 0;
+      vc->round = last + 1;
+    }
+    __threadfence();
   }
+  TAIL_MARK(4, 0);
+  compact_mis(a, wcnt, wnext, s_stage);
+  TAIL_MARK(7, 0);
 }
 
 }  // namespace tcmis_b200

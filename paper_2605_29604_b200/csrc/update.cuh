@@ -125,16 +125,23 @@ __device__ __forceinline__ void round_end_tail(const UpdateArgs &a, unsigned lon
     __threadfence();
     volatile Ctrl *vc = ctrl;
     const int32_t alive = vc->wl_count[out_slot];
-    DevRound r;
-    r.sel = vc->sel;
-    r.rem = vc->rem;
-    r.alive = (unsigned long long)alive;
-    r.eval = a.seg_mode == 1 ? vc->eval : 0;
-    r.skip = a.seg_mode == 1 ? (unsigned long long)a.total_tiles - vc->eval : 0;
     // a ring: the host loop drains one slot per round; the graph loop flags
-    // the (pathological, > max_rounds) case and the host re-runs step-wise
-    a.rounds[(round - 1) % vc->max_rounds] = r;
+    // the (pathological, > max_rounds) case and the host re-runs step-wise.
+    // The Phase start stamps t[0..2] are already in the slot.
+    DevRound *r = &a.rounds[(round - 1) % vc->max_rounds];
+    const unsigned long long sel = vc->sel, rem_all = vc->rem;
+    r->sel = sel;
+    r->rem = rem_all;
+    r->alive = (unsigned long long)alive;
+    r->eval = a.seg_mode == 1 ? vc->eval : 0;
+    r->skip = a.seg_mode == 1 ? (unsigned long long)a.total_tiles - vc->eval : 0;
+    r->t[3] = gtimer_ns();
     if (round > vc->max_rounds) vc->overflow = 1;
+    // engine.cpp:138-160: every alive vertex leaves as selected or removed or
+    // stays alive; anything else is a corrupt candidate (logic_error).  On a
+    // rank of a partitioned solve the counts are the rank's own.
+    if (!a.pub.bits && (unsigned long long)vc->alive != sel + rem_all + (unsigned long long)alive)
+      vc->corrupt = 1;
     vc->alive = alive;
     vc->sel = 0;
     vc->rem = 0;
@@ -166,6 +173,8 @@ __global__ void __launch_bounds__(kBlock)
   __shared__ int s_base;
   Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
+  // push: Phase 2 is fused into the select kernels (its time is Phase 1's)
+  stamp_phase(a.rounds, ctrl, round, kEnd ? 1 : 2, 2);
   const int64_t cnt = round == 1 ? a.n : ctrl->wl_count[round & 1];
   constexpr int64_t kChunk = (int64_t)kBlock * kUpdItems;
   if (!kEnd && (int64_t)blockIdx.x * kChunk >= cnt) return;  // kEnd: every block ends the round
@@ -235,6 +244,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
   __shared__ int32_t s_und[kBlock / 32][64];
   Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
+  stamp_phase(a.rounds, ctrl, round, 1, 1);
   const int64_t cnt = round == 1 ? a.n1 : ctrl->wl_count[round & 1];
   if ((int64_t)blockIdx.x * kBlock >= cnt) return;
   const int32_t *wl = round == 1 ? a.nz : ((round & 1) ? a.wl1 : a.wl0);
@@ -371,6 +381,7 @@ __global__ void __launch_bounds__(kBlock)
   pdl_entry();
   Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
+  stamp_phase(a.rounds, ctrl, round, 2, 2);
   int32_t *out = (round & 1) ? a.wl0 : a.wl1;
   const int out_slot = (round + 1) & 1;
   const int lane = threadIdx.x & 31;

@@ -580,3 +580,39 @@ def test_upload_tiled_edge_cases(ctx):
     for bad in (0, 65):
         with pytest.raises(Exception):
             tc.DeviceGraph.upload(as_tc(g), ctx, tile_dim=bad)
+
+
+@pytest.mark.parametrize("host_loop", [False, True])
+def test_phase_timers_default_path(ctx, host_loop):
+    """The reference fills phase1/2/3_ms every round (engine.cpp:253-284):
+    the default path (one CUDA graph, or the host loop) stamps %globaltimer
+    per phase, so every round has a positive time and total_ms() > 0."""
+    dg = tc.DeviceGraph.rmat(16, 16, 1, ctx)
+    for heur in (tc.Heuristic.H2, tc.Heuristic.H1, tc.Heuristic.LubyPerm):
+        res = tc.run_mis(dg, tc.EngineConfig(heuristic=heur, host_loop=host_loop))
+        assert res.total_ms() > 0.0
+        for it in res.iterations:
+            assert it.phase1_ms > 0.0, (heur, it.iteration)
+            assert it.phase1_ms + it.phase2_ms + it.phase3_ms < 1000.0
+        # round 1 runs in the per-round kernels: pull exclusion on R-MAT has
+        # its own Phase 2 kernels and the update its own Phase 3
+        assert res.iterations[0].phase2_ms > 0.0 and res.iterations[0].phase3_ms > 0.0
+    dg.close()
+
+
+@pytest.mark.parametrize("host_loop", [False, True])
+@pytest.mark.parametrize("thr", ["1", "65536", "1000000000"])
+def test_device_corruption_flag(ctx, host_loop, thr, monkeypatch):
+    """engine.cpp:138-141,152-153: a corrupt candidate is a logic_error.  The
+    device checks every round's selected + removed + alive against the alive
+    count before it (round-end kernel and k_tail); TCMIS_F_DEBUG_CORRUPT starts
+    the solve from a control block one vertex off, which must be reported."""
+    monkeypatch.setenv("TCMIS_TAIL_THRESHOLD", thr)
+    dg = as_tc(O.gen("rmat", 12, 16, 1))
+    with pytest.raises(tc.LogicError):
+        tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, host_loop=host_loop,
+                                       flags=tc.F_DEBUG_CORRUPT))
+    # and the next solve on the same graph is clean
+    res = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, host_loop=host_loop))
+    exp = O.solve(O.gen("rmat", 12, 16, 1), "h2", 1, tile_dim=16)
+    assert np.array_equal(res.mis, exp.mis)

@@ -4,7 +4,8 @@ import paper_2605_29604_b200 as tc
 import bench
 L = tc.load()
 ctx = tc.Context(0)
-TAG = {1: "start", 2: "pass", 3: "barrier", 4: "compact0", 5: "count", 6: "countbar", 7: "compact1"}
+TAG = {1: "start", 2: "pass", 3: "barrier", 4: "compact0", 5: "count", 6: "countbar", 7: "compact1",
+       8: "fill", 9: "thr", 10: "grp", 11: "blk"}
 buf = (C.c_ulonglong * 256)()
 for cfg in sys.argv[1:]:
     dg = bench.make_device_graph(tc, cfg, ctx)
@@ -23,6 +24,6 @@ blk = (C.c_ulonglong * (3 * 1024))()
 L.tcmis_debug_tail_blk(blk)
 a = np.frombuffer(blk, dtype=np.uint64).reshape(3, 1024)[:, :148].astype(np.int64)
 t0 = a[0].min()
-print("short-pass end us: min %.1f med %.1f max %.1f" % ((a[0].min()-t0)/1e3, (np.median(a[0])-t0)/1e3, (a[0].max()-t0)/1e3))
-print("long-pass end us: min %.1f med %.1f max %.1f" % ((a[1].min()-t0)/1e3, (np.median(a[1])-t0)/1e3, (a[1].max()-t0)/1e3))
-print("nlong per block: min %d med %d max %d sum %d" % (a[2].min(), np.median(a[2]), a[2].max(), a[2].sum()))
+print("thread-phase end us: min %.1f med %.1f max %.1f" % ((a[0].min()-t0)/1e3, (np.median(a[0])-t0)/1e3, (a[0].max()-t0)/1e3))
+print("block-phase end us: min %.1f med %.1f max %.1f" % ((a[1].min()-t0)/1e3, (np.median(a[1])-t0)/1e3, (a[1].max()-t0)/1e3))
+print("deferred per block: min %d med %d max %d sum %d" % (a[2].min(), np.median(a[2]), a[2].max(), a[2].sum()))
