@@ -1382,7 +1382,7 @@ extern "C" __attribute__((visibility("default"))) int tcmis_debug_tail_prof(
 }
 extern "C" __attribute__((visibility("default"))) int tcmis_debug_tail_blk(
     unsigned long long *out) {
-  return (int)cudaMemcpyFromSymbol(out, tcmis_b200::g_tail_blk, sizeof(unsigned long long) * 3 * 1024);
+  return (int)cudaMemcpyFromSymbol(out, tcmis_b200::g_tail_blk, sizeof(unsigned long long) * 5 * 1024);
 }
 #endif
 

@@ -63,7 +63,7 @@ namespace tcmis_b200 {
 // into g_tail_prof (read back by tcmis_debug_tail_prof, solver.cu)
 __device__ unsigned long long g_tail_prof[256];
 __device__ int g_tail_prof_n;
-__device__ unsigned long long g_tail_blk[3][1024];  // first round: per block (t_thread, t_end, ndeferred)
+__device__ unsigned long long g_tail_blk[5][1024];  // first round, per block: t_thread, t_end, ndeferred, entries, t_start
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -85,18 +85,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 #ifndef TCMIS_TAIL_GROUP
-#define TCMIS_TAIL_GROUP 8
+#define TCMIS_TAIL_GROUP 16
 #endif
 constexpr int kGroup = TCMIS_TAIL_GROUP;  // lanes per deferred row
 #ifndef TCMIS_TAIL_UNROLL
-#define TCMIS_TAIL_UNROLL 16
+#define TCMIS_TAIL_UNROLL 8
 #endif
 constexpr int kTU = TCMIS_TAIL_UNROLL;  // independent loads per lane per group step
 constexpr int kTailBlock = 1024;        // one block per SM: 148 arrivals per barrier
 constexpr int kTailWarps = kTailBlock / 32;
 constexpr int kTailGroups = kTailBlock / kGroup;
 #ifndef TCMIS_TAIL_THR_SCAN
-#define TCMIS_TAIL_THR_SCAN 16
+#define TCMIS_TAIL_THR_SCAN 8
 #endif
 constexpr int kThrScan = TCMIS_TAIL_THR_SCAN;  // row entries a thread scans on its own
 #ifndef TCMIS_TAIL_LONG
@@ -131,7 +131,8 @@ struct TailArgs {
   Ctrl *ctrl;
   int32_t *wl0, *wl1;
   DevRound *rounds;
-  unsigned *bar;            // grid_barrier_sum: [0..1] arrivals | sum, [2] generation
+  unsigned *bar;            // grid_barrier_sum: [0..1] arrivals | sum, [2] generation;
+                            // [3] arrivals for the publishing block
   // the solve's final step, fused: ascending MIS ids (engine.cpp:293)
   int32_t n;
   int32_t *mis;
@@ -186,14 +187,17 @@ __device__ __forceinline__ WarpRange warp_range(int32_t n, int nwarps, int gw) {
   return r;
 }
 
-// A candidate of the tail: InMIS, its compaction range counted, and the tile
-// counter of seg_mode 1 (exactly one candidate of the round counts its block
-// column).  next[] is not written: it keeps marking the per-round kernels'
-// candidates, which the compaction's count pass reads while the tail runs.
-__device__ __forceinline__ void tail_candidate(const TailArgs &a, int32_t v, int round,
-                                               unsigned *wcnt, int32_t wlen,
-                                               unsigned long long &sel,
-                                               unsigned long long &ev) {
+// A candidate of the tail: InMIS, its compaction range counted, and for the
+// tile counter of seg_mode 1 its block column queued in the block's pending
+// list: the next pass decides (atomicMax on segmark) whether it is the
+// round's first candidate there and adds the column's tiles, off the
+// critical path (the atomic's round trip and the tile-count load used to
+// sit between a candidate and the block's next barrier).  next[] is not
+// written: it keeps marking the per-round kernels' candidates, which the
+// compaction's count pass reads while the tail runs.
+__device__ __forceinline__ void tail_candidate(const TailArgs &a, int32_t v, unsigned *wcnt,
+                                               int32_t wlen, unsigned long long &sel,
+                                               int32_t *pend, int *npend) {
   a.state[v] = TCMIS_IN_MIS;
   atomicAdd(&wcnt[v / wlen], 1u);
   ++sel;
@@ -201,8 +205,7 @@ __device__ __forceinline__ void tail_candidate(const TailArgs &a, int32_t v, int
   if (a.seg_mode == 2) {
     a.segflag[sb] = 1;
   } else if (a.seg_mode == 1) {
-    if (atomicMax(&a.segmark[sb], (unsigned)round) < (unsigned)round)
-      ev += (unsigned long long)a.rowtiles[sb];
+    pend[atomicAdd(npend, 1)] = sb;
   }
 }
 
@@ -267,6 +270,7 @@ __device__ void compact_mis(const TailArgs &a, unsigned *wcnt, unsigned *wnext, 
   if (lane == 0 && before) atomicAdd(&s_base, before);
   if (w == 0) {  // exclusive scan of the block's 32 warp counts
     static_assert(kTailWarps == 32, "one warp count per lane");
+    static_assert(kTailWarps * kCompactV >= kTailBlock * kThrScan, "staging holds the windows");
     const unsigned t = __ldcg(&wcnt[blockIdx.x * kTailWarps + lane]);
     unsigned sc = t;
 #pragma unroll
@@ -320,18 +324,6 @@ __device__ void compact_mis(const TailArgs &a, unsigned *wcnt, unsigned *wnext, 
     *a.mis_count = total;
     if (a.pack) a.pack->mis_count = total;
   }
-  if (a.pack && blockIdx.x == gridDim.x - 1) {  // k_pack's job, done here: one graph node less
-    // word copies through L2 (ld.global.cg): written by other blocks
-    const int32_t cap = __ldcg(&a.ctrl->max_rounds);
-    const int nr = (int)(sizeof(DevRound) / 4) * (cap < 64 ? cap : 64);
-    const uint32_t *rs = reinterpret_cast<const uint32_t *>(a.rounds);
-    uint32_t *rd = reinterpret_cast<uint32_t *>(a.pack->rounds);
-    for (int i = threadIdx.x; i < nr; i += kTailBlock) rd[i] = __ldcg(rs + i);
-    const uint32_t *cs = reinterpret_cast<const uint32_t *>(a.ctrl);
-    uint32_t *cd = reinterpret_cast<uint32_t *>(&a.pack->ctrl);
-    for (int i = threadIdx.x; i < (int)(sizeof(Ctrl) / 4); i += kTailBlock) cd[i] = __ldcg(cs + i);
-    __threadfence_system();
-  }
 }
 
 #ifndef TCMIS_TAIL_MINB
@@ -344,9 +336,16 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
   __shared__ int64_t s_s[kTailBlock], s_e[kTailBlock];
   __shared__ uint16_t s_q[kTailBlock];
   __shared__ uint8_t s_keep[kTailBlock];  // the entry's verdict: 1 = non-candidate
+  // a deferred entry's thread-phase windows: their alive neighbours (bit j of
+  // s_live[k] = s_stage[k * kThrScan + j]; the compaction's staging area is
+  // free until the rounds end), so the group neither re-gathers them nor
+  // rescans them to push
+  __shared__ uint32_t s_live[kTailBlock];
   __shared__ int16_t s_def[kTailBlock];   // entries left to the groups
   __shared__ int16_t s_long[kTailLongCap];  // ... and to the whole block
   __shared__ int s_nd, s_nlong, s_nl;
+  __shared__ int32_t s_pend[2][kTailBlock];  // candidates' block columns (seg_mode 1), by round parity
+  __shared__ int s_npend[2];
   __shared__ unsigned long long s_acc[4];
   Ctrl *ctrl = a.ctrl;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -359,6 +358,7 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
     s_nd = 0;
     s_nlong = 0;
     s_nl = 0;
+    s_npend[0] = s_npend[1] = 0;
   }
   const uint32_t base0 = __ldcg(&a.tslot[0]);
   const uint32_t solve = __ldcg(&a.tslot[1]);
@@ -369,13 +369,16 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
   const int r0 = *(volatile int *)&ctrl->round;
   const int64_t cnt0 = *(volatile int *)&ctrl->wl_count[r0 & 1];
   TAIL_MARK(1, cnt0);
-  // the block's slice of the starting list (<= kTailBlock entries: host cap)
-  int nl = (int)(cnt0 * (blockIdx.x + 1) / gridDim.x - cnt0 * blockIdx.x / gridDim.x);
+  // the block's share of the starting list (<= kTailBlock entries: host
+  // cap): entries b, b + G, b + 2G, ... -- interleaved, because the list's
+  // order is not random (its end holds the rows the round kernels' engines
+  // finished last, the longer ones; contiguous slices left the last blocks
+  // ~30 % more work at s22)
+  int nl = cnt0 > blockIdx.x ? (int)((cnt0 - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
   {
-    const int64_t lo = cnt0 * blockIdx.x / gridDim.x;
     const int32_t *in0 = (r0 & 1) ? a.wl1 : a.wl0;
     if (threadIdx.x < nl) {
-      const int32_t v = __ldcg(&in0[lo + threadIdx.x]);
+      const int32_t v = __ldcg(&in0[blockIdx.x + (int64_t)threadIdx.x * gridDim.x]);
       s_v[threadIdx.x] = v;
       s_s[threadIdx.x] = __ldg(&a.off[v]);
       s_e[threadIdx.x] = __ldg(&a.off[v + 1]);
@@ -415,13 +418,32 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
       break;
     }
     const bool first = round == r0;
+#ifdef TCMIS_TAIL_PROF
+    if (first && threadIdx.x == 0) g_tail_blk[4][blockIdx.x] = gtimer();
+#endif
     const uint32_t tprev = base + 1u + (uint32_t)(round - r0);  // tag(round - 1)
     const uint32_t tcur = tprev + 1u;                           // tag(round)
     if (blockIdx.x == 0 && threadIdx.x == 0)
       a.rounds[(round - 1) % ctrl->max_rounds].t[0] = gtimer_ns();
     unsigned long long sel = 0, ev = 0, rem = 0, alive = 0;
+    int32_t *pend = s_pend[round & 1];
+    int *npend = &s_npend[round & 1];
+    // the previous round's pending block columns: the atomic and the tile
+    // count are issued now and consumed at the end of this pass
+    const int kp = threadIdx.x;
+    const bool have_p = !first && kp < s_npend[(round - 1) & 1];
+    unsigned p_old = 0xffffffffu;
+    int32_t p_tiles = 0;
+    if (have_p) {
+      const int32_t sb = s_pend[(round - 1) & 1][kp];
+      p_old = atomicMax(&a.segmark[sb], (unsigned)(round - 1));
+      p_tiles = __ldg(&a.rowtiles[sb]);
+    }
     const int k = threadIdx.x;
     const bool have = k < nl;
+    // a handful of entries: one warp per entry, not the thread + group pair
+    // (two dependent scans where one suffices for a round of few vertices)
+    const bool small = nl <= kTailWarps;
     int32_t v = -1;
     int64_t s = 0, e = 0;
     uint32_t qv = 0;
@@ -431,6 +453,83 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
       s = s_s[k];
       e = s_e[k];
       qv = s_q[k];
+    }
+    if (small && w < nl) {
+      if (lane == 0) {
+        s_keep[w] = 0;
+        s_live[w] = 0;
+      }
+      const int32_t wv = s_v[w];
+      const int64_t ws = s_s[w], we = s_e[w];
+      const uint32_t wq = s_q[w];
+      const uint32_t tv = first ? 0u : __ldcg(&a.xt[wv]);
+      if (we - ws > kTailLong && !(!first && tv == (uint16_t)tprev)) {
+        if (lane == 0) {
+          ++alive;
+          const int kk = atomicAdd(&s_nlong, 1);  // < kTailWarps <= kTailLongCap
+          s_long[kk] = (int16_t)w;
+        }
+      } else {
+        int32_t u[kTU];
+#pragma unroll
+        for (int j = 0; j < kTU; ++j) {
+          const int64_t idx = we - 1 - lane - 32 * j;
+          u[j] = idx >= ws ? __ldg(&a.nbr[idx]) : -1;
+        }
+        if (!first && tv == (uint16_t)tprev) {  // excluded in round - 1
+          if (lane == 0) {
+            mark_removed(wv, a.state, a.q);
+            ++rem;
+          }
+        } else {
+          if (lane == 0) ++alive;
+          constexpr int64_t kWW = 32 * kTU;
+          bool blocked = false;
+          uint32_t live = 0;
+          for (int64_t top = we;;) {
+            bool b = false;
+            live = 0;
+#pragma unroll
+            for (int j = 0; j < kTU; ++j)
+              if (u[j] >= 0) {
+                bool al;
+                b |= tail_blocks(a, u[j], tprev, first, wq, wv, al);
+                live |= (uint32_t)al << j;
+              }
+            blocked = __any_sync(0xffffffffu, b);
+            top -= kWW;
+            if (blocked || top <= ws) break;
+#pragma unroll
+            for (int j = 0; j < kTU; ++j) {
+              const int64_t idx = top - 1 - lane - 32 * j;
+              u[j] = idx >= ws ? __ldg(&a.nbr[idx]) : -1;
+            }
+          }
+          if (!blocked) {
+            if (lane == 0) tail_candidate(a, wv, wcnt, wlen, sel, pend, npend);
+            if (we - ws <= kWW) {
+#pragma unroll
+              for (int j = 0; j < kTU; ++j)
+                if ((live >> j) & 1u) a.xt[u[j]] = (uint16_t)tcur;
+            } else {
+              for (int64_t top = we; top > ws; top -= kWW) {
+#pragma unroll
+                for (int j = 0; j < kTU; ++j) {
+                  const int64_t idx = top - 1 - lane - 32 * j;
+                  u[j] = idx >= ws ? __ldg(&a.nbr[idx]) : -1;
+                }
+#pragma unroll
+                for (int j = 0; j < kTU; ++j)
+                  if (u[j] >= 0 && tail_alive(a, u[j], tprev, first)) a.xt[u[j]] = (uint16_t)tcur;
+              }
+            }
+          } else if (lane == 0) {
+            s_keep[w] = 1;
+          }
+        }
+      }
+    }
+    if (have && !small) {
       // 1. the entry's tag and the last kThrScan row entries, loaded together
       const uint32_t tv = first ? 0u : __ldcg(&a.xt[v]);  // loaded with the row entries
       // the row's last kThrScan/4 aligned 16-byte windows (13-16 entries):
@@ -462,12 +561,18 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
         if (b) {
           keep = 1;
         } else if (hi <= s) {  // the whole row was in the windows
-          tail_candidate(a, v, round, wcnt, wlen, sel, ev);
+          tail_candidate(a, v, wcnt, wlen, sel, pend, npend);
 #pragma unroll
           for (int j = 0; j < kThrScan; ++j)
             if ((live >> j) & 1u) a.xt[u[j]] = (uint16_t)tcur;
         } else {
           s_def[atomicAdd(&s_nd, 1)] = (int16_t)k;
+          s_e[k] = hi;  // the group scans [s, hi): [hi, e) was examined here
+          s_live[k] = live;
+          int32_t *su = s_stage + k * kThrScan;
+#pragma unroll
+          for (int j = 0; j < kThrScan; ++j)
+            if ((live >> j) & 1u) su[j] = u[j];
         }
       }
       s_keep[k] = keep;
@@ -478,10 +583,11 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
     if (first && threadIdx.x == 0) {
       g_tail_blk[0][blockIdx.x] = gtimer();
       g_tail_blk[2][blockIdx.x] = (unsigned long long)s_nd;
+      g_tail_blk[3][blockIdx.x] = (unsigned long long)nl;
     }
 #endif
-    // 2. the deferred rows: kGroup lanes each (the whole row again, from the
-    // end, so a row of <= kW entries pushes from registers)
+    // 2. the deferred rows: kGroup lanes each, over the part of the row the
+    // thread did not examine (a part of <= kW entries pushes from registers)
     const int nd = s_nd;
     for (int d = grp; d < nd; d += kTailGroups) {
       const int kd = s_def[d];
@@ -520,7 +626,10 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
         blocked = __ballot_sync(gmask, b) != 0;
       }
       if (!blocked) {
-        if (gl == 0) tail_candidate(a, dv, round, wcnt, wlen, sel, ev);
+        if (gl == 0) tail_candidate(a, dv, wcnt, wlen, sel, pend, npend);
+        const uint32_t sl = s_live[kd];
+        for (int j = gl; j < kThrScan; j += kGroup)
+          if ((sl >> j) & 1u) a.xt[s_stage[kd * kThrScan + j]] = (uint16_t)tcur;
         if (de - ds <= kW) {
 #pragma unroll
           for (int j = 0; j < kTU; ++j)
@@ -574,7 +683,9 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
         blocked = __syncthreads_or(b) != 0;
       }
       if (!blocked) {
-        if (threadIdx.x == 0) tail_candidate(a, dv, round, wcnt, wlen, sel, ev);
+        if (threadIdx.x == 0) tail_candidate(a, dv, wcnt, wlen, sel, pend, npend);
+        if (threadIdx.x < kThrScan && ((s_live[kd] >> threadIdx.x) & 1u))
+          a.xt[s_stage[kd * kThrScan + threadIdx.x]] = (uint16_t)tcur;
         if (de - ds <= kBW) {
 #pragma unroll
           for (int j = 0; j < kBU; ++j)
@@ -599,8 +710,9 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
 #ifdef TCMIS_TAIL_PROF
     if (first && threadIdx.x == 0) g_tail_blk[1][blockIdx.x] = gtimer();
 #endif
+    if (have_p && p_old < (unsigned)(round - 1)) ev += (unsigned long long)p_tiles;
     // 4. the round's counters: fire-and-forget atomics into the ring
-    // (round: sel, eval; round - 1: rem, alive)
+    // (round: sel; round - 1: rem, alive and -- from the pending columns -- eval)
     sel = __reduce_add_sync(0xffffffffu, (unsigned)sel);
     ev = __reduce_add_sync(0xffffffffu, (unsigned)ev);  // < 2^32 per warp
     rem = __reduce_add_sync(0xffffffffu, (unsigned)rem);
@@ -614,14 +726,15 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
     __syncthreads();  // s_keep, s_acc complete; the entry arrays are read no more
     if (threadIdx.x == 0) {
       if (s_acc[0]) atomicAdd(slot_field(a, round, 0), s_acc[0]);
-      if (s_acc[1]) atomicAdd(slot_field(a, round, 3), s_acc[1]);
       if (!first) {
+        if (s_acc[1]) atomicAdd(slot_field(a, round - 1, 3), s_acc[1]);
         if (s_acc[2]) atomicAdd(slot_field(a, round - 1, 1), s_acc[2]);
         if (s_acc[3]) atomicAdd(slot_field(a, round - 1, 2), s_acc[3]);
       }
       s_acc[0] = s_acc[1] = s_acc[2] = s_acc[3] = 0;
       s_nd = 0;
       s_nlong = 0;
+      s_npend[(round + 1) & 1] = 0;  // the next round's list (round - 1's was read above)
     }
     // 5. the block's survivors (round's non-candidates) stay with it
     if (have && s_keep[k]) {
@@ -644,13 +757,37 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
     }
   }
   // every block has passed the last round's barrier: states and counts are
-  // final.  Pass `round - 1` was the last one run; it was a round of the
-  // reference iff it had an alive vertex, i.e. selected one (a pass of only
-  // removals closes round - 2).  Its non-candidates were 0, so the ring's
-  // zeroed rem / alive of that round are already right.  The last block
-  // publishes: it also packs the control block and the ring for the host
-  // (compact_mis), after its own writes.
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+  // final but for the last pass's pending block columns (seg_mode 1)
+  {
+    const int np = s_npend[(round - 1) & 1];
+    unsigned long long ev = 0;
+    if (threadIdx.x < np) {
+      const int32_t sb = s_pend[(round - 1) & 1][threadIdx.x];
+      if (atomicMax(&a.segmark[sb], (unsigned)(round - 1)) < (unsigned)(round - 1))
+        ev = (unsigned long long)__ldg(&a.rowtiles[sb]);
+    }
+    ev = __reduce_add_sync(0xffffffffu, (unsigned)ev);
+    if (lane == 0 && ev) atomicAdd(slot_field(a, round - 1, 3), ev);
+    __syncthreads();
+    if (threadIdx.x == 0) {  // arrival for the publishing block (below), nobody waits here
+      __threadfence();
+      atomicAdd(&a.bar[3], 1u);
+    }
+  }
+  TAIL_MARK(4, 0);
+  compact_mis(a, wcnt, wnext, s_stage);
+  TAIL_MARK(7, 0);
+  // The last block publishes the tail's rounds and packs the control block
+  // and the ring for the host, once every block's counters are in.  Pass
+  // `round - 1` was the last one run; it was a round of the reference iff it
+  // had an alive vertex, i.e. selected one (a pass of only removals closes
+  // round - 2).  Its non-candidates were 0, so the ring's zeroed rem / alive
+  // of that round are already right.
+  if (blockIdx.x != gridDim.x - 1) return;
+  if (threadIdx.x == 0) {
+    while (*(volatile unsigned *)&a.bar[3] < gridDim.x) __nanosleep(32);
+    a.bar[3] = 0;
+    __threadfence();
     a.tslot[0] = base + 2u + (uint32_t)(round - r0);  // one past every tag this solve used
     a.tslot[1] = solve + 1u;
     volatile Ctrl *vc = ctrl;
@@ -674,9 +811,19 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
     }
     __threadfence();
   }
-  TAIL_MARK(4, 0);
-  compact_mis(a, wcnt, wnext, s_stage);
-  TAIL_MARK(7, 0);
+  __syncthreads();
+  if (a.pack) {  // k_pack's job, done here: one graph node less
+    // word copies through L2 (ld.global.cg): written by other blocks
+    const int32_t cap = __ldcg(&a.ctrl->max_rounds);
+    const int nr = (int)(sizeof(DevRound) / 4) * (cap < 64 ? cap : 64);
+    const uint32_t *rs = reinterpret_cast<const uint32_t *>(a.rounds);
+    uint32_t *rd = reinterpret_cast<uint32_t *>(a.pack->rounds);
+    for (int i = threadIdx.x; i < nr; i += kTailBlock) rd[i] = __ldcg(rs + i);
+    const uint32_t *cs = reinterpret_cast<const uint32_t *>(a.ctrl);
+    uint32_t *cd = reinterpret_cast<uint32_t *>(&a.pack->ctrl);
+    for (int i = threadIdx.x; i < (int)(sizeof(Ctrl) / 4); i += kTailBlock) cd[i] = __ldcg(cs + i);
+    __threadfence_system();
+  }
 }
 
 }  // namespace tcmis_b200

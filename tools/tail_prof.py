@@ -20,10 +20,15 @@ for cfg in sys.argv[1:]:
     dg.close()
 # per-block view of the first tail round (last solve of the last config)
 import numpy as np
-blk = (C.c_ulonglong * (3 * 1024))()
+blk = (C.c_ulonglong * (5 * 1024))()
 L.tcmis_debug_tail_blk(blk)
-a = np.frombuffer(blk, dtype=np.uint64).reshape(3, 1024)[:, :148].astype(np.int64)
-t0 = a[0].min()
-print("thread-phase end us: min %.1f med %.1f max %.1f" % ((a[0].min()-t0)/1e3, (np.median(a[0])-t0)/1e3, (a[0].max()-t0)/1e3))
-print("block-phase end us: min %.1f med %.1f max %.1f" % ((a[1].min()-t0)/1e3, (np.median(a[1])-t0)/1e3, (a[1].max()-t0)/1e3))
+a = np.frombuffer(blk, dtype=np.uint64).reshape(5, 1024)[:, :148].astype(np.int64)
+t0 = a[4].min()
+for name, row in (("round start", a[4]), ("thread-phase end", a[0]), ("block-phase end", a[1])):
+    x = (row - t0) / 1e3
+    print(f"{name} us: min {x.min():.1f} med {np.median(x):.1f} max {x.max():.1f}")
 print("deferred per block: min %d med %d max %d sum %d" % (a[2].min(), np.median(a[2]), a[2].max(), a[2].sum()))
+print("entries per block: min %d med %d max %d sum %d" % (a[3].min(), np.median(a[3]), a[3].max(), a[3].sum()))
+order = np.argsort(-a[1])[:8]
+for b in order:
+    print(f"  slow block {b}: start {(a[4][b]-t0)/1e3:.1f} thr {(a[0][b]-t0)/1e3:.1f} end {(a[1][b]-t0)/1e3:.1f} entries {a[3][b]} deferred {a[2][b]}")
