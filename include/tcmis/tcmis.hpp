@@ -14,6 +14,7 @@
 // both this library and the reference without ODR clashes.
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <functional>
 #include <iosfwd>
@@ -256,11 +257,37 @@ MISResult run_luby_reference(const Graph &g, std::uint64_t seed, LubyMode mode,
 
 MISResult run_mis(const Graph &g, const EngineConfig &config);
 
+// ----------------------------------------------- multi-GPU
+// Not in the reference (a single-process CPU engine): the row-partitioned
+// solve over several B200s (csrc/partitioned.cu, tcmis_solve_partitioned).
+// For h1 / h2 / h3 / luby-perm the result (mis, iterations, every counter)
+// equals run_mis(g, cfg) at any world size; luby-fresh throws
+// std::invalid_argument.  Phase times are the calling rank's.
+
+/// Edge-balanced contiguous row ranges rank_lo[world + 1] (rank_lo[0] = 0,
+/// rank_lo[world] = n), inner boundaries at multiples of lcm(64, tile_dim).
+std::vector<VertexId> partition_rows(const Graph &g, int world, int tile_dim = 16);
+
+using NcclUniqueId = std::array<std::uint8_t, 128>;
+/// Rank 0 creates it; the caller broadcasts it to the other ranks (MPI, a
+/// file, torch.distributed, ...).
+NcclUniqueId nccl_unique_id();
+
+/// One process per GPU: this rank uploads its rows of g to `device` and
+/// solves with its world - 1 peers over NCCL.
+MISResult run_mis_partitioned(const Graph &g, const EngineConfig &config, int world, int rank,
+                              const NcclUniqueId &id, int device);
+
+/// One process: one rank per entry of `devices` (repeats allowed), each
+/// driven by its own host thread, exchanging through UVA / peer copies.
+MISResult run_mis_partitioned(const Graph &g, const EngineConfig &config,
+                              const std::vector<int> &devices);
+
 /// The result row of the reference's `cmd_run` (the absent
 /// CLI): graph, n, m, heuristic, seed, |MIS|, iterations, total ms, phase 1/2/3
 /// ms, tiles evaluated, tiles skipped -- comma-separated, no trailing newline.
-/// Phase times are the device times the result carries (0 for a graph-launched
-/// solve, which has no per-phase timers).
+/// Phase times are the device times the result carries (the round kernels'
+/// %globaltimer stamps on every solve path).
 std::string csv_header();
 std::string csv_row(const std::string &graph_name, const Graph &g, const MISResult &r);
 

@@ -237,6 +237,48 @@ int tcmis_dist_state(tcmis_graph *g, uint8_t *own_state);
  * iteration's tiles_evaluated and its tile total (sum over ranks on the host). */
 int tcmis_dist_h3_tiles(tcmis_graph *g, int64_t *tiles_evaluated, int64_t *tile_total);
 
+/* The native partitioned solve (csrc/partitioned.cu): the whole
+ * solve of one rank in one call, every round driven from C++ with the
+ * exchange below -- bitmap slices in the first rounds, id lists once the
+ * all-reduced alive count bounds a round's decisions below a slice -- and, for
+ * a capturable exchange (NCCL), each round one CUDA graph launch with the host
+ * one round ahead of the counters it reads.  The reference has no multi-GPU
+ * path; this partitions its run_tc_mis loop (engine.cpp:247-291) so that the
+ * MIS, the iteration count and every per-iteration statistic equal the
+ * single-GPU solve for any world size.  `part` holds this rank's rows
+ * (tcmis_graph_upload_partition / tcmis_graph_partition); rank_lo[world + 1]
+ * as for tcmis_dist_apply.  Outputs (each may be NULL but n_iterations):
+ * state_out[n] the final VertexState of ALL n vertices, mis_out[n] the
+ * ascending ids of the whole MIS (every rank holds the replicated state at
+ * the end), stats as tcmis_solve (counters summed over the ranks; phase
+ * times are this rank's).  Every rank must call it with the same arguments
+ * (collectives); a rank's error leaves its peers blocked in the exchange. */
+typedef struct tcmis_exchange tcmis_exchange;
+/* ncclGetUniqueId (128 bytes) for rank 0 to broadcast; NCCL (libnccl.so.2) is
+ * bound at run time -- the copy the process already loaded first, else the
+ * loader's (TCMIS_NCCL_LIB overrides) -- so the library has no link-time
+ * NCCL dependency. */
+int tcmis_nccl_unique_id(uint8_t id[128]);
+/* a communicator of its own (ncclCommInitRank on the context's device) */
+int tcmis_exchange_nccl(tcmis_ctx *ctx, int32_t world, int32_t rank, const uint8_t id[128],
+                        tcmis_exchange **out);
+/* an ncclComm_t the caller owns and keeps alive (created by the same libnccl) */
+int tcmis_exchange_nccl_comm(void *nccl_comm, tcmis_exchange **out);
+/* world ranks of ONE process, one host thread each (one context per rank, on
+ * any devices): all-gathers are copies through UVA / peer access.  out[world]. */
+int tcmis_exchange_local_group(int32_t world, tcmis_exchange **out);
+void tcmis_exchange_destroy(tcmis_exchange *x);
+/* in-process group: release the peers of a rank that failed before (or
+ * outside) tcmis_solve_partitioned from the exchange; a failing solve does
+ * this itself.  No-op for NCCL. */
+void tcmis_exchange_abort(tcmis_exchange *x);
+int32_t tcmis_exchange_world(const tcmis_exchange *x);
+int32_t tcmis_exchange_rank(const tcmis_exchange *x);
+int tcmis_solve_partitioned(tcmis_graph *part, tcmis_exchange *x, const int32_t *rank_lo,
+                            int32_t world, const tcmis_config *cfg, uint8_t *state_out,
+                            int32_t *mis_out, int64_t *mis_count, tcmis_iter_stats *stats,
+                            int32_t max_stats, int32_t *n_iterations);
+
 /* h1_random (priorities.cpp:33-41) without a graph: n priorities on the
  * device of the context, copied to p_out[n]. */
 int tcmis_h1_random(tcmis_ctx *ctx, int32_t n, uint64_t seed, uint32_t *p_out);

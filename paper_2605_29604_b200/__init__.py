@@ -150,6 +150,16 @@ def load():
         "tcmis_gen_gnp_host": (C.c_int, [i32, C.c_double, u64, P(P(i64)), P(P(i32)), P(i64)]),
         "tcmis_free": (None, [vp]),
         "tcmis_rgg_radius": (u64, [i32, C.c_double]),
+        "tcmis_nccl_unique_id": (C.c_int, [vp]),
+        "tcmis_exchange_nccl": (C.c_int, [vp, i32, i32, vp, P(vp)]),
+        "tcmis_exchange_nccl_comm": (C.c_int, [vp, P(vp)]),
+        "tcmis_exchange_local_group": (C.c_int, [i32, P(vp)]),
+        "tcmis_exchange_destroy": (None, [vp]),
+        "tcmis_exchange_abort": (None, [vp]),
+        "tcmis_exchange_world": (i32, [vp]),
+        "tcmis_exchange_rank": (i32, [vp]),
+        "tcmis_solve_partitioned": (C.c_int, [vp, vp, vp, i32, P(_Config), vp, vp, P(i64),
+                                              P(_Stats), i32, P(i32)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -283,6 +293,10 @@ class Context:
         _check(L.tcmis_ctx_create(int(device), C.byref(h)))
         self.h = h
         self.device = device
+        # shared with every graph of this context: a graph whose context is
+        # gone (e.g. both finalised by one garbage-collected cycle, in either
+        # order) must not call into the destroyed context
+        self._alive = [True]
 
     @property
     def stream(self) -> int:
@@ -296,6 +310,7 @@ class Context:
 
     def close(self) -> None:
         if getattr(self, "h", None):
+            self._alive[0] = False
             load().tcmis_ctx_destroy(self.h)
             self.h = None
 
@@ -322,6 +337,7 @@ class DeviceGraph:
     def __init__(self, handle, ctx: Context, keepalive=None):
         self.h = handle
         self.ctx = ctx
+        self._ctx_alive = ctx._alive
         self._keep = keepalive
 
     @classmethod
@@ -417,7 +433,8 @@ class DeviceGraph:
 
     def close(self) -> None:
         if getattr(self, "h", None):
-            load().tcmis_graph_destroy(self.h)
+            if self._ctx_alive[0]:  # else leaked: the context it frees through is gone
+                load().tcmis_graph_destroy(self.h)
             self.h = None
 
     def __del__(self):

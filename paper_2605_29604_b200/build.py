@@ -30,7 +30,7 @@ NVCC_FLAGS = ARCH + [
     "-I", INC, "-I", CSRC,
 ] + os.environ.get("TCMIS_NVCC_EXTRA", "").split()
 CU_SOURCES = ["capi.cu", "solver.cu", "tiles.cu", "gen.cu", "tiled_spmv.cu", "dist.cu",
-              "validate.cu"]
+              "partitioned.cu", "validate.cu"]
 CXX_SOURCES = ["engine.cpp"]
 
 
@@ -81,7 +81,7 @@ def build(verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=len(srcs)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
     if _stale(LIB, objs):
-        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-Xlinker", "-z,defs"]
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-ldl", "-Xlinker", "-z,defs"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

@@ -254,6 +254,7 @@ TCMIS_API void tcmis_graph_destroy(tcmis_graph *g) {
   dev_free(g->d_nz);
   dev_free(g->d_off_full);
   free_dist(g);
+  free_partitioned(g);
   free_tile_store(g);
   Workspace &sp = g->ctx->spare;
   if (g->ws.ctrl && g->ws.n_cap >= sp.n_cap) {

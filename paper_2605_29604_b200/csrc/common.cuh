@@ -131,15 +131,25 @@ __device__ __forceinline__ void mark_candidate(int32_t v, uint8_t *next, uint8_t
   if (segflag) segflag[seg_of(v, T)] = 1;
 }
 
-// Multi-GPU: a rank publishes its own range's decisions as a bitmap slice
-// (bit v - lo) that the host allgathers over NCCL (distributed.py).
+// Multi-GPU: a rank publishes its own range's decisions for the exchange
+// (partitioned.cu), either as a bitmap slice (bit v - lo) or, in the late
+// rounds, as an id list (list[0] = count, ids from list[1]; the host sizes
+// `cap` from an all-reduced alive count that bounds the round's decisions,
+// and a count beyond cap is reported as an overflow, never written past).
 struct Publish {
-  uint32_t *bits;  // null on a single GPU
+  uint32_t *bits;  // dense slice; null on a single GPU
   int32_t lo;
+  int32_t *list;   // sparse list (bits == null)
+  int32_t cap;
 };
 
 __device__ __forceinline__ void publish(const Publish &p, int32_t v) {
-  if (p.bits) atomicOr(&p.bits[(uint32_t)(v - p.lo) >> 5], 1u << ((uint32_t)(v - p.lo) & 31u));
+  if (p.bits) {
+    atomicOr(&p.bits[(uint32_t)(v - p.lo) >> 5], 1u << ((uint32_t)(v - p.lo) & 31u));
+  } else if (p.list) {
+    const int i = atomicAdd(p.list, 1);
+    if (i < p.cap) p.list[1 + i] = v;
+  }
 }
 
 // The gathered summary of the key order: q[v] = clamp(p[v] >> shift, 1,

@@ -4,6 +4,7 @@
 // context, runs the sm_100a kernels through tcmis_b200.h and maps the status
 // codes back onto the reference's exception types (SURVEY 8(b) "Errors").
 #include <algorithm>
+#include <numeric>
 #include <cmath>
 #include <memory>
 #include <mutex>
@@ -13,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
+#include <thread>
 
 #include "tcmis/tcmis.hpp"
 #include "tcmis_b200.h"
@@ -653,6 +655,162 @@ MISResult run_mis(const Graph &g, const EngineConfig &cfg) {  // engine.cpp:354-
     default:
       return run_tc_mis(g, cfg);
   }
+}
+
+// ---------------------------------------------------------- multi-GPU
+
+std::vector<VertexId> partition_rows(const Graph &g, int world, int tile_dim) {
+  if (world < 1) throw std::invalid_argument("world must be >= 1");
+  check_tile_dim(tile_dim);
+  const int64_t align = std::lcm<int64_t>(64, tile_dim);
+  const int64_t n = g.n;
+  const int64_t total = g.offsets.empty() ? 0 : g.offsets.back();
+  std::vector<VertexId> lo{0};
+  for (int r = 1; r < world; ++r) {
+    const int64_t target = total * r / world;
+    int64_t v = std::lower_bound(g.offsets.begin(), g.offsets.end(), target) - g.offsets.begin();
+    v = std::min(n / align * align, std::max<int64_t>(lo.back(), (v + align / 2) / align * align));
+    lo.push_back(static_cast<VertexId>(v));
+  }
+  lo.push_back(g.n);
+  return lo;
+}
+
+NcclUniqueId nccl_unique_id() {
+  NcclUniqueId id{};
+  check(tcmis_nccl_unique_id(id.data()));
+  return id;
+}
+
+namespace {
+
+struct OwnedCtx {
+  tcmis_ctx *h = nullptr;
+  explicit OwnedCtx(int device) { check(tcmis_ctx_create(device, &h)); }
+  ~OwnedCtx() { tcmis_ctx_destroy(h); }
+  OwnedCtx(const OwnedCtx &) = delete;
+  OwnedCtx &operator=(const OwnedCtx &) = delete;
+};
+
+struct OwnedGraph {
+  tcmis_graph *h = nullptr;
+  ~OwnedGraph() { tcmis_graph_destroy(h); }
+};
+
+struct OwnedExchange {
+  tcmis_exchange *h = nullptr;
+  ~OwnedExchange() { tcmis_exchange_destroy(h); }
+};
+
+void check_partitioned(const Graph &g, const EngineConfig &cfg) {
+  check_tile_dim(cfg.tile_dim);
+  if (cfg.heuristic == Heuristic::LubyFresh)
+    throw std::invalid_argument(
+        "luby-fresh redraws every alive key per round; the partitioned solve runs h1, h2, h3 "
+        "and luby-perm");
+  if (cfg.heuristic != Heuristic::H1 &&
+      (cfg.scale_bits < kMinScaleBits || cfg.scale_bits > kMaxScaleBits))
+    throw std::invalid_argument("scale_bits must be in [8, 30]");
+  (void)g;
+}
+
+// one rank: upload its rows, solve through the exchange, the whole result
+int solve_rank(const Graph &g, const EngineConfig &cfg, tcmis_ctx *ctx, tcmis_exchange *x,
+               const std::vector<VertexId> &lo, int rank, MISResult *out) {
+  OwnedGraph part;
+  const int64_t a = g.offsets[lo[rank]], b = g.offsets[lo[rank + 1]];
+  if (int rc = tcmis_graph_upload_partition(ctx, g.n, lo[rank], lo[rank + 1], g.offsets.data(),
+                                            b > a ? g.neighbors.data() + a : nullptr, &part.h))
+    return rc;
+  tcmis_config c;
+  tcmis_config_init(&c);
+  c.heuristic = static_cast<int32_t>(cfg.heuristic);
+  c.tile_dim = cfg.tile_dim;
+  c.seed = cfg.seed;
+  c.scale_bits = cfg.scale_bits;
+  std::vector<int32_t> mis(static_cast<std::size_t>(std::max<VertexId>(g.n, 1)));
+  std::vector<tcmis_iter_stats> st(static_cast<std::size_t>(std::max<VertexId>(g.n, 1)));
+  int64_t cnt = 0;
+  int32_t nit = 0;
+  if (int rc = tcmis_solve_partitioned(part.h, x, lo.data(), static_cast<int32_t>(lo.size() - 1),
+                                       &c, nullptr, mis.data(), &cnt, st.data(),
+                                       static_cast<int32_t>(st.size()), &nit))
+    return rc;
+  out->heuristic = cfg.heuristic;
+  out->seed = cfg.seed;
+  out->mis.assign(mis.begin(), mis.begin() + cnt);
+  for (int32_t i = 0; i < nit; ++i) {
+    IterationStats s;
+    s.iteration = st[i].iteration;
+    s.candidates_selected = st[i].candidates_selected;
+    s.vertices_removed = st[i].vertices_removed;
+    s.alive_remaining = st[i].alive_remaining;
+    s.tiles_evaluated = st[i].tiles_evaluated;
+    s.tiles_skipped = st[i].tiles_skipped;
+    s.phase1_ms = st[i].phase1_ms;
+    s.phase2_ms = st[i].phase2_ms;
+    s.phase3_ms = st[i].phase3_ms;
+    out->iterations.push_back(s);
+  }
+  return 0;
+}
+
+}  // namespace
+
+MISResult run_mis_partitioned(const Graph &g, const EngineConfig &cfg, int world, int rank,
+                              const NcclUniqueId &id, int device) {
+  check_partitioned(g, cfg);
+  if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("bad rank / world");
+  MISResult r;
+  r.heuristic = cfg.heuristic;
+  r.seed = cfg.seed;
+  const std::vector<VertexId> lo = partition_rows(g, world, cfg.tile_dim);
+  OwnedCtx ctx(device);
+  OwnedExchange x;
+  check(tcmis_exchange_nccl(ctx.h, world, rank, id.data(), &x.h));
+  if (g.n == 0) return r;
+  check(solve_rank(g, cfg, ctx.h, x.h, lo, rank, &r));
+  return r;
+}
+
+MISResult run_mis_partitioned(const Graph &g, const EngineConfig &cfg,
+                              const std::vector<int> &devices) {
+  check_partitioned(g, cfg);
+  const int world = static_cast<int>(devices.size());
+  if (world < 1) throw std::invalid_argument("no devices");
+  MISResult r;
+  r.heuristic = cfg.heuristic;
+  r.seed = cfg.seed;
+  if (g.n == 0) return r;
+  const std::vector<VertexId> lo = partition_rows(g, world, cfg.tile_dim);
+  std::vector<std::unique_ptr<OwnedCtx>> ctxs;
+  for (int d : devices) ctxs.push_back(std::make_unique<OwnedCtx>(d));
+  std::vector<tcmis_exchange *> xs(static_cast<std::size_t>(world), nullptr);
+  check(tcmis_exchange_local_group(world, xs.data()));
+  std::vector<MISResult> res(static_cast<std::size_t>(world));
+  std::vector<int> rcs(static_cast<std::size_t>(world), 0);
+  std::vector<std::string> errs(static_cast<std::size_t>(world));
+  std::vector<std::thread> th;
+  for (int k = 0; k < world; ++k)
+    th.emplace_back([&, k] {
+      rcs[k] = solve_rank(g, cfg, ctxs[k]->h, xs[k], lo, k, &res[k]);
+      if (rcs[k]) {
+        errs[k] = tcmis_last_error();  // thread-local
+        tcmis_exchange_abort(xs[k]);   // the peers must not wait for this rank
+      }
+    });
+  for (auto &t : th) t.join();
+  for (tcmis_exchange *x : xs) tcmis_exchange_destroy(x);
+  for (int k = 0; k < world; ++k)
+    if (rcs[k]) {
+      const std::string msg = errs[k];
+      switch (rcs[k]) {
+        case TCMIS_E_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case TCMIS_E_LOGIC: throw std::logic_error(msg);
+        default: throw std::runtime_error(msg);
+      }
+    }
+  return std::move(res[0]);
 }
 
 std::string csv_header() {

@@ -264,6 +264,9 @@ struct RoundArgs {
   uint32_t *pub_cand;   // multi-GPU publish slices (null on one GPU)
   uint32_t *pub_dead;
   int32_t pub_lo;
+  int32_t pub_cap;      // sparse publish lists (late rounds of a partitioned solve)
+  int32_t *pub_lcand;
+  int32_t *pub_ldead;
   int tail_grid;
   int tile;             // tile exclusion over the compact T = 16 store: 0 off, 1 bits, 2 mma
   int32_t nb16;         // block rows of the store
@@ -288,6 +291,8 @@ void free_workspace(Workspace &ws);
 
 // partitioned-solve state (dist.cu)
 void free_dist(tcmis_graph *g);
+// native partitioned-solve buffers and round graphs (partitioned.cu)
+void free_partitioned(tcmis_graph *g);
 
 // tiling (tiles.cu)
 int build_tile_counts(tcmis_graph *g, int T);

@@ -1,0 +1,768 @@
+// partitioned.cu -- the row-partitioned multi-GPU solve, driven natively.
+//
+// rank r owns the contiguous rows [lo_r, hi_r) (edge-balanced,
+// boundaries at multiples of 64 and of tile_dim; dist.cu holds the partial
+// CSR and the per-rank device side).  tcmis_solve_partitioned runs the whole
+// solve of one rank from C++: no Python in the round, one host thread per
+// rank.  One round (the reference's bulk-synchronous round,
+// engine.cpp:247-291) is
+//
+//   select own list            -> own candidates published (bitmap slice or id list)
+//   all_gather                 -> remote candidates marked (next = 1, InMIS)
+//   pull exclusion + update    -> own removals published
+//   all_gather                 -> remote removals applied (Removed, q = 0)
+//   all_reduce of the counters -> (sel, rem, alive, eval, skip, overflow) of the round
+//   k_ring                     -> the reduced counters into mapped host memory
+//
+// all stream-ordered on the context stream.  With a capturable exchange
+// (NCCL) a round is ONE CUDA graph launch; the host keeps one round in flight
+// ahead of the counters it reads (the termination test lags one round, the
+// stream never drains between rounds; the extra round after the last runs on
+// empty lists).  Every rank sees the same reduced counters, so every rank
+// takes the same decisions and enqueues the same collectives.
+//
+// Exchange format: the first rounds publish n/32-word bitmap slices.  Once the
+// all-reduced alive count of round k-1 (known when round k+1 is enqueued)
+// bounds round k+1's decisions below the dense slice size, the ranks publish
+// id lists of that capacity (a power of two) instead: R-MAT s26's late rounds
+// move a few KB per rank instead of 8.4 MB / world, and the apply kernels
+// touch only the listed vertices.
+//
+// Exchanges: NCCL (libnccl.so.2 bound at run time, the process's loaded copy
+// first, so a comm created by torch's NCCL can be passed in), or an in-process
+// group (one host thread per rank, copies through UVA / NVLink peer access;
+// also what the single-GPU test box uses to run 2-4 ranks on one device).
+#include <cub/cub.cuh>
+#include <dlfcn.h>
+#include <thrust/iterator/counting_iterator.h>
+#include <nccl.h>  // types only: the library is bound with dlopen
+
+#include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "internal.cuh"
+
+#define TCMIS_API extern "C" __attribute__((visibility("default")))
+
+namespace tcmis_b200 {
+
+int solve_prepare(tcmis_graph *g, const tcmis_config *cfg, RoundArgs &a, int64_t own_isolated);
+int seg_total(tcmis_graph *g, int64_t *ev);
+
+// ------------------------------------------------------------------ NCCL
+
+namespace {
+
+struct NcclApi {
+  void *h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommCount)(const ncclComm_t, int *) = nullptr;
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int *) = nullptr;
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t,
+                            ncclComm_t, cudaStream_t) = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  std::string error;
+};
+
+NcclApi &nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char *names[] = {std::getenv("TCMIS_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+    for (const char *nm : names)  // a copy the process already loaded (torch's) first
+      if (nm && !api.h) api.h = dlopen(nm, RTLD_NOW | RTLD_NOLOAD);
+    for (const char *nm : names)
+      if (nm && !api.h) api.h = dlopen(nm, RTLD_NOW | RTLD_LOCAL);
+    if (!api.h) {
+      api.error = "libnccl.so.2 not found (set TCMIS_NCCL_LIB)";
+      return;
+    }
+#define TCMIS_NCCL_SYM(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(api.h, "nccl" #f))
+    TCMIS_NCCL_SYM(GetUniqueId);
+    TCMIS_NCCL_SYM(CommInitRank);
+    TCMIS_NCCL_SYM(CommDestroy);
+    TCMIS_NCCL_SYM(CommCount);
+    TCMIS_NCCL_SYM(CommUserRank);
+    TCMIS_NCCL_SYM(AllGather);
+    TCMIS_NCCL_SYM(AllReduce);
+    TCMIS_NCCL_SYM(GetErrorString);
+#undef TCMIS_NCCL_SYM
+    if (!api.GetUniqueId || !api.CommInitRank || !api.CommDestroy || !api.AllGather ||
+        !api.AllReduce || !api.CommCount || !api.CommUserRank)
+      api.error = "libnccl.so.2 lacks a required symbol";
+  });
+  return api;
+}
+
+int nccl_error(ncclResult_t r, const char *what) {
+  NcclApi &A = nccl();
+  return set_error(TCMIS_E_RUNTIME, std::string("NCCL error in ") + what + ": " +
+                                        (A.GetErrorString ? A.GetErrorString(r) : "?"));
+}
+
+// an in-process group: world ranks, one host thread each
+struct LocalGroup {
+  int world = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t generation = 0;
+  std::vector<const void *> send;
+  std::vector<cudaEvent_t> ready, done;
+  std::vector<int> device;
+  bool aborted = false;  // a rank failed: its peers leave the barrier with an error
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (aborted) return false;
+    const uint64_t g = generation;
+    if (++arrived == world) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != g || aborted; });
+    }
+    return !aborted;
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    aborted = true;
+    cv.notify_all();
+  }
+};
+
+}  // namespace
+
+}  // namespace tcmis_b200
+
+// The exchange a partitioned solve talks through (one handle per rank).
+struct tcmis_exchange {
+  int kind = 0;  // 1 NCCL, 2 in-process group
+  int32_t world = 1, rank = 0;
+  bool capturable = false;
+  // NCCL
+  ncclComm_t comm = nullptr;
+  bool owns_comm = false;
+  // in-process group
+  std::shared_ptr<tcmis_b200::LocalGroup> group;
+  int64_t *scratch = nullptr;  // all-reduce staging, world x 8 (device of the rank)
+  int scratch_dev = -1;
+};
+
+namespace tcmis_b200 {
+namespace {
+
+__global__ void k_sum_i64(const int64_t *__restrict__ parts, int32_t world, int32_t count,
+                          int64_t *__restrict__ out) {
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    int64_t s = 0;
+    for (int r = 0; r < world; ++r) s += parts[(size_t)r * count + i];
+    out[i] = s;
+  }
+}
+
+int x_all_gather(tcmis_exchange *x, const void *send, void *recv, size_t bytes, cudaStream_t st) {
+  if (x->kind == 1) {
+    ncclResult_t r = nccl().AllGather(send, recv, bytes, ncclUint8, x->comm, st);
+    return r == ncclSuccess ? 0 : nccl_error(r, "ncclAllGather");
+  }
+  LocalGroup &G = *x->group;
+  const int me = x->rank;
+  G.send[me] = send;
+  TCMIS_CUDA(cudaEventRecord(G.ready[me], st));
+  if (!G.barrier()) return set_error(TCMIS_E_RUNTIME, "a peer rank of the in-process group failed");
+  for (int q = 0; q < G.world; ++q) {
+    TCMIS_CUDA(cudaStreamWaitEvent(st, G.ready[q], 0));
+    TCMIS_CUDA(cudaMemcpyAsync(static_cast<char *>(recv) + (size_t)q * bytes, G.send[q], bytes,
+                               cudaMemcpyDefault, st));
+  }
+  TCMIS_CUDA(cudaEventRecord(G.done[me], st));
+  // every rank enqueued its copies: the send buffers may be reused after done[]
+  if (!G.barrier()) return set_error(TCMIS_E_RUNTIME, "a peer rank of the in-process group failed");
+  for (int q = 0; q < G.world; ++q) TCMIS_CUDA(cudaStreamWaitEvent(st, G.done[q], 0));
+  return 0;
+}
+
+int x_all_reduce(tcmis_exchange *x, int64_t *buf, int32_t count, cudaStream_t st) {
+  if (x->kind == 1) {
+    ncclResult_t r = nccl().AllReduce(buf, buf, (size_t)count, ncclInt64, ncclSum, x->comm, st);
+    return r == ncclSuccess ? 0 : nccl_error(r, "ncclAllReduce");
+  }
+  if (count > 8) return set_error(TCMIS_E_LOGIC, "in-process all-reduce holds at most 8 values");
+  int dev = 0;
+  TCMIS_CUDA(cudaGetDevice(&dev));
+  if (!x->scratch || x->scratch_dev != dev) {
+    if (x->scratch) cudaFree(x->scratch);
+    x->scratch = nullptr;
+    TCMIS_CUDA(cudaMalloc(&x->scratch, sizeof(int64_t) * 8 * (x->world + 1)));
+    x->scratch_dev = dev;
+  }
+  int64_t *mine = x->scratch + 8 * x->world;  // the send copy: `buf` is overwritten by the sum
+  TCMIS_CUDA(cudaMemcpyAsync(mine, buf, sizeof(int64_t) * count, cudaMemcpyDeviceToDevice, st));
+  if (int rc = x_all_gather(x, mine, x->scratch, sizeof(int64_t) * count, st)) return rc;
+  k_sum_i64<<<1, 32, 0, st>>>(x->scratch, x->world, count, buf);
+  TCMIS_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// ------------------------------------------------------------- kernels
+
+// remote decisions from gathered id lists: rank r's list sits at r * stride
+// (count, then ids)
+__global__ void k_apply_list(const int32_t *__restrict__ gathered, int32_t world, int32_t stride,
+                             int32_t me, int what, uint8_t *__restrict__ next,
+                             uint8_t *__restrict__ state, uint16_t *__restrict__ q) {
+  const int64_t total = (int64_t)world * (stride - 1);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = (int32_t)(i / (stride - 1));
+    const int32_t k = (int32_t)(i - (int64_t)r * (stride - 1));
+    if (r == me) continue;
+    const int32_t *lst = gathered + (int64_t)r * stride;
+    if (k >= min(__ldg(lst), stride - 1)) continue;
+    const int32_t v = __ldg(lst + 1 + k);
+    if (what == 0) {
+      next[v] = 1;
+      state[v] = TCMIS_IN_MIS;
+    } else {
+      state[v] = TCMIS_REMOVED;
+      q[v] = 0;
+    }
+  }
+}
+
+// remote decisions from gathered bitmap slices (rank r's slice at word r *
+// maxw, bit v - lo_r): zero words cost one coalesced load
+__global__ void k_apply_words(const uint32_t *__restrict__ gathered,
+                              const int32_t *__restrict__ rank_lo, int32_t world, int32_t maxw,
+                              int32_t me, int what, uint8_t *__restrict__ next,
+                              uint8_t *__restrict__ state, uint16_t *__restrict__ q) {
+  const int64_t total = (int64_t)world * maxw;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t bits = __ldg(&gathered[w]);
+    if (!bits) continue;
+    const int32_t r = (int32_t)(w / maxw);
+    if (r == me) continue;
+    const int64_t first = rank_lo[r] + (w - (int64_t)r * maxw) * 32;
+    const int64_t end = rank_lo[r + 1];
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int64_t v = first + b;
+      if (v >= end) break;
+      if (what == 0) {
+        next[v] = 1;
+        state[v] = TCMIS_IN_MIS;
+      } else {
+        state[v] = TCMIS_REMOVED;
+        q[v] = 0;
+      }
+    }
+  }
+}
+
+// the finished round's own counters (DevRound, first 5 x u64) + the sparse
+// overflow flag into the all-reduce buffer
+__global__ void k_stage_counts(const Ctrl *__restrict__ ctrl, const DevRound *__restrict__ rounds,
+                               const int32_t *lcand, const int32_t *ldead, int32_t cap,
+                               int64_t *__restrict__ buf) {
+  if (threadIdx.x != 0) return;
+  const int r = ctrl->round - 1;  // round_end_tail advanced ctrl->round
+  const DevRound &d = rounds[(r - 1) % ctrl->max_rounds];
+  buf[0] = (int64_t)d.sel;
+  buf[1] = (int64_t)d.rem;
+  buf[2] = (int64_t)d.alive;
+  buf[3] = (int64_t)d.eval;
+  buf[4] = (int64_t)d.skip;
+  buf[5] = (lcand && *lcand > cap ? 1 : 0) + (ldead && *ldead > cap ? 1 : 0);
+}
+
+struct InMIS {
+  const uint8_t *s;
+  __device__ __forceinline__ bool operator()(int32_t v) const { return s[v] == TCMIS_IN_MIS; }
+};
+
+struct RingEntry {
+  int64_t round;
+  int64_t v[6];
+};
+constexpr int kRing = 8;
+
+__global__ void k_ring(const int64_t *__restrict__ buf, const Ctrl *__restrict__ ctrl,
+                       RingEntry *ring) {
+  if (threadIdx.x != 0) return;
+  const int r = ctrl->round - 1;
+  RingEntry *e = &ring[r % kRing];
+  for (int i = 0; i < 6; ++i) e->v[i] = buf[i];
+  __threadfence_system();
+  *(volatile int64_t *)&e->round = r;
+  __threadfence_system();
+}
+
+// per-rank buffers of a partitioned solve, kept on the graph's DistState
+struct PartBufs {
+  int32_t maxw = 0, world = 0;
+  uint32_t *mine = nullptr, *gathered = nullptr;  // dense slices
+  int32_t cap = 0;                                  // sparse capacity the lists hold
+  int32_t *lcand = nullptr, *ldead = nullptr, *lgathered = nullptr;
+  int64_t *counts = nullptr;  // all-reduce buffer (8)
+  int32_t *d_rank_lo = nullptr;
+  RingEntry *h_ring = nullptr, *d_ring = nullptr;
+  std::map<int32_t, cudaGraphExec_t> graphs;  // per publish capacity (0 = dense)
+  std::vector<unsigned char> key;             // what the graphs were captured for
+};
+
+void free_bufs(PartBufs &b) {
+  dev_free(b.mine);
+  dev_free(b.gathered);
+  dev_free(b.lcand);
+  dev_free(b.ldead);
+  dev_free(b.lgathered);
+  dev_free(b.counts);
+  dev_free(b.d_rank_lo);
+  if (b.h_ring) cudaFreeHost(b.h_ring);
+  for (auto &kv : b.graphs) cudaGraphExecDestroy(kv.second);
+  b = PartBufs{};
+}
+
+std::map<const tcmis_graph *, PartBufs> &bufs_of() {
+  static auto *m = new std::map<const tcmis_graph *, PartBufs>();
+  return *m;
+}
+std::mutex &bufs_mu() {
+  static std::mutex mu;
+  return mu;
+}
+
+}  // namespace
+
+void free_partitioned(tcmis_graph *g) {
+  std::lock_guard<std::mutex> lk(bufs_mu());
+  auto it = bufs_of().find(g);
+  if (it == bufs_of().end()) return;
+  free_bufs(it->second);
+  bufs_of().erase(it);
+}
+
+namespace {
+
+// Enqueue one round on the context stream.  cap == 0: bitmap slices.
+int enqueue_round(tcmis_graph *g, tcmis_exchange *x, RoundArgs &a, PartBufs &b, int32_t cap) {
+  tcmis_ctx *ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  Workspace &ws = g->ws;
+  const int world = x->world, me = x->rank;
+  const int agrid = grid_for(ctx, cap ? (int64_t)world * cap : (int64_t)world * b.maxw, 256, 4);
+  a.pub_cap = cap;
+  // 1. select + candidate exchange
+  if (cap) {
+    TCMIS_CUDA(cudaMemsetAsync(b.lcand, 0, sizeof(int32_t), st));
+    a.pub_cand = nullptr;
+    a.pub_lcand = b.lcand;
+  } else {
+    TCMIS_CUDA(cudaMemsetAsync(b.mine, 0, 4ull * b.maxw, st));
+    a.pub_cand = b.mine;
+    a.pub_lcand = nullptr;
+  }
+  a.pub_dead = nullptr;
+  a.pub_ldead = nullptr;
+  if (int rc = launch_select(g, a)) return rc;
+  if (cap) {
+    if (int rc = x_all_gather(x, b.lcand, b.lgathered, 4ull * (cap + 1), st)) return rc;
+    k_apply_list<<<agrid, 256, 0, st>>>(b.lgathered, world, cap + 1, me, 0, ws.next, ws.state,
+                                         ws.q);
+  } else {
+    if (int rc = x_all_gather(x, b.mine, b.gathered, 4ull * b.maxw, st)) return rc;
+    k_apply_words<<<agrid, 256, 0, st>>>(b.gathered, b.d_rank_lo, world, b.maxw, me, 0, ws.next,
+                                          ws.state, ws.q);
+  }
+  TCMIS_LAUNCHED(ctx);
+  // 2. exclusion + update + removal exchange
+  a.pub_lcand = nullptr;
+  a.pub_cand = nullptr;
+  if (cap) {
+    TCMIS_CUDA(cudaMemsetAsync(b.ldead, 0, sizeof(int32_t), st));
+    a.pub_ldead = b.ldead;
+  } else {
+    TCMIS_CUDA(cudaMemsetAsync(b.mine, 0, 4ull * b.maxw, st));
+    a.pub_dead = b.mine;
+  }
+  if (int rc = launch_update(g, a, 0, 0)) return rc;
+  if (cap) {
+    if (int rc = x_all_gather(x, b.ldead, b.lgathered, 4ull * (cap + 1), st)) return rc;
+    k_apply_list<<<agrid, 256, 0, st>>>(b.lgathered, world, cap + 1, me, 1, ws.next, ws.state,
+                                         ws.q);
+  } else {
+    if (int rc = x_all_gather(x, b.mine, b.gathered, 4ull * b.maxw, st)) return rc;
+    k_apply_words<<<agrid, 256, 0, st>>>(b.gathered, b.d_rank_lo, world, b.maxw, me, 1, ws.next,
+                                          ws.state, ws.q);
+  }
+  TCMIS_LAUNCHED(ctx);
+  // 3. the round's counters: all-reduced, then into the host ring
+  k_stage_counts<<<1, 32, 0, st>>>(ws.ctrl, ws.rounds, cap ? b.lcand : nullptr,
+                                   cap ? b.ldead : nullptr, cap, b.counts);
+  TCMIS_LAUNCHED(ctx);
+  if (int rc = x_all_reduce(x, b.counts, 6, st)) return rc;
+  k_ring<<<1, 32, 0, st>>>(b.counts, ws.ctrl, b.d_ring);
+  TCMIS_LAUNCHED(ctx);
+  return 0;
+}
+
+constexpr int kKernelsPerRoundExtra = 4;  // apply x2, stage, ring
+
+int launch_round(tcmis_graph *g, tcmis_exchange *x, RoundArgs &a, PartBufs &b, int32_t cap) {
+  tcmis_ctx *ctx = g->ctx;
+  if (!x->capturable) return enqueue_round(g, x, a, b, cap);
+  auto it = b.graphs.find(cap);
+  if (it == b.graphs.end()) {
+    const int64_t launches0 = ctx->launches;
+    cudaGraph_t graph = nullptr;
+    TCMIS_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+    int rc = enqueue_round(g, x, a, b, cap);
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+    ctx->launches = launches0;
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (e != cudaSuccess) return cuda_error(e, "partitioned round capture");
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_error(e, "partitioned round instantiate");
+    it = b.graphs.emplace(cap, exec).first;
+  }
+  TCMIS_CUDA(cudaGraphLaunch(it->second, ctx->stream));
+  ctx->launches += (a.pull ? 6 : 4) + kKernelsPerRoundExtra;
+  return 0;
+}
+
+int32_t pow2_at_least(int64_t x) {
+  int64_t c = 256;
+  while (c < x) c <<= 1;
+  return (int32_t)std::min<int64_t>(c, INT32_MAX / 2);
+}
+
+}  // namespace
+
+int solve_partitioned_impl(tcmis_graph *g, tcmis_exchange *x, const int32_t *rank_lo,
+                           int32_t world, const tcmis_config *cfg, uint8_t *state_out,
+                           int32_t *mis_out, int64_t *mis_count, tcmis_iter_stats *stats,
+                           int32_t max_stats, int32_t *n_iter) {
+  if (g->part_hi < 0) return set_error(TCMIS_E_INVALID_ARGUMENT, "graph is not a row partition");
+  if (world != x->world) return set_error(TCMIS_E_INVALID_ARGUMENT, "world differs from the exchange's");
+  const int32_t n = g->n, me = x->rank;
+  if (rank_lo[0] != 0 || rank_lo[world] != n)
+    return set_error(TCMIS_E_INVALID_ARGUMENT, "rank_lo must start at 0 and end at n");
+  const int T = cfg->tile_dim;
+  for (int r = 0; r < world; ++r) {
+    if (rank_lo[r + 1] < rank_lo[r])
+      return set_error(TCMIS_E_INVALID_ARGUMENT, "rank_lo must be non-decreasing");
+    if (rank_lo[r] != n && ((rank_lo[r] % 64) || (T > 0 && rank_lo[r] % T)))
+      return set_error(TCMIS_E_INVALID_ARGUMENT,
+                       "partition boundaries must be multiples of 64 and of tile_dim");
+  }
+  if (rank_lo[me] != g->part_lo || rank_lo[me + 1] != g->part_hi)
+    return set_error(TCMIS_E_INVALID_ARGUMENT, "rank_lo disagrees with this rank's rows");
+  if (cfg->heuristic == TCMIS_LUBY_FRESH)
+    return set_error(TCMIS_E_INVALID_ARGUMENT,
+                     "luby-fresh redraws every alive key per round; the partitioned solve runs "
+                     "the fixed-priority heuristics (h1, h2, h3, luby-perm)");
+  *n_iter = 0;
+  if (mis_count) *mis_count = 0;
+  if (n == 0) return 0;
+  tcmis_ctx *ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  if (int rc = ensure_workspace(g)) return rc;
+  RoundArgs a;
+  const int64_t own = (int64_t)g->part_hi - g->part_lo;
+  if (int rc = solve_prepare(g, cfg, a, own - g->nz_count)) return rc;
+  a.pull = 1;  // a push would have to reach remote rows
+  a.tail_thr = 0;
+  a.pub_lo = g->part_lo;
+  Workspace &ws = g->ws;
+
+  std::unique_lock<std::mutex> lk(bufs_mu());
+  PartBufs &b = bufs_of()[g];
+  lk.unlock();
+  int32_t maxw = 1;
+  for (int r = 0; r < world; ++r) maxw = std::max(maxw, (rank_lo[r + 1] - rank_lo[r] + 31) / 32);
+  // buffers and graphs are per (layout, round arguments, exchange)
+  std::vector<unsigned char> key(sizeof(RoundArgs) + sizeof(void *) + 4 * (world + 1));
+  std::memcpy(key.data(), &a, sizeof(a));
+  std::memcpy(key.data() + sizeof(a), &x, sizeof(void *));
+  std::memcpy(key.data() + sizeof(a) + sizeof(void *), rank_lo, 4 * (world + 1));
+  if (b.key != key) {
+    free_bufs(b);
+    b.key = key;
+    b.maxw = maxw;
+    b.world = world;
+    if (int rc = dev_alloc(&b.mine, (size_t)maxw)) return rc;
+    if (int rc = dev_alloc(&b.gathered, (size_t)maxw * world)) return rc;
+    if (int rc = dev_alloc(&b.counts, 8)) return rc;
+    if (int rc = dev_alloc(&b.d_rank_lo, (size_t)world + 1)) return rc;
+    TCMIS_CUDA(cudaMemcpyAsync(b.d_rank_lo, rank_lo, 4ull * (world + 1), cudaMemcpyHostToDevice,
+                               st));
+    TCMIS_CUDA(cudaHostAlloc((void **)&b.h_ring, sizeof(RingEntry) * kRing, cudaHostAllocMapped));
+    TCMIS_CUDA(cudaHostGetDevicePointer((void **)&b.d_ring, b.h_ring, 0));
+    // the largest list capacity that is still smaller than a dense slice
+    int32_t cap = maxw > 512 ? pow2_at_least(maxw / 2) : 0;
+    if (const char *env = std::getenv("TCMIS_PART_CAP")) cap = std::atoi(env);  // test hook
+    if (cap > 0 && (cap < maxw - 1 || std::getenv("TCMIS_PART_CAP"))) {
+      b.cap = cap;
+      if (int rc = dev_alloc(&b.lcand, (size_t)cap + 1)) return rc;
+      if (int rc = dev_alloc(&b.ldead, (size_t)cap + 1)) return rc;
+      if (int rc = dev_alloc(&b.lgathered, (size_t)(cap + 1) * world)) return rc;
+    }
+  }
+  for (int i = 0; i < kRing; ++i) b.h_ring[i].round = -1;
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+
+  const int32_t cap_rounds = n;  // engine.cpp:248-249
+  std::vector<RingEntry> got;
+  int64_t alive_prev[2] = {n, n};  // reduced alive after rounds k-1, k-2 (n before round 1)
+  auto choose = [&](int64_t bound) -> int32_t {
+    if (!b.cap || bound > b.cap) return 0;
+    return std::min(b.cap, pow2_at_least(bound));
+  };
+  auto wait_ring = [&](int r, RingEntry &out) -> int {
+    volatile RingEntry *e = &b.h_ring[r % kRing];
+    for (int spin = 0;; ++spin) {
+      if (e->round == r) break;
+      if ((spin & 1023) == 1023) {
+        cudaError_t q = cudaStreamQuery(st);
+        if (q != cudaSuccess && q != cudaErrorNotReady) return cuda_error(q, "partitioned round");
+        if (e->round == r) break;
+        std::this_thread::yield();
+      }
+    }
+    out.round = r;
+    for (int i = 0; i < 6; ++i) out.v[i] = e->v[i];
+    return 0;
+  };
+  // round k+1 is enqueued before round k's counters are read; its decisions
+  // are bounded by the alive count after round k-1
+  if (int rc = launch_round(g, x, a, b, 0)) return rc;
+  bool done = false;
+  int32_t rounds_run = 0;
+  for (int32_t it = 1; !done; ++it) {
+    if (it > cap_rounds)
+      return set_error(TCMIS_E_RUNTIME, "iteration cap exceeded; engine livelock");
+    if (it < cap_rounds)
+      if (int rc = launch_round(g, x, a, b, choose(alive_prev[0]))) return rc;
+    RingEntry e;
+    if (int rc = wait_ring(it, e)) return rc;
+    if (e.v[5]) return set_error(TCMIS_E_LOGIC, "exchange list overflow (a round decided more "
+                                                 "vertices than the alive bound)");
+    got.push_back(e);
+    alive_prev[1] = alive_prev[0];
+    alive_prev[0] = e.v[2];
+    rounds_run = it;
+    done = e.v[2] == 0;
+  }
+  TCMIS_CUDA(cudaStreamSynchronize(st));  // the extra (empty) round too
+
+  // every rank now holds the final state of all n vertices (own decisions +
+  // the applied remote ones): the ascending MIS from one compaction
+  thrust::counting_iterator<int32_t> ids(0);
+  size_t bytes = ws.cub_bytes;
+  TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count, (int)n,
+                                   InMIS{ws.state}, st));
+  ctx->launches++;
+  int64_t h_cnt = 0;
+  TCMIS_CUDA(cudaMemcpyAsync(&h_cnt, ws.mis_count, 8, cudaMemcpyDeviceToHost, st));
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  if (mis_count) *mis_count = h_cnt;
+  if (mis_out && h_cnt)
+    TCMIS_CUDA(cudaMemcpyAsync(mis_out, ws.mis, 4ull * h_cnt, cudaMemcpyDeviceToHost, st));
+  if (state_out) TCMIS_CUDA(cudaMemcpyAsync(state_out, ws.state, (size_t)n, cudaMemcpyDeviceToHost, st));
+  // this rank's phase stamps (the reference's timers, engine.cpp:253-284)
+  std::vector<DevRound> stamps((size_t)std::min(rounds_run, ws.round_cap));
+  if (!stamps.empty())
+    TCMIS_CUDA(cudaMemcpyAsync(stamps.data(), ws.rounds, sizeof(DevRound) * stamps.size(),
+                               cudaMemcpyDeviceToHost, st));
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  auto span_ms = [](unsigned long long a0, unsigned long long a1) {
+    return (a0 && a1 && a1 > a0) ? (double)(a1 - a0) * 1e-6 : 0.0;
+  };
+  const int H = cfg->heuristic;
+  if (H == TCMIS_H3) {
+    // engine.cpp:255-258: one collapsed iteration; tiles of the block columns
+    // holding any MIS vertex, summed over the ranks
+    int64_t ev = 0;
+    if (int rc = seg_total(g, &ev)) return rc;
+    TCMIS_CUDA(cudaMemcpyAsync(b.counts, &ev, 8, cudaMemcpyHostToDevice, st));
+    TCMIS_CUDA(cudaMemcpyAsync(b.counts + 1, &g->tile_total, 8, cudaMemcpyHostToDevice, st));
+    if (int rc = x_all_reduce(x, b.counts, 2, st)) return rc;
+    int64_t red[2] = {0, 0};
+    TCMIS_CUDA(cudaMemcpyAsync(red, b.counts, 16, cudaMemcpyDeviceToHost, st));
+    TCMIS_CUDA(cudaStreamSynchronize(st));
+    if (stats && max_stats > 0) {
+      tcmis_iter_stats s{};
+      s.iteration = 1;
+      s.candidates_selected = h_cnt;
+      s.vertices_removed = n - h_cnt;
+      s.alive_remaining = 0;
+      s.tiles_evaluated = red[0];
+      s.tiles_skipped = red[1] - red[0];
+      for (const DevRound &d : stamps) {
+        const unsigned long long p2 = d.t[1] ? d.t[1] : d.t[2];
+        s.phase1_ms += span_ms(d.t[0], p2 ? p2 : d.t[3]);
+        s.phase2_ms += span_ms(d.t[1], d.t[2]);
+        s.phase3_ms += span_ms(d.t[2], d.t[3]);
+      }
+      stats[0] = s;
+    }
+    *n_iter = 1;
+    return 0;
+  }
+  for (int32_t r = 0; r < rounds_run && stats && r < max_stats; ++r) {
+    tcmis_iter_stats s{};
+    s.iteration = r + 1;
+    s.candidates_selected = got[r].v[0];
+    s.vertices_removed = got[r].v[1];
+    s.alive_remaining = got[r].v[2];
+    s.tiles_evaluated = got[r].v[3];
+    s.tiles_skipped = got[r].v[4];
+    if (r < (int32_t)stamps.size()) {
+      const DevRound &d = stamps[r];
+      const unsigned long long p2 = d.t[1] ? d.t[1] : d.t[2];
+      s.phase1_ms = span_ms(d.t[0], p2 ? p2 : d.t[3]);
+      s.phase2_ms = span_ms(d.t[1], d.t[2]);
+      s.phase3_ms = span_ms(d.t[2], d.t[3]);
+    }
+    stats[r] = s;
+  }
+  *n_iter = rounds_run;
+  return 0;
+}
+
+}  // namespace tcmis_b200
+
+using namespace tcmis_b200;
+
+#define NEED(cond, msg) \
+  if (!(cond)) return set_error(TCMIS_E_INVALID_ARGUMENT, msg)
+
+TCMIS_API int tcmis_nccl_unique_id(uint8_t id[128]) {
+  NEED(id, "null buffer");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  NcclApi &A = nccl();
+  if (!A.error.empty()) return set_error(TCMIS_E_RUNTIME, A.error);
+  ncclUniqueId u;
+  ncclResult_t r = A.GetUniqueId(&u);
+  if (r != ncclSuccess) return nccl_error(r, "ncclGetUniqueId");
+  std::memcpy(id, &u, 128);
+  return 0;
+}
+
+TCMIS_API int tcmis_exchange_nccl(tcmis_ctx *ctx, int32_t world, int32_t rank, const uint8_t id[128],
+                                  tcmis_exchange **out) {
+  NEED(ctx && id && out, "null handle");
+  NEED(world >= 1 && rank >= 0 && rank < world, "bad rank / world");
+  NcclApi &A = nccl();
+  if (!A.error.empty()) return set_error(TCMIS_E_RUNTIME, A.error);
+  TCMIS_CUDA(cudaSetDevice(ctx->device));
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  ncclComm_t comm = nullptr;
+  ncclResult_t r = A.CommInitRank(&comm, world, u, rank);
+  if (r != ncclSuccess) return nccl_error(r, "ncclCommInitRank");
+  auto *x = new tcmis_exchange();
+  x->kind = 1;
+  x->world = world;
+  x->rank = rank;
+  x->capturable = std::getenv("TCMIS_PART_NO_GRAPH") == nullptr;
+  x->comm = comm;
+  x->owns_comm = true;
+  *out = x;
+  return 0;
+}
+
+TCMIS_API int tcmis_exchange_nccl_comm(void *nccl_comm, tcmis_exchange **out) {
+  NEED(nccl_comm && out, "null handle");
+  NcclApi &A = nccl();
+  if (!A.error.empty()) return set_error(TCMIS_E_RUNTIME, A.error);
+  int world = 0, rank = 0;
+  ncclResult_t r = A.CommCount(static_cast<ncclComm_t>(nccl_comm), &world);
+  if (r == ncclSuccess) r = A.CommUserRank(static_cast<ncclComm_t>(nccl_comm), &rank);
+  if (r != ncclSuccess) return nccl_error(r, "ncclCommCount / ncclCommUserRank");
+  auto *x = new tcmis_exchange();
+  x->kind = 1;
+  x->world = world;
+  x->rank = rank;
+  x->capturable = std::getenv("TCMIS_PART_NO_GRAPH") == nullptr;
+  x->comm = static_cast<ncclComm_t>(nccl_comm);
+  x->owns_comm = false;
+  *out = x;
+  return 0;
+}
+
+TCMIS_API int tcmis_exchange_local_group(int32_t world, tcmis_exchange **out) {
+  NEED(out && world >= 1, "bad arguments");
+  auto G = std::make_shared<LocalGroup>();
+  G->world = world;
+  G->send.assign(world, nullptr);
+  G->ready.assign(world, nullptr);
+  G->done.assign(world, nullptr);
+  for (int r = 0; r < world; ++r) {
+    TCMIS_CUDA(cudaEventCreateWithFlags(&G->ready[r], cudaEventDisableTiming));
+    TCMIS_CUDA(cudaEventCreateWithFlags(&G->done[r], cudaEventDisableTiming));
+  }
+  for (int r = 0; r < world; ++r) {
+    auto *x = new tcmis_exchange();
+    x->kind = 2;
+    x->world = world;
+    x->rank = r;
+    x->capturable = false;  // cross-thread events cannot be captured
+    x->group = G;
+    out[r] = x;
+  }
+  return 0;
+}
+
+TCMIS_API void tcmis_exchange_destroy(tcmis_exchange *x) {
+  if (!x) return;
+  if (x->kind == 1 && x->owns_comm && x->comm) nccl().CommDestroy(x->comm);
+  if (x->scratch) cudaFree(x->scratch);
+  if (x->group && x->group.use_count() == 1) {
+    for (cudaEvent_t e : x->group->ready) cudaEventDestroy(e);
+    for (cudaEvent_t e : x->group->done) cudaEventDestroy(e);
+  }
+  delete x;
+}
+
+TCMIS_API void tcmis_exchange_abort(tcmis_exchange *x) {
+  if (x && x->kind == 2) x->group->abort();
+}
+
+TCMIS_API int32_t tcmis_exchange_world(const tcmis_exchange *x) { return x ? x->world : 0; }
+TCMIS_API int32_t tcmis_exchange_rank(const tcmis_exchange *x) { return x ? x->rank : -1; }
+
+TCMIS_API int tcmis_solve_partitioned(tcmis_graph *part, tcmis_exchange *x, const int32_t *rank_lo,
+                                      int32_t world, const tcmis_config *cfg, uint8_t *state_out,
+                                      int32_t *mis_out, int64_t *mis_count,
+                                      tcmis_iter_stats *stats, int32_t max_stats,
+                                      int32_t *n_iterations) {
+  NEED(part && x && rank_lo && cfg && n_iterations, "null handle");
+  NEED(world >= 1, "bad world");
+  TCMIS_CUDA(cudaSetDevice(part->ctx->device));
+  t_alloc_stream = part->ctx->stream;
+  const int rc = solve_partitioned_impl(part, x, rank_lo, world, cfg, state_out, mis_out,
+                                        mis_count, stats, max_stats, n_iterations);
+  if (rc && x->kind == 2) x->group->abort();  // do not leave the peers in the barrier
+  return rc;
+}

@@ -566,8 +566,8 @@ SelectArgs select_args(tcmis_graph *g, const RoundArgs &a) {
   s.long_list = ws.long_list;
   s.vlong = ws.vlong;
   s.undecided = ws.undec_sel;
-  s.pub = Publish{a.pub_cand, a.pub_lo};
-  if (a.tile) s.pub = Publish{ws.cbits, 0};  // the candidate segments of the tile kernels
+  s.pub = Publish{a.pub_cand, a.pub_lo, a.pub_lcand, a.pub_cap};
+  if (a.tile) s.pub = Publish{ws.cbits, 0, nullptr, 0};  // the candidate segments of the tile kernels
   s.rounds = ws.rounds;
   return s;
 }
@@ -594,7 +594,7 @@ UpdateArgs update_args(tcmis_graph *g, const RoundArgs &a) {
   u.prow = ws.prow;
   u.pitems = ws.pitems;
   u.undecided = ws.undec_pull;
-  u.pub = Publish{a.pub_dead, a.pub_lo};
+  u.pub = Publish{a.pub_dead, a.pub_lo, a.pub_ldead, a.pub_cap};
   u.segflag = ws.segflag;
   u.tile_hit = a.tile ? ws.tile_hit : nullptr;
   u.rowtiles = a.rowtiles;

@@ -140,7 +140,7 @@ __device__ __forceinline__ void round_end_tail(const UpdateArgs &a, unsigned lon
     // engine.cpp:138-160: every alive vertex leaves as selected or removed or
     // stays alive; anything else is a corrupt candidate (logic_error).  On a
     // rank of a partitioned solve the counts are the rank's own.
-    if (!a.pub.bits && (unsigned long long)vc->alive != sel + rem_all + (unsigned long long)alive)
+    if (!a.pub.bits && !a.pub.list && (unsigned long long)vc->alive != sel + rem_all + (unsigned long long)alive)
       vc->corrupt = 1;
     vc->alive = alive;
     vc->sel = 0;

@@ -19,6 +19,16 @@ Per round (the reference's bulk-synchronous round, engine.cpp:247-291):
 so the MIS, the round count and every per-round statistic equal the
 single-GPU solve (tests/test_distributed.py checks world sizes 2 and 3 with
 gloo on CPU through the same driver; the device side is csrc/dist.cu).
+
+Two drivers run this round:
+  * ``solve_native`` -- the production path: ``tcmis_solve_partitioned``
+    (csrc/partitioned.cu) runs every round from C++, each round one CUDA
+    graph launch over NCCL (bitmap slices, then id lists in the late rounds);
+    Python only creates the exchange (the NCCL id travels over
+    torch.distributed) and makes one call per solve;
+  * ``solve_partitioned`` -- the same protocol step by step from Python over
+    torch.distributed, kept as the executable specification the CPU (gloo)
+    tests run.
 Slices are padded to the largest rank's word count (``maxw``) so one
 all_gather_into_tensor moves them; rank r's slice sits at word r * maxw.
 """
@@ -310,3 +320,124 @@ def solve_partitioned_local(ranks: list, rank_lo: list[int], heuristic: str = "h
         rounds = collapse_h3(rounds, n, ev, tot)
     state = np.concatenate([r.state() for r in ranks])
     return state, rounds
+
+
+# --------------------------------------------------------- native driver
+
+class Exchange:
+    """A tcmis_exchange handle (include/tcmis_b200.h)."""
+
+    def __init__(self, h):
+        import paper_2605_29604_b200 as tc
+        self.tc, self.h = tc, h
+
+    @classmethod
+    def nccl(cls, ctx, world: int, rank: int, dist=None, unique_id: bytes | None = None):
+        """One communicator per rank: rank 0's ncclGetUniqueId is broadcast over
+        ``dist`` (torch.distributed, any backend) unless ``unique_id`` is given."""
+        import paper_2605_29604_b200 as tc
+        L = tc.load()
+        if unique_id is None:
+            buf = (C.c_uint8 * 128)()
+            if rank == 0:
+                tc._check(L.tcmis_nccl_unique_id(buf))
+            if dist is not None and world > 1:
+                import torch
+                t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+                if dist.get_backend() == "nccl":
+                    t = t.cuda()
+                dist.broadcast(t, 0)
+                buf = (C.c_uint8 * 128)(*t.cpu().tolist())
+        else:
+            buf = (C.c_uint8 * 128)(*unique_id)
+        h = C.c_void_p()
+        tc._check(L.tcmis_exchange_nccl(ctx.h, world, rank, buf, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def local_group(cls, world: int) -> list:
+        """world handles of one in-process group (one host thread per rank)."""
+        import paper_2605_29604_b200 as tc
+        arr = (C.c_void_p * world)()
+        tc._check(tc.load().tcmis_exchange_local_group(world, arr))
+        return [cls(C.c_void_p(arr[r])) for r in range(world)]
+
+    def abort(self):
+        self.tc.load().tcmis_exchange_abort(self.h)
+
+    def close(self):
+        if self.h:
+            self.tc.load().tcmis_exchange_destroy(self.h)
+            self.h = None
+
+
+@dataclass
+class NativeResult:
+    state: np.ndarray      # final VertexState of all n vertices
+    mis: np.ndarray        # ascending ids of the whole MIS
+    rounds: list           # RoundStats (counters summed over the ranks)
+    phase_ms: list         # this rank's (phase1, phase2, phase3) per iteration
+
+
+def solve_native(part, exchange: Exchange, rank_lo: list[int], heuristic: str = "h2",
+                 seed: int = 1, tile_dim: int = 16, scale_bits: int = 20,
+                 want_state: bool = True) -> NativeResult:
+    """One rank's whole partitioned solve (tcmis_solve_partitioned); ``part`` is
+    the rank's DeviceGraph of rows (GpuRank.g)."""
+    import paper_2605_29604_b200 as tc
+    if heuristic not in HEURISTICS:
+        raise ValueError(f"partitioned solve runs {sorted(HEURISTICS)}, not {heuristic!r}")
+    L = tc.load()
+    cfg = tc.EngineConfig(heuristic=HEURISTICS[heuristic], seed=seed, tile_dim=tile_dim,
+                          scale_bits=scale_bits)
+    c, keep = cfg._c()
+    n = rank_lo[-1]
+    lo = np.ascontiguousarray(rank_lo, np.int32)
+    state = np.zeros(max(n, 1), np.uint8)
+    mis = np.zeros(max(n, 1), np.int32)
+    cnt = C.c_int64(0)
+    cap = 4096
+    stats = (tc._Stats * cap)()
+    nit = C.c_int32(0)
+    tc._check(L.tcmis_solve_partitioned(part.h, exchange.h, C.c_void_p(lo.ctypes.data),
+                                        len(rank_lo) - 1, C.byref(c),
+                                        C.c_void_p(state.ctypes.data) if want_state else None,
+                                        C.c_void_p(mis.ctypes.data), C.byref(cnt), stats, cap,
+                                        C.byref(nit)))
+    del keep
+    rounds, phases = [], []
+    for i in range(min(nit.value, cap)):
+        s = stats[i]
+        rounds.append(RoundStats(s.iteration, s.candidates_selected, s.vertices_removed,
+                                 s.alive_remaining, s.tiles_evaluated, s.tiles_skipped))
+        phases.append((s.phase1_ms, s.phase2_ms, s.phase3_ms))
+    return NativeResult(state[:n] if want_state else None, mis[:cnt.value].copy(), rounds, phases)
+
+
+def solve_native_local(ranks: list, rank_lo: list[int], **kw) -> list:
+    """All ranks of one process (a GpuRank each, e.g. all on cuda:0), one host
+    thread per rank through an in-process exchange group; returns every rank's
+    NativeResult."""
+    import threading
+    xs = Exchange.local_group(len(ranks))
+    out: list = [None] * len(ranks)
+    err: list = [None] * len(ranks)
+
+    def run(k):
+        try:
+            out[k] = solve_native(ranks[k].g, xs[k], rank_lo, **kw)
+        except BaseException as e:  # noqa: BLE001 -- re-raised below
+            err[k] = e
+            xs[k].abort()
+
+    th = [threading.Thread(target=run, args=(k,)) for k in range(len(ranks))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for x in xs:
+        x.close()
+    for e in err:
+        if e is not None:
+            raise e
+    return out
