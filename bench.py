@@ -165,7 +165,7 @@ def run_ours(args) -> dict:
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or args.partitioned:
         return run_partitioned(args, rank, world, local)
     dist = None
     torch.cuda.set_device(local)
@@ -513,6 +513,9 @@ def run_partitioned(args, rank: int, world: int, local: int) -> dict | None:
     dev = local % ndev  # one GPU per rank; ranks share a GPU only in emulation runs
     torch.cuda.set_device(dev)
     device = f"cuda:{dev}"
+    for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29533"), ("RANK", str(rank)),
+                 ("WORLD_SIZE", str(world))):
+        os.environ.setdefault(k, v)  # --partitioned at N = 1 without torchrun
     dist.init_process_group(args.dist_backend)
     ctx = tc.Context(dev)
     L = tc.load()
@@ -567,10 +570,26 @@ def run_partitioned(args, rank: int, world: int, local: int) -> dict | None:
     me = D.GpuRank(ctx, n, rank_lo[rank], rank_lo[rank + 1], None, None, device, full=full)
     full.close()
     stream = torch.cuda.ExternalStream(ctx.stream, device=device)
+    # the native driver (tcmis_solve_partitioned: every round one CUDA graph over
+    # NCCL, driven from C++) needs one GPU per rank; the gloo emulation runs
+    # (ranks sharing a GPU) take the step-wise Python driver
+    native = args.dist_backend == "nccl" and args.dist_driver == "native"
+    xch = D.Exchange.nccl(ctx, world, rank, dist) if native else None
+    own_n = rank_lo[rank + 1] - rank_lo[rank]
+    mis_buf = torch.empty(max(own_n, 1), dtype=torch.int32).pin_memory().numpy()
 
     def solve():
+        if native:
+            # this rank's MIS ids land in pinned host memory (the N = 1 value's
+            # definition: the ids back on the host), each rank its own rows
+            return D.solve_native(me.g, xch, rank_lo, heuristic=args.heuristic, seed=1,
+                                  tile_dim=16, want_state=False, own_range=True,
+                                  mis_out=mis_buf)
         return D.solve_partitioned(me, rank_lo, rank, world, dist, heuristic=args.heuristic,
                                    seed=1, tile_dim=16)
+
+    def mis_of(res):
+        return int(res.mis.size) if native else int((res.own_state == 1).sum())
 
     for _ in range(args.warmup):
         res = solve()
@@ -593,7 +612,7 @@ def run_partitioned(args, rank: int, world: int, local: int) -> dict | None:
     dist.all_reduce(total, op=dist.ReduceOp.MAX)
     ms_per_step = float(total.item()) / args.steps
     # result: |MIS| over all ranks (own ranges), rounds from the all-reduced stats
-    mis_own = torch.tensor([int((res.own_state == 1).sum())], device=tdev)
+    mis_own = torch.tensor([mis_of(res)], device=tdev)
     dist.all_reduce(mis_own)
     mis_size = int(mis_own.item())
     # e2e: the drop-in host path per rank (own rows uploaded from pinned host
@@ -614,8 +633,14 @@ def run_partitioned(args, rank: int, world: int, local: int) -> dict | None:
             t_a = time.perf_counter()
             rk = D.GpuRank(ctx, n, rank_lo[rank], rank_lo[rank + 1], h_off, None, device,
                            rows=own_rows)
-            r2 = D.solve_partitioned(rk, rank_lo, rank, world, dist, heuristic=args.heuristic,
-                                     seed=1, tile_dim=16, max_rounds=len(res.rounds) + 1)
+            if native:
+                r2 = D.solve_native(rk.g, xch, rank_lo, heuristic=args.heuristic, seed=1,
+                                    tile_dim=16, want_state=False, own_range=True,
+                                    mis_out=mis_buf)
+            else:
+                r2 = D.solve_partitioned(rk, rank_lo, rank, world, dist,
+                                         heuristic=args.heuristic, seed=1, tile_dim=16,
+                                         max_rounds=len(res.rounds) + 1)
             rk.close()
             if [tuple(vars(x).values()) for x in r2.rounds] != [tuple(vars(x).values())
                                                                 for x in res.rounds]:
@@ -628,15 +653,19 @@ def run_partitioned(args, rank: int, world: int, local: int) -> dict | None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e_ms1 = float(t.item())
         own_nnz = int(own_rows.size)
-        hb = torch.tensor([8 * (n + 1) + 4 * own_nnz, max(0, rank_lo[rank + 1] - rank_lo[rank])],
+        hb = torch.tensor([8 * (n + 1) + 4 * own_nnz,
+                           4 * mis_of(res) if native else max(0, own_n)],
                           device=tdev, dtype=torch.int64)
         dist.all_reduce(hb)
         e2e = {"value": round(m / (e_ms1 * 1e-3) / 1e9, 4), "unit": "Gedges/s",
                "ms": round(e_ms1, 3), "h2d_bytes_per_step": int(hb[0]),
                "d2h_bytes_per_step": int(hb[1]), "steps": steps,
                "clock": "host wall clock between barriers (max over ranks)",
-               "path": "tcmis_graph_upload_partition (own rows, pinned host CSR) + the "
-                       "partitioned rounds + tcmis_dist_state, per rank"}
+               "path": ("tcmis_graph_upload_partition (own rows, pinned host CSR) + "
+                        "tcmis_solve_partitioned (own MIS ids to pinned host memory), per rank"
+                        if native else
+                        "tcmis_graph_upload_partition (own rows, pinned host CSR) + the "
+                        "partitioned rounds + tcmis_dist_state, per rank")}
     line = {
         "metric": "Gedges/s (MIS solve, BASELINE config)",
         "value": round(m / (ms_per_step * 1e-3) / 1e9, 4), "unit": "Gedges/s",
@@ -647,13 +676,20 @@ def run_partitioned(args, rank: int, world: int, local: int) -> dict | None:
         "config": {"workload": CONFIGS[args.config]["workload"], "graph": args.config, "n": n,
                    "m": m, "heuristic": args.heuristic, "seed": 1, "tile_dim": 16,
                    "iterations": len(res.rounds), "mis_size": mis_size,
-                   "parallelism": f"row-partitioned x{world} (NCCL all-gather of candidate / "
-                                  f"removal bitmaps, all-reduce of round counters)",
+                   "parallelism": f"row-partitioned x{world} (all-gather of candidate / "
+                                  f"removal bitmaps, id lists in the late rounds; all-reduce "
+                                  f"of the round counters)",
+                   "driver": ("native: tcmis_solve_partitioned, one CUDA graph per round over "
+                              "NCCL" if native else "python: distributed.solve_partitioned"),
                    "rank_lo": rank_lo, "backend": args.dist_backend,
                    "l2": "no flush: the per-rank CSR slices exceed L2 at s26"},
         "mis_ms": round(ms_per_step, 4),
         "single_gpu_same_graph": single,
         "roofline": None, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
+        "host_profile": D.native_profile(me.g) if native else None,
+        "value_definition": ("each rank's own MIS ids in pinned host memory (the whole MIS "
+                             "across the ranks), max-over-ranks CUDA-event time"
+                             if native else "device-resident states"),
     }
     if single is not None:
         single["matches_partitioned"] = (single["iterations"] == len(res.rounds)
@@ -880,6 +916,11 @@ def main():
                     help="default: rmat22 at N = 1, rmat26 (row-partitioned) at N > 1")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: single-GPU emulation of N ranks (test only)")
+    ap.add_argument("--dist-driver", default="native", choices=["native", "python"],
+                    help="N > 1 over NCCL: tcmis_solve_partitioned (native) or the step-wise "
+                         "Python protocol")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="run the partitioned leg even at N = 1 (a one-rank NCCL group)")
     ap.add_argument("--no-single", action="store_true",
                     help="N > 1: skip rank 0's single-GPU solve of the same graph")
     ap.add_argument("--no-e2e", action="store_true")

@@ -90,6 +90,9 @@ typedef struct tcmis_config {
 
 #define TCMIS_F_TIMING 0x1u     /* record per-phase device times in the stats */
 #define TCMIS_F_HOST_LOOP 0x2u  /* drive rounds from the host (no CUDA-graph while loop) */
+/* tcmis_solve_partitioned: mis_out / state_out cover this rank's rows only
+ * (its share of a distributed result) instead of all n vertices */
+#define TCMIS_F_OWN_RANGE 0x4u
 /* test hook: start the solve from a control block that disagrees with the
  * vertex states; the device's round invariant check must then fail the solve
  * with TCMIS_E_LOGIC (the reference's logic_error, engine.cpp:152-153) */
@@ -250,7 +253,7 @@ int tcmis_dist_h3_tiles(tcmis_graph *g, int64_t *tiles_evaluated, int64_t *tile_
  * as for tcmis_dist_apply.  Outputs (each may be NULL but n_iterations):
  * state_out[n] the final VertexState of ALL n vertices, mis_out[n] the
  * ascending ids of the whole MIS (every rank holds the replicated state at
- * the end), stats as tcmis_solve (counters summed over the ranks; phase
+ * the end; with TCMIS_F_OWN_RANGE both cover this rank's rows only), stats as tcmis_solve (counters summed over the ranks; phase
  * times are this rank's).  Every rank must call it with the same arguments
  * (collectives); a rank's error leaves its peers blocked in the exchange. */
 typedef struct tcmis_exchange tcmis_exchange;
@@ -278,6 +281,13 @@ int tcmis_solve_partitioned(tcmis_graph *part, tcmis_exchange *x, const int32_t 
                             int32_t world, const tcmis_config *cfg, uint8_t *state_out,
                             int32_t *mis_out, int64_t *mis_count, tcmis_iter_stats *stats,
                             int32_t max_stats, int32_t *n_iterations);
+
+/* Host-side profile of the last tcmis_solve_partitioned on `part`: out[0]
+ * rounds, out[1] total host time spent enqueueing rounds (graph launches or
+ * direct launches + exchange calls), out[2] total time the host waited for
+ * round counters, out[3] wall time of the round loop (all us), out[4] rounds
+ * enqueued with id lists. */
+int tcmis_partitioned_profile(const tcmis_graph *part, double out[5]);
 
 /* h1_random (priorities.cpp:33-41) without a graph: n priorities on the
  * device of the context, copied to p_out[n]. */

@@ -99,6 +99,7 @@ class _Config(C.Structure):
 
 F_TIMING = 0x1
 F_HOST_LOOP = 0x2
+F_OWN_RANGE = 0x4
 F_DEBUG_CORRUPT = 0x100  # test hook (include/tcmis_b200.h)
 
 
@@ -158,6 +159,7 @@ def load():
         "tcmis_exchange_abort": (None, [vp]),
         "tcmis_exchange_world": (i32, [vp]),
         "tcmis_exchange_rank": (i32, [vp]),
+        "tcmis_partitioned_profile": (C.c_int, [vp, vp]),
         "tcmis_solve_partitioned": (C.c_int, [vp, vp, vp, i32, P(_Config), vp, vp, P(i64),
                                               P(_Stats), i32, P(i32)]),
     }

@@ -347,9 +347,23 @@ std::mutex &bufs_mu() {
   return mu;
 }
 
+// host-side profile of the last partitioned solve of a graph
+struct PartProfile {
+  int32_t rounds = 0, sparse_rounds = 0;
+  double enqueue_us = 0, wait_us = 0, rounds_us = 0;
+};
+std::map<const tcmis_graph *, PartProfile> &profiles() {
+  static auto *m = new std::map<const tcmis_graph *, PartProfile>();
+  return *m;
+}
+
 }  // namespace
 
 void free_partitioned(tcmis_graph *g) {
+  {
+    std::lock_guard<std::mutex> lk(bufs_mu());
+    profiles().erase(g);
+  }
   std::lock_guard<std::mutex> lk(bufs_mu());
   auto it = bufs_of().find(g);
   if (it == bufs_of().end()) return;
@@ -555,16 +569,31 @@ int solve_partitioned_impl(tcmis_graph *g, tcmis_exchange *x, const int32_t *ran
   };
   // round k+1 is enqueued before round k's counters are read; its decisions
   // are bounded by the alive count after round k-1
-  if (int rc = launch_round(g, x, a, b, 0)) return rc;
+  using clk = std::chrono::steady_clock;
+  const auto t_start = clk::now();
+  double enqueue_us = 0, wait_us = 0;
+  int32_t sparse_rounds = 0;
+  auto timed_launch = [&](int32_t cap) -> int {
+    const auto t0 = clk::now();
+    const int rc = launch_round(g, x, a, b, cap);
+    enqueue_us += std::chrono::duration<double, std::micro>(clk::now() - t0).count();
+    return rc;
+  };
+  if (int rc = timed_launch(0)) return rc;
   bool done = false;
   int32_t rounds_run = 0;
   for (int32_t it = 1; !done; ++it) {
     if (it > cap_rounds)
       return set_error(TCMIS_E_RUNTIME, "iteration cap exceeded; engine livelock");
-    if (it < cap_rounds)
-      if (int rc = launch_round(g, x, a, b, choose(alive_prev[0]))) return rc;
+    if (it < cap_rounds) {
+      const int32_t c = choose(alive_prev[0]);
+      sparse_rounds += c ? 1 : 0;
+      if (int rc = timed_launch(c)) return rc;
+    }
     RingEntry e;
+    const auto tw = clk::now();
     if (int rc = wait_ring(it, e)) return rc;
+    wait_us += std::chrono::duration<double, std::micro>(clk::now() - tw).count();
     if (e.v[5]) return set_error(TCMIS_E_LOGIC, "exchange list overflow (a round decided more "
                                                  "vertices than the alive bound)");
     got.push_back(e);
@@ -575,20 +604,38 @@ int solve_partitioned_impl(tcmis_graph *g, tcmis_exchange *x, const int32_t *ran
   }
   TCMIS_CUDA(cudaStreamSynchronize(st));  // the extra (empty) round too
 
+  const auto t_rounds = clk::now();
+  {
+    std::lock_guard<std::mutex> lk2(bufs_mu());
+    PartProfile &pf = profiles()[g];
+    pf.rounds = rounds_run;
+    pf.enqueue_us = enqueue_us;
+    pf.wait_us = wait_us;
+    pf.rounds_us = std::chrono::duration<double, std::micro>(t_rounds - t_start).count();
+    pf.sparse_rounds = sparse_rounds;
+  }
   // every rank now holds the final state of all n vertices (own decisions +
-  // the applied remote ones): the ascending MIS from one compaction
-  thrust::counting_iterator<int32_t> ids(0);
-  size_t bytes = ws.cub_bytes;
-  TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count, (int)n,
-                                   InMIS{ws.state}, st));
-  ctx->launches++;
-  int64_t h_cnt = 0;
-  TCMIS_CUDA(cudaMemcpyAsync(&h_cnt, ws.mis_count, 8, cudaMemcpyDeviceToHost, st));
-  TCMIS_CUDA(cudaStreamSynchronize(st));
+  // the applied remote ones): the ascending MIS from one compaction -- of all
+  // n, or with TCMIS_F_OWN_RANGE of the own rows only (a distributed result)
+  const bool own_only = (cfg->flags & TCMIS_F_OWN_RANGE) != 0;
+  const int32_t out_lo = own_only ? g->part_lo : 0, out_hi = own_only ? g->part_hi : n;
+  int64_t h_cnt = 0, global_cnt = 0;
+  for (const RingEntry &e : got) global_cnt += e.v[0];
+  if (mis_out || mis_count) {
+    thrust::counting_iterator<int32_t> ids(out_lo);
+    size_t bytes = ws.cub_bytes;
+    TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
+                                     (int)(out_hi - out_lo), InMIS{ws.state}, st));
+    ctx->launches++;
+    TCMIS_CUDA(cudaMemcpyAsync(&h_cnt, ws.mis_count, 8, cudaMemcpyDeviceToHost, st));
+    TCMIS_CUDA(cudaStreamSynchronize(st));
+  }
   if (mis_count) *mis_count = h_cnt;
   if (mis_out && h_cnt)
     TCMIS_CUDA(cudaMemcpyAsync(mis_out, ws.mis, 4ull * h_cnt, cudaMemcpyDeviceToHost, st));
-  if (state_out) TCMIS_CUDA(cudaMemcpyAsync(state_out, ws.state, (size_t)n, cudaMemcpyDeviceToHost, st));
+  if (state_out && out_hi > out_lo)
+    TCMIS_CUDA(cudaMemcpyAsync(state_out, ws.state + out_lo, (size_t)(out_hi - out_lo),
+                               cudaMemcpyDeviceToHost, st));
   // this rank's phase stamps (the reference's timers, engine.cpp:253-284)
   std::vector<DevRound> stamps((size_t)std::min(rounds_run, ws.round_cap));
   if (!stamps.empty())
@@ -613,8 +660,8 @@ int solve_partitioned_impl(tcmis_graph *g, tcmis_exchange *x, const int32_t *ran
     if (stats && max_stats > 0) {
       tcmis_iter_stats s{};
       s.iteration = 1;
-      s.candidates_selected = h_cnt;
-      s.vertices_removed = n - h_cnt;
+      s.candidates_selected = global_cnt;
+      s.vertices_removed = n - global_cnt;
       s.alive_remaining = 0;
       s.tiles_evaluated = red[0];
       s.tiles_skipped = red[1] - red[0];
@@ -765,4 +812,17 @@ TCMIS_API int tcmis_solve_partitioned(tcmis_graph *part, tcmis_exchange *x, cons
                                         mis_count, stats, max_stats, n_iterations);
   if (rc && x->kind == 2) x->group->abort();  // do not leave the peers in the barrier
   return rc;
+}
+
+TCMIS_API int tcmis_partitioned_profile(const tcmis_graph *part, double out[5]) {
+  NEED(part && out, "null handle");
+  std::lock_guard<std::mutex> lk(bufs_mu());
+  auto it = profiles().find(part);
+  if (it == profiles().end()) return set_error(TCMIS_E_INVALID_ARGUMENT, "no partitioned solve yet");
+  out[0] = it->second.rounds;
+  out[1] = it->second.enqueue_us;
+  out[2] = it->second.wait_us;
+  out[3] = it->second.rounds_us;
+  out[4] = it->second.sparse_rounds;
+  return 0;
 }

@@ -123,6 +123,7 @@ class GpuRank:
                 ctx.h, n, lo, hi, C.c_void_p(off.ctypes.data),
                 C.c_void_p(rows.ctypes.data) if rows.size else None, C.byref(h)))
         self.g = tc.DeviceGraph(h, ctx)
+        self.g.lo, self.g.hi = lo, hi  # the rows this partition holds
         self.n, self.lo, self.hi = n, lo, hi
         self.stream = torch.cuda.ExternalStream(ctx.stream, device=device)
         with torch.cuda.stream(self.stream):
@@ -381,9 +382,11 @@ class NativeResult:
 
 def solve_native(part, exchange: Exchange, rank_lo: list[int], heuristic: str = "h2",
                  seed: int = 1, tile_dim: int = 16, scale_bits: int = 20,
-                 want_state: bool = True) -> NativeResult:
+                 want_state: bool = True, own_range: bool = False, mis_out=None) -> NativeResult:
     """One rank's whole partitioned solve (tcmis_solve_partitioned); ``part`` is
-    the rank's DeviceGraph of rows (GpuRank.g)."""
+    the rank's DeviceGraph of rows (GpuRank.g).  own_range: MIS ids and states
+    of this rank's rows only (TCMIS_F_OWN_RANGE); mis_out: a caller-owned
+    (e.g. pinned) int32 buffer for the ids."""
     import paper_2605_29604_b200 as tc
     if heuristic not in HEURISTICS:
         raise ValueError(f"partitioned solve runs {sorted(HEURISTICS)}, not {heuristic!r}")
@@ -391,10 +394,12 @@ def solve_native(part, exchange: Exchange, rank_lo: list[int], heuristic: str = 
     cfg = tc.EngineConfig(heuristic=HEURISTICS[heuristic], seed=seed, tile_dim=tile_dim,
                           scale_bits=scale_bits)
     c, keep = cfg._c()
+    if own_range:
+        c.flags |= tc.F_OWN_RANGE
     n = rank_lo[-1]
     lo = np.ascontiguousarray(rank_lo, np.int32)
     state = np.zeros(max(n, 1), np.uint8)
-    mis = np.zeros(max(n, 1), np.int32)
+    mis = mis_out if mis_out is not None else np.zeros(max(n, 1), np.int32)
     cnt = C.c_int64(0)
     cap = 4096
     stats = (tc._Stats * cap)()
@@ -411,7 +416,25 @@ def solve_native(part, exchange: Exchange, rank_lo: list[int], heuristic: str = 
         rounds.append(RoundStats(s.iteration, s.candidates_selected, s.vertices_removed,
                                  s.alive_remaining, s.tiles_evaluated, s.tiles_skipped))
         phases.append((s.phase1_ms, s.phase2_ms, s.phase3_ms))
-    return NativeResult(state[:n] if want_state else None, mis[:cnt.value].copy(), rounds, phases)
+    ns = (part_range(part)[1] - part_range(part)[0]) if own_range else n
+    return NativeResult(state[:ns] if want_state else None,
+                        mis[:cnt.value] if mis_out is not None else mis[:cnt.value].copy(),
+                        rounds, phases)
+
+
+def part_range(part) -> tuple:
+    return part.lo, part.hi
+
+
+def native_profile(part) -> dict:
+    """Host-side profile of the rank's last native solve (tcmis_partitioned_profile)."""
+    import paper_2605_29604_b200 as tc
+    out = (C.c_double * 5)()
+    tc._check(tc.load().tcmis_partitioned_profile(part.h, out))
+    r = max(1.0, out[0])
+    return {"rounds": int(out[0]), "enqueue_us_per_round": round(out[1] / r, 2),
+            "wait_us_per_round": round(out[2] / r, 2),
+            "round_loop_us_per_round": round(out[3] / r, 2), "list_rounds": int(out[4])}
 
 
 def solve_native_local(ranks: list, rank_lo: list[int], **kw) -> list:

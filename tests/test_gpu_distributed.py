@@ -103,6 +103,10 @@ def test_native_partitioned_local_group(world, cap, spec, heuristic, monkeypatch
         assert np.array_equal(r.mis, exp.mis)
         assert np.array_equal(r.state == 1, exp.state == 1)
         assert np.all(r.state != 0)
+    if cap is None:  # the distributed form: each rank's own rows
+        own = D.solve_native_local(ranks, rank_lo, heuristic=heuristic, own_range=True)
+        assert np.array_equal(np.concatenate([r.mis for r in own]), exp.mis)
+        assert np.array_equal(np.concatenate([r.state for r in own]) == 1, exp.state == 1)
     for rk in ranks:
         rk.close()
 
@@ -154,5 +158,8 @@ def test_native_partitioned_nccl_world1(heuristic):
         res = D.solve_native(me.g, x, rank_lo, heuristic=heuristic)
         assert _got(res.rounds) == _want(exp, heuristic)
         assert np.array_equal(res.mis, exp.mis)
+    prof = D.native_profile(me.g)
+    assert prof["rounds"] == len(exp.rounds) or heuristic == "h3"
+    print("nccl world-1 host profile:", prof)
     x.close()
     me.close()
