@@ -266,6 +266,9 @@ def run_ours(args) -> dict:
     roofline = kernel_roofline(tc, dg, cfg, kernels, args, ms_per_step)
     # ---- e2e through the drop-in C-ABI with host buffers
     e2e = run_e2e(tc, torch, dg, ctx, stream, cfg, args, local, dist, flush)
+    if e2e is not None and rank == 0 and world == 1:
+        # the reference user's own call: tcmis::run_mis on std::vector storage
+        e2e["cpp_dropin_pageable"] = run_cpp_dropin(dg, args, mis_count)
 
     line = {
         "metric": "Gedges/s (MIS solve, BASELINE config)", "value": round(value, 4),
@@ -497,6 +500,49 @@ def run_e2e(tc, torch, dg, ctx, stream, cfg, args, local, dist, flush):
             "d2h_bytes_per_step": int(4 * cnt + 64 * 4096), "steps": steps,
             "path": "tcmis_graph_upload_tiled (upload with the K1 tile count overlapped) + "
                     "tcmis_solve (host buffers)"}
+
+
+def run_cpp_dropin(dg, args, want_mis: int) -> dict | None:
+    """tests/cpp/e2e_main.cpp: a C++ program written against the reference's
+    headers times tcmis::run_mis(const Graph &, cfg) with the Graph in plain
+    std::vector (pageable) memory -- upload (pinned staging ring + host copy
+    threads, csrc/staging.cu), tile count, solve, MIS ids back into a
+    std::vector.  Wall clock around each call, median of 5 after a warm-up."""
+    import subprocess
+    import tempfile
+    import numpy as np
+    h = dg.download()
+    d = tempfile.mkdtemp(prefix="tcmis_e2e_")
+    path, exe = os.path.join(d, "g.bin"), os.path.join(d, "e2e")
+    pkg = os.path.join(ROOT, "paper_2605_29604_b200")
+    try:
+        with open(path, "wb") as f:
+            f.write(np.int32(h.n).tobytes())
+            f.write(np.int64(h.neighbors.size).tobytes())
+            f.write(h.offsets.astype(np.int64).tobytes())
+            f.write(h.neighbors.astype(np.int32).tobytes())
+        del h
+        subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "e2e_main.cpp"), "-L", pkg, "-ltcmis",
+                        "-ltcmis_b200", f"-Wl,-rpath,{pkg}", "-o", exe], check=True)
+        out = subprocess.run([exe, path, "5", args.heuristic], capture_output=True, text=True,
+                             check=True, timeout=600).stdout
+        r = json.loads(out.strip().splitlines()[-1])
+    except Exception as e:  # reported, not fatal: the device line stands
+        log(f"[bench] C++ drop-in e2e failed: {e}")
+        return {"error": str(e)[:200]}
+    finally:
+        for p in (path, exe):
+            if os.path.exists(p):
+                os.remove(p)
+        os.rmdir(d)
+    m = r["m"]
+    return {"value": round(m / (r["median_ms"] * 1e-3) / 1e9, 4), "unit": "Gedges/s",
+            "ms": r["median_ms"], "ms_all": r["ms"], "mis_size": r["mis_size"],
+            "capi_breakdown_ms": r.get("capi_breakdown_ms"),
+            "matches_device_solve": r["mis_size"] == want_mis,
+            "path": "tcmis::run_mis(const Graph &, cfg) from tests/cpp/e2e_main.cpp, Graph in "
+                    "std::vector (pageable) storage, wall clock per call"}
 
 
 # ------------------------------------------- N > 1: row-partitioned solve

@@ -146,6 +146,7 @@ TCMIS_API void tcmis_ctx_destroy(tcmis_ctx *ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   t_alloc_stream = ctx->stream;
+  free_staging(ctx);
   free_workspace(ctx->spare);
   cudaStreamSynchronize(ctx->stream);
   cudaMemPool_t pool;
@@ -212,16 +213,17 @@ TCMIS_API int tcmis_graph_upload(tcmis_ctx *ctx, int32_t n, const int64_t *offse
     dev_free(d_off);
     return rc;
   }
-  cudaError_t e = cudaSuccess;
-  if (offsets) e = cudaMemcpyAsync(d_off, offsets, 8ull * (n + 1), cudaMemcpyHostToDevice, ctx->stream);
-  else e = cudaMemsetAsync(d_off, 0, 8, ctx->stream);
-  if (e == cudaSuccess && nnz)
-    e = cudaMemcpyAsync(d_nbr, neighbors, 4ull * nnz, cudaMemcpyHostToDevice, ctx->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  if (e != cudaSuccess) {
+  int rc = 0;
+  if (offsets) rc = h2d(ctx, d_off, offsets, 8ull * (n + 1), ctx->stream);
+  else if (cudaMemsetAsync(d_off, 0, 8, ctx->stream) != cudaSuccess)
+    rc = cuda_error(cudaGetLastError(), "graph upload");
+  if (!rc && nnz) rc = h2d(ctx, d_nbr, neighbors, 4ull * nnz, ctx->stream);
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (!rc && e != cudaSuccess) rc = cuda_error(e, "graph upload");
+  if (rc) {
     dev_free(d_off);
     dev_free(d_nbr);
-    return cuda_error(e, "graph upload");
+    return rc;
   }
   return wrap_owned(ctx, n, nnz, d_off, d_nbr, out);
 }
@@ -396,9 +398,9 @@ TCMIS_API int tcmis_solve(tcmis_graph *g, const tcmis_config *cfg, uint8_t *stat
   if (g->n == 0) return 0;
   cudaStream_t st = g->ctx->stream;
   if (state_out)
-    TCMIS_CUDA(cudaMemcpyAsync(state_out, g->ws.state, g->n, cudaMemcpyDeviceToHost, st));
+    if (int rc = d2h(g->ctx, state_out, g->ws.state, (size_t)g->n, st)) return rc;
   if (mis_out && mc)
-    TCMIS_CUDA(cudaMemcpyAsync(mis_out, g->ws.mis, 4ull * mc, cudaMemcpyDeviceToHost, st));
+    if (int rc = d2h(g->ctx, mis_out, g->ws.mis, 4ull * mc, st)) return rc;
   TCMIS_CUDA(cudaStreamSynchronize(st));
   return 0;
 }

@@ -86,8 +86,9 @@ int upload_partition(tcmis_ctx *ctx, int32_t n, int32_t lo, int32_t hi, const in
   if (int rc = dev_alloc(&d_full, (size_t)n + 1)) return rc;
   if (int rc = dev_alloc(&d_part, (size_t)n + 1)) return rc;
   if (int rc = dev_alloc(&d_nbr, (size_t)nnz)) return rc;
-  TCMIS_CUDA(cudaMemcpyAsync(d_full, full, 8ull * (n + 1), cudaMemcpyHostToDevice, st));
-  if (nnz) TCMIS_CUDA(cudaMemcpyAsync(d_nbr, rows, 4ull * nnz, cudaMemcpyHostToDevice, st));
+  if (int rc = h2d(ctx, d_full, full, 8ull * (n + 1), st)) return rc;
+  if (nnz)
+    if (int rc = h2d(ctx, d_nbr, rows, 4ull * nnz, st)) return rc;
   k_partial_offsets<<<grid_for(ctx, (int64_t)n + 1, 256, 16), 256, 0, st>>>(n, lo, hi, d_full,
                                                                             d_part);
   TCMIS_LAUNCHED(ctx);

@@ -115,7 +115,32 @@ struct ObserverBridge {
   }
 };
 
-MISResult solve(tcmis_graph *g, VertexId n, const EngineConfig &cfg, Heuristic h) {
+// The result's id vector, allocated and page-faulted on a helper thread while
+// the upload and the solve run on the device (a fresh 16 MB std::vector costs
+// ~2 ms of page faults and zero-fill on the calling thread); the ids are then
+// copied straight into it (d2h staging of the C-ABI) and the vector is
+// shrunk to |MIS| without reallocating.
+class ResultIds {
+ public:
+  explicit ResultIds(VertexId n)
+      : th_([this, n] { ids_.resize(static_cast<std::size_t>(std::max<VertexId>(n, 1))); }) {}
+  ~ResultIds() {
+    if (th_.joinable()) th_.join();
+  }
+  std::vector<VertexId> &get() {
+    if (th_.joinable()) th_.join();
+    return ids_;
+  }
+  ResultIds(const ResultIds &) = delete;
+  ResultIds &operator=(const ResultIds &) = delete;
+
+ private:
+  std::vector<VertexId> ids_;
+  std::thread th_;
+};
+
+MISResult solve(tcmis_graph *g, VertexId n, const EngineConfig &cfg, Heuristic h,
+                ResultIds *ids = nullptr) {
   tcmis_config c;
   tcmis_config_init(&c);
   c.heuristic = static_cast<int32_t>(h);
@@ -132,7 +157,9 @@ MISResult solve(tcmis_graph *g, VertexId n, const EngineConfig &cfg, Heuristic h
   r.heuristic = h;
   r.seed = cfg.seed;
   std::vector<tcmis_iter_stats> st(4096);
-  std::vector<int32_t> mis(static_cast<std::size_t>(std::max<VertexId>(n, 1)));
+  std::optional<ResultIds> own;
+  if (!ids) ids = &own.emplace(n);
+  std::vector<VertexId> &mis = ids->get();
   int64_t cnt = 0;
   int32_t nit = 0;
   check(tcmis_solve(g, &c, nullptr, mis.data(), &cnt, st.data(), static_cast<int32_t>(st.size()),
@@ -146,7 +173,8 @@ MISResult solve(tcmis_graph *g, VertexId n, const EngineConfig &cfg, Heuristic h
     c.observer_user = nullptr;
     check(tcmis_solve(g, &c, nullptr, mis.data(), &cnt, st.data(), nit, &nit));
   }
-  r.mis.assign(mis.begin(), mis.begin() + cnt);
+  mis.resize(static_cast<std::size_t>(cnt));  // shrinks in place
+  r.mis = std::move(mis);
   r.iterations.reserve(static_cast<std::size_t>(nit));
   for (int32_t i = 0; i < nit; ++i) {
     IterationStats s;
@@ -625,8 +653,9 @@ MISResult run_tc_mis(const Graph &g, const EngineConfig &cfg) {
   if (cfg.heuristic != Heuristic::H1 && cfg.heuristic != Heuristic::H2 &&
       cfg.heuristic != Heuristic::H3)
     throw std::invalid_argument("tiled engine only runs h1/h2/h3; use run_luby_reference");
+  ResultIds ids(g.n);               // faulted in while the device works
   DeviceGraph dg(g, cfg.tile_dim);  // tile_graph on the device, overlapped with the upload
-  return solve(dg.h, g.n, cfg, cfg.heuristic);
+  return solve(dg.h, g.n, cfg, cfg.heuristic, &ids);
 }
 
 MISResult run_luby_reference(const Graph &g, std::uint64_t seed, LubyMode mode, int scale_bits,
@@ -641,8 +670,9 @@ MISResult run_luby_reference(const Graph &g, std::uint64_t seed, LubyMode mode, 
   r.heuristic = h;
   r.seed = seed;
   if (g.n == 0) return r;  // engine.cpp:307
+  ResultIds ids(g.n);
   DeviceGraph dg(g);
-  return solve(dg.h, g.n, cfg, h);
+  return solve(dg.h, g.n, cfg, h, &ids);
 }
 
 MISResult run_mis(const Graph &g, const EngineConfig &cfg) {  // engine.cpp:354-365

@@ -95,6 +95,7 @@ struct HostRes {
 };
 
 struct DistState;
+struct Staging;
 
 struct Workspace {
   size_t n_cap = 0;
@@ -165,6 +166,8 @@ struct tcmis_ctx {
   // graph that fits (upload -> solve -> destroy loops re-use buffers, pinned
   // staging and the instantiated round graph)
   tcmis_b200::Workspace spare;
+  // pinned staging ring + host copy threads for pageable caller memory (staging.cu)
+  tcmis_b200::Staging *staging = nullptr;
 };
 
 struct tcmis_graph {
@@ -288,6 +291,13 @@ int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bi
 int ensure_workspace(tcmis_graph *g);
 int ensure_cub(tcmis_graph *g, size_t bytes);
 void free_workspace(Workspace &ws);
+
+// copies of caller host memory (staging.cu): pinned memory goes straight to
+// the copy engine, pageable memory through a pinned ring filled by host threads
+int h2d(tcmis_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t st);
+int d2h(tcmis_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t st);
+bool host_pinned(const void *p);  // page-locked / registered / device-accessible
+void free_staging(tcmis_ctx *ctx);
 
 // partitioned-solve state (dist.cu)
 void free_dist(tcmis_graph *g);

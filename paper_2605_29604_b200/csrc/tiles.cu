@@ -710,8 +710,11 @@ int upload_tiled(tcmis_ctx *ctx, int32_t n, const int64_t *off, const int32_t *n
     dev_free(d_off);
     return rc;
   }
-  if (off) TCMIS_CUDA(cudaMemcpyAsync(d_off, off, 8ull * (n + 1), cudaMemcpyHostToDevice, st));
-  else TCMIS_CUDA(cudaMemsetAsync(d_off, 0, 8, st));
+  if (off) {
+    if (int rc = h2d(ctx, d_off, off, 8ull * (n + 1), st)) return rc;
+  } else {
+    TCMIS_CUDA(cudaMemsetAsync(d_off, 0, 8, st));
+  }
   tcmis_graph *g = nullptr;
   if (int rc = wrap_owned(ctx, n, nnz, d_off, d_nbr, &g)) return rc;
   *out = g;
@@ -749,17 +752,8 @@ int upload_tiled(tcmis_ctx *ctx, int32_t n, const int64_t *off, const int32_t *n
     if (b_c > bnd.back()) bnd.push_back(b_c);
   }
   const int chunks = (int)bnd.size() - 1;
-  for (int c = 0; c < chunks; ++c) {
-    const int64_t e0 = off[(int64_t)bnd[c] * T];
-    const int64_t e1 = off[std::min<int64_t>(n, (int64_t)bnd[c + 1] * T)];
-    if (e1 > e0)
-      TCMIS_CUDA(cudaMemcpyAsync(d_nbr + e0, nbr + e0, 4ull * (e1 - e0), cudaMemcpyHostToDevice, st));
-    TCMIS_CUDA(cudaEventRecord(ctx->side_ev[c], st));
-  }
-  if (p.nb == 0 && nnz)
-    TCMIS_CUDA(cudaMemcpyAsync(d_nbr, nbr, 4ull * nnz, cudaMemcpyHostToDevice, st));
   int32_t hub0 = 0, mid0 = 0, big0 = 0;
-  for (int c = 0; c < chunks; ++c) {
+  auto count_chunk = [&](int c) -> int {
     TCMIS_CUDA(cudaStreamWaitEvent(ctx->side, ctx->side_ev[c], 0));
     if (int rc = k1_light(g, p, bnd[c], bnd[c + 1], ctx->side)) return rc;
     int32_t hub = 0, mid = 0, big = 0;
@@ -768,7 +762,25 @@ int upload_tiled(tcmis_ctx *ctx, int32_t n, const int64_t *off, const int32_t *n
     hub0 = hub;
     mid0 = mid;
     big0 = big;
+    return 0;
+  };
+  // pinned ids: every copy is enqueued at once, then the counts chunk by
+  // chunk; pageable ids keep the host busy staging each chunk (staging.cu),
+  // so chunk c-1 is counted right after chunk c's ids are staged
+  const bool staged = nnz > 0 && !host_pinned(nbr);
+  for (int c = 0; c < chunks; ++c) {
+    const int64_t e0 = off[(int64_t)bnd[c] * T];
+    const int64_t e1 = off[std::min<int64_t>(n, (int64_t)bnd[c + 1] * T)];
+    if (e1 > e0)
+      if (int rc = h2d(ctx, d_nbr + e0, nbr + e0, 4ull * (e1 - e0), st)) return rc;
+    TCMIS_CUDA(cudaEventRecord(ctx->side_ev[c], st));
+    if (staged && c > 0)
+      if (int rc = count_chunk(c - 1)) return rc;
   }
+  if (p.nb == 0 && nnz)
+    if (int rc = h2d(ctx, d_nbr, nbr, 4ull * nnz, st)) return rc;
+  for (int c = staged ? std::max(0, chunks - 1) : 0; c < chunks; ++c)
+    if (int rc = count_chunk(c)) return rc;
   if (chunks > 0) {
     TCMIS_CUDA(cudaEventRecord(ctx->side_ev[kUploadChunks], ctx->side));
     TCMIS_CUDA(cudaStreamWaitEvent(st, ctx->side_ev[kUploadChunks], 0));
