@@ -19,13 +19,14 @@
 // the same pipeline backwards.  Pinned / registered caller memory goes
 // straight to the copy engine.
 #include <emmintrin.h>
+#include <pthread.h>
 
 #include <algorithm>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
-#include <thread>
+#include <thread>  // hardware_concurrency
 #include <vector>
 
 #include "internal.cuh"
@@ -56,11 +57,19 @@ void copy_cached(char *d, const char *s, size_t len) {
   if (i < len) std::memcpy(d + i, s + i, len - i);
 }
 
-// A fixed pool of host threads running one parallel copy at a time.
+// A fixed pool of host threads running one parallel copy at a time.  (POSIX
+// threads: nvcc gives anonymous namespaces external linkage, so a
+// std::thread instantiation over these types would be exported from the
+// library next to the C-ABI.)
 class CopyPool {
  public:
   CopyPool(int threads, bool cached) : cached_(cached) {
-    for (int i = 0; i < threads; ++i) th_.emplace_back([this, i] { loop(i); });
+    args_.resize((size_t)threads);
+    for (int i = 0; i < threads; ++i) {
+      args_[i] = {this, i};
+      pthread_t t;
+      if (pthread_create(&t, nullptr, &CopyPool::entry, &args_[i]) == 0) th_.push_back(t);
+    }
   }
   ~CopyPool() {
     {
@@ -68,7 +77,7 @@ class CopyPool {
       stop_ = true;
     }
     cv_.notify_all();
-    for (auto &t : th_) t.join();
+    for (pthread_t t : th_) pthread_join(t, nullptr);
   }
   // dst[0, bytes) = src[0, bytes), split over the pool and the calling thread
   void copy(void *dst, const void *src, size_t bytes) {
@@ -97,6 +106,15 @@ class CopyPool {
   }
 
  private:
+  struct Arg {
+    CopyPool *self;
+    int i;
+  };
+  static void *entry(void *p) {
+    const Arg *a = static_cast<const Arg *>(p);
+    a->self->loop(a->i);
+    return nullptr;
+  }
   void one(char *d, const char *s, size_t len) {
     if (cached_) copy_cached(d, s, len);
     else std::memcpy(d, s, len);
@@ -126,7 +144,8 @@ class CopyPool {
     }
   }
   bool cached_;
-  std::vector<std::thread> th_;
+  std::vector<Arg> args_;
+  std::vector<pthread_t> th_;
   std::mutex mu_;
   std::condition_variable cv_, done_cv_;
   bool stop_ = false;
