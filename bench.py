@@ -179,6 +179,23 @@ def run_ours(args) -> dict:
     m = nnz // 2
     tiles = dg.tile(16)
     log(f"[bench] {args.config}: n={n} m={m} tiles={tiles} (setup {time.time() - t0:.1f}s)")
+    order_ms = None
+    if args.order == "auto":
+        # measured per config (tools/gpu_order.sh): the
+        # spatial order takes RGG 24M 1.10 -> 0.95 ms, the degree order R-MAT
+        # s26 3.82 -> 3.43 ms; at s22 (q fits L2) and on ER / grid no order helps
+        args.order = {"rgg": "spatial", "rmat26": "degree"}.get(args.config, "none")
+    if args.order != "none":
+        # an internal vertex order for the solve kernels (tcmis_graph_reorder):
+        # graph preparation like the tiling, outside the timed region, results
+        # in the graph's own ids; its one-off cost is reported
+        ctx.synchronize()
+        t_o = time.perf_counter()
+        dg.reorder({"degree": tc.DeviceGraph.ORDER_DEGREE,
+                    "spatial": tc.DeviceGraph.ORDER_SPATIAL}[args.order])
+        ctx.synchronize()
+        order_ms = round((time.perf_counter() - t_o) * 1e3, 3)
+        log(f"[bench] vertex order {args.order}: {order_ms} ms")
     excl = {"auto": tc.Exclusion.AUTO, "push": tc.Exclusion.PUSH,
             "pull": tc.Exclusion.CSR_PULL, "tile-bits": tc.Exclusion.TILE_BITS,
             "tile-mma": tc.Exclusion.TILE_MMA}[args.exclusion]
@@ -193,7 +210,7 @@ def run_ours(args) -> dict:
         stats = (tc._Stats * 4096)()
         nit = C.c_int32(0)
         tc._check(L.tcmis_solve_device(dg.h, C.byref(c_cfg), C.byref(d_mis), C.byref(cnt),
-                                       C.byref(d_state), stats, 4096, C.byref(nit)))
+                                       None, stats, 4096, C.byref(nit)))
         return cnt.value, nit.value
 
     h_mis = torch.empty(max(n, 1), dtype=torch.int32).pin_memory()  # the step's result buffer
@@ -280,7 +297,8 @@ def run_ours(args) -> dict:
                    "n": n, "m": m, "heuristic": args.heuristic, "seed": 1, "tile_dim": 16,
                    "iterations": iters, "mis_size": mis_count, "tiles_t16": tiles,
                    "parallelism": "replicas" if world > 1 else "single",
-                   "l2": "256 MB flush between steps; CSR > L2"},
+                   "l2": "256 MB flush between steps; CSR > L2",
+                   "vertex_order": args.order, "vertex_order_ms": order_ms},
         "mis_ms": round(ms_per_step, 4),
         "device_resident": device_resident,
         "kernels_ms": [[k, r, round(ms, 4)] for k, r, ms in kernels],
@@ -588,7 +606,7 @@ def run_partitioned(args, rank: int, world: int, local: int) -> dict | None:
             d_mis, d_state = C.c_void_p(), C.c_void_p()
             cnt, nit = C.c_int64(0), C.c_int32(0)
             tc._check(L.tcmis_solve_device(full.h, C.byref(c1), C.byref(d_mis), C.byref(cnt),
-                                           C.byref(d_state), stats, 4096, C.byref(nit)))
+                                           None, stats, 4096, C.byref(nit)))
             return cnt.value, nit.value
 
         for _ in range(3):
@@ -972,6 +990,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--heuristic", default="h2", choices=list(HEUR))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--order", default="auto", choices=["auto", "none", "degree", "spatial"],
+                    help="internal vertex order of the device graph (tcmis_graph_reorder)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exclusion", default="auto", choices=["auto", "push", "pull", "tile-bits", "tile-mma"])
     ap.add_argument("--traffic", type=float, default=None,

@@ -168,6 +168,19 @@ int tcmis_graph_set_tiling(tcmis_graph *g, int32_t tile_dim, const int64_t *bloc
  * tcmis_graph_tile()'s count. */
 int tcmis_graph_export_tiles(tcmis_graph *g, int32_t tile_dim, int32_t *tile_row,
                              int32_t *tile_col, uint64_t *row_bits, int64_t *block_row_offsets);
+/* An internal vertex order for the solve kernels (csrc/order.cu): the graph
+ * keeps the caller's CSR and ids and adds a relabeled copy the round kernels
+ * run on, for locality of their neighbour gathers.  Results, statistics and
+ * every other entry point stay in the caller's ids and are bit-identical to
+ * the unordered solve (keys, hash priorities and tile counters are taken on
+ * the caller's ids).  TCMIS_ORDER_NONE drops the copy; SPATIAL needs a graph
+ * from tcmis_gen_rgg; GIVEN takes order[n] (host), order[i] = the caller's id
+ * of solve id i, a permutation of [0, n).  Not for row partitions.  Solves
+ * with an iteration observer or a tile exclusion form use the caller's CSR. */
+enum { TCMIS_ORDER_NONE = 0, TCMIS_ORDER_DEGREE = 1, TCMIS_ORDER_SPATIAL = 2,
+       TCMIS_ORDER_GIVEN = 3 };
+int tcmis_graph_reorder(tcmis_graph *g, int32_t mode, const int32_t *order);
+
 /* The compact device tile store the tile-form exclusion kernels read
  * (tile_dim 8 or 16; same tile set and order as tile_graph, tiling.cpp:44-84):
  * builds it if needed and reports its tile count; with non-null buffers also

@@ -151,6 +151,7 @@ def load():
         "tcmis_gen_gnp_host": (C.c_int, [i32, C.c_double, u64, P(P(i64)), P(P(i32)), P(i64)]),
         "tcmis_free": (None, [vp]),
         "tcmis_rgg_radius": (u64, [i32, C.c_double]),
+        "tcmis_graph_reorder": (C.c_int, [vp, i32, vp]),
         "tcmis_nccl_unique_id": (C.c_int, [vp]),
         "tcmis_exchange_nccl": (C.c_int, [vp, i32, i32, vp, P(vp)]),
         "tcmis_exchange_nccl_comm": (C.c_int, [vp, P(vp)]),
@@ -427,6 +428,15 @@ class DeviceGraph:
         nbr = np.zeros(max(nnz, 1), np.int32)
         _check(load().tcmis_graph_download(self.h, _ptr(off), _ptr(nbr)))
         return Graph(n, off, nbr[:nnz])
+
+    ORDER_NONE, ORDER_DEGREE, ORDER_SPATIAL, ORDER_GIVEN = 0, 1, 2, 3
+
+    def reorder(self, mode: int, order: Optional[np.ndarray] = None) -> "DeviceGraph":
+        """An internal vertex order for the solve kernels (tcmis_graph_reorder):
+        results stay in this graph's ids and bit-identical."""
+        o = None if order is None else np.ascontiguousarray(order, np.int32)
+        _check(load().tcmis_graph_reorder(self.h, int(mode), _ptr(o)))
+        return self
 
     def tile(self, tile_dim: int = 16) -> int:
         cnt = C.c_int64(0)

@@ -257,6 +257,8 @@ TCMIS_API void tcmis_graph_destroy(tcmis_graph *g) {
   dev_free(g->d_off_full);
   free_dist(g);
   free_partitioned(g);
+  free_order(g);
+  dev_free(g->d_spatial);
   free_tile_store(g);
   Workspace &sp = g->ctx->spare;
   if (g->ws.ctrl && g->ws.n_cap >= sp.n_cap) {
@@ -397,8 +399,12 @@ TCMIS_API int tcmis_solve(tcmis_graph *g, const tcmis_config *cfg, uint8_t *stat
   if (mis_count) *mis_count = mc;
   if (g->n == 0) return 0;
   cudaStream_t st = g->ctx->stream;
-  if (state_out)
-    if (int rc = d2h(g->ctx, state_out, g->ws.state, (size_t)g->n, st)) return rc;
+  if (state_out) {
+    if (int rc = states_in_caller_order(g)) return rc;
+    if (int rc = d2h(g->ctx, state_out, g->ws.relabeled ? g->ws.state_o : g->ws.state,
+                     (size_t)g->n, st))
+      return rc;
+  }
   if (mis_out && mc)
     if (int rc = d2h(g->ctx, mis_out, g->ws.mis, 4ull * mc, st)) return rc;
   TCMIS_CUDA(cudaStreamSynchronize(st));
@@ -411,8 +417,17 @@ TCMIS_API int tcmis_solve_device(tcmis_graph *g, const tcmis_config *cfg, const 
                                  int32_t *n_iterations) {
   if (int rc = solve_common(g, cfg, stats, max_stats, n_iterations, mis_count)) return rc;
   if (d_mis) *d_mis = g->ws.mis;
-  if (d_state) *d_state = g->ws.state;
+  if (d_state) {
+    if (int rc = states_in_caller_order(g)) return rc;
+    *d_state = g->ws.relabeled ? g->ws.state_o : g->ws.state;
+  }
   return 0;
+}
+
+TCMIS_API int tcmis_graph_reorder(tcmis_graph *g, int32_t mode, const int32_t *order) {
+  NEED(g, "null handle");
+  ENTER(g->ctx);
+  return reorder_impl(g, mode, order);
 }
 
 TCMIS_API int tcmis_graph_upload_partition(tcmis_ctx *ctx, int32_t n, int32_t lo, int32_t hi,

@@ -124,11 +124,28 @@ __device__ __forceinline__ int32_t seg_of(int32_t v, int T) {
   return (T & (T - 1)) == 0 ? (v >> (__ffs(T) - 1)) : v / T;
 }
 
+// The caller's id of solve id v: graphs with an internal vertex order
+// (tcmis_graph_reorder) run the kernels on relabeled ids, while keys, hash
+// priorities and the tile counters stay defined on the caller's ids
+// (priorities.hpp:61-64, spmv.cpp:37-46); perm == null: identity.
+__device__ __forceinline__ int32_t orig_id(const int32_t *perm, int32_t v) {
+  return perm ? __ldg(&perm[v]) : v;
+}
+
+// A relabeled solve of an L2-sized graph also keeps the MIS membership in the
+// caller's order (mis_o[caller id] = 1, one fire-and-forget byte store per
+// candidate): the final ascending-id compaction then streams it like the
+// unrelabeled states instead of gathering every vertex's state through the
+// permutation (solver.cu kMisOMax).
 __device__ __forceinline__ void mark_candidate(int32_t v, uint8_t *next, uint8_t *state,
-                                               uint8_t *segflag, int T) {
+                                               uint8_t *segflag, int T,
+                                               const int32_t *perm = nullptr,
+                                               uint8_t *mis_o = nullptr) {
   next[v] = 1;
   state[v] = TCMIS_IN_MIS;
-  if (segflag) segflag[seg_of(v, T)] = 1;
+  const int32_t o = orig_id(perm, v);
+  if (mis_o) mis_o[o] = TCMIS_IN_MIS;
+  if (segflag) segflag[seg_of(o, T)] = 1;
 }
 
 // Multi-GPU: a rank publishes its own range's decisions for the exchange
@@ -206,10 +223,12 @@ __device__ __forceinline__ uint32_t ld_gather_q(const uint16_t *p) {
 // stream of p per visited vertex)
 __device__ __forceinline__ bool blocks(const uint16_t *__restrict__ q,
                                        const uint32_t *__restrict__ prio, int32_t u,
-                                       uint32_t qv, int32_t v) {
+                                       uint32_t qv, int32_t v, const int32_t *perm = nullptr) {
   const uint32_t qu = ld_gather_q(&q[u]);
   if (qu != qv) return qu > qv;  // qu == 0 (removed) never blocks: qv >= 1
-  return key_of(__ldg(&prio[u]), u) > key_of(__ldg(&prio[v]), v);
+  const uint32_t pu = __ldg(&prio[u]), pv = __ldg(&prio[v]);
+  if (pu != pv) return pu > pv;
+  return orig_id(perm, u) > orig_id(perm, v);  // the key's id half (priorities.hpp:61-64)
 }
 
 __device__ __forceinline__ uint32_t fresh_prio(int32_t v, uint64_t fresh_m) {
@@ -218,8 +237,8 @@ __device__ __forceinline__ uint32_t fresh_prio(int32_t v, uint64_t fresh_m) {
 }
 
 __device__ __forceinline__ void set_fresh(uint32_t *prio, uint16_t *q, int32_t v,
-                                          uint64_t fresh_m) {
-  const uint32_t p = fresh_prio(v, fresh_m);
+                                          uint64_t fresh_m, const int32_t *perm = nullptr) {
+  const uint32_t p = fresh_prio(orig_id(perm, v), fresh_m);
   prio[v] = p;
   q[v] = q_of(p, 16);
 }

@@ -114,6 +114,27 @@ __global__ void k_rgg_points(int32_t n, uint64_t mseed, uint64_t R, uint64_t C,
   }
 }
 
+// Morton (Z-order) code of a point's grid cell: the RGG's spatial vertex
+// order (order.cu, TCMIS_ORDER_SPATIAL)
+__device__ __forceinline__ uint64_t spread2(uint64_t v) {
+  v &= 0xffffffffull;
+  v = (v | (v << 16)) & 0x0000ffff0000ffffull;
+  v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
+  v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+__global__ void k_rgg_morton(int32_t n, uint64_t R, const uint32_t *__restrict__ x,
+                             const uint32_t *__restrict__ y, unsigned long long *__restrict__ key,
+                             int32_t *__restrict__ ids) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    key[v] = (spread2(x[v] / R) << 1) | spread2(y[v] / R);
+    ids[v] = (int32_t)v;
+  }
+}
+
 __global__ void k_cell_starts(int64_t ncell, int32_t n, const unsigned long long *__restrict__ cell,
                               int64_t *__restrict__ cs) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
@@ -417,10 +438,30 @@ int gen_rgg(tcmis_ctx *ctx, int32_t n, uint64_t R, uint64_t seed, tcmis_graph **
   k_rgg_rows<true><<<grid_for(ctx, n, 256, 16), 256, 0, st>>>(n, R, C, x.p, y.p, cs.p, pts.p,
                                                               nullptr, off.p, nbr.p);
   TCMIS_LAUNCHED(ctx);
+  // the points in Z-order of their cells: the graph's spatial vertex order
+  // (kept on the graph for tcmis_graph_reorder(TCMIS_ORDER_SPATIAL))
+  DevBuf<int32_t> spatial;
+  if (int rc = spatial.alloc(n)) return rc;
+  {
+    k_rgg_morton<<<grid_for(ctx, n, 256, 16), 256, 0, st>>>(n, R, x.p, y.p, cell.p, ids.p);
+    TCMIS_LAUNCHED(ctx);
+    int bits = 2;
+    while (bits < 64 && (1ull << (bits / 2)) < C) bits += 2;
+    size_t bytes = 0;
+    TCMIS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, cell.p, cell2.p, ids.p, spatial.p,
+                                               (int64_t)n, 0, bits, st));
+    DevBuf<char> tmp;
+    if (int rc = tmp.alloc(bytes)) return rc;
+    TCMIS_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, cell.p, cell2.p, ids.p, spatial.p,
+                                               (int64_t)n, 0, bits, st));
+    ctx->launches++;
+  }
   TCMIS_CUDA(cudaStreamSynchronize(st));
   int64_t *o = off.release();
   int32_t *q = nbr.release();
-  return wrap_owned(ctx, n, m, o, q, out);
+  if (int rc = wrap_owned(ctx, n, m, o, q, out)) return rc;
+  (*out)->d_spatial = spatial.release();
+  return 0;
 }
 
 // generate.cpp:30-66 on the host: the gap sequence is one serial RNG stream.

@@ -103,6 +103,9 @@ struct Workspace {
   uint32_t *prio = nullptr;
   uint16_t *q = nullptr;          // q_of(prio) (common.cuh), 0 once removed
   uint8_t *state = nullptr;
+  uint8_t *state_o = nullptr;     // relabeled solves: the final states in the caller's order (on demand)
+  uint8_t *mis_o = nullptr;       // relabeled solves: membership in the caller's order (1 = InMIS)
+  bool relabeled = false;         // the last solve ran on a relabeled CSR
   uint8_t *next = nullptr;
   uint16_t *xt = nullptr;         // k_tail round tags (tail.cuh), zeroed at allocation
   int32_t *wl[2] = {nullptr, nullptr};
@@ -201,6 +204,16 @@ struct tcmis_graph {
   int64_t *d_off_full = nullptr;
   int64_t nnz_global = -1;
   tcmis_b200::DistState *dist = nullptr;  // partitioned-solve state (dist.cu), freed with the graph
+  // internal vertex order (order.cu, tcmis_graph_reorder): the solve kernels
+  // run on a relabeled copy of the CSR, solve id i = the caller's d_perm[i]
+  int32_t order_mode = 0;
+  int32_t *d_perm = nullptr;
+  int32_t *d_inv = nullptr;   // its inverse: the solve id of the caller's vertex v
+  int64_t *d_roff = nullptr;
+  int32_t *d_rnbr = nullptr;
+  int32_t *d_rnz = nullptr;   // non-isolated solve ids, ascending
+  int32_t rnz_count = 0;
+  int32_t *d_spatial = nullptr;  // tcmis_gen_rgg's points in Z-order of their cells
   tcmis_b200::Workspace ws;
 };
 
@@ -277,6 +290,8 @@ struct RoundArgs {
   const int32_t *trow;
   const int32_t *tcol;
   const uint16_t *tbits;
+  const int32_t *perm;  // solve id -> caller id (relabeled CSR), else null
+  uint8_t *mis_o;       // relabeled: caller-order membership kept by the kernels, or null
   bool operator==(const RoundArgs &o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
 
@@ -286,7 +301,8 @@ int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bi
                       uint32_t *p_out, uint16_t *q_out, uint8_t *state, uint8_t *next,
                       uint8_t *segflag = nullptr, int T = 1, Ctrl *ctrl = nullptr,
                       const Ctrl *ctrl0 = nullptr, DevRound *rounds = nullptr,
-                      int32_t nrounds = 0);
+                      int32_t nrounds = 0, const int64_t *solve_off = nullptr,
+                      const int32_t *perm = nullptr, uint8_t *mis_o = nullptr);
 // workspace management (solver.cu)
 int ensure_workspace(tcmis_graph *g);
 int ensure_cub(tcmis_graph *g, size_t bytes);
@@ -298,6 +314,12 @@ int h2d(tcmis_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t s
 int d2h(tcmis_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t st);
 bool host_pinned(const void *p);  // page-locked / registered / device-accessible
 void free_staging(tcmis_ctx *ctx);
+
+// internal vertex order (order.cu)
+int reorder_impl(tcmis_graph *g, int32_t mode, const int32_t *order);
+// a relabeled solve's final states in the caller's order (ws.state_o), on demand
+int states_in_caller_order(tcmis_graph *g);
+void free_order(tcmis_graph *g);
 
 // partitioned-solve state (dist.cu)
 void free_dist(tcmis_graph *g);

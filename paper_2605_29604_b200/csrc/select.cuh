@@ -59,6 +59,8 @@ struct SelectArgs {
   int32_t *undecided;      // rows the probe could not settle (ctrl->sel_undec)
   Publish pub;             // multi-GPU: this round's candidates of the own range
   DevRound *rounds;        // Phase 1 start stamp (null: none)
+  const int32_t *perm;     // solve id -> caller id (relabeled graphs), else null
+  uint8_t *mis_o;          // ... and the membership in the caller's order
 };
 
 // push: every neighbour of a candidate is excluded this round (spmv.cpp:18-59
@@ -104,11 +106,11 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
       bool blocked = false;
 #pragma unroll
       for (int j = 0; j < kProbeK; ++j)
-        if (u[j] >= 0) blocked |= blocks(q, prio, u[j], qv, v);
+        if (u[j] >= 0) blocked |= blocks(q, prio, u[j], qv, v, a.perm);
       if (blocked) {
         // a non-candidate: the pull exclusion finds it on the worklist
       } else if (e - s <= kProbeK) {
-        mark_candidate(v, a.next, a.state, a.segflag, a.T);
+        mark_candidate(v, a.next, a.state, a.segflag, a.T, a.perm, a.mis_o);
         publish(a.pub, v);
         ++sel;
         if (a.push) {
@@ -183,12 +185,12 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
       bool blocked = false;
 #pragma unroll
       for (int j = 0; j < kU; ++j)
-        if (u[j] >= 0) blocked |= blocks(q, prio, u[j], qv, v);
+        if (u[j] >= 0) blocked |= blocks(q, prio, u[j], qv, v, a.perm);
       hi = w;
       if (blocked) {
         mode = kFetch;
       } else if (hi <= s) {
-        mark_candidate(v, a.next, a.state, a.segflag, a.T);
+        mark_candidate(v, a.next, a.state, a.segflag, a.T, a.perm, a.mis_o);
         publish(a.pub, v);
         ++sel;
         mode = a.push ? kPush : kFetch;
@@ -243,13 +245,13 @@ __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
       bool b = false;
 #pragma unroll
       for (int j = 0; j < kWarpU; ++j)
-        if (u[j] >= 0) b |= blocks(a.q, prio, u[j], qv, v);
+        if (u[j] >= 0) b |= blocks(a.q, prio, u[j], qv, v, a.perm);
       blocked = __any_sync(0xffffffffu, b);
       hi -= 32 * kWarpU;
     }
     if (!blocked) {
       if (lane == 0) {
-        mark_candidate(v, a.next, a.state, a.segflag, a.T);
+        mark_candidate(v, a.next, a.state, a.segflag, a.T, a.perm, a.mis_o);
         publish(a.pub, v);
         ++sel;
       }
@@ -268,14 +270,14 @@ __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
 #pragma unroll
       for (int j = 0; j < kWarpU; ++j) {
         const int64_t idx = hi - 1 - threadIdx.x - (int64_t)kBlock * j;
-        if (idx >= s) b |= blocks(a.q, prio, ld_stream(&nbr[idx]), qv, v);
+        if (idx >= s) b |= blocks(a.q, prio, ld_stream(&nbr[idx]), qv, v, a.perm);
       }
       blocked = __syncthreads_or(b) != 0;
       hi -= (int64_t)kBlock * kWarpU;
     }
     if (!blocked) {
       if (threadIdx.x == 0) {
-        mark_candidate(v, a.next, a.state, a.segflag, a.T);
+        mark_candidate(v, a.next, a.state, a.segflag, a.T, a.perm, a.mis_o);
         publish(a.pub, v);
         ++sel;
       }

@@ -60,7 +60,8 @@ __global__ void __launch_bounds__(256)
                  uint16_t *__restrict__ q_out, int qshift, uint8_t *__restrict__ state,
                  uint8_t *__restrict__ next, uint8_t *__restrict__ segflag, int T, int tshift,
                  Ctrl *ctrl, Ctrl ctrl0,
-                 DevRound *rounds, int32_t nrounds) {
+                 DevRound *rounds, int32_t nrounds, const int32_t *__restrict__ perm,
+                 uint8_t *__restrict__ mis_o) {
   // the solve's control block and (for k_tail, which accumulates into it)
   // the zeroed statistics ring: no separate copy / memset on the stream
   if (ctrl && blockIdx.x == 0 && threadIdx.x == 0) *ctrl = ctrl0;
@@ -91,6 +92,9 @@ __global__ void __launch_bounds__(256)
     uint64_t x = mseed + (uint64_t)(v0 + 1) * kGolden;  // vertex_hash, priorities.cpp:21-23
 #pragma unroll
     for (int j = 0; j < kPrioV; ++j, x += kGolden) {
+      // a relabeled graph hashes the caller's id of its vertex (tcmis_graph_reorder)
+      const int32_t vid = perm ? (v0 + j < n ? __ldg(&perm[v0 + j]) : 0) : v0 + j;
+      if (perm) x = mseed + (uint64_t)(vid + 1) * kGolden;
       const int32_t deg = (int32_t)(o[j + 1] - o[j]);
       // an isolated vertex has no alive neighbour: it is a round-1 candidate
       // (engine.cpp:94-99 leaves max_np at kNoNeighborKey) and round 1's
@@ -113,7 +117,8 @@ __global__ void __launch_bounds__(256)
       }
       st4 |= (uint32_t)(iso ? TCMIS_IN_MIS : TCMIS_ALIVE) << (8 * j);
       nx4 |= (uint32_t)(iso ? 1 : 0) << (8 * j);
-      if (iso && segflag) segflag[tshift >= 0 ? (v0 + j) >> tshift : (v0 + j) / T] = 1;
+      if (iso && segflag) segflag[tshift >= 0 ? vid >> tshift : vid / T] = 1;
+      if (iso && mis_o) mis_o[vid] = TCMIS_IN_MIS;  // relabeled: caller-order membership
     }
     if (full) {
       if (p_out) *reinterpret_cast<uint4 *>(p_out + v0) = make_uint4(pv[0], pv[1], pv[2], pv[3]);
@@ -206,6 +211,26 @@ __global__ void k_seg_total(const uint8_t *__restrict__ segflag,
   block_add3(0, 0, ev, ctrl);
 }
 
+// the caller's vertex v is InMIS (relabeled solves without the caller-order
+// membership plane: the compaction walks the caller's ids in order and
+// gathers the solve-order state)
+struct IsInMISInv {
+  const uint8_t *state;
+  const int32_t *inv;
+  __device__ __forceinline__ bool operator()(int32_t v) const {
+    return state[__ldg(&inv[v])] == TCMIS_IN_MIS;
+  }
+};
+
+// relabeled solves: the final states in the caller's order (coalesced
+// writes, a gather of the solve-order states)
+__global__ void k_unpermute(int32_t n, const int32_t *__restrict__ inv,
+                            const uint8_t *__restrict__ state, uint8_t *__restrict__ state_o) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    state_o[v] = state[__ldg(&inv[v])];
+}
+
 struct IsInMIS {
   const uint8_t *state;
   __device__ __forceinline__ bool operator()(int32_t v) const { return state[v] == TCMIS_IN_MIS; }
@@ -296,6 +321,8 @@ void free_workspace(Workspace &ws) {
   dev_free(ws.prio);
   dev_free(ws.q);
   dev_free(ws.state);
+  dev_free(ws.state_o);
+  dev_free(ws.mis_o);
   dev_free(ws.next);
   dev_free(ws.xt);
   dev_free(ws.wl[0]);
@@ -352,6 +379,10 @@ int ensure_workspace(tcmis_graph *g) {
     dev_free(ws.prio);
   dev_free(ws.q);
     dev_free(ws.state);
+    dev_free(ws.state_o);
+    ws.state_o = nullptr;
+    dev_free(ws.mis_o);
+    ws.mis_o = nullptr;
     dev_free(ws.next);
     dev_free(ws.xt);
     dev_free(ws.wl[0]);
@@ -486,6 +517,8 @@ namespace {
 
 }  // namespace
 
+constexpr int64_t kMisOMax = 48ll << 20;  // vertices: caller-order membership plane up to here
+
 // common.cuh q_of: the degree-aware priorities of vertices with an edge are
 // <= 2^scale_bits (avg / (avg + deg - eps) <= 1), hash priorities span u32
 int q_shift(int heuristic, int scale_bits) {
@@ -496,7 +529,8 @@ int q_shift(int heuristic, int scale_bits) {
 int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
                       uint32_t *p_out, uint16_t *q_out, uint8_t *state, uint8_t *next,
                       uint8_t *segflag, int T, Ctrl *ctrl, const Ctrl *ctrl0, DevRound *rounds,
-                      int32_t nrounds) {
+                      int32_t nrounds, const int64_t *solve_off, const int32_t *perm,
+                      uint8_t *mis_o) {
   tcmis_ctx *ctx = g->ctx;
   int mode = 1;
   uint64_t mseed = mix64(seed);
@@ -507,7 +541,7 @@ int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bi
     mseed = mix64(combine_seed(seed, 1));  // engine.cpp:324-325, iteration 1
   }
   const double scale = mode ? (double)(1u << scale_bits) : 0.0;
-  const int64_t *off = g->d_off_full ? g->d_off_full : g->d_off;
+  const int64_t *off = solve_off ? solve_off : (g->d_off_full ? g->d_off_full : g->d_off);
   const int aligned = ((uintptr_t)off & 15) == 0 ? 1 : 0;
   const int tshift = (T & (T - 1)) == 0 ? __builtin_ctz((unsigned)T) : -1;
   const int grid = grid_for(ctx, ((int64_t)g->n + kPrioV - 1) / kPrioV, 256, 8);
@@ -517,7 +551,7 @@ int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bi
                                                           p_out, q_out, q_shift(heuristic, scale_bits),
                                                           state, next, segflag, T, tshift, ctrl,
                                                           ctrl0 ? *ctrl0 : Ctrl{},
-                                                          rounds, nrounds)));
+                                                          rounds, nrounds, perm, mis_o)));
   TCMIS_LAUNCHED(ctx);
   return 0;
 }
@@ -569,6 +603,8 @@ SelectArgs select_args(tcmis_graph *g, const RoundArgs &a) {
   s.pub = Publish{a.pub_cand, a.pub_lo, a.pub_lcand, a.pub_cap};
   if (a.tile) s.pub = Publish{ws.cbits, 0, nullptr, 0};  // the candidate segments of the tile kernels
   s.rounds = ws.rounds;
+  s.perm = a.perm;
+  s.mis_o = a.mis_o;
   return s;
 }
 
@@ -603,6 +639,7 @@ UpdateArgs update_args(tcmis_graph *g, const RoundArgs &a) {
   u.seg_mode = a.seg_mode;
   u.rounds = ws.rounds;
   u.tail_thr = a.tail_thr;
+  u.perm = a.perm;
   return u;
 }
 
@@ -635,6 +672,8 @@ TailArgs tail_args(tcmis_graph *g, const RoundArgs &a) {
   t.mis_count = ws.mis_count;
   t.warpcnt = ws.warpcnt;
   t.pack = nullptr;
+  t.perm = a.perm;
+  t.mis_o = a.mis_o;
   return t;
 }
 
@@ -786,10 +825,14 @@ int ensure_solve_graph(tcmis_graph *g, const RoundArgs &a, const SolvePre &pre) 
       e = cudaMemsetAsync(ws.segflag, 0, (size_t)pre.nseg, st);
       if (e != cudaSuccess) rc = cuda_error(e, "memset(segflag)");
     }
+    if (!rc && a.mis_o) {
+      e = cudaMemsetAsync(a.mis_o, 0, (size_t)g->n, st);
+      if (e != cudaSuccess) rc = cuda_error(e, "memset(mis_o)");
+    }
     if (!rc)
       rc = launch_priorities(g, pre.H, pre.seed, pre.scale_bits, ws.prio, ws.q, ws.state, ws.next,
                              pre.seg_mode ? ws.segflag : nullptr, pre.T, ws.ctrl, &pre.c0,
-                             ws.rounds, ws.round_cap);
+                             ws.rounds, ws.round_cap, a.off, a.perm, a.mis_o);
     e = cudaStreamEndCapture(st, &captured);
     if (!rc && e != cudaSuccess) rc = cuda_error(e, "cudaStreamEndCapture(pre)");
   }
@@ -837,14 +880,16 @@ int ensure_solve_graph(tcmis_graph *g, const RoundArgs &a, const SolvePre &pre) 
     e = cudaStreamBeginCaptureToGraph(st, graph, &node, nullptr, 1, cudaStreamCaptureModeRelaxed);
     if (e != cudaSuccess) rc = cuda_error(e, "cudaStreamBeginCaptureToGraph(post)");
     if (!rc) {
-      const bool tail_packs = a.tail_thr > 0 && pre.seg_mode != 2;
-      if (a.tail_thr > 0) {
-        rc = launch_tail(g, a, tail_packs ? ws.d_res : nullptr);
-      } else {
+      const bool gather = a.perm && !a.mis_o;  // no fused compaction (tail.cuh)
+      const bool tail_packs = a.tail_thr > 0 && pre.seg_mode != 2 && !gather;
+      if (a.tail_thr > 0) rc = launch_tail(g, a, tail_packs ? ws.d_res : nullptr);
+      if (!rc && (a.tail_thr == 0 || gather)) {
         thrust::counting_iterator<int32_t> ids(0);
         size_t bytes = ws.cub_bytes;
-        e = cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count, (int)g->n,
-                                  IsInMIS{ws.state}, st);
+        e = gather ? cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
+                                           (int)g->n, IsInMISInv{ws.state, g->d_inv}, st)
+                   : cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
+                                           (int)g->n, IsInMIS{a.mis_o ? a.mis_o : ws.state}, st);
         if (e != cudaSuccess) rc = cuda_error(e, "MIS compaction");
       }
       if (!rc && pre.seg_mode == 2) {
@@ -955,6 +1000,25 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   tcmis_config cfg_local = *cfg;
   if (!tiled) cfg_local.observer = nullptr;
   cfg = &cfg_local;
+  // an internal vertex order (order.cu): the kernels run on the relabeled CSR
+  // (not for the observer, whose snapshots are in the caller's order, nor for
+  // the tile forms, whose store is built on the caller's CSR)
+  const bool tile_form =
+      cfg->exclusion == TCMIS_EXCL_TILE_BITS || cfg->exclusion == TCMIS_EXCL_TILE_MMA;
+  const bool relabel = g->d_perm && !cfg->observer && !tile_form;
+  const int64_t *s_off = relabel ? g->d_roff : g->d_off;
+  const int32_t *s_nbr = relabel ? g->d_rnbr : g->d_nbr;
+  const int32_t *s_perm = relabel ? g->d_perm : nullptr;
+  // the caller-order membership plane: kept while it stays L2-resident next
+  // to the gathered vectors (R-MAT s26's 67 MB plane cost its select kernels
+  // more in scattered stores, 3.45 -> 3.56 ms, than the gather compaction)
+  int64_t mis_o_max = kMisOMax;
+  if (const char *env = std::getenv("TCMIS_MIS_O_MAX")) mis_o_max = std::atoll(env);  // test hook
+  const bool use_mis_o = relabel && (int64_t)g->n <= mis_o_max;
+  if (use_mis_o && !ws.mis_o)
+    if (int rc = dev_alloc(&ws.mis_o, (size_t)g->n + 16)) return rc;  // uint4 reads past n
+  uint8_t *s_mis_o = use_mis_o ? ws.mis_o : nullptr;
+  ws.relabeled = relabel;
 
   if (timing) timeline_begin(ctx);
   uint8_t *seg0 = seg_mode ? ws.segflag : nullptr;
@@ -972,8 +1036,10 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   // the control block + zeroed statistics ring (k_tail accumulates into it)
   auto launch_pre = [&]() -> int {
     if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
+    if (s_mis_o) TCMIS_CUDA(cudaMemsetAsync(s_mis_o, 0, (size_t)g->n, st));
     return launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio, ws.q, ws.state, ws.next,
-                             seg0, T > 0 ? T : 1, ws.ctrl, &c0, ws.rounds, ws.round_cap);
+                             seg0, T > 0 ? T : 1, ws.ctrl, &c0, ws.rounds, ws.round_cap, s_off,
+                             s_perm, s_mis_o);
   };
   if (step)
     if (int rc = launch_pre()) return rc;
@@ -981,8 +1047,10 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   RoundArgs a;
   std::memset(&a, 0, sizeof(a));
   a.n = g->n;
-  a.off = g->d_off;
-  a.nbr = g->d_nbr;
+  a.off = s_off;
+  a.nbr = s_nbr;
+  a.perm = s_perm;
+  a.mis_o = s_mis_o;
   a.T = T > 0 ? T : 1;
   a.seg_mode = seg_mode;
   a.nseg = nseg;
@@ -992,9 +1060,9 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   a.seed = cfg->seed;
   a.sel_grid = ctx->num_sms * 8;
   a.upd_grid = ctx->num_sms * 4;
-  a.nz = g->d_nz;
-  a.vnnz = ((uintptr_t)g->d_nbr & 15) == 0 ? g->nnz : -g->nnz;
-  a.nz_count = g->nz_count;
+  a.nz = relabel ? g->d_rnz : g->d_nz;
+  a.vnnz = ((uintptr_t)s_nbr & 15) == 0 ? g->nnz : -g->nnz;
+  a.nz_count = relabel ? g->rnz_count : g->nz_count;
   // exclusion form: pull on degree-skewed graphs, where the
   // neighbours of candidates concentrate on hubs and early-exit pulls are
   // cheap; push elsewhere.  Both produce the same next[] decisions.
@@ -1044,8 +1112,12 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     if (!tail_compacted) {
       thrust::counting_iterator<int32_t> ids(0);
       size_t bytes = ws.cub_bytes;
-      TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
-                                       (int)g->n, IsInMIS{ws.state}, st));
+      if (a.perm && !a.mis_o)
+        TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
+                                         (int)g->n, IsInMISInv{ws.state, g->d_inv}, st));
+      else
+        TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
+                                         (int)g->n, IsInMIS{a.mis_o ? a.mis_o : ws.state}, st));
       ctx->launches += 1;
     }
     TCMIS_CUDA(cudaMemcpyAsync(&ws.h_misc[0], ws.mis_count, sizeof(int64_t),
@@ -1098,9 +1170,10 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       const int mr = hr.ctrl.main_rounds;
       // k_priorities, the rounds, the tail (or cub's compaction), and k_pack
       // unless the tail packed (h3 adds k_seg_total)
-      const bool tail_packs = a.tail_thr > 0 && seg_mode != 2;
+      const bool gather = a.perm && !a.mis_o;
+      const bool tail_packs = a.tail_thr > 0 && seg_mode != 2 && !gather;
       ctx->launches += 2 + launches_per_round(a) * (int64_t)mr + (seg_mode == 2 ? 1 : 0) +
-                       (tail_packs ? 0 : 1);
+                       (tail_packs ? 0 : 1) + (gather && a.tail_thr > 0 ? 1 : 0);
       const int pre_n = std::min(rr, std::min(ws.round_cap, 64));
       rounds_h.assign(hr.rounds, hr.rounds + pre_n);
       if (rr > pre_n) {
@@ -1147,7 +1220,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       if (a.tail_thr > 0 && ws.h_ctrl->alive <= a.tail_thr) {
         ctx->rec_round = round + 1;
         if (int rc = launch_tail(g, a)) return rc;
-        tail_compacted = true;
+        tail_compacted = !(a.perm && !a.mis_o);
         TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
         TCMIS_CUDA(cudaStreamSynchronize(st));
         const int rr = ws.h_ctrl->round - 1;
@@ -1266,6 +1339,17 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     stats[r] = s;
   }
   *n_iter = rounds_run;
+  return 0;
+}
+
+int states_in_caller_order(tcmis_graph *g) {
+  Workspace &ws = g->ws;
+  if (!ws.relabeled || !g->d_inv) return 0;
+  if (!ws.state_o)
+    if (int rc = dev_alloc(&ws.state_o, (size_t)g->n + 16)) return rc;
+  k_unpermute<<<grid_for(g->ctx, g->n, 256, 8), 256, 0, g->ctx->stream>>>(g->n, g->d_inv,
+                                                                          ws.state, ws.state_o);
+  TCMIS_LAUNCHED(g->ctx);
   return 0;
 }
 

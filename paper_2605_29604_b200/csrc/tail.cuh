@@ -139,6 +139,10 @@ struct TailArgs {
   int64_t *mis_count;
   unsigned *warpcnt;        // 2 x kTailMaxWarps per-warp InMIS counts, by solve parity
   HostRes *pack;            // non-null: also leave the solve's results in mapped host memory
+  const int32_t *perm;      // solve id -> caller id (relabeled graphs), else null;
+  uint8_t *mis_o;           // ... and, when kept, the membership in the caller's
+                            // order, which the count pass and the compaction
+                            // stream instead of the solve-order states
 };
 
 // Grid barrier whose arrival also sums one value per block: bar[0..1] is a
@@ -199,9 +203,11 @@ __device__ __forceinline__ void tail_candidate(const TailArgs &a, int32_t v, uns
                                                int32_t wlen, unsigned long long &sel,
                                                int32_t *pend, int *npend) {
   a.state[v] = TCMIS_IN_MIS;
-  atomicAdd(&wcnt[v / wlen], 1u);
+  const int32_t o = orig_id(a.perm, v);
+  if (a.mis_o) a.mis_o[o] = TCMIS_IN_MIS;
+  if (!a.perm || a.mis_o) atomicAdd(&wcnt[o / wlen], 1u);
   ++sel;
-  const int32_t sb = seg_of(v, a.T);
+  const int32_t sb = seg_of(o, a.T);
   if (a.seg_mode == 2) {
     a.segflag[sb] = 1;
   } else if (a.seg_mode == 1) {
@@ -219,7 +225,9 @@ __device__ __forceinline__ bool tail_blocks(const TailArgs &a, int32_t u, uint32
   if (qu == 0) return false;
   alive = first || __ldcg(&a.xt[u]) != (uint16_t)tprev;  // no tag is tag(r0 - 1)
   if (!alive) return false;
-  return qu != qv ? qu > qv : key_of(__ldg(&a.prio[u]), u) > key_of(__ldg(&a.prio[v]), v);
+  if (qu != qv) return qu > qv;
+  const uint32_t pu = __ldg(&a.prio[u]), pv = __ldg(&a.prio[v]);
+  return pu != pv ? pu > pv : orig_id(a.perm, u) > orig_id(a.perm, v);
 }
 
 __device__ __forceinline__ bool tail_alive(const TailArgs &a, int32_t u, uint32_t tprev,
@@ -286,13 +294,14 @@ __device__ void compact_mis(const TailArgs &a, unsigned *wcnt, unsigned *wnext, 
   const WarpRange R = warp_range(a.n, nwarps, gw);
   int32_t *stg = stage + w * kCompactV;
   uint4 xn = make_uint4(0, 0, 0, 0);
+  const uint8_t *memb = a.mis_o ? a.mis_o : a.state;  // InMIS == 1 in both
   if (R.lo + lane * 16 < R.hi)
-    xn = __ldcg(reinterpret_cast<const uint4 *>(a.state + R.lo + lane * 16));
+    xn = __ldcg(reinterpret_cast<const uint4 *>(memb + R.lo + lane * 16));
   for (int64_t t0 = R.lo; t0 < R.hi; t0 += kCompactV) {
     const int64_t v0 = t0 + lane * 16;
     const uint4 x = xn;
     if (v0 + kCompactV < R.hi)
-      xn = __ldcg(reinterpret_cast<const uint4 *>(a.state + v0 + kCompactV));
+      xn = __ldcg(reinterpret_cast<const uint4 *>(memb + v0 + kCompactV));
     uint32_t m = 0;
     if (v0 < R.hi) {
       m = eq_mask16(x, TCMIS_IN_MIS);
@@ -385,12 +394,18 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
       s_q[threadIdx.x] = __ldcg(&a.q[v]);
     }
   }
-  {  // count pass: the per-round kernels' candidates in this warp's range
+  // the fused compaction runs in the caller's id order: on the states, or on
+  // a relabeled solve's caller-order membership; a relabeled solve without
+  // one compacts after the tail (solver.cu, a gather through the permutation)
+  const bool compact = !a.perm || a.mis_o;
+  if (compact) {  // count pass: the per-round kernels' candidates in this warp's range
+     // (next == 1, or the caller-order membership)
+    const uint8_t *cand = a.mis_o ? a.mis_o : a.next;
     const WarpRange R = warp_range(a.n, nwarps, blockIdx.x * kTailWarps + w);
     unsigned c = 0;
 #pragma unroll 4
     for (int64_t v0 = R.lo + lane * 16; v0 < R.hi; v0 += 32 * 16) {
-      uint32_t m = eq_mask16(__ldcg(reinterpret_cast<const uint4 *>(a.next + v0)), 1u);
+      uint32_t m = eq_mask16(__ldcg(reinterpret_cast<const uint4 *>(cand + v0)), 1u);
       const int64_t left = R.hi - v0;
       if (left < 16) m &= (1u << left) - 1u;
       c += __popc(m);
@@ -775,7 +790,11 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
     }
   }
   TAIL_MARK(4, 0);
-  compact_mis(a, wcnt, wnext, s_stage);
+  if (compact) {
+    compact_mis(a, wcnt, wnext, s_stage);
+  } else if (lane == 0) {
+    wnext[blockIdx.x * kTailWarps + w] = 0;  // the next solve's count buffer, as compact_mis does
+  }
   TAIL_MARK(7, 0);
   // The last block publishes the tail's rounds and packs the control block
   // and the ring for the host, once every block's counters are in.  Pass

@@ -69,6 +69,7 @@ struct UpdateArgs {
   int seg_mode;            // 0 none, 1 count + clear per round, 2 accumulate (h3)
   DevRound *rounds;
   int32_t tail_thr;        // the WHILE loop continues while alive > tail_thr
+  const int32_t *perm;     // solve id -> caller id (relabeled graphs), else null
 };
 
 // The end of a round, run by every block of the round's last kernel: the
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(kBlock)
         ++rem;
       } else {
         ++mine;
-        if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m);
+        if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m, a.perm);
       }
     }
     int pos, total;
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
         ++rem;
       } else if (e - s <= kPullK) {
         survive = true;
-        if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m);
+        if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m, a.perm);
       } else {
         undecided = true;
       }
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
         mode = kFetch;
       } else if (hi <= s) {
         survive = true;
-        if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m);
+        if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m, a.perm);
         mode = kFetch;
       } else if (e - hi >= kThreadMax) {
         defer = true;
@@ -399,7 +400,7 @@ __global__ void __launch_bounds__(kBlock)
       publish(a.pub, v);
       ++rem;
     } else {
-      if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m);
+      if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m, a.perm);
       out[atomicAdd(&ctrl->wl_count[out_slot], 1)] = v;
     }
   };

@@ -1,0 +1,113 @@
+"""GPU: an internal vertex order (tcmis_graph_reorder, csrc/order.cu) changes
+nothing a caller sees.  The kernels run on a relabeled CSR, but keys, hash
+priorities and tile counters stay on the caller's ids, so MIS membership,
+|MIS|, the iteration count and every per-iteration statistic equal the
+oracle's (and therefore the direct solve's) for every heuristic, both
+exclusion forms, graph and host-loop drivers, and any tail switch point."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2605_29604_b200 as tc
+
+pytestmark = pytest.mark.gpu
+
+HEUR = {"h1": tc.Heuristic.H1, "h2": tc.Heuristic.H2, "h3": tc.Heuristic.H3,
+        "luby-fresh": tc.Heuristic.LubyFresh, "luby-perm": tc.Heuristic.LubyPerm}
+
+
+def rounds_tuple(its):
+    return [(i.candidates_selected, i.vertices_removed, i.alive_remaining, i.tiles_evaluated,
+             i.tiles_skipped) for i in its]
+
+
+def oracle_tuple(s):
+    return [(r["sel"], r["rem"], r["alive"], r["tiles_eval"], r["tiles_skip"]) for r in s.rounds]
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return tc.Context(0)
+
+
+def _orders(g, rng):
+    yield "degree", tc.DeviceGraph.ORDER_DEGREE, None
+    yield "random", tc.DeviceGraph.ORDER_GIVEN, rng.permutation(g.n).astype(np.int32)
+    yield "reverse", tc.DeviceGraph.ORDER_GIVEN, np.arange(g.n - 1, -1, -1, dtype=np.int32)
+
+
+@pytest.mark.parametrize("kind,args", [("rmat", (12, 16, 3)), ("gnp_avg", (3000, 12.0, 2)),
+                                       ("grid", (45,)), ("rmat", (10, 4, 7))])
+@pytest.mark.parametrize("thr", [None, "0", "1000000000"])
+@pytest.mark.parametrize("plane", [None, "0"])
+def test_reordered_solves_equal_the_reference(ctx, kind, args, thr, plane, monkeypatch):
+    """plane: the caller-order membership plane (None: kept, as for every
+    graph up to 48M vertices) or "0" (never kept: the compaction gathers
+    through the permutation, as at R-MAT s26)."""
+    if thr is not None:
+        monkeypatch.setenv("TCMIS_TAIL_THRESHOLD", thr)
+    if plane is not None:
+        monkeypatch.setenv("TCMIS_MIS_O_MAX", plane)
+    g = O.gen(kind, *args)
+    rng = np.random.default_rng(5)
+    for name, mode, order in _orders(g, rng):
+        dg = tc.DeviceGraph.upload(tc.Graph(g.n, g.off, g.nbr), ctx).reorder(mode, order)
+        for heur in ("h2", "h1", "h3", "luby-fresh", "luby-perm"):
+            exp = O.solve(g, heur, 3, tile_dim=16)
+            for excl in (tc.Exclusion.PUSH, tc.Exclusion.CSR_PULL):
+                for host_loop in (False, True):
+                    got = tc.run_mis(dg, tc.EngineConfig(heuristic=HEUR[heur], seed=3,
+                                                         exclusion=excl, host_loop=host_loop))
+                    where = (kind, name, heur, excl, host_loop)
+                    assert np.array_equal(got.mis, exp.mis), where
+                    assert rounds_tuple(got.iterations) == oracle_tuple(exp), where
+                    assert np.array_equal(got.state == 1, exp.state == 1), where
+        dg.close()
+
+
+def test_spatial_order_of_the_rgg(ctx):
+    """tcmis_gen_rgg keeps its points' Z-order; solving on it is bit-exact."""
+    dg = tc.DeviceGraph.rgg(20000, 3.0, 1, ctx)
+    g = dg.download()
+    og = O.Graph(g.n, g.offsets, g.neighbors)
+    dg.reorder(tc.DeviceGraph.ORDER_SPATIAL)
+    for heur in ("h2", "h3", "h1"):
+        exp = O.solve(og, heur, 1, tile_dim=16)
+        got = tc.run_mis(dg, tc.EngineConfig(heuristic=HEUR[heur], seed=1))
+        assert np.array_equal(got.mis, exp.mis), heur
+        assert rounds_tuple(got.iterations) == oracle_tuple(exp), heur
+    # back to the caller's order: still the same
+    dg.reorder(tc.DeviceGraph.ORDER_NONE)
+    got = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=1))
+    assert np.array_equal(got.mis, O.solve(og, "h2", 1, tile_dim=16).mis)
+    dg.close()
+
+
+def test_observer_and_tile_forms_ignore_the_order(ctx):
+    g = O.gen("rmat", 11, 16, 1)
+    dg = tc.DeviceGraph.upload(tc.Graph(g.n, g.off, g.nbr), ctx).reorder(tc.DeviceGraph.ORDER_DEGREE)
+    exp = O.solve(g, "h2", 1, tile_dim=16)
+    seen = []
+    got = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=1,
+                                         iteration_observer=lambda it, c, s: seen.append(it)))
+    assert np.array_equal(got.mis, exp.mis)
+    assert seen == list(range(1, exp.n_rounds + 1))
+    for excl in (tc.Exclusion.TILE_BITS, tc.Exclusion.TILE_MMA):
+        got = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=1, exclusion=excl))
+        assert rounds_tuple(got.iterations) == oracle_tuple(exp)
+    dg.close()
+
+
+def test_order_errors(ctx):
+    g = O.gen("rmat", 9, 8, 1)
+    dg = tc.DeviceGraph.upload(tc.Graph(g.n, g.off, g.nbr), ctx)
+    with pytest.raises(ValueError, match="permutation"):
+        dg.reorder(tc.DeviceGraph.ORDER_GIVEN, np.zeros(g.n, np.int32))
+    with pytest.raises(ValueError, match="tcmis_gen_rgg"):
+        dg.reorder(tc.DeviceGraph.ORDER_SPATIAL)
+    with pytest.raises(ValueError):
+        dg.reorder(9)
+    # a failed reorder leaves the graph usable in the caller's order
+    got = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=1))
+    assert np.array_equal(got.mis, O.solve(g, "h2", 1, tile_dim=16).mis)
+    dg.close()
