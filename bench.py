@@ -52,6 +52,10 @@ CONFIGS = {
     "rgg": {"workload": "random geometric graph n=24M avg degree ~3 (integer lattice, ids in "
                         "draw order)"},
     "rmat26": {"workload": "R-MAT scale 26 edge factor 16 (rmat_graph(26,16,1))"},
+    # not a BASELINE config: the RGG with its ids in the generator's spatial
+    # (Z-order) order, for the tile-format experiments (8.4 nnz / 16x16 tile)
+    "rgg_spatial_ids": {"workload": "random geometric graph n=24M avg degree ~3, ids in "
+                                    "spatial Z-order (tcmis_graph_permuted)"},
 }
 HEUR = {"h1": 0, "h2": 1, "h3": 2, "luby-fresh": 3, "luby-perm": 4}
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -144,6 +148,11 @@ def make_device_graph(tc, name: str, ctx):
         return tc.DeviceGraph.rgg(24_000_000, 3.0, 1, ctx)
     if name == "rmat26":
         return tc.DeviceGraph.rmat(26, 16, 1, ctx)
+    if name == "rgg_spatial_ids":
+        g = tc.DeviceGraph.rgg(24_000_000, 3.0, 1, ctx).reorder(tc.DeviceGraph.ORDER_SPATIAL)
+        p = g.permuted()
+        g.close()
+        return p
     raise ValueError(name)
 
 
@@ -199,7 +208,13 @@ def run_ours(args) -> dict:
     excl = {"auto": tc.Exclusion.AUTO, "push": tc.Exclusion.PUSH,
             "pull": tc.Exclusion.CSR_PULL, "tile-bits": tc.Exclusion.TILE_BITS,
             "tile-mma": tc.Exclusion.TILE_MMA}[args.exclusion]
-    cfg = tc.EngineConfig(heuristic=HEUR[args.heuristic], seed=1, tile_dim=16, exclusion=excl)
+    cand_flags = tc.F_TILE_CAND if args.candidates == "tile" else 0
+    cfg = tc.EngineConfig(heuristic=HEUR[args.heuristic], seed=1, tile_dim=16, exclusion=excl,
+                          flags=cand_flags)
+    tile_cand_build = None
+    if cand_flags:  # A-up store: per priority configuration, outside the timed region
+        ms_b, up_tiles = dg.tile_cand_prepare(cfg)
+        tile_cand_build = {"ms": round(ms_b, 3), "a_up_tiles": up_tiles}
     c_cfg, _keep = cfg._c()
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")  # > 126 MB L2
@@ -269,7 +284,7 @@ def run_ours(args) -> dict:
     # ---- kernel roofline: per-kernel CUDA events around every launch of a
     # step-wise solve (same kernels as the graph; TCMIS_F_TIMING)
     cfg_t = tc.EngineConfig(heuristic=HEUR[args.heuristic], seed=1, tile_dim=16, timing=True,
-                            exclusion=excl)
+                            exclusion=excl, flags=cand_flags)
     runs = []
     for _ in range(max(3, min(args.steps, 5))):
         tc.run_mis(dg, cfg_t)
@@ -298,13 +313,26 @@ def run_ours(args) -> dict:
                    "iterations": iters, "mis_size": mis_count, "tiles_t16": tiles,
                    "parallelism": "replicas" if world > 1 else "single",
                    "l2": "256 MB flush between steps; CSR > L2",
-                   "vertex_order": args.order, "vertex_order_ms": order_ms},
+                   "vertex_order": args.order, "vertex_order_ms": order_ms,
+                   "candidates": args.candidates, "exclusion": args.exclusion,
+                   "tile_cand_build": tile_cand_build},
         "mis_ms": round(ms_per_step, 4),
         "device_resident": device_resident,
         "kernels_ms": [[k, r, round(ms, 4)] for k, r, ms in kernels],
         "roofline": roofline, "e2e": e2e, "clocks": clk.summary(),
         "gpu_launches": launches,
     }
+    if rank == 0 and not args.no_k1:
+        try:
+            line["k1_tile_conversion"] = k1_timing(tc, dg, ctx)
+            ref = {"rmat22": 47302.1}.get(args.config)
+            if ref:
+                line["k1_tile_conversion"]["reference_tile_graph_ms"] = ref
+                line["k1_tile_conversion"]["reference_source"] = (
+                    "tests/golden/rmat22_ef16.json tile_graph_ms (the reference's serial "
+                    "tile_graph, tiling.cpp:44-84)")
+        except Exception as e:
+            line["k1_tile_conversion"] = {"error": str(e)[:200]}
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(dg, args)
     if dist:
@@ -331,7 +359,8 @@ def timeline(tc, ctx):
 # also scans the pull exclusion's longest rows but is booked as Phase 3
 PHASE = {"k_probe_select": 1, "k_select": 1, "k_select_long": 1,
          "k_probe_pull": 2, "k_update_pull": 2, "k_tile_excl_bits": 2, "k_tile_excl_mma": 2,
-         "k_update": 3, "k_round_end": 3, "k_priorities": 0, "k_tail": 4}
+         "k_update": 3, "k_round_end": 3, "k_priorities": 0, "k_tail": 4,
+         "k_alive_bits": 1, "k_tile_cand_bits": 1, "k_tile_mark": 1}
 PHASE_NAME = {0: "init (priorities, states)", 1: "Phase 1 candidate detection",
               2: "Phase 2 neighbour exclusion (SpMV)", 3: "Phase 3 state update + compaction",
               12: "Phases 1+2 (push exclusion fused into candidate detection)",
@@ -518,6 +547,81 @@ def run_e2e(tc, torch, dg, ctx, stream, cfg, args, local, dist, flush):
             "d2h_bytes_per_step": int(4 * cnt + 64 * 4096), "steps": steps,
             "path": "tcmis_graph_upload_tiled (upload with the K1 tile count overlapped) + "
                     "tcmis_solve (host buffers)"}
+
+
+def k1_timing(tc, dg, ctx, reps: int = 3) -> dict:
+    """The CSR -> tile converter (tile_graph, tiling.cpp:44-84, K1) on the
+    device, each part on a fresh handle over the same device CSR
+    (tcmis_graph_wrap_device: no cached tiling), wall clock around the
+    synchronous call, median of `reps`:
+      * count: the tile counts per block row the solve's counters use;
+      * compact store: the T = 16 store of the tile-form kernels (36 B/tile);
+      * reference layout: the full TiledAdjacency (136 B/tile: 16 u64 rows +
+        row / column) built on the device and copied to host memory.
+    Bytes: CSR read (8 B/row + 4 B/entry) + tile bytes written; the roofline
+    fraction is against the HBM peak (the export also crosses PCIe)."""
+    import numpy as np
+    L = tc.load()
+    hbm, _ = peaks()
+    n, nnz = dg.n, dg.nnz
+    csr_b = 8 * (n + 1) + 4 * nnz
+    d_off, d_nbr = dg.device_offsets(), dg.device_neighbors()
+
+    def fresh():
+        h = C.c_void_p()
+        tc._check(L.tcmis_graph_wrap_device(ctx.h, n, nnz, C.c_void_p(d_off), C.c_void_p(d_nbr),
+                                            C.byref(h)))
+        return h
+
+    def timed(fn):
+        ts = []
+        for _ in range(reps):
+            h = fresh()
+            ctx.synchronize()
+            t0 = time.perf_counter()
+            out = fn(h)
+            t1 = time.perf_counter()
+            L.tcmis_graph_destroy(h)
+            ts.append((t1 - t0) * 1e3)
+        return sorted(ts)[len(ts) // 2], out
+
+    cnt = C.c_int64(0)
+    ms_count, _ = timed(lambda h: tc._check(L.tcmis_graph_tile(h, 16, C.byref(cnt))))
+    tiles = int(cnt.value)
+    st_cnt = C.c_int64(0)
+    ms_store, _ = timed(lambda h: tc._check(L.tcmis_graph_tile_store(h, 16, C.byref(st_cnt), None,
+                                                                    None, None)))
+    out = {"tiles_t16": tiles,
+           "count": {"ms": round(ms_count, 3), "bytes": csr_b,
+                     "gbs": round(csr_b / (ms_count * 1e-3) / 1e9, 1),
+                     "frac": round(csr_b / (ms_count * 1e-3) / 1e9 / hbm, 4)},
+           "compact_store": {"ms": round(ms_store, 3), "bytes": csr_b + 36 * tiles,
+                             "gbs": round((csr_b + 36 * tiles) / (ms_store * 1e-3) / 1e9, 1),
+                             "frac": round((csr_b + 36 * tiles) / (ms_store * 1e-3) / 1e9 / hbm, 4)}}
+    ref_bytes = 136 * tiles
+    try:
+        import psutil
+        room = psutil.virtual_memory().available
+    except Exception:
+        room = 0
+    if room > 3 * ref_bytes:
+        nb = (n + 15) // 16
+        tr = np.empty(max(tiles, 1), np.int32)
+        tcol = np.empty(max(tiles, 1), np.int32)
+        rb = np.empty(max(tiles * 16, 1), np.uint64)
+        bro = np.empty(nb + 1, np.int64)
+        tr[:] = 0  # fault the pages in outside the timed call
+        tcol[:] = 0
+        rb[:] = 0
+        ms_exp, _ = timed(lambda h: tc._check(L.tcmis_graph_export_tiles(
+            h, 16, tc._ptr(tr), tc._ptr(tcol), tc._ptr(rb), tc._ptr(bro))))
+        out["reference_layout"] = {"ms": round(ms_exp, 3), "bytes_written": ref_bytes,
+                                   "gbs": round(ref_bytes / (ms_exp * 1e-3) / 1e9, 1),
+                                   "note": "device merge + copy of the tiles to host memory"}
+        del tr, tcol, rb, bro
+    else:
+        out["reference_layout"] = {"skipped": f"needs {3 * ref_bytes >> 30} GB of host memory"}
+    return out
 
 
 def run_cpp_dropin(dg, args, want_mis: int) -> dict | None:
@@ -988,6 +1092,9 @@ def main():
     ap.add_argument("--no-single", action="store_true",
                     help="N > 1: skip rank 0's single-GPU solve of the same graph")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-k1", action="store_true", help="skip the tile-converter timings")
+    ap.add_argument("--candidates", default="csr", choices=["csr", "tile"],
+                    help="Phase 1 form: CSR scan engines or A-up tiles x alive bitmap")
     ap.add_argument("--heuristic", default="h2", choices=list(HEUR))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--order", default="auto", choices=["auto", "none", "degree", "spatial"],

@@ -93,6 +93,14 @@ typedef struct tcmis_config {
 /* tcmis_solve_partitioned: mis_out / state_out cover this rank's rows only
  * (its share of a distributed result) instead of all n vertices */
 #define TCMIS_F_OWN_RANGE 0x4u
+/* Phase 1 as a tile x bit-vector product: the oriented adjacency A-up (u in
+ * N(v) with key(u) > key(v)) in the compact T = 16 tile store times
+ * the round's alive bitmap (csrc/tile_cand.cu), with the tile-form exclusion
+ * (TCMIS_EXCL_TILE_MMA stays MMA, anything else becomes TILE_BITS).  A-up
+ * depends on the priorities: it is built on first use per (heuristic, seed,
+ * scale_bits) and cached on the graph (tcmis_graph_tile_cand_prepare builds
+ * it ahead).  Not for luby-fresh (its keys change every round). */
+#define TCMIS_F_TILE_CAND 0x8u
 /* test hook: start the solve from a control block that disagrees with the
  * vertex states; the device's round invariant check must then fail the solve
  * with TCMIS_E_LOGIC (the reference's logic_error, engine.cpp:152-153) */
@@ -180,6 +188,9 @@ int tcmis_graph_export_tiles(tcmis_graph *g, int32_t tile_dim, int32_t *tile_row
 enum { TCMIS_ORDER_NONE = 0, TCMIS_ORDER_DEGREE = 1, TCMIS_ORDER_SPATIAL = 2,
        TCMIS_ORDER_GIVEN = 3 };
 int tcmis_graph_reorder(tcmis_graph *g, int32_t mode, const int32_t *order);
+/* A new graph whose ids ARE the order's solve ids (the relabeled CSR as an
+ * ordinary graph, e.g. an RGG with spatially ordered ids). */
+int tcmis_graph_permuted(tcmis_graph *g, tcmis_graph **out);
 
 /* The compact device tile store the tile-form exclusion kernels read
  * (tile_dim 8 or 16; same tile set and order as tile_graph, tiling.cpp:44-84):
@@ -188,6 +199,12 @@ int tcmis_graph_reorder(tcmis_graph *g, int32_t mode, const int32_t *order);
  * T bits per tile: u16 rows for T = 16, u8 rows for T = 8) to the host. */
 int tcmis_graph_tile_store(tcmis_graph *g, int32_t tile_dim, int64_t *tile_count,
                            int64_t *block_row_offsets, int32_t *tile_col, void *payload);
+
+/* Build (or find cached) the A-up tile store TCMIS_F_TILE_CAND solves with
+ * cfg's priorities use; *build_ms = device time of the orientation + tiling
+ * (0 when cached), *tiles = its tile count. */
+int tcmis_graph_tile_cand_prepare(tcmis_graph *g, const tcmis_config *cfg, double *build_ms,
+                                  int64_t *tiles);
 
 /* validate.cpp:45-75 check_independence + check_maximality on the device, in
  * one pass, with the reference's witnesses: *independent (else the violating

@@ -100,6 +100,7 @@ class _Config(C.Structure):
 F_TIMING = 0x1
 F_HOST_LOOP = 0x2
 F_OWN_RANGE = 0x4
+F_TILE_CAND = 0x8  # Phase 1 as A-up tiles x alive bitmap (csrc/tile_cand.cu)
 F_DEBUG_CORRUPT = 0x100  # test hook (include/tcmis_b200.h)
 
 
@@ -152,6 +153,8 @@ def load():
         "tcmis_free": (None, [vp]),
         "tcmis_rgg_radius": (u64, [i32, C.c_double]),
         "tcmis_graph_reorder": (C.c_int, [vp, i32, vp]),
+        "tcmis_graph_permuted": (C.c_int, [vp, P(vp)]),
+        "tcmis_graph_tile_cand_prepare": (C.c_int, [vp, P(_Config), P(C.c_double), P(i64)]),
         "tcmis_nccl_unique_id": (C.c_int, [vp]),
         "tcmis_exchange_nccl": (C.c_int, [vp, i32, i32, vp, P(vp)]),
         "tcmis_exchange_nccl_comm": (C.c_int, [vp, P(vp)]),
@@ -437,6 +440,21 @@ class DeviceGraph:
         o = None if order is None else np.ascontiguousarray(order, np.int32)
         _check(load().tcmis_graph_reorder(self.h, int(mode), _ptr(o)))
         return self
+
+    def permuted(self) -> "DeviceGraph":
+        """A new graph whose ids are this graph's internal order (tcmis_graph_permuted)."""
+        h = C.c_void_p()
+        _check(load().tcmis_graph_permuted(self.h, C.byref(h)))
+        return DeviceGraph(h, self.ctx)
+
+    def tile_cand_prepare(self, cfg: "EngineConfig") -> tuple:
+        """The A-up tile store of cfg's priorities (TCMIS_F_TILE_CAND):
+        (build ms, 0 when cached; tile count)."""
+        c, _k = cfg._c()
+        ms, tiles = C.c_double(0), C.c_int64(0)
+        _check(load().tcmis_graph_tile_cand_prepare(self.h, C.byref(c), C.byref(ms),
+                                                   C.byref(tiles)))
+        return float(ms.value), int(tiles.value)
 
     def tile(self, tile_dim: int = 16) -> int:
         cnt = C.c_int64(0)

@@ -30,7 +30,7 @@ NVCC_FLAGS = ARCH + [
     "-I", INC, "-I", CSRC,
 ] + os.environ.get("TCMIS_NVCC_EXTRA", "").split()
 CU_SOURCES = ["capi.cu", "solver.cu", "tiles.cu", "gen.cu", "tiled_spmv.cu", "dist.cu",
-              "partitioned.cu", "staging.cu", "order.cu", "validate.cu"]
+              "partitioned.cu", "staging.cu", "order.cu", "tile_cand.cu", "validate.cu"]
 CXX_SOURCES = ["engine.cpp"]
 
 

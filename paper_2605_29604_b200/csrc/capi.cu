@@ -5,6 +5,7 @@
 // launches only sm_100a kernels from this library.  There is deliberately no
 // CPU fallback: without a usable CUDA device every compute call fails with
 // TCMIS_E_CUDA.
+#include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -258,6 +259,7 @@ TCMIS_API void tcmis_graph_destroy(tcmis_graph *g) {
   free_dist(g);
   free_partitioned(g);
   free_order(g);
+  free_up_store(g);
   dev_free(g->d_spatial);
   free_tile_store(g);
   Workspace &sp = g->ctx->spare;
@@ -422,6 +424,61 @@ TCMIS_API int tcmis_solve_device(tcmis_graph *g, const tcmis_config *cfg, const 
     *d_state = g->ws.relabeled ? g->ws.state_o : g->ws.state;
   }
   return 0;
+}
+
+TCMIS_API int tcmis_graph_tile_cand_prepare(tcmis_graph *g, const tcmis_config *cfg,
+                                            double *build_ms, int64_t *tiles) {
+  NEED(g && cfg, "null handle");
+  if (cfg->heuristic < TCMIS_H1 || cfg->heuristic > TCMIS_LUBY_PERM ||
+      cfg->heuristic == TCMIS_LUBY_FRESH)
+    return set_error(TCMIS_E_INVALID_ARGUMENT, "the A-up store needs fixed priorities");
+  if (cfg->heuristic != TCMIS_H1 && (cfg->scale_bits < 8 || cfg->scale_bits > 30))
+    return set_error(TCMIS_E_INVALID_ARGUMENT, "scale_bits must be in [8, 30]");
+  ENTER(g->ctx);
+  const int64_t key[3] = {cfg->heuristic, (int64_t)cfg->seed, cfg->scale_bits};
+  double ms = 0;
+  if (g->n > 0)
+    if (int rc = tile_cand_prepare(g, cfg->heuristic, cfg->seed, cfg->scale_bits, key, &ms))
+      return rc;
+  if (build_ms) *build_ms = ms;
+  if (tiles) *tiles = g->up_tiles;
+  return 0;
+}
+
+TCMIS_API int tcmis_graph_permuted(tcmis_graph *g, tcmis_graph **out) {
+  NEED(g && out, "null handle");
+  NEED(g->d_perm || g->n == 0, "tcmis_graph_reorder first");
+  ENTER(g->ctx);
+  int64_t *off = nullptr;
+  int32_t *nbr = nullptr;
+  if (int rc = dev_alloc(&off, (size_t)g->n + 1)) return rc;
+  if (int rc = dev_alloc(&nbr, (size_t)std::max<int64_t>(g->nnz, 1))) return rc;
+  cudaStream_t st = g->ctx->stream;
+  if (g->n) {
+    TCMIS_CUDA(cudaMemcpyAsync(off, g->d_roff, 8ull * (g->n + 1), cudaMemcpyDeviceToDevice, st));
+    if (g->nnz)
+      TCMIS_CUDA(cudaMemcpyAsync(nbr, g->d_rnbr, 4ull * g->nnz, cudaMemcpyDeviceToDevice, st));
+  } else {
+    TCMIS_CUDA(cudaMemsetAsync(off, 0, 8, st));
+  }
+  if (g->nnz && g->n) {
+    // rows ascending again (graph.hpp:21 Graph invariant; the tilings merge
+    // sorted rows): a segmented sort of the relabeled rows
+    int32_t *sorted = nullptr;
+    if (int rc = dev_alloc(&sorted, (size_t)g->nnz)) return rc;
+    size_t bytes = 0;
+    cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, nbr, sorted, g->nnz, g->n, off, off + 1, st);
+    void *tmp = nullptr;
+    if (int rc = dev_alloc((char **)&tmp, bytes)) return rc;
+    TCMIS_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp, bytes, nbr, sorted, g->nnz, g->n, off,
+                                                  off + 1, st));
+    g->ctx->launches++;
+    dev_free(tmp);
+    dev_free(nbr);
+    nbr = sorted;
+  }
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  return wrap_owned(g->ctx, g->n, g->nnz, off, nbr, out);
 }
 
 TCMIS_API int tcmis_graph_reorder(tcmis_graph *g, int32_t mode, const int32_t *order) {

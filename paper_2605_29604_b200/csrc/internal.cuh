@@ -137,6 +137,8 @@ struct Workspace {
   cudaGraphExec_t exec = nullptr;  // cached WHILE{select; update} graph
   uint32_t *cbits = nullptr;      // tile exclusion: this round's candidates, bit per vertex
   uint32_t *tile_hit = nullptr;   // tile exclusion: per T=16 block row, rows with a candidate nbr
+  uint32_t *alive_bits = nullptr; // tile Phase 1: the round's alive set, bit per vertex
+  uint32_t *blocked = nullptr;    // tile Phase 1: per T=16 block row, rows with an alive higher nbr
   alignas(8) unsigned char graph_key[512] = {};
 };
 
@@ -214,6 +216,14 @@ struct tcmis_graph {
   int32_t *d_rnz = nullptr;   // non-isolated solve ids, ascending
   int32_t rnz_count = 0;
   int32_t *d_spatial = nullptr;  // tcmis_gen_rgg's points in Z-order of their cells
+  // Phase 1 tile form (tile_cand.cu): the A-up store of one priority
+  // configuration (heuristic, seed, scale_bits)
+  int64_t up_key[3] = {-1, -1, -1};
+  int64_t up_tiles = 0;
+  int32_t *d_up_trow = nullptr;
+  int32_t *d_up_tcol = nullptr;
+  uint16_t *d_up_tbits = nullptr;
+  double up_build_ms = 0;
   tcmis_b200::Workspace ws;
 };
 
@@ -290,6 +300,12 @@ struct RoundArgs {
   const int32_t *trow;
   const int32_t *tcol;
   const uint16_t *tbits;
+  int tile_cand;        // Phase 1 as A-up tiles x alive bitmap (tile_cand.cu) ...
+  int32_t tile_gate;    // ... in the rounds starting with >= tile_gate alive
+  int64_t up_tiles;
+  const int32_t *up_trow;
+  const int32_t *up_tcol;
+  const uint16_t *up_tbits;
   const int32_t *perm;  // solve id -> caller id (relabeled CSR), else null
   uint8_t *mis_o;       // relabeled: caller-order membership kept by the kernels, or null
   bool operator==(const RoundArgs &o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
@@ -314,6 +330,12 @@ int h2d(tcmis_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t s
 int d2h(tcmis_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t st);
 bool host_pinned(const void *p);  // page-locked / registered / device-accessible
 void free_staging(tcmis_ctx *ctx);
+
+// Phase 1 tile form (tile_cand.cu)
+int build_up_store(tcmis_graph *g, const uint32_t *p, const int64_t key[3], double *build_ms);
+int tile_cand_prepare(tcmis_graph *g, int H, uint64_t seed, int scale_bits, const int64_t key[3],
+                      double *build_ms);
+void free_up_store(tcmis_graph *g);
 
 // internal vertex order (order.cu)
 int reorder_impl(tcmis_graph *g, int32_t mode, const int32_t *order);

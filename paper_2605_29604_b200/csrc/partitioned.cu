@@ -596,6 +596,8 @@ int solve_partitioned_impl(tcmis_graph *g, tcmis_exchange *x, const int32_t *ran
     wait_us += std::chrono::duration<double, std::micro>(clk::now() - tw).count();
     if (e.v[5]) return set_error(TCMIS_E_LOGIC, "exchange list overflow (a round decided more "
                                                  "vertices than the alive bound)");
+    if (e.v[0] == 0 && e.v[2] > 0)  // the largest alive key is always a candidate
+      return set_error(TCMIS_E_LOGIC, "a round selected nothing while vertices are alive");
     got.push_back(e);
     alive_prev[1] = alive_prev[0];
     alive_prev[0] = e.v[2];

@@ -61,6 +61,8 @@ struct SelectArgs {
   DevRound *rounds;        // Phase 1 start stamp (null: none)
   const int32_t *perm;     // solve id -> caller id (relabeled graphs), else null
   uint8_t *mis_o;          // ... and the membership in the caller's order
+  int32_t tile_gate;       // > 0: rounds starting with >= this many alive vertices run
+                           // Phase 1 as A-up tiles (k_tile_mark), these kernels idle
 };
 
 // push: every neighbour of a candidate is excluded this round (spmv.cpp:18-59
@@ -77,6 +79,7 @@ constexpr int kProbeK = 4;  // row entries the straight-line probe examines
 // rows <= kProbeK (the whole grid, most of the RGG).
 __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
   pdl_entry();
+  if (a.tile_gate && a.ctrl->alive >= a.tile_gate) return;  // a tile round (tile_cand.cu)
   __shared__ int32_t s_und[kBlock / 32][64];
   Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
@@ -139,6 +142,7 @@ constexpr int32_t kSelWideN = 1 << 25;
 template <int kWin>
 __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a) {
   pdl_entry();
+  if (a.tile_gate && a.ctrl->alive >= a.tile_gate) return;  // a tile round (tile_cand.cu)
   Ctrl *ctrl = a.ctrl;
   const int64_t cnt = ctrl->sel_undec;
   if ((int64_t)blockIdx.x * kBlock >= cnt) return;
@@ -218,6 +222,7 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
 
 __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
   pdl_entry();
+  if (a.tile_gate && a.ctrl->alive >= a.tile_gate) return;  // a tile round (tile_cand.cu)
   Ctrl *ctrl = a.ctrl;
   const int cnt = ctrl->long_count, nvl = ctrl->sel_vlong;
   if ((int64_t)blockIdx.x * (kBlock / 32) >= cnt && blockIdx.x >= nvl) return;

@@ -348,6 +348,8 @@ void free_workspace(Workspace &ws) {
   dev_free(ws.cub_tmp);
   dev_free(ws.cbits);
   dev_free(ws.tile_hit);
+  dev_free(ws.alive_bits);
+  dev_free(ws.blocked);
   if (ws.exec) cudaGraphExecDestroy(ws.exec);
   ws = Workspace{};
 }
@@ -394,6 +396,8 @@ int ensure_workspace(tcmis_graph *g) {
     dev_free(ws.segmark);
     dev_free(ws.cbits);
     dev_free(ws.tile_hit);
+    dev_free(ws.alive_bits);
+    dev_free(ws.blocked);
     ws.n_cap = 0;
     if (int rc = dev_alloc(&ws.prio, n)) return rc;
     if (int rc = dev_alloc(&ws.q, n + 8)) return rc;
@@ -410,6 +414,11 @@ int ensure_workspace(tcmis_graph *g) {
     if (int rc = dev_alloc(&ws.segmark, n)) return rc;
     if (int rc = dev_alloc(&ws.cbits, n / 32 + 2)) return rc;
     if (int rc = dev_alloc(&ws.tile_hit, n / 16 + 2)) return rc;
+    if (int rc = dev_alloc(&ws.alive_bits, n / 32 + 2)) return rc;
+    if (int rc = dev_alloc(&ws.blocked, n / 16 + 2)) return rc;
+    // tile Phase 1 rows blocked: zero between tile rounds (k_tile_mark clears
+    // what it reads)
+    TCMIS_CUDA(cudaMemsetAsync(ws.blocked, 0, 4 * (n / 16 + 2), g->ctx->stream));
     TCMIS_CUDA(cudaMemsetAsync(ws.next, 0, n + 16, g->ctx->stream));
     ws.n_cap = n;
   }
@@ -605,6 +614,7 @@ SelectArgs select_args(tcmis_graph *g, const RoundArgs &a) {
   s.rounds = ws.rounds;
   s.perm = a.perm;
   s.mis_o = a.mis_o;
+  s.tile_gate = a.tile_cand ? a.tile_gate : 0;
   return s;
 }
 
@@ -735,6 +745,28 @@ int launch_select(tcmis_graph *g, const RoundArgs &a) {
   const SelectArgs s = select_args(g, a);
   if (a.tile)
     TCMIS_CUDA(cudaMemsetAsync(g->ws.cbits, 0, 4 * ((size_t)a.n / 32 + 1), st));
+  if (a.tile_cand) {
+    // Phase 1 as a tile product in the rounds that start with >= tile_gate
+    // alive vertices (tile_cand.cu): alive bitmap, A-up tiles x alive ->
+    // blocked rows, unblocked alive vertices -> candidates; in the other
+    // rounds these three idle and the CSR select kernels below run
+    Workspace &ws = g->ws;
+    const int64_t words = ((int64_t)a.n + 31) / 32;
+    TCMIS_TIMED(ctx, "k_alive_bits",
+                (k_alive_bits<<<grid_for(ctx, words, 256, 8), 256, 0, st>>>(
+                    a.n, ws.state, ws.alive_bits, ws.rounds, ws.ctrl, a.tile_gate)));
+    TCMIS_LAUNCHED(ctx);
+    TileExclArgs t{a.up_tiles, a.up_trow, a.up_tcol, a.up_tbits, ws.alive_bits, ws.blocked,
+                   ws.ctrl, a.tile_gate};
+    TCMIS_TIMED(ctx, "k_tile_cand_bits",
+                (k_tile_excl_bits<<<grid_for(ctx, a.up_tiles, 256, 8), 256, 0, st>>>(t)));
+    TCMIS_LAUNCHED(ctx);
+    TCMIS_TIMED(ctx, "k_tile_mark",
+                (k_tile_mark<<<grid_for(ctx, 32 * words, 256, 8), 256, 0, st>>>(
+                    a.n, ws.alive_bits, ws.blocked, ws.cbits, ws.next, ws.state, s.segflag, a.T,
+                    ws.ctrl, a.tile_gate, s.push, a.off, a.nbr)));
+    TCMIS_LAUNCHED(ctx);
+  }
   TCMIS_TIMED(ctx, "k_probe_select", (launch_round_kernel(k_probe_select, a.sel_grid, st, s)));
   TCMIS_LAUNCHED(ctx);
   TCMIS_TIMED(ctx, "k_select",
@@ -757,7 +789,7 @@ int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle
     TCMIS_TIMED(ctx, "k_update_pull", (launch_round_kernel(k_update_pull, a.sel_grid, st, u)));
   } else if (a.tile) {
     TCMIS_CUDA(cudaMemsetAsync(g->ws.tile_hit, 0, 4 * ((size_t)a.nb16 + 1), st));
-    TileExclArgs t{a.store_tiles, a.trow, a.tcol, a.tbits, g->ws.cbits, g->ws.tile_hit};
+    TileExclArgs t{a.store_tiles, a.trow, a.tcol, a.tbits, g->ws.cbits, g->ws.tile_hit, nullptr, 0};
     const int grid = grid_for(ctx, a.store_tiles, 256, 8);
     if (a.tile == 2)
       TCMIS_TIMED(ctx, "k_tile_excl_mma", (k_tile_excl_mma<<<grid, 256, 0, st>>>(t)));
@@ -779,7 +811,9 @@ int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle
   return 0;
 }
 
-inline int launches_per_round(const RoundArgs &a) { return (a.pull || a.tile) ? 6 : 4; }
+inline int launches_per_round(const RoundArgs &a) {
+  return ((a.pull || a.tile) ? 6 : 4) + (a.tile_cand ? 3 : 0);
+}
 
 // The parameters of a solve's first kernels (segment-flag clear,
 // k_priorities with the control-block init), part of the graph's cache key.
@@ -1003,8 +1037,12 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   // an internal vertex order (order.cu): the kernels run on the relabeled CSR
   // (not for the observer, whose snapshots are in the caller's order, nor for
   // the tile forms, whose store is built on the caller's CSR)
-  const bool tile_form =
-      cfg->exclusion == TCMIS_EXCL_TILE_BITS || cfg->exclusion == TCMIS_EXCL_TILE_MMA;
+  const bool tile_cand = (cfg->flags & TCMIS_F_TILE_CAND) != 0;
+  if (tile_cand && fresh)
+    return set_error(TCMIS_E_INVALID_ARGUMENT,
+                     "TCMIS_F_TILE_CAND needs fixed priorities (not luby-fresh)");
+  const bool tile_form = cfg->exclusion == TCMIS_EXCL_TILE_BITS ||
+                         cfg->exclusion == TCMIS_EXCL_TILE_MMA;
   const bool relabel = g->d_perm && !cfg->observer && !tile_form;
   const int64_t *s_off = relabel ? g->d_roff : g->d_off;
   const int32_t *s_nbr = relabel ? g->d_rnbr : g->d_nbr;
@@ -1070,7 +1108,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     a.pull = 0;
   } else if (cfg->exclusion == TCMIS_EXCL_CSR_PULL) {
     a.pull = 1;
-  } else if (cfg->exclusion == TCMIS_EXCL_TILE_BITS || cfg->exclusion == TCMIS_EXCL_TILE_MMA) {
+  } else if (tile_form) {
     // the paper's tile form over the compact T = 16 store (tile_excl.cuh);
     // built once per graph, like tile_graph in run_tc_mis(g, cfg)
     if (int rc = build_tile_store(g, 16)) return rc;
@@ -1083,6 +1121,21 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     a.tbits = static_cast<const uint16_t *>(g->d_tbits);
   } else {
     a.pull = (double)g->max_degree > 64.0 * std::max(1.0, avg_degree(g)) ? 1 : 0;
+  }
+  if (tile_cand) {
+    const int64_t key[3] = {H, (int64_t)cfg->seed, cfg->scale_bits};
+    if (int rc = tile_cand_prepare(g, H, cfg->seed, cfg->scale_bits, key, nullptr)) return rc;
+    a.tile_cand = 1;
+    a.up_tiles = g->up_tiles;
+    a.up_trow = g->d_up_trow;
+    a.up_tcol = g->d_up_tcol;
+    a.up_tbits = g->d_up_tbits;
+    a.nb16 = (int32_t)(((int64_t)g->n + 15) / 16);
+    // tile rounds: those starting with at least a quarter of the vertices
+    // alive (the tile kernels pay for every tile each round; the CSR scan
+    // engines only for the alive rows).  TCMIS_TILE_CAND_GATE overrides.
+    a.tile_gate = std::max<int32_t>(1, g->n / 4);
+    if (const char *env = std::getenv("TCMIS_TILE_CAND_GATE")) a.tile_gate = std::atoi(env);
   }
   // small late rounds run in the persistent k_tail (not with the per-round
   // observer hook, which needs every round's snapshot)
@@ -1216,7 +1269,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
                                  cudaMemcpyDeviceToHost, st));
       TCMIS_CUDA(cudaStreamSynchronize(st));
       rounds_h.push_back(dr);
-      if (ws.h_ctrl->alive == 0) break;
+      if (ws.h_ctrl->alive == 0 || ws.h_ctrl->corrupt) break;
       if (a.tail_thr > 0 && ws.h_ctrl->alive <= a.tail_thr) {
         ctx->rec_round = round + 1;
         if (int rc = launch_tail(g, a)) return rc;
@@ -1340,6 +1393,22 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   }
   *n_iter = rounds_run;
   return 0;
+}
+
+// the A-up store of the priorities (H, seed, scale_bits), built from the
+// priorities of this graph if not cached (tile_cand.cu)
+int tile_cand_prepare(tcmis_graph *g, int H, uint64_t seed, int scale_bits, const int64_t key[3],
+                      double *build_ms) {
+  if (build_ms) *build_ms = 0;
+  if (g->d_up_trow && g->up_key[0] == key[0] && g->up_key[1] == key[1] && g->up_key[2] == key[2])
+    return 0;
+  uint32_t *d_p = nullptr;
+  if (int rc = dev_alloc(&d_p, (size_t)g->n)) return rc;
+  int rc = launch_priorities(g, H, seed, scale_bits, d_p, nullptr, nullptr, nullptr);
+  if (!rc) rc = build_up_store(g, d_p, key, build_ms);
+  dev_free(d_p);
+  if (!rc && build_ms) g->up_build_ms = *build_ms;
+  return rc;
 }
 
 int states_in_caller_order(tcmis_graph *g) {
@@ -1549,9 +1618,11 @@ int h3_resolution_impl(tcmis_graph *g, const uint32_t *p, const uint8_t *states,
       cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st);
       cudaError_t e = cudaStreamSynchronize(st);
       if (e != cudaSuccess) rc = cuda_error(e, "h3 resolution");
-      if (ws.h_ctrl->alive == 0) break;
+      if (ws.h_ctrl->alive == 0 || ws.h_ctrl->corrupt) break;
     }
   }
+  if (!rc && ws.h_ctrl->corrupt)
+    rc = set_error(TCMIS_E_LOGIC, "pending set stopped shrinking");  // engine.cpp:224-225
   if (!rc) {
     std::vector<uint8_t> fin(g->n);
     cudaError_t e = cudaMemcpy(fin.data(), ws.state, g->n, cudaMemcpyDeviceToHost);

@@ -375,6 +375,17 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
   unsigned *wcnt = a.warpcnt + (solve & 1u) * kTailMaxWarps;
   unsigned *wnext = a.warpcnt + ((solve + 1u) & 1u) * kTailMaxWarps;
   const int32_t wlen = warp_range(a.n, nwarps, 0).len;
+  if (*(volatile int *)&ctrl->corrupt) {
+    // the per-round kernels flagged corrupt state (update.cuh): no rounds
+    // (the list may not fit the blocks), just the control block for the host
+    if (blockIdx.x == gridDim.x - 1 && a.pack) {
+      const uint32_t *cs = reinterpret_cast<const uint32_t *>(a.ctrl);
+      uint32_t *cd = reinterpret_cast<uint32_t *>(&a.pack->ctrl);
+      for (int i = threadIdx.x; i < (int)(sizeof(Ctrl) / 4); i += kTailBlock) cd[i] = __ldcg(cs + i);
+      __threadfence_system();
+    }
+    return;
+  }
   const int r0 = *(volatile int *)&ctrl->round;
   const int64_t cnt0 = *(volatile int *)&ctrl->wl_count[r0 & 1];
   TAIL_MARK(1, cnt0);

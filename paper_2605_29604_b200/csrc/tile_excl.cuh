@@ -42,6 +42,8 @@ struct TileExclArgs {
   const uint16_t *tbits;         // 16 rows of 16 bits per tile
   const uint32_t *cbits;         // this round's candidates, bit per vertex
   uint32_t *hit;                 // out: per block row, rows with a candidate neighbour
+  const Ctrl *gate_ctrl;         // Phase 1 use: run only in a tile round (alive >= gate)
+  int32_t gate;
 };
 
 __device__ __forceinline__ uint32_t seg16(const uint32_t *__restrict__ cbits, int32_t c) {
@@ -60,6 +62,7 @@ __device__ __forceinline__ void or_by_row(uint32_t *hit, int32_t b, uint32_t m, 
 }
 
 __global__ void __launch_bounds__(256) k_tile_excl_bits(TileExclArgs a) {
+  if (a.gate_ctrl && a.gate_ctrl->alive < a.gate) return;
   const uint4 *__restrict__ pay = reinterpret_cast<const uint4 *>(a.tbits);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < a.tiles;
@@ -160,6 +163,86 @@ __global__ void __launch_bounds__(256) k_tile_excl_mma(TileExclArgs a) {
     }
     if (cur >= 0) flush();
   }
+}
+
+// ---------------------------------------------- Phase 1 as a tile product
+// (tile_cand.cu): the round's alive set as a bitmap, k_tile_excl_bits over
+// the A-up store and that bitmap (blocked[b] = rows of block row b with an
+// alive higher-key neighbour), then the candidates.
+
+// bit v of word v/32 = (state[v] == Alive), 32 states per thread (two
+// 16-byte loads); the round's Phase 1 start stamp
+__global__ void __launch_bounds__(256)
+    k_alive_bits(int32_t n, const uint8_t *__restrict__ state, uint32_t *__restrict__ bits,
+                 DevRound *rounds, const Ctrl *ctrl, int32_t gate) {
+  if (ctrl->alive < gate) return;  // not a tile round: the CSR select kernels run
+  stamp_phase(rounds, ctrl, ctrl->round, 0, 0);
+  const int64_t words = ((int64_t)n + 31) / 32;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v0 = w * 32;
+    uint32_t m = 0;
+    if (v0 + 32 <= n) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4 *>(state + v0));
+      const uint4 b = __ldg(reinterpret_cast<const uint4 *>(state + v0 + 16));
+      const uint32_t x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t e = __vcmpeq4(x[k], 0u);  // 0xff per Alive byte
+#pragma unroll
+        for (int j = 0; j < 4; ++j) m |= ((e >> (8 * j + 7)) & 1u) << (4 * k + j);
+      }
+    } else {
+      for (int64_t v = v0; v < n; ++v) m |= (uint32_t)(state[v] == TCMIS_ALIVE) << (v - v0);
+    }
+    bits[w] = m;
+  }
+}
+
+// The candidates: a warp per 32-vertex word, C = alive AND NOT blocked from
+// one word of each bitmap (the round's alive set is exactly the alive
+// bitmap, so no worklist is read).  Lane j owns vertex 32w + j: the marks are
+// coalesced byte stores (generate_candidates, engine.cpp:105-119) and, with
+// the push exclusion, each candidate lane excludes its own CSR neighbours (the
+// pull form reads next == 1 itself).  C also goes out as the candidate bitmap
+// of the tile-form exclusion, and blocked is cleared behind the read for the
+// next tile round.
+__global__ void __launch_bounds__(256)
+    k_tile_mark(int32_t n, const uint32_t *__restrict__ alive, uint32_t *__restrict__ blocked,
+                uint32_t *__restrict__ cbits, uint8_t *__restrict__ next, uint8_t *__restrict__ state,
+                uint8_t *__restrict__ segflag, int T, Ctrl *ctrl, int32_t gate, int push,
+                const int64_t *__restrict__ off, const int32_t *__restrict__ nbr) {
+  if (ctrl->alive < gate) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t words = ((int64_t)n + 31) / 32;
+  unsigned long long sel = 0;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < words;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    uint32_t c = 0;
+    if (lane == 0) {
+      const uint32_t a = __ldg(&alive[w]);
+      const bool hi = (2 * w + 1) * 16 < n;
+      const uint32_t blk = (blocked[2 * w] & 0xffffu) | (hi ? (blocked[2 * w + 1] << 16) : 0u);
+      if (blk) {
+        blocked[2 * w] = 0;
+        if (hi) blocked[2 * w + 1] = 0;
+      }
+      c = a & ~blk;
+      cbits[w] = c;
+      sel += __popc(c);
+    }
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if ((c >> lane) & 1u) {
+      const int32_t v = (int32_t)(w * 32 + lane);
+      next[v] = 1;
+      state[v] = TCMIS_IN_MIS;
+      if (segflag) segflag[seg_of(v, T)] = 1;
+      if (push)
+        for (int64_t e = __ldg(&off[v]), e1 = __ldg(&off[v + 1]); e < e1; ++e)
+          next[__ldg(&nbr[e])] = 2;
+    }
+  }
+  block_add3(sel, 0, 0, ctrl);
 }
 
 }  // namespace tcmis_b200

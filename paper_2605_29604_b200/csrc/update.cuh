@@ -143,6 +143,10 @@ __device__ __forceinline__ void round_end_tail(const UpdateArgs &a, unsigned lon
     // rank of a partitioned solve the counts are the rank's own.
     if (!a.pub.bits && !a.pub.list && (unsigned long long)vc->alive != sel + rem_all + (unsigned long long)alive)
       vc->corrupt = 1;
+    // progress: the alive vertex of the largest key is always a candidate, so
+    // a round that selects nothing while vertices are alive can only come from
+    // corrupt state -- stop there instead of spinning to the iteration cap
+    if (!a.pub.bits && !a.pub.list && vc->alive > 0 && sel == 0) vc->corrupt = 1;
     vc->alive = alive;
     vc->sel = 0;
     vc->rem = 0;
@@ -157,7 +161,7 @@ __device__ __forceinline__ void round_end_tail(const UpdateArgs &a, unsigned lon
     vc->pull_undec = 0;
     vc->main_rounds = vc->main_rounds + 1;
     vc->round = round + 1;
-    if (use_cond) cudaGraphSetConditional(cond, alive > a.tail_thr ? 1u : 0u);
+    if (use_cond) cudaGraphSetConditional(cond, alive > a.tail_thr && !vc->corrupt ? 1u : 0u);
   }
 }
 

@@ -111,3 +111,28 @@ def test_order_errors(ctx):
     got = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=1))
     assert np.array_equal(got.mis, O.solve(g, "h2", 1, tile_dim=16).mis)
     dg.close()
+
+
+def test_permuted_graph_is_normalised(ctx):
+    """tcmis_graph_permuted: the order's ids as an ordinary graph -- rows
+    sorted, symmetric, the same degrees under the permutation -- which solves
+    like any graph (here with both Phase 1 forms)."""
+    dg = tc.DeviceGraph.rgg(20000, 3.0, 2, ctx).reorder(tc.DeviceGraph.ORDER_SPATIAL)
+    p = dg.permuted()
+    h = p.download()
+    og = O.Graph(h.n, h.offsets, h.neighbors)
+    for v in range(h.n):
+        row = h.neighbors[h.offsets[v]:h.offsets[v + 1]]
+        assert np.all(np.diff(row) > 0)
+    src = dg.download()
+    assert sorted(np.diff(src.offsets).tolist()) == sorted(np.diff(h.offsets).tolist())
+    u = np.repeat(np.arange(h.n), np.diff(h.offsets))
+    fwd = set(zip(u.tolist(), h.neighbors.tolist()))
+    assert all((b, a) in fwd for a, b in fwd)
+    exp = O.solve(og, "h2", 1, tile_dim=16)
+    for flags in (0, tc.F_TILE_CAND):
+        got = tc.run_mis(p, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=1, flags=flags))
+        assert np.array_equal(got.mis, exp.mis), flags
+        assert rounds_tuple(got.iterations) == oracle_tuple(exp), flags
+    p.close()
+    dg.close()
