@@ -179,6 +179,7 @@ TCMIS_API int tcmis_ctx_synchronize(tcmis_ctx *ctx) {
 TCMIS_API int tcmis_graph_upload_tiled(tcmis_ctx *ctx, int32_t n, const int64_t *offsets,
                                        const int32_t *neighbors, int32_t tile_dim,
                                        tcmis_graph **out, int64_t *tile_count) {
+  TCMIS_RANGE("tcmis_graph_upload_tiled");
   NEED(ctx && out, "null handle");
   NEED(n >= 0, "vertex count must be non-negative");
   NEED(n == 0 || offsets, "null offsets");
@@ -199,6 +200,7 @@ TCMIS_API int tcmis_graph_upload_tiled(tcmis_ctx *ctx, int32_t n, const int64_t 
 
 TCMIS_API int tcmis_graph_upload(tcmis_ctx *ctx, int32_t n, const int64_t *offsets,
                                  const int32_t *neighbors, tcmis_graph **out) {
+  TCMIS_RANGE("tcmis_graph_upload");
   NEED(ctx && out, "null handle");
   NEED(n >= 0, "vertex count must be non-negative");
   NEED(n == 0 || offsets, "null offsets");
@@ -293,6 +295,7 @@ TCMIS_API int tcmis_graph_download(tcmis_graph *g, int64_t *offsets, int32_t *ne
 }
 
 TCMIS_API int tcmis_graph_tile(tcmis_graph *g, int32_t tile_dim, int64_t *tile_count) {
+  TCMIS_RANGE("tcmis_graph_tile");
   NEED(g, "null graph");
   ENTER(g->ctx);
   if (g->tile_T != tile_dim)
@@ -303,6 +306,7 @@ TCMIS_API int tcmis_graph_tile(tcmis_graph *g, int32_t tile_dim, int64_t *tile_c
 
 TCMIS_API int tcmis_graph_set_tiling(tcmis_graph *g, int32_t T, const int64_t *bro,
                                      int32_t nb, const int32_t *tile_col, int64_t tile_count) {
+  TCMIS_RANGE("tcmis_graph_set_tiling");
   NEED(g, "null graph");
   ENTER(g->ctx);
   if (T < 1 || T > 64)
@@ -337,6 +341,7 @@ TCMIS_API int tcmis_graph_set_tiling(tcmis_graph *g, int32_t T, const int64_t *b
 
 TCMIS_API int tcmis_graph_export_tiles(tcmis_graph *g, int32_t T, int32_t *tile_row,
                                        int32_t *tile_col, uint64_t *row_bits, int64_t *bro) {
+  TCMIS_RANGE("tcmis_graph_export_tiles");
   NEED(g && bro, "null handle");
   ENTER(g->ctx);
   return export_tiles(g, T, tile_row, tile_col, row_bits, bro);
@@ -344,6 +349,7 @@ TCMIS_API int tcmis_graph_export_tiles(tcmis_graph *g, int32_t T, int32_t *tile_
 
 TCMIS_API int tcmis_graph_tile_store(tcmis_graph *g, int32_t T, int64_t *tile_count,
                                      int64_t *bro, int32_t *tile_col, void *payload) {
+  TCMIS_RANGE("tcmis_graph_tile_store");
   NEED(g, "null graph");
   ENTER(g->ctx);
   if (int rc = build_tile_store(g, T)) return rc;
@@ -366,6 +372,7 @@ TCMIS_API int tcmis_graph_tile_store(tcmis_graph *g, int32_t T, int64_t *tile_co
 TCMIS_API int tcmis_validate(tcmis_graph *g, const int32_t *set, int64_t count,
                              int32_t *independent, int32_t *violating_u, int32_t *violating_v,
                              int32_t *maximal, int32_t *addable_vertex) {
+  TCMIS_RANGE("tcmis_validate");
   NEED(g && independent && violating_u && violating_v && maximal && addable_vertex,
        "null handle");
   NEED(count >= 0 && (count == 0 || set), "null set");
@@ -376,6 +383,7 @@ TCMIS_API int tcmis_validate(tcmis_graph *g, const int32_t *set, int64_t count,
 
 TCMIS_API int tcmis_priorities(tcmis_graph *g, int32_t heuristic, uint64_t seed,
                                int32_t scale_bits, uint32_t *p_out) {
+  TCMIS_RANGE("tcmis_priorities");
   NEED(g && p_out, "null handle");
   ENTER(g->ctx);
   return priorities_impl(g, heuristic, seed, scale_bits, p_out);
@@ -396,6 +404,7 @@ static int solve_common(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stat
 TCMIS_API int tcmis_solve(tcmis_graph *g, const tcmis_config *cfg, uint8_t *state_out,
                           int32_t *mis_out, int64_t *mis_count, tcmis_iter_stats *stats,
                           int32_t max_stats, int32_t *n_iterations) {
+  TCMIS_RANGE("tcmis_solve");
   int64_t mc = 0;
   if (int rc = solve_common(g, cfg, stats, max_stats, n_iterations, &mc)) return rc;
   if (mis_count) *mis_count = mc;
@@ -417,6 +426,7 @@ TCMIS_API int tcmis_solve_device(tcmis_graph *g, const tcmis_config *cfg, const 
                                  int64_t *mis_count, const uint8_t **d_state,
                                  tcmis_iter_stats *stats, int32_t max_stats,
                                  int32_t *n_iterations) {
+  TCMIS_RANGE("tcmis_solve_device");
   if (int rc = solve_common(g, cfg, stats, max_stats, n_iterations, mis_count)) return rc;
   if (d_mis) *d_mis = g->ws.mis;
   if (d_state) {
@@ -428,6 +438,7 @@ TCMIS_API int tcmis_solve_device(tcmis_graph *g, const tcmis_config *cfg, const 
 
 TCMIS_API int tcmis_graph_tile_cand_prepare(tcmis_graph *g, const tcmis_config *cfg,
                                             double *build_ms, int64_t *tiles) {
+  TCMIS_RANGE("tcmis_graph_tile_cand_prepare");
   NEED(g && cfg, "null handle");
   if (cfg->heuristic < TCMIS_H1 || cfg->heuristic > TCMIS_LUBY_PERM ||
       cfg->heuristic == TCMIS_LUBY_FRESH)
@@ -446,6 +457,7 @@ TCMIS_API int tcmis_graph_tile_cand_prepare(tcmis_graph *g, const tcmis_config *
 }
 
 TCMIS_API int tcmis_graph_permuted(tcmis_graph *g, tcmis_graph **out) {
+  TCMIS_RANGE("tcmis_graph_permuted");
   NEED(g && out, "null handle");
   NEED(g->d_perm || g->n == 0, "tcmis_graph_reorder first");
   ENTER(g->ctx);
@@ -482,6 +494,7 @@ TCMIS_API int tcmis_graph_permuted(tcmis_graph *g, tcmis_graph **out) {
 }
 
 TCMIS_API int tcmis_graph_reorder(tcmis_graph *g, int32_t mode, const int32_t *order) {
+  TCMIS_RANGE("tcmis_graph_reorder");
   NEED(g, "null handle");
   ENTER(g->ctx);
   return reorder_impl(g, mode, order);
@@ -490,6 +503,7 @@ TCMIS_API int tcmis_graph_reorder(tcmis_graph *g, int32_t mode, const int32_t *o
 TCMIS_API int tcmis_graph_upload_partition(tcmis_ctx *ctx, int32_t n, int32_t lo, int32_t hi,
                                            const int64_t *full_offsets,
                                            const int32_t *row_neighbors, tcmis_graph **out) {
+  TCMIS_RANGE("tcmis_graph_upload_partition");
   NEED(ctx && out && full_offsets, "null handle");
   NEED(n >= 0, "vertex count must be non-negative");
   ENTER(ctx);
@@ -498,6 +512,7 @@ TCMIS_API int tcmis_graph_upload_partition(tcmis_ctx *ctx, int32_t n, int32_t lo
 
 TCMIS_API int tcmis_graph_partition(tcmis_graph *full, int32_t lo, int32_t hi,
                                     tcmis_graph **out) {
+  TCMIS_RANGE("tcmis_graph_partition");
   NEED(full && out, "null handle");
   ENTER(full->ctx);
   return partition_device(full, lo, hi, out);
@@ -552,6 +567,7 @@ TCMIS_API int tcmis_h1_random(tcmis_ctx *ctx, int32_t n, uint64_t seed, uint32_t
 
 TCMIS_API int tcmis_h3_resolution(tcmis_graph *g, const uint32_t *p, const uint8_t *states,
                                   uint8_t *c_out) {
+  TCMIS_RANGE("tcmis_h3_resolution");
   NEED(g && (g->n == 0 || (p && states && c_out)), "null handle");
   ENTER(g->ctx);
   return h3_resolution_impl(g, p, states, c_out);
@@ -561,6 +577,7 @@ TCMIS_API int tcmis_tiled_spmv_tiles(tcmis_ctx *ctx, int32_t n, int32_t T, int64
                                      const int32_t *tile_col, const uint64_t *row_bits,
                                      const int64_t *bro, const uint64_t *seg, int32_t exclusion,
                                      int32_t *nc, int64_t *ev, int64_t *sk) {
+  TCMIS_RANGE("tcmis_tiled_spmv_tiles");
   NEED(ctx && ev && sk, "null handle");
   NEED(n == 0 || (bro && seg && nc), "null buffers");
   NEED(tiles == 0 || (tile_col && row_bits), "null tile buffers");
@@ -595,6 +612,7 @@ TCMIS_API int tcmis_tiled_spmv(tcmis_graph *g, int32_t T, const uint8_t *c, int3
 
 TCMIS_API int tcmis_gen_rmat(tcmis_ctx *ctx, int32_t scale, int32_t ef, uint64_t seed,
                              tcmis_graph **out) {
+  TCMIS_RANGE("tcmis_gen_rmat");
   NEED(ctx && out, "null handle");
   ENTER(ctx);
   return gen_rmat(ctx, scale, ef, seed, out);
@@ -602,12 +620,14 @@ TCMIS_API int tcmis_gen_rmat(tcmis_ctx *ctx, int32_t scale, int32_t ef, uint64_t
 
 TCMIS_API int tcmis_graph_from_edges(tcmis_ctx *ctx, int32_t n, int64_t m, const int32_t *u,
                                      const int32_t *v, tcmis_graph **out) {
+  TCMIS_RANGE("tcmis_graph_from_edges");
   NEED(ctx && out && (m == 0 || (u && v)), "null handle");
   ENTER(ctx);
   return gen_from_edges(ctx, n, m, u, v, out);
 }
 
 TCMIS_API int tcmis_gen_grid(tcmis_ctx *ctx, int32_t side, tcmis_graph **out) {
+  TCMIS_RANGE("tcmis_gen_grid");
   NEED(ctx && out, "null handle");
   ENTER(ctx);
   return gen_grid(ctx, side, out);
@@ -615,6 +635,7 @@ TCMIS_API int tcmis_gen_grid(tcmis_ctx *ctx, int32_t side, tcmis_graph **out) {
 
 TCMIS_API int tcmis_gen_rgg(tcmis_ctx *ctx, int32_t n, uint64_t radius, uint64_t seed,
                             tcmis_graph **out) {
+  TCMIS_RANGE("tcmis_gen_rgg");
   NEED(ctx && out, "null handle");
   ENTER(ctx);
   return gen_rgg(ctx, n, radius, seed, out);

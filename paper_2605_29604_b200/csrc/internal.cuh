@@ -14,6 +14,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <cstring>
@@ -228,6 +229,16 @@ struct tcmis_graph {
 };
 
 namespace tcmis_b200 {
+
+// NVTX ranges around the C-ABI calls and the host-driven rounds (header-only
+// NVTX3: free unless a profiler such as nsys / ncu attaches)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+#define TCMIS_RANGE(name) ::tcmis_b200::NvtxRange tcmis_nvtx_range_(name)
 
 // error plumbing (capi.cu)
 int set_error(int code, const std::string &msg);

@@ -438,6 +438,7 @@ int enqueue_round(tcmis_graph *g, tcmis_exchange *x, RoundArgs &a, PartBufs &b, 
 constexpr int kKernelsPerRoundExtra = 4;  // apply x2, stage, ring
 
 int launch_round(tcmis_graph *g, tcmis_exchange *x, RoundArgs &a, PartBufs &b, int32_t cap) {
+  TCMIS_RANGE(cap ? "partitioned round (id lists)" : "partitioned round (bitmaps)");
   tcmis_ctx *ctx = g->ctx;
   if (!x->capturable) return enqueue_round(g, x, a, b, cap);
   auto it = b.graphs.find(cap);
@@ -808,6 +809,7 @@ TCMIS_API int tcmis_solve_partitioned(tcmis_graph *part, tcmis_exchange *x, cons
                                       int32_t *n_iterations) {
   NEED(part && x && rank_lo && cfg && n_iterations, "null handle");
   NEED(world >= 1, "bad world");
+  TCMIS_RANGE("tcmis_solve_partitioned");
   TCMIS_CUDA(cudaSetDevice(part->ctx->device));
   t_alloc_stream = part->ctx->stream;
   const int rc = solve_partitioned_impl(part, x, rank_lo, world, cfg, state_out, mis_out,

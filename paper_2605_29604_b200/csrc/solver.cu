@@ -1246,6 +1246,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       if (round > g->n)  // engine.cpp:248-249
         return set_error(TCMIS_E_RUNTIME, "iteration cap exceeded; engine livelock");
       ctx->rec_round = round;
+      TCMIS_RANGE("host-loop round");
       if (int rc = launch_select(g, a)) return rc;
       if (cfg->observer && H != TCMIS_H3) {
         // the select kernels already moved this round's candidates to InMIS;

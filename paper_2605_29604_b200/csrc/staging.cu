@@ -229,6 +229,7 @@ int h2d(tcmis_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t s
   }
   Staging *s = nullptr;
   if (int rc = staging(ctx, &s)) return rc;
+  TCMIS_RANGE("staged h2d");
   const char *from = static_cast<const char *>(src);
   char *to = static_cast<char *>(dst);
   for (size_t off = 0; off < bytes; off += s->piece) {
@@ -255,6 +256,7 @@ int d2h(tcmis_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t s
   }
   Staging *s = nullptr;
   if (int rc = staging(ctx, &s)) return rc;
+  TCMIS_RANGE("staged d2h");
   const char *from = static_cast<const char *>(src);
   char *to = static_cast<char *>(dst);
   const size_t pieces = (bytes + s->piece - 1) / s->piece;
