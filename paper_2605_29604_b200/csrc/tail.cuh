@@ -199,11 +199,13 @@ __device__ __forceinline__ WarpRange warp_range(int32_t n, int nwarps, int gw) {
 // sit between a candidate and the block's next barrier).  next[] is not
 // written: it keeps marking the per-round kernels' candidates, which the
 // compaction's count pass reads while the tail runs.
-__device__ __forceinline__ void tail_candidate(const TailArgs &a, int32_t v, unsigned *wcnt,
-                                               int32_t wlen, unsigned long long &sel,
-                                               int32_t *pend, int *npend) {
+__device__ __forceinline__ void tail_candidate(const TailArgs &a, int32_t v, int32_t o,
+                                               unsigned *wcnt, int32_t wlen,
+                                               unsigned long long &sel, int32_t *pend,
+                                               int *npend) {
+  // o: the caller's id of v (relabeled graphs), kept with the list entry so
+  // no permutation load sits between a decision and the block's barrier
   a.state[v] = TCMIS_IN_MIS;
-  const int32_t o = orig_id(a.perm, v);
   if (a.mis_o) a.mis_o[o] = TCMIS_IN_MIS;
   if (!a.perm || a.mis_o) atomicAdd(&wcnt[o / wlen], 1u);
   ++sel;
@@ -342,6 +344,7 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
   extern __shared__ int32_t s_stage[];  // kTailDynSmem: compact_mis's staging
   // the block's list: entry k = (id, row extent, q), handled by thread k
   __shared__ int32_t s_v[kTailBlock];
+  __shared__ int32_t s_o[kTailBlock];  // the entry's caller id (relabeled graphs; else = s_v)
   __shared__ int64_t s_s[kTailBlock], s_e[kTailBlock];
   __shared__ uint16_t s_q[kTailBlock];
   __shared__ uint8_t s_keep[kTailBlock];  // the entry's verdict: 1 = non-candidate
@@ -400,6 +403,7 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
     if (threadIdx.x < nl) {
       const int32_t v = __ldcg(&in0[blockIdx.x + (int64_t)threadIdx.x * gridDim.x]);
       s_v[threadIdx.x] = v;
+      s_o[threadIdx.x] = a.perm ? __ldg(&a.perm[v]) : v;
       s_s[threadIdx.x] = __ldg(&a.off[v]);
       s_e[threadIdx.x] = __ldg(&a.off[v + 1]);
       s_q[threadIdx.x] = __ldcg(&a.q[v]);
@@ -470,12 +474,13 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
     // a handful of entries: one warp per entry, not the thread + group pair
     // (two dependent scans where one suffices for a round of few vertices)
     const bool small = nl <= kTailWarps;
-    int32_t v = -1;
+    int32_t v = -1, o = -1;
     int64_t s = 0, e = 0;
     uint32_t qv = 0;
     uint8_t keep = 0;
     if (have) {
       v = s_v[k];
+      o = s_o[k];
       s = s_s[k];
       e = s_e[k];
       qv = s_q[k];
@@ -532,7 +537,7 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
             }
           }
           if (!blocked) {
-            if (lane == 0) tail_candidate(a, wv, wcnt, wlen, sel, pend, npend);
+            if (lane == 0) tail_candidate(a, wv, s_o[w], wcnt, wlen, sel, pend, npend);
             if (we - ws <= kWW) {
 #pragma unroll
               for (int j = 0; j < kTU; ++j)
@@ -587,7 +592,7 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
         if (b) {
           keep = 1;
         } else if (hi <= s) {  // the whole row was in the windows
-          tail_candidate(a, v, wcnt, wlen, sel, pend, npend);
+          tail_candidate(a, v, o, wcnt, wlen, sel, pend, npend);
 #pragma unroll
           for (int j = 0; j < kThrScan; ++j)
             if ((live >> j) & 1u) a.xt[u[j]] = (uint16_t)tcur;
@@ -652,7 +657,7 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
         blocked = __ballot_sync(gmask, b) != 0;
       }
       if (!blocked) {
-        if (gl == 0) tail_candidate(a, dv, wcnt, wlen, sel, pend, npend);
+        if (gl == 0) tail_candidate(a, dv, s_o[kd], wcnt, wlen, sel, pend, npend);
         const uint32_t sl = s_live[kd];
         for (int j = gl; j < kThrScan; j += kGroup)
           if ((sl >> j) & 1u) a.xt[s_stage[kd * kThrScan + j]] = (uint16_t)tcur;
@@ -709,7 +714,7 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
         blocked = __syncthreads_or(b) != 0;
       }
       if (!blocked) {
-        if (threadIdx.x == 0) tail_candidate(a, dv, wcnt, wlen, sel, pend, npend);
+        if (threadIdx.x == 0) tail_candidate(a, dv, s_o[kd], wcnt, wlen, sel, pend, npend);
         if (threadIdx.x < kThrScan && ((s_live[kd] >> threadIdx.x) & 1u))
           a.xt[s_stage[kd * kThrScan + threadIdx.x]] = (uint16_t)tcur;
         if (de - ds <= kBW) {
@@ -766,6 +771,7 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
     if (have && s_keep[k]) {
       const int j = atomicAdd(&s_nl, 1);
       s_v[j] = v;
+      s_o[j] = o;
       s_s[j] = s;
       s_e[j] = e;
       s_q[j] = (uint16_t)qv;
