@@ -231,6 +231,12 @@ __global__ void k_unpermute(int32_t n, const int32_t *__restrict__ inv,
     state_o[v] = state[__ldg(&inv[v])];
 }
 
+// a relabeled solve's caller-order membership plane: 1 / 2 = InMIS (tail.cuh)
+struct IsMember {
+  const uint8_t *plane;
+  __device__ __forceinline__ bool operator()(int32_t v) const { return plane[v] != 0; }
+};
+
 struct IsInMIS {
   const uint8_t *state;
   __device__ __forceinline__ bool operator()(int32_t v) const { return state[v] == TCMIS_IN_MIS; }
@@ -922,8 +928,10 @@ int ensure_solve_graph(tcmis_graph *g, const RoundArgs &a, const SolvePre &pre) 
         size_t bytes = ws.cub_bytes;
         e = gather ? cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
                                            (int)g->n, IsInMISInv{ws.state, g->d_inv}, st)
-                   : cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
-                                           (int)g->n, IsInMIS{a.mis_o ? a.mis_o : ws.state}, st);
+                   : a.mis_o ? cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
+                                                     (int)g->n, IsMember{a.mis_o}, st)
+                             : cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
+                                                     (int)g->n, IsInMIS{ws.state}, st);
         if (e != cudaSuccess) rc = cuda_error(e, "MIS compaction");
       }
       if (!rc && pre.seg_mode == 2) {
@@ -1054,7 +1062,9 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   if (const char *env = std::getenv("TCMIS_MIS_O_MAX")) mis_o_max = std::atoll(env);  // test hook
   const bool use_mis_o = relabel && (int64_t)g->n <= mis_o_max;
   if (use_mis_o && !ws.mis_o)
-    if (int rc = dev_alloc(&ws.mis_o, (size_t)g->n + 16)) return rc;  // uint4 reads past n
+    // sized by the workspace's capacity, not this graph's n: the workspace is
+    // adopted by later graphs up to n_cap vertices (tcmis_graph_destroy)
+    if (int rc = dev_alloc(&ws.mis_o, ws.n_cap + 16)) return rc;  // uint4 reads past n
   uint8_t *s_mis_o = use_mis_o ? ws.mis_o : nullptr;
   ws.relabeled = relabel;
 
@@ -1168,9 +1178,12 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       if (a.perm && !a.mis_o)
         TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
                                          (int)g->n, IsInMISInv{ws.state, g->d_inv}, st));
+      else if (a.mis_o)
+        TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
+                                         (int)g->n, IsMember{a.mis_o}, st));
       else
         TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
-                                         (int)g->n, IsInMIS{a.mis_o ? a.mis_o : ws.state}, st));
+                                         (int)g->n, IsInMIS{ws.state}, st));
       ctx->launches += 1;
     }
     TCMIS_CUDA(cudaMemcpyAsync(&ws.h_misc[0], ws.mis_count, sizeof(int64_t),
@@ -1416,7 +1429,7 @@ int states_in_caller_order(tcmis_graph *g) {
   Workspace &ws = g->ws;
   if (!ws.relabeled || !g->d_inv) return 0;
   if (!ws.state_o)
-    if (int rc = dev_alloc(&ws.state_o, (size_t)g->n + 16)) return rc;
+    if (int rc = dev_alloc(&ws.state_o, ws.n_cap + 16)) return rc;  // capacity, as mis_o
   k_unpermute<<<grid_for(g->ctx, g->n, 256, 8), 256, 0, g->ctx->stream>>>(g->n, g->d_inv,
                                                                           ws.state, ws.state_o);
   TCMIS_LAUNCHED(g->ctx);

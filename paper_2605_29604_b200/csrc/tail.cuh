@@ -206,7 +206,9 @@ __device__ __forceinline__ void tail_candidate(const TailArgs &a, int32_t v, int
   // o: the caller's id of v (relabeled graphs), kept with the list entry so
   // no permutation load sits between a decision and the block's barrier
   a.state[v] = TCMIS_IN_MIS;
-  if (a.mis_o) a.mis_o[o] = TCMIS_IN_MIS;
+  // 2, not 1: the count pass (other blocks may still be in it) counts the
+  // per-round kernels' 1s; the compaction takes every non-zero byte
+  if (a.mis_o) a.mis_o[o] = 2;
   if (!a.perm || a.mis_o) atomicAdd(&wcnt[o / wlen], 1u);
   ++sel;
   const int32_t sb = seg_of(o, a.T);
@@ -306,7 +308,9 @@ __device__ void compact_mis(const TailArgs &a, unsigned *wcnt, unsigned *wnext, 
       xn = __ldcg(reinterpret_cast<const uint4 *>(memb + v0 + kCompactV));
     uint32_t m = 0;
     if (v0 < R.hi) {
-      m = eq_mask16(x, TCMIS_IN_MIS);
+      // states: InMIS; a relabeled solve's membership plane: 1 (per-round
+      // kernels) or 2 (this kernel)
+      m = a.mis_o ? (0xffffu & ~eq_mask16(x, 0u)) : eq_mask16(x, TCMIS_IN_MIS);
       const int64_t left = R.hi - v0;
       if (left < 16) m &= (1u << left) - 1u;
     }
