@@ -7,6 +7,10 @@ ctx = tc.Context(0)
 import bench
 dg = bench.make_device_graph(tc, cfgname, ctx)
 dg.tile(16)
+# the bench's vertex order for this config (bench.py --order auto)
+order = os.environ.get("ORDER") or {"rgg": "spatial", "rmat26": "degree"}.get(cfgname, "none")
+if order != "none":
+    dg.reorder({"degree": tc.DeviceGraph.ORDER_DEGREE, "spatial": tc.DeviceGraph.ORDER_SPATIAL}[order])
 ex = {"auto": tc.Exclusion.AUTO, "push": tc.Exclusion.PUSH, "pull": tc.Exclusion.CSR_PULL,
       "tile-bits": tc.Exclusion.TILE_BITS, "tile-mma": tc.Exclusion.TILE_MMA}[os.environ.get("EXCL", "auto")]
 for _ in range(2):
