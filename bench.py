@@ -296,11 +296,18 @@ def run_ours(args) -> dict:
     kernels = sorted(((k[0], k[1], sum(v) / len(v)) for k, v in kern.items()),
                      key=lambda x: -x[2])
     roofline = kernel_roofline(tc, dg, cfg, kernels, args, ms_per_step)
+    # ---- the reference user's own call: tcmis::run_mis on std::vector storage
+    # (first: the pinned e2e below leaves ~0.6 GB of pinned host memory in
+    # torch's host cache, which slowed the pageable path's host copies)
+    cpp = None
+    if not args.no_e2e and rank == 0 and world == 1 and args.exclusion == "auto" \
+            and args.candidates == "csr":
+        cpp = run_cpp_dropin(dg, args, mis_count)
     # ---- e2e through the drop-in C-ABI with host buffers
-    e2e = run_e2e(tc, torch, dg, ctx, stream, cfg, args, local, dist, flush)
-    if e2e is not None and rank == 0 and world == 1:
-        # the reference user's own call: tcmis::run_mis on std::vector storage
-        e2e["cpp_dropin_pageable"] = run_cpp_dropin(dg, args, mis_count)
+    e2e = None if args.no_e2e else run_e2e(tc, torch, dg, ctx, stream, cfg, args, local, dist,
+                                            flush)
+    if e2e is not None and cpp is not None:
+        e2e["cpp_dropin_pageable"] = cpp
 
     line = {
         "metric": "Gedges/s (MIS solve, BASELINE config)", "value": round(value, 4),
@@ -565,7 +572,7 @@ def k1_timing(tc, dg, ctx, reps: int = 3) -> dict:
     hbm, _ = peaks()
     n, nnz = dg.n, dg.nnz
     csr_b = 8 * (n + 1) + 4 * nnz
-    d_off, d_nbr = dg.device_offsets(), dg.device_neighbors()
+    d_off, d_nbr = dg.device_offsets, dg.device_neighbors
 
     def fresh():
         h = C.c_void_p()

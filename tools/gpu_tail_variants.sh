@@ -5,7 +5,7 @@ for v in "$@"; do
   TCMIS_NVCC_EXTRA="$v" python -m paper_2605_29604_b200.build > /dev/null 2>&1
   echo "=== variant '$v'"
   for c in rmat22 er grid rmat26; do
-    timeout 300 python bench.py --config $c --no-e2e --no-cpu-baseline --steps 10 > gpurun_out/var_$c.json 2>/dev/null
+    timeout 300 python bench.py --config $c --no-e2e --no-cpu-baseline --no-k1 --steps 10 > gpurun_out/var_$c.json 2>/dev/null
     python tools/bench_summary.py gpurun_out/var_$c.json | cut -c1-80
   done
   rm -f paper_2605_29604_b200/_obj/solver.cu.o
