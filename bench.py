@@ -208,7 +208,8 @@ def run_ours(args) -> dict:
     excl = {"auto": tc.Exclusion.AUTO, "push": tc.Exclusion.PUSH,
             "pull": tc.Exclusion.CSR_PULL, "tile-bits": tc.Exclusion.TILE_BITS,
             "tile-mma": tc.Exclusion.TILE_MMA}[args.exclusion]
-    cand_flags = tc.F_TILE_CAND if args.candidates == "tile" else 0
+    cand_flags = {"csr": 0, "tile": tc.F_TILE_CAND,
+                  "tile-umma": tc.F_TILE_CAND | tc.F_TILE_UMMA}[args.candidates]
     cfg = tc.EngineConfig(heuristic=HEUR[args.heuristic], seed=1, tile_dim=16, exclusion=excl,
                           flags=cand_flags)
     tile_cand_build = None
@@ -367,7 +368,7 @@ def timeline(tc, ctx):
 PHASE = {"k_probe_select": 1, "k_select": 1, "k_select_long": 1,
          "k_probe_pull": 2, "k_update_pull": 2, "k_tile_excl_bits": 2, "k_tile_excl_mma": 2,
          "k_update": 3, "k_round_end": 3, "k_priorities": 0, "k_tail": 4,
-         "k_alive_bits": 1, "k_tile_cand_bits": 1, "k_tile_mark": 1}
+         "k_alive_bits": 1, "k_tile_cand_bits": 1, "k_tile_cand_umma": 1, "k_tile_mark": 1}
 PHASE_NAME = {0: "init (priorities, states)", 1: "Phase 1 candidate detection",
               2: "Phase 2 neighbour exclusion (SpMV)", 3: "Phase 3 state update + compaction",
               12: "Phases 1+2 (push exclusion fused into candidate detection)",
@@ -1100,7 +1101,7 @@ def main():
                     help="N > 1: skip rank 0's single-GPU solve of the same graph")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-k1", action="store_true", help="skip the tile-converter timings")
-    ap.add_argument("--candidates", default="csr", choices=["csr", "tile"],
+    ap.add_argument("--candidates", default="csr", choices=["csr", "tile", "tile-umma"],
                     help="Phase 1 form: CSR scan engines or A-up tiles x alive bitmap")
     ap.add_argument("--heuristic", default="h2", choices=list(HEUR))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

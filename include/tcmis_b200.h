@@ -101,6 +101,9 @@ typedef struct tcmis_config {
  * scale_bits) and cached on the graph (tcmis_graph_tile_cand_prepare builds
  * it ahead).  Not for luby-fresh (its keys change every round). */
 #define TCMIS_F_TILE_CAND 0x8u
+/* with TCMIS_F_TILE_CAND: the A-up tile x alive product on the tensor cores
+ * (tcgen05.mma kind::i8, accumulator in TMEM; csrc/tile_umma.cuh) */
+#define TCMIS_F_TILE_UMMA 0x10u
 /* test hook: start the solve from a control block that disagrees with the
  * vertex states; the device's round invariant check must then fail the solve
  * with TCMIS_E_LOGIC (the reference's logic_error, engine.cpp:152-153) */

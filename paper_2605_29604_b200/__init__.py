@@ -101,6 +101,7 @@ F_TIMING = 0x1
 F_HOST_LOOP = 0x2
 F_OWN_RANGE = 0x4
 F_TILE_CAND = 0x8  # Phase 1 as A-up tiles x alive bitmap (csrc/tile_cand.cu)
+F_TILE_UMMA = 0x10  # ... with the product on tcgen05 (csrc/tile_umma.cuh)
 F_DEBUG_CORRUPT = 0x100  # test hook (include/tcmis_b200.h)
 
 

@@ -311,7 +311,7 @@ struct RoundArgs {
   const int32_t *trow;
   const int32_t *tcol;
   const uint16_t *tbits;
-  int tile_cand;        // Phase 1 as A-up tiles x alive bitmap (tile_cand.cu) ...
+  int tile_cand;        // Phase 1 as A-up tiles x alive bitmap (tile_cand.cu; 2: tcgen05) ...
   int32_t tile_gate;    // ... in the rounds starting with >= tile_gate alive
   int64_t up_tiles;
   const int32_t *up_trow;

@@ -30,6 +30,7 @@
 #include "update.cuh"
 #include "tail.cuh"
 #include "tile_excl.cuh"
+#include "tile_umma.cuh"
 
 namespace tcmis_b200 {
 
@@ -762,10 +763,17 @@ int launch_select(tcmis_graph *g, const RoundArgs &a) {
                 (k_alive_bits<<<grid_for(ctx, words, 256, 8), 256, 0, st>>>(
                     a.n, ws.state, ws.alive_bits, ws.rounds, ws.ctrl, a.tile_gate)));
     TCMIS_LAUNCHED(ctx);
-    TileExclArgs t{a.up_tiles, a.up_trow, a.up_tcol, a.up_tbits, ws.alive_bits, ws.blocked,
-                   ws.ctrl, a.tile_gate};
-    TCMIS_TIMED(ctx, "k_tile_cand_bits",
-                (k_tile_excl_bits<<<grid_for(ctx, a.up_tiles, 256, 8), 256, 0, st>>>(t)));
+    if (a.tile_cand == 2) {  // the same product on tcgen05 (tile_umma.cuh)
+      UmmaArgs u{a.up_tiles, a.up_trow, a.up_tcol, a.up_tbits, ws.alive_bits, ws.blocked,
+                 ws.ctrl, a.tile_gate};
+      TCMIS_TIMED(ctx, "k_tile_cand_umma",
+                  (k_tile_umma<<<ctx->num_sms * 8, 128, 0, st>>>(u)));
+    } else {
+      TileExclArgs t{a.up_tiles, a.up_trow, a.up_tcol, a.up_tbits, ws.alive_bits, ws.blocked,
+                     ws.ctrl, a.tile_gate};
+      TCMIS_TIMED(ctx, "k_tile_cand_bits",
+                  (k_tile_excl_bits<<<grid_for(ctx, a.up_tiles, 256, 8), 256, 0, st>>>(t)));
+    }
     TCMIS_LAUNCHED(ctx);
     TCMIS_TIMED(ctx, "k_tile_mark",
                 (k_tile_mark<<<grid_for(ctx, 32 * words, 256, 8), 256, 0, st>>>(
@@ -1135,7 +1143,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   if (tile_cand) {
     const int64_t key[3] = {H, (int64_t)cfg->seed, cfg->scale_bits};
     if (int rc = tile_cand_prepare(g, H, cfg->seed, cfg->scale_bits, key, nullptr)) return rc;
-    a.tile_cand = 1;
+    a.tile_cand = (cfg->flags & TCMIS_F_TILE_UMMA) ? 2 : 1;
     a.up_tiles = g->up_tiles;
     a.up_trow = g->d_up_trow;
     a.up_tcol = g->d_up_tcol;

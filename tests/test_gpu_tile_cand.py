@@ -1,7 +1,9 @@
 """GPU: Phase 1 as a tile x bit-vector product (TCMIS_F_TILE_CAND,
 csrc/tile_cand.cu): the oriented adjacency A-up in the compact T = 16 store
-times the round's alive bitmap gives compute_max_np + generate_candidates
-(engine.cpp:86-119) bit for bit, so whole solves equal the reference's."""
+times the round's alive bitmap -- on CUDA cores, or on the tensor cores with
+TCMIS_F_TILE_UMMA (tcgen05.mma kind::i8, TMEM accumulator) -- gives
+compute_max_np + generate_candidates (engine.cpp:86-119) bit for bit, so
+whole solves equal the reference's."""
 import numpy as np
 import pytest
 
@@ -45,13 +47,16 @@ def test_tile_phase1_bit_exact(ctx, kind, args, thr, gate, monkeypatch):
     for heur in HEUR:
         for seed in (1, 9):
             exp = O.solve(g, heur, seed, tile_dim=16)
-            for excl in (tc.Exclusion.AUTO, tc.Exclusion.PUSH, tc.Exclusion.CSR_PULL,
-                         tc.Exclusion.TILE_BITS, tc.Exclusion.TILE_MMA):
+            for excl, umma in ((tc.Exclusion.AUTO, False), (tc.Exclusion.PUSH, False),
+                               (tc.Exclusion.CSR_PULL, False), (tc.Exclusion.TILE_BITS, False),
+                               (tc.Exclusion.TILE_MMA, False), (tc.Exclusion.AUTO, True),
+                               (tc.Exclusion.CSR_PULL, True)):
                 for host_loop in (False, True):
+                    flags = tc.F_TILE_CAND | (tc.F_TILE_UMMA if umma else 0)
                     cfg = tc.EngineConfig(heuristic=HEUR[heur], seed=seed, exclusion=excl,
-                                          host_loop=host_loop, flags=tc.F_TILE_CAND)
+                                          host_loop=host_loop, flags=flags)
                     got = tc.run_mis(dg, cfg)
-                    where = (kind, heur, seed, excl, host_loop)
+                    where = (kind, heur, seed, excl, umma, host_loop)
                     assert np.array_equal(got.mis, exp.mis), where
                     assert rounds_tuple(got.iterations) == oracle_tuple(exp), where
     dg.close()

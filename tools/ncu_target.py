@@ -13,6 +13,12 @@ if order != "none":
     dg.reorder({"degree": tc.DeviceGraph.ORDER_DEGREE, "spatial": tc.DeviceGraph.ORDER_SPATIAL}[order])
 ex = {"auto": tc.Exclusion.AUTO, "push": tc.Exclusion.PUSH, "pull": tc.Exclusion.CSR_PULL,
       "tile-bits": tc.Exclusion.TILE_BITS, "tile-mma": tc.Exclusion.TILE_MMA}[os.environ.get("EXCL", "auto")]
+# env CAND = csr | tile | tile-umma: Phase 1 form (tile forms: A-up prepared outside)
+cand = os.environ.get("CAND", "csr")
+flags = {"csr": 0, "tile": tc.F_TILE_CAND, "tile-umma": tc.F_TILE_CAND | tc.F_TILE_UMMA}[cand]
+cfg = tc.EngineConfig(heuristic=tc.Heuristic.H2, host_loop=True, exclusion=ex, flags=flags)
+if flags:
+    dg.tile_cand_prepare(cfg)
 for _ in range(2):
-    r = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, host_loop=True, exclusion=ex))
+    r = tc.run_mis(dg, cfg)
 print("ok", r.cardinality(), len(r.iterations))
