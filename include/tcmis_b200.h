@@ -319,8 +319,9 @@ int tcmis_solve_partitioned(tcmis_graph *part, tcmis_exchange *x, const int32_t 
  * rounds, out[1] total host time spent enqueueing rounds (graph launches or
  * direct launches + exchange calls), out[2] total time the host waited for
  * round counters, out[3] wall time of the round loop (all us), out[4] rounds
- * enqueued with id lists. */
-int tcmis_partitioned_profile(const tcmis_graph *part, double out[5]);
+ * enqueued with id lists, out[5] rounds run by the single-device tail (the
+ * alive subgraph gathered on every rank once it fits k_tail). */
+int tcmis_partitioned_profile(const tcmis_graph *part, double out[6]);
 
 /* h1_random (priorities.cpp:33-41) without a graph: n priorities on the
  * device of the context, copied to p_out[n]. */

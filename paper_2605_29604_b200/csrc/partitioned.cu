@@ -38,6 +38,7 @@
 #include <nccl.h>  // types only: the library is bound with dlopen
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <condition_variable>
 #include <cstdlib>
@@ -55,7 +56,13 @@
 namespace tcmis_b200 {
 
 int solve_prepare(tcmis_graph *g, const tcmis_config *cfg, RoundArgs &a, int64_t own_isolated);
+int tail_grid(tcmis_ctx *ctx);
+constexpr int64_t kTailBlockPart = 1024;  // k_tail's per-block list capacity (tail.cuh kTailBlock)
 int seg_total(tcmis_graph *g, int64_t *ev);
+int partitioned_tail(tcmis_graph *g, const RoundArgs &ra, int32_t round0, const int32_t *ids,
+                     int32_t A, int64_t *sub_off, int32_t *sub_nbr, int64_t E,
+                     const int32_t *rowtiles_global, int64_t total_tiles_global,
+                     std::vector<DevRound> &out);
 
 // ------------------------------------------------------------------ NCCL
 
@@ -149,6 +156,15 @@ struct LocalGroup {
 
 // The exchange a partitioned solve talks through (one handle per rank).
 struct tcmis_exchange {
+  // a process-unique id: the per-graph buffers and captured round graphs are
+  // keyed on it (a pointer could be re-used by the next exchange object, and
+  // a cache hit on some ranks but not on others would desynchronise their
+  // collectives)
+  uint64_t uid = next_uid();
+  static uint64_t next_uid() {
+    static std::atomic<uint64_t> c{1};
+    return c.fetch_add(1);
+  }
   int kind = 0;  // 1 NCCL, 2 in-process group
   int32_t world = 1, rank = 0;
   bool capturable = false;
@@ -185,8 +201,15 @@ int x_all_gather(tcmis_exchange *x, const void *send, void *recv, size_t bytes, 
   if (!G.barrier()) return set_error(TCMIS_E_RUNTIME, "a peer rank of the in-process group failed");
   for (int q = 0; q < G.world; ++q) {
     TCMIS_CUDA(cudaStreamWaitEvent(st, G.ready[q], 0));
-    TCMIS_CUDA(cudaMemcpyAsync(static_cast<char *>(recv) + (size_t)q * bytes, G.send[q], bytes,
-                               cudaMemcpyDefault, st));
+    const cudaError_t e = cudaMemcpyAsync(static_cast<char *>(recv) + (size_t)q * bytes,
+                                          G.send[q], bytes, cudaMemcpyDefault, st);
+    if (e != cudaSuccess) {
+      G.abort();
+      return set_error(TCMIS_E_CUDA, std::string("in-process all-gather (rank ") +
+                                         std::to_string(me) + " <- " + std::to_string(q) +
+                                         ", " + std::to_string(bytes) + " bytes): " +
+                                         cudaGetErrorString(e));
+    }
   }
   TCMIS_CUDA(cudaEventRecord(G.done[me], st));
   // every rank enqueued its copies: the send buffers may be reused after done[]
@@ -312,6 +335,83 @@ __global__ void k_ring(const int64_t *__restrict__ buf, const Ctrl *__restrict__
   __threadfence_system();
 }
 
+// ---- the tail: the alive subgraph gathered on every rank (partitioned_tail)
+
+struct IsAliveV {
+  const uint8_t *s;
+  __device__ __forceinline__ bool operator()(int32_t v) const { return s[v] == TCMIS_ALIVE; }
+};
+
+// warp per own alive row: its alive neighbours counted (kFill false) or
+// written in row order (kFill true)
+template <bool kFill>
+__global__ void k_alive_rows(int32_t A, const int32_t *__restrict__ ids,
+                             const int64_t *__restrict__ off, const int32_t *__restrict__ nbr,
+                             const uint8_t *__restrict__ state, int32_t *__restrict__ deg,
+                             const int64_t *__restrict__ doff, int32_t *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < A;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int32_t v = ids[i];
+    const int64_t s0 = off[v], e0 = off[v + 1];
+    int64_t base = kFill ? doff[i] : 0;
+    int32_t cnt = 0;
+    for (int64_t k0 = s0; k0 < e0; k0 += 32) {
+      const int64_t k = k0 + lane;
+      const int32_t u = k < e0 ? __ldg(&nbr[k]) : -1;
+      const bool keep = u >= 0 && state[u] == TCMIS_ALIVE;
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (kFill && keep) out[base + __popc(m & ((1u << lane) - 1u))] = u;
+      base += __popc(m);
+      cnt += __popc(m);
+    }
+    if (!kFill && lane == 0) deg[i] = cnt;
+  }
+}
+
+__global__ void k_widen(int32_t A, const int32_t *__restrict__ d32, int64_t *__restrict__ d64) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= A;
+       i += (int64_t)gridDim.x * blockDim.x)
+    d64[i] = i < A ? d32[i] : 0;
+}
+
+// rank r's padded slices -> the concatenation (rank order = ascending ids)
+__global__ void k_concat(int32_t world, int64_t stride, const int32_t *__restrict__ gathered,
+                         const int64_t *__restrict__ pref, int32_t *__restrict__ out) {
+  for (int r = 0; r < world; ++r) {
+    const int64_t cnt = pref[r + 1] - pref[r];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x)
+      out[pref[r] + i] = gathered[(int64_t)r * stride + i];
+  }
+}
+
+// global ids -> positions in the ascending alive list
+__global__ void k_to_sub(int64_t E, int32_t *__restrict__ nbr, const int32_t *__restrict__ ids,
+                         int32_t A) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = nbr[k];
+    int32_t lo = 0, hi = A;
+    while (lo < hi) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (__ldg(&ids[mid]) < u) lo = mid + 1;
+      else hi = mid;
+    }
+    nbr[k] = lo;
+  }
+}
+
+__global__ void k_sum_slices(int32_t world, int64_t nb, const int32_t *__restrict__ gathered,
+                             int32_t *__restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t t = 0;
+    for (int r = 0; r < world; ++r) t += gathered[(int64_t)r * nb + i];
+    out[i] = t;
+  }
+}
+
 // per-rank buffers of a partitioned solve, kept on the graph's DistState
 struct PartBufs {
   int32_t maxw = 0, world = 0;
@@ -322,6 +422,8 @@ struct PartBufs {
   int32_t *d_rank_lo = nullptr;
   RingEntry *h_ring = nullptr, *d_ring = nullptr;
   std::map<int32_t, cudaGraphExec_t> graphs;  // per publish capacity (0 = dense)
+  int32_t *rowtiles_global = nullptr;         // the tail's tile counts of every block row
+  int64_t total_tiles_global = -1;
   std::vector<unsigned char> key;             // what the graphs were captured for
 };
 
@@ -333,6 +435,7 @@ void free_bufs(PartBufs &b) {
   dev_free(b.lgathered);
   dev_free(b.counts);
   dev_free(b.d_rank_lo);
+  dev_free(b.rowtiles_global);
   if (b.h_ring) cudaFreeHost(b.h_ring);
   for (auto &kv : b.graphs) cudaGraphExecDestroy(kv.second);
   b = PartBufs{};
@@ -349,7 +452,7 @@ std::mutex &bufs_mu() {
 
 // host-side profile of the last partitioned solve of a graph
 struct PartProfile {
-  int32_t rounds = 0, sparse_rounds = 0;
+  int32_t rounds = 0, sparse_rounds = 0, tail_rounds = 0;
   double enqueue_us = 0, wait_us = 0, rounds_us = 0;
 };
 std::map<const tcmis_graph *, PartProfile> &profiles() {
@@ -465,6 +568,156 @@ int launch_round(tcmis_graph *g, tcmis_exchange *x, RoundArgs &a, PartBufs &b, i
   return 0;
 }
 
+// The late rounds on one device per rank: every rank gathers the alive
+// subgraph (each rank contributes its own alive rows, restricted to alive
+// neighbours: two all-gathers of padded slices after one of the counts) and
+// runs the same k_tail on it (solver.cu partitioned_tail).  round0 is the
+// first round the tail runs.
+int run_tail(tcmis_graph *g, tcmis_exchange *x, const RoundArgs &a, PartBufs &b,
+             int32_t round0, std::vector<DevRound> &tail_rounds) {
+  tcmis_ctx *ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  Workspace &ws = g->ws;
+  const int world = x->world;
+  const int32_t lo = g->part_lo, own = g->part_hi - g->part_lo;
+  // tile counts of every block row and the global tile total (cached)
+  if (a.seg_mode == 1 && !b.rowtiles_global) {
+    const int64_t nb = g->tile_nb;
+    int32_t *gath = nullptr;
+    if (int rc = dev_alloc(&gath, (size_t)nb * world + 1)) return rc;
+    if (int rc = dev_alloc(&b.rowtiles_global, (size_t)nb + 1)) return rc;
+    if (int rc = x_all_gather(x, g->d_rowtiles, gath, 4ull * nb, st)) return rc;
+    k_sum_slices<<<grid_for(ctx, nb, 256, 8), 256, 0, st>>>(world, nb, gath, b.rowtiles_global);
+    TCMIS_LAUNCHED(ctx);
+    TCMIS_CUDA(cudaMemcpyAsync(b.counts, &g->tile_total, 8, cudaMemcpyHostToDevice, st));
+    if (int rc = x_all_reduce(x, b.counts, 1, st)) return rc;
+    TCMIS_CUDA(cudaMemcpyAsync(&b.total_tiles_global, b.counts, 8, cudaMemcpyDeviceToHost, st));
+    TCMIS_CUDA(cudaStreamSynchronize(st));
+    dev_free(gath);
+  }
+  // own alive rows, restricted to alive neighbours
+  int32_t *own_ids = nullptr, *own_deg = nullptr, *own_nbr = nullptr;
+  int64_t *own_off = nullptr, *d_cnt = nullptr;
+  struct Frees {
+    std::vector<void *> p;
+    ~Frees() {
+      for (void *q : p) dev_free(q);
+    }
+  } frees;
+  if (int rc = dev_alloc(&own_ids, (size_t)own + 1)) return rc;
+  frees.p.push_back(own_ids);
+  if (int rc = dev_alloc(&d_cnt, 2)) return rc;
+  frees.p.push_back(d_cnt);
+  {
+    thrust::counting_iterator<int32_t> it(lo);
+    size_t bytes = ws.cub_bytes;
+    TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, it, own_ids, d_cnt, (int)own,
+                                     IsAliveV{ws.state}, st));
+    ctx->launches++;
+  }
+  int64_t h_a = 0;
+  TCMIS_CUDA(cudaMemcpyAsync(&h_a, d_cnt, 8, cudaMemcpyDeviceToHost, st));
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  const int32_t a_r = (int32_t)h_a;
+  if (int rc = dev_alloc(&own_deg, (size_t)a_r + 1)) return rc;
+  frees.p.push_back(own_deg);
+  if (int rc = dev_alloc(&own_off, (size_t)a_r + 1)) return rc;
+  frees.p.push_back(own_off);
+  k_alive_rows<false><<<grid_for(ctx, 32ll * std::max(a_r, 1), 256, 8), 256, 0, st>>>(
+      a_r, own_ids, g->d_off, g->d_nbr, ws.state, own_deg, nullptr, nullptr);
+  TCMIS_LAUNCHED(ctx);
+  k_widen<<<grid_for(ctx, (int64_t)a_r + 1, 256, 8), 256, 0, st>>>(a_r, own_deg, own_off);
+  TCMIS_LAUNCHED(ctx);
+  {
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, own_off, own_off, (int64_t)a_r + 1, st);
+    void *tmp = nullptr;
+    if (int rc = dev_alloc((char **)&tmp, bytes)) return rc;
+    TCMIS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, own_off, own_off, (int64_t)a_r + 1, st));
+    ctx->launches++;
+    dev_free(tmp);
+  }
+  // counts of every rank (int64 pairs)
+  int64_t *cnts = nullptr;
+  if (int rc = dev_alloc(&cnts, 2ull * world + 2)) return rc;
+  frees.p.push_back(cnts);
+  TCMIS_CUDA(cudaMemcpyAsync(d_cnt + 1, own_off + a_r, 8, cudaMemcpyDeviceToDevice, st));
+  if (int rc = x_all_gather(x, d_cnt, cnts, 16, st)) return rc;
+  std::vector<int64_t> h_cnts(2 * (size_t)world);
+  TCMIS_CUDA(cudaMemcpyAsync(h_cnts.data(), cnts, 16ull * world, cudaMemcpyDeviceToHost, st));
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  std::vector<int64_t> pa(world + 1, 0), pe(world + 1, 0);
+  int64_t maxa = 1, maxe = 1;
+  for (int r = 0; r < world; ++r) {
+    pa[r + 1] = pa[r] + h_cnts[2 * r];
+    pe[r + 1] = pe[r] + h_cnts[2 * r + 1];
+    maxa = std::max(maxa, h_cnts[2 * r]);
+    maxe = std::max(maxe, h_cnts[2 * r + 1]);
+  }
+  const int32_t A = (int32_t)pa[world];
+  const int64_t E = pe[world];
+  const int64_t e_r = h_cnts[2 * x->rank + 1];
+  if (int rc = dev_alloc(&own_nbr, (size_t)maxe)) return rc;
+  frees.p.push_back(own_nbr);
+  k_alive_rows<true><<<grid_for(ctx, 32ll * std::max(a_r, 1), 256, 8), 256, 0, st>>>(
+      a_r, own_ids, g->d_off, g->d_nbr, ws.state, nullptr, own_off, own_nbr);
+  TCMIS_LAUNCHED(ctx);
+  (void)e_r;
+  // padded all-gathers of ids, degrees, neighbour lists
+  int32_t *send = nullptr, *g_ids = nullptr, *g_deg = nullptr, *g_nbr = nullptr;
+  if (int rc = dev_alloc(&send, (size_t)maxa)) return rc;
+  frees.p.push_back(send);
+  if (int rc = dev_alloc(&g_ids, (size_t)maxa * world)) return rc;
+  frees.p.push_back(g_ids);
+  if (int rc = dev_alloc(&g_deg, (size_t)maxa * world)) return rc;
+  frees.p.push_back(g_deg);
+  if (int rc = dev_alloc(&g_nbr, (size_t)maxe * world)) return rc;
+  frees.p.push_back(g_nbr);
+  if (a_r) TCMIS_CUDA(cudaMemcpyAsync(send, own_ids, 4ull * a_r, cudaMemcpyDeviceToDevice, st));
+  if (int rc = x_all_gather(x, send, g_ids, 4ull * maxa, st)) return rc;
+  if (a_r) TCMIS_CUDA(cudaMemcpyAsync(send, own_deg, 4ull * a_r, cudaMemcpyDeviceToDevice, st));
+  if (int rc = x_all_gather(x, send, g_deg, 4ull * maxa, st)) return rc;
+  if (int rc = x_all_gather(x, own_nbr, g_nbr, 4ull * maxe, st)) return rc;
+  // the subgraph: ids ascending (rank order), offsets, neighbours as sub ids
+  int64_t *d_pref = nullptr;
+  if (int rc = dev_alloc(&d_pref, 2ull * (world + 1))) return rc;
+  frees.p.push_back(d_pref);
+  TCMIS_CUDA(cudaMemcpyAsync(d_pref, pa.data(), 8ull * (world + 1), cudaMemcpyHostToDevice, st));
+  TCMIS_CUDA(cudaMemcpyAsync(d_pref + world + 1, pe.data(), 8ull * (world + 1),
+                             cudaMemcpyHostToDevice, st));
+  int32_t *sub_ids = nullptr, *sub_deg = nullptr, *sub_nbr = nullptr;
+  int64_t *sub_off = nullptr;
+  if (int rc = dev_alloc(&sub_ids, (size_t)A + 1)) return rc;
+  frees.p.push_back(sub_ids);
+  if (int rc = dev_alloc(&sub_deg, (size_t)A + 1)) return rc;
+  frees.p.push_back(sub_deg);
+  if (int rc = dev_alloc(&sub_off, (size_t)A + 1)) return rc;  // owned by the subgraph
+  if (int rc = dev_alloc(&sub_nbr, (size_t)std::max<int64_t>(E, 1))) {
+    dev_free(sub_off);
+    return rc;
+  }
+  k_concat<<<grid_for(ctx, maxa, 256, 8), 256, 0, st>>>(world, maxa, g_ids, d_pref, sub_ids);
+  k_concat<<<grid_for(ctx, maxa, 256, 8), 256, 0, st>>>(world, maxa, g_deg, d_pref, sub_deg);
+  k_concat<<<grid_for(ctx, maxe, 256, 8), 256, 0, st>>>(world, maxe, g_nbr, d_pref + world + 1,
+                                                       sub_nbr);
+  k_widen<<<grid_for(ctx, (int64_t)A + 1, 256, 8), 256, 0, st>>>(A, sub_deg, sub_off);
+  k_to_sub<<<grid_for(ctx, std::max<int64_t>(E, 1), 256, 8), 256, 0, st>>>(E, sub_nbr, sub_ids, A);
+  ctx->launches += 5;
+  {
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, sub_off, sub_off, (int64_t)A + 1, st);
+    void *tmp = nullptr;
+    if (int rc = dev_alloc((char **)&tmp, bytes)) return rc;
+    TCMIS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, sub_off, sub_off, (int64_t)A + 1, st));
+    ctx->launches++;
+    dev_free(tmp);
+  }
+  TCMIS_CUDA(cudaGetLastError());
+  return partitioned_tail(g, a, round0, sub_ids, A, sub_off, sub_nbr, E,
+                          a.seg_mode == 1 ? b.rowtiles_global : g->d_rowtiles,
+                          a.seg_mode == 1 ? b.total_tiles_global : g->tile_total, tail_rounds);
+}
+
 int32_t pow2_at_least(int64_t x) {
   int64_t c = 256;
   while (c < x) c <<= 1;
@@ -516,10 +769,10 @@ int solve_partitioned_impl(tcmis_graph *g, tcmis_exchange *x, const int32_t *ran
   int32_t maxw = 1;
   for (int r = 0; r < world; ++r) maxw = std::max(maxw, (rank_lo[r + 1] - rank_lo[r] + 31) / 32);
   // buffers and graphs are per (layout, round arguments, exchange)
-  std::vector<unsigned char> key(sizeof(RoundArgs) + sizeof(void *) + 4 * (world + 1));
+  std::vector<unsigned char> key(sizeof(RoundArgs) + sizeof(uint64_t) + 4 * (world + 1));
   std::memcpy(key.data(), &a, sizeof(a));
-  std::memcpy(key.data() + sizeof(a), &x, sizeof(void *));
-  std::memcpy(key.data() + sizeof(a) + sizeof(void *), rank_lo, 4 * (world + 1));
+  std::memcpy(key.data() + sizeof(a), &x->uid, sizeof(uint64_t));
+  std::memcpy(key.data() + sizeof(a) + sizeof(uint64_t), rank_lo, 4 * (world + 1));
   if (b.key != key) {
     free_bufs(b);
     b.key = key;
@@ -580,13 +833,27 @@ int solve_partitioned_impl(tcmis_graph *g, tcmis_exchange *x, const int32_t *ran
     enqueue_us += std::chrono::duration<double, std::micro>(clk::now() - t0).count();
     return rc;
   };
+  // the late rounds on one device per rank (run_tail) once the alive count
+  // fits k_tail: round it+1 is not enqueued when the alive count after round
+  // it-1 (a bound of the one after round it) is that small.  Off by default:
+  // gathering the subgraph costs ~0.3 ms of host round trips and
+  // allocations, measured on one device (s22 1.17 -> 1.41 ms, s26 8.9 ->
+  // 9.2 ms at world 1), which 2-3 late exchange rounds do not cost; it pays
+  // for graphs with many late rounds on many GPUs.  TCMIS_PART_TAIL = the
+  // alive threshold (capped at k_tail's capacity).
+  int64_t tail_thr = 0;
+  if (const char *env = std::getenv("TCMIS_PART_TAIL")) tail_thr = std::atoll(env);
+  tail_thr = std::min<int64_t>(tail_thr, (int64_t)tail_grid(ctx) * kTailBlockPart);
+  std::vector<DevRound> tail_rounds;
+  int32_t tail_from = 0;  // first round run by the tail (0: none)
   if (int rc = timed_launch(0)) return rc;
   bool done = false;
   int32_t rounds_run = 0;
   for (int32_t it = 1; !done; ++it) {
     if (it > cap_rounds)
       return set_error(TCMIS_E_RUNTIME, "iteration cap exceeded; engine livelock");
-    if (it < cap_rounds) {
+    const bool to_tail = tail_thr > 0 && it >= 2 && alive_prev[0] <= tail_thr;
+    if (it < cap_rounds && !to_tail) {
       const int32_t c = choose(alive_prev[0]);
       sparse_rounds += c ? 1 : 0;
       if (int rc = timed_launch(c)) return rc;
@@ -604,6 +871,22 @@ int solve_partitioned_impl(tcmis_graph *g, tcmis_exchange *x, const int32_t *ran
     alive_prev[0] = e.v[2];
     rounds_run = it;
     done = e.v[2] == 0;
+    if (!done && to_tail) {
+      TCMIS_CUDA(cudaStreamSynchronize(st));
+      if (int rc = run_tail(g, x, a, b, it + 1, tail_rounds)) return rc;
+      tail_from = it + 1;
+      for (const DevRound &d : tail_rounds) {
+        RingEntry t{};
+        t.round = ++rounds_run;
+        t.v[0] = (int64_t)d.sel;
+        t.v[1] = (int64_t)d.rem;
+        t.v[2] = (int64_t)d.alive;
+        t.v[3] = (int64_t)d.eval;
+        t.v[4] = (int64_t)d.skip;
+        got.push_back(t);
+      }
+      done = true;
+    }
   }
   TCMIS_CUDA(cudaStreamSynchronize(st));  // the extra (empty) round too
 
@@ -616,6 +899,7 @@ int solve_partitioned_impl(tcmis_graph *g, tcmis_exchange *x, const int32_t *ran
     pf.wait_us = wait_us;
     pf.rounds_us = std::chrono::duration<double, std::micro>(t_rounds - t_start).count();
     pf.sparse_rounds = sparse_rounds;
+    pf.tail_rounds = (int32_t)tail_rounds.size();
   }
   // every rank now holds the final state of all n vertices (own decisions +
   // the applied remote ones): the ascending MIS from one compaction -- of all
@@ -640,11 +924,13 @@ int solve_partitioned_impl(tcmis_graph *g, tcmis_exchange *x, const int32_t *ran
     TCMIS_CUDA(cudaMemcpyAsync(state_out, ws.state + out_lo, (size_t)(out_hi - out_lo),
                                cudaMemcpyDeviceToHost, st));
   // this rank's phase stamps (the reference's timers, engine.cpp:253-284)
-  std::vector<DevRound> stamps((size_t)std::min(rounds_run, ws.round_cap));
+  const int32_t own_rounds = tail_from ? tail_from - 1 : rounds_run;
+  std::vector<DevRound> stamps((size_t)std::min(own_rounds, ws.round_cap));
   if (!stamps.empty())
     TCMIS_CUDA(cudaMemcpyAsync(stamps.data(), ws.rounds, sizeof(DevRound) * stamps.size(),
                                cudaMemcpyDeviceToHost, st));
   TCMIS_CUDA(cudaStreamSynchronize(st));
+  stamps.insert(stamps.end(), tail_rounds.begin(), tail_rounds.end());  // the tail's stamps
   auto span_ms = [](unsigned long long a0, unsigned long long a1) {
     return (a0 && a1 && a1 > a0) ? (double)(a1 - a0) * 1e-6 : 0.0;
   };
@@ -818,7 +1104,7 @@ TCMIS_API int tcmis_solve_partitioned(tcmis_graph *part, tcmis_exchange *x, cons
   return rc;
 }
 
-TCMIS_API int tcmis_partitioned_profile(const tcmis_graph *part, double out[5]) {
+TCMIS_API int tcmis_partitioned_profile(const tcmis_graph *part, double out[6]) {
   NEED(part && out, "null handle");
   std::lock_guard<std::mutex> lk(bufs_mu());
   auto it = profiles().find(part);
@@ -828,5 +1114,6 @@ TCMIS_API int tcmis_partitioned_profile(const tcmis_graph *part, double out[5]) 
   out[2] = it->second.wait_us;
   out[3] = it->second.rounds_us;
   out[4] = it->second.sparse_rounds;
+  out[5] = it->second.tail_rounds;
   return 0;
 }

@@ -1444,6 +1444,119 @@ int states_in_caller_order(tcmis_graph *g) {
   return 0;
 }
 
+// ----------------------------------------------- partitioned solve's tail
+
+// the alive subgraph's starting state from the rank's replicated vectors
+__global__ void k_sub_init(int32_t A, const int32_t *__restrict__ ids,
+                           const uint32_t *__restrict__ prio, const uint16_t *__restrict__ q,
+                           uint32_t *__restrict__ sprio, uint16_t *__restrict__ sq,
+                           uint8_t *__restrict__ sstate, uint8_t *__restrict__ snext,
+                           int32_t *__restrict__ wl) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = ids[i];
+    sprio[i] = prio[v];
+    sq[i] = q[v];
+    sstate[i] = TCMIS_ALIVE;
+    snext[i] = 0;
+    wl[i] = (int32_t)i;
+  }
+}
+
+__global__ void k_sub_scatter(int32_t A, const int32_t *__restrict__ ids,
+                              const uint8_t *__restrict__ sstate, uint8_t *__restrict__ state,
+                              uint16_t *__restrict__ q) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = ids[i];
+    const uint8_t s = sstate[i];
+    state[v] = s;
+    if (s == TCMIS_REMOVED) q[v] = 0;
+  }
+}
+
+// The late rounds of a partitioned solve on ONE device (partitioned.cu): the
+// alive subgraph -- sub vertex i = the caller's vertex ids[i], ids ascending,
+// so the key order of (p, id) is kept; rows hold only alive neighbours (a
+// vertex with an InMIS neighbour is not alive, removed ones are invisible) --
+// gets the rank's priorities and runs all remaining rounds in one k_tail, its
+// tile counters flagging the caller's block columns against the GLOBAL
+// per-block-row tile counts.  The rounds are the global rounds (every rank
+// runs the same tail redundantly); their statistics go to `out`, the final
+// states back into the rank's replicated state.  Takes ownership of
+// sub_off / sub_nbr.
+int partitioned_tail(tcmis_graph *g, const RoundArgs &ra, int32_t round0, const int32_t *ids,
+                     int32_t A, int64_t *sub_off, int32_t *sub_nbr, int64_t E,
+                     const int32_t *rowtiles_global, int64_t total_tiles_global,
+                     std::vector<DevRound> &out) {
+  tcmis_ctx *ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  tcmis_graph *sub = nullptr;
+  if (int rc = wrap_owned(ctx, A, E, sub_off, sub_nbr, &sub)) return rc;
+  struct Guard {
+    tcmis_graph *h;
+    ~Guard() { tcmis_graph_destroy(h); }
+  } guard{sub};
+  if (int rc = ensure_workspace(sub)) return rc;
+  Workspace &ws = sub->ws;
+  Workspace &gw = g->ws;
+  const int par = round0 & 1;
+  k_sub_init<<<grid_for(ctx, A, 256, 8), 256, 0, st>>>(A, ids, gw.prio, gw.q, ws.prio, ws.q,
+                                                       ws.state, ws.next, ws.wl[par]);
+  TCMIS_LAUNCHED(ctx);
+  Ctrl c0{};
+  c0.round = round0;
+  c0.wl_count[par] = A;
+  c0.alive = A;
+  c0.max_rounds = ws.round_cap;
+  *ws.h_ctrl = c0;
+  TCMIS_CUDA(cudaMemcpyAsync(ws.ctrl, ws.h_ctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+  TCMIS_CUDA(cudaMemsetAsync(ws.rounds, 0, sizeof(DevRound) * ws.round_cap, st));
+  if (ra.seg_mode == 1) TCMIS_CUDA(cudaMemsetAsync(gw.segmark, 0, 4ull * ra.nseg, st));
+  RoundArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.n = A;
+  a.off = sub->d_off;
+  a.nbr = sub->d_nbr;
+  a.vnnz = ((uintptr_t)sub->d_nbr & 15) == 0 ? E : -E;
+  a.T = ra.T;
+  a.seg_mode = ra.seg_mode;
+  a.nseg = ra.nseg;
+  a.total_tiles = total_tiles_global;
+  a.rowtiles = rowtiles_global;
+  a.perm = ids;  // sub id -> caller id: ties, tile columns
+  a.tail_grid = tail_grid(ctx);
+  TailArgs t = tail_args(sub, a);
+  t.segflag = gw.segflag;  // the caller's block columns (rank-sized arrays)
+  t.segmark = gw.segmark;
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(a.tail_grid);
+  lc.blockDim = dim3(kTailBlock);
+  lc.dynamicSmemBytes = kTailDynSmem;
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  TCMIS_CUDA(cudaLaunchKernelEx(&lc, k_tail, t));
+  ctx->launches++;
+  k_sub_scatter<<<grid_for(ctx, A, 256, 8), 256, 0, st>>>(A, ids, ws.state, gw.state, gw.q);
+  TCMIS_LAUNCHED(ctx);
+  TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  TCMIS_CUDA(cudaStreamSynchronize(st));
+  if (ws.h_ctrl->overflow)
+    return set_error(TCMIS_E_RUNTIME, "partitioned tail: more rounds than the statistics ring");
+  if (ws.h_ctrl->corrupt)
+    return set_error(TCMIS_E_LOGIC, "partitioned tail: a round's counts do not add up");
+  const int32_t rr = ws.h_ctrl->round - round0;  // the tail's rounds
+  out.resize((size_t)std::max(rr, 0));
+  if (rr > 0)
+    TCMIS_CUDA(cudaMemcpy(out.data(), ws.rounds + (round0 - 1), sizeof(DevRound) * rr,
+                          cudaMemcpyDeviceToHost));
+  return 0;
+}
+
 int priorities_impl(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bits,
                     uint32_t *p_out) {
   if (heuristic == TCMIS_H1) {

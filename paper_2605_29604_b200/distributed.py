@@ -429,12 +429,13 @@ def part_range(part) -> tuple:
 def native_profile(part) -> dict:
     """Host-side profile of the rank's last native solve (tcmis_partitioned_profile)."""
     import paper_2605_29604_b200 as tc
-    out = (C.c_double * 5)()
+    out = (C.c_double * 6)()
     tc._check(tc.load().tcmis_partitioned_profile(part.h, out))
     r = max(1.0, out[0])
     return {"rounds": int(out[0]), "enqueue_us_per_round": round(out[1] / r, 2),
             "wait_us_per_round": round(out[2] / r, 2),
-            "round_loop_us_per_round": round(out[3] / r, 2), "list_rounds": int(out[4])}
+            "round_loop_us_per_round": round(out[3] / r, 2), "list_rounds": int(out[4]),
+            "tail_rounds": int(out[5])}
 
 
 def solve_native_local(ranks: list, rank_lo: list[int], **kw) -> list:

@@ -80,18 +80,24 @@ def _got(rounds):
 
 @pytest.mark.parametrize("world", [1, 2, 3, 4])
 @pytest.mark.parametrize("cap", [None, "64", "1"])
+@pytest.mark.parametrize("tail", [None, "65536"])
 @pytest.mark.parametrize("spec,heuristic", [(("rmat", 12, 16, 1), "h2"),
                                             (("rmat", 11, 8, 4), "h3"),
                                             (("grid", 64), "h1"),
                                             (("gnp_avg", 5000, 12.0, 3), "luby-perm")])
-def test_native_partitioned_local_group(world, cap, spec, heuristic, monkeypatch):
+def test_native_partitioned_local_group(world, cap, tail, spec, heuristic, monkeypatch):
     """tcmis_solve_partitioned, `world` ranks on cuda:0 (one host thread and
     one context each).  cap = the id-list capacity (TCMIS_PART_CAP test hook):
     None = the default rule (bitmaps on these small graphs), 64 = id lists
     from the round the alive count allows it, 1 = lists that can overflow,
-    which must never be used (the alive bound keeps the slices then)."""
+    which must never be used (the alive bound keeps the slices then).
+    tail: None = every round through the exchange (the default), "65536" =
+    the late rounds on the gathered alive subgraph (k_tail on every rank, from
+    the round after the one whose alive count fits)."""
     if cap is not None:
         monkeypatch.setenv("TCMIS_PART_CAP", cap)
+    if tail is not None:
+        monkeypatch.setenv("TCMIS_PART_TAIL", tail)
     g = O.gen(*spec)
     rank_lo = D.partition_rows(g.off, world, 16)
     ranks = [D.GpuRank(tc.Context(0), g.n, rank_lo[r], rank_lo[r + 1], g.off, g.nbr, "cuda:0")
@@ -144,10 +150,13 @@ def test_native_partitioned_errors():
 
 
 @pytest.mark.parametrize("heuristic", ["h2", "h3", "luby-perm"])
-def test_native_partitioned_nccl_world1(heuristic):
+@pytest.mark.parametrize("tail", [None, "65536"])
+def test_native_partitioned_nccl_world1(heuristic, tail, monkeypatch):
     """tcmis_exchange_nccl on a one-rank communicator (the only NCCL group one
     GPU can form): every round one CUDA graph with the NCCL collectives
     captured in it; repeated solves re-launch the cached round graphs."""
+    if tail is not None:
+        monkeypatch.setenv("TCMIS_PART_TAIL", tail)
     g = O.gen("rmat", 13, 16, 5)
     rank_lo = D.partition_rows(g.off, 1, 16)
     ctx = tc.Context(0)
@@ -160,6 +169,8 @@ def test_native_partitioned_nccl_world1(heuristic):
         assert np.array_equal(res.mis, exp.mis)
     prof = D.native_profile(me.g)
     assert prof["rounds"] == len(exp.rounds) or heuristic == "h3"
+    assert (prof["tail_rounds"] > 0) == (tail is not None and len(exp.rounds) > 2) \
+        or heuristic == "h3"
     print("nccl world-1 host profile:", prof)
     x.close()
     me.close()
