@@ -441,14 +441,21 @@ def kernel_roofline(tc, dg, cfg, kernels, args, ms_per_step):
     total_b = 13 * n + sum(12 * A + 4 * nnzA + 8 * NC + 4 * nnzNC + 2 * A
                            for A, nnzA, NC, nnzNC in traj)
     solve_ach = total_b / (ms_per_step * 1e-3) / 1e9
+    # the second fraction: what the kernels actually moved (ncu DRAM bytes of
+    # the same launches) over the same time -- early exit makes the
+    # algorithmic fraction above overstate the streaming rate
+    traffic_frac = (round(traffic / (dom["ms"] * 1e-3) / 1e9 / hbm, 4)
+                    if traffic and dom["ms"] > 0 else None)
     return {"kernel": f"{dom['phase']}, round {dom['round']}: " + " + ".join(dom["kernels"]),
             "bound": "hbm", "achieved": dom["achieved"], "peak": hbm, "peak_kind": peak_kind,
             "unit": "GB/s", "frac": dom["frac"], "traffic": traffic,
+            "traffic_frac": traffic_frac,
             "algorithmic_bytes": dom["algorithmic_bytes"], "launch_ms": dom["ms"],
             "share_of_step": round(dom["ms"] / ms_per_step, 4),
             "definition": "SURVEY 8(d) algorithmic bytes of the phase-round / summed CUDA-event "
                           "time of its kernels (step-wise timing solve); traffic = ncu DRAM "
-                          "bytes of the same kernels",
+                          "bytes of the same kernels (profiles/ncu_summary.json); traffic_frac "
+                          "= traffic / the same time / peak",
             "phases": phases,
             "solve": {"algorithmic_bytes": int(total_b), "ms": round(ms_per_step, 4),
                       "achieved": round(solve_ach, 1), "frac": round(solve_ach / hbm, 4)}}
