@@ -129,6 +129,8 @@ struct LocalGroup {
   std::vector<const void *> send;
   std::vector<cudaEvent_t> ready, done;
   std::vector<int> device;
+  bool peer_ok = true;  // x_peer_setup's vote
+  int peer_votes = 0;
   bool aborted = false;  // a rank failed: its peers leave the barrier with an error
   bool barrier() {
     std::unique_lock<std::mutex> lk(mu);
@@ -175,6 +177,8 @@ struct tcmis_exchange {
   std::shared_ptr<tcmis_b200::LocalGroup> group;
   int64_t *scratch = nullptr;  // all-reduce staging, world x 8 (device of the rank)
   int scratch_dev = -1;
+  int peer = -1;  // in-process group: apply kernels read the peers' buffers directly (1)
+                  // or through all-gather copies (0); -1 = not yet decided
 };
 
 namespace tcmis_b200 {
@@ -213,6 +217,75 @@ int x_all_gather(tcmis_exchange *x, const void *send, void *recv, size_t bytes, 
   }
   TCMIS_CUDA(cudaEventRecord(G.done[me], st));
   // every rank enqueued its copies: the send buffers may be reused after done[]
+  if (!G.barrier()) return set_error(TCMIS_E_RUNTIME, "a peer rank of the in-process group failed");
+  for (int q = 0; q < G.world; ++q) TCMIS_CUDA(cudaStreamWaitEvent(st, G.done[q], 0));
+  return 0;
+}
+
+// ---- the fused exchange of an in-process group: no all-gather copies; the
+// apply kernels read every rank's published buffer straight from its memory
+// (same device, or a peer over NVLink with peer access enabled)
+struct PeerSlices {
+  const void *p[8];
+};
+constexpr int kPeerMax = 8;
+
+// decided once per exchange, identically on every rank (after a barrier all
+// ranks see every rank's device): peer mode iff every pair of devices can
+// access each other (peer access is enabled here) and world <= kPeerMax
+int x_peer_setup(tcmis_exchange *x, int device) {
+  if (x->peer >= 0) return 0;
+  LocalGroup &G = *x->group;
+  {
+    std::lock_guard<std::mutex> lk(G.mu);
+    if (G.device.size() != (size_t)G.world) G.device.assign(G.world, -1);
+    G.device[x->rank] = device;
+  }
+  if (!G.barrier()) return set_error(TCMIS_E_RUNTIME, "a peer rank of the in-process group failed");
+  bool ok = G.world <= kPeerMax && std::getenv("TCMIS_PART_NO_PEER") == nullptr;
+  for (int q = 0; q < G.world && ok; ++q) {
+    const int d = G.device[q];
+    if (d == device) continue;
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, device, d);
+    if (!can) {
+      ok = false;
+      break;
+    }
+    const cudaError_t e = cudaDeviceEnablePeerAccess(d, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ok = false;
+    cudaGetLastError();
+  }
+  // every rank must take the same decision: AND over the ranks
+  static_assert(sizeof(int) == 4, "");
+  {
+    std::lock_guard<std::mutex> lk(G.mu);
+    G.peer_ok = (G.peer_votes++ == 0 ? ok : (G.peer_ok && ok));
+  }
+  if (!G.barrier()) return set_error(TCMIS_E_RUNTIME, "a peer rank of the in-process group failed");
+  x->peer = G.peer_ok ? 1 : 0;
+  return 0;
+}
+
+// publish `mine`; when this returns, the stream waits for every rank's
+// buffer to be complete, and `out` holds all of them
+int x_share(tcmis_exchange *x, const void *mine, cudaStream_t st, PeerSlices &out) {
+  LocalGroup &G = *x->group;
+  const int me = x->rank;
+  G.send[me] = mine;
+  TCMIS_CUDA(cudaEventRecord(G.ready[me], st));
+  if (!G.barrier()) return set_error(TCMIS_E_RUNTIME, "a peer rank of the in-process group failed");
+  for (int q = 0; q < G.world; ++q) {
+    TCMIS_CUDA(cudaStreamWaitEvent(st, G.ready[q], 0));
+    out.p[q] = G.send[q];
+  }
+  return 0;
+}
+
+// every rank has finished reading every rank's buffer (before any is reused)
+int x_release(tcmis_exchange *x, cudaStream_t st) {
+  LocalGroup &G = *x->group;
+  TCMIS_CUDA(cudaEventRecord(G.done[x->rank], st));
   if (!G.barrier()) return set_error(TCMIS_E_RUNTIME, "a peer rank of the in-process group failed");
   for (int q = 0; q < G.world; ++q) TCMIS_CUDA(cudaStreamWaitEvent(st, G.done[q], 0));
   return 0;
@@ -293,6 +366,58 @@ __global__ void k_apply_words(const uint32_t *__restrict__ gathered,
         state[v] = TCMIS_REMOVED;
         q[v] = 0;
       }
+    }
+  }
+}
+
+// the same two applies reading the publishing ranks' buffers directly
+__global__ void k_apply_words_peer(PeerSlices sl, const int32_t *__restrict__ rank_lo,
+                                   int32_t world, int32_t maxw, int32_t me, int what,
+                                   uint8_t *__restrict__ next, uint8_t *__restrict__ state,
+                                   uint16_t *__restrict__ q) {
+  const int64_t total = (int64_t)world * maxw;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = (int32_t)(w / maxw);
+    if (r == me) continue;
+    const int64_t k = w - (int64_t)r * maxw;
+    uint32_t bits = static_cast<const uint32_t *>(sl.p[r])[k];
+    if (!bits) continue;
+    const int64_t first = rank_lo[r] + k * 32, end = rank_lo[r + 1];
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int64_t v = first + b;
+      if (v >= end) break;
+      if (what == 0) {
+        next[v] = 1;
+        state[v] = TCMIS_IN_MIS;
+      } else {
+        state[v] = TCMIS_REMOVED;
+        q[v] = 0;
+      }
+    }
+  }
+}
+
+__global__ void k_apply_list_peer(PeerSlices sl, int32_t world, int32_t cap, int32_t me,
+                                  int what, uint8_t *__restrict__ next,
+                                  uint8_t *__restrict__ state, uint16_t *__restrict__ q) {
+  const int64_t total = (int64_t)world * cap;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = (int32_t)(i / cap);
+    if (r == me) continue;
+    const int32_t k = (int32_t)(i - (int64_t)r * cap);
+    const int32_t *lst = static_cast<const int32_t *>(sl.p[r]);
+    if (k >= min(lst[0], cap)) continue;
+    const int32_t v = lst[1 + k];
+    if (what == 0) {
+      next[v] = 1;
+      state[v] = TCMIS_IN_MIS;
+    } else {
+      state[v] = TCMIS_REMOVED;
+      q[v] = 0;
     }
   }
 }
@@ -497,7 +622,17 @@ int enqueue_round(tcmis_graph *g, tcmis_exchange *x, RoundArgs &a, PartBufs &b, 
   a.pub_dead = nullptr;
   a.pub_ldead = nullptr;
   if (int rc = launch_select(g, a)) return rc;
-  if (cap) {
+  const bool peer = x->kind == 2 && x->peer == 1;
+  if (peer) {  // fused: the apply reads the ranks' candidate buffers in place
+    PeerSlices sl{};
+    if (int rc = x_share(x, cap ? (const void *)b.lcand : (const void *)b.mine, st, sl)) return rc;
+    if (cap)
+      k_apply_list_peer<<<agrid, 256, 0, st>>>(sl, world, cap, me, 0, ws.next, ws.state, ws.q);
+    else
+      k_apply_words_peer<<<agrid, 256, 0, st>>>(sl, b.d_rank_lo, world, b.maxw, me, 0, ws.next,
+                                                 ws.state, ws.q);
+    if (int rc = x_release(x, st)) return rc;
+  } else if (cap) {
     if (int rc = x_all_gather(x, b.lcand, b.lgathered, 4ull * (cap + 1), st)) return rc;
     k_apply_list<<<agrid, 256, 0, st>>>(b.lgathered, world, cap + 1, me, 0, ws.next, ws.state,
                                          ws.q);
@@ -518,7 +653,16 @@ int enqueue_round(tcmis_graph *g, tcmis_exchange *x, RoundArgs &a, PartBufs &b, 
     a.pub_dead = b.mine;
   }
   if (int rc = launch_update(g, a, 0, 0)) return rc;
-  if (cap) {
+  if (peer) {
+    PeerSlices sl{};
+    if (int rc = x_share(x, cap ? (const void *)b.ldead : (const void *)b.mine, st, sl)) return rc;
+    if (cap)
+      k_apply_list_peer<<<agrid, 256, 0, st>>>(sl, world, cap, me, 1, ws.next, ws.state, ws.q);
+    else
+      k_apply_words_peer<<<agrid, 256, 0, st>>>(sl, b.d_rank_lo, world, b.maxw, me, 1, ws.next,
+                                                 ws.state, ws.q);
+    if (int rc = x_release(x, st)) return rc;
+  } else if (cap) {
     if (int rc = x_all_gather(x, b.ldead, b.lgathered, 4ull * (cap + 1), st)) return rc;
     k_apply_list<<<agrid, 256, 0, st>>>(b.lgathered, world, cap + 1, me, 1, ws.next, ws.state,
                                          ws.q);
@@ -1098,6 +1242,12 @@ TCMIS_API int tcmis_solve_partitioned(tcmis_graph *part, tcmis_exchange *x, cons
   TCMIS_RANGE("tcmis_solve_partitioned");
   TCMIS_CUDA(cudaSetDevice(part->ctx->device));
   t_alloc_stream = part->ctx->stream;
+  if (x->kind == 2 && x->peer < 0) {
+    if (int rc = x_peer_setup(x, part->ctx->device)) {
+      x->group->abort();
+      return rc;
+    }
+  }
   const int rc = solve_partitioned_impl(part, x, rank_lo, world, cfg, state_out, mis_out,
                                         mis_count, stats, max_stats, n_iterations);
   if (rc && x->kind == 2) x->group->abort();  // do not leave the peers in the barrier

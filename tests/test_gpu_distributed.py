@@ -81,11 +81,12 @@ def _got(rounds):
 @pytest.mark.parametrize("world", [1, 2, 3, 4])
 @pytest.mark.parametrize("cap", [None, "64", "1"])
 @pytest.mark.parametrize("tail", [None, "65536"])
+@pytest.mark.parametrize("peer", [True, False])
 @pytest.mark.parametrize("spec,heuristic", [(("rmat", 12, 16, 1), "h2"),
                                             (("rmat", 11, 8, 4), "h3"),
                                             (("grid", 64), "h1"),
                                             (("gnp_avg", 5000, 12.0, 3), "luby-perm")])
-def test_native_partitioned_local_group(world, cap, tail, spec, heuristic, monkeypatch):
+def test_native_partitioned_local_group(world, cap, tail, peer, spec, heuristic, monkeypatch):
     """tcmis_solve_partitioned, `world` ranks on cuda:0 (one host thread and
     one context each).  cap = the id-list capacity (TCMIS_PART_CAP test hook):
     None = the default rule (bitmaps on these small graphs), 64 = id lists
@@ -93,7 +94,12 @@ def test_native_partitioned_local_group(world, cap, tail, spec, heuristic, monke
     which must never be used (the alive bound keeps the slices then).
     tail: None = every round through the exchange (the default), "65536" =
     the late rounds on the gathered alive subgraph (k_tail on every rank, from
-    the round after the one whose alive count fits)."""
+    the round after the one whose alive count fits).
+    peer: the apply kernels read the other ranks' decisions in place (the
+    fused exchange of an in-process group) or from all-gathered copies
+    (TCMIS_PART_NO_PEER)."""
+    if not peer:
+        monkeypatch.setenv("TCMIS_PART_NO_PEER", "1")
     if cap is not None:
         monkeypatch.setenv("TCMIS_PART_CAP", cap)
     if tail is not None:

@@ -8,3 +8,5 @@ for c in rmat22; do
 import json; d=json.loads(open('gpurun_out/part1_$c.json').read().strip().splitlines()[-1])
 print('$c', d['ms_per_step'], d['config']['iterations'], d['config']['mis_size'], d['single_gpu_same_graph'], d['host_profile'], (d['e2e'] or {}).get('ms'))"
 done
+timeout 600 python tools/part_local_ab.py 22 5 > gpurun_out/part_local_ab.txt 2>&1; echo ab=$?
+cat gpurun_out/part_local_ab.txt | tail -8
