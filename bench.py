@@ -190,10 +190,12 @@ def run_ours(args) -> dict:
     log(f"[bench] {args.config}: n={n} m={m} tiles={tiles} (setup {time.time() - t0:.1f}s)")
     order_ms = None
     if args.order == "auto":
-        # measured per config (tools/gpu_order.sh): the
-        # spatial order takes RGG 24M 1.10 -> 0.95 ms, the degree order R-MAT
-        # s26 3.82 -> 3.43 ms; at s22 (q fits L2) and on ER / grid no order helps
-        args.order = {"rgg": "spatial", "rmat26": "degree"}.get(args.config, "none")
+        # measured per config (tools/gpu_order.sh, tools/gpu_cb.sh, DESIGN.md
+        # section 8): the spatial order takes RGG 24M 1.10 -> 0.95 ms; the
+        # degree order with sorted rows and the degree-class bounds takes R-MAT
+        # s22 0.357 -> 0.256 ms and s26 3.82 -> 1.77 ms; ER / grid gain nothing
+        args.order = {"rgg": "spatial", "rmat22": "degree",
+                      "rmat26": "degree"}.get(args.config, "none")
     if args.order != "none":
         # an internal vertex order for the solve kernels (tcmis_graph_reorder):
         # graph preparation like the tiling, outside the timed region, results

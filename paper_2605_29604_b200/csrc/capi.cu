@@ -473,22 +473,10 @@ TCMIS_API int tcmis_graph_permuted(tcmis_graph *g, tcmis_graph **out) {
   } else {
     TCMIS_CUDA(cudaMemsetAsync(off, 0, 8, st));
   }
-  if (g->nnz && g->n) {
-    // rows ascending again (graph.hpp:21 Graph invariant; the tilings merge
-    // sorted rows): a segmented sort of the relabeled rows
-    int32_t *sorted = nullptr;
-    if (int rc = dev_alloc(&sorted, (size_t)g->nnz)) return rc;
-    size_t bytes = 0;
-    cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, nbr, sorted, g->nnz, g->n, off, off + 1, st);
-    void *tmp = nullptr;
-    if (int rc = dev_alloc((char **)&tmp, bytes)) return rc;
-    TCMIS_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp, bytes, nbr, sorted, g->nnz, g->n, off,
-                                                  off + 1, st));
-    g->ctx->launches++;
-    dev_free(tmp);
-    dev_free(nbr);
-    nbr = sorted;
-  }
+  // rows ascending (graph.hpp:21 Graph invariant): reorder_impl sorted the
+  // rows of <= kSortedMax entries, the longer ones here
+  if (g->nnz && g->n)
+    if (int rc = sort_rows(g->ctx, g->n, off, nbr, 2)) return rc;
   TCMIS_CUDA(cudaStreamSynchronize(st));
   return wrap_owned(g->ctx, g->n, g->nnz, off, nbr, out);
 }

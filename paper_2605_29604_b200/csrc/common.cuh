@@ -231,6 +231,17 @@ __device__ __forceinline__ bool blocks(const uint16_t *__restrict__ q,
   return orig_id(perm, u) > orig_id(perm, v);  // the key's id half (priorities.hpp:61-64)
 }
 
+// Degree-class bounds (solver.cu k_class_bounds; a degree-ordered graph under
+// the H2 priorities): for a vertex of degree d, cb[d] = (lo, hi) with every
+// solve id u >= hi of a certainly higher key (p(u) > p(v) whatever the hashes)
+// and every u < lo of a certainly lower one.  Rows are sorted ascending, so a
+// scan from a row's end that reaches an entry below lo has nothing left that
+// could block v or be a candidate above it.  (0, INT_MAX) without bounds:
+// every test below then reduces to the plain one.
+__device__ __forceinline__ int2 class_bounds(const int2 *cb, int64_t deg) {
+  return cb ? __ldg(&cb[deg]) : make_int2(0, 0x7fffffff);
+}
+
 __device__ __forceinline__ uint32_t fresh_prio(int32_t v, uint64_t fresh_m) {
   // engine.cpp:324-325: next round's redrawn h1 priority
   return (uint32_t)(vertex_hash_m((uint64_t)v, fresh_m) >> 32);

@@ -216,6 +216,14 @@ struct tcmis_graph {
   int32_t *d_rnbr = nullptr;
   int32_t *d_rnz = nullptr;   // non-isolated solve ids, ascending
   int32_t rnz_count = 0;
+  // TCMIS_ORDER_DEGREE: the degree classes (solve ids [cls_start[c],
+  // cls_start[c+1]) share one degree, classes in descending degree;
+  // cls_start[n_cls] = n) and, per scale_bits, the class bounds of the H2
+  // priorities (class_bounds.cu): cb[d] = (lo, hi) for a vertex of degree d
+  int32_t *d_cls_start = nullptr;
+  int32_t n_cls = 0;
+  int2 *d_cb = nullptr;
+  int32_t cb_scale_bits = -1;
   int32_t *d_spatial = nullptr;  // tcmis_gen_rgg's points in Z-order of their cells
   // Phase 1 tile form (tile_cand.cu): the A-up store of one priority
   // configuration (heuristic, seed, scale_bits)
@@ -229,6 +237,11 @@ struct tcmis_graph {
 };
 
 namespace tcmis_b200 {
+
+// order.cu: relabeled rows are kept ascending up to this many entries (the
+// select / pull scans stop early on them, common.cuh class_bounds)
+constexpr int64_t kSortedMax = 4096;
+int sort_rows(tcmis_ctx *ctx, int32_t n, const int64_t *off, int32_t *nbr, int which);
 
 // NVTX ranges around the C-ABI calls and the host-driven rounds (header-only
 // NVTX3: free unless a profiler such as nsys / ncu attaches)
@@ -319,6 +332,7 @@ struct RoundArgs {
   const uint16_t *up_tbits;
   const int32_t *perm;  // solve id -> caller id (relabeled CSR), else null
   uint8_t *mis_o;       // relabeled: caller-order membership kept by the kernels, or null
+  const int2 *cb;       // degree-class bounds of the H2 priorities (degree order), or null
   bool operator==(const RoundArgs &o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
 

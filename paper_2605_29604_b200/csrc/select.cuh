@@ -63,7 +63,31 @@ struct SelectArgs {
   uint8_t *mis_o;          // ... and the membership in the caller's order
   int32_t tile_gate;       // > 0: rounds starting with >= this many alive vertices run
                            // Phase 1 as A-up tiles (k_tile_mark), these kernels idle
+  const int2 *cb;          // degree-class bounds (common.cuh class_bounds), or null
 };
+
+// kU row entries of v against the class bounds: in round 1 (everybody alive)
+// an entry >= hi blocks without a gather; entries < lo never block and are
+// not gathered; the rest take the key comparison.  `below`: an examined
+// entry lies under lo, so the rest of the row (smaller ids) cannot block.
+template <int kU>
+__device__ __forceinline__ bool blocks_row(const SelectArgs &a, const int32_t *u, int2 cb,
+                                           bool all_alive, uint32_t qv, int32_t v, bool &below) {
+  bool blocked = false;
+  below = false;
+#pragma unroll
+  for (int j = 0; j < kU; ++j) below |= u[j] >= 0 && u[j] < cb.x;
+  if (all_alive) {
+#pragma unroll
+    for (int j = 0; j < kU; ++j) blocked |= u[j] >= cb.y;
+  }
+  if (!blocked) {
+#pragma unroll
+    for (int j = 0; j < kU; ++j)
+      if (u[j] >= cb.x) blocked |= blocks(a.q, a.prio, u[j], qv, v, a.perm);
+  }
+  return blocked;
+}
 
 // push: every neighbour of a candidate is excluded this round (spmv.cpp:18-59
 // nc > 0, engine.cpp:144-147).  Neighbours of a candidate are never
@@ -90,7 +114,6 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
   if ((int64_t)blockIdx.x * kBlock >= cnt) return;
   const int32_t *wl = round == 1 ? a.nz : ((round & 1) ? a.wl1 : a.wl0);
   const int32_t *__restrict__ nbr = a.nbr;
-  const uint32_t *__restrict__ prio = a.prio;
   const uint16_t *__restrict__ q = a.q;
   const int lane = threadIdx.x & 31;
   WarpOut und{s_und[threadIdx.x >> 5], 0};
@@ -104,15 +127,14 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
       v = (round == 1 && a.nz_identity) ? (int32_t)i : __ldg(&wl[i]);
       const int64_t s = ld_stream(&a.off[v]), e = ld_stream(&a.off[v + 1]);
       const uint32_t qv = __ldg(&q[v]);
+      const int2 cb = class_bounds(a.cb, e - s);
       int32_t u[4];
       load_tail4(nbr, a.vnnz, s, e, u);
-      bool blocked = false;
-#pragma unroll
-      for (int j = 0; j < kProbeK; ++j)
-        if (u[j] >= 0) blocked |= blocks(q, prio, u[j], qv, v, a.perm);
+      bool below;
+      const bool blocked = blocks_row<kProbeK>(a, u, cb, round == 1, qv, v, below);
       if (blocked) {
         // a non-candidate: the pull exclusion finds it on the worklist
-      } else if (e - s <= kProbeK) {
+      } else if (e - s <= kProbeK || (below && !a.push)) {  // push: the whole row in k_select
         mark_candidate(v, a.next, a.state, a.segflag, a.T, a.perm, a.mis_o);
         publish(a.pub, v);
         ++sel;
@@ -147,8 +169,8 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
   const int64_t cnt = ctrl->sel_undec;
   if ((int64_t)blockIdx.x * kBlock >= cnt) return;
   const int32_t *__restrict__ nbr = a.nbr;
-  const uint32_t *__restrict__ prio = a.prio;
   const uint16_t *__restrict__ q = a.q;
+  const bool all_alive = ctrl->round == 1;
   const int64_t stride = (int64_t)gridDim.x * kBlock;
   unsigned long long sel = 0;
   int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x - stride;
@@ -156,6 +178,7 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
   int32_t v = 0;
   int64_t s = 0, e = 0, hi = 0;
   uint32_t qv = 0;
+  int2 cb = make_int2(0, 0);
   auto fetch = [&]() {
     i += stride;
     if (i < cnt) {
@@ -163,6 +186,7 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
       s = __ldg(&a.off[v]);
       e = __ldg(&a.off[v + 1]);
       qv = __ldg(&q[v]);
+      cb = class_bounds(a.cb, e - s);
       hi = e - kProbeK;  // the probe examined the last kProbeK entries
       mode = kScan;
     } else {
@@ -186,14 +210,12 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
           for (int j = 0; j < 4; ++j) u[4 * k + j] = -1;
         }
       }
-      bool blocked = false;
-#pragma unroll
-      for (int j = 0; j < kU; ++j)
-        if (u[j] >= 0) blocked |= blocks(q, prio, u[j], qv, v, a.perm);
+      bool below;
+      const bool blocked = blocks_row<kU>(a, u, cb, all_alive, qv, v, below);
       hi = w;
       if (blocked) {
         mode = kFetch;
-      } else if (hi <= s) {
+      } else if (hi <= s || below) {
         mark_candidate(v, a.next, a.state, a.segflag, a.T, a.perm, a.mis_o);
         publish(a.pub, v);
         ++sel;
@@ -228,7 +250,7 @@ __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
   if ((int64_t)blockIdx.x * (kBlock / 32) >= cnt && blockIdx.x >= nvl) return;
   const int lane = threadIdx.x & 31;
   const int32_t *__restrict__ nbr = a.nbr;
-  const uint32_t *__restrict__ prio = a.prio;
+  const bool all_alive = ctrl->round == 1;
   unsigned long long sel = 0;
   // one warp per row; rows longer than kBlockRow by the whole block below
   for (int64_t q = ((int64_t)blockIdx.x * kBlock + threadIdx.x) >> 5; q < cnt;
@@ -236,22 +258,22 @@ __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
     const int32_t v = a.long_list[q];
     const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
     const uint32_t qv = __ldg(&a.q[v]);
+    const int2 cb = class_bounds(a.cb, e - s);
     // the thread stage examined at least the last kThreadMax - 3 entries (its
     // first window may be short); rescanning an entry is harmless
     int64_t hi = e - (kThreadMax - 3);
-    bool blocked = false;
-    while (!blocked && hi > s) {
+    bool blocked = false, done = false;
+    while (!blocked && !done && hi > s) {
       int32_t u[kWarpU];
 #pragma unroll
       for (int j = 0; j < kWarpU; ++j) {
         const int64_t idx = hi - 1 - lane - 32 * j;
         u[j] = idx >= s ? ld_stream(&nbr[idx]) : -1;
       }
-      bool b = false;
-#pragma unroll
-      for (int j = 0; j < kWarpU; ++j)
-        if (u[j] >= 0) b |= blocks(a.q, prio, u[j], qv, v, a.perm);
+      bool below;
+      const bool b = blocks_row<kWarpU>(a, u, cb, all_alive, qv, v, below);
       blocked = __any_sync(0xffffffffu, b);
+      done = __any_sync(0xffffffffu, below);
       hi -= 32 * kWarpU;
     }
     if (!blocked) {
@@ -268,16 +290,20 @@ __global__ void __launch_bounds__(kBlock) k_select_long(SelectArgs a) {
     const int32_t v = a.vlong[q];
     const int64_t s = __ldg(&a.off[v]), e = __ldg(&a.off[v + 1]);
     const uint32_t qv = __ldg(&a.q[v]);
+    const int2 cb = class_bounds(a.cb, e - s);
     int64_t hi = e - (kThreadMax - 3);
-    bool blocked = false;
-    while (!blocked && hi > s) {
-      bool b = false;
+    bool blocked = false, done = false;
+    while (!blocked && !done && hi > s) {
+      int32_t u[kWarpU];
 #pragma unroll
       for (int j = 0; j < kWarpU; ++j) {
         const int64_t idx = hi - 1 - threadIdx.x - (int64_t)kBlock * j;
-        if (idx >= s) b |= blocks(a.q, prio, ld_stream(&nbr[idx]), qv, v, a.perm);
+        u[j] = idx >= s ? ld_stream(&nbr[idx]) : -1;
       }
+      bool below;
+      const bool b = blocks_row<kWarpU>(a, u, cb, all_alive, qv, v, below);
       blocked = __syncthreads_or(b) != 0;
+      done = __syncthreads_or(below) != 0;
       hi -= (int64_t)kBlock * kWarpU;
     }
     if (!blocked) {

@@ -46,6 +46,47 @@ __device__ __forceinline__ uint32_t h2_value(double avg, int32_t deg, double eps
   return __double2uint_rd(__dmul_rn(__ddiv_rn(avg, d), scale));
 }
 
+// Degree-class bounds of the H2 priorities on a degree-ordered graph
+// (common.cuh class_bounds).  In p = h2_value(avg, deg, eps), eps in
+// [0, 1 - 2^-53] (hash_to_unit), d = avg + deg - eps falls as eps grows, so p
+// is non-decreasing in eps: every vertex of degree k has p in
+// [h2(k, 0), h2(k, eps_max)], each IEEE step (add, subtract, clamp, divide,
+// multiply, round down) being monotone.  Both ends are non-increasing in k,
+// i.e. non-decreasing along the classes (descending degree).  For class c
+// (degree k):
+//   hi = first id of the first class c' with h2(deg c', 0) > h2(k, eps_max):
+//        every u >= hi has p(u) > p(v) for every v of degree k;
+//   lo = first id of the first class c'' with h2(deg c'', eps_max) >= h2(k, 0):
+//        every u < lo has p(u) < p(v).
+// The rest of the ids take the key comparison (ties resolved by the caller's
+// ids, priorities.hpp:61-64).  One thread per class, two binary searches.
+// lo relies on sorted rows (the early stop), so the unsorted hub rows get 0.
+__global__ void k_class_bounds(int32_t ncls, const int32_t *__restrict__ cls,
+                               const int64_t *__restrict__ off, double avg, double scale,
+                               int2 *__restrict__ cb) {
+  constexpr double kEpsMax = (double)((1ull << 53) - 1) * 0x1.0p-53;
+  auto deg_of = [&](int32_t c) { return (int32_t)(off[cls[c] + 1] - off[cls[c]]); };
+  for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < ncls; c += gridDim.x * blockDim.x) {
+    const int32_t k = deg_of(c);
+    const uint32_t plo = h2_value(avg, k, 0.0, scale), phi = h2_value(avg, k, kEpsMax, scale);
+    int32_t a = 0, b = ncls;  // first c' with h2(deg c', 0) > phi
+    while (a < b) {
+      const int32_t m = (a + b) >> 1;
+      if (h2_value(avg, deg_of(m), 0.0, scale) > phi) b = m; else a = m + 1;
+    }
+    const int32_t hi = cls[a];
+    a = 0;
+    b = ncls;  // first c'' with h2(deg c'', eps_max) >= plo
+    while (a < b) {
+      const int32_t m = (a + b) >> 1;
+      if (h2_value(avg, deg_of(m), kEpsMax, scale) >= plo) b = m; else a = m + 1;
+    }
+    // rows past kSortedMax entries are not sorted (order.cu): no lower bound,
+    // so their scans neither skip nor stop early
+    cb[k] = make_int2(k > kSortedMax ? 0 : cls[a], hi);
+  }
+}
+
 // K2: priorities (priorities.cpp:33-67) + state / decision initialisation.
 // mode 0: h1 / luby-fresh hash priorities from `mseed` (= mix64(seed'));
 // mode 1: h2 degree-aware priorities.
@@ -621,6 +662,7 @@ SelectArgs select_args(tcmis_graph *g, const RoundArgs &a) {
   s.rounds = ws.rounds;
   s.perm = a.perm;
   s.mis_o = a.mis_o;
+  s.cb = a.cb;
   s.tile_gate = a.tile_cand ? a.tile_gate : 0;
   return s;
 }
@@ -657,6 +699,7 @@ UpdateArgs update_args(tcmis_graph *g, const RoundArgs &a) {
   u.rounds = ws.rounds;
   u.tail_thr = a.tail_thr;
   u.perm = a.perm;
+  u.cb = a.cb;
   return u;
 }
 
@@ -1075,6 +1118,23 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     if (int rc = dev_alloc(&ws.mis_o, ws.n_cap + 16)) return rc;  // uint4 reads past n
   uint8_t *s_mis_o = use_mis_o ? ws.mis_o : nullptr;
   ws.relabeled = relabel;
+  // the degree-class bounds: a degree order under the H2 priorities
+  // (h2 / h3 / luby-perm), computed once per scale_bits
+  const int2 *s_cb = nullptr;
+  if (relabel && g->order_mode == TCMIS_ORDER_DEGREE && g->d_cls_start && g->n_cls > 0 &&
+      (H == TCMIS_H2 || H == TCMIS_H3 || H == TCMIS_LUBY_PERM) &&
+      std::getenv("TCMIS_NO_CLASS_BOUNDS") == nullptr) {
+    if (g->cb_scale_bits != cfg->scale_bits) {
+      if (!g->d_cb)
+        if (int rc = dev_alloc(&g->d_cb, (size_t)g->max_degree + 1)) return rc;
+      k_class_bounds<<<grid_for(ctx, g->n_cls, 128, 4), 128, 0, st>>>(
+          g->n_cls, g->d_cls_start, g->d_roff, avg_degree(g), (double)(1u << cfg->scale_bits),
+          g->d_cb);
+      TCMIS_LAUNCHED(ctx);
+      g->cb_scale_bits = cfg->scale_bits;
+    }
+    s_cb = g->d_cb;
+  }
 
   if (timing) timeline_begin(ctx);
   uint8_t *seg0 = seg_mode ? ws.segflag : nullptr;
@@ -1107,6 +1167,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   a.nbr = s_nbr;
   a.perm = s_perm;
   a.mis_o = s_mis_o;
+  a.cb = s_cb;
   a.T = T > 0 ? T : 1;
   a.seg_mode = seg_mode;
   a.nseg = nseg;

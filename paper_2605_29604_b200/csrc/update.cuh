@@ -70,7 +70,25 @@ struct UpdateArgs {
   DevRound *rounds;
   int32_t tail_thr;        // the WHILE loop continues while alive > tail_thr
   const int32_t *perm;     // solve id -> caller id (relabeled graphs), else null
+  const int2 *cb;          // degree-class bounds (common.cuh class_bounds), or null
 };
+
+// kU row entries of v: a candidate neighbour has a key above v's (it beat v,
+// alive at the round's start), so entries under the class bound lo are
+// neither gathered nor, with the rows sorted, followed by anything that could
+// be one (`below`).
+template <int kU>
+__device__ __forceinline__ bool hits_row(const uint8_t *__restrict__ next, const int32_t *u,
+                                         int2 cb, bool &below) {
+  bool hit = false;
+  below = false;
+#pragma unroll
+  for (int j = 0; j < kU; ++j) {
+    below |= u[j] >= 0 && u[j] < cb.x;
+    if (u[j] >= cb.x) hit |= next[u[j]] == 1;
+  }
+  return hit;
+}
 
 // The end of a round, run by every block of the round's last kernel: the
 // segment flags swept into the tile counters, the block's counts added, and
@@ -272,15 +290,13 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
       const int64_t s = ld_stream(&a.off[v]), e = ld_stream(&a.off[v + 1]);
       int32_t u[4];
       load_tail4(a.nbr, a.vnnz, s, e, u);
-      bool hit = false;
-#pragma unroll
-      for (int j = 0; j < kPullK; ++j)
-        if (u[j] >= 0) hit |= next[u[j]] == 1;
+      bool below;
+      const bool hit = hits_row<kPullK>(next, u, class_bounds(a.cb, e - s), below);
       if (hit) {
         mark_removed(v, a.state, a.q);
         publish(a.pub, v);
         ++rem;
-      } else if (e - s <= kPullK) {
+      } else if (e - s <= kPullK || below) {
         survive = true;
         if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m, a.perm);
       } else {
@@ -316,12 +332,14 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
   int mode = kFetch;
   int32_t v = 0;
   int64_t s = 0, e = 0, hi = 0;
+  int2 cb = make_int2(0, 0);
   auto fetch = [&]() {
     i += stride;
     if (i < cnt) {
       v = __ldg(&a.undecided[i]);
       s = __ldg(&a.off[v]);
       e = __ldg(&a.off[v + 1]);
+      cb = class_bounds(a.cb, e - s);
       hi = e - kPullK;
       mode = kScan;
     } else {
@@ -344,17 +362,15 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
           for (int j = 0; j < 4; ++j) u[4 * k + j] = -1;
         }
       }
-      bool hit = false;
-#pragma unroll
-      for (int j = 0; j < kU; ++j)
-        if (u[j] >= 0) hit |= next[u[j]] == 1;
+      bool below;
+      const bool hit = hits_row<kU>(next, u, cb, below);
       hi = w;
       if (hit) {
         mark_removed(v, a.state, a.q);
         publish(a.pub, v);
         ++rem;
         mode = kFetch;
-      } else if (hi <= s) {
+      } else if (hi <= s || below) {
         survive = true;
         if (a.fresh) set_fresh(a.prio, a.q, v, fresh_m, a.perm);
         mode = kFetch;
@@ -417,8 +433,9 @@ __global__ void __launch_bounds__(kBlock)
     const int32_t v = __ldcg(&row->v), first = __ldcg(&row->first);
     int64_t hi = hi0 - (int64_t)(it - first) * kPullChunk;
     const int64_t lo = hi - kPullChunk > lo0 ? hi - kPullChunk : lo0;
-    bool hit = false, other = false;
-    while (!hit && !other && hi > lo) {
+    const int2 cb = class_bounds(a.cb, a.cb ? __ldg(&a.off[v + 1]) - lo0 : 0);
+    bool hit = false, other = false, done = false;
+    while (!hit && !other && !done && hi > lo) {
       int32_t u[kWarpU];
 #pragma unroll
       for (int j = 0; j < kWarpU; ++j) {
@@ -426,11 +443,10 @@ __global__ void __launch_bounds__(kBlock)
         u[j] = idx >= lo ? ld_stream(&nbr[idx]) : -1;
       }
       other = __ldcg(&row->hit) != 0;  // in flight with the row loads
-      bool b = false;
-#pragma unroll
-      for (int j = 0; j < kWarpU; ++j)
-        if (u[j] >= 0) b |= next[u[j]] == 1;
+      bool below;
+      const bool b = hits_row<kWarpU>(next, u, cb, below);
       hit = __any_sync(0xffffffffu, b);
+      done = __any_sync(0xffffffffu, below);
       other = __shfl_sync(0xffffffffu, other, 0);
       hi -= 32 * kWarpU;
     }

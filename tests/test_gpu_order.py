@@ -136,3 +136,68 @@ def test_permuted_graph_is_normalised(ctx):
         assert rounds_tuple(got.iterations) == oracle_tuple(exp), flags
     p.close()
     dg.close()
+
+
+@pytest.mark.parametrize("spec", [("rmat", 14, 16, 2), ("rmat", 12, 4, 5), ("gnp_avg", 4000, 9.0, 1),
+                                  ("grid", 40)])
+@pytest.mark.parametrize("scale_bits", [8, 11, 20, 30])
+def test_degree_class_bounds(ctx, spec, scale_bits, monkeypatch):
+    """Degree order + H2 priorities: the select and pull kernels settle rows by
+    the degree-class bounds (solver.cu k_class_bounds) without gathering the
+    neighbours' keys.  Small scale_bits make p ties across neighbouring degrees
+    common (floor of avg/d * 2^sb), i.e. wide uncertain bands; large ones make
+    the bands narrow.  Bit-exact either way, and equal to the solve without
+    the bounds (TCMIS_NO_CLASS_BOUNDS)."""
+    g = O.gen(*spec)
+    dg = tc.DeviceGraph.upload(tc.Graph(g.n, g.off, g.nbr), ctx).reorder(tc.DeviceGraph.ORDER_DEGREE)
+    for heur in ("h2", "h3", "luby-perm"):
+        exp = O.solve(g, heur, 4, tile_dim=16, scale_bits=scale_bits)
+        for excl in (tc.Exclusion.AUTO, tc.Exclusion.PUSH, tc.Exclusion.CSR_PULL):
+            for host_loop in (False, True):
+                got = tc.run_mis(dg, tc.EngineConfig(heuristic=HEUR[heur], seed=4, exclusion=excl,
+                                                     scale_bits=scale_bits, host_loop=host_loop))
+                where = (spec, heur, excl, host_loop)
+                assert np.array_equal(got.mis, exp.mis), where
+                assert rounds_tuple(got.iterations) == oracle_tuple(exp), where
+    monkeypatch.setenv("TCMIS_NO_CLASS_BOUNDS", "1")
+    got = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=4, scale_bits=scale_bits))
+    assert np.array_equal(got.mis, O.solve(g, "h2", 4, tile_dim=16, scale_bits=scale_bits).mis)
+    dg.close()
+
+
+def _hub_graph():
+    """Random edges plus hubs of 9000, 3000, 700, 200 and 40 neighbours: rows
+    in every tier of the row sort (order.cu sort_rows)."""
+    rng = np.random.default_rng(11)
+    n = 12000
+    edges = set()
+    for hub, d in ((0, 9000), (1, 3000), (2, 700), (3, 200), (4, 40)):
+        for u in rng.choice(np.arange(5, n), d, replace=False):
+            edges.add((min(hub, int(u)), max(hub, int(u))))
+    for _ in range(30000):
+        a, b = rng.integers(0, n, 2)
+        if a != b:
+            edges.add((int(min(a, b)), int(max(a, b))))
+    return O.graph_from_edges(n, sorted(edges))
+
+
+@pytest.mark.parametrize("kind", ["rmat", "hubs"])
+def test_reordered_rows_are_sorted(ctx, kind):
+    """tcmis_graph_reorder sorts every relabeled row (the scans' early stop
+    relies on it): the permuted graph's rows ascend for each order and hold
+    the relabeled neighbours; the solves stay bit-exact."""
+    g = O.gen("rmat", 11, 8, 3) if kind == "rmat" else _hub_graph()
+    dg = tc.DeviceGraph.upload(tc.Graph(g.n, g.off, g.nbr), ctx)
+    for mode in (tc.DeviceGraph.ORDER_DEGREE, tc.DeviceGraph.ORDER_GIVEN):
+        order = np.random.default_rng(1).permutation(g.n).astype(np.int32) \
+            if mode == tc.DeviceGraph.ORDER_GIVEN else None
+        h = dg.reorder(mode, order).permuted().download()
+        for v in range(h.n):
+            assert np.all(np.diff(h.neighbors[h.offsets[v]:h.offsets[v + 1]]) > 0)
+        assert sorted(np.diff(h.offsets).tolist()) == sorted(np.diff(g.off).tolist())
+        for heur in ("h2", "h3", "h1"):
+            got = tc.run_mis(dg, tc.EngineConfig(heuristic=HEUR[heur], seed=2))
+            exp = O.solve(g, heur, 2, tile_dim=16)
+            assert np.array_equal(got.mis, exp.mis), (kind, mode, heur)
+            assert rounds_tuple(got.iterations) == oracle_tuple(exp), (kind, mode, heur)
+    dg.close()

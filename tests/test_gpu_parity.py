@@ -333,7 +333,7 @@ def _device_graph_for(spec, ctx):
     return tc.DeviceGraph.upload(as_tc(O.gen("petersen")), ctx)
 
 
-def _check_golden(name, ctx, exclusion=tc.Exclusion.AUTO, only=None):
+def _check_golden(name, ctx, exclusion=tc.Exclusion.AUTO, only=None, order=None):
     gd = golden(name)
     dg = _device_graph_for(gd["spec"], ctx)
     assert (dg.n, dg.num_edges()) == (gd["n"], gd["m"])
@@ -341,6 +341,9 @@ def _check_golden(name, ctx, exclusion=tc.Exclusion.AUTO, only=None):
     assert O.checksum(h.offsets) == gd["off_checksum"]
     assert O.checksum(h.neighbors) == gd["nbr_checksum"]
     assert dg.tile(gd["tile_dim"]) == gd["tile_count"]
+    del h
+    if order is not None:  # the solve on an internal vertex order (tcmis_graph_reorder)
+        dg.reorder(order)
     for key, exp in gd["results"].items():
         if only and key != only:
             continue
@@ -366,6 +369,23 @@ def test_golden_baseline_configs(ctx, name):
     """The BASELINE.json configs at full size, against the reference's own
     results (tests/golden/make_golden.py)."""
     _check_golden(name, ctx)
+
+
+@pytest.mark.parametrize("name", golden_names(large=True))
+def test_golden_baseline_configs_bench_order(ctx, name):
+    """The same fixtures solved the way bench.py solves them: R-MAT on the
+    degree order (sorted rows, degree-class bounds), the RGG on its points'
+    spatial order, the rest on the caller's ids."""
+    order = {"rmat": tc.DeviceGraph.ORDER_DEGREE,
+             "rgg": tc.DeviceGraph.ORDER_SPATIAL}.get(golden(name)["spec"]["kind"])
+    if order is None:
+        pytest.skip("bench.py solves this config on the caller's ids")
+    _check_golden(name, ctx, order=order)
+
+
+def test_rmat26_golden_rounds_degree_order(ctx):
+    """R-MAT s26 against the reference's fixture on the bench's degree order."""
+    _check_golden("rmat26_ef16", ctx, order=tc.DeviceGraph.ORDER_DEGREE)
 
 
 def test_rmat26_golden_rounds(ctx):
