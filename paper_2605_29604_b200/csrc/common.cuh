@@ -306,6 +306,39 @@ __device__ __forceinline__ void warp_append(bool have, int32_t v, int32_t *out, 
   if (have) out[pos + __popc(m & ((1u << lane) - 1u))] = v;
 }
 
+// Block-aggregated list output for kernels whose every thread emits up to
+// kPer entries per loop iteration: warp ballots into a shared-memory buffer,
+// then ONE global atomic per block and iteration and a coalesced copy (a
+// warp-level atomic per emission contends on the tail: 1.25M atomics on one
+// word took R-MAT s26's round-1 settle kernel to 376 us).  Block-uniform.
+template <int kBlockT, int kPer>
+struct BlockOut {
+  int32_t buf[kBlockT * kPer];
+  int n, base;
+  __device__ __forceinline__ void reset() {
+    if (threadIdx.x == 0) n = 0;
+    __syncthreads();
+  }
+  __device__ __forceinline__ void put(bool have, int32_t v) {
+    const int lane = threadIdx.x & 31;
+    const unsigned m = __ballot_sync(0xffffffffu, have);
+    if (!m) return;
+    int pos = 0;
+    if (lane == 0) pos = atomicAdd(&n, __popc(m));
+    pos = __shfl_sync(0xffffffffu, pos, 0);
+    if (have) buf[pos + __popc(m & ((1u << lane) - 1u))] = v;
+  }
+  __device__ __forceinline__ void flush(int32_t *out, int *tail) {
+    __syncthreads();
+    if (threadIdx.x == 0) base = n ? atomicAdd(tail, n) : 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += kBlockT) out[base + i] = buf[i];
+    __syncthreads();
+    if (threadIdx.x == 0) n = 0;
+    __syncthreads();
+  }
+};
+
 // Per-lane reservation of `cnt` (>= 0) consecutive slots at *tail, one atomic
 // per warp; returns the lane's first slot.  Warp-uniform call.
 __device__ __forceinline__ int warp_reserve(int cnt, int *tail) {

@@ -75,6 +75,8 @@ struct Ctrl {
   int32_t pull_items;  // chunks of the pull long rows (k_round_end work items)
   int32_t corrupt;     // a round broke selected + removed + alive == alive before
                        // (engine.cpp:138-141,152-153 logic_error): set on the device
+  int32_t r1_sel_left;   // round 1, degree order: vertices k_r1_settle left to the probe
+  int32_t r1_pull_left;  // ... and that k_r1_pull left to the pull probe
 };
 
 // A pull row that outlived k_update_pull's engine (update.cuh): entries
@@ -125,6 +127,12 @@ struct Workspace {
   unsigned *warpcnt = nullptr;    // k_tail's fused MIS compaction: 2 x kTailMaxWarps per-warp
                                   // counts by solve parity, then tslot[2] (tag base, solve counter)
   int64_t *mis_count = nullptr;
+  // relabeled solves without the caller-order plane: the compaction's
+  // membership words (32 caller ids each) and per-block counts -> offsets
+  uint32_t *gc_bits = nullptr;
+  int64_t *gc_blk = nullptr;
+  void *gc_tmp = nullptr;
+  size_t gc_tmp_bytes = 0;
   Ctrl *ctrl = nullptr;        // device
   Ctrl *h_ctrl = nullptr;      // pinned host mirror
   int64_t *h_misc = nullptr;   // pinned: [0] MIS count, [1] h3 tiles evaluated
@@ -224,6 +232,9 @@ struct tcmis_graph {
   int32_t n_cls = 0;
   int2 *d_cb = nullptr;
   int32_t cb_scale_bits = -1;
+  int2 *d_cbc = nullptr;       // the same bounds by class index
+  int32_t *d_rmax = nullptr;   // per solve id: its largest neighbour id (-1: isolated)
+  uint16_t *d_vcls = nullptr;  // per solve id: its degree class (n_cls <= 65535)
   int32_t *d_spatial = nullptr;  // tcmis_gen_rgg's points in Z-order of their cells
   // Phase 1 tile form (tile_cand.cu): the A-up store of one priority
   // configuration (heuristic, seed, scale_bits)
@@ -333,6 +344,10 @@ struct RoundArgs {
   const int32_t *perm;  // solve id -> caller id (relabeled CSR), else null
   uint8_t *mis_o;       // relabeled: caller-order membership kept by the kernels, or null
   const int2 *cb;       // degree-class bounds of the H2 priorities (degree order), or null
+  const int2 *cbc;      // ... by class index, with r1_max / r1_cls: round 1's settling
+  const int32_t *r1_max;  // per vertex: its largest neighbour id
+  const uint16_t *r1_cls; // per vertex: its degree class
+  int nz_prefix;        // the round-1 list is 0 .. nz_count-1 (degree order)
   bool operator==(const RoundArgs &o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
 

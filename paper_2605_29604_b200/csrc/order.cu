@@ -218,6 +218,51 @@ __global__ void k_long_rows_copy(int32_t cnt, const int32_t *__restrict__ rows,
   }
 }
 
+// round 1's settling data (select.cuh r1_max / r1_cls): per solve id the
+// largest neighbour id -- the row's last entry when the row is sorted, a
+// block reduction for the hub rows, which are the ids [0, H) of the degree
+// order -- and the degree class
+__global__ void k_row_max(int32_t n, const int64_t *__restrict__ off, const int32_t *__restrict__ nbr,
+                          int32_t *__restrict__ rmax, int32_t *__restrict__ hub_end) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = off[v], e = off[v + 1];
+    rmax[v] = e == s ? -1 : (e - s <= kSortedMax ? nbr[e - 1] : -2);
+    // the first id whose row is sorted (degrees descend)
+    if (e - s <= kSortedMax && (v == 0 || off[v] - off[v - 1] > kSortedMax)) *hub_end = (int32_t)v;
+  }
+}
+__global__ void k_hub_max(const int32_t *__restrict__ hub_end, const int64_t *__restrict__ off,
+                          const int32_t *__restrict__ nbr, int32_t *__restrict__ rmax) {
+  __shared__ int32_t s_m[32];
+  const int32_t h = *hub_end;
+  for (int32_t v = blockIdx.x; v < h; v += gridDim.x) {
+    int32_t m = -1;
+    for (int64_t k = off[v] + threadIdx.x; k < off[v + 1]; k += blockDim.x) m = max(m, nbr[k]);
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      m = threadIdx.x < (int)(blockDim.x >> 5) ? s_m[threadIdx.x] : -1;
+      m = __reduce_max_sync(0xffffffffu, m);
+      if (threadIdx.x == 0) rmax[v] = m;
+    }
+    __syncthreads();
+  }
+}
+__global__ void k_vertex_class(int32_t n, int32_t ncls, const int32_t *__restrict__ cls,
+                               uint16_t *__restrict__ vcls) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int32_t a = 0, b = ncls - 1;  // last class starting at or before v
+    while (a < b) {
+      const int32_t m = (a + b + 1) >> 1;
+      if (__ldg(&cls[m]) <= v) a = m; else b = m - 1;
+    }
+    vcls[v] = (uint16_t)a;
+  }
+}
+
 struct HasEdgesR {
   const int64_t *off;
   __device__ __forceinline__ bool operator()(int32_t v) const { return off[v + 1] > off[v]; }
@@ -233,6 +278,12 @@ void free_order(tcmis_graph *g) {
   dev_free(g->d_rnz);
   dev_free(g->d_cls_start);
   dev_free(g->d_cb);
+  dev_free(g->d_cbc);
+  dev_free(g->d_rmax);
+  dev_free(g->d_vcls);
+  g->d_cbc = nullptr;
+  g->d_rmax = nullptr;
+  g->d_vcls = nullptr;
   g->d_cls_start = nullptr;
   g->d_cb = nullptr;
   g->n_cls = 0;
@@ -512,9 +563,31 @@ int reorder_impl(tcmis_graph *g, int32_t mode, const int32_t *order) {
     dev_free(tmp);
     dev_free(d_cnt);
   }
+  // round 1's settling data (degree order, classes fit a u16)
+  int32_t *rmax = nullptr;
+  uint16_t *vcls = nullptr;
+  if (!rc && mode == TCMIS_ORDER_DEGREE && g->n_cls > 0 && g->n_cls <= 65535) {
+    int32_t *hub_end = nullptr;
+    rc = dev_alloc(&rmax, (size_t)n);
+    if (!rc) rc = dev_alloc(&vcls, (size_t)n);
+    if (!rc) rc = dev_alloc(&hub_end, 1);
+    if (!rc) {
+      // every row a hub (no sorted row to find): H = n
+      cudaMemcpyAsync(hub_end, &n, 4, cudaMemcpyHostToDevice, st);
+      k_row_max<<<grid_for(ctx, n, 256, 8), 256, 0, st>>>(n, roff, rnbr, rmax, hub_end);
+      k_hub_max<<<ctx->num_sms * 4, 256, 0, st>>>(hub_end, roff, rnbr, rmax);
+      k_vertex_class<<<grid_for(ctx, n, 256, 8), 256, 0, st>>>(n, g->n_cls, cls, vcls);
+      ctx->launches += 3;
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) rc = cuda_error(e, "round-1 settling data");
+    }
+    dev_free(hub_end);
+  }
   clk.mark("classes + non-isolated list");
   dev_free(bad);
   if (rc) {
+    dev_free(rmax);
+    dev_free(vcls);
     dev_free(cls);
     g->n_cls = 0;
     dev_free(inv);
@@ -530,6 +603,8 @@ int reorder_impl(tcmis_graph *g, int32_t mode, const int32_t *order) {
   g->d_rnbr = rnbr;
   g->d_rnz = rnz;
   g->d_cls_start = cls;
+  g->d_rmax = rmax;
+  g->d_vcls = vcls;
   g->order_mode = mode;
   return 0;
 }

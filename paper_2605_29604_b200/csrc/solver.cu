@@ -63,7 +63,7 @@ __device__ __forceinline__ uint32_t h2_value(double avg, int32_t deg, double eps
 // lo relies on sorted rows (the early stop), so the unsorted hub rows get 0.
 __global__ void k_class_bounds(int32_t ncls, const int32_t *__restrict__ cls,
                                const int64_t *__restrict__ off, double avg, double scale,
-                               int2 *__restrict__ cb) {
+                               int2 *__restrict__ cb, int2 *__restrict__ cbc) {
   constexpr double kEpsMax = (double)((1ull << 53) - 1) * 0x1.0p-53;
   auto deg_of = [&](int32_t c) { return (int32_t)(off[cls[c] + 1] - off[cls[c]]); };
   for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < ncls; c += gridDim.x * blockDim.x) {
@@ -84,6 +84,7 @@ __global__ void k_class_bounds(int32_t ncls, const int32_t *__restrict__ cls,
     // rows past kSortedMax entries are not sorted (order.cu): no lower bound,
     // so their scans neither skip nor stop early
     cb[k] = make_int2(k > kSortedMax ? 0 : cls[a], hi);
+    if (cbc) cbc[c] = cb[k];
   }
 }
 
@@ -253,16 +254,104 @@ __global__ void k_seg_total(const uint8_t *__restrict__ segflag,
   block_add3(0, 0, ev, ctrl);
 }
 
-// the caller's vertex v is InMIS (relabeled solves without the caller-order
-// membership plane: the compaction walks the caller's ids in order and
-// gathers the solve-order state)
-struct IsInMISInv {
-  const uint8_t *state;
-  const int32_t *inv;
-  __device__ __forceinline__ bool operator()(int32_t v) const {
-    return state[__ldg(&inv[v])] == TCMIS_IN_MIS;
+// Relabeled solves without the caller-order membership plane (R-MAT s26):
+// ascending MIS ids of the caller's order in two passes instead of one cub
+// select gathering through inv per id (262 us at s26):
+//   1. k_gc_bits: warp per 1024 caller ids, 32 coalesced steps of inv + a
+//      gather of the solve-order state (L2-resident), one ballot word each;
+//      per-block counts;
+//   2. an exclusive sum of the block counts (cub, 8k blocks at s26);
+//   3. k_gc_ids: words -> ids, block scan of the words' popcounts.
+// DRAM: inv once (4 B/id), 1 bit/id twice, the ids once.
+constexpr int kGcBlock = 256;                       // words per block
+constexpr int64_t kGcIdsPerBlock = 32ll * kGcBlock;  // caller ids per block
+
+__global__ void __launch_bounds__(kGcBlock) k_gc_bits(int32_t n, const int32_t *__restrict__ inv,
+                                                      const uint8_t *__restrict__ state,
+                                                      uint32_t *__restrict__ bits,
+                                                      int64_t *__restrict__ blk) {
+  __shared__ int s_cnt;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // the warp's 32 words: caller ids [base, base + 1024)
+  const int64_t base = blockIdx.x * kGcIdsPerBlock + (int64_t)w * 1024;
+  uint32_t mine = 0;
+#pragma unroll 8
+  for (int k = 0; k < 32; ++k) {
+    const int64_t o = base + 32 * k + lane;
+    const bool in = o < n && state[__ldg(&inv[o])] == TCMIS_IN_MIS;
+    const uint32_t m = __ballot_sync(0xffffffffu, in);
+    if (lane == k) mine = m;
   }
-};
+  const int64_t word = blockIdx.x * (int64_t)kGcBlock + threadIdx.x;
+  if (word * 32 < n) bits[word] = mine;
+  const int c = __reduce_add_sync(0xffffffffu, __popc(mine));
+  if (lane == 0 && c) atomicAdd(&s_cnt, c);
+  __syncthreads();
+  if (threadIdx.x == 0) blk[blockIdx.x] = s_cnt;
+}
+
+__global__ void __launch_bounds__(kGcBlock) k_gc_ids(int32_t n, const uint32_t *__restrict__ bits,
+                                                     const int64_t *__restrict__ blk_off,
+                                                     int32_t nblk, int32_t *__restrict__ mis,
+                                                     int64_t *__restrict__ mis_count) {
+  // each warp's ids (<= 32 words x 32) staged in shared memory, then stored
+  // coalesced: the warp's words are contiguous, so are its ids
+  using Scan = cub::BlockScan<int, kGcBlock>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int32_t s_ids[kGcBlock / 32][1024];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t word = blockIdx.x * (int64_t)kGcBlock + threadIdx.x;
+  uint32_t m = word * 32 < n ? bits[word] : 0u;
+  const int c = __popc(m);
+  int pos = 0;
+  Scan(tmp).ExclusiveSum(c, pos);
+  const int wbase = __shfl_sync(0xffffffffu, pos, 0);
+  const int wtotal = __shfl_sync(0xffffffffu, pos + c, 31) - wbase;
+  int k = pos - wbase;
+  while (m) {
+    const int b = __ffs(m) - 1;
+    m &= m - 1;
+    s_ids[w][k++] = (int32_t)(word * 32 + b);
+  }
+  __syncwarp();
+  int32_t *out = mis + blk_off[blockIdx.x] + wbase;
+  for (int i = lane; i < wtotal; i += 32) out[i] = s_ids[w][i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *mis_count = blk_off[nblk];
+}
+
+int gc_blocks(int32_t n) { return (int)((n + kGcIdsPerBlock - 1) / kGcIdsPerBlock); }
+
+// the buffers (outside any capture)
+int gc_prepare(tcmis_graph *g) {
+  Workspace &ws = g->ws;
+  if (ws.gc_bits) return 0;
+  const int nb = gc_blocks((int32_t)ws.n_cap);
+  if (int rc = dev_alloc(&ws.gc_bits, (size_t)nb * kGcBlock)) return rc;
+  if (int rc = dev_alloc(&ws.gc_blk, 2 * ((size_t)nb + 1))) return rc;
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, ws.gc_blk, ws.gc_blk + nb + 1, nb + 1, g->ctx->stream);
+  if (int rc = dev_alloc((char **)&ws.gc_tmp, bytes)) return rc;
+  ws.gc_tmp_bytes = bytes;
+  return 0;
+}
+
+// enqueue the three steps (capturable)
+int gc_compact(tcmis_graph *g) {
+  Workspace &ws = g->ws;
+  cudaStream_t st = g->ctx->stream;
+  const int32_t n = g->n;
+  const int nb = gc_blocks(n);
+  int64_t *cnt = ws.gc_blk, *offs = ws.gc_blk + nb + 1;
+  k_gc_bits<<<nb, kGcBlock, 0, st>>>(n, g->d_inv, ws.state, ws.gc_bits, cnt);
+  TCMIS_CUDA(cudaMemsetAsync(cnt + nb, 0, 8, st));
+  size_t bytes = ws.gc_tmp_bytes;
+  TCMIS_CUDA(cub::DeviceScan::ExclusiveSum(ws.gc_tmp, bytes, cnt, offs, nb + 1, st));
+  k_gc_ids<<<nb, kGcBlock, 0, st>>>(n, ws.gc_bits, offs, nb, ws.mis, ws.mis_count);
+  g->ctx->launches += 4;
+  return 0;
+}
 
 // relabeled solves: the final states in the caller's order (coalesced
 // writes, a gather of the solve-order states)
@@ -377,6 +466,9 @@ void free_workspace(Workspace &ws) {
   dev_free(ws.wl[1]);
   dev_free(ws.segflag);
   dev_free(ws.mis);
+  dev_free(ws.gc_bits);
+  dev_free(ws.gc_blk);
+  dev_free(ws.gc_tmp);
   dev_free(ws.long_list);
   dev_free(ws.prow);
   dev_free(ws.pitems);
@@ -438,6 +530,12 @@ int ensure_workspace(tcmis_graph *g) {
     dev_free(ws.wl[0]);
     dev_free(ws.wl[1]);
     dev_free(ws.mis);
+    dev_free(ws.gc_bits);
+    dev_free(ws.gc_blk);
+    dev_free(ws.gc_tmp);
+    ws.gc_bits = nullptr;
+    ws.gc_blk = nullptr;
+    ws.gc_tmp = nullptr;
     dev_free(ws.long_list);
     dev_free(ws.undec_sel);
     dev_free(ws.undec_pull);
@@ -640,7 +738,7 @@ SelectArgs select_args(tcmis_graph *g, const RoundArgs &a) {
   SelectArgs s;
   s.n1 = a.nz_count;
   s.nz = a.nz;
-  s.nz_identity = a.nz_count == a.n ? 1 : 0;
+  s.nz_identity = a.nz_count == a.n || a.nz_prefix ? 1 : 0;
   s.off = a.off;
   s.nbr = a.nbr;
   s.vnnz = a.vnnz;
@@ -663,6 +761,9 @@ SelectArgs select_args(tcmis_graph *g, const RoundArgs &a) {
   s.perm = a.perm;
   s.mis_o = a.mis_o;
   s.cb = a.cb;
+  s.r1_max = a.r1_max;
+  s.r1_cls = a.r1_cls;
+  s.cbc = a.cbc;
   s.tile_gate = a.tile_cand ? a.tile_gate : 0;
   return s;
 }
@@ -685,7 +786,7 @@ UpdateArgs update_args(tcmis_graph *g, const RoundArgs &a) {
   u.seed = a.seed;
   u.n1 = a.nz_count;
   u.nz = a.nz;
-  u.nz_identity = a.nz_count == a.n ? 1 : 0;
+  u.nz_identity = a.nz_count == a.n || a.nz_prefix ? 1 : 0;
   u.prow = ws.prow;
   u.pitems = ws.pitems;
   u.undecided = ws.undec_pull;
@@ -700,6 +801,7 @@ UpdateArgs update_args(tcmis_graph *g, const RoundArgs &a) {
   u.tail_thr = a.tail_thr;
   u.perm = a.perm;
   u.cb = a.cb;
+  u.r1_max = a.r1_max;
   return u;
 }
 
@@ -824,6 +926,10 @@ int launch_select(tcmis_graph *g, const RoundArgs &a) {
                     ws.ctrl, a.tile_gate, s.push, a.off, a.nbr)));
     TCMIS_LAUNCHED(ctx);
   }
+  if (a.r1_max) {
+    TCMIS_TIMED(ctx, "k_r1_settle", (launch_round_kernel(k_r1_settle, a.sel_grid, st, s)));
+    TCMIS_LAUNCHED(ctx);
+  }
   TCMIS_TIMED(ctx, "k_probe_select", (launch_round_kernel(k_probe_select, a.sel_grid, st, s)));
   TCMIS_LAUNCHED(ctx);
   TCMIS_TIMED(ctx, "k_select",
@@ -841,6 +947,10 @@ int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle
   cudaStream_t st = ctx->stream;
   const UpdateArgs u = update_args(g, a);
   if (a.pull) {
+    if (a.r1_max) {
+      TCMIS_TIMED(ctx, "k_r1_pull", (launch_round_kernel(k_r1_pull, a.sel_grid, st, u)));
+      TCMIS_LAUNCHED(ctx);
+    }
     TCMIS_TIMED(ctx, "k_probe_pull", (launch_round_kernel(k_probe_pull, a.sel_grid, st, u)));
     TCMIS_LAUNCHED(ctx);
     TCMIS_TIMED(ctx, "k_update_pull", (launch_round_kernel(k_update_pull, a.sel_grid, st, u)));
@@ -974,12 +1084,12 @@ int ensure_solve_graph(tcmis_graph *g, const RoundArgs &a, const SolvePre &pre) 
       const bool gather = a.perm && !a.mis_o;  // no fused compaction (tail.cuh)
       const bool tail_packs = a.tail_thr > 0 && pre.seg_mode != 2 && !gather;
       if (a.tail_thr > 0) rc = launch_tail(g, a, tail_packs ? ws.d_res : nullptr);
-      if (!rc && (a.tail_thr == 0 || gather)) {
+      if (!rc && gather) {
+        rc = gc_compact(g);
+      } else if (!rc && a.tail_thr == 0) {
         thrust::counting_iterator<int32_t> ids(0);
         size_t bytes = ws.cub_bytes;
-        e = gather ? cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
-                                           (int)g->n, IsInMISInv{ws.state, g->d_inv}, st)
-                   : a.mis_o ? cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
+        e = a.mis_o ? cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
                                                      (int)g->n, IsMember{a.mis_o}, st)
                              : cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
                                                      (int)g->n, IsInMIS{ws.state}, st);
@@ -1118,6 +1228,8 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     if (int rc = dev_alloc(&ws.mis_o, ws.n_cap + 16)) return rc;  // uint4 reads past n
   uint8_t *s_mis_o = use_mis_o ? ws.mis_o : nullptr;
   ws.relabeled = relabel;
+  if (relabel && !use_mis_o)
+    if (int rc = gc_prepare(g)) return rc;
   // the degree-class bounds: a degree order under the H2 priorities
   // (h2 / h3 / luby-perm), computed once per scale_bits
   const int2 *s_cb = nullptr;
@@ -1127,9 +1239,11 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     if (g->cb_scale_bits != cfg->scale_bits) {
       if (!g->d_cb)
         if (int rc = dev_alloc(&g->d_cb, (size_t)g->max_degree + 1)) return rc;
+      if (!g->d_cbc)
+        if (int rc = dev_alloc(&g->d_cbc, (size_t)g->n_cls)) return rc;
       k_class_bounds<<<grid_for(ctx, g->n_cls, 128, 4), 128, 0, st>>>(
           g->n_cls, g->d_cls_start, g->d_roff, avg_degree(g), (double)(1u << cfg->scale_bits),
-          g->d_cb);
+          g->d_cb, g->d_cbc);
       TCMIS_LAUNCHED(ctx);
       g->cb_scale_bits = cfg->scale_bits;
     }
@@ -1168,6 +1282,12 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   a.perm = s_perm;
   a.mis_o = s_mis_o;
   a.cb = s_cb;
+  if (s_cb && g->d_rmax && g->d_vcls && std::getenv("TCMIS_NO_R1_SETTLE") == nullptr) {
+    a.cbc = g->d_cbc;
+    a.r1_max = g->d_rmax;
+    a.r1_cls = g->d_vcls;
+  }
+  a.nz_prefix = relabel && g->order_mode == TCMIS_ORDER_DEGREE ? 1 : 0;
   a.T = T > 0 ? T : 1;
   a.seg_mode = seg_mode;
   a.nseg = nseg;
@@ -1244,10 +1364,9 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     if (!tail_compacted) {
       thrust::counting_iterator<int32_t> ids(0);
       size_t bytes = ws.cub_bytes;
-      if (a.perm && !a.mis_o)
-        TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
-                                         (int)g->n, IsInMISInv{ws.state, g->d_inv}, st));
-      else if (a.mis_o)
+      if (a.perm && !a.mis_o) {
+        if (int rc = gc_compact(g)) return rc;
+      } else if (a.mis_o)
         TCMIS_CUDA(cub::DeviceSelect::If(ws.cub_tmp, bytes, ids, ws.mis, ws.mis_count,
                                          (int)g->n, IsMember{a.mis_o}, st));
       else

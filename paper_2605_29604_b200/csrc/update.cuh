@@ -71,6 +71,7 @@ struct UpdateArgs {
   int32_t tail_thr;        // the WHILE loop continues while alive > tail_thr
   const int32_t *perm;     // solve id -> caller id (relabeled graphs), else null
   const int2 *cb;          // degree-class bounds (common.cuh class_bounds), or null
+  const int32_t *r1_max;   // round 1: the largest neighbour id first (select.cuh), or null
 };
 
 // kU row entries of v: a candidate neighbour has a key above v's (it beat v,
@@ -267,10 +268,11 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
   __shared__ int32_t s_und[kBlock / 32][64];
   Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
-  stamp_phase(a.rounds, ctrl, round, 1, 1);
-  const int64_t cnt = round == 1 ? a.n1 : ctrl->wl_count[round & 1];
+  const bool r1s = round == 1 && a.r1_max;  // after k_r1_pull: the vertices it left
+  if (!r1s) stamp_phase(a.rounds, ctrl, round, 1, 1);
+  const int64_t cnt = r1s ? ctrl->r1_pull_left : round == 1 ? a.n1 : ctrl->wl_count[round & 1];
   if ((int64_t)blockIdx.x * kBlock >= cnt) return;
-  const int32_t *wl = round == 1 ? a.nz : ((round & 1) ? a.wl1 : a.wl0);
+  const int32_t *wl = r1s ? a.wl1 : round == 1 ? a.nz : ((round & 1) ? a.wl1 : a.wl0);
   int32_t *out = (round & 1) ? a.wl0 : a.wl1;
   int *tail = &ctrl->wl_count[(round + 1) & 1];
   const uint64_t fresh_m = a.fresh ? mix64(combine_seed(a.seed, (uint64_t)round + 1)) : 0;
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
     bool survive = false, undecided = false;
     int32_t v = 0;
     if (i < cnt) {
-      v = (round == 1 && a.nz_identity) ? (int32_t)i : __ldg(&wl[i]);
+      v = (round == 1 && a.nz_identity && !r1s) ? (int32_t)i : __ldg(&wl[i]);
     }
     if (i < cnt && a.state[v] == TCMIS_ALIVE) {
       const int64_t s = ld_stream(&a.off[v]), e = ld_stream(&a.off[v + 1]);
@@ -308,6 +310,61 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
   }
   warp_flush(srv, out, tail);
   warp_flush(und, a.undecided, &ctrl->pull_undec);
+  block_add3(0, rem, 0, ctrl);
+}
+
+// Round 1 on a degree-ordered graph: an alive non-candidate's largest
+// neighbour id is its lowest-degree, highest-priority neighbour, most often
+// a candidate -- one gather of next, no row.  Four consecutive vertices per
+// thread (state and r1_max as vector loads, four gathers in flight); an
+// alive vertex not settled so goes to wl1 (the select side is done with it)
+// for k_probe_pull.
+__global__ void __launch_bounds__(kBlock) k_r1_pull(UpdateArgs a) {
+  pdl_entry();
+  Ctrl *ctrl = a.ctrl;
+  if (ctrl->round != 1) return;
+  stamp_phase(a.rounds, ctrl, 1, 1, 1);
+  constexpr int kV = 4;
+  __shared__ BlockOut<kBlock, kV> left;
+  left.reset();
+  const int64_t n1 = a.n1;
+  unsigned long long rem = 0;
+  const int64_t quads = (n1 + kV - 1) / kV;
+  for (int64_t t = blockIdx.x * (int64_t)kBlock + threadIdx.x; t - threadIdx.x < quads;
+       t += (int64_t)gridDim.x * kBlock) {
+    const int64_t v0 = t * kV;
+    int32_t mx[kV];
+    uint32_t st4 = 0;
+    if (v0 + kV <= n1) {
+      const int4 m4 = __ldg(reinterpret_cast<const int4 *>(a.r1_max + v0));
+      mx[0] = m4.x; mx[1] = m4.y; mx[2] = m4.z; mx[3] = m4.w;
+      st4 = *reinterpret_cast<const uint32_t *>(a.state + v0);
+    } else {
+#pragma unroll
+      for (int j = 0; j < kV; ++j) {
+        const bool ok = t < quads && v0 + j < n1;
+        mx[j] = ok ? __ldg(&a.r1_max[v0 + j]) : -1;
+        st4 |= (uint32_t)(ok ? a.state[v0 + j] : TCMIS_REMOVED) << (8 * j);
+      }
+    }
+    bool alive[kV], hit[kV];
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+      alive[j] = ((st4 >> (8 * j)) & 0xffu) == TCMIS_ALIVE;
+      hit[j] = alive[j] && a.next[mx[j]] == 1;
+    }
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+      const int32_t v = (int32_t)(v0 + j);
+      if (hit[j]) {
+        mark_removed(v, a.state, a.q);
+        publish(a.pub, v);
+        ++rem;
+      }
+      left.put(alive[j] && !hit[j], v);
+    }
+    left.flush(a.wl1, &ctrl->r1_pull_left);
+  }
   block_add3(0, rem, 0, ctrl);
 }
 

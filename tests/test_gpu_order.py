@@ -201,3 +201,37 @@ def test_reordered_rows_are_sorted(ctx, kind):
             assert np.array_equal(got.mis, exp.mis), (kind, mode, heur)
             assert rounds_tuple(got.iterations) == oracle_tuple(exp), (kind, mode, heur)
     dg.close()
+
+
+@pytest.mark.parametrize("pendants", [0, 50])
+def test_degree_order_all_hub_rows(ctx, pendants):
+    """A clique of 4200 vertices (every row longer than the sorted-row limit,
+    order.cu kSortedMax) with or without pendant vertices: the round-1
+    settling data (largest neighbour, class) and the bounds stay exact."""
+    k = 4200
+    iu, ju = np.triu_indices(k, 1)
+    rng = np.random.default_rng(3)
+    pend = np.stack([rng.integers(0, k, pendants), k + np.arange(pendants)], 1)
+    g = O.graph_from_edges(k + pendants, np.concatenate([np.stack([iu, ju], 1), pend]))
+    dg = tc.DeviceGraph.upload(tc.Graph(g.n, g.off, g.nbr), ctx).reorder(tc.DeviceGraph.ORDER_DEGREE)
+    for heur in ("h2", "h3", "luby-perm"):
+        exp = O.solve(g, heur, 5, tile_dim=16)
+        got = tc.run_mis(dg, tc.EngineConfig(heuristic=HEUR[heur], seed=5))
+        assert np.array_equal(got.mis, exp.mis), heur
+        assert rounds_tuple(got.iterations) == oracle_tuple(exp), heur
+    dg.close()
+
+
+def test_round1_settling_switch(ctx, monkeypatch):
+    """The round-1 settling (select.cuh r1_max) on and off give the same solve."""
+    g = O.gen("rmat", 13, 16, 6)
+    dg = tc.DeviceGraph.upload(tc.Graph(g.n, g.off, g.nbr), ctx).reorder(tc.DeviceGraph.ORDER_DEGREE)
+    exp = O.solve(g, "h2", 1, tile_dim=16)
+    for off in (None, "1"):
+        if off:
+            monkeypatch.setenv("TCMIS_NO_R1_SETTLE", off)
+        for excl in (tc.Exclusion.AUTO, tc.Exclusion.PUSH, tc.Exclusion.CSR_PULL):
+            got = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=1, exclusion=excl))
+            assert np.array_equal(got.mis, exp.mis), (off, excl)
+            assert rounds_tuple(got.iterations) == oracle_tuple(exp), (off, excl)
+    dg.close()

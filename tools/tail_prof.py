@@ -10,6 +10,13 @@ buf = (C.c_ulonglong * 256)()
 for cfg in sys.argv[1:]:
     dg = bench.make_device_graph(tc, cfg, ctx)
     dg.tile(16)
+    import os
+    order = os.environ.get("ORDER") or {"rgg": "spatial", "rmat22": "degree",
+                                        "rmat26": "degree"}.get(cfg, "none")
+    if order != "none":
+        dg.reorder({"degree": tc.DeviceGraph.ORDER_DEGREE,
+                    "spatial": tc.DeviceGraph.ORDER_SPATIAL}[order])
+    print(cfg, "order", order)
     for i in range(3):
         L.tcmis_debug_tail_prof(buf, 256)
         tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2))
