@@ -370,8 +370,9 @@ def timeline(tc, ctx):
 PHASE = {"k_probe_select": 1, "k_select": 1, "k_select_long": 1,
          "k_probe_pull": 2, "k_update_pull": 2, "k_tile_excl_bits": 2, "k_tile_excl_mma": 2,
          "k_update": 3, "k_round_end": 3, "k_priorities": 0, "k_tail": 4,
+         "k_prio_settle": 0, "k_r1_pull": 2,
          "k_alive_bits": 1, "k_tile_cand_bits": 1, "k_tile_cand_umma": 1, "k_tile_mark": 1}
-PHASE_NAME = {0: "init (priorities, states)", 1: "Phase 1 candidate detection",
+PHASE_NAME = {0: "init (priorities, states; on the degree order also round 1's class-bound verdicts)", 1: "Phase 1 candidate detection",
               2: "Phase 2 neighbour exclusion (SpMV)", 3: "Phase 3 state update + compaction",
               12: "Phases 1+2 (push exclusion fused into candidate detection)",
               4: "Tail rounds (Phases 1-3 of every remaining round in one persistent kernel, "

@@ -235,6 +235,7 @@ struct tcmis_graph {
   int2 *d_cbc = nullptr;       // the same bounds by class index
   int32_t *d_rmax = nullptr;   // per solve id: its largest neighbour id (-1: isolated)
   uint16_t *d_vcls = nullptr;  // per solve id: its degree class (n_cls <= 65535)
+  int32_t *d_cls_deg = nullptr;  // per class: its degree
   int32_t *d_spatial = nullptr;  // tcmis_gen_rgg's points in Z-order of their cells
   // Phase 1 tile form (tile_cand.cu): the A-up store of one priority
   // configuration (heuristic, seed, scale_bits)

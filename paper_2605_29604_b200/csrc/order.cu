@@ -250,6 +250,11 @@ __global__ void k_hub_max(const int32_t *__restrict__ hub_end, const int64_t *__
     __syncthreads();
   }
 }
+__global__ void k_class_degree(int32_t ncls, const int32_t *__restrict__ cls,
+                               const int64_t *__restrict__ off, int32_t *__restrict__ deg) {
+  for (int32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < ncls; c += gridDim.x * blockDim.x)
+    deg[c] = (int32_t)(off[cls[c] + 1] - off[cls[c]]);
+}
 __global__ void k_vertex_class(int32_t n, int32_t ncls, const int32_t *__restrict__ cls,
                                uint16_t *__restrict__ vcls) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
@@ -281,6 +286,8 @@ void free_order(tcmis_graph *g) {
   dev_free(g->d_cbc);
   dev_free(g->d_rmax);
   dev_free(g->d_vcls);
+  dev_free(g->d_cls_deg);
+  g->d_cls_deg = nullptr;
   g->d_cbc = nullptr;
   g->d_rmax = nullptr;
   g->d_vcls = nullptr;
@@ -564,20 +571,22 @@ int reorder_impl(tcmis_graph *g, int32_t mode, const int32_t *order) {
     dev_free(d_cnt);
   }
   // round 1's settling data (degree order, classes fit a u16)
-  int32_t *rmax = nullptr;
+  int32_t *rmax = nullptr, *cls_deg = nullptr;
   uint16_t *vcls = nullptr;
   if (!rc && mode == TCMIS_ORDER_DEGREE && g->n_cls > 0 && g->n_cls <= 65535) {
     int32_t *hub_end = nullptr;
     rc = dev_alloc(&rmax, (size_t)n);
     if (!rc) rc = dev_alloc(&vcls, (size_t)n);
     if (!rc) rc = dev_alloc(&hub_end, 1);
+    if (!rc) rc = dev_alloc(&cls_deg, (size_t)g->n_cls);
     if (!rc) {
       // every row a hub (no sorted row to find): H = n
       cudaMemcpyAsync(hub_end, &n, 4, cudaMemcpyHostToDevice, st);
       k_row_max<<<grid_for(ctx, n, 256, 8), 256, 0, st>>>(n, roff, rnbr, rmax, hub_end);
       k_hub_max<<<ctx->num_sms * 4, 256, 0, st>>>(hub_end, roff, rnbr, rmax);
       k_vertex_class<<<grid_for(ctx, n, 256, 8), 256, 0, st>>>(n, g->n_cls, cls, vcls);
-      ctx->launches += 3;
+      k_class_degree<<<grid_for(ctx, g->n_cls, 256, 4), 256, 0, st>>>(g->n_cls, cls, roff, cls_deg);
+      ctx->launches += 4;
       cudaError_t e = cudaStreamSynchronize(st);
       if (e != cudaSuccess) rc = cuda_error(e, "round-1 settling data");
     }
@@ -586,6 +595,7 @@ int reorder_impl(tcmis_graph *g, int32_t mode, const int32_t *order) {
   clk.mark("classes + non-isolated list");
   dev_free(bad);
   if (rc) {
+    dev_free(cls_deg);
     dev_free(rmax);
     dev_free(vcls);
     dev_free(cls);
@@ -604,6 +614,7 @@ int reorder_impl(tcmis_graph *g, int32_t mode, const int32_t *order) {
   g->d_rnz = rnz;
   g->d_cls_start = cls;
   g->d_rmax = rmax;
+  g->d_cls_deg = cls_deg;
   g->d_vcls = vcls;
   g->order_mode = mode;
   return 0;

@@ -64,10 +64,9 @@ struct SelectArgs {
   int32_t tile_gate;       // > 0: rounds starting with >= this many alive vertices run
                            // Phase 1 as A-up tiles (k_tile_mark), these kernels idle
   const int2 *cb;          // degree-class bounds (common.cuh class_bounds), or null
-  // round 1 on a degree-ordered graph (everybody alive): a vertex whose
-  // largest neighbour id is >= its class's hi is blocked, one whose largest
-  // neighbour id is < lo is a candidate -- 6 bytes per vertex, no row, no
-  // gather; the rest take the probe below.  Null: off.
+  // round 1 on a degree-ordered graph: k_prio_settle (solver.cu) decided
+  // every vertex it could from the class bounds and listed the rest in wl1
+  // (ctrl->r1_sel_left) for the probe.  Null: off.
   const int32_t *r1_max;
   const uint16_t *r1_cls;
   const int2 *cbc;
@@ -103,62 +102,6 @@ __device__ __forceinline__ void exclude(uint8_t *__restrict__ next, int32_t u) {
 
 constexpr int kProbeK = 4;  // row entries the straight-line probe examines
 
-// Round 1 on a degree-ordered graph (everybody alive; the round-1 list is the
-// id prefix 0 .. n1-1): a vertex whose largest neighbour id (r1_max) is at or
-// above its class's hi is blocked, one whose largest neighbour id is below lo
-// a candidate (pull exclusion only: a push candidate needs its row).  Four
-// consecutive vertices per thread, their 16-byte / 8-byte loads and the four
-// bound lookups in flight together; the vertices left (the uncertain band)
-// go to wl1 (free in round 1) for the probe.
-constexpr int kR1V = 4;
-__global__ void __launch_bounds__(kBlock) k_r1_settle(SelectArgs a) {
-  pdl_entry();
-  Ctrl *ctrl = a.ctrl;
-  if (ctrl->round != 1 || (a.tile_gate && ctrl->alive >= a.tile_gate)) return;
-  stamp_phase(a.rounds, ctrl, 1, 0, 0);
-  __shared__ BlockOut<kBlock, kR1V> left;
-  left.reset();
-  const int64_t n1 = a.n1;
-  unsigned long long sel = 0;
-  const int64_t quads = (n1 + kR1V - 1) / kR1V;
-  for (int64_t t = blockIdx.x * (int64_t)kBlock + threadIdx.x; t - threadIdx.x < quads;
-       t += (int64_t)gridDim.x * kBlock) {
-    const int64_t v0 = t * kR1V;
-    int32_t mx[kR1V], cls[kR1V];
-    if (v0 + kR1V <= n1) {
-      const int4 m4 = __ldg(reinterpret_cast<const int4 *>(a.r1_max + v0));
-      const uint2 c4 = __ldg(reinterpret_cast<const uint2 *>(a.r1_cls + v0));
-      mx[0] = m4.x; mx[1] = m4.y; mx[2] = m4.z; mx[3] = m4.w;
-      cls[0] = c4.x & 0xffff; cls[1] = c4.x >> 16; cls[2] = c4.y & 0xffff; cls[3] = c4.y >> 16;
-    } else {
-#pragma unroll
-      for (int j = 0; j < kR1V; ++j) {
-        const bool ok = t < quads && v0 + j < n1;
-        mx[j] = ok ? __ldg(&a.r1_max[v0 + j]) : -1;
-        cls[j] = ok ? __ldg(&a.r1_cls[v0 + j]) : -1;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kR1V; ++j) {
-      const int32_t v = (int32_t)(v0 + j);
-      int r = -1;  // -1 none, 0 left, 1 blocked, 2 candidate
-      if (cls[j] >= 0) {
-        const int2 cb = __ldg(&a.cbc[cls[j]]);
-        r = mx[j] >= cb.y ? 1 : (mx[j] < cb.x && !a.push ? 2 : 0);
-      }
-      if (r == 2) {
-        mark_candidate(v, a.next, a.state, a.segflag, a.T, a.perm, a.mis_o);
-        publish(a.pub, v);
-        ++sel;
-      }
-      left.put(r == 0, v);
-    }
-    // wl1 is round 2's output list, free in round 1
-    left.flush(const_cast<int32_t *>(a.wl1), &ctrl->r1_sel_left);
-  }
-  block_add3(sel, 0, 0, ctrl);
-}
-
 // Probe: one thread per worklist vertex, straight-line code in warp lockstep
 // (no per-lane loop): coalesced row extents and own key, the last <= 8 row
 // entries with two aligned 16-byte loads, keys of the last kProbeK gathered.
@@ -170,10 +113,11 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
   __shared__ int32_t s_und[kBlock / 32][64];
   Ctrl *ctrl = a.ctrl;
   const int round = ctrl->round;
+  stamp_phase(a.rounds, ctrl, round, 0, 0);
   // round 1 visits only the non-isolated vertices (k_priorities already made
-  // the isolated ones candidates), and after k_r1_settle only those it left
+  // the isolated ones candidates), and on a degree order only those that
+  // k_prio_settle (solver.cu) left undecided
   const bool r1s = round == 1 && a.r1_max;
-  if (!r1s) stamp_phase(a.rounds, ctrl, round, 0, 0);
   const int64_t cnt = r1s ? ctrl->r1_sel_left : round == 1 ? a.n1 : ctrl->wl_count[round & 1];
   if ((int64_t)blockIdx.x * kBlock >= cnt) return;
   const int32_t *wl = r1s ? a.wl1 : round == 1 ? a.nz : ((round & 1) ? a.wl1 : a.wl0);

@@ -182,6 +182,131 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// K2 and round 1's Phase 1 in one pass, for a degree-ordered graph under the
+// H2 priorities (the class bounds, common.cuh class_bounds): per vertex its
+// degree from its class (2 bytes instead of two 8-byte offsets), p and q as
+// k_priorities computes them, and -- everybody being alive in round 1 -- the
+// round-1 verdict from its largest neighbour id: at or above the class's hi
+// blocked (Alive; the pull finds it), below lo a candidate (InMIS, next = 1,
+// the tile column and caller-order marks), else listed in wl1 for the probe.
+// Isolated vertices (degree 0, the end of the order) are candidates as in
+// k_priorities.  The control block and the statistics ring are set by
+// k_init_ctrl before (blocks add to the control block here).
+struct PrioSettleArgs {
+  int32_t n;
+  const int32_t *perm;
+  const uint16_t *cls;
+  const int32_t *cls_deg;
+  const int2 *cbc;
+  const int32_t *rmax;
+  uint64_t mseed;
+  double avg, scale;
+  int qshift;
+  uint32_t *p;
+  uint16_t *q;
+  uint8_t *state, *next, *segflag;
+  int T;
+  uint8_t *mis_o;
+  int push;
+  int32_t *left;
+  Ctrl *ctrl;
+};
+
+__global__ void k_init_ctrl(Ctrl *ctrl, Ctrl c0, DevRound *rounds, int32_t nrounds) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ctrl = c0;
+  for (int32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nrounds; r += gridDim.x * blockDim.x)
+    rounds[r] = DevRound{};
+}
+
+// per-thread inputs of one quad (prefetched one iteration ahead)
+struct PsQuad {
+  int32_t vid[4], cl[4], mx[4];
+};
+__device__ __forceinline__ PsQuad ps_load(const PrioSettleArgs &a, int64_t t, int64_t quads) {
+  PsQuad d;
+  const int64_t v0 = t * 4;
+  if (v0 + 4 <= a.n) {
+    const int4 p4 = __ldg(reinterpret_cast<const int4 *>(a.perm + v0));
+    const uint2 c4 = __ldg(reinterpret_cast<const uint2 *>(a.cls + v0));
+    const int4 m4 = __ldg(reinterpret_cast<const int4 *>(a.rmax + v0));
+    d.vid[0] = p4.x; d.vid[1] = p4.y; d.vid[2] = p4.z; d.vid[3] = p4.w;
+    d.cl[0] = c4.x & 0xffff; d.cl[1] = c4.x >> 16; d.cl[2] = c4.y & 0xffff; d.cl[3] = c4.y >> 16;
+    d.mx[0] = m4.x; d.mx[1] = m4.y; d.mx[2] = m4.z; d.mx[3] = m4.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool ok = t < quads && v0 + j < a.n;
+      d.vid[j] = ok ? __ldg(&a.perm[v0 + j]) : 0;
+      d.cl[j] = ok ? __ldg(&a.cls[v0 + j]) : -1;
+      d.mx[j] = ok ? __ldg(&a.rmax[v0 + j]) : -1;
+    }
+  }
+  return d;
+}
+
+constexpr int kPsFlush = 4;  // iterations between the residual list's flushes
+__global__ void __launch_bounds__(256) k_prio_settle(PrioSettleArgs a) {
+  constexpr int kV = 4;
+  // the residual list leaves the block every kPsFlush iterations: its
+  // barriers stall every warp of the block, and the next quad's loads are in
+  // flight across them (prefetched)
+  __shared__ BlockOut<256, kV * kPsFlush> left;
+  left.reset();
+  unsigned long long sel = 0;
+  const int64_t quads = ((int64_t)a.n + kV - 1) / kV;
+  const int64_t stride = (int64_t)gridDim.x * 256;
+  int64_t t = blockIdx.x * 256ll + threadIdx.x;
+  PsQuad cur = ps_load(a, t, quads);
+  for (int it = 1; t - threadIdx.x < quads; t += stride, ++it) {
+    const PsQuad nx = ps_load(a, t + stride, quads);
+    const int64_t v0 = t * kV;
+    uint32_t pv[kV], st4 = 0, nx4 = 0;
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+      const int32_t deg = cur.cl[j] >= 0 ? __ldg(&a.cls_deg[cur.cl[j]]) : 0;
+      const bool iso = deg == 0;
+      int r = -1;  // -1 none, 0 left to the probe, 1 blocked, 2 candidate
+      if (iso) {
+        pv[j] = 0;  // as k_priorities: never compared
+      } else {
+        const uint64_t h = mix64(a.mseed + (uint64_t)(cur.vid[j] + 1) * kGolden);
+        const double eps = (double)(h >> 11) * 0x1.0p-53;  // hash_to_unit, priorities.cpp:25-27
+        pv[j] = h2_value(a.avg, deg, eps, a.scale);
+        const int2 cb = __ldg(&a.cbc[cur.cl[j]]);
+        r = cur.mx[j] >= cb.y ? 1 : (cur.mx[j] < cb.x && !a.push ? 2 : 0);
+      }
+      const bool in = cur.cl[j] >= 0 && (iso || r == 2);
+      st4 |= (uint32_t)(in ? TCMIS_IN_MIS : TCMIS_ALIVE) << (8 * j);
+      nx4 |= (uint32_t)(in ? 1 : 0) << (8 * j);
+      if (in) {
+        if (a.segflag) a.segflag[seg_of(cur.vid[j], a.T)] = 1;
+        if (a.mis_o) a.mis_o[cur.vid[j]] = TCMIS_IN_MIS;
+      }
+      if (r == 2) ++sel;
+      left.put(r == 0, (int32_t)(v0 + j));
+    }
+    if (v0 + kV <= a.n) {
+      *reinterpret_cast<uint4 *>(a.p + v0) = make_uint4(pv[0], pv[1], pv[2], pv[3]);
+      *reinterpret_cast<uint2 *>(a.q + v0) =
+          make_uint2((uint32_t)q_of(pv[0], a.qshift) | ((uint32_t)q_of(pv[1], a.qshift) << 16),
+                     (uint32_t)q_of(pv[2], a.qshift) | ((uint32_t)q_of(pv[3], a.qshift) << 16));
+      *reinterpret_cast<uint32_t *>(a.state + v0) = st4;
+      *reinterpret_cast<uint32_t *>(a.next + v0) = nx4;
+    } else {
+      for (int j = 0; j < kV && v0 + j < a.n; ++j) {
+        a.p[v0 + j] = pv[j];
+        a.q[v0 + j] = q_of(pv[j], a.qshift);
+        a.state[v0 + j] = (uint8_t)(st4 >> (8 * j));
+        a.next[v0 + j] = (uint8_t)(nx4 >> (8 * j));
+      }
+    }
+    // block-uniform: the block's last iteration, or every kPsFlush
+    if (it % kPsFlush == 0 || t - threadIdx.x + stride >= quads) left.flush(a.left, &a.ctrl->r1_sel_left);
+    cur = nx;
+  }
+  block_add3(sel, 0, 0, a.ctrl);
+}
+
 __global__ void k_max_degree(int32_t n, const int64_t *__restrict__ off,
                              unsigned long long *__restrict__ out) {
   unsigned long long mx = 0;
@@ -711,6 +836,41 @@ int launch_priorities(tcmis_graph *g, int heuristic, uint64_t seed, int scale_bi
   return 0;
 }
 
+// the fused init + round-1 settle (k_prio_settle) of a degree-ordered H2 solve
+int launch_prio_settle(tcmis_graph *g, const RoundArgs &a, uint64_t seed, int scale_bits,
+                       int heuristic, uint8_t *segflag, const Ctrl &c0) {
+  tcmis_ctx *ctx = g->ctx;
+  cudaStream_t st = ctx->stream;
+  Workspace &ws = g->ws;
+  k_init_ctrl<<<4, 1024, 0, st>>>(ws.ctrl, c0, ws.rounds, ws.round_cap);
+  TCMIS_LAUNCHED(ctx);
+  PrioSettleArgs p;
+  p.n = g->n;
+  p.perm = a.perm;
+  p.cls = a.r1_cls;
+  p.cls_deg = g->d_cls_deg;
+  p.cbc = a.cbc;
+  p.rmax = a.r1_max;
+  p.mseed = mix64(seed);
+  p.avg = avg_degree(g);
+  p.scale = (double)(1u << scale_bits);
+  p.qshift = q_shift(heuristic, scale_bits);
+  p.p = ws.prio;
+  p.q = ws.q;
+  p.state = ws.state;
+  p.next = ws.next;
+  p.segflag = segflag;
+  p.T = a.T;
+  p.mis_o = a.mis_o;
+  p.push = a.pull ? 0 : 1;
+  p.left = ws.wl[1];
+  p.ctrl = ws.ctrl;
+  const int grid = grid_for(ctx, ((int64_t)g->n + 3) / 4, 256, 8);
+  TCMIS_TIMED(ctx, "k_prio_settle", (k_prio_settle<<<grid, 256, 0, st>>>(p)));
+  TCMIS_LAUNCHED(ctx);
+  return 0;
+}
+
 namespace {
 
 int validate(const tcmis_graph *g, const tcmis_config *c) {
@@ -926,10 +1086,6 @@ int launch_select(tcmis_graph *g, const RoundArgs &a) {
                     ws.ctrl, a.tile_gate, s.push, a.off, a.nbr)));
     TCMIS_LAUNCHED(ctx);
   }
-  if (a.r1_max) {
-    TCMIS_TIMED(ctx, "k_r1_settle", (launch_round_kernel(k_r1_settle, a.sel_grid, st, s)));
-    TCMIS_LAUNCHED(ctx);
-  }
   TCMIS_TIMED(ctx, "k_probe_select", (launch_round_kernel(k_probe_select, a.sel_grid, st, s)));
   TCMIS_LAUNCHED(ctx);
   TCMIS_TIMED(ctx, "k_select",
@@ -979,7 +1135,7 @@ int launch_update(tcmis_graph *g, const RoundArgs &a, cudaGraphConditionalHandle
 }
 
 inline int launches_per_round(const RoundArgs &a) {
-  return ((a.pull || a.tile) ? 6 : 4) + (a.tile_cand ? 3 : 0);
+  return ((a.pull || a.tile) ? 6 : 4) + (a.tile_cand ? 3 : 0) + (a.r1_max && a.pull ? 1 : 0);
 }
 
 // The parameters of a solve's first kernels (segment-flag clear,
@@ -1030,7 +1186,10 @@ int ensure_solve_graph(tcmis_graph *g, const RoundArgs &a, const SolvePre &pre) 
       e = cudaMemsetAsync(a.mis_o, 0, (size_t)g->n, st);
       if (e != cudaSuccess) rc = cuda_error(e, "memset(mis_o)");
     }
-    if (!rc)
+    if (!rc && a.r1_max)  // degree order: init and round 1's settle in one pass
+      rc = launch_prio_settle(g, a, pre.seed, pre.scale_bits, pre.H,
+                              pre.seg_mode ? ws.segflag : nullptr, pre.c0);
+    else if (!rc)
       rc = launch_priorities(g, pre.H, pre.seed, pre.scale_bits, ws.prio, ws.q, ws.state, ws.next,
                              pre.seg_mode ? ws.segflag : nullptr, pre.T, ws.ctrl, &pre.c0,
                              ws.rounds, ws.round_cap, a.off, a.perm, a.mis_o);
@@ -1264,18 +1423,18 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
   bool step = cfg->observer || timing || (cfg->flags & TCMIS_F_HOST_LOOP);
   // the solve's first kernels: segment flags cleared, priorities, states, and
   // the control block + zeroed statistics ring (k_tail accumulates into it)
+  RoundArgs a;
+  std::memset(&a, 0, sizeof(a));
   auto launch_pre = [&]() -> int {
     if (seg_mode) TCMIS_CUDA(cudaMemsetAsync(ws.segflag, 0, (size_t)nseg, st));
     if (s_mis_o) TCMIS_CUDA(cudaMemsetAsync(s_mis_o, 0, (size_t)g->n, st));
+    if (a.r1_max)  // degree order: init and round 1's settle in one pass
+      return launch_prio_settle(g, a, cfg->seed, cfg->scale_bits, H, seg0, c0);
     return launch_priorities(g, H, cfg->seed, cfg->scale_bits, ws.prio, ws.q, ws.state, ws.next,
                              seg0, T > 0 ? T : 1, ws.ctrl, &c0, ws.rounds, ws.round_cap, s_off,
                              s_perm, s_mis_o);
   };
-  if (step)
-    if (int rc = launch_pre()) return rc;
 
-  RoundArgs a;
-  std::memset(&a, 0, sizeof(a));
   a.n = g->n;
   a.off = s_off;
   a.nbr = s_nbr;
@@ -1349,6 +1508,8 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     // one vertex per thread (tail.cuh): at most kTailBlock per block
     a.tail_thr = (int32_t)std::min<int64_t>(a.tail_thr, (int64_t)a.tail_grid * kTailBlock);
   }
+  if (step)
+    if (int rc = launch_pre()) return rc;
   if (seg_mode == 1 && a.tail_thr > 0)
     TCMIS_CUDA(cudaMemsetAsync(ws.segmark, 0, sizeof(uint32_t) * (size_t)nseg, st));
 
@@ -1426,8 +1587,9 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       // unless the tail packed (h3 adds k_seg_total)
       const bool gather = a.perm && !a.mis_o;
       const bool tail_packs = a.tail_thr > 0 && seg_mode != 2 && !gather;
-      ctx->launches += 2 + launches_per_round(a) * (int64_t)mr + (seg_mode == 2 ? 1 : 0) +
-                       (tail_packs ? 0 : 1) + (gather && a.tail_thr > 0 ? 1 : 0);
+      ctx->launches += 2 + (a.r1_max ? 1 : 0) + launches_per_round(a) * (int64_t)mr +
+                       (seg_mode == 2 ? 1 : 0) + (tail_packs ? 0 : 1) +
+                       (gather && a.tail_thr > 0 ? 3 : 0);
       const int pre_n = std::min(rr, std::min(ws.round_cap, 64));
       rounds_h.assign(hr.rounds, hr.rounds + pre_n);
       if (rr > pre_n) {
