@@ -8,9 +8,12 @@
 // tcmis_graph_reorder keeps the caller's CSR and ids and adds a relabeled
 // copy of the CSR (solve id i = the caller's vertex perm[i]):
 //
-//   TCMIS_ORDER_DEGREE   by degree, descending, ties by id (stable): R-MAT's
-//                        hubs -- the most gathered vertices -- share sectors,
-//                        and the isolated vertices leave the gathered range;
+//   TCMIS_ORDER_DEGREE   by degree, descending, ties by id (stable; for a
+//                        tcmis_gen_rgg graph ties in its points' spatial
+//                        order): R-MAT's hubs -- the most gathered vertices
+//                        -- share sectors, the isolated vertices leave the
+//                        gathered range, and the degree classes carry the
+//                        H2 key bounds (solver.cu k_class_bounds);
 //   TCMIS_ORDER_SPATIAL  tcmis_gen_rgg's points by Morton code of their grid
 //                        cell: a vertex's neighbours sit in the same or the
 //                        adjacent cells, i.e. at nearby solve ids;
@@ -37,13 +40,18 @@ namespace tcmis_b200 {
 
 namespace {
 
+// the sort's input sequence: the caller's ids, or (tcmis_gen_rgg graphs) its
+// points in spatial order, so that the stable sort keeps each degree class
+// in that order and the gathers keep their locality within a class
 __global__ void k_degree_keys(int32_t n, const int64_t *__restrict__ off,
-                              uint32_t *__restrict__ key, int32_t *__restrict__ id) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
+                              const int32_t *__restrict__ seq, uint32_t *__restrict__ key,
+                              int32_t *__restrict__ id) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = seq ? seq[i] : (int32_t)i;
     const int64_t d = off[v + 1] - off[v];
-    key[v] = ~(uint32_t)(d > 0xffffffffLL ? 0xffffffffLL : d);  // ascending key = descending degree
-    id[v] = (int32_t)v;
+    key[i] = ~(uint32_t)(d > 0xffffffffLL ? 0xffffffffLL : d);  // ascending key = descending degree
+    id[i] = v;
   }
 }
 
@@ -465,7 +473,8 @@ int reorder_impl(tcmis_graph *g, int32_t mode, const int32_t *order) {
     if (!rc) rc = dev_alloc(&key2, (size_t)n);
     if (!rc) rc = dev_alloc(&id, (size_t)n);
     if (!rc) {
-      k_degree_keys<<<grid_for(ctx, n, 256, 16), 256, 0, st>>>(n, g->d_off, key, id);
+      k_degree_keys<<<grid_for(ctx, n, 256, 16), 256, 0, st>>>(n, g->d_off, g->d_spatial, key,
+                                                                id);
       ctx->launches++;
       size_t bytes = 0;
       cub::DeviceRadixSort::SortPairs(nullptr, bytes, key, key2, id, perm, n, 0, 32, st);
