@@ -210,12 +210,12 @@ struct PrioSettleArgs {
   int push;
   int32_t *left;
   Ctrl *ctrl;
+  DevRound *rounds;  // the statistics ring, zeroed here (nothing stamps it in this kernel)
+  int32_t nrounds;
 };
 
-__global__ void k_init_ctrl(Ctrl *ctrl, Ctrl c0, DevRound *rounds, int32_t nrounds) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) *ctrl = c0;
-  for (int32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nrounds; r += gridDim.x * blockDim.x)
-    rounds[r] = DevRound{};
+__global__ void k_init_ctrl(Ctrl *ctrl, Ctrl c0) {
+  if (threadIdx.x == 0) *ctrl = c0;
 }
 
 // per-thread inputs of one quad (prefetched one iteration ahead)
@@ -252,6 +252,8 @@ __global__ void __launch_bounds__(256) k_prio_settle(PrioSettleArgs a) {
   // flight across them (prefetched)
   __shared__ BlockOut<256, kV * kPsFlush> left;
   left.reset();
+  for (int32_t r = blockIdx.x * 256 + threadIdx.x; r < a.nrounds; r += gridDim.x * 256)
+    a.rounds[r] = DevRound{};
   unsigned long long sel = 0;
   const int64_t quads = ((int64_t)a.n + kV - 1) / kV;
   const int64_t stride = (int64_t)gridDim.x * 256;
@@ -421,28 +423,25 @@ __global__ void __launch_bounds__(kGcBlock) k_gc_ids(int32_t n, const uint32_t *
                                                      const int64_t *__restrict__ blk_off,
                                                      int32_t nblk, int32_t *__restrict__ mis,
                                                      int64_t *__restrict__ mis_count) {
-  // each warp's ids (<= 32 words x 32) staged in shared memory, then stored
-  // coalesced: the warp's words are contiguous, so are its ids
+  // each warp expands its 32 words one at a time: lane j writes bit j's id
+  // at the word's position + the set bits below j -- every store of a step
+  // lands in one contiguous run (no per-thread bit loop, no staging)
   using Scan = cub::BlockScan<int, kGcBlock>;
   __shared__ typename Scan::TempStorage tmp;
-  __shared__ int32_t s_ids[kGcBlock / 32][1024];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int64_t word = blockIdx.x * (int64_t)kGcBlock + threadIdx.x;
-  uint32_t m = word * 32 < n ? bits[word] : 0u;
-  const int c = __popc(m);
+  const uint32_t m = word * 32 < n ? bits[word] : 0u;
   int pos = 0;
-  Scan(tmp).ExclusiveSum(c, pos);
-  const int wbase = __shfl_sync(0xffffffffu, pos, 0);
-  const int wtotal = __shfl_sync(0xffffffffu, pos + c, 31) - wbase;
-  int k = pos - wbase;
-  while (m) {
-    const int b = __ffs(m) - 1;
-    m &= m - 1;
-    s_ids[w][k++] = (int32_t)(word * 32 + b);
+  Scan(tmp).ExclusiveSum(__popc(m), pos);
+  const int64_t gpos = blk_off[blockIdx.x] + pos;
+  const int64_t w0 = word - lane;
+  const uint32_t below = (1u << lane) - 1u;
+#pragma unroll 4
+  for (int k = 0; k < 32; ++k) {
+    const uint32_t wk = __shfl_sync(0xffffffffu, m, k);
+    const int64_t pk = __shfl_sync(0xffffffffu, gpos, k);
+    if ((wk >> lane) & 1u) mis[pk + __popc(wk & below)] = (int32_t)((w0 + k) * 32 + lane);
   }
-  __syncwarp();
-  int32_t *out = mis + blk_off[blockIdx.x] + wbase;
-  for (int i = lane; i < wtotal; i += 32) out[i] = s_ids[w][i];
   if (blockIdx.x == 0 && threadIdx.x == 0) *mis_count = blk_off[nblk];
 }
 
@@ -842,7 +841,7 @@ int launch_prio_settle(tcmis_graph *g, const RoundArgs &a, uint64_t seed, int sc
   tcmis_ctx *ctx = g->ctx;
   cudaStream_t st = ctx->stream;
   Workspace &ws = g->ws;
-  k_init_ctrl<<<4, 1024, 0, st>>>(ws.ctrl, c0, ws.rounds, ws.round_cap);
+  k_init_ctrl<<<1, 32, 0, st>>>(ws.ctrl, c0);
   TCMIS_LAUNCHED(ctx);
   PrioSettleArgs p;
   p.n = g->n;
@@ -865,6 +864,8 @@ int launch_prio_settle(tcmis_graph *g, const RoundArgs &a, uint64_t seed, int sc
   p.push = a.pull ? 0 : 1;
   p.left = ws.wl[1];
   p.ctrl = ws.ctrl;
+  p.rounds = ws.rounds;
+  p.nrounds = ws.round_cap;
   const int grid = grid_for(ctx, ((int64_t)g->n + 3) / 4, 256, 8);
   TCMIS_TIMED(ctx, "k_prio_settle", (k_prio_settle<<<grid, 256, 0, st>>>(p)));
   TCMIS_LAUNCHED(ctx);
@@ -996,6 +997,7 @@ TailArgs tail_args(tcmis_graph *g, const RoundArgs &a) {
   t.pack = nullptr;
   t.perm = a.perm;
   t.mis_o = a.mis_o;
+
   return t;
 }
 

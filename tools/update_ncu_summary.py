@@ -27,7 +27,10 @@ for cfg, path in zip(args[::2], args[1::2]):
         k = launches.setdefault(int(d["ID"]), {"name": d["Kernel Name"]})
         k[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
     seq = [launches[i] for i in sorted(launches)]
-    starts = [i for i, k in enumerate(seq) if "k_priorities" in k["name"]]
+    # a solve starts with k_priorities, or on the degree order k_init_ctrl +
+    # k_prio_settle (the fused init)
+    starts = [i for i, k in enumerate(seq)
+              if "k_priorities" in k["name"] or "k_init_ctrl" in k["name"]]
     if not starts:
         continue
     solve = seq[starts[-1]:]
@@ -41,4 +44,4 @@ for cfg, path in zip(args[::2], args[1::2]):
         entry[short] = {"dram_bytes": int(tb), "duration_us": k.get("gpu__time_duration.sum", 0) / 1e3}
     summ[cfg] = entry
 json.dump(summ, open(out_path, "w"), indent=1)
-print(json.dumps(summ, indent=1)[:3000])
+print({c: sorted(v) for c, v in summ.items() if isinstance(v, dict)})
