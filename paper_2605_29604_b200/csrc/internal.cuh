@@ -322,6 +322,8 @@ struct RoundArgs {
   int32_t nz_count;     // round-1 select list
   const int32_t *nz;
   int32_t tail_thr;     // rounds start in k_tail once alive <= tail_thr
+  int tail_from1;       // the whole solve in k_tail (small graphs: every non-isolated
+                        // vertex fits the tail's block-resident lists)
   int64_t vnnz;         // nnz, negated when the neighbour array is not 16-byte aligned
   uint32_t *pub_cand;   // multi-GPU publish slices (null on one GPU)
   uint32_t *pub_dead;

@@ -997,6 +997,9 @@ TailArgs tail_args(tcmis_graph *g, const RoundArgs &a) {
   t.pack = nullptr;
   t.perm = a.perm;
   t.mis_o = a.mis_o;
+  t.nz = a.nz;
+  t.nz_count = a.nz_count;
+  t.nz_identity = a.nz_count == a.n || a.nz_prefix ? 1 : 0;
 
   return t;
 }
@@ -1216,7 +1219,10 @@ int ensure_solve_graph(tcmis_graph *g, const RoundArgs &a, const SolvePre &pre) 
   cudaGraphConditionalHandle cond;
   cudaGraphNode_t node = nullptr;
   if (!rc) {
-    e = cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault);
+    // the loop's first test: round 1 runs in the round kernels unless the
+    // whole solve is the tail's
+    e = cudaGraphConditionalHandleCreate(&cond, graph, a.tail_from1 ? 0 : 1,
+                                         cudaGraphCondAssignDefault);
     cudaGraphNodeParams p{};
     p.type = cudaGraphNodeTypeConditional;
     p.conditional.handle = cond;
@@ -1509,6 +1515,21 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     // k_tail keeps each block's share of its starting list in shared memory,
     // one vertex per thread (tail.cuh): at most kTailBlock per block
     a.tail_thr = (int32_t)std::min<int64_t>(a.tail_thr, (int64_t)a.tail_grid * kTailBlock);
+    // a small graph whose non-isolated vertices all fit the tail's lists
+    // runs every round there: no round-kernel launches at all (not with the
+    // degree order's fused round-1 verdicts, which are round-kernel work)
+    // (AUTO exclusion only: an explicit exclusion form or the tile Phase 1
+    // asks for the round kernels; with TCMIS_TAIL_THRESHOLD set, only when
+    // the non-isolated vertices are within it)
+    const int64_t cap = (int64_t)a.tail_grid * kTailBlock;
+    const char *whole = std::getenv("TCMIS_TAIL_WHOLE");
+    const bool thr_env = std::getenv("TCMIS_TAIL_THRESHOLD") != nullptr;
+    if (a.nz_count > 0 && a.nz_count <= cap && (!thr_env || a.nz_count <= a.tail_thr) && a.tail_thr > 0 &&
+        !a.r1_max && !a.tile_cand && cfg->exclusion == TCMIS_EXCL_AUTO &&
+        !(whole && whole[0] == '0')) {
+      a.tail_thr = (int32_t)cap;
+      a.tail_from1 = 1;
+    }
   }
   if (step)
     if (int rc = launch_pre()) return rc;
@@ -1579,6 +1600,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       // the statistics every round (pathological inputs such as long paths)
       step = true;
       a.tail_thr = 0;
+      a.tail_from1 = 0;
       tail_compacted = false;
       *ws.h_ctrl = c0;
       if (int rc = launch_pre()) return rc;
@@ -1604,7 +1626,27 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       finished = true;
     }
   }
-  if (step) {
+  // the rounds after `done` (0 = all of them) in k_tail, their statistics to the host
+  auto run_tail_from = [&](int done) -> int {
+    ctx->rec_round = done + 1;
+    if (int rc = launch_tail(g, a)) return rc;
+    tail_compacted = !(a.perm && !a.mis_o);
+    TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    TCMIS_CUDA(cudaStreamSynchronize(st));
+    const int rr = ws.h_ctrl->round - 1;
+    if (rr - done > ws.round_cap)
+      return set_error(TCMIS_E_RUNTIME, "round statistics capacity exceeded in k_tail");
+    for (int r = done; r < rr; ++r) {
+      DevRound dr;
+      TCMIS_CUDA(cudaMemcpy(&dr, ws.rounds + r % ws.round_cap, sizeof(DevRound),
+                            cudaMemcpyDeviceToHost));
+      rounds_h.push_back(dr);
+    }
+    return 0;
+  };
+  if (step && a.tail_from1) {
+    if (int rc = run_tail_from(0)) return rc;
+  } else if (step) {
     int round = 0;
     for (;;) {
       ++round;
@@ -1637,20 +1679,7 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
       rounds_h.push_back(dr);
       if (ws.h_ctrl->alive == 0 || ws.h_ctrl->corrupt) break;
       if (a.tail_thr > 0 && ws.h_ctrl->alive <= a.tail_thr) {
-        ctx->rec_round = round + 1;
-        if (int rc = launch_tail(g, a)) return rc;
-        tail_compacted = !(a.perm && !a.mis_o);
-        TCMIS_CUDA(cudaMemcpyAsync(ws.h_ctrl, ws.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
-        TCMIS_CUDA(cudaStreamSynchronize(st));
-        const int rr = ws.h_ctrl->round - 1;
-        if (rr - round > ws.round_cap)
-          return set_error(TCMIS_E_RUNTIME, "round statistics capacity exceeded in k_tail");
-        for (int r = round; r < rr; ++r) {
-          DevRound dr;
-          TCMIS_CUDA(cudaMemcpy(&dr, ws.rounds + r % ws.round_cap, sizeof(DevRound),
-                                cudaMemcpyDeviceToHost));
-          rounds_h.push_back(dr);
-        }
+        if (int rc = run_tail_from(round)) return rc;
         break;
       }
     }

@@ -143,6 +143,12 @@ struct TailArgs {
   uint8_t *mis_o;           // ... and, when kept, the membership in the caller's
                             // order, which the count pass and the compaction
                             // stream instead of the solve-order states
+  // a solve that starts in the tail (round 1): its list is the non-isolated
+  // vertices, and round 1's statistics also hold the isolated candidates
+  // k_priorities marked (ctrl->sel, their segment flags)
+  const int32_t *nz;
+  int32_t nz_count;
+  int nz_identity;
 };
 
 // Grid barrier whose arrival also sums one value per block: bar[0..1] is a
@@ -394,7 +400,26 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
     return;
   }
   const int r0 = *(volatile int *)&ctrl->round;
-  const int64_t cnt0 = *(volatile int *)&ctrl->wl_count[r0 & 1];
+  const bool from1 = r0 == 1;  // the whole solve in this kernel
+  const int64_t cnt0 = from1 ? a.nz_count : *(volatile int *)&ctrl->wl_count[r0 & 1];
+  if (from1) {
+    // round 1's isolated candidates (k_priorities): their count, and for the
+    // seg_mode-1 tile counters their block columns, marked as counted in
+    // round 1 so that the round's own candidates there add nothing twice
+    if (blockIdx.x == 0 && threadIdx.x == 0 && ctrl->sel)
+      atomicAdd(slot_field(a, 1, 0), (unsigned long long)ctrl->sel);
+    if (a.seg_mode == 1) {
+      unsigned long long ev = 0;
+      for (int64_t sb = blockIdx.x * (int64_t)kTailBlock + threadIdx.x; sb < a.nseg;
+           sb += (int64_t)gridDim.x * kTailBlock)
+        if (a.segflag[sb]) {
+          a.segmark[sb] = 1u;
+          ev += (unsigned long long)__ldg(&a.rowtiles[sb]);
+        }
+      ev = __reduce_add_sync(0xffffffffu, (unsigned)ev);
+      if ((threadIdx.x & 31) == 0 && ev) atomicAdd(slot_field(a, 1, 3), ev);
+    }
+  }
   TAIL_MARK(1, cnt0);
   // the block's share of the starting list (<= kTailBlock entries: host
   // cap): entries b, b + G, b + 2G, ... -- interleaved, because the list's
@@ -405,7 +430,8 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
   {
     const int32_t *in0 = (r0 & 1) ? a.wl1 : a.wl0;
     if (threadIdx.x < nl) {
-      const int32_t v = __ldcg(&in0[blockIdx.x + (int64_t)threadIdx.x * gridDim.x]);
+      const int64_t idx = blockIdx.x + (int64_t)threadIdx.x * gridDim.x;
+      const int32_t v = !from1 ? __ldcg(&in0[idx]) : a.nz_identity ? (int32_t)idx : __ldg(&a.nz[idx]);
       s_v[threadIdx.x] = v;
       s_o[threadIdx.x] = a.perm ? __ldg(&a.perm[v]) : v;
       s_s[threadIdx.x] = __ldg(&a.off[v]);

@@ -603,10 +603,16 @@ def test_upload_tiled_edge_cases(ctx):
 
 
 @pytest.mark.parametrize("host_loop", [False, True])
-def test_phase_timers_default_path(ctx, host_loop):
+@pytest.mark.parametrize("whole", [None, "0"])
+def test_phase_timers_default_path(ctx, host_loop, whole, monkeypatch):
     """The reference fills phase1/2/3_ms every round (engine.cpp:253-284):
     the default path (one CUDA graph, or the host loop) stamps %globaltimer
-    per phase, so every round has a positive time and total_ms() > 0."""
+    per phase, so every round has a positive time and total_ms() > 0.
+    whole: None = this 65k-vertex graph runs every round in k_tail (one pass
+    per round: the round's time is booked as Phase 1); "0" = round 1 in the
+    per-round kernels (TCMIS_TAIL_WHOLE=0)."""
+    if whole is not None:
+        monkeypatch.setenv("TCMIS_TAIL_WHOLE", whole)
     dg = tc.DeviceGraph.rmat(16, 16, 1, ctx)
     for heur in (tc.Heuristic.H2, tc.Heuristic.H1, tc.Heuristic.LubyPerm):
         res = tc.run_mis(dg, tc.EngineConfig(heuristic=heur, host_loop=host_loop))
@@ -614,9 +620,10 @@ def test_phase_timers_default_path(ctx, host_loop):
         for it in res.iterations:
             assert it.phase1_ms > 0.0, (heur, it.iteration)
             assert it.phase1_ms + it.phase2_ms + it.phase3_ms < 1000.0
-        # round 1 runs in the per-round kernels: pull exclusion on R-MAT has
-        # its own Phase 2 kernels and the update its own Phase 3
-        assert res.iterations[0].phase2_ms > 0.0 and res.iterations[0].phase3_ms > 0.0
+        if whole == "0":
+            # round 1 in the per-round kernels: pull exclusion on R-MAT has
+            # its own Phase 2 kernels and the update its own Phase 3
+            assert res.iterations[0].phase2_ms > 0.0 and res.iterations[0].phase3_ms > 0.0
     dg.close()
 
 
