@@ -328,6 +328,30 @@ struct BlockOut {
     pos = __shfl_sync(0xffffffffu, pos, 0);
     if (have) buf[pos + __popc(m & ((1u << lane) - 1u))] = v;
   }
+  // up to kN entries per lane (have[j] -> v[j]) with ONE warp scan and one
+  // shared atomic per warp; call from converged code (no per-entry ballots,
+  // which the compiler must emulate when it cannot prove convergence)
+  template <int kN>
+  __device__ __forceinline__ void put_n(const bool (&have)[kN], const int32_t (&v)[kN]) {
+    const int lane = threadIdx.x & 31;
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < kN; ++j) c += have[j] ? 1 : 0;
+    int incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) return;
+    int base = 0;
+    if (lane == 31) base = atomicAdd(&n, total);
+    base = __shfl_sync(0xffffffffu, base, 31) + incl - c;
+#pragma unroll
+    for (int j = 0; j < kN; ++j)
+      if (have[j]) buf[base++] = v[j];
+  }
   __device__ __forceinline__ void flush(int32_t *out, int *tail) {
     __syncthreads();
     if (threadIdx.x == 0) base = n ? atomicAdd(tail, n) : 0;

@@ -245,24 +245,108 @@ __device__ __forceinline__ PsQuad ps_load(const PrioSettleArgs &a, int64_t t, in
 }
 
 constexpr int kPsFlush = 4;  // iterations between the residual list's flushes
+
+// The per-vertex inputs (perm, r1_max, class) of a chunk of 1024 vertices
+// reach shared memory by TMA bulk copies (cp.async.bulk, completion on an
+// mbarrier), kPsStages chunks ahead of the chunk being processed: the loads
+// need no registers, so the kernel keeps DRAM busy at its register-limited
+// occupancy (ncu, the register-prefetch version: 19 % of the warps' stalls
+// sat on the first use of a just-loaded class index).
+constexpr int kPsChunk = 1024, kPsStages = 3;
+struct __align__(16) PsStage {
+  int32_t perm[kPsChunk];
+  int32_t rmax[kPsChunk];
+  uint16_t cls[kPsChunk];
+};
+
+__device__ __forceinline__ void ps_issue(const PrioSettleArgs &a, PsStage &st, uint64_t &bar,
+                                         int64_t c) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
+  constexpr uint32_t kBytes = sizeof(PsStage);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kBytes)
+               : "memory");
+  const int64_t v0 = c * kPsChunk;
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(st.perm)),
+      "l"(a.perm + v0), "r"(4u * kPsChunk), "r"(b)
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(st.rmax)),
+      "l"(a.rmax + v0), "r"(4u * kPsChunk), "r"(b)
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(st.cls)),
+      "l"(a.cls + v0), "r"(2u * kPsChunk), "r"(b)
+      : "memory");
+}
+
+__device__ __forceinline__ void ps_wait(uint64_t &bar, uint32_t parity) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(b), "r"(parity)
+        : "memory");
+  }
+}
+
 __global__ void __launch_bounds__(256) k_prio_settle(PrioSettleArgs a) {
   constexpr int kV = 4;
-  // the residual list leaves the block every kPsFlush iterations: its
-  // barriers stall every warp of the block, and the next quad's loads are in
-  // flight across them (prefetched)
+  static_assert(256 * kV == kPsChunk, "a thread per quad of the chunk");
+  __shared__ PsStage stg[kPsStages];
+  __shared__ __align__(8) uint64_t bar[kPsStages];
+  // the residual list leaves the block every kPsFlush chunks (its barriers
+  // stall every warp of the block)
   __shared__ BlockOut<256, kV * kPsFlush> left;
-  left.reset();
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kPsStages; ++st)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(&bar[st])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  left.reset();  // (a block barrier: the barriers are initialised)
   for (int32_t r = blockIdx.x * 256 + threadIdx.x; r < a.nrounds; r += gridDim.x * 256)
     a.rounds[r] = DevRound{};
   unsigned long long sel = 0;
   const int64_t quads = ((int64_t)a.n + kV - 1) / kV;
-  const int64_t stride = (int64_t)gridDim.x * 256;
-  int64_t t = blockIdx.x * 256ll + threadIdx.x;
-  PsQuad cur = ps_load(a, t, quads);
-  for (int it = 1; t - threadIdx.x < quads; t += stride, ++it) {
-    const PsQuad nx = ps_load(a, t + stride, quads);
-    const int64_t v0 = t * kV;
+  const int64_t nchunks = ((int64_t)a.n + kPsChunk - 1) / kPsChunk;
+  const int64_t full = (int64_t)a.n / kPsChunk;  // chunks wholly inside [0, n)
+  const int64_t G = gridDim.x;
+  if (threadIdx.x == 0)
+    for (int st = 0; st < kPsStages; ++st) {
+      const int64_t c = blockIdx.x + st * G;
+      if (c < full) ps_issue(a, stg[st], bar[st], c);
+    }
+  uint32_t parity = 0;  // bit st: the parity stage st waits for next
+  int it = 0;
+  for (int64_t c = blockIdx.x; c < nchunks; c += G, ++it) {
+    const int st = it % kPsStages;
+    PsQuad cur;
+    if (c < full) {
+      ps_wait(bar[st], (parity >> st) & 1u);
+      parity ^= 1u << st;
+      const int4 p4 = *reinterpret_cast<const int4 *>(stg[st].perm + kV * threadIdx.x);
+      const int4 m4 = *reinterpret_cast<const int4 *>(stg[st].rmax + kV * threadIdx.x);
+      const uint2 c4 = *reinterpret_cast<const uint2 *>(stg[st].cls + kV * threadIdx.x);
+      cur.vid[0] = p4.x; cur.vid[1] = p4.y; cur.vid[2] = p4.z; cur.vid[3] = p4.w;
+      cur.mx[0] = m4.x; cur.mx[1] = m4.y; cur.mx[2] = m4.z; cur.mx[3] = m4.w;
+      cur.cl[0] = c4.x & 0xffff; cur.cl[1] = c4.x >> 16; cur.cl[2] = c4.y & 0xffff; cur.cl[3] = c4.y >> 16;
+      __syncthreads();  // stage st is read: refill it kPsStages chunks ahead
+      if (threadIdx.x == 0 && c + kPsStages * G < full)
+        ps_issue(a, stg[st], bar[st], c + kPsStages * G);
+    } else {
+      cur = ps_load(a, c * 256 + threadIdx.x, quads);  // the partial last chunk
+    }
+    const int64_t v0 = c * kPsChunk + kV * threadIdx.x;
     uint32_t pv[kV], st4 = 0, nx4 = 0;
+    bool lft[kV];
+    int32_t lid[kV];
 #pragma unroll
     for (int j = 0; j < kV; ++j) {
       const int32_t deg = cur.cl[j] >= 0 ? __ldg(&a.cls_deg[cur.cl[j]]) : 0;
@@ -285,8 +369,10 @@ __global__ void __launch_bounds__(256) k_prio_settle(PrioSettleArgs a) {
         if (a.mis_o) a.mis_o[cur.vid[j]] = TCMIS_IN_MIS;
       }
       if (r == 2) ++sel;
-      left.put(r == 0, (int32_t)(v0 + j));
+      lft[j] = r == 0;
+      lid[j] = (int32_t)(v0 + j);
     }
+    left.put_n<kV>(lft, lid);
     if (v0 + kV <= a.n) {
       *reinterpret_cast<uint4 *>(a.p + v0) = make_uint4(pv[0], pv[1], pv[2], pv[3]);
       *reinterpret_cast<uint2 *>(a.q + v0) =
@@ -302,9 +388,8 @@ __global__ void __launch_bounds__(256) k_prio_settle(PrioSettleArgs a) {
         a.next[v0 + j] = (uint8_t)(nx4 >> (8 * j));
       }
     }
-    // block-uniform: the block's last iteration, or every kPsFlush
-    if (it % kPsFlush == 0 || t - threadIdx.x + stride >= quads) left.flush(a.left, &a.ctrl->r1_sel_left);
-    cur = nx;
+    // block-uniform: the block's last chunk, or every kPsFlush
+    if ((it + 1) % kPsFlush == 0 || c + G >= nchunks) left.flush(a.left, &a.ctrl->r1_sel_left);
   }
   block_add3(sel, 0, 0, a.ctrl);
 }
@@ -866,7 +951,7 @@ int launch_prio_settle(tcmis_graph *g, const RoundArgs &a, uint64_t seed, int sc
   p.ctrl = ws.ctrl;
   p.rounds = ws.rounds;
   p.nrounds = ws.round_cap;
-  const int grid = grid_for(ctx, ((int64_t)g->n + 3) / 4, 256, 8);
+  const int grid = grid_for(ctx, ((int64_t)g->n + 3) / 4, 256, 4);
   TCMIS_TIMED(ctx, "k_prio_settle", (k_prio_settle<<<grid, 256, 0, st>>>(p)));
   TCMIS_LAUNCHED(ctx);
   return 0;
