@@ -169,6 +169,40 @@ __device__ __forceinline__ void publish(const Publish &p, int32_t v) {
   }
 }
 
+// publish() for a whole warp (every lane calls it; `have` marks the lanes
+// with a decision): bitmap slices take one atomicOr per distinct word (lanes
+// grouped by __match_any_sync, their bits OR-reduced with redux.sync), id
+// lists one atomicAdd per warp.  The per-decision atomics of publish()
+// doubled the cost of round 1's kernels in the partitioned solve (bitmap
+// words collecting up to 32 atomics each).
+__device__ __forceinline__ void publish_warp(const Publish &p, int32_t v, bool have) {
+  if (p.bits) {
+    uint32_t w = 0xffffffffu, bit = 0;
+    if (have) {
+      const uint32_t off = (uint32_t)(v - p.lo);
+      w = off >> 5;
+      bit = 1u << (off & 31u);
+    }
+    if (!__any_sync(0xffffffffu, have)) return;
+    const unsigned peers = __match_any_sync(0xffffffffu, w);
+    if (have) {
+      const uint32_t m = __reduce_or_sync(peers, bit);
+      if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicOr(&p.bits[w], m);
+    }
+  } else if (p.list) {
+    const unsigned act = __ballot_sync(0xffffffffu, have);
+    if (!act) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(p.list, __popc(act));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (have) {
+      const int i = base + __popc(act & ((1u << lane) - 1u));
+      if (i < p.cap) p.list[1 + i] = v;
+    }
+  }
+}
+
 // The gathered summary of the key order: q[v] = clamp(p[v] >> shift, 1,
 // 0xffff) is monotone in p, so q[u] != q[v] decides key(u) > key(v) with a
 // 2-byte gather from a vector half the size of p (RGG 24M: 48 MB against

@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
   const int64_t stride = (int64_t)gridDim.x * kBlock;
   for (int64_t wb = (int64_t)blockIdx.x * kBlock + (threadIdx.x & ~31); wb < cnt; wb += stride) {
     const int64_t i = wb + lane;
-    bool undecided = false;
+    bool undecided = false, pub = false;
     int32_t v = 0;
     if (i < cnt) {
       v = (round == 1 && a.nz_identity && !r1s) ? (int32_t)i : __ldg(&wl[i]);
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
           // a non-candidate: the pull exclusion finds it on the worklist
         } else if (e - s <= kProbeK || (below && !a.push)) {  // push: the whole row in k_select
           mark_candidate(v, a.next, a.state, a.segflag, a.T, a.perm, a.mis_o);
-          publish(a.pub, v);
+          pub = true;
           ++sel;
           if (a.push) {
 #pragma unroll
@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
         }
       }
     }
+    publish_warp(a.pub, v, pub);
     warp_emit(und, undecided, v, a.undecided, &ctrl->sel_undec);
   }
   warp_flush(und, a.undecided, &ctrl->sel_undec);
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
   };
   fetch();
   while (__any_sync(0xffffffffu, mode != kDone)) {
-    bool defer = false;
+    bool defer = false, pub = false;
     if (mode == kScan) {
       // kWin 16-byte windows per step: 4 kWin entries and their q gathers in flight
       constexpr int kU = 4 * kWin;
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
         mode = kFetch;
       } else if (hi <= s || below) {
         mark_candidate(v, a.next, a.state, a.segflag, a.T, a.perm, a.mis_o);
-        publish(a.pub, v);
+        pub = true;
         ++sel;
         mode = a.push ? kPush : kFetch;
         hi = s;  // push cursor runs upward from s
@@ -244,6 +245,7 @@ __global__ void __launch_bounds__(kBlock, TCMIS_SEL_MINB) k_select(SelectArgs a)
       hi = p;
       if (hi >= e) mode = kFetch;
     }
+    publish_warp(a.pub, v, pub);
     const bool vl = defer && e - s > kBlockRow;
     warp_append(defer && !vl, v, a.long_list, &ctrl->long_count);
     warp_append(vl, v, a.vlong, &ctrl->sel_vlong);

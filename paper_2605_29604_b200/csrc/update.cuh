@@ -229,10 +229,10 @@ __global__ void __launch_bounds__(kBlock)
 #pragma unroll
     for (int j = 0; j < kUpdItems; ++j) {
       const int32_t v = vs[j];
+      publish_warp(a.pub, v, v >= 0 && ds[j] == 2);
       if (v < 0 || ds[j] == 1) continue;  // candidates were settled by k_select
       if (ds[j] == 2) {
         mark_removed(v, a.state, a.q);
-        publish(a.pub, v);
         ++rem;
       } else {
         ++mine;
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
   const int64_t stride = (int64_t)gridDim.x * kBlock;
   for (int64_t wb = (int64_t)blockIdx.x * kBlock + (threadIdx.x & ~31); wb < cnt; wb += stride) {
     const int64_t i = wb + lane;
-    bool survive = false, undecided = false;
+    bool survive = false, undecided = false, pub = false;
     int32_t v = 0;
     if (i < cnt) {
       v = (round == 1 && a.nz_identity && !r1s) ? (int32_t)i : __ldg(&wl[i]);
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
       const bool hit = hits_row<kPullK>(next, u, class_bounds(a.cb, e - s), below);
       if (hit) {
         mark_removed(v, a.state, a.q);
-        publish(a.pub, v);
+        pub = true;
         ++rem;
       } else if (e - s <= kPullK || below) {
         survive = true;
@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
         undecided = true;
       }
     }
+    publish_warp(a.pub, v, pub);
     warp_emit(srv, survive, v, out, tail);
     warp_emit(und, undecided, v, a.undecided, &ctrl->pull_undec);
   }
@@ -358,9 +359,9 @@ __global__ void __launch_bounds__(kBlock) k_r1_pull(UpdateArgs a) {
       const int32_t v = (int32_t)(v0 + j);
       if (hit[j]) {
         mark_removed(v, a.state, a.q);
-        publish(a.pub, v);
         ++rem;
       }
+      publish_warp(a.pub, v, hit[j]);
       left.put(alive[j] && !hit[j], v);
     }
     left.flush(a.wl1, &ctrl->r1_pull_left);
@@ -405,7 +406,7 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
   };
   fetch();
   while (__any_sync(0xffffffffu, mode != kDone)) {
-    bool survive = false, defer = false;
+    bool survive = false, defer = false, pub = false;
     if (mode == kScan) {
       constexpr int kU = 4 * kSelWin;
       int32_t u[kU];
@@ -424,7 +425,7 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
       hi = w;
       if (hit) {
         mark_removed(v, a.state, a.q);
-        publish(a.pub, v);
+        pub = true;
         ++rem;
         mode = kFetch;
       } else if (hi <= s || below) {
@@ -436,6 +437,7 @@ __global__ void __launch_bounds__(kBlock) k_update_pull(UpdateArgs a) {
         mode = kFetch;
       }
     }
+    publish_warp(a.pub, v, pub);
     warp_emit(wo, survive, v, out, tail);
     if (__any_sync(0xffffffffu, defer)) {  // entries [s, hi) are left
       const int nch = defer ? (int)((hi - s + kPullChunk - 1) / kPullChunk) : 0;
