@@ -1464,7 +1464,8 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
                      "TCMIS_F_TILE_CAND needs fixed priorities (not luby-fresh)");
   const bool tile_form = cfg->exclusion == TCMIS_EXCL_TILE_BITS ||
                          cfg->exclusion == TCMIS_EXCL_TILE_MMA;
-  const bool relabel = g->d_perm && !cfg->observer && !tile_form;
+  // (nor for the tile-form Phase 1, whose A-up store is too)
+  const bool relabel = g->d_perm && !cfg->observer && !tile_form && !tile_cand;
   const int64_t *s_off = relabel ? g->d_roff : g->d_off;
   const int32_t *s_nbr = relabel ? g->d_rnbr : g->d_nbr;
   const int32_t *s_perm = relabel ? g->d_perm : nullptr;

@@ -95,6 +95,16 @@ def test_observer_and_tile_forms_ignore_the_order(ctx):
     for excl in (tc.Exclusion.TILE_BITS, tc.Exclusion.TILE_MMA):
         got = tc.run_mis(dg, tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=1, exclusion=excl))
         assert rounds_tuple(got.iterations) == oracle_tuple(exp)
+    # the tile-form Phase 1 (its A-up store is on the caller's CSR) also runs
+    # in the caller's order, with or without the degree order's settle data
+    for flags in (tc.F_TILE_CAND, tc.F_TILE_CAND | tc.F_TILE_UMMA):
+        cfg = tc.EngineConfig(heuristic=tc.Heuristic.H2, seed=1, flags=flags)
+        dg.tile_cand_prepare(cfg)
+        for host_loop in (False, True):
+            cfg.host_loop = host_loop
+            got = tc.run_mis(dg, cfg)
+            assert np.array_equal(got.mis, exp.mis), (flags, host_loop)
+            assert rounds_tuple(got.iterations) == oracle_tuple(exp), (flags, host_loop)
     dg.close()
 
 
