@@ -1085,6 +1085,9 @@ TailArgs tail_args(tcmis_graph *g, const RoundArgs &a) {
   t.nz = a.nz;
   t.nz_count = a.nz_count;
   t.nz_identity = a.nz_count == a.n || a.nz_prefix ? 1 : 0;
+  t.cb = a.cb;
+  t.q_l1 = std::getenv("TCMIS_TAIL_Q_L2") ? 0 : 1;
+  t.bar_fenced = std::getenv("TCMIS_TAIL_BAR_FENCE") ? 1 : 0;
 
   return t;
 }

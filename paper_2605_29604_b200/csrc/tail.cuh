@@ -110,6 +110,9 @@ constexpr int kCompactV = 512;                  // vertices per warp step of the
 constexpr int kTailMaxWarps = 32 * 2048;        // capacity of one per-warp count buffer
 // dynamic shared memory of k_tail: the write pass's per-warp staging
 constexpr size_t kTailDynSmem = sizeof(int32_t) * kTailWarps * kCompactV;
+static_assert(sizeof(int32_t) * kTailBlock * kThrScan + sizeof(long long) * (kTailBlock + 1) +
+                      sizeof(int16_t) * kTailBlock <= kTailDynSmem,
+              "the windows, the push offsets and the push list share the staging area");
 
 struct TailArgs {
   const int64_t *off;
@@ -149,33 +152,72 @@ struct TailArgs {
   const int32_t *nz;
   int32_t nz_count;
   int nz_identity;
+  // degree-class bounds of a degree-ordered H2 solve (common.cuh
+  // class_bounds), or null: a row entry below its row's lo has a lower key,
+  // and so has every entry before it (sorted rows), so a scan from the row's
+  // end stops there
+  const int2 *cb;
+  int q_l1;        // 0: every q gather from L2 (TCMIS_TAIL_Q_L2, an A/B knob), 1: see tail_q
+  int bar_fenced;  // 1: the __threadfence grid barrier (TCMIS_TAIL_BAR_FENCE, an A/B knob)
 };
+
+__device__ __forceinline__ unsigned long long atom_add_acq_rel_gpu(unsigned long long *p,
+                                                                  unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // Grid barrier whose arrival also sums one value per block: bar[0..1] is a
 // u64 word (arrivals << 40 | sum), bar[2] the generation word (gen << 1 |
 // "the sum was 0").  The last block to arrive resets the word and publishes
 // the next generation with the flag, so the waiting blocks learn the sum's
 // verdict from the very load that releases them.  Returns the flag.
-__device__ __forceinline__ bool grid_barrier_sum(unsigned *bar, unsigned x) {
+// Ordering: the block's writes precede thread 0's arrival by the block
+// barrier; the arrival is an acq_rel atomic and the release of the next
+// generation a st.release, which the waiters' ld.acquire observes -- no
+// separate fence.sc (`fenced`: the __threadfence form, an A/B knob).
+__device__ __forceinline__ bool grid_barrier_sum(unsigned *bar, unsigned x, bool fenced = false) {
   __shared__ unsigned s_flag;
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned long long *word = reinterpret_cast<unsigned long long *>(bar);
-    volatile unsigned *gen = bar + 2;
-    const unsigned g = *gen;
-    __threadfence();
-    const unsigned long long old = atomicAdd(word, (1ull << 40) | (unsigned long long)x);
     unsigned res;
-    if ((unsigned)(old >> 40) == gridDim.x - 1) {
-      const unsigned long long sum = (old & ((1ull << 40) - 1)) + x;
-      *word = 0;
+    if (fenced) {
+      volatile unsigned *gen = bar + 2;
+      const unsigned g = *gen;
       __threadfence();
-      res = (((g >> 1) + 1u) << 1) | (sum == 0 ? 1u : 0u);
-      atomicExch(bar + 2, res);
+      const unsigned long long old = atomicAdd(word, (1ull << 40) | (unsigned long long)x);
+      if ((unsigned)(old >> 40) == gridDim.x - 1) {
+        const unsigned long long sum = (old & ((1ull << 40) - 1)) + x;
+        *word = 0;
+        __threadfence();
+        res = (((g >> 1) + 1u) << 1) | (sum == 0 ? 1u : 0u);
+        atomicExch(bar + 2, res);
+      } else {
+        while (((res = *gen) >> 1) == (g >> 1)) __nanosleep(32);
+      }
+      __threadfence();
     } else {
-      while (((res = *gen) >> 1) == (g >> 1)) __nanosleep(32);
+      const unsigned g = ld_acquire_gpu(bar + 2);
+      const unsigned long long old = atom_add_acq_rel_gpu(word, (1ull << 40) | (unsigned long long)x);
+      if ((unsigned)(old >> 40) == gridDim.x - 1) {
+        const unsigned long long sum = (old & ((1ull << 40) - 1)) + x;
+        *(volatile unsigned long long *)word = 0;
+        res = (((g >> 1) + 1u) << 1) | (sum == 0 ? 1u : 0u);
+        st_release_gpu(bar + 2, res);
+      } else {
+        while (((res = ld_acquire_gpu(bar + 2)) >> 1) == (g >> 1)) __nanosleep(32);
+      }
     }
-    __threadfence();
     s_flag = res & 1u;
   }
   __syncthreads();
@@ -225,12 +267,25 @@ __device__ __forceinline__ void tail_candidate(const TailArgs &a, int32_t v, int
   }
 }
 
+// q[u] during the tail.  The tail never redraws priorities (no luby-fresh
+// here), so q only falls, once, from its key summary to 0 (mark_removed): a 0
+// read through the SM's L1 (ld.global.nc) is final, and only a non-zero one
+// is re-read from L2.  Most neighbours the late rounds gather left in round
+// 1 -- at R-MAT s22 the pushes of round 2's 45k candidates hit the same few
+// hub lines from every SM --, so those gathers stay on-chip instead of
+// queueing at the one L2 slice that holds each hot line.
+// (`probe` is off in solves that start in this kernel, see k_tail.)
+__device__ __forceinline__ uint32_t tail_q(const TailArgs &a, int32_t u, bool probe) {
+  if (probe && __ldg(&a.q[u]) == 0) return 0u;
+  return __ldcg(&a.q[u]);
+}
+
 // u blocks v in round r: alive at the start of round r (q != 0, not tagged
-// for round r-1), higher key; `alive` reports the first part.  q[u] and the
-// tag are independent loads: one round trip for both.
+// for round r-1), higher key; `alive` reports the first part.
 __device__ __forceinline__ bool tail_blocks(const TailArgs &a, int32_t u, uint32_t tprev,
-                                            bool first, uint32_t qv, int32_t v, bool &alive) {
-  const uint32_t qu = __ldcg(&a.q[u]);
+                                            bool first, bool probe, uint32_t qv, int32_t v,
+                                            bool &alive) {
+  const uint32_t qu = tail_q(a, u, probe);
   alive = false;
   if (qu == 0) return false;
   alive = first || __ldcg(&a.xt[u]) != (uint16_t)tprev;  // no tag is tag(r0 - 1)
@@ -241,8 +296,8 @@ __device__ __forceinline__ bool tail_blocks(const TailArgs &a, int32_t u, uint32
 }
 
 __device__ __forceinline__ bool tail_alive(const TailArgs &a, int32_t u, uint32_t tprev,
-                                           bool first) {
-  return __ldcg(&a.q[u]) != 0 && (first || __ldcg(&a.xt[u]) != (uint16_t)tprev);
+                                           bool first, bool probe) {
+  return tail_q(a, u, probe) != 0 && (first || __ldcg(&a.xt[u]) != (uint16_t)tprev);
 }
 
 __device__ __forceinline__ unsigned long long *slot_field(const TailArgs &a, int round, int f) {
@@ -365,7 +420,14 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
   __shared__ uint32_t s_live[kTailBlock];
   __shared__ int16_t s_def[kTailBlock];   // entries left to the groups
   __shared__ int16_t s_long[kTailLongCap];  // ... and to the whole block
-  __shared__ int s_nd, s_nlong, s_nl;
+  __shared__ int32_t s_lo[kTailBlock];      // the entry's class lower bound (0: none)
+  // candidates whose row below the examined part is still to be pushed: the
+  // entries [s_s, s_e) of every listed entry, flattened over the whole block
+  // (list and offsets in the staging area's upper half, which s_live's
+  // windows leave free during the rounds)
+  long long *s_pofs = reinterpret_cast<long long *>(s_stage + kTailBlock * kThrScan);
+  int16_t *s_pk = reinterpret_cast<int16_t *>(s_pofs + kTailBlock + 1);
+  __shared__ int s_nd, s_nlong, s_nl, s_np;
   __shared__ int32_t s_pend[2][kTailBlock];  // candidates' block columns (seg_mode 1), by round parity
   __shared__ int s_npend[2];
   __shared__ unsigned long long s_acc[4];
@@ -380,6 +442,7 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
     s_nd = 0;
     s_nlong = 0;
     s_nl = 0;
+    s_np = 0;
     s_npend[0] = s_npend[1] = 0;
   }
   const uint32_t base0 = __ldcg(&a.tslot[0]);
@@ -434,9 +497,11 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
       const int32_t v = !from1 ? __ldcg(&in0[idx]) : a.nz_identity ? (int32_t)idx : __ldg(&a.nz[idx]);
       s_v[threadIdx.x] = v;
       s_o[threadIdx.x] = a.perm ? __ldg(&a.perm[v]) : v;
-      s_s[threadIdx.x] = __ldg(&a.off[v]);
-      s_e[threadIdx.x] = __ldg(&a.off[v + 1]);
+      const int64_t rs = __ldg(&a.off[v]), re = __ldg(&a.off[v + 1]);
+      s_s[threadIdx.x] = rs;
+      s_e[threadIdx.x] = re;
       s_q[threadIdx.x] = __ldcg(&a.q[v]);
+      s_lo[threadIdx.x] = class_bounds(a.cb, re - rs).x;
     }
   }
   // the fused compaction runs in the caller's id order: on the states, or on
@@ -465,12 +530,12 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
     __syncthreads();
     if (threadIdx.x < nl) a.xt[s_v[threadIdx.x]] = 0;
     base = 0;
-    grid_barrier_sum(a.bar, 1);
+    grid_barrier_sum(a.bar, 1, a.bar_fenced);
   }
   TAIL_MARK(8, 0);
   int round = r0;
   bool done = cnt0 == 0;
-  if (done) grid_barrier_sum(a.bar, 0);  // the count pass must be complete before the compaction
+  if (done) grid_barrier_sum(a.bar, 0, a.bar_fenced);  // the count pass must be complete before the compaction
   __syncthreads();                       // the list's shared-memory fill
   for (; !done; ++round) {
     if (round - r0 >= kMaxTailRounds) {  // uniform: the ring overflows, the host re-runs step-wise
@@ -478,6 +543,11 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
       break;
     }
     const bool first = round == r0;
+    // tail_q's L1 probe: on when the tail takes over from the round kernels
+    // (most neighbours are gone by then); a solve run here from round 1 (small
+    // graphs: ER 100k keeps a quarter of its vertices alive into round 2) would
+    // only pay the probe's extra round trip (ER k_tail 87 -> 94 us with it)
+    const bool probe = a.q_l1 && !from1;
 #ifdef TCMIS_TAIL_PROF
     if (first && threadIdx.x == 0) g_tail_blk[4][blockIdx.x] = gtimer();
 #endif
@@ -504,7 +574,7 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
     // a handful of entries: one warp per entry, not the thread + group pair
     // (two dependent scans where one suffices for a round of few vertices)
     const bool small = nl <= kTailWarps;
-    int32_t v = -1, o = -1;
+    int32_t v = -1, o = -1, lo = 0;
     int64_t s = 0, e = 0;
     uint32_t qv = 0;
     uint8_t keep = 0;
@@ -514,6 +584,7 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
       s = s_s[k];
       e = s_e[k];
       qv = s_q[k];
+      lo = s_lo[k];
     }
     if (small && w < nl) {
       if (lane == 0) {
@@ -547,19 +618,22 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
           constexpr int64_t kWW = 32 * kTU;
           bool blocked = false;
           uint32_t live = 0;
+          const int32_t wlo = s_lo[w];
           for (int64_t top = we;;) {
-            bool b = false;
+            bool b = false, bl = false;
             live = 0;
 #pragma unroll
             for (int j = 0; j < kTU; ++j)
               if (u[j] >= 0) {
                 bool al;
-                b |= tail_blocks(a, u[j], tprev, first, wq, wv, al);
+                b |= tail_blocks(a, u[j], tprev, first, probe, wq, wv, al);
                 live |= (uint32_t)al << j;
+                bl |= u[j] < wlo;
               }
             blocked = __any_sync(0xffffffffu, b);
             top -= kWW;
-            if (blocked || top <= ws) break;
+            // below the class bound: nothing further down can block
+            if (blocked || top <= ws || __any_sync(0xffffffffu, bl)) break;
 #pragma unroll
             for (int j = 0; j < kTU; ++j) {
               const int64_t idx = top - 1 - lane - 32 * j;
@@ -581,7 +655,7 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
                 }
 #pragma unroll
                 for (int j = 0; j < kTU; ++j)
-                  if (u[j] >= 0 && tail_alive(a, u[j], tprev, first)) a.xt[u[j]] = (uint16_t)tcur;
+                  if (u[j] >= 0 && tail_alive(a, u[j], tprev, first, probe)) a.xt[u[j]] = (uint16_t)tcur;
               }
             }
           } else if (lane == 0) {
@@ -610,22 +684,27 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
         ++rem;
       } else {
         ++alive;
-        bool b = false;
+        bool b = false, below = false;
         uint32_t live = 0;
 #pragma unroll
         for (int j = 0; j < kThrScan; ++j)
           if (u[j] >= 0) {
             bool al;
-            b |= tail_blocks(a, u[j], tprev, first, qv, v, al);
+            b |= tail_blocks(a, u[j], tprev, first, probe, qv, v, al);
             live |= (uint32_t)al << j;
+            below |= u[j] < lo;
           }
         if (b) {
           keep = 1;
-        } else if (hi <= s) {  // the whole row was in the windows
+        } else if (hi <= s || below) {  // the whole row, or all of it that could block
           tail_candidate(a, v, o, wcnt, wlen, sel, pend, npend);
 #pragma unroll
           for (int j = 0; j < kThrScan; ++j)
             if ((live >> j) & 1u) a.xt[u[j]] = (uint16_t)tcur;
+          if (hi > s) {  // the rest of the row: the block's flat push below
+            s_pk[atomicAdd(&s_np, 1)] = (int16_t)k;
+            s_e[k] = hi;
+          }
         } else {
           s_def[atomicAdd(&s_nd, 1)] = (int16_t)k;
           s_e[k] = hi;  // the group scans [s, hi): [hi, e) was examined here
@@ -666,46 +745,40 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
         if (__shfl_sync(gmask, listed, lane & ~(kGroup - 1))) continue;
       }
       const uint32_t dq = s_q[kd];
-      bool blocked = false;
+      const int32_t dlo = s_lo[kd];
+      bool blocked = false, stop = false;
       int32_t u[kTU];
       uint32_t live = 0;
-      for (int64_t top = de; top > ds && !blocked; top -= kW) {
+      for (int64_t top = de; top > ds && !blocked && !stop; top -= kW) {
 #pragma unroll
         for (int j = 0; j < kTU; ++j) {
           const int64_t idx = top - 1 - gl - kGroup * j;
           u[j] = idx >= ds ? __ldg(&a.nbr[idx]) : -1;
         }
-        bool b = false;
+        bool b = false, bl = false;
         live = 0;
 #pragma unroll
         for (int j = 0; j < kTU; ++j)
           if (u[j] >= 0) {
             bool al;
-            b |= tail_blocks(a, u[j], tprev, first, dq, dv, al);
+            b |= tail_blocks(a, u[j], tprev, first, probe, dq, dv, al);
             live |= (uint32_t)al << j;
+            bl |= u[j] < dlo;
           }
         blocked = __ballot_sync(gmask, b) != 0;
+        stop = __ballot_sync(gmask, bl) != 0;  // below the class bound
       }
       if (!blocked) {
         if (gl == 0) tail_candidate(a, dv, s_o[kd], wcnt, wlen, sel, pend, npend);
         const uint32_t sl = s_live[kd];
         for (int j = gl; j < kThrScan; j += kGroup)
           if ((sl >> j) & 1u) a.xt[s_stage[kd * kThrScan + j]] = (uint16_t)tcur;
-        if (de - ds <= kW) {
+        if (de - ds <= kW) {  // one step held the whole part
 #pragma unroll
           for (int j = 0; j < kTU; ++j)
             if ((live >> j) & 1u) a.xt[u[j]] = (uint16_t)tcur;
-        } else {
-          for (int64_t top = de; top > ds; top -= kW) {
-#pragma unroll
-            for (int j = 0; j < kTU; ++j) {
-              const int64_t idx = top - 1 - gl - kGroup * j;
-              u[j] = idx >= ds ? __ldg(&a.nbr[idx]) : -1;
-            }
-#pragma unroll
-            for (int j = 0; j < kTU; ++j)
-              if (u[j] >= 0 && tail_alive(a, u[j], tprev, first)) a.xt[u[j]] = (uint16_t)tcur;
-          }
+        } else if (gl == 0) {  // [ds, de): the block's flat push below
+          s_pk[atomicAdd(&s_np, 1)] = (int16_t)kd;
         }
       } else if (gl == 0) {
         s_keep[kd] = 1;
@@ -721,27 +794,30 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
       const int32_t dv = s_v[kd];
       const int64_t ds = s_s[kd], de = s_e[kd];
       const uint32_t dq = s_q[kd];
+      const int32_t dlo = s_lo[kd];
       constexpr int kBU = 8;
       constexpr int64_t kBW = (int64_t)kBU * kTailBlock;
-      bool blocked = false;
+      bool blocked = false, stop = false;
       int32_t x[kBU];
       uint32_t live = 0;
-      for (int64_t top = de; top > ds && !blocked; top -= kBW) {
+      for (int64_t top = de; top > ds && !blocked && !stop; top -= kBW) {
 #pragma unroll
         for (int j = 0; j < kBU; ++j) {
           const int64_t idx = top - 1 - threadIdx.x - (int64_t)kTailBlock * j;
           x[j] = idx >= ds ? __ldg(&a.nbr[idx]) : -1;
         }
-        bool b = false;
+        bool b = false, bl = false;
         live = 0;
 #pragma unroll
         for (int j = 0; j < kBU; ++j)
           if (x[j] >= 0) {
             bool al;
-            b |= tail_blocks(a, x[j], tprev, first, dq, dv, al);
+            b |= tail_blocks(a, x[j], tprev, first, probe, dq, dv, al);
             live |= (uint32_t)al << j;
+            bl |= x[j] < dlo;
           }
         blocked = __syncthreads_or(b) != 0;
+        stop = __syncthreads_or(bl) != 0;  // below the class bound
       }
       if (!blocked) {
         if (threadIdx.x == 0) tail_candidate(a, dv, s_o[kd], wcnt, wlen, sel, pend, npend);
@@ -751,23 +827,53 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
 #pragma unroll
           for (int j = 0; j < kBU; ++j)
             if ((live >> j) & 1u) a.xt[x[j]] = (uint16_t)tcur;
-        } else {
-          for (int64_t top = de; top > ds; top -= kBW) {
-#pragma unroll
-            for (int j = 0; j < kBU; ++j) {
-              const int64_t idx = top - 1 - threadIdx.x - (int64_t)kTailBlock * j;
-              x[j] = idx >= ds ? __ldg(&a.nbr[idx]) : -1;
-            }
-#pragma unroll
-            for (int j = 0; j < kBU; ++j)
-              if (x[j] >= 0 && tail_alive(a, x[j], tprev, first)) a.xt[x[j]] = (uint16_t)tcur;
-          }
+        } else if (threadIdx.x == 0) {  // [ds, de): the flat push below
+          s_pk[atomicAdd(&s_np, 1)] = (int16_t)kd;
         }
       } else if (threadIdx.x == 0) {
         s_keep[kd] = 1;
       }
     }
-    TAIL_MARK(11, 0);
+    __syncthreads();  // the push list is complete
+    TAIL_MARK(11, s_np);
+    // 4. the candidates' rows beyond their examined part, flattened over the
+    // block: each thread takes every kTailBlock-th entry of the concatenation
+    // (neighbouring threads read neighbouring row entries), kPU of them per
+    // step with their loads in flight together; alive neighbours get tag(round)
+    long long ptotal = 0;
+    if (const int np = s_np) {
+      using Scan = cub::BlockScan<long long, kTailBlock, cub::BLOCK_SCAN_WARP_SCANS>;
+      __shared__ typename Scan::TempStorage s_scan;
+      const long long len = threadIdx.x < np ? s_e[s_pk[threadIdx.x]] - s_s[s_pk[threadIdx.x]] : 0;
+      long long incl;
+      Scan(s_scan).InclusiveSum(len, incl);
+      s_pofs[threadIdx.x + 1] = incl;
+      if (threadIdx.x == 0) s_pofs[0] = 0;
+      __syncthreads();
+      const long long total = s_pofs[np];
+      ptotal = total;
+      constexpr int kPU = 8;
+      for (long long j0 = threadIdx.x; j0 < total; j0 += (long long)kPU * kTailBlock) {
+        int32_t x[kPU];
+#pragma unroll
+        for (int p = 0; p < kPU; ++p) {
+          const long long j = j0 + (long long)p * kTailBlock;
+          x[p] = -1;
+          if (j < total) {
+            int lo = 0, hi = np - 1;  // the last listed row whose offset <= j
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (s_pofs[mid] <= j) lo = mid; else hi = mid - 1;
+            }
+            x[p] = __ldg(&a.nbr[s_s[s_pk[lo]] + (j - s_pofs[lo])]);
+          }
+        }
+#pragma unroll
+        for (int p = 0; p < kPU; ++p)
+          if (x[p] >= 0 && tail_alive(a, x[p], tprev, first, probe)) a.xt[x[p]] = (uint16_t)tcur;
+      }
+    }
+    TAIL_MARK(12, ptotal);
 #ifdef TCMIS_TAIL_PROF
     if (first && threadIdx.x == 0) g_tail_blk[1][blockIdx.x] = gtimer();
 #endif
@@ -795,6 +901,7 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
       s_acc[0] = s_acc[1] = s_acc[2] = s_acc[3] = 0;
       s_nd = 0;
       s_nlong = 0;
+      s_np = 0;
       s_npend[(round + 1) & 1] = 0;  // the next round's list (round - 1's was read above)
     }
     // 5. the block's survivors (round's non-candidates) stay with it
@@ -805,11 +912,12 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
       s_s[j] = s;
       s_e[j] = e;
       s_q[j] = (uint16_t)qv;
+      s_lo[j] = lo;
     }
     __syncthreads();
     nl = s_nl;
     TAIL_MARK(2, nl);
-    done = grid_barrier_sum(a.bar, (unsigned)nl);
+    done = grid_barrier_sum(a.bar, (unsigned)nl, a.bar_fenced);
     if (threadIdx.x == 0) s_nl = 0;
     TAIL_MARK(3, round);
     if (blockIdx.x == 0 && threadIdx.x == 0) {

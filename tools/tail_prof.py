@@ -5,7 +5,7 @@ import bench
 L = tc.load()
 ctx = tc.Context(0)
 TAG = {1: "start", 2: "pass", 3: "barrier", 4: "compact0", 5: "count", 6: "countbar", 7: "compact1",
-       8: "fill", 9: "thr", 10: "grp", 11: "blk"}
+       8: "fill", 9: "thr", 10: "grp", 11: "blk", 12: "push"}
 buf = (C.c_ulonglong * 256)()
 for cfg in sys.argv[1:]:
     dg = bench.make_device_graph(tc, cfg, ctx)
