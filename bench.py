@@ -190,11 +190,14 @@ def run_ours(args) -> dict:
     log(f"[bench] {args.config}: n={n} m={m} tiles={tiles} (setup {time.time() - t0:.1f}s)")
     order_ms = None
     if args.order == "auto":
-        # measured per config (tools/gpu_order.sh, tools/gpu_cb.sh, DESIGN.md
-        # section 8): the spatial order takes RGG 24M 1.10 -> 0.95 ms; the
-        # degree order with sorted rows and the degree-class bounds takes R-MAT
-        # s22 0.357 -> 0.256 ms and s26 3.82 -> 1.77 ms; ER / grid gain nothing
-        args.order = {"rgg": "spatial", "rmat22": "degree",
+        # measured per config (tools/gpu_order.sh, tools/gpu_cb.sh,
+        # tools/gpu_order2.sh): the spatial order takes
+        # RGG 24M 1.10 -> 0.95 ms, and since k_tail uses the degree-class bounds
+        # the degree order (ties in the points' spatial order) beats it, 0.991
+        # -> 0.953 ms; the degree order with sorted rows and the degree-class
+        # bounds takes R-MAT s22 0.357 -> 0.256 ms and s26 3.82 -> 1.77 ms;
+        # ER / grid gain nothing (ER 0.135 -> 0.155 ms, grid 0.686 -> 0.789)
+        args.order = {"rgg": "degree", "rmat22": "degree",
                       "rmat26": "degree"}.get(args.config, "none")
     if args.order != "none":
         # an internal vertex order for the solve kernels (tcmis_graph_reorder):
