@@ -36,6 +36,9 @@ namespace tcmis_b200 {
 #ifndef TCMIS_SEL_MINB
 #define TCMIS_SEL_MINB 8
 #endif
+#ifndef TCMIS_PROBE_MINB
+#define TCMIS_PROBE_MINB 8  // resident blocks of the probes (k_probe_select, k_probe_pull)
+#endif
 
 
 struct SelectArgs {
@@ -107,7 +110,7 @@ constexpr int kProbeK = 4;  // row entries the straight-line probe examines
 // entries with two aligned 16-byte loads, keys of the last kProbeK gathered.
 // This settles 84 % of R-MAT s22's round-1 vertices and every vertex of
 // rows <= kProbeK (the whole grid, most of the RGG).
-__global__ void __launch_bounds__(kBlock, 8) k_probe_select(SelectArgs a) {
+__global__ void __launch_bounds__(kBlock, TCMIS_PROBE_MINB) k_probe_select(SelectArgs a) {
   pdl_entry();
   if (a.tile_gate && a.ctrl->alive >= a.tile_gate) return;  // a tile round (tile_cand.cu)
   __shared__ int32_t s_und[kBlock / 32][64];

@@ -262,7 +262,7 @@ constexpr int kPullK = 4;  // row entries the straight-line pull probe examines
 // InMIS, so state == Alive marks exactly the alive non-candidates.
 // Straight-line: the last <= 8 row entries with two aligned 16-byte loads,
 // candidate flags of the last kPullK.
-__global__ void __launch_bounds__(kBlock, 8) k_probe_pull(UpdateArgs a) {
+__global__ void __launch_bounds__(kBlock, TCMIS_PROBE_MINB) k_probe_pull(UpdateArgs a) {
   pdl_entry();
   __shared__ int32_t s_srv[kBlock / 32][64];
   __shared__ int32_t s_und[kBlock / 32][64];

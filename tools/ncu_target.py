@@ -8,7 +8,7 @@ import bench
 dg = bench.make_device_graph(tc, cfgname, ctx)
 dg.tile(16)
 # the bench's vertex order for this config (bench.py --order auto)
-order = os.environ.get("ORDER") or {"rgg": "spatial", "rmat22": "degree",
+order = os.environ.get("ORDER") or {"rgg": "degree", "rmat22": "degree",
                                      "rmat26": "degree"}.get(cfgname, "none")
 if order != "none":
     dg.reorder({"degree": tc.DeviceGraph.ORDER_DEGREE, "spatial": tc.DeviceGraph.ORDER_SPATIAL}[order])
