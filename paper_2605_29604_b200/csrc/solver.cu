@@ -1088,6 +1088,7 @@ TailArgs tail_args(tcmis_graph *g, const RoundArgs &a) {
   t.cb = a.cb;
   t.q_l1 = std::getenv("TCMIS_TAIL_Q_L2") ? 0 : 1;
   t.bar_fenced = std::getenv("TCMIS_TAIL_BAR_FENCE") ? 1 : 0;
+  t.tag_par = std::getenv("TCMIS_TAIL_TAG_PAR") ? 1 : 0;
 
   return t;
 }

@@ -158,6 +158,7 @@ struct TailArgs {
   // end stops there
   const int2 *cb;
   int q_l1;        // 0: every q gather from L2 (TCMIS_TAIL_Q_L2, an A/B knob), 1: see tail_q
+  int tag_par;     // A/B knob (TCMIS_TAIL_TAG_PAR): tag loaded with the L2 q (tail_blocks)
   int bar_fenced;  // 1: the __threadfence grid barrier (TCMIS_TAIL_BAR_FENCE, an A/B knob)
 };
 
@@ -285,10 +286,21 @@ __device__ __forceinline__ uint32_t tail_q(const TailArgs &a, int32_t u, bool pr
 __device__ __forceinline__ bool tail_blocks(const TailArgs &a, int32_t u, uint32_t tprev,
                                             bool first, bool probe, uint32_t qv, int32_t v,
                                             bool &alive) {
-  const uint32_t qu = tail_q(a, u, probe);
   alive = false;
-  if (qu == 0) return false;
-  alive = first || __ldcg(&a.xt[u]) != (uint16_t)tprev;  // no tag is tag(r0 - 1)
+  uint32_t qu;
+  if (probe && a.tag_par) {
+    // past the L1 probe the neighbour is likely alive: its L2 q and its tag
+    // in one round trip
+    if (__ldg(&a.q[u]) == 0) return false;
+    qu = __ldcg(&a.q[u]);
+    const uint16_t tu = first ? (uint16_t)0 : __ldcg(&a.xt[u]);
+    if (qu == 0) return false;
+    alive = first || tu != (uint16_t)tprev;
+  } else {
+    qu = tail_q(a, u, probe);
+    if (qu == 0) return false;
+    alive = first || __ldcg(&a.xt[u]) != (uint16_t)tprev;  // no tag is tag(r0 - 1)
+  }
   if (!alive) return false;
   if (qu != qv) return qu > qv;
   const uint32_t pu = __ldg(&a.prio[u]), pv = __ldg(&a.prio[v]);
@@ -297,6 +309,12 @@ __device__ __forceinline__ bool tail_blocks(const TailArgs &a, int32_t u, uint32
 
 __device__ __forceinline__ bool tail_alive(const TailArgs &a, int32_t u, uint32_t tprev,
                                            bool first, bool probe) {
+  if (probe && a.tag_par) {
+    if (__ldg(&a.q[u]) == 0) return false;
+    const uint32_t qu = __ldcg(&a.q[u]);
+    const uint16_t tu = first ? (uint16_t)0 : __ldcg(&a.xt[u]);
+    return qu != 0 && (first || tu != (uint16_t)tprev);
+  }
   return tail_q(a, u, probe) != 0 && (first || __ldcg(&a.xt[u]) != (uint16_t)tprev);
 }
 
