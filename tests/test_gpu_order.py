@@ -245,3 +245,53 @@ def test_round1_settling_switch(ctx, monkeypatch):
             assert np.array_equal(got.mis, exp.mis), (off, excl)
             assert rounds_tuple(got.iterations) == oracle_tuple(exp), (off, excl)
     dg.close()
+
+
+def _star_forest(n_hubs=6, leaves=1500, extra=20000, seed=7):
+    """Hubs of 1500 leaves whose leaves also link at random: after round 1
+    the hubs and many mid-degree rows stay alive, so k_tail scans and pushes
+    rows of every length class (thread window, 16-lane groups, whole-block
+    rows above 512 and above 8192 entries pushed through the flat list)."""
+    rng = np.random.default_rng(seed)
+    n = n_hubs + n_hubs * leaves
+    edges = set()
+    for h in range(n_hubs):
+        for u in range(n_hubs + h * leaves, n_hubs + (h + 1) * leaves):
+            edges.add((h, u))
+        for h2 in range(h + 1, n_hubs):
+            edges.add((h, h2))
+    for _ in range(extra):
+        a, b = rng.integers(n_hubs, n, 2)
+        if a != b:
+            edges.add((int(min(a, b)), int(max(a, b))))
+    return O.graph_from_edges(n, sorted(edges))
+
+
+@pytest.mark.parametrize("kind", ["hubs", "stars", "rmat"])
+@pytest.mark.parametrize("knob", [None, "TCMIS_TAIL_Q_L2", "TCMIS_TAIL_TAG_PAR",
+                                  "TCMIS_TAIL_BAR_FENCE"])
+def test_tail_class_bound_scans(ctx, kind, knob, monkeypatch):
+    """k_tail on a degree-ordered H2 solve: the scans stop at the row's lower
+    class bound, early candidates push the rest of their rows through the
+    block's flat push list, q is probed in L1 first (tail.cuh).  Bit-exact
+    for every tail switch point, seed and scale_bits, with each A/B knob of
+    the tail (L2-only q reads, the tag loaded with q, the fenced barrier)."""
+    if knob:
+        monkeypatch.setenv(knob, "1")
+    g = (_hub_graph() if kind == "hubs" else _star_forest() if kind == "stars"
+         else O.gen("rmat", 13, 16, 4))
+    dg = tc.DeviceGraph.upload(tc.Graph(g.n, g.off, g.nbr), ctx).reorder(tc.DeviceGraph.ORDER_DEGREE)
+    for thr in (None, "1000000000", "64"):
+        if thr is None:
+            monkeypatch.delenv("TCMIS_TAIL_THRESHOLD", raising=False)
+        else:
+            monkeypatch.setenv("TCMIS_TAIL_THRESHOLD", thr)
+        for seed, sb in ((1, 20), (2, 8), (3, 30)):
+            for heur in ("h2", "h3"):
+                exp = O.solve(g, heur, seed, tile_dim=16, scale_bits=sb)
+                got = tc.run_mis(dg, tc.EngineConfig(heuristic=HEUR[heur], seed=seed,
+                                                     scale_bits=sb))
+                where = (kind, knob, thr, seed, sb, heur)
+                assert np.array_equal(got.mis, exp.mis), where
+                assert rounds_tuple(got.iterations) == oracle_tuple(exp), where
+    dg.close()
