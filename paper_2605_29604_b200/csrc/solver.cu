@@ -252,7 +252,10 @@ constexpr int kPsFlush = 4;  // iterations between the residual list's flushes
 // need no registers, so the kernel keeps DRAM busy at its register-limited
 // occupancy (ncu, the register-prefetch version: 19 % of the warps' stalls
 // sat on the first use of a just-loaded class index).
-constexpr int kPsChunk = 1024, kPsStages = 3;
+#ifndef TCMIS_PS_STAGES
+#define TCMIS_PS_STAGES 3
+#endif
+constexpr int kPsChunk = 1024, kPsStages = TCMIS_PS_STAGES;
 struct __align__(16) PsStage {
   int32_t perm[kPsChunk];
   int32_t rmax[kPsChunk];
@@ -338,8 +341,12 @@ __global__ void __launch_bounds__(256) k_prio_settle(PrioSettleArgs a) {
       cur.mx[0] = m4.x; cur.mx[1] = m4.y; cur.mx[2] = m4.z; cur.mx[3] = m4.w;
       cur.cl[0] = c4.x & 0xffff; cur.cl[1] = c4.x >> 16; cur.cl[2] = c4.y & 0xffff; cur.cl[3] = c4.y >> 16;
       __syncthreads();  // stage st is read: refill it kPsStages chunks ahead
-      if (threadIdx.x == 0 && c + kPsStages * G < full)
+      if (threadIdx.x == 0 && c + kPsStages * G < full) {
+        // the block's generic-proxy reads of the stage before the bulk copy's
+        // async-proxy writes into it (cross-proxy WAR)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         ps_issue(a, stg[st], bar[st], c + kPsStages * G);
+      }
     } else {
       cur = ps_load(a, c * 256 + threadIdx.x, quads);  // the partial last chunk
     }
