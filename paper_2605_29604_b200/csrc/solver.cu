@@ -1613,19 +1613,22 @@ int solve_impl(tcmis_graph *g, const tcmis_config *cfg, tcmis_iter_stats *stats,
     // one vertex per thread (tail.cuh): at most kTailBlock per block
     a.tail_thr = (int32_t)std::min<int64_t>(a.tail_thr, (int64_t)a.tail_grid * kTailBlock);
     // a small graph whose non-isolated vertices all fit the tail's lists
-    // runs every round there: no round-kernel launches at all (not with the
-    // degree order's fused round-1 verdicts, which are round-kernel work)
-    // (AUTO exclusion only: an explicit exclusion form or the tile Phase 1
-    // asks for the round kernels; with TCMIS_TAIL_THRESHOLD set, only when
-    // the non-isolated vertices are within it)
+    // runs every round there: no round-kernel launches at all.  On a degree
+    // order the fused round-1 verdicts (k_prio_settle, round-kernel work)
+    // give way to the plain init, and the tail's scans use the class bounds
+    // from round 1 on.  (AUTO exclusion only: an explicit exclusion form or
+    // the tile Phase 1 asks for the round kernels; with TCMIS_TAIL_THRESHOLD
+    // set, only when the non-isolated vertices are within it)
     const int64_t cap = (int64_t)a.tail_grid * kTailBlock;
     const char *whole = std::getenv("TCMIS_TAIL_WHOLE");
     const bool thr_env = std::getenv("TCMIS_TAIL_THRESHOLD") != nullptr;
     if (a.nz_count > 0 && a.nz_count <= cap && (!thr_env || a.nz_count <= a.tail_thr) && a.tail_thr > 0 &&
-        !a.r1_max && !a.tile_cand && cfg->exclusion == TCMIS_EXCL_AUTO &&
-        !(whole && whole[0] == '0')) {
+        !a.tile_cand && cfg->exclusion == TCMIS_EXCL_AUTO && !(whole && whole[0] == '0')) {
       a.tail_thr = (int32_t)cap;
       a.tail_from1 = 1;
+      a.r1_max = nullptr;
+      a.r1_cls = nullptr;
+      a.cbc = nullptr;
     }
   }
   if (step)

@@ -704,14 +704,23 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
         ++alive;
         bool b = false, below = false;
         uint32_t live = 0;
+        if (first && from1 && a.cb) {
+          // a solve's round 1 here: everybody is alive, so an entry at or
+          // above the row's upper class bound blocks without a gather
+          const int32_t hb = class_bounds(a.cb, e - s).y;
 #pragma unroll
-        for (int j = 0; j < kThrScan; ++j)
-          if (u[j] >= 0) {
-            bool al;
-            b |= tail_blocks(a, u[j], tprev, first, probe, qv, v, al);
-            live |= (uint32_t)al << j;
-            below |= u[j] < lo;
-          }
+          for (int j = 0; j < kThrScan; ++j) b |= u[j] >= hb;
+        }
+        if (!b) {
+#pragma unroll
+          for (int j = 0; j < kThrScan; ++j)
+            if (u[j] >= 0) {
+              bool al;
+              b |= tail_blocks(a, u[j], tprev, first, probe, qv, v, al);
+              live |= (uint32_t)al << j;
+              below |= u[j] < lo;
+            }
+        }
         if (b) {
           keep = 1;
         } else if (hi <= s || below) {  // the whole row, or all of it that could block
