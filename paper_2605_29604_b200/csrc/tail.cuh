@@ -886,13 +886,22 @@ __global__ void __launch_bounds__(kTailBlock, TCMIS_TAIL_MINB) k_tail(TailArgs a
         for (int p = 0; p < kPU; ++p) {
           const long long j = j0 + (long long)p * kTailBlock;
           x[p] = -1;
-          if (j < total) {
-            int lo = 0, hi = np - 1;  // the last listed row whose offset <= j
+          // the warp's 32 entries are consecutive: the row of its first entry
+          // by a warp-uniform binary search (broadcast reads), then each lane
+          // steps over the few row starts between it and its own entry (a
+          // per-lane search read 10 scattered 8-byte words per entry: bank
+          // conflicts made it the push's cost)
+          const long long jw = j - (threadIdx.x & 31);
+          if (jw < total) {
+            int lo = 0, hi = np - 1;  // the last listed row whose offset <= jw
             while (lo < hi) {
               const int mid = (lo + hi + 1) >> 1;
-              if (s_pofs[mid] <= j) lo = mid; else hi = mid - 1;
+              if (s_pofs[mid] <= jw) lo = mid; else hi = mid - 1;
             }
-            x[p] = __ldg(&a.nbr[s_s[s_pk[lo]] + (j - s_pofs[lo])]);
+            if (j < total) {
+              while (lo < np - 1 && s_pofs[lo + 1] <= j) ++lo;
+              x[p] = __ldg(&a.nbr[s_s[s_pk[lo]] + (j - s_pofs[lo])]);
+            }
           }
         }
 #pragma unroll
