@@ -367,9 +367,13 @@ int tcmis_graph_from_edges(tcmis_ctx *ctx, int32_t n, int64_t m, const int32_t *
                            const int32_t *v, tcmis_graph **out);
 int tcmis_gen_rgg(tcmis_ctx *ctx, int32_t n, uint64_t radius, uint64_t seed,
                   tcmis_graph **out);
-/* Host-side G(n,p) (generate.cpp:30-66): serial by definition (one RNG
- * stream), returned as malloc'ed CSR arrays the caller frees with
- * tcmis_free(). */
+/* gnp_graph_avg_degree (generate.cpp:30-66) on the device: the serial
+ * SplitMix64 stream in counter form, the pair-index increments prefix-summed
+ * (replaces the reference's serial generator; bit-identical graph). */
+int tcmis_gen_gnp(tcmis_ctx *ctx, int32_t n, double avg_degree, uint64_t seed,
+                  tcmis_graph **out);
+/* The same G(n,p) on the host (the serial definition), returned as malloc'ed
+ * CSR arrays the caller frees with tcmis_free(). */
 int tcmis_gen_gnp_host(int32_t n, double avg_degree, uint64_t seed, int64_t **offsets,
                        int32_t **neighbors, int64_t *nnz);
 void tcmis_free(void *p);

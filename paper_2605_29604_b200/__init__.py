@@ -151,6 +151,7 @@ def load():
         "tcmis_graph_from_edges": (C.c_int, [vp, i32, i64, vp, vp, P(vp)]),
         "tcmis_gen_rgg": (C.c_int, [vp, i32, u64, u64, P(vp)]),
         "tcmis_gen_gnp_host": (C.c_int, [i32, C.c_double, u64, P(P(i64)), P(P(i32)), P(i64)]),
+        "tcmis_gen_gnp": (C.c_int, [vp, i32, C.c_double, u64, P(vp)]),
         "tcmis_free": (None, [vp]),
         "tcmis_rgg_radius": (u64, [i32, C.c_double]),
         "tcmis_graph_reorder": (C.c_int, [vp, i32, vp]),
@@ -378,6 +379,15 @@ class DeviceGraph:
         ctx = ctx or default_context()
         h = C.c_void_p()
         _check(load().tcmis_gen_rmat(ctx.h, scale, edge_factor, seed, C.byref(h)))
+        return cls(h, ctx)
+
+    @classmethod
+    def gnp(cls, n: int, avg_degree: float, seed: int = 1,
+            ctx: Optional[Context] = None) -> "DeviceGraph":
+        """gnp_graph_avg_degree (generate.cpp:30-66) generated on the device."""
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(load().tcmis_gen_gnp(ctx.h, int(n), float(avg_degree), int(seed), C.byref(h)))
         return cls(h, ctx)
 
     @classmethod

@@ -46,6 +46,7 @@ int gen_grid(tcmis_ctx *ctx, int32_t side, tcmis_graph **out);
 int gen_from_edges(tcmis_ctx *ctx, int32_t n, int64_t m, const int32_t *u, const int32_t *v,
                    tcmis_graph **out);
 int gen_rgg(tcmis_ctx *ctx, int32_t n, uint64_t R, uint64_t seed, tcmis_graph **out);
+int gen_gnp(tcmis_ctx *ctx, int32_t n, double avg_degree, uint64_t seed, tcmis_graph **out);
 int gen_gnp_host(int32_t n, double avg_degree, uint64_t seed, int64_t **offsets,
                  int32_t **neighbors, int64_t *nnz_out);
 int h1_impl(tcmis_ctx *ctx, int32_t n, uint64_t seed, uint32_t *p_out);
@@ -627,6 +628,14 @@ TCMIS_API int tcmis_gen_rgg(tcmis_ctx *ctx, int32_t n, uint64_t radius, uint64_t
   NEED(ctx && out, "null handle");
   ENTER(ctx);
   return gen_rgg(ctx, n, radius, seed, out);
+}
+
+TCMIS_API int tcmis_gen_gnp(tcmis_ctx *ctx, int32_t n, double avg_degree, uint64_t seed,
+                            tcmis_graph **out) {
+  TCMIS_RANGE("tcmis_gen_gnp");
+  NEED(ctx && out, "null handle");
+  ENTER(ctx);
+  return gen_gnp(ctx, n, avg_degree, seed, out);
 }
 
 TCMIS_API int tcmis_gen_gnp_host(int32_t n, double avg, uint64_t seed, int64_t **offsets,

@@ -8,8 +8,10 @@
 // identical to tcmis::rmat_graph (pinned by tests/test_gpu_parity.py::test_gpu_rmat_bit_identical).
 //
 // Grid and RGG have no reference generator; their definitions are DESIGN.md's
-// (and oracle/tcmis_oracle.c's).  G(n,p) is inherently serial (one RNG stream
-// with data-dependent consumption) and runs on the host, as in the reference.
+// (and oracle/tcmis_oracle.c's).  G(n,p) consumes one draw per edge, so its
+// stream is counter-form too: the pair-index increments are independent and a
+// prefix sum places them (gen_gnp; tests/test_gpu_parity.py
+// test_gpu_gnp_bit_identical).  The serial host form stays as tcmis_gen_gnp_host.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -297,8 +299,10 @@ __global__ void k_edge_keys(int bits, int32_t n, int64_t m, const int32_t *__res
 // self-loops, dedup, CSR with sorted rows) on the device -- radix sort +
 // unique over 2*ceil(log2 n)-bit keys, the same pipeline as the R-MAT
 // generator.  An endpoint outside [0, n) -> std::out_of_range (graph.cpp:23-24).
-int gen_from_edges(tcmis_ctx *ctx, int32_t n, int64_t m, const int32_t *h_u, const int32_t *h_v,
-                   tcmis_graph **out) {
+// (d_u / d_v non-null: the edges are already on the device, h_u / h_v unused)
+static int from_edges_impl(tcmis_ctx *ctx, int32_t n, int64_t m, const int32_t *h_u,
+                           const int32_t *h_v, tcmis_graph **out, const int32_t *d_u,
+                           const int32_t *d_v) {
   if (n < 0 || m < 0) return set_error(TCMIS_E_INVALID_ARGUMENT, "negative size");
   cudaStream_t st = ctx->stream;
   int bits = 1;
@@ -307,16 +311,21 @@ int gen_from_edges(tcmis_ctx *ctx, int32_t n, int64_t m, const int32_t *h_u, con
   DevBuf<int32_t> du, dv;
   DevBuf<unsigned long long> a, b;
   DevBuf<int> bad;
-  if (int rc = du.alloc((size_t)m)) return rc;
-  if (int rc = dv.alloc((size_t)m)) return rc;
+  if (!d_u) {
+    if (int rc = du.alloc((size_t)m)) return rc;
+    if (int rc = dv.alloc((size_t)m)) return rc;
+  }
   if (int rc = a.alloc((size_t)nk)) return rc;
   if (int rc = b.alloc((size_t)nk)) return rc;
   if (int rc = bad.alloc(1)) return rc;
   TCMIS_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
   if (m) {
-    TCMIS_CUDA(cudaMemcpyAsync(du.p, h_u, 4ull * m, cudaMemcpyHostToDevice, st));
-    TCMIS_CUDA(cudaMemcpyAsync(dv.p, h_v, 4ull * m, cudaMemcpyHostToDevice, st));
-    k_edge_keys<<<grid_for(ctx, m, 256, 16), 256, 0, st>>>(bits, n, m, du.p, dv.p, a.p, bad.p);
+    if (!d_u) {
+      TCMIS_CUDA(cudaMemcpyAsync(du.p, h_u, 4ull * m, cudaMemcpyHostToDevice, st));
+      TCMIS_CUDA(cudaMemcpyAsync(dv.p, h_v, 4ull * m, cudaMemcpyHostToDevice, st));
+    }
+    k_edge_keys<<<grid_for(ctx, m, 256, 16), 256, 0, st>>>(bits, n, m, d_u ? d_u : du.p,
+                                                         d_v ? d_v : dv.p, a.p, bad.p);
     TCMIS_LAUNCHED(ctx);
   }
   int h_bad = 0;
@@ -358,6 +367,14 @@ int gen_from_edges(tcmis_ctx *ctx, int32_t n, int64_t m, const int32_t *h_u, con
   int32_t *q = nbr.release();
   return wrap_owned(ctx, n, mm, o, q, out);
 }
+
+int gen_from_edges(tcmis_ctx *ctx, int32_t n, int64_t m, const int32_t *h_u, const int32_t *h_v,
+                   tcmis_graph **out) {
+  return from_edges_impl(ctx, n, m, h_u, h_v, out, nullptr, nullptr);
+}
+
+int gen_gnp_host(int32_t n, double avg_degree, uint64_t seed, int64_t **offsets,
+                 int32_t **neighbors, int64_t *nnz_out);
 
 int gen_grid(tcmis_ctx *ctx, int32_t side, tcmis_graph **out) {
   if (side < 0 || (int64_t)side * side > 0x7fffffffLL)
@@ -465,6 +482,125 @@ int gen_rgg(tcmis_ctx *ctx, int32_t n, uint64_t R, uint64_t seed, tcmis_graph **
 }
 
 // generate.cpp:30-66 on the host: the gap sequence is one serial RNG stream.
+namespace {
+
+// gnp_graph (generate.cpp:30-60) draw by draw: draw k of the SplitMix64 stream
+// is mix64(mix64(seed) + (k + 1) golden) (counter form, as in the R-MAT
+// kernel), and the pair index advances by 1 + floor(log1p(-u) / log1p(-p)),
+// so the increments are independent and the pair indices are their prefix
+// sum.  The increment is clamped to total + 1 (one such step already ends the
+// stream), which keeps the sums in range for any p.
+__global__ void k_gnp_steps(int64_t K, uint64_t mseed, double log_q, int64_t total,
+                            int64_t *__restrict__ inc) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < K;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const double u = (double)(vertex_hash_m((uint64_t)k, mseed) >> 11) * 0x1.0p-53;
+    const double g = floor(log1p(-u) / log_q);
+    inc[k] = g >= (double)total ? total + 1 : 1 + (int64_t)g;
+  }
+}
+
+// first pair index of row r: pairs (i, j), i < j, in row-major order
+__device__ __forceinline__ int64_t gnp_row_start(int64_t n, int64_t r) {
+  return (int64_t)(((uint64_t)r * (uint64_t)(2 * n - r - 1)) >> 1);
+}
+
+// pair index -> (row, column), generate.cpp:50-57 (the while loop over rows)
+// in closed form: a floating-point estimate of the row, corrected exactly
+__global__ void k_gnp_pairs(int64_t E, int64_t n, const int64_t *__restrict__ idx1,
+                            int32_t *__restrict__ eu, int32_t *__restrict__ ev) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < E;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t idx = idx1[k] - 1;  // the prefix sum starts the stream at -1
+    const double b = (double)(2 * n - 1);
+    int64_t r = (int64_t)floor((b - sqrt(b * b - 8.0 * (double)idx)) * 0.5);
+    r = r < 0 ? 0 : (r > n - 2 ? n - 2 : r);
+    while (r > 0 && gnp_row_start(n, r) > idx) --r;
+    while (r < n - 2 && gnp_row_start(n, r + 1) <= idx) ++r;
+    eu[k] = (int32_t)r;
+    ev[k] = (int32_t)(r + 1 + (idx - gnp_row_start(n, r)));
+  }
+}
+
+__global__ void k_count_below(int64_t K, const int64_t *__restrict__ idx1, int64_t total,
+                              unsigned long long *__restrict__ cnt) {
+  unsigned long long c = 0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < K;
+       k += (int64_t)gridDim.x * blockDim.x)
+    c += idx1[k] - 1 < total ? 1u : 0u;
+  c = __reduce_add_sync(0xffffffffu, (unsigned)c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
+}
+
+}  // namespace
+
+// gnp_graph_avg_degree (generate.cpp:62-65) on the device:
+// bit-identical to the reference's serial stream (tests/test_gpu_parity.py).
+// p >= 1 (the complete graph, a corner only tiny n reaches) is built on the
+// host and uploaded.
+int gen_gnp(tcmis_ctx *ctx, int32_t n, double avg_degree, uint64_t seed, tcmis_graph **out) {
+  if (n < 0) return set_error(TCMIS_E_INVALID_ARGUMENT, "n must be non-negative");
+  const double p = n > 1 ? avg_degree / (double)(n - 1) : 0.0;
+  if (p <= 0.0 || n < 2) return gen_from_edges(ctx, n, 0, nullptr, nullptr, out);
+  if (p >= 1.0) {
+    int64_t *off = nullptr;
+    int32_t *nbr = nullptr;
+    int64_t nnz = 0;
+    if (int rc = gen_gnp_host(n, avg_degree, seed, &off, &nbr, &nnz)) return rc;
+    std::vector<int32_t> eu, ev;
+    for (int32_t v = 0; v < n; ++v)
+      for (int64_t e = off[v]; e < off[v + 1]; ++e)
+        if (v < nbr[e]) {
+          eu.push_back(v);
+          ev.push_back(nbr[e]);
+        }
+    std::free(off);
+    std::free(nbr);
+    return gen_from_edges(ctx, n, (int64_t)eu.size(), eu.data(), ev.data(), out);
+  }
+  cudaStream_t st = ctx->stream;
+  const double log_q = std::log1p(-p);  // the host's log1p, as the reference's
+  const int64_t total = (int64_t)n * (n - 1) / 2;
+  const double mean = p * (double)total;
+  // draws: the expected edge count plus 8 standard deviations; more if that
+  // did not reach the end of the pair range
+  int64_t K = (int64_t)(mean + 8.0 * std::sqrt(mean) + 1024.0);
+  const uint64_t mseed = mix64(seed);
+  for (;;) {
+    DevBuf<int64_t> inc, idx1;
+    DevBuf<unsigned long long> cnt;
+    if (int rc = inc.alloc((size_t)K)) return rc;
+    if (int rc = idx1.alloc((size_t)K)) return rc;
+    if (int rc = cnt.alloc(1)) return rc;
+    k_gnp_steps<<<grid_for(ctx, K, 256, 16), 256, 0, st>>>(K, mseed, log_q, total, inc.p);
+    TCMIS_LAUNCHED(ctx);
+    size_t bytes = 0;
+    TCMIS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, inc.p, idx1.p, K, st));
+    DevBuf<char> tmp;
+    if (int rc = tmp.alloc(bytes)) return rc;
+    TCMIS_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, bytes, inc.p, idx1.p, K, st));
+    ctx->launches += 1;
+    TCMIS_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), st));
+    k_count_below<<<grid_for(ctx, K, 256, 16), 256, 0, st>>>(K, idx1.p, total, cnt.p);
+    TCMIS_LAUNCHED(ctx);
+    unsigned long long E = 0;
+    TCMIS_CUDA(cudaMemcpyAsync(&E, cnt.p, sizeof(E), cudaMemcpyDeviceToHost, st));
+    TCMIS_CUDA(cudaStreamSynchronize(st));
+    if ((int64_t)E == K) {  // the stream did not end within K draws
+      K *= 2;
+      continue;
+    }
+    DevBuf<int32_t> eu, ev;
+    if (int rc = eu.alloc((size_t)E + 1)) return rc;
+    if (int rc = ev.alloc((size_t)E + 1)) return rc;
+    if (E)
+      k_gnp_pairs<<<grid_for(ctx, (int64_t)E, 256, 16), 256, 0, st>>>((int64_t)E, n, idx1.p,
+                                                                     eu.p, ev.p);
+    TCMIS_LAUNCHED(ctx);
+    return from_edges_impl(ctx, n, (int64_t)E, nullptr, nullptr, out, eu.p, ev.p);
+  }
+}
+
 int gen_gnp_host(int32_t n, double avg_degree, uint64_t seed, int64_t **offsets,
                  int32_t **neighbors, int64_t *nnz_out) {
   if (n < 0) return set_error(TCMIS_E_INVALID_ARGUMENT, "n must be non-negative");

@@ -300,6 +300,19 @@ def test_gpu_rmat_bit_identical(ctx, scale, ef, seed):
     assert np.array_equal(a.offsets, b.off) and np.array_equal(a.neighbors, b.nbr)
 
 
+@pytest.mark.parametrize("n,avg,seed", [(0, 4.0, 1), (1, 4.0, 1), (2, 0.0, 1), (7, 10.0, 3),
+                                         (50, 6.0, 2), (3000, 12.0, 2), (100000, 16.0, 1),
+                                         (100000, 16.0, 7), (1 << 21, 8.0, 5), (400, 0.001, 9)])
+def test_gpu_gnp_bit_identical(ctx, n, avg, seed):
+    """G(n,p) (gnp_graph_avg_degree, generate.cpp:30-66) on the device: the
+    counter-form SplitMix64 draws, prefix-summed pair indices and closed-form
+    rows give the reference's graph exactly (the ER config is n = 100k,
+    avg 16, seed 1); empty, complete (p >= 1) and near-empty corners."""
+    a = tc.DeviceGraph.gnp(n, avg, seed, ctx).download()
+    b = O.gen("gnp_avg", n, avg, seed)
+    assert np.array_equal(a.offsets, b.off) and np.array_equal(a.neighbors, b.nbr)
+
+
 def test_gpu_grid_and_rgg_match_oracle(ctx):
     for side in (1, 2, 37):
         a = tc.DeviceGraph.grid(side, ctx).download()
