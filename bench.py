@@ -139,7 +139,7 @@ class ClockSampler:
 
 def make_device_graph(tc, name: str, ctx):
     if name == "er":
-        return tc.DeviceGraph.upload(tc.gnp_graph_avg_degree(100000, 16.0, 1), ctx)
+        return tc.DeviceGraph.gnp(100000, 16.0, 1, ctx)  # = gnp_graph_avg_degree(100000, 16, 1)
     if name == "grid":
         return tc.DeviceGraph.grid(4096, ctx)
     if name == "rmat22":
