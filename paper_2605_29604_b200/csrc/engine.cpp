@@ -7,6 +7,7 @@
 #include <numeric>
 #include <cmath>
 #include <memory>
+#include <cstdlib>
 #include <mutex>
 #include <bit>
 #include <istream>
@@ -201,8 +202,39 @@ bool Graph::has_edge(VertexId u, VertexId v) const {
   return std::binary_search(row.begin(), row.end(), v);
 }
 
+// graph.cpp:14-41.  Large edge lists are normalised on the device
+// (tcmis_graph_from_edges: radix sort + unique) and the CSR comes back; small
+// ones stay on the host, where the copies would cost more than the sort.
+// TCMIS_FROM_EDGES_DEVICE_MIN (edges; default 2^20) moves the switch (tests).
+static Graph graph_from_edges_device(VertexId n,
+                                     std::span<const std::pair<VertexId, VertexId>> edges) {
+  const std::size_t m = edges.size();
+  std::vector<std::int32_t> u(m), v(m);
+  for (std::size_t i = 0; i < m; ++i) {
+    u[i] = edges[i].first;
+    v[i] = edges[i].second;
+  }
+  ContextLease lease;
+  tcmis_graph *h = nullptr;
+  check(tcmis_graph_from_edges(lease.get(), n, static_cast<std::int64_t>(m), u.data(), v.data(),
+                               &h));
+  Graph g;
+  g.n = n;
+  g.offsets.assign(static_cast<std::size_t>(n) + 1, 0);
+  g.neighbors.resize(static_cast<std::size_t>(tcmis_graph_nnz(h)));
+  const int rc = tcmis_graph_download(h, g.offsets.data(),
+                                      g.neighbors.empty() ? nullptr : g.neighbors.data());
+  tcmis_graph_destroy(h);
+  check(rc);
+  return g;
+}
+
 Graph graph_from_edges(VertexId n, std::span<const std::pair<VertexId, VertexId>> edges) {
   if (n < 0) throw std::invalid_argument("vertex count must be non-negative");
+  std::size_t device_min = std::size_t(1) << 20;
+  if (const char *env = std::getenv("TCMIS_FROM_EDGES_DEVICE_MIN"))
+    device_min = static_cast<std::size_t>(std::atoll(env));
+  if (edges.size() >= device_min && !edges.empty()) return graph_from_edges_device(n, edges);
   std::vector<std::uint64_t> keys;
   keys.reserve(edges.size() * 2);
   for (const auto &[u, v] : edges) {

@@ -36,7 +36,12 @@ def dropin(tmp_path_factory):
 
 @pytest.mark.parametrize("kind,args", [("rmat", (12, 16, 2)), ("gnp_avg", (3000, 10.0, 5)),
                                        ("grid", (30,))])
-def test_cpp_dropin_matches_reference(dropin, kind, args):
+@pytest.mark.parametrize("device_edges", [False, True])
+def test_cpp_dropin_matches_reference(dropin, kind, args, device_edges, monkeypatch):
+    """device_edges: the C++ graph_from_edges (and so the tiled round trip
+    and the edge-range error) through the device normaliser at any size."""
+    if device_edges:
+        monkeypatch.setenv("TCMIS_FROM_EDGES_DEVICE_MIN", "1")
     exe, d = dropin
     g = O.gen(kind, *args)
     path = str(d / f"{kind}.bin")
